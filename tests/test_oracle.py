@@ -1,0 +1,67 @@
+"""The oracle is pinned before it is trusted (task ③): the Philox restatement
+against numpy's own Philox4x64-10 and the Random123 known answer, and the C
+port of the sampler against golden outputs of the reference itself
+(tests/golden/make_golden.py, reference run with injected uniforms)."""
+
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from oracle import oracle as O
+from oracle.philox import philox4x64_10, uniforms
+
+
+def test_philox_random123_kat():
+    out = philox4x64_10(np.zeros(4, np.uint64), np.zeros(2, np.uint64))
+    assert [int(x) for x in out] == [
+        0x16554D9ECA36314C, 0xDB20FE9D672D0FDC, 0xD7E772CEE186176B, 0x7E68B68AEC7BA23B]
+
+
+def test_philox_matches_numpy_bitgenerator():
+    rng = np.random.default_rng(0)
+    for _ in range(100):
+        ctr = rng.integers(0, 2**63, size=4, dtype=np.int64).astype(np.uint64)
+        ctr[0] |= np.uint64(1)  # numpy pre-increments; avoid a borrow below
+        key = rng.integers(0, 2**63, size=2, dtype=np.int64).astype(np.uint64)
+        ref = np.random.Philox(key=key, counter=ctr - np.array([1, 0, 0, 0], np.uint64))
+        assert np.array_equal(ref.random_raw(4), philox4x64_10(ctr, key))
+
+
+def test_c_uniform_matches_numpy_restatement():
+    rows = np.array([0, 1, 7, 2**40 + 3, 16_700_000_000])
+    for t in range(9):
+        want = uniforms(5, 2, 3, rows, t)
+        got = [O.uniform(5, 2, 3, int(r), t) for r in rows]
+        assert np.array_equal(want, np.array(got))
+
+
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLDEN, "epoch_*.npz"))))
+def test_oracle_matches_reference_golden(path):
+    g, want = O.load_golden(path)
+    if g["kind"] == "sage":
+        got = O.sage_bulk(g["n"], g["rowptr"], g["col"], g["batches"], g["batch_size"],
+                          g["fanouts"], g["seed"], g["epoch"], g["batch_offset"])
+    else:
+        got = O.ladies_bulk(g["n"], g["rowptr"], g["col"], g["batches"], g["fanouts"],
+                            g["seed"], g["epoch"], g["batch_offset"])
+    assert O.compare_epochs(want, got) == []
+
+
+def test_oracle_its_matches_reference_rows():
+    z = dict(np.load(os.path.join(GOLDEN, "its_rows.npz")))
+    for i in range(len(z["deg"])):
+        w = z["w_cat"][z["w_off"][i]:z["w_off"][i + 1]]
+        want = z["picks"][i]
+        want = want[want >= 0]
+        assert np.array_equal(O.its_sample_row(w, int(z["fanout"][i]), z["u"][i]), want)
+
+
+def test_oracle_threads_do_not_change_output():
+    g, want = O.load_golden(os.path.join(GOLDEN, "epoch_rmat12_sage.npz"))
+    for th in (1, 3):
+        got = O.sage_bulk(g["n"], g["rowptr"], g["col"], g["batches"], g["batch_size"],
+                          g["fanouts"], g["seed"], threads=th)
+        assert O.compare_epochs(want, got) == []
