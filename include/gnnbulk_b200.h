@@ -1,0 +1,104 @@
+/*
+ * gnnbulk_b200 — C ABI of the B200-native matrix-based bulk GNN sampler
+ * (arXiv 2311.02909).  The reference (`gnnbulk`, pure Python + numpy/scipy)
+ * has no FFI of its own; these are the entry points a ctypes/cffi binding of
+ * its hot path binds.  Each entry point cites the
+ * reference function it replaces.
+ *
+ * Conventions
+ *   - Plain C types only; every array argument prefixed d_ is DEVICE memory,
+ *     h_ is host memory.  `stream` is a cudaStream_t passed as void*.
+ *   - Calls are stream-ordered and do not synchronise the host unless the
+ *     comment says so (graph creation, size queries).
+ *   - Return 0 (GB_OK) or a negative status; gb_last_error() describes the
+ *     last failure of the calling thread.  GB_ERR_CONTRACT is what the
+ *     Python shim maps to reference `ContractViolation`
+ *     (pkg/src/gnnbulk/errors.py:4-11).
+ *   - Vertex ids are int32 (n < 2^31), row offsets int64, keys int64.
+ *   - The caller owns every buffer; sizes are obtained with the *_workspace
+ *     queries.  Column arrays of a graph must be 16-byte aligned and readable
+ *     for nnz + GB_COL_PAD entries (streaming loads are 16 B wide).
+ */
+#ifndef GNNBULK_B200_H
+#define GNNBULK_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GB_OK 0
+#define GB_ERR_CONTRACT (-1)
+#define GB_ERR_CUDA (-2)
+#define GB_ERR_CAPACITY (-3)
+#define GB_ERR_UNSUPPORTED (-4)
+
+#define GB_COL_PAD 4
+
+/* SAGE sample-kernel modes (identical outputs) */
+#define GB_SAGE_STREAM 0 /* Alg. 1: P row formed on chip by streaming A rows */
+#define GB_SAGE_PFREE 1  /* P-free fast path: read only the picked entries  */
+
+const char* gb_last_error(void);
+int gb_version(void);
+
+/* ------------------------------------------------------------------ RNG
+ * u(seed, epoch, depth, row, t) for count (row, t) pairs — the injected
+ * replacement of RowRng.stream(global_row).random() (sampler.py:97-116);
+ * the t-th call of row `row`.  Known-answer tested against numpy Philox. */
+int gb_uniforms(uint64_t seed, uint64_t epoch, uint64_t depth, const int64_t* d_rows,
+                const int64_t* d_t, int64_t count, double* d_out, void* stream);
+
+/* ---------------------------------------------------------------- graph
+ * Graph (sparse.py:194-227) on the device: CSR rows = out-neighbours,
+ * values implicitly 1.0.  Creation builds the per-degree exact-replay
+ * tables of the SAGE sampler (synchronises `stream`). */
+typedef struct gb_graph gb_graph;
+int gb_graph_create(int64_t n, int64_t nnz, const int64_t* d_rowptr, const int32_t* d_col,
+                    void* stream, gb_graph** out);
+int gb_graph_destroy(gb_graph* g);
+int gb_graph_info(const gb_graph* g, int64_t* h_max_deg, int64_t* h_table_slots);
+
+/* ---------------------------------------------------------- SAGE bulk
+ * sample_epoch_bulk with SamplerConfig.kind == SAGE (sampler.py:325-387):
+ * all L layers for k stacked minibatches, entirely on the device.
+ *
+ * Per layer l the caller provides buffers with capacity r_cap rows and
+ * f_cap = r_cap * fanouts[l] entries, r_cap(1) >= total batch vertices,
+ * r_cap(l+1) = f_cap(l).  Outputs (device):
+ *   fptr  [R+1]  frontier row offsets == adjacency row offsets
+ *   fcol  [F]    frontier columns (sorted per row) == sampled_vertices, and
+ *                the next layer's row vertices (expand_row_extraction)
+ *   acol  [F]    block-diagonal adjacency columns (block_diag of
+ *                compact_columns per batch, sparse.py:321-357)
+ *   colv  [U]    col_vertices, per batch sorted unique, concatenated
+ *   eoff  [k+1]  per-batch offsets into fcol (sampled_vertices) == next
+ *                layer's batch row offsets
+ *   coloff[k+1]  per-batch offsets into colv
+ * d_sizes[3*l + {0,1,2}] = (R, F, U) of layer l.  Layer 1 rows are the batch
+ * vertices d_bverts with batch offsets d_bptr (sage_seed_matrix). */
+typedef struct {
+  int64_t* fptr;
+  int32_t* fcol;
+  int32_t* acol;
+  int32_t* colv;
+  int64_t* eoff;
+  int64_t* coloff;
+  int64_t r_cap;
+  int64_t f_cap;
+} gb_sage_layer_out;
+
+int gb_sage_bulk_workspace(const gb_graph* g, int64_t k, int64_t r1_cap, int32_t layers,
+                           const int64_t* h_fanouts, size_t* h_bytes);
+int gb_sage_bulk(const gb_graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d_bverts,
+                 int64_t r1_cap, int64_t batch_size, int32_t layers, const int64_t* h_fanouts,
+                 uint64_t seed, uint64_t epoch, int64_t batch_offset, int32_t mode,
+                 gb_sage_layer_out* h_layers, int64_t* d_sizes, void* d_ws, size_t ws_bytes,
+                 void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GNNBULK_B200_H */

@@ -1,0 +1,130 @@
+// extern "C" boundary of libgnnbulk_b200.so (include/gnnbulk_b200.h).
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "gb_common.cuh"
+#include "gb_internal.h"
+
+namespace gb {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_status(cudaError_t e, const char* what) {
+  set_error("CUDA error in %s: %s", what, cudaGetErrorString(e));
+  return GB_ERR_CUDA;
+}
+
+__global__ void k_uniforms(uint64_t seed, uint64_t epoch, uint64_t depth,
+                           const int64_t* __restrict__ rows, const int64_t* __restrict__ t,
+                           int64_t count, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = uniform53(seed, epoch, depth, (uint64_t)rows[i], (uint64_t)t[i]);
+}
+
+}  // namespace gb
+
+using namespace gb;
+
+struct gb_graph : public gb::Graph {};
+
+extern "C" {
+
+const char* gb_last_error(void) { return g_err; }
+int gb_version(void) { return 1; }
+
+int gb_uniforms(uint64_t seed, uint64_t epoch, uint64_t depth, const int64_t* d_rows,
+                const int64_t* d_t, int64_t count, double* d_out, void* stream) {
+  if (count < 0) { set_error("count must be >= 0"); return GB_ERR_CONTRACT; }
+  if (count == 0) return GB_OK;
+  int64_t g = (count + 255) / 256;
+  if (g > 16 * kNumSMs) g = 16 * kNumSMs;
+  k_uniforms<<<(int)g, 256, 0, (cudaStream_t)stream>>>(seed, epoch, depth, d_rows, d_t, count,
+                                                       d_out);
+  GB_LAUNCH_CHECK("k_uniforms");
+  return GB_OK;
+}
+
+int gb_graph_create(int64_t n, int64_t nnz, const int64_t* d_rowptr, const int32_t* d_col,
+                    void* stream, gb_graph** out) {
+  if (!out || n < 0 || nnz < 0 || n >= ((int64_t)1 << 31)) {
+    set_error("graph: need 0 <= n < 2^31 and nnz >= 0");
+    return GB_ERR_CONTRACT;
+  }
+  if (((uintptr_t)d_col & 15) != 0) {
+    set_error("graph: column array must be 16-byte aligned");
+    return GB_ERR_CONTRACT;
+  }
+  gb_graph* g = new gb_graph();
+  g->n = n;
+  g->nnz = nnz;
+  g->rowptr = d_rowptr;
+  g->col = d_col;
+  int rc = graph_build_tables(g, (cudaStream_t)stream);
+  if (rc) {
+    gb_graph_destroy(g);
+    return rc;
+  }
+  *out = g;
+  return GB_OK;
+}
+
+int gb_graph_destroy(gb_graph* g) {
+  if (!g) return GB_OK;
+  cudaFree(g->deg_slot);
+  cudaFree(g->slot_deg);
+  cudaFree(g->run_j0);
+  cudaFree(g->run_s0);
+  cudaFree(g->run_d);
+  cudaFree(g->run_n);
+  delete g;
+  return GB_OK;
+}
+
+int gb_graph_info(const gb_graph* g, int64_t* h_max_deg, int64_t* h_table_slots) {
+  if (!g) { set_error("null graph"); return GB_ERR_CONTRACT; }
+  if (h_max_deg) *h_max_deg = g->max_deg;
+  if (h_table_slots) *h_table_slots = g->slots;
+  return GB_OK;
+}
+
+int gb_sage_bulk_workspace(const gb_graph* g, int64_t k, int64_t r1_cap, int32_t layers,
+                           const int64_t* h_fanouts, size_t* h_bytes) {
+  if (!g || !h_bytes || k < 0 || layers < 1) {
+    set_error("sage workspace: bad arguments");
+    return GB_ERR_CONTRACT;
+  }
+  return sage_workspace(g, k, r1_cap, layers, h_fanouts, h_bytes);
+}
+
+int gb_sage_bulk(const gb_graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d_bverts,
+                 int64_t r1_cap, int64_t batch_size, int32_t layers, const int64_t* h_fanouts,
+                 uint64_t seed, uint64_t epoch, int64_t batch_offset, int32_t mode,
+                 gb_sage_layer_out* h_layers, int64_t* d_sizes, void* d_ws, size_t ws_bytes,
+                 void* stream) {
+  if (!g || k < 0 || layers < 1 || batch_size < 1 || !h_fanouts || !h_layers) {
+    set_error("sage bulk: bad arguments");
+    return GB_ERR_CONTRACT;
+  }
+  for (int32_t l = 0; l < layers; ++l)
+    if (h_fanouts[l] < 1 || h_fanouts[l] > 32) {
+      set_error("sage bulk: fanout %lld outside [1, 32]", (long long)h_fanouts[l]);
+      return h_fanouts[l] < 1 ? GB_ERR_CONTRACT : GB_ERR_UNSUPPORTED;
+    }
+  if (mode != GB_SAGE_STREAM && mode != GB_SAGE_PFREE) {
+    set_error("sage bulk: unknown mode %d", mode);
+    return GB_ERR_CONTRACT;
+  }
+  return sage_bulk(g, k, d_bptr, d_bverts, r1_cap, batch_size, layers, h_fanouts, seed, epoch,
+                   batch_offset, mode, h_layers, d_sizes, d_ws, ws_bytes, (cudaStream_t)stream);
+}
+
+}  // extern "C"

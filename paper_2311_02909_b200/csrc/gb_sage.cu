@@ -1,0 +1,706 @@
+// GraphSAGE node-wise bulk sampling, Alg. 1 of arXiv 2311.02909
+// (P <- Q^l A; NORM; SAMPLE; EXTRACT) for k stacked minibatches, sm_100a.
+//
+// Reference behaviour reproduced bit for bit (with the injected uniforms of
+// gb_common.cuh): sample_epoch_bulk SAGE path, pkg/src/gnnbulk/sampler.py:325-387.
+//
+//   * Q^l is never built: row r of Q^l is one-hot at rowv[r]
+//     (sage_seed_matrix sampler.py:122-127, expand_row_extraction
+//     sparse.py:360-370), so row r of P = Q^l A is row rowv[r] of A.
+//   * NORM: every entry of P row r is fl(1/deg) (norm_rows_sage,
+//     sparse.py:254-286; row sums of 1.0-valued rows are exact).
+//   * SAMPLE: its_sample_row (sampler.py:157-189) replayed exactly.  With
+//     equal weights w = fl(1/deg) and removed weights contributing exactly
+//     0.0, the sequential fp64 cumsum over the live entries is the prefix
+//     table S[j] = fl(S[j-1] + w) of the degree alone (SURVEY.md Appendix
+//     A.2).  S is stored once per distinct degree as "runs" of constant
+//     increment inside one binade, so S[j] and its inverse are O(1) exact
+//     look-ups (replay tables, built by gb_graph_create).
+//   * EXTRACT (sage_batch_blocks / compact_columns / block_diag,
+//     sampler.py:390-417, sparse.py:321-357): per-batch sorted-unique
+//     columns via one bit per (batch, vertex), a popcount prefix scan for
+//     the block-diagonal renumbering, and an enumerate pass for
+//     col_vertices.
+//
+// Two modes of the SAMPLE kernel, identical outputs:
+//   GB_SAGE_STREAM: P row formed on chip — the warp streams the whole A row
+//     (coalesced 16-B loads, merge-path balanced over rows+entries) and
+//     catches the picked entries out of registers.  This is Alg. 1 with P
+//     never written to HBM; its algorithmic bytes are SURVEY.md §8(d).
+//   GB_SAGE_PFREE: the P-free fast path: only the picked
+//     entries of A are read.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include "gb_common.cuh"
+#include "gb_scan.cuh"
+#include "gb_internal.h"
+
+namespace gb {
+
+// ============================================================ replay tables
+
+__global__ void k_degree_max(const int64_t* __restrict__ rowptr, int64_t n,
+                             unsigned long long* __restrict__ out_max) {
+  int64_t best = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x)
+    best = max(best, rowptr[v + 1] - rowptr[v]);
+  best = max(best, (int64_t)__reduce_max_sync(0xffffffffu, (unsigned)min(best, (int64_t)0x7fffffff)));
+  if ((threadIdx.x & 31) == 0) atomicMax(out_max, (unsigned long long)best);
+}
+
+__global__ void k_degree_flags(const int64_t* __restrict__ rowptr, int64_t n,
+                               int32_t* __restrict__ flags) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    int64_t d = rowptr[v + 1] - rowptr[v];
+    if (d >= 2) flags[d] = 1;
+  }
+}
+
+struct FlagF {
+  const int32_t* flags;
+  __device__ int64_t operator()(int64_t i) const { return flags[i]; }
+};
+
+__global__ void k_degree_slots(const int32_t* __restrict__ flags, const int64_t* __restrict__ pre,
+                               int64_t nd, int32_t* __restrict__ deg_slot,
+                               int32_t* __restrict__ slot_deg) {
+  for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < nd;
+       d += (int64_t)gridDim.x * blockDim.x) {
+    if (flags[d]) {
+      deg_slot[d] = (int32_t)pre[d];
+      slot_deg[pre[d]] = (int32_t)d;
+    } else {
+      deg_slot[d] = -1;
+    }
+  }
+}
+
+__device__ __forceinline__ uint64_t binade(double x) {
+  return (uint64_t)__double_as_longlong(x) >> 52;
+}
+
+// One thread per distinct degree m: walk S[j] = fl(S[j-1] + fl(1/m)),
+// j = 1..m, exactly as numpy's sequential cumsum does, and cut it into runs
+// of constant increment inside one binade.
+__global__ void k_build_runs(const int32_t* __restrict__ slot_deg, int64_t slots,
+                             int32_t* __restrict__ run_j0, double* __restrict__ run_s0,
+                             double* __restrict__ run_d, int32_t* __restrict__ run_n,
+                             int32_t* __restrict__ overflow) {
+  for (int64_t sl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sl < slots;
+       sl += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = slot_deg[sl];
+    const double w = 1.0 / (double)m;
+    int32_t* J = run_j0 + sl * (kMaxRuns + 1);
+    double* S0 = run_s0 + sl * kMaxRuns;
+    double* D = run_d + sl * kMaxRuns;
+    int nr = 0;
+    int64_t j0 = 1, len = 1;
+    double s0 = w, d = 0.0, S = w;
+    bool bad = false;
+    for (int64_t j = 2; j <= m; ++j) {
+      const double S2 = __dadd_rn(S, w);
+      const double step = __dadd_rn(S2, -S);
+      if (len == 1 && binade(S2) == binade(s0)) {
+        d = step;
+        len = 2;
+      } else if (len >= 2 && step == d && binade(S2) == binade(s0)) {
+        ++len;
+      } else {
+        if (nr < kMaxRuns) { J[nr] = (int32_t)j0; S0[nr] = s0; D[nr] = d; } else bad = true;
+        ++nr;
+        j0 = j; s0 = S2; len = 1; d = 0.0;
+      }
+      S = S2;
+    }
+    if (nr < kMaxRuns) { J[nr] = (int32_t)j0; S0[nr] = s0; D[nr] = d; } else bad = true;
+    ++nr;
+    if (nr <= kMaxRuns) J[nr] = (int32_t)(m + 1);  // sentinel
+    run_n[sl] = nr;
+    if (bad) atomicExch(overflow, 1);
+  }
+}
+
+// ========================================================= exact replay math
+
+// Table of one degree staged in (warp-private) shared memory.
+struct RunTable {
+  int32_t* j0;   // nr + 1 (sentinel m + 1)
+  double* s0;    // nr
+  double* d;     // nr
+  int nr;
+};
+
+// S[n], 1 <= n <= m.
+__device__ __forceinline__ double table_S(const RunTable& t, int64_t n) {
+  int lo = 0, hi = t.nr;  // last run with j0 <= n
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (t.j0[mid] <= n) lo = mid; else hi = mid;
+  }
+  return __dadd_rn(t.s0[lo], __dmul_rn((double)(n - t.j0[lo]), t.d[lo]));
+}
+
+// first j >= 1 with S[j] > target (may be m + 1 when none)
+__device__ __forceinline__ int64_t table_first_gt(const RunTable& t, double target) {
+  if (target < t.s0[0]) return 1;
+  int lo = 0, hi = t.nr;  // last run with s0 <= target
+  while (hi - lo > 1) {
+    int mid = (lo + hi) >> 1;
+    if (t.s0[mid] <= target) lo = mid; else hi = mid;
+  }
+  const int64_t j0 = t.j0[lo];
+  const int64_t len = (int64_t)t.j0[lo + 1] - j0;
+  if (len == 1) return j0 + 1;
+  const double s0 = t.s0[lo], d = t.d[lo];
+  int64_t q = (int64_t)((target - s0) / d);
+  q = q < 0 ? 0 : (q > len - 1 ? len - 1 : q);
+  while (q > 0 && __dadd_rn(s0, __dmul_rn((double)q, d)) > target) --q;
+  while (q + 1 < len && __dadd_rn(s0, __dmul_rn((double)(q + 1), d)) <= target) ++q;
+  return j0 + q + 1;
+}
+
+// ============================================================ layer kernels
+
+__global__ void k_sage_prep(const int64_t* __restrict__ R_ptr, const int32_t* __restrict__ rowv,
+                            const int64_t* __restrict__ rowptr, int32_t* __restrict__ deg) {
+  const int64_t R = *R_ptr;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = rowv[r];
+    deg[r] = (int32_t)(rowptr[v + 1] - rowptr[v]);
+  }
+}
+
+struct TakeF {
+  const int32_t* deg;
+  int32_t s;
+  __device__ int64_t operator()(int64_t i) const { return min(deg[i], s); }
+};
+struct DegF {
+  const int32_t* deg;
+  __device__ int64_t operator()(int64_t i) const { return deg[i]; }
+};
+
+struct SageArgs {
+  const int64_t* rowptr;
+  const int32_t* col;
+  const int32_t* deg_slot;
+  const int32_t* run_j0;
+  const double* run_s0;
+  const double* run_d;
+  const int32_t* run_n;
+  const int32_t* rowv;
+  const int32_t* deg;
+  const int64_t* fptr;
+  const int64_t* gstart;
+  const int64_t* brow;   // k + 1
+  int64_t k;
+  int32_t s;
+  int64_t stride;
+  int64_t batch_offset;
+  uint64_t seed, epoch, depth;
+  uint32_t* bitmap;
+  int64_t nwords;
+  int32_t* fcol;
+};
+
+constexpr int kSampleThreads = 256;
+constexpr int kSampleWarps = kSampleThreads / 32;
+constexpr int kRowCost = 48;       // merge-path weight of one row (in entries)
+constexpr int kStreamUnroll = 4;   // int4 loads in flight per lane
+constexpr int kBrowSmem = 1024;
+
+__device__ __forceinline__ int4 ld_stream_v4(const int32_t* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ int64_t batch_of(const int64_t* sb, const int64_t* gb_, int64_t k,
+                                            int64_t r) {
+  // last b with brow[b] <= r
+  const int64_t* a = k + 1 <= kBrowSmem ? sb : gb_;
+  int64_t lo = 0, hi = k;
+  while (hi - lo > 1) {
+    int64_t mid = (lo + hi) >> 1;
+    if (a[mid] <= r) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+
+// Warp-cooperative processing of one row.  Lanes t < take own pick t; the
+// warp writes the picks whose row-relative index lies in [lo, hi).
+template <bool STREAM>
+__device__ __forceinline__ void sage_row(const SageArgs& A, RunTable& tab, uint64_t key,
+                                         int32_t deg, int64_t fp, int64_t rs, int64_t bb,
+                                         int64_t lo, int64_t hi) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = lane_id();
+  const int32_t take = min(deg, A.s);
+  int64_t myidx = lane;  // row-relative index of my pick (draw order = lane)
+  int32_t rank = lane;   // position among the row's sorted picks
+  if (take < deg) {
+    // ---- stage this degree's replay table (warp-private shared memory)
+    const int32_t slot = A.deg_slot[deg];
+    const int nr = A.run_n[slot];
+    int32_t* j0 = tab.j0;
+    double* s0 = tab.s0;
+    double* dd = tab.d;
+    for (int i = lane; i < nr; i += 32) {
+      j0[i] = A.run_j0[(int64_t)slot * (kMaxRuns + 1) + i];
+      s0[i] = A.run_s0[(int64_t)slot * kMaxRuns + i];
+      dd[i] = A.run_d[(int64_t)slot * kMaxRuns + i];
+    }
+    if (lane == 0) j0[nr] = deg + 1;
+    __syncwarp();
+    tab.nr = nr;
+    // ---- draw t = lane: which live entry (1-based rank j) it selects.
+    // n_live = deg - t, total = S[n_live], target = u * total,
+    // j = first j with S[j] > target, clamped to n_live (sampler.py:176-186)
+    int64_t j = 0;
+    if (lane < take) {
+      const double u = uniform53(A.seed, A.epoch, A.depth, key, (uint64_t)lane);
+      const int64_t n_live = deg - lane;
+      const double total = table_S(tab, n_live);
+      const double target = __dmul_rn(u, total);
+      j = table_first_gt(tab, target);
+      if (j > n_live) j = n_live;
+    }
+    // ---- remove-and-renormalise: draw t takes the j_t-th live index
+    for (int t = 0; t < take; ++t) {
+      const int64_t jt = __shfl_sync(FULL, j, t);
+      int64_t idx = jt - 1;
+      while (true) {
+        const unsigned m = __ballot_sync(FULL, lane < t && myidx <= idx);
+        const int64_t nidx = jt - 1 + __popc(m);
+        if (nidx == idx) break;
+        idx = nidx;
+      }
+      if (lane == t) myidx = idx;
+    }
+    // ---- frontier rows are stored sorted (frontier_from_rows, sampler.py:216)
+    rank = 0;
+    for (int t = 0; t < take; ++t) {
+      const int64_t o = __shfl_sync(FULL, myidx, t);
+      rank += (o < myidx) ? 1 : 0;
+    }
+    __syncwarp();
+  }
+  const bool active = lane < take;
+  int32_t c = 0;
+  bool have = false;
+  if (!STREAM) {
+    if (active) {
+      c = A.col[rs + myidx];
+      have = true;
+    }
+  } else {
+    // ---- P row on chip: stream entries [lo, hi) of A row, catch the picks
+    const int64_t e_lo = rs + lo, e_hi = rs + hi;
+    const int64_t pabs = rs + myidx;
+    const bool want = active && pabs >= e_lo && pabs < e_hi;
+    for (int64_t w0 = e_lo & ~3LL; w0 < e_hi; w0 += 128 * kStreamUnroll) {
+      int4 vals[kStreamUnroll];
+#pragma unroll
+      for (int u = 0; u < kStreamUnroll; ++u) {
+        const int64_t e = w0 + 128 * u + 4 * lane;
+        vals[u] = e < e_hi ? ld_stream_v4(A.col + e) : make_int4(0, 0, 0, 0);
+      }
+      const int64_t off = pabs - w0;
+      const bool mine = want && off >= 0 && off < 128 * kStreamUnroll;
+      if (__any_sync(FULL, mine)) {
+#pragma unroll
+        for (int u = 0; u < kStreamUnroll; ++u) {
+          const int64_t o = off - 128 * u;
+          const int src = (int)((o >> 2) & 31);
+          const int comp = (int)(o & 3);
+          const int x = __shfl_sync(FULL, vals[u].x, src);
+          const int y = __shfl_sync(FULL, vals[u].y, src);
+          const int z = __shfl_sync(FULL, vals[u].z, src);
+          const int w = __shfl_sync(FULL, vals[u].w, src);
+          if (mine && o >= 0 && o < 128) {
+            c = comp == 0 ? x : comp == 1 ? y : comp == 2 ? z : w;
+            have = true;
+          }
+        }
+      }
+    }
+  }
+  if (have) {
+    A.fcol[fp + rank] = c;
+    atomicOr(&A.bitmap[bb * A.nwords + (c >> 5)], 1u << (c & 31));
+  }
+}
+
+template <bool STREAM>
+__global__ void __launch_bounds__(kSampleThreads) k_sage_sample(SageArgs A,
+                                                              const int64_t* __restrict__ R_ptr) {
+  __shared__ int64_t s_brow[kBrowSmem];
+  __shared__ int32_t s_j0[kSampleWarps][kMaxRuns + 1];
+  __shared__ double s_s0[kSampleWarps][kMaxRuns];
+  __shared__ double s_d[kSampleWarps][kMaxRuns];
+  const unsigned FULL = 0xffffffffu;
+  const int64_t R = *R_ptr;
+  const bool brow_in_smem = A.k + 1 <= kBrowSmem;
+  if (brow_in_smem)
+    for (int64_t i = threadIdx.x; i <= A.k; i += blockDim.x) s_brow[i] = A.brow[i];
+  __syncthreads();
+  const int wib = threadIdx.x >> 5, lane = lane_id();
+  const int64_t NW = grid_warps(), w = global_warp();
+  int64_t r_begin, r_end, path_a = 0, path_b = 0;
+  if (STREAM) {
+    const int64_t G = A.gstart[R];
+    const int64_t total = R * kRowCost + G;
+    const int64_t share = (total + NW - 1) / NW;
+    path_a = min(w * share, total);
+    path_b = min(path_a + share, total);
+    if (path_a >= path_b) return;
+    // last r with P_r <= path_a, P_r = r * kRowCost + gstart[r]
+    int64_t lo = 0, hi = R;
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (mid * kRowCost + A.gstart[mid] <= path_a) lo = mid; else hi = mid;
+    }
+    r_begin = lo;
+    // first r with P_r >= path_b
+    lo = r_begin; hi = R;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (mid * kRowCost + A.gstart[mid] >= path_b) hi = mid; else lo = mid + 1;
+    }
+    r_end = lo;
+  } else {
+    const int64_t share = (R + NW - 1) / NW;
+    r_begin = min(w * share, R);
+    r_end = min(r_begin + share, R);
+  }
+  RunTable tab{s_j0[wib], s_s0[wib], s_d[wib], 0};
+  for (int64_t rb = r_begin; rb < r_end; rb += 32) {
+    // batched per-row metadata: lane l describes row rb + l
+    const int64_t r = rb + lane;
+    int32_t deg = 0;
+    int64_t fp = 0, rs = 0, gs = 0, bb = 0, key = 0;
+    if (r < r_end) {
+      const int32_t v = A.rowv[r];
+      deg = A.deg[r];
+      fp = A.fptr[r];
+      rs = A.rowptr[v];
+      if (STREAM) gs = A.gstart[r];
+      bb = batch_of(s_brow, A.brow, A.k, r);
+      const int64_t b0 = brow_in_smem ? s_brow[bb] : A.brow[bb];
+      key = (A.batch_offset + bb) * A.stride + (r - b0);  // global_row_keys, sampler.py:309-322
+    }
+    const int nrows = (int)min((int64_t)32, r_end - rb);
+    for (int i = 0; i < nrows; ++i) {
+      const int32_t d_i = __shfl_sync(FULL, deg, i);
+      if (d_i == 0) continue;  // empty P row: no picks (sample_rows_ordered, sampler.py:202-204)
+      int64_t lo = 0, hi = d_i;
+      if (STREAM) {
+        const int64_t pe = (rb + i) * kRowCost + __shfl_sync(FULL, gs, i) + kRowCost;
+        lo = max(path_a - pe, (int64_t)0);
+        hi = min(path_b - pe, (int64_t)d_i);
+        if (lo >= hi) continue;
+      }
+      sage_row<STREAM>(A, tab, (uint64_t)__shfl_sync(FULL, key, i), d_i,
+                       __shfl_sync(FULL, fp, i), __shfl_sync(FULL, rs, i),
+                       __shfl_sync(FULL, bb, i), lo, hi);
+    }
+  }
+}
+
+// ============================================================== extraction
+
+struct PopF {
+  const uint32_t* bitmap;
+  __device__ int64_t operator()(int64_t i) const { return __popc(bitmap[i]); }
+};
+
+// eoff[b] = fptr[brow[b]] (entry offsets per batch = next layer's batch row
+// offsets); coloff[b] = wpre[b * nwords]; sizes = (R, F, U)
+__global__ void k_sage_layer_meta(const int64_t* __restrict__ brow, int64_t k,
+                                  const int64_t* __restrict__ fptr,
+                                  const int32_t* __restrict__ wpre, int64_t nwords,
+                                  int64_t* __restrict__ eoff, int64_t* __restrict__ coloff,
+                                  int64_t* __restrict__ sizes) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b <= k;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    eoff[b] = fptr[brow[b]];
+    coloff[b] = wpre[b * nwords];
+    if (b == k) {
+      sizes[0] = brow[k];
+      sizes[1] = fptr[brow[k]];
+      sizes[2] = wpre[k * nwords];
+    }
+  }
+}
+
+// acol[e] = block-diagonal column of frontier entry e:
+//   coloff[batch] + rank of fcol[e] among the batch's sorted unique columns
+// (compact_columns sparse.py:352-357 + block_diag sparse.py:321-342)
+__global__ void k_sage_rank(const int64_t* __restrict__ F_ptr, const int64_t* __restrict__ eoff,
+                            int64_t k, const int32_t* __restrict__ fcol,
+                            const uint32_t* __restrict__ bitmap, const int32_t* __restrict__ wpre,
+                            int64_t nwords, int32_t* __restrict__ acol) {
+  __shared__ int64_t s_eoff[kBrowSmem];
+  const bool sm = k + 1 <= kBrowSmem;
+  if (sm)
+    for (int64_t i = threadIdx.x; i <= k; i += blockDim.x) s_eoff[i] = eoff[i];
+  __syncthreads();
+  const int64_t F = *F_ptr;
+  const int64_t* eo = sm ? s_eoff : eoff;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < F;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = k;
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (eo[mid] <= e) lo = mid; else hi = mid;
+    }
+    const int32_t v = fcol[e];
+    const int64_t wi = lo * nwords + (v >> 5);
+    const uint32_t mask = (1u << (v & 31)) - 1u;
+    acol[e] = wpre[wi] + __popc(bitmap[wi] & mask);
+  }
+}
+
+// col_vertices: enumerate set bits in (batch, vertex) order; clears the map.
+__global__ void k_sage_enumerate(int64_t W, int64_t nwords, uint32_t* __restrict__ bitmap,
+                                 const int32_t* __restrict__ wpre, int32_t* __restrict__ colv) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < W;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t x = bitmap[i];
+    if (!x) continue;
+    const int64_t b = i / nwords;
+    const int32_t vb = (int32_t)((i - b * nwords) << 5);
+    int32_t o = wpre[i];
+    while (x) {
+      const int bit = __ffs(x) - 1;
+      colv[o++] = vb + bit;
+      x &= x - 1;
+    }
+    bitmap[i] = 0;
+  }
+}
+
+__global__ void k_set_i64(int64_t* p, int64_t v) { *p = v; }
+
+// ===================================================================== host
+
+static int grid_for(int64_t n, int threads, int cap_blocks) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > cap_blocks) g = cap_blocks;
+  return (int)g;
+}
+
+int graph_build_tables(Graph* g, cudaStream_t st) {
+  // max degree
+  unsigned long long* d_max = nullptr;
+  GB_CUDA(cudaMallocAsync(&d_max, sizeof(unsigned long long), st));
+  GB_CUDA(cudaMemsetAsync(d_max, 0, sizeof(unsigned long long), st));
+  k_degree_max<<<grid_for(g->n, 256, 4 * kNumSMs), 256, 0, st>>>(g->rowptr, g->n, d_max);
+  GB_LAUNCH_CHECK("k_degree_max");
+  unsigned long long h_max = 0;
+  GB_CUDA(cudaMemcpyAsync(&h_max, d_max, sizeof(h_max), cudaMemcpyDeviceToHost, st));
+  GB_CUDA(cudaStreamSynchronize(st));
+  g->max_deg = (int64_t)h_max;
+  const int64_t nd = g->max_deg + 1;
+  int32_t* flags = nullptr;
+  int64_t* pre = nullptr;
+  int64_t* scan_ws = nullptr;
+  int64_t* d_nd = nullptr;
+  GB_CUDA(cudaMallocAsync(&flags, sizeof(int32_t) * nd, st));
+  GB_CUDA(cudaMallocAsync(&pre, sizeof(int64_t) * (nd + 1), st));
+  GB_CUDA(cudaMallocAsync(&scan_ws, sizeof(int64_t) * scan_workspace_elems<int64_t>(nd), st));
+  GB_CUDA(cudaMallocAsync(&d_nd, sizeof(int64_t), st));
+  GB_CUDA(cudaMemsetAsync(flags, 0, sizeof(int32_t) * nd, st));
+  k_set_i64<<<1, 1, 0, st>>>(d_nd, nd);
+  k_degree_flags<<<grid_for(g->n, 256, 8 * kNumSMs), 256, 0, st>>>(g->rowptr, g->n, flags);
+  GB_LAUNCH_CHECK("k_degree_flags");
+  int rc = device_exclusive_scan<int64_t>(d_nd, nd, FlagF{flags}, pre, scan_ws, st);
+  if (rc) return rc;
+  int64_t slots = 0;
+  GB_CUDA(cudaMemcpyAsync(&slots, pre + nd, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  GB_CUDA(cudaStreamSynchronize(st));
+  g->slots = slots;
+  GB_CUDA(cudaMalloc(&g->deg_slot, sizeof(int32_t) * nd));
+  const int64_t sl = slots > 0 ? slots : 1;
+  GB_CUDA(cudaMalloc(&g->slot_deg, sizeof(int32_t) * sl));
+  GB_CUDA(cudaMalloc(&g->run_j0, sizeof(int32_t) * sl * (kMaxRuns + 1)));
+  GB_CUDA(cudaMalloc(&g->run_s0, sizeof(double) * sl * kMaxRuns));
+  GB_CUDA(cudaMalloc(&g->run_d, sizeof(double) * sl * kMaxRuns));
+  GB_CUDA(cudaMalloc(&g->run_n, sizeof(int32_t) * sl));
+  int32_t* d_over = nullptr;
+  GB_CUDA(cudaMallocAsync(&d_over, sizeof(int32_t), st));
+  GB_CUDA(cudaMemsetAsync(d_over, 0, sizeof(int32_t), st));
+  k_degree_slots<<<grid_for(nd, 256, 8 * kNumSMs), 256, 0, st>>>(flags, pre, nd, g->deg_slot,
+                                                                  g->slot_deg);
+  GB_LAUNCH_CHECK("k_degree_slots");
+  if (slots > 0) {
+    k_build_runs<<<grid_for(slots, 64, 1 << 20), 64, 0, st>>>(g->slot_deg, slots, g->run_j0,
+                                                               g->run_s0, g->run_d, g->run_n,
+                                                               d_over);
+    GB_LAUNCH_CHECK("k_build_runs");
+  }
+  int32_t h_over = 0;
+  GB_CUDA(cudaMemcpyAsync(&h_over, d_over, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  GB_CUDA(cudaStreamSynchronize(st));
+  GB_CUDA(cudaFreeAsync(d_max, st));
+  GB_CUDA(cudaFreeAsync(flags, st));
+  GB_CUDA(cudaFreeAsync(pre, st));
+  GB_CUDA(cudaFreeAsync(scan_ws, st));
+  GB_CUDA(cudaFreeAsync(d_nd, st));
+  GB_CUDA(cudaFreeAsync(d_over, st));
+  GB_CUDA(cudaStreamSynchronize(st));
+  if (h_over) {
+    set_error("replay table overflow: a degree needs more than %d runs", kMaxRuns);
+    return GB_ERR_UNSUPPORTED;
+  }
+  return GB_OK;
+}
+
+// ---------------------------------------------------------- workspace plan
+struct SageWs {
+  int32_t* deg;
+  int64_t* gstart;
+  int64_t* scan_ws;
+  uint32_t* bitmap;
+  int32_t* wpre;
+  int64_t* d_W;
+  size_t bytes;
+};
+
+static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static SageWs sage_ws_layout(char* base, int64_t k, int64_t n, int64_t r_cap_max) {
+  SageWs w{};
+  const int64_t nwords = (n + 31) / 32;
+  const int64_t W = k * nwords;
+  const int64_t scan_n = r_cap_max > W ? r_cap_max : W;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { char* p = base ? base + off : nullptr; off += align_up(bytes); return p; };
+  w.deg = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
+  w.gstart = (int64_t*)take(sizeof(int64_t) * (r_cap_max + 1));
+  w.scan_ws = (int64_t*)take(sizeof(int64_t) * scan_workspace_elems<int64_t>(scan_n + 1));
+  w.bitmap = (uint32_t*)take(sizeof(uint32_t) * (W + 1));
+  w.wpre = (int32_t*)take(sizeof(int32_t) * (W + 1));
+  w.d_W = (int64_t*)take(sizeof(int64_t));
+  w.bytes = off;
+  return w;
+}
+
+static int64_t sage_rcap_max(int64_t r1_cap, int32_t layers, const int64_t* fanouts) {
+  int64_t r = r1_cap, mx = r1_cap;
+  for (int32_t l = 0; l + 1 < layers; ++l) {
+    r *= fanouts[l];
+    if (r > mx) mx = r;
+  }
+  return mx;
+}
+
+int sage_workspace(const Graph* g, int64_t k, int64_t r1_cap, int32_t layers,
+                   const int64_t* fanouts, size_t* bytes) {
+  *bytes = sage_ws_layout(nullptr, k, g->n, sage_rcap_max(r1_cap, layers, fanouts)).bytes;
+  return GB_OK;
+}
+
+static int sample_grid(bool stream) {
+  static int occ[2] = {0, 0};
+  int& o = occ[stream ? 1 : 0];
+  if (!o) {
+    if (stream)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_sage_sample<true>, kSampleThreads, 0);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_sage_sample<false>, kSampleThreads, 0);
+    if (o < 1) o = 1;
+  }
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  return o * (sms > 0 ? sms : kNumSMs);
+}
+
+int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d_bverts,
+              int64_t r1_cap, int64_t batch_size, int32_t layers, const int64_t* fanouts,
+              uint64_t seed, uint64_t epoch, int64_t batch_offset, int32_t mode,
+              gb_sage_layer_out* L, int64_t* d_sizes, void* d_ws, size_t ws_bytes,
+              cudaStream_t st) {
+  const bool stream = mode == GB_SAGE_STREAM;
+  const int64_t nwords = (g->n + 31) / 32;
+  const int64_t W = k * nwords;
+  const int64_t rmax = sage_rcap_max(r1_cap, layers, fanouts);
+  SageWs ws = sage_ws_layout((char*)d_ws, k, g->n, rmax);
+  if (ws.bytes > ws_bytes) {
+    set_error("sage workspace too small: need %zu bytes, got %zu", ws.bytes, ws_bytes);
+    return GB_ERR_CAPACITY;
+  }
+  int64_t r_cap = r1_cap;
+  for (int32_t l = 0; l < layers; ++l) {
+    const int64_t f_cap = r_cap * fanouts[l];
+    if (L[l].r_cap < r_cap || L[l].f_cap < f_cap) {
+      set_error("layer %d output too small: need rows %lld entries %lld", (int)l + 1,
+                (long long)r_cap, (long long)f_cap);
+      return GB_ERR_CAPACITY;
+    }
+    if (f_cap >= (int64_t)1 << 31) {
+      set_error("layer %d bound %lld entries exceeds int32 indexing", (int)l + 1, (long long)f_cap);
+      return GB_ERR_UNSUPPORTED;
+    }
+    r_cap = f_cap;
+  }
+  GB_CUDA(cudaMemsetAsync(ws.bitmap, 0, sizeof(uint32_t) * (W + 1), st));
+  k_set_i64<<<1, 1, 0, st>>>(ws.d_W, W);
+  int64_t stride = batch_size;
+  r_cap = r1_cap;
+  for (int32_t l = 0; l < layers; ++l) {
+    const int32_t d = l + 1;
+    if (l > 0) stride *= fanouts[l - 1];
+    gb_sage_layer_out& o = L[l];
+    const int32_t* rowv = l == 0 ? d_bverts : L[l - 1].fcol;
+    const int64_t* brow = l == 0 ? d_bptr : L[l - 1].eoff;
+    const int64_t* R_ptr = brow + k;
+    const int32_t s = (int32_t)fanouts[l];
+    k_sage_prep<<<grid_for(r_cap, 256, 16 * kNumSMs), 256, 0, st>>>(R_ptr, rowv, g->rowptr, ws.deg);
+    GB_LAUNCH_CHECK("k_sage_prep");
+    int rc = device_exclusive_scan<int64_t>(R_ptr, r_cap, TakeF{ws.deg, s}, o.fptr, ws.scan_ws, st);
+    if (rc) return rc;
+    if (stream) {
+      rc = device_exclusive_scan<int64_t>(R_ptr, r_cap, DegF{ws.deg}, ws.gstart, ws.scan_ws, st);
+      if (rc) return rc;
+    }
+    SageArgs A{};
+    A.rowptr = g->rowptr; A.col = g->col;
+    A.deg_slot = g->deg_slot; A.run_j0 = g->run_j0; A.run_s0 = g->run_s0; A.run_d = g->run_d;
+    A.run_n = g->run_n;
+    A.rowv = rowv; A.deg = ws.deg; A.fptr = o.fptr; A.gstart = ws.gstart;
+    A.brow = brow; A.k = k; A.s = s; A.stride = stride; A.batch_offset = batch_offset;
+    A.seed = seed; A.epoch = epoch; A.depth = (uint64_t)d;
+    A.bitmap = ws.bitmap; A.nwords = nwords; A.fcol = o.fcol;
+    if (stream)
+      k_sage_sample<true><<<sample_grid(true), kSampleThreads, 0, st>>>(A, R_ptr);
+    else
+      k_sage_sample<false><<<sample_grid(false), kSampleThreads, 0, st>>>(A, R_ptr);
+    GB_LAUNCH_CHECK("k_sage_sample");
+    rc = device_exclusive_scan<int64_t>(ws.d_W, W, PopF{ws.bitmap}, ws.wpre, ws.scan_ws, st);
+    if (rc) return rc;
+    int64_t* sizes = d_sizes + 3 * l;
+    k_sage_layer_meta<<<grid_for(k + 1, 128, 64), 128, 0, st>>>(brow, k, o.fptr, ws.wpre, nwords,
+                                                                 o.eoff, o.coloff, sizes);
+    GB_LAUNCH_CHECK("k_sage_layer_meta");
+    const int64_t f_cap = r_cap * s;
+    k_sage_rank<<<grid_for(f_cap, 256, 16 * kNumSMs), 256, 0, st>>>(
+        sizes + 1, o.eoff, k, o.fcol, ws.bitmap, ws.wpre, nwords, o.acol);
+    GB_LAUNCH_CHECK("k_sage_rank");
+    k_sage_enumerate<<<grid_for(W, 256, 16 * kNumSMs), 256, 0, st>>>(W, nwords, ws.bitmap, ws.wpre,
+                                                                       o.colv);
+    GB_LAUNCH_CHECK("k_sage_enumerate");
+    r_cap = f_cap;
+  }
+  return GB_OK;
+}
+
+}  // namespace gb

@@ -1,0 +1,133 @@
+"""Device orchestration of the bulk samplers: buffer planning, C-ABI launches,
+and conversion of device results into `SampledEpoch` objects.
+
+`SageBulk` owns every buffer of one bulk shape (graph, k, rows, fanouts);
+`launch()` is a single host call that enqueues all layers on the current
+stream without any host synchronisation, so repeated bulks can be captured
+in a CUDA graph (bench.py does).  Results are read back only when
+`epoch()` is called.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .errors import ContractViolation
+from .sampler import LayerSample, SampledEpoch, SamplerConfig, SamplerKind, _flatten_batches
+from .sparse import Graph
+
+MODES = {"stream": _lib.GB_SAGE_STREAM, "pfree": _lib.GB_SAGE_PFREE}
+
+
+def sage_caps(r1_cap, fanouts):
+    """Upper bounds (rows, entries) per layer: R_{l+1} = F_l <= R_l * s_l."""
+    caps, r = [], int(r1_cap)
+    for s in fanouts:
+        caps.append((r, r * int(s)))
+        r = r * int(s)
+    return caps
+
+
+class SageBulk:
+    """Reusable device buffers + launcher for SAGE bulks of one shape."""
+
+    def __init__(self, dg, k, r1_cap, batch_size, fanouts, mode="stream"):
+        import torch
+
+        self.dg, self.k, self.r1_cap = dg, int(k), int(r1_cap)
+        self.batch_size = int(batch_size)
+        self.fanouts = tuple(int(s) for s in fanouts)
+        if mode not in MODES:
+            raise ContractViolation(f"unknown SAGE mode {mode!r}")
+        self.mode = mode
+        L = len(self.fanouts)
+        dev = torch.device("cuda")
+        self.caps = sage_caps(self.r1_cap, self.fanouts)
+        self.out = []
+        self.c_layers = (_lib.SageLayerOut * L)()
+        for l, (rc, fc) in enumerate(self.caps):
+            o = {
+                "fptr": torch.empty(rc + 1, dtype=torch.int64, device=dev),
+                "fcol": torch.empty(max(fc, 1), dtype=torch.int32, device=dev),
+                "acol": torch.empty(max(fc, 1), dtype=torch.int32, device=dev),
+                "colv": torch.empty(max(fc, 1), dtype=torch.int32, device=dev),
+                "eoff": torch.empty(self.k + 1, dtype=torch.int64, device=dev),
+                "coloff": torch.empty(self.k + 1, dtype=torch.int64, device=dev),
+            }
+            self.out.append(o)
+            c = self.c_layers[l]
+            for name in ("fptr", "fcol", "acol", "colv", "eoff", "coloff"):
+                setattr(c, name, o[name].data_ptr())
+            c.r_cap, c.f_cap = rc, fc
+        self.h_fanouts = np.ascontiguousarray(self.fanouts, dtype=np.int64)
+        nbytes = ctypes.c_size_t()
+        _lib.check(_lib.lib().gb_sage_bulk_workspace(
+            dg.handle, self.k, self.r1_cap, L, self.h_fanouts.ctypes.data,
+            ctypes.byref(nbytes)), "gb_sage_bulk_workspace")
+        self.ws = torch.empty(max(int(nbytes.value), 1), dtype=torch.uint8, device=dev)
+        self.sizes = torch.zeros(3 * L, dtype=torch.int64, device=dev)
+
+    def launch(self, d_bptr, d_bverts, seed, epoch, batch_offset, stream=None):
+        """Enqueue the whole bulk (all layers) on `stream`; no host sync."""
+        L = len(self.fanouts)
+        _lib.check(_lib.lib().gb_sage_bulk(
+            self.dg.handle, self.k, _lib.ptr(d_bptr), _lib.ptr(d_bverts), self.r1_cap,
+            self.batch_size, L, self.h_fanouts.ctypes.data, int(seed), int(epoch),
+            int(batch_offset), MODES[self.mode], self.c_layers, _lib.ptr(self.sizes),
+            _lib.ptr(self.ws), self.ws.numel(), _lib.stream_ptr(stream)), "gb_sage_bulk")
+
+    def layers(self, d_bptr, d_bverts, sizes=None):
+        """Device-resident LayerSamples (views sized by the per-layer counts)."""
+        if sizes is None:
+            sizes = self.sizes.cpu().numpy()
+        n = self.dg.n
+        out = []
+        rowv, brow = d_bverts, d_bptr
+        for l in range(len(self.fanouts)):
+            R, F, U = (int(x) for x in sizes[3 * l: 3 * l + 3])
+            o = self.out[l]
+            dev = {
+                "frontier_shape": (R, n), "frontier_ptr": o["fptr"][: R + 1],
+                "frontier_col": o["fcol"][:F],
+                "adj_shape": (R, U), "adj_ptr": o["fptr"][: R + 1], "adj_col": o["acol"][:F],
+                "rowv_off": brow, "rowv_cat": rowv[:R],
+                "colv_off": o["coloff"], "colv_cat": o["colv"][:U],
+                "sampv_off": o["eoff"], "sampv_cat": o["fcol"][:F],
+            }
+            out.append(LayerSample(l + 1, device=dev, n=n))
+            rowv, brow = o["fcol"], o["eoff"]
+        return out
+
+
+def upload_batches(batches, n, batch_size=None, sort_within=False):
+    """Validate batches on the host (reference _flatten_batches checks) and
+    upload (offsets int64, vertices int32)."""
+    import torch
+
+    cat, off = _flatten_batches(batches, n, sort_within=sort_within)
+    if batch_size is not None and len(batches) and int(np.max(np.diff(off))) > batch_size:
+        raise ContractViolation("actual rows exceed the nominal stride")
+    d_off = torch.as_tensor(off).cuda()
+    d_cat = torch.as_tensor(cat.astype(np.int32)).cuda() if cat.size else torch.zeros(
+        1, dtype=torch.int32, device="cuda")
+    return d_off, d_cat, int(off[-1])
+
+
+def sage_epoch(G: Graph, cfg: SamplerConfig, batches, epoch, batch_offset, mode="stream"):
+    dg = G.device()
+    d_off, d_cat, r1 = upload_batches(batches, G.n, cfg.batch_size)
+    bulk = SageBulk(dg, len(batches), max(r1, 1), cfg.batch_size, cfg.fanouts, mode=mode)
+    bulk.launch(d_off, d_cat, cfg.seed, epoch, batch_offset)
+    layers = bulk.layers(d_off, d_cat)
+    return SampledEpoch(SamplerKind.SAGE, epoch, batches, layers, cfg.layers)
+
+
+def ladies_epoch(G, cfg, batches, epoch, batch_offset):
+    raise NotImplementedError("LADIES device path: see engine_ladies")
+
+
+def sample_epoch_generic(G, cfg, batches, epoch, batch_offset, prob_spgemm):
+    raise NotImplementedError("prob_spgemm hook path")

@@ -1,0 +1,273 @@
+"""CSR containers and the device graph.
+
+`SparseMatrix` and `Graph` keep the reference's value semantics
+(`pkg/src/gnnbulk/sparse.py:31-227`): canonical CSR with int64 offsets and
+columns, float64 values, strictly increasing columns per row, frozen
+arrays, bitwise `equals`.  They are the host-side *compatibility edge*: the
+sampler itself runs on the device through `DeviceGraph`, which holds the
+adjacency as int64 row offsets + int32 columns in HBM (values are implicit
+1.0) together with the exact-replay tables built by the C ABI.
+
+The sparse *kernels* of the reference module (spgemm, normalisation,
+extraction helpers) live in `paper_2311_02909_b200.ops` and run on the GPU.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .errors import ContractViolation
+
+INDEX_DTYPE = np.int64
+VALUE_DTYPE = np.float64
+
+
+def _frozen(a, dtype):
+    out = np.ascontiguousarray(np.asarray(a, dtype=dtype))
+    out.setflags(write=False)
+    return out
+
+
+class SparseMatrix:
+    """Immutable canonical CSR matrix (reference `sparse.py:31-191`)."""
+
+    __slots__ = ("n_rows", "n_cols", "row_offsets", "col_indices", "values")
+
+    def __init__(self, n_rows, n_cols, row_offsets, col_indices, values, validate=True):
+        self.n_rows = int(n_rows)
+        self.n_cols = int(n_cols)
+        self.row_offsets = _frozen(row_offsets, INDEX_DTYPE)
+        self.col_indices = _frozen(col_indices, INDEX_DTYPE)
+        self.values = _frozen(values, VALUE_DTYPE)
+        if validate:
+            self.check()
+
+    # -- invariants (reference sparse.py:52-77) --------------------------------
+    def check(self):
+        if self.n_rows < 0 or self.n_cols < 0:
+            raise ContractViolation("matrix dimensions must be non-negative")
+        ptr, col = self.row_offsets, self.col_indices
+        nnz = col.shape[0]
+        if ptr.shape != (self.n_rows + 1,):
+            raise ContractViolation("row_offsets must have length n_rows + 1")
+        if ptr[0] != 0 or ptr[-1] != nnz:
+            raise ContractViolation("row_offsets must start at 0 and end at nnz")
+        if self.n_rows and np.min(np.diff(ptr)) < 0:
+            raise ContractViolation("row_offsets must be non-decreasing")
+        if self.values.shape[0] != nnz:
+            raise ContractViolation("col_indices and values must have equal length")
+        if nnz:
+            if col.min() < 0 or col.max() >= self.n_cols:
+                raise ContractViolation("column index out of range")
+            # a non-increasing step is legal only where a new row starts
+            row_of = np.repeat(np.arange(self.n_rows), np.diff(ptr))
+            same_row = row_of[1:] == row_of[:-1]
+            if np.any(same_row & (col[1:] <= col[:-1])):
+                raise ContractViolation("column indices must be sorted and unique per row")
+        if not np.isfinite(self.values).all():
+            raise ContractViolation("values must be finite")
+
+    # -- constructors -------------------------------------------------------------
+    @classmethod
+    def from_coo(cls, n_rows, n_cols, rows, cols, vals, dedup="sum"):
+        """Triplets -> canonical CSR; duplicates summed ('sum', in input order)
+        or collapsed to the first occurrence's pattern entry ('first')."""
+        rows = np.asarray(rows, dtype=INDEX_DTYPE).ravel()
+        cols = np.asarray(cols, dtype=INDEX_DTYPE).ravel()
+        vals = np.asarray(vals, dtype=VALUE_DTYPE).ravel()
+        if rows.size and (rows.min() < 0 or rows.max() >= n_rows):
+            raise ContractViolation("row index out of range")
+        if cols.size and (cols.min() < 0 or cols.max() >= n_cols):
+            raise ContractViolation("column index out of range")
+        order = np.lexsort((cols, rows)) if dedup == "first" else np.argsort(
+            rows * max(int(n_cols), 1) + cols, kind="stable")
+        r, c, v = rows[order], cols[order], vals[order]
+        start = np.ones(r.shape[0], dtype=bool)
+        start[1:] = (r[1:] != r[:-1]) | (c[1:] != c[:-1])
+        seg = np.flatnonzero(start)
+        if dedup == "first":
+            v = v[seg]
+        else:
+            v = np.add.reduceat(v, seg) if seg.size else v[:0]
+        r, c = r[seg], c[seg]
+        ptr = np.zeros(int(n_rows) + 1, dtype=INDEX_DTYPE)
+        np.cumsum(np.bincount(r, minlength=int(n_rows)), out=ptr[1:])
+        return cls(n_rows, n_cols, ptr, c, v)
+
+    @classmethod
+    def from_dense(cls, array):
+        a = np.asarray(array, dtype=VALUE_DTYPE)
+        r, c = np.nonzero(a)
+        return cls.from_coo(a.shape[0], a.shape[1], r, c, a[r, c])
+
+    @classmethod
+    def from_scipy(cls, mat, shape=None):
+        csr = mat.tocsr()
+        csr.sort_indices()
+        n_rows, n_cols = shape if shape is not None else csr.shape
+        return cls(n_rows, n_cols, csr.indptr, csr.indices, csr.data)
+
+    @classmethod
+    def empty(cls, n_rows, n_cols):
+        return cls(n_rows, n_cols, np.zeros(int(n_rows) + 1, dtype=INDEX_DTYPE), [], [])
+
+    @classmethod
+    def identity(cls, n):
+        return cls(n, n, np.arange(n + 1), np.arange(n), np.ones(n))
+
+    # -- accessors ------------------------------------------------------------------
+    @property
+    def nnz(self):
+        return int(self.col_indices.shape[0])
+
+    @property
+    def shape(self):
+        return (self.n_rows, self.n_cols)
+
+    def row_slice(self, start, stop):
+        if not (0 <= start <= stop <= self.n_rows):
+            raise ContractViolation(f"row slice [{start}, {stop}) out of range")
+        a, b = int(self.row_offsets[start]), int(self.row_offsets[stop])
+        return SparseMatrix(stop - start, self.n_cols, self.row_offsets[start:stop + 1] - a,
+                            self.col_indices[a:b], self.values[a:b], validate=False)
+
+    def row_cols(self, r):
+        return self.col_indices[self.row_offsets[r]:self.row_offsets[r + 1]]
+
+    def row_vals(self, r):
+        return self.values[self.row_offsets[r]:self.row_offsets[r + 1]]
+
+    def row_nnz(self):
+        return np.diff(self.row_offsets)
+
+    def nonzero_cols(self):
+        return np.unique(self.col_indices)
+
+    def to_scipy(self):
+        import scipy.sparse as sp
+
+        return sp.csr_matrix((self.values, self.col_indices, self.row_offsets),
+                             shape=self.shape)
+
+    def to_dense(self):
+        out = np.zeros(self.shape, dtype=VALUE_DTYPE)
+        rows = np.repeat(np.arange(self.n_rows), self.row_nnz())
+        out[rows, self.col_indices] = self.values
+        return out
+
+    def equals(self, other):
+        return (self.shape == other.shape
+                and np.array_equal(self.row_offsets, other.row_offsets)
+                and np.array_equal(self.col_indices, other.col_indices)
+                and np.array_equal(self.values, other.values))
+
+    def __repr__(self):
+        return f"SparseMatrix({self.n_rows}x{self.n_cols}, nnz={self.nnz})"
+
+
+class Graph:
+    """Unweighted graph as an n x n 0/1 adjacency (reference `sparse.py:194-227`).
+
+    The device copy (`device()`) is created on first use and cached.
+    """
+
+    __slots__ = ("adjacency", "n", "_dev")
+
+    def __init__(self, adjacency: SparseMatrix):
+        if adjacency.n_rows != adjacency.n_cols:
+            raise ContractViolation("adjacency matrix must be square")
+        if adjacency.nnz and not np.all(adjacency.values == 1.0):
+            raise ContractViolation("adjacency values must all equal 1.0")
+        self.adjacency = adjacency
+        self.n = adjacency.n_rows
+        self._dev = None
+
+    @classmethod
+    def from_edges(cls, n, sources, targets):
+        src = np.asarray(sources, dtype=INDEX_DTYPE)
+        dst = np.asarray(targets, dtype=INDEX_DTYPE)
+        return cls(SparseMatrix.from_coo(n, n, src, dst, np.ones(src.shape[0]), dedup="first"))
+
+    @classmethod
+    def from_device(cls, dev: "DeviceGraph"):
+        """Wrap a graph that only lives on the device (e.g. GPU R-MAT)."""
+        g = cls.__new__(cls)
+        g._dev = dev
+        g.n = dev.n
+        g.adjacency = None
+        return g
+
+    def host_adjacency(self) -> SparseMatrix:
+        if self.adjacency is None:
+            rowptr = self._dev.rowptr.cpu().numpy()
+            col = self._dev.col[: self._dev.nnz].cpu().numpy()
+            self.adjacency = SparseMatrix(self.n, self.n, rowptr, col,
+                                          np.ones(col.shape[0]), validate=False)
+        return self.adjacency
+
+    def device(self) -> "DeviceGraph":
+        if self._dev is None:
+            A = self.adjacency
+            self._dev = DeviceGraph.upload(self.n, A.row_offsets, A.col_indices)
+        return self._dev
+
+    def degrees(self):
+        return self.host_adjacency().row_nnz()
+
+    def has_edge(self, u, v):
+        cols = self.host_adjacency().row_cols(u)
+        i = np.searchsorted(cols, v)
+        return bool(i < len(cols) and cols[i] == v)
+
+    def __repr__(self):
+        nnz = self.adjacency.nnz if self.adjacency is not None else self._dev.nnz
+        return f"Graph(n={self.n}, edges={nnz})"
+
+
+class DeviceGraph:
+    """Adjacency in HBM: rowptr int64[n+1], col int32[nnz + GB_COL_PAD]
+    (16-B aligned, padded for 16-B streaming loads), plus the C-ABI handle
+    owning the per-degree exact-replay tables."""
+
+    def __init__(self, n, rowptr, col, nnz):
+        from . import _lib
+
+        self.n = int(n)
+        self.nnz = int(nnz)
+        self.rowptr = rowptr
+        self.col = col
+        h = _lib.ctypes.c_void_p()
+        _lib.check(_lib.lib().gb_graph_create(self.n, self.nnz, _lib.ptr(rowptr), _lib.ptr(col),
+                                              _lib.stream_ptr(), _lib.ctypes.byref(h)),
+                   "gb_graph_create")
+        self.handle = h
+        md, sl = _lib.ctypes.c_int64(), _lib.ctypes.c_int64()
+        _lib.check(_lib.load().gb_graph_info(h, _lib.ctypes.byref(md), _lib.ctypes.byref(sl)))
+        self.max_degree = int(md.value)
+        self.table_slots = int(sl.value)
+
+    @classmethod
+    def upload(cls, n, rowptr, col):
+        import torch
+
+        from . import _lib
+
+        nnz = int(len(col))
+        d_ptr = torch.as_tensor(np.array(rowptr, dtype=np.int64)).cuda()
+        d_col = torch.zeros(nnz + _lib.GB_COL_PAD, dtype=torch.int32, device="cuda")
+        if nnz:
+            d_col[:nnz] = torch.as_tensor(np.asarray(col, dtype=np.int32)).cuda()
+        return cls(n, d_ptr, d_col, nnz)
+
+    @classmethod
+    def from_tensors(cls, n, rowptr, col_padded, nnz):
+        return cls(n, rowptr, col_padded, nnz)
+
+    def __del__(self):
+        try:
+            from . import _lib
+
+            if getattr(self, "handle", None):
+                _lib.load().gb_graph_destroy(self.handle)
+        except Exception:
+            pass

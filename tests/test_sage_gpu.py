@@ -1,0 +1,134 @@
+"""Parity of the CUDA SAGE bulk sampler (both kernel modes) with the oracle.
+
+Bit-exact: the reference's own outputs (golden fixtures, reference run with
+the injected uniforms) and the C oracle on seeded random graphs."""
+
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from oracle import oracle as O
+from oracle.philox import uniforms as np_uniforms
+
+pytestmark = pytest.mark.gpu
+
+MODES = ("stream", "pfree")
+
+
+def _pkg():
+    import paper_2311_02909_b200 as gb
+
+    return gb
+
+
+def _graph(n, rowptr, col):
+    gb = _pkg()
+    A = gb.SparseMatrix(n, n, rowptr, col, np.ones(len(col)), validate=False)
+    return gb.Graph(A)
+
+
+def test_device_uniforms_match_oracle():
+    from paper_2311_02909_b200 import ops
+
+    rows = np.array([0, 1, 5, 2**33 + 7, 16_700_000_000] * 8)
+    t = np.repeat(np.arange(8), 5)
+    got = ops.uniforms(3, 1, 2, rows, t)
+    assert np.array_equal(got, np_uniforms(3, 1, 2, rows, t))
+
+
+SAGE_GOLDEN = [p for p in sorted(glob.glob(os.path.join(GOLDEN, "epoch_*sage*.npz")))]
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("path", SAGE_GOLDEN, ids=os.path.basename)
+def test_sage_matches_reference_golden(path, mode):
+    gb = _pkg()
+    g, want = O.load_golden(path)
+    G = _graph(g["n"], g["rowptr"], g["col"])
+    cfg = gb.SamplerConfig.sage(g["layers_cfg"], g["batch_size"], tuple(g["fanouts"]),
+                                bulk_count=len(g["batches"]), seed=g["seed"])
+    ep = gb.sample_epoch_bulk(G, cfg, g["batches"], epoch=g["epoch"],
+                              batch_offset=g["batch_offset"], mode=mode)
+    assert O.compare_epochs(want, ep.to_arrays()) == []
+    assert ep.spgemm_calls == g["spgemm_calls"]
+
+
+def _rmat(scale, m, seed):
+    rng = np.random.default_rng(seed)
+    n = 1 << scale
+    u = np.zeros(4 * m, np.int64)
+    v = np.zeros(4 * m, np.int64)
+    for lvl in range(scale):
+        r = rng.random(4 * m)
+        u |= (r >= 0.76).astype(np.int64) << lvl
+        v |= (((r >= 0.57) & (r < 0.76)) | (r >= 0.95)).astype(np.int64) << lvl
+    keep = u != v
+    src = np.concatenate([u[keep], v[keep]])
+    dst = np.concatenate([v[keep], u[keep]])
+    key = np.unique(src * n + dst)
+    rowptr = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(key // n, minlength=n), out=rowptr[1:])
+    return n, rowptr, (key % n).astype(np.int64)
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("case", range(4))
+def test_sage_matches_oracle_random(case, mode):
+    gb = _pkg()
+    rng = np.random.default_rng(100 + case)
+    n, rowptr, col = _rmat(12 + case % 2, 30000 * (1 + case), seed=case)
+    G = _graph(n, rowptr, col)
+    b = [17, 64, 100, 256][case]
+    k = [1, 3, 8, 5][case]
+    fan = [(15, 10, 5), (3, 2), (25, 1, 32), (10, 10)][case]
+    batches = [rng.permutation(n)[: rng.integers(1, b + 1)] for _ in range(k)]
+    cfg = gb.SamplerConfig.sage(len(fan), b, fan, bulk_count=k, seed=case * 7 + 1)
+    ep = gb.sample_epoch_bulk(G, cfg, batches, epoch=case, batch_offset=3 * case, mode=mode)
+    want = O.sage_bulk(n, rowptr, col, batches, b, fan, case * 7 + 1, case, 3 * case)
+    assert O.compare_epochs(want, ep.to_arrays()) == []
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_sage_edge_cases(mode):
+    gb = _pkg()
+    # isolated vertices, degree == fanout, degree < fanout, duplicates in a
+    # batch, an empty batch
+    n = 40
+    src = [0, 0, 0, 1, 1, 2, 3, 3, 3, 3, 3]
+    dst = [1, 2, 3, 0, 4, 0, 5, 6, 7, 8, 9]
+    G = gb.Graph.from_edges(n, src, dst)
+    A = G.adjacency
+    batches = [[0, 1, 2, 3, 39], [], [3, 3, 39, 0]]
+    for fan in ((3, 2), (1, 1), (5, 32)):
+        cfg = gb.SamplerConfig.sage(2, 5, fan, bulk_count=3, seed=9)
+        ep = gb.sample_epoch_bulk(G, cfg, batches, mode=mode)
+        want = O.sage_bulk(n, A.row_offsets, A.col_indices, batches, 5, fan, 9)
+        assert O.compare_epochs(want, ep.to_arrays()) == []
+
+
+def test_sage_host_fields_match_reference_types():
+    gb = _pkg()
+    g, want = O.load_golden(os.path.join(GOLDEN, "epoch_fig_sage.npz"))
+    G = _graph(g["n"], g["rowptr"], g["col"])
+    cfg = gb.SamplerConfig.sage(2, 2, (2, 2), seed=3)
+    ep = gb.sample_epoch_bulk(G, cfg, [[1, 5]])
+    layer = ep.layers[0]
+    assert layer.frontier.shape == (2, 6)
+    assert layer.adjacency.n_rows == 2
+    assert np.array_equal(ep.deepest_frontier(0), ep.layers[-1].sampled_vertices[0])
+    assert all(isinstance(v, np.ndarray) for v in layer.col_vertices)
+    same = gb.sample_epoch_bulk(G, cfg, [[1, 5]], mode="pfree")
+    assert ep.equals(same)
+
+
+def test_sage_rejects_bad_batches():
+    gb = _pkg()
+    G = gb.Graph.from_edges(6, [0, 1], [1, 0])
+    cfg = gb.SamplerConfig.sage(1, 2, 2)
+    with pytest.raises(gb.ContractViolation):
+        gb.sample_epoch_bulk(G, cfg, [[6]])
+    with pytest.raises(gb.ContractViolation):
+        gb.sample_epoch_bulk(G, cfg, [[0, 1, 2]])  # longer than batch_size
