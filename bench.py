@@ -1,0 +1,432 @@
+"""Benchmark: sampled minibatches/s of the 3-layer GraphSAGE (15,10,5) bulk
+sampler (BASELINE.json metric; workload = configs[1]: ogbn-products-shape
+synthetic R-MAT, b=1024, k=64 per GPU).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload products|cfg1|papers] [--mode stream|pfree]
+
+One step = one bulk: all 3 layers (P = Q^l A formed on chip, norm, exact
+keyed ITS, extraction) for the k minibatches of this rank, inputs resident in
+HBM.  Multi-GPU (torchrun): replicated graph, disjoint contiguous batch
+ranges per rank (dist.py:417-429 replicated mode), no data-path collective
+-> weak scaling; time = max over ranks of the per-rank device time.
+
+Timing: W warm-up bulks, then K bulks each bracketed by CUDA events on the
+launching stream (one CUDA-graph replay per bulk); between bulks a 256 MiB
+buffer is written to flush L2 (outside the events).  nvidia-smi clocks are
+sampled during the timed region.  Rank 0 prints one JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "sampled minibatches/sec (3-layer SAGE, k-batch bulk)"
+UNIT = "minibatches/s"
+FANOUTS = (15, 10, 5)
+BATCH = 1024
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--workload", default="products", choices=["products", "cfg1", "papers"])
+    p.add_argument("--k", type=int, default=None, help="minibatches per bulk per GPU")
+    p.add_argument("--mode", default="stream", choices=["stream", "pfree"])
+    p.add_argument("--cpu-seconds", type=float, default=15.0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-pfree", action="store_true")
+    return p.parse_args()
+
+
+def default_k(workload):
+    return 8 if workload == "cfg1" else 64
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    def __init__(self):
+        self.proc = None
+        self.path = os.path.join(REPO, "gpurun_out", f"clocks_{os.getpid()}.csv")
+
+    def start(self, index):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ helpers
+
+def make_batches_for(n, k_total):
+    from paper_2311_02909_b200.pipeline import make_batches
+
+    return make_batches(np.arange(n), BATCH, seed=0, epoch=0)[:k_total]
+
+
+def layer_stats(bulk, dg, sizes):
+    """R, G (gathered entries = sum of row degrees), F, U per layer."""
+    import torch
+
+    out = []
+    rowv = None
+    for l in range(len(FANOUTS)):
+        R, F, U = (int(x) for x in sizes[3 * l:3 * l + 3])
+        if l == 0:
+            rv = bulk._bverts[:R].long()
+        else:
+            rv = bulk.out[l - 1]["fcol"][:R].long()
+        G = int((dg.rowptr[rv + 1] - dg.rowptr[rv]).sum().item()) if R else 0
+        out.append({"R": R, "G": G, "F": F, "U": U})
+        del rv
+    del rowv
+    torch.cuda.synchronize()
+    return out
+
+
+def sage_bytes(st):
+    """SURVEY.md §8(d) SAGE algorithmic bytes per bulk: sum_l 28R + 4G + 12F + 4U + 8."""
+    return sum(28 * s["R"] + 4 * s["G"] + 12 * s["F"] + 4 * s["U"] + 8 for s in st)
+
+
+def sample_kernel_bytes(s, mode):
+    """Algorithmic bytes of one sample-kernel launch:
+    stream: 20 B/row (vertex id + row_ptr pair) + 4 B/gathered entry + 4 B/pick;
+    pfree:  20 B/row + 4 B read + 4 B written per pick."""
+    if mode == "stream":
+        return 20 * s["R"] + 4 * s["G"] + 4 * s["F"]
+    return 20 * s["R"] + 8 * s["F"]
+
+
+def oracle_prefix(layers, kc):
+    """Restrict per-layer arrays of a k-batch bulk to its first kc batches."""
+    out = []
+    for a in layers:
+        R = int(a["rowv_off"][kc])
+        F = int(a["sampv_off"][kc])
+        U = int(a["colv_off"][kc])
+        out.append({
+            "frontier_shape": np.array([R, a["frontier_shape"][1]]),
+            "frontier_ptr": a["frontier_ptr"][:R + 1], "frontier_col": a["frontier_col"][:F],
+            "adj_shape": np.array([R, U]), "adj_ptr": a["adj_ptr"][:R + 1],
+            "adj_col": a["adj_col"][:F],
+            "rowv_off": a["rowv_off"][:kc + 1], "rowv_cat": a["rowv_cat"][:R],
+            "colv_off": a["colv_off"][:kc + 1], "colv_cat": a["colv_cat"][:U],
+            "sampv_off": a["sampv_off"][:kc + 1], "sampv_cat": a["sampv_cat"][:F],
+        })
+    return out
+
+
+def cpu_baseline(host_graph, batches, seconds, gpu_layers=None):
+    """Oracle port (oracle/, C + OpenMP, all host threads) on a bounded sample
+    of the same workload: the first kc batches (batch_offset 0).  Also checks
+    the GPU bulk's first kc batches against it bit for bit."""
+    from oracle import oracle as O
+
+    n, rowptr, col = host_graph
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    O.sage_bulk(n, rowptr, col, batches[:1], BATCH, FANOUTS, 0, 0, 0, threads=threads)
+    t1 = time.perf_counter() - t0
+    kc = int(max(1, min(len(batches), seconds / max(t1, 1e-3))))
+    t0 = time.perf_counter()
+    want = O.sage_bulk(n, rowptr, col, batches[:kc], BATCH, FANOUTS, 0, 0, 0, threads=threads)
+    dt = time.perf_counter() - t0
+    parity = None
+    if gpu_layers is not None:
+        errs = O.compare_epochs(want, oracle_prefix(gpu_layers, kc))
+        parity = "bit-exact" if not errs else f"MISMATCH: {errs[:3]}"
+    return {"value": kc / dt, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"first {kc} of the bulk's minibatches (batch_offset 0), same graph; "
+                      f"{dt:.1f} s"}, kc, parity
+
+
+# ------------------------------------------------------------------ arms
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle port of the reference CPU sampler on the
+    host cores, rank 0 only, same graph/batches/metric."""
+    if rank != 0:
+        return
+    import torch
+
+    from paper_2311_02909_b200 import graphgen
+
+    n, m, sym = graphgen.SHAPES[args.workload]
+    dg = graphgen.rmat_device_graph(n, m, symmetric=sym, seed=0)  # input generation only
+    host = (n, dg.rowptr.cpu().numpy(), dg.col[:dg.nnz].cpu().numpy())
+    del dg
+    torch.cuda.empty_cache()
+    k = args.k or default_k(args.workload)
+    batches = make_batches_for(n, k)
+    from oracle import oracle as O
+
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    O.sage_bulk(n, host[1], host[2], batches[:1], BATCH, FANOUTS, 0, 0, 0, threads=threads)
+    t1 = time.perf_counter() - t0
+    per_step = max(10.0, min(60.0, 150.0 / max(1, args.steps + args.warmup)))
+    kc = int(max(1, min(k, per_step / max(t1, 1e-3))))
+    times = []
+    for i in range(args.warmup + args.steps):
+        lo = (i * kc) % max(1, k - kc + 1)
+        t0 = time.perf_counter()
+        O.sage_bulk(n, host[1], host[2], batches[lo:lo + kc], BATCH, FANOUTS, 0, 0, lo,
+                    threads=threads)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    T = float(np.sum(times))
+    value = kc * len(times) / T
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{args.workload}-shape R-MAT, GraphSAGE (15,10,5), b=1024",
+                   "k_per_step": kc, "n": n, "nnz": int(len(host[2]))},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{kc} minibatches per step of the {k}-minibatch bulk"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    import paper_2311_02909_b200 as gb
+    from paper_2311_02909_b200 import _lib, graphgen
+    from paper_2311_02909_b200.engine import BulkSampler, SageBulk
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    n, m, sym = graphgen.SHAPES[args.workload]
+    t0 = time.perf_counter()
+    dg = graphgen.rmat_device_graph(n, m, symmetric=sym, seed=0)
+    t_graph = time.perf_counter() - t0
+    k = args.k or default_k(args.workload)
+    all_batches = make_batches_for(n, k * world)
+    batches = all_batches[rank * k:(rank + 1) * k]
+    boff = rank * k
+    off = np.zeros(k + 1, np.int64)
+    off[1:] = np.cumsum([len(b) for b in batches])
+    d_off = torch.as_tensor(off).cuda()
+    d_cat = torch.as_tensor(np.concatenate(batches).astype(np.int32)).cuda()
+    lib = _lib.lib()
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
+
+    def measure(mode):
+        bulk = SageBulk(dg, k, int(off[-1]), BATCH, FANOUTS, mode=mode)
+        bulk._bverts = d_cat
+        for _ in range(max(args.warmup, 3)):
+            bulk.launch(d_off, d_cat, 0, 0, boff)
+        torch.cuda.synchronize()
+        lib.gb_launch_counter(1)
+        bulk.launch(d_off, d_cat, 0, 0, boff)
+        launches_per_bulk = int(lib.gb_launch_counter(1))
+        graph = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            bulk.launch(d_off, d_cat, 0, 0, boff)  # warm the capture stream
+            with torch.cuda.graph(graph, stream=s):
+                bulk.launch(d_off, d_cat, 0, 0, boff)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        for _ in range(2):
+            graph.replay()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        clk = ClockSampler()
+        clk.start(local_rank)
+        for i in range(args.steps):
+            flush.fill_(i)
+            evs[i][0].record()
+            graph.replay()
+            evs[i][1].record()
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        clocks = clk.stop()
+        step_ms = [a.elapsed_time(b) for a, b in evs]
+        # dominant kernel (sample kernel) durations, eager launches, same stream
+        lib.gb_profile_begin(2 * len(FANOUTS) * 4)
+        for i in range(4):
+            flush.fill_(i)
+            bulk.launch(d_off, d_cat, 0, 0, boff)
+        ms = (ctypes.c_float * (len(FANOUTS) * 4))()
+        npairs = ctypes.c_int32()
+        lib.gb_profile_end(ms, len(FANOUTS) * 4, ctypes.byref(npairs))
+        kern_ms = np.array(ms[:npairs.value]).reshape(4, len(FANOUTS))
+        sizes = bulk.sizes.cpu().numpy()
+        return bulk, step_ms, clocks, kern_ms, sizes, launches_per_bulk, graph
+
+    bulk, step_ms, clocks, kern_ms, sizes, lpb, graph = measure(args.mode)
+    total_ms = float(np.sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = world * k * args.steps / (total_ms / 1e3)
+    st = layer_stats(bulk, dg, sizes)
+    peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(REPO, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    kb = [sample_kernel_bytes(s, args.mode) for s in st]
+    kern_avg = kern_ms.mean(axis=0)  # per layer
+    achieved = sum(kb) / (kern_avg.sum() / 1e3) / 1e9
+    bulk_bytes = sage_bytes(st)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {
+            "workload": f"{args.workload}-shape R-MAT (n={n}, nnz={dg.nnz}), GraphSAGE "
+                        f"(15,10,5), b=1024, k={k} per GPU, replicated graph",
+            "mode": args.mode, "l2": "flushed between steps (256 MiB write, untimed)",
+            "parallelism": f"replicated x{world}", "graph_build_s": round(t_graph, 2),
+        },
+        "gpu_launches": lpb * args.steps,
+        "clocks": clocks,
+        "layers": st,
+        "edges_per_s": world * sum(s["G"] for s in st) * args.steps / (total_ms / 1e3),
+        "bulk_bytes": bulk_bytes,
+        "bulk_gbs": bulk_bytes / (total_ms / args.steps / 1e3) / 1e9,
+        "roofline": {
+            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": None,
+            "kernel": f"k_sage_sample<{'true' if args.mode == 'stream' else 'false'}>",
+            "per_layer_ms": [round(x, 4) for x in kern_avg.tolist()],
+            "per_layer_bytes": kb, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)",
+            "kernel_share_of_step": float(kern_avg.sum() / (total_ms / args.steps)),
+        },
+    }
+    # P-free exact fast path, same workload
+    if not args.no_pfree and args.mode == "stream":
+        b2, sm2, _, km2, sz2, lpb2, g2 = measure("pfree")
+        t2 = float(np.sum(sm2))
+        if world > 1:
+            t = torch.tensor([t2], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            t2 = float(t.item())
+        kb2 = [sample_kernel_bytes(s, "pfree") for s in st]
+        a2 = sum(kb2) / (km2.mean(axis=0).sum() / 1e3) / 1e9
+        same = bool(np.array_equal(sz2, sizes))
+        line["pfree"] = {"value": world * k * args.steps / (t2 / 1e3), "unit": UNIT,
+                         "ms_per_step": t2 / args.steps, "same_sizes_as_stream": same,
+                         "roofline": {"achieved": a2, "peak": peak, "unit": "GB/s",
+                                      "frac": a2 / peak, "kernel": "k_sage_sample<false>",
+                                      "per_layer_ms": km2.mean(axis=0).tolist()}}
+        del b2, g2
+    # end-to-end through the public API (host batches in, host arrays out)
+    G = gb.Graph.from_device(dg)
+    cfg = gb.SamplerConfig.sage(3, BATCH, FANOUTS, bulk_count=k, seed=0)
+    bs = BulkSampler(G, cfg, mode=args.mode)
+    for _ in range(2):
+        bs.sample(batches, 0, boff)
+    torch.cuda.synchronize()
+    e2e_t = []
+    for _ in range(max(3, min(args.steps, 10))):
+        t0 = time.perf_counter()
+        ep = bs.sample(batches, 0, boff)
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_s = float(np.mean(e2e_t))
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    line["e2e"] = {"value": world * k / e2e_s, "unit": UNIT, "h2d_bytes_per_step": bs.h2d_bytes,
+                   "d2h_bytes_per_step": bs.d2h_bytes,
+                   "api": "paper_2311_02909_b200.engine.BulkSampler.sample (host batches -> "
+                          "host SampledEpoch arrays)"}
+    # CPU baseline (oracle port) on rank 0 at N=1, with a full-size parity check
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        gpu_layers = ep.to_arrays()
+        host = (n, dg.rowptr.cpu().numpy(), dg.col[:dg.nnz].cpu().numpy())
+        cb, kc, parity = cpu_baseline(host, batches, args.cpu_seconds, gpu_layers)
+        line["cpu_baseline"] = cb
+        line["parity_full_size"] = f"{parity} on the first {kc} of {k} minibatches vs oracle"
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        if args.impl == "reference":
+            run_reference(args, rank, world)
+        else:
+            run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

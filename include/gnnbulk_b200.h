@@ -98,6 +98,25 @@ int gb_sage_bulk(const gb_graph* g, int64_t k, const int64_t* d_bptr, const int3
                  gb_sage_layer_out* h_layers, int64_t* d_sizes, void* d_ws, size_t ws_bytes,
                  void* stream);
 
+/* ----------------------------------------------------- synthetic inputs
+ * R-MAT edge candidates first..first+count (Graph500 quadrant recursion over
+ * `scale` levels with probabilities a, b, c; rejected candidates = -1) and
+ * a keyed 64-bit hash for relabelling; the device side of the canonical
+ * generator (graph_io.py:79-197 is the reference's
+ * host-only ingestion). */
+int gb_rmat_edges(uint64_t seed, int32_t scale, int64_t n, int64_t first, int64_t count,
+                  double a, double b, double c, int64_t* d_src, int64_t* d_dst, void* stream);
+int gb_hash64(uint64_t seed, const int64_t* d_x, int64_t count, int64_t* d_out, void* stream);
+
+/* ------------------------------------------------------- instrumentation
+ * gb_launch_counter: kernels this host thread has launched through the
+ * library (optionally reset).  gb_profile_begin/end: CUDA events recorded
+ * around every dominant-kernel launch (the SAGE sample kernel) until end;
+ * end synchronises and returns the per-launch durations in ms. */
+int64_t gb_launch_counter(int32_t reset);
+int gb_profile_begin(int32_t max_marks);
+int gb_profile_end(float* h_ms, int32_t cap, int32_t* h_pairs);
+
 #ifdef __cplusplus
 }
 #endif

@@ -17,6 +17,21 @@ void set_error(const char* fmt, ...) {
   va_end(ap);
 }
 
+static thread_local int64_t g_launches = 0;
+void count_launches(int n) { g_launches += n; }
+
+struct Profile {
+  cudaEvent_t ev[256];
+  int created = 0, used = 0;
+  bool on = false;
+};
+static thread_local Profile g_prof;
+
+void prof_mark(cudaStream_t st) {
+  if (!g_prof.on || g_prof.used >= g_prof.created) return;
+  cudaEventRecord(g_prof.ev[g_prof.used++], st);
+}
+
 int cuda_status(cudaError_t e, const char* what) {
   set_error("CUDA error in %s: %s", what, cudaGetErrorString(e));
   return GB_ERR_CUDA;
@@ -39,6 +54,31 @@ struct gb_graph : public gb::Graph {};
 extern "C" {
 
 const char* gb_last_error(void) { return g_err; }
+
+int64_t gb_launch_counter(int32_t reset) {
+  int64_t v = g_launches;
+  if (reset) g_launches = 0;
+  return v;
+}
+
+int gb_profile_begin(int32_t max_marks) {
+  if (max_marks < 0 || max_marks > 256) { set_error("profile: 0..256 marks"); return GB_ERR_CONTRACT; }
+  while (g_prof.created < max_marks) GB_CUDA(cudaEventCreate(&g_prof.ev[g_prof.created++]));
+  g_prof.used = 0;
+  g_prof.on = true;
+  return GB_OK;
+}
+
+int gb_profile_end(float* h_ms, int32_t cap, int32_t* h_pairs) {
+  g_prof.on = false;
+  const int pairs = g_prof.used / 2;
+  if (pairs > 0) GB_CUDA(cudaEventSynchronize(g_prof.ev[2 * pairs - 1]));
+  for (int i = 0; i < pairs && i < cap; ++i)
+    GB_CUDA(cudaEventElapsedTime(&h_ms[i], g_prof.ev[2 * i], g_prof.ev[2 * i + 1]));
+  if (h_pairs) *h_pairs = pairs;
+  g_prof.used = 0;
+  return GB_OK;
+}
 int gb_version(void) { return 1; }
 
 int gb_uniforms(uint64_t seed, uint64_t epoch, uint64_t depth, const int64_t* d_rows,

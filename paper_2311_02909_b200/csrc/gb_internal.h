@@ -23,6 +23,11 @@ struct Graph {
   int32_t* run_n = nullptr;         // [slots]
 };
 
+// Launch accounting (gb_launch_counter) and optional CUDA-event marks around
+// the dominant kernels (gb_profile_begin / gb_profile_end), host-thread local.
+void count_launches(int n);
+void prof_mark(cudaStream_t st);
+
 int graph_build_tables(Graph* g, cudaStream_t st);
 int sage_workspace(const Graph* g, int64_t k, int64_t r1_cap, int32_t layers,
                    const int64_t* fanouts, size_t* bytes);

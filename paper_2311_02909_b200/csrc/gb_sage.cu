@@ -654,6 +654,7 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
   }
   GB_CUDA(cudaMemsetAsync(ws.bitmap, 0, sizeof(uint32_t) * (W + 1), st));
   k_set_i64<<<1, 1, 0, st>>>(ws.d_W, W);
+  count_launches(1);
   int64_t stride = batch_size;
   r_cap = r1_cap;
   for (int32_t l = 0; l < layers; ++l) {
@@ -680,11 +681,13 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     A.brow = brow; A.k = k; A.s = s; A.stride = stride; A.batch_offset = batch_offset;
     A.seed = seed; A.epoch = epoch; A.depth = (uint64_t)d;
     A.bitmap = ws.bitmap; A.nwords = nwords; A.fcol = o.fcol;
+    prof_mark(st);
     if (stream)
       k_sage_sample<true><<<sample_grid(true), kSampleThreads, 0, st>>>(A, R_ptr);
     else
       k_sage_sample<false><<<sample_grid(false), kSampleThreads, 0, st>>>(A, R_ptr);
     GB_LAUNCH_CHECK("k_sage_sample");
+    prof_mark(st);
     rc = device_exclusive_scan<int64_t>(ws.d_W, W, PopF{ws.bitmap}, ws.wpre, ws.scan_ws, st);
     if (rc) return rc;
     int64_t* sizes = d_sizes + 3 * l;
@@ -698,6 +701,7 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     k_sage_enumerate<<<grid_for(W, 256, 16 * kNumSMs), 256, 0, st>>>(W, nwords, ws.bitmap, ws.wpre,
                                                                        o.colv);
     GB_LAUNCH_CHECK("k_sage_enumerate");
+    count_launches(5);  // prep, sample, meta, rank, enumerate
     r_cap = f_cap;
   }
   return GB_OK;

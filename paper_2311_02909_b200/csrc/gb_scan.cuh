@@ -7,6 +7,7 @@
 // n + 1 entries; out[n] is the total.
 #pragma once
 #include "gb_common.cuh"
+#include "gb_internal.h"
 
 namespace gb {
 
@@ -119,6 +120,7 @@ inline int device_exclusive_scan(const int64_t* d_n, int64_t max_n, F f, OutT* o
   scan_tiles<T, OutT, F><<<grid, kScanThreads, 0, st>>>(d_n, f, tile_sums, out);
   scan_write_total<T, OutT><<<1, 1, 0, st>>>(d_n, total, out);
   GB_LAUNCH_CHECK("device_exclusive_scan");
+  count_launches(4);
   return GB_OK;
 }
 

@@ -131,3 +131,75 @@ def ladies_epoch(G, cfg, batches, epoch, batch_offset):
 
 def sample_epoch_generic(G, cfg, batches, epoch, batch_offset, prob_spgemm):
     raise NotImplementedError("prob_spgemm hook path")
+
+
+class BulkSampler:
+    """Public reusable bulk sampler bound to (graph, config).
+
+    `sample(batches)` is the drop-in for `sample_epoch_bulk` when the same
+    shapes recur (an epoch loop): device buffers are planned once, host
+    batches travel through pinned memory, and with `to_host=True` the result
+    arrays are copied back into pinned host buffers (the reference returns
+    host numpy arrays).  With `to_host=False` the results stay in HBM.
+    """
+
+    def __init__(self, G: Graph, cfg: SamplerConfig, max_batch_vertices=None, mode="stream"):
+        import torch
+
+        if cfg.kind is not SamplerKind.SAGE:
+            raise ContractViolation("BulkSampler currently drives the SAGE path")
+        self.G, self.cfg, self.mode = G, cfg, mode
+        self.dg = G.device()
+        k = cfg.bulk_count
+        r1 = int(max_batch_vertices or k * cfg.batch_size)
+        self.bulk = SageBulk(self.dg, k, r1, cfg.batch_size, cfg.fanouts, mode=mode)
+        self.h_off = torch.empty(k + 1, dtype=torch.int64, pin_memory=True)
+        self.h_cat = torch.empty(max(r1, 1), dtype=torch.int32, pin_memory=True)
+        self.d_off = torch.empty(k + 1, dtype=torch.int64, device="cuda")
+        self.d_cat = torch.empty(max(r1, 1), dtype=torch.int32, device="cuda")
+        self.h_sizes = torch.empty(3 * cfg.layers, dtype=torch.int64, pin_memory=True)
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
+
+    def sample(self, batches, epoch=0, batch_offset=0, to_host=True) -> SampledEpoch:
+        import torch
+
+        k = self.cfg.bulk_count
+        if len(batches) != k:
+            raise ContractViolation(f"BulkSampler built for {k} batches, got {len(batches)}")
+        cat, off = _flatten_batches(batches, self.G.n)
+        if k and int(np.max(np.diff(off))) > self.cfg.batch_size:
+            raise ContractViolation("actual rows exceed the nominal stride")
+        if cat.size > self.h_cat.numel():
+            raise ContractViolation("more batch vertices than the sampler was built for")
+        r1 = int(off[-1])
+        self.h_off.numpy()[:] = off
+        self.h_cat.numpy()[:r1] = cat
+        self.d_off.copy_(self.h_off, non_blocking=True)
+        self.d_cat[:r1].copy_(self.h_cat[:r1], non_blocking=True)
+        self.h2d_bytes = 8 * (k + 1) + 4 * r1
+        self.bulk.launch(self.d_off, self.d_cat, self.cfg.seed, epoch, batch_offset)
+        self.h_sizes.copy_(self.bulk.sizes, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        sizes = self.h_sizes.numpy().copy()
+        layers = self.bulk.layers(self.d_off, self.d_cat, sizes)
+        self.d2h_bytes = 8 * sizes.size
+        if to_host:
+            host_layers = []
+            pend = []
+            for layer in layers:
+                h = {}
+                for key, v in layer.device.items():
+                    if isinstance(v, tuple):
+                        h[key] = v
+                        continue
+                    buf = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
+                    buf.copy_(v, non_blocking=True)
+                    self.d2h_bytes += v.numel() * v.element_size()
+                    pend.append((h, key, buf))
+                host_layers.append((layer.depth, h))
+            torch.cuda.current_stream().synchronize()
+            for h, key, buf in pend:
+                h[key] = buf.numpy()
+            layers = [LayerSample(d, device=h, n=self.G.n) for d, h in host_layers]
+        return SampledEpoch(SamplerKind.SAGE, epoch, batches, layers, self.cfg.layers)

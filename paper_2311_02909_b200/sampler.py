@@ -185,8 +185,8 @@ class LayerSample:
     # flat host arrays in the oracle's format (oracle/oracle.py LAYER_KEYS)
     def to_arrays(self):
         if self.device is not None:
-            d = {k: v.cpu().numpy().astype(np.int64) for k, v in self.device.items()
-                 if k not in ("frontier_shape", "adj_shape")}
+            d = {k: (v if isinstance(v, np.ndarray) else v.cpu().numpy()).astype(np.int64)
+                 for k, v in self.device.items() if k not in ("frontier_shape", "adj_shape")}
             d["frontier_shape"] = np.asarray(self.device["frontier_shape"], dtype=np.int64)
             d["adj_shape"] = np.asarray(self.device["adj_shape"], dtype=np.int64)
             return d
