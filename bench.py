@@ -41,7 +41,7 @@ BATCH = 1024
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--workload", default="products", choices=["products", "cfg1", "papers"])
@@ -137,13 +137,19 @@ def sage_bytes(st):
     return sum(28 * s["R"] + 4 * s["G"] + 12 * s["F"] + 4 * s["U"] + 8 for s in st)
 
 
-def sample_kernel_bytes(s, mode):
-    """Algorithmic bytes of one sample-kernel launch:
-    stream: 20 B/row (vertex id + row_ptr pair) + 4 B/gathered entry + 4 B/pick;
-    pfree:  20 B/row + 4 B read + 4 B written per pick."""
-    if mode == "stream":
-        return 20 * s["R"] + 4 * s["G"] + 4 * s["F"]
-    return 20 * s["R"] + 8 * s["F"]
+def kernel_bytes(s, kernel):
+    """Algorithmic bytes of one launch: every byte the
+    kernel must move by design, no re-reads, per layer statistics s.
+      stream (k_sage_stream): deg 4 + fptr 8 + vertex 4 + row_ptr 8 + gstart 8
+                              per row, 4 per gathered entry, pick idx 4 + col 4;
+      pick   (k_sage_pick<false>): deg 4 + fptr 8 per row, 4 per pick idx;
+      pfree  (k_sage_pick<true>):  deg 4 + fptr 8 + vertex 4 + row_ptr 8 per
+                                   row, col read 4 + write 4 per pick."""
+    if kernel == "stream":
+        return 32 * s["R"] + 4 * s["G"] + 8 * s["F"]
+    if kernel == "pick":
+        return 12 * s["R"] + 4 * s["F"]
+    return 24 * s["R"] + 8 * s["F"]
 
 
 def oracle_prefix(layers, kc):
@@ -302,15 +308,17 @@ def run_ours(args, rank, world, local_rank):
             torch.distributed.barrier()
         clocks = clk.stop()
         step_ms = [a.elapsed_time(b) for a, b in evs]
-        # dominant kernel (sample kernel) durations, eager launches, same stream
-        lib.gb_profile_begin(2 * len(FANOUTS) * 4)
+        # sample-kernel durations (events around each launch, same stream)
+        ppl = 2 if mode == "stream" else 1
+        cap = ppl * len(FANOUTS) * 4
+        lib.gb_profile_begin(2 * cap)
         for i in range(4):
             flush.fill_(i)
             bulk.launch(d_off, d_cat, 0, 0, boff)
-        ms = (ctypes.c_float * (len(FANOUTS) * 4))()
+        ms = (ctypes.c_float * cap)()
         npairs = ctypes.c_int32()
-        lib.gb_profile_end(ms, len(FANOUTS) * 4, ctypes.byref(npairs))
-        kern_ms = np.array(ms[:npairs.value]).reshape(4, len(FANOUTS))
+        lib.gb_profile_end(ms, cap, ctypes.byref(npairs))
+        kern_ms = np.array(ms[:npairs.value]).reshape(4, len(FANOUTS), ppl)
         sizes = bulk.sizes.cpu().numpy()
         return bulk, step_ms, clocks, kern_ms, sizes, launches_per_bulk, graph
 
@@ -325,8 +333,10 @@ def run_ours(args, rank, world, local_rank):
     peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(REPO, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    kb = [sample_kernel_bytes(s, args.mode) for s in st]
-    kern_avg = kern_ms.mean(axis=0)  # per layer
+    dom = "stream" if args.mode == "stream" else "pfree"
+    kb = [kernel_bytes(s, dom) for s in st]
+    kern_avg = kern_ms.mean(axis=0)[:, -1]  # dominant kernel, per layer
+    pick_avg = kern_ms.mean(axis=0)[:, 0]
     achieved = sum(kb) / (kern_avg.sum() / 1e3) / 1e9
     bulk_bytes = sage_bytes(st)
     line = {
@@ -349,7 +359,8 @@ def run_ours(args, rank, world, local_rank):
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": None,
-            "kernel": f"k_sage_sample<{'true' if args.mode == 'stream' else 'false'}>",
+            "kernel": "k_sage_stream" if args.mode == "stream" else "k_sage_pick<true>",
+            "pick_kernel_ms": [round(x, 4) for x in pick_avg.tolist()],
             "per_layer_ms": [round(x, 4) for x in kern_avg.tolist()],
             "per_layer_bytes": kb, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)",
             "kernel_share_of_step": float(kern_avg.sum() / (total_ms / args.steps)),
@@ -363,14 +374,14 @@ def run_ours(args, rank, world, local_rank):
             t = torch.tensor([t2], device=dev, dtype=torch.float64)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             t2 = float(t.item())
-        kb2 = [sample_kernel_bytes(s, "pfree") for s in st]
-        a2 = sum(kb2) / (km2.mean(axis=0).sum() / 1e3) / 1e9
+        kb2 = [kernel_bytes(s, "pfree") for s in st]
+        a2 = sum(kb2) / (km2.mean(axis=0)[:, 0].sum() / 1e3) / 1e9
         same = bool(np.array_equal(sz2, sizes))
         line["pfree"] = {"value": world * k * args.steps / (t2 / 1e3), "unit": UNIT,
                          "ms_per_step": t2 / args.steps, "same_sizes_as_stream": same,
                          "roofline": {"achieved": a2, "peak": peak, "unit": "GB/s",
-                                      "frac": a2 / peak, "kernel": "k_sage_sample<false>",
-                                      "per_layer_ms": km2.mean(axis=0).tolist()}}
+                                      "frac": a2 / peak, "kernel": "k_sage_pick<true>",
+                                      "per_layer_ms": km2.mean(axis=0)[:, 0].tolist()}}
         del b2, g2
     # end-to-end through the public API (host batches in, host arrays out)
     G = gb.Graph.from_device(dg)

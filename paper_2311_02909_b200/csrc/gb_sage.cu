@@ -123,45 +123,6 @@ __global__ void k_build_runs(const int32_t* __restrict__ slot_deg, int64_t slots
   }
 }
 
-// ========================================================= exact replay math
-
-// Table of one degree staged in (warp-private) shared memory.
-struct RunTable {
-  int32_t* j0;   // nr + 1 (sentinel m + 1)
-  double* s0;    // nr
-  double* d;     // nr
-  int nr;
-};
-
-// S[n], 1 <= n <= m.
-__device__ __forceinline__ double table_S(const RunTable& t, int64_t n) {
-  int lo = 0, hi = t.nr;  // last run with j0 <= n
-  while (hi - lo > 1) {
-    int mid = (lo + hi) >> 1;
-    if (t.j0[mid] <= n) lo = mid; else hi = mid;
-  }
-  return __dadd_rn(t.s0[lo], __dmul_rn((double)(n - t.j0[lo]), t.d[lo]));
-}
-
-// first j >= 1 with S[j] > target (may be m + 1 when none)
-__device__ __forceinline__ int64_t table_first_gt(const RunTable& t, double target) {
-  if (target < t.s0[0]) return 1;
-  int lo = 0, hi = t.nr;  // last run with s0 <= target
-  while (hi - lo > 1) {
-    int mid = (lo + hi) >> 1;
-    if (t.s0[mid] <= target) lo = mid; else hi = mid;
-  }
-  const int64_t j0 = t.j0[lo];
-  const int64_t len = (int64_t)t.j0[lo + 1] - j0;
-  if (len == 1) return j0 + 1;
-  const double s0 = t.s0[lo], d = t.d[lo];
-  int64_t q = (int64_t)((target - s0) / d);
-  q = q < 0 ? 0 : (q > len - 1 ? len - 1 : q);
-  while (q > 0 && __dadd_rn(s0, __dmul_rn((double)q, d)) > target) --q;
-  while (q + 1 < len && __dadd_rn(s0, __dmul_rn((double)(q + 1), d)) <= target) ++q;
-  return j0 + q + 1;
-}
-
 // ============================================================ layer kernels
 
 __global__ void k_sage_prep(const int64_t* __restrict__ R_ptr, const int32_t* __restrict__ rowv,
@@ -204,14 +165,16 @@ struct SageArgs {
   uint64_t seed, epoch, depth;
   uint32_t* bitmap;
   int64_t nwords;
-  int32_t* fcol;
+  int32_t* fcol;         // frontier columns (output)
+  int32_t* pidx;         // stream mode: row-relative pick indices (scratch)
 };
 
-constexpr int kSampleThreads = 256;
-constexpr int kSampleWarps = kSampleThreads / 32;
+constexpr int kPickThreads = 128;
+constexpr int kStreamThreads = 256;
 constexpr int kRowCost = 48;       // merge-path weight of one row (in entries)
-constexpr int kStreamUnroll = 4;   // int4 loads in flight per lane
+constexpr int kStreamUnroll = 8;   // 16-B loads in flight per lane
 constexpr int kBrowSmem = 1024;
+constexpr int kMaxFan = 32;
 
 __device__ __forceinline__ int4 ld_stream_v4(const int32_t* p) {
   int4 r;
@@ -233,183 +196,212 @@ __device__ __forceinline__ int64_t batch_of(const int64_t* sb, const int64_t* gb
   return lo;
 }
 
+// Replay table of one degree read through the read-only path (L1-resident:
+// a few KB per hot degree).
+struct GTable {
+  const int32_t* j0;
+  const double* s0;
+  const double* d;
+  int nr;
+};
 
-// Warp-cooperative processing of one row.  Lanes t < take own pick t; the
-// warp writes the picks whose row-relative index lies in [lo, hi).
-template <bool STREAM>
-__device__ __forceinline__ void sage_row(const SageArgs& A, RunTable& tab, uint64_t key,
-                                         int32_t deg, int64_t fp, int64_t rs, int64_t bb,
-                                         int64_t lo, int64_t hi) {
-  const unsigned FULL = 0xffffffffu;
-  const int lane = lane_id();
-  const int32_t take = min(deg, A.s);
-  int64_t myidx = lane;  // row-relative index of my pick (draw order = lane)
-  int32_t rank = lane;   // position among the row's sorted picks
-  if (take < deg) {
-    // ---- stage this degree's replay table (warp-private shared memory)
-    const int32_t slot = A.deg_slot[deg];
-    const int nr = A.run_n[slot];
-    int32_t* j0 = tab.j0;
-    double* s0 = tab.s0;
-    double* dd = tab.d;
-    for (int i = lane; i < nr; i += 32) {
-      j0[i] = A.run_j0[(int64_t)slot * (kMaxRuns + 1) + i];
-      s0[i] = A.run_s0[(int64_t)slot * kMaxRuns + i];
-      dd[i] = A.run_d[(int64_t)slot * kMaxRuns + i];
-    }
-    if (lane == 0) j0[nr] = deg + 1;
-    __syncwarp();
-    tab.nr = nr;
-    // ---- draw t = lane: which live entry (1-based rank j) it selects.
-    // n_live = deg - t, total = S[n_live], target = u * total,
-    // j = first j with S[j] > target, clamped to n_live (sampler.py:176-186)
-    int64_t j = 0;
-    if (lane < take) {
-      const double u = uniform53(A.seed, A.epoch, A.depth, key, (uint64_t)lane);
-      const int64_t n_live = deg - lane;
-      const double total = table_S(tab, n_live);
-      const double target = __dmul_rn(u, total);
-      j = table_first_gt(tab, target);
-      if (j > n_live) j = n_live;
-    }
-    // ---- remove-and-renormalise: draw t takes the j_t-th live index
-    for (int t = 0; t < take; ++t) {
-      const int64_t jt = __shfl_sync(FULL, j, t);
-      int64_t idx = jt - 1;
-      while (true) {
-        const unsigned m = __ballot_sync(FULL, lane < t && myidx <= idx);
-        const int64_t nidx = jt - 1 + __popc(m);
-        if (nidx == idx) break;
-        idx = nidx;
-      }
-      if (lane == t) myidx = idx;
-    }
-    // ---- frontier rows are stored sorted (frontier_from_rows, sampler.py:216)
-    rank = 0;
-    for (int t = 0; t < take; ++t) {
-      const int64_t o = __shfl_sync(FULL, myidx, t);
-      rank += (o < myidx) ? 1 : 0;
-    }
-    __syncwarp();
+// S[n], 1 <= n <= m
+__device__ __forceinline__ double gt_S(const GTable& t, int64_t n) {
+  int lo = 0, hi = t.nr;  // last run with j0 <= n
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(t.j0 + mid) <= n) lo = mid; else hi = mid;
   }
-  const bool active = lane < take;
-  int32_t c = 0;
-  bool have = false;
-  if (!STREAM) {
-    if (active) {
-      c = A.col[rs + myidx];
-      have = true;
-    }
-  } else {
-    // ---- P row on chip: stream entries [lo, hi) of A row, catch the picks
-    const int64_t e_lo = rs + lo, e_hi = rs + hi;
-    const int64_t pabs = rs + myidx;
-    const bool want = active && pabs >= e_lo && pabs < e_hi;
-    for (int64_t w0 = e_lo & ~3LL; w0 < e_hi; w0 += 128 * kStreamUnroll) {
-      int4 vals[kStreamUnroll];
-#pragma unroll
-      for (int u = 0; u < kStreamUnroll; ++u) {
-        const int64_t e = w0 + 128 * u + 4 * lane;
-        vals[u] = e < e_hi ? ld_stream_v4(A.col + e) : make_int4(0, 0, 0, 0);
-      }
-      const int64_t off = pabs - w0;
-      const bool mine = want && off >= 0 && off < 128 * kStreamUnroll;
-      if (__any_sync(FULL, mine)) {
-#pragma unroll
-        for (int u = 0; u < kStreamUnroll; ++u) {
-          const int64_t o = off - 128 * u;
-          const int src = (int)((o >> 2) & 31);
-          const int comp = (int)(o & 3);
-          const int x = __shfl_sync(FULL, vals[u].x, src);
-          const int y = __shfl_sync(FULL, vals[u].y, src);
-          const int z = __shfl_sync(FULL, vals[u].z, src);
-          const int w = __shfl_sync(FULL, vals[u].w, src);
-          if (mine && o >= 0 && o < 128) {
-            c = comp == 0 ? x : comp == 1 ? y : comp == 2 ? z : w;
-            have = true;
-          }
+  return __dadd_rn(__ldg(t.s0 + lo), __dmul_rn((double)(n - __ldg(t.j0 + lo)), __ldg(t.d + lo)));
+}
+
+// first j >= 1 with S[j] > target (m + 1 when none)
+__device__ __forceinline__ int64_t gt_first_gt(const GTable& t, double target) {
+  if (target < __ldg(t.s0)) return 1;
+  int lo = 0, hi = t.nr;  // last run with s0 <= target
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(t.s0 + mid) <= target) lo = mid; else hi = mid;
+  }
+  const int64_t j0 = __ldg(t.j0 + lo);
+  const int64_t len = (int64_t)__ldg(t.j0 + lo + 1) - j0;
+  if (len == 1) return j0 + 1;
+  const double s0 = __ldg(t.s0 + lo), d = __ldg(t.d + lo);
+  int64_t q = (int64_t)((target - s0) / d);
+  q = q < 0 ? 0 : (q > len - 1 ? len - 1 : q);
+  while (q > 0 && __dadd_rn(s0, __dmul_rn((double)q, d)) > target) --q;
+  while (q + 1 < len && __dadd_rn(s0, __dmul_rn((double)(q + 1), d)) <= target) ++q;
+  return j0 + q + 1;
+}
+
+// NORM + SAMPLE, one thread per P row.  Draw t of row r uses
+// u = uniform53(seed, epoch, depth, key_r, t); n_live = deg - t live entries
+// of weight fl(1/deg); target = u * S[n_live]; the draw selects the j-th live
+// entry, j = first j with S[j] > target clamped to n_live — exactly
+// its_sample_row's cumsum/searchsorted/clamp/walk-back (sampler.py:176-188).
+// Picks are kept sorted (frontier_from_rows sorts, sampler.py:216).
+// GATHER (P-free): read the picked columns of A directly and finish the row;
+// otherwise write the row-relative indices for the streaming kernel.
+template <bool GATHER>
+__global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
+                                                          const int64_t* __restrict__ R_ptr) {
+  __shared__ int64_t s_brow[kBrowSmem];
+  const int64_t R = *R_ptr;
+  const bool brow_in_smem = A.k + 1 <= kBrowSmem;
+  if (brow_in_smem)
+    for (int64_t i = threadIdx.x; i <= A.k; i += blockDim.x) s_brow[i] = A.brow[i];
+  __syncthreads();
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t deg = A.deg[r];
+    if (deg == 0) continue;  // empty P row (sample_rows_ordered, sampler.py:202-204)
+    const int32_t take = min(deg, A.s);
+    const int64_t fp = A.fptr[r];
+    int32_t sorted[kMaxFan];
+    if (take == deg) {
+      // exhaustion: every index, no uniform consumed (sampler.py:172-174)
+      for (int t = 0; t < take; ++t) sorted[t] = t;
+    } else {
+      const int64_t bb = batch_of(s_brow, A.brow, A.k, r);
+      const int64_t b0 = brow_in_smem ? s_brow[bb] : A.brow[bb];
+      // global_row_keys (sampler.py:309-322)
+      const uint64_t key = (uint64_t)((A.batch_offset + bb) * A.stride + (r - b0));
+      const int32_t slot = __ldg(A.deg_slot + deg);
+      GTable tab{A.run_j0 + (int64_t)slot * (kMaxRuns + 1), A.run_s0 + (int64_t)slot * kMaxRuns,
+                 A.run_d + (int64_t)slot * kMaxRuns, __ldg(A.run_n + slot)};
+      uint64_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;
+      for (int t = 0; t < take; ++t) {
+        if ((t & 3) == 0) {
+          w0 = key; w1 = A.depth; w2 = (uint64_t)(t >> 2); w3 = 0;
+          philox4x64_10(w0, w1, w2, w3, A.seed, A.epoch);
         }
+        const uint64_t w = (t & 3) == 0 ? w0 : (t & 3) == 1 ? w1 : (t & 3) == 2 ? w2 : w3;
+        const double u = (double)(w >> 11) * 0x1.0p-53;
+        const int64_t n_live = deg - t;
+        const double target = __dmul_rn(u, gt_S(tab, n_live));
+        int64_t j = gt_first_gt(tab, target);
+        if (j > n_live) j = n_live;
+        // j-th live index: skip over the removed (sorted) ones
+        int32_t x = (int32_t)(j - 1);
+        int i = 0;
+        while (i < t && sorted[i] <= x) { ++x; ++i; }
+        for (int q = t; q > i; --q) sorted[q] = sorted[q - 1];
+        sorted[i] = x;
       }
     }
-  }
-  if (have) {
-    A.fcol[fp + rank] = c;
-    atomicOr(&A.bitmap[bb * A.nwords + (c >> 5)], 1u << (c & 31));
+    if (GATHER) {
+      const int64_t bb = batch_of(s_brow, A.brow, A.k, r);
+      const int64_t rs = A.rowptr[A.rowv[r]];
+      int32_t cv[kMaxFan];
+      for (int t = 0; t < take; ++t) cv[t] = __ldg(A.col + rs + sorted[t]);
+      uint32_t* bm = A.bitmap + bb * A.nwords;
+      for (int t = 0; t < take; ++t) {
+        A.fcol[fp + t] = cv[t];
+        atomicOr(bm + (cv[t] >> 5), 1u << (cv[t] & 31));
+      }
+    } else {
+      for (int t = 0; t < take; ++t) A.pidx[fp + t] = sorted[t];
+    }
   }
 }
 
-template <bool STREAM>
-__global__ void __launch_bounds__(kSampleThreads) k_sage_sample(SageArgs A,
+// Q^l A with the P row formed on chip: warps stream every A row of the
+// layer (16-B coalesced loads, kStreamUnroll in flight per lane), balanced
+// by merge path over (rows x kRowCost + gathered entries), and catch the
+// picked entries (row-relative indices from k_sage_pick) out of registers.
+__global__ void __launch_bounds__(kStreamThreads, 4) k_sage_stream(SageArgs A,
                                                               const int64_t* __restrict__ R_ptr) {
   __shared__ int64_t s_brow[kBrowSmem];
-  __shared__ int32_t s_j0[kSampleWarps][kMaxRuns + 1];
-  __shared__ double s_s0[kSampleWarps][kMaxRuns];
-  __shared__ double s_d[kSampleWarps][kMaxRuns];
   const unsigned FULL = 0xffffffffu;
   const int64_t R = *R_ptr;
   const bool brow_in_smem = A.k + 1 <= kBrowSmem;
   if (brow_in_smem)
     for (int64_t i = threadIdx.x; i <= A.k; i += blockDim.x) s_brow[i] = A.brow[i];
   __syncthreads();
-  const int wib = threadIdx.x >> 5, lane = lane_id();
+  const int lane = lane_id();
   const int64_t NW = grid_warps(), w = global_warp();
-  int64_t r_begin, r_end, path_a = 0, path_b = 0;
-  if (STREAM) {
-    const int64_t G = A.gstart[R];
-    const int64_t total = R * kRowCost + G;
-    const int64_t share = (total + NW - 1) / NW;
-    path_a = min(w * share, total);
-    path_b = min(path_a + share, total);
-    if (path_a >= path_b) return;
-    // last r with P_r <= path_a, P_r = r * kRowCost + gstart[r]
-    int64_t lo = 0, hi = R;
-    while (hi - lo > 1) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (mid * kRowCost + A.gstart[mid] <= path_a) lo = mid; else hi = mid;
-    }
-    r_begin = lo;
-    // first r with P_r >= path_b
-    lo = r_begin; hi = R;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (mid * kRowCost + A.gstart[mid] >= path_b) hi = mid; else lo = mid + 1;
-    }
-    r_end = lo;
-  } else {
-    const int64_t share = (R + NW - 1) / NW;
-    r_begin = min(w * share, R);
-    r_end = min(r_begin + share, R);
+  const int64_t G = A.gstart[R];
+  const int64_t total = R * kRowCost + G;
+  const int64_t share = (total + NW - 1) / NW;
+  const int64_t path_a = min(w * share, total);
+  const int64_t path_b = min(path_a + share, total);
+  if (path_a >= path_b) return;
+  // last r with P_r <= path_a, P_r = r * kRowCost + gstart[r]
+  int64_t lo = 0, hi = R;
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (mid * kRowCost + A.gstart[mid] <= path_a) lo = mid; else hi = mid;
   }
-  RunTable tab{s_j0[wib], s_s0[wib], s_d[wib], 0};
+  const int64_t r_begin = lo;
+  lo = r_begin;
+  hi = R;  // first r with P_r >= path_b
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (mid * kRowCost + A.gstart[mid] >= path_b) hi = mid; else lo = mid + 1;
+  }
+  const int64_t r_end = lo;
   for (int64_t rb = r_begin; rb < r_end; rb += 32) {
-    // batched per-row metadata: lane l describes row rb + l
     const int64_t r = rb + lane;
     int32_t deg = 0;
-    int64_t fp = 0, rs = 0, gs = 0, bb = 0, key = 0;
+    int64_t fp = 0, rs = 0, gs = 0, bb = 0;
     if (r < r_end) {
-      const int32_t v = A.rowv[r];
       deg = A.deg[r];
       fp = A.fptr[r];
-      rs = A.rowptr[v];
-      if (STREAM) gs = A.gstart[r];
+      rs = A.rowptr[A.rowv[r]];
+      gs = A.gstart[r];
       bb = batch_of(s_brow, A.brow, A.k, r);
-      const int64_t b0 = brow_in_smem ? s_brow[bb] : A.brow[bb];
-      key = (A.batch_offset + bb) * A.stride + (r - b0);  // global_row_keys, sampler.py:309-322
     }
     const int nrows = (int)min((int64_t)32, r_end - rb);
     for (int i = 0; i < nrows; ++i) {
       const int32_t d_i = __shfl_sync(FULL, deg, i);
-      if (d_i == 0) continue;  // empty P row: no picks (sample_rows_ordered, sampler.py:202-204)
-      int64_t lo = 0, hi = d_i;
-      if (STREAM) {
-        const int64_t pe = (rb + i) * kRowCost + __shfl_sync(FULL, gs, i) + kRowCost;
-        lo = max(path_a - pe, (int64_t)0);
-        hi = min(path_b - pe, (int64_t)d_i);
-        if (lo >= hi) continue;
+      if (d_i == 0) continue;
+      const int64_t pe = (rb + i) * kRowCost + __shfl_sync(FULL, gs, i) + kRowCost;
+      const int64_t e0 = max(path_a - pe, (int64_t)0);
+      const int64_t e1 = min(path_b - pe, (int64_t)d_i);
+      if (e0 >= e1) continue;
+      const int32_t take = min(d_i, A.s);
+      const int64_t fp_i = __shfl_sync(FULL, fp, i);
+      const int64_t rs_i = __shfl_sync(FULL, rs, i);
+      const int64_t b_i = __shfl_sync(FULL, bb, i);
+      const int32_t myidx = lane < take ? A.pidx[fp_i + lane] : -1;
+      const int64_t e_lo = rs_i + e0, e_hi = rs_i + e1;
+      const int64_t pabs = rs_i + myidx;
+      const bool want = lane < take && pabs >= e_lo && pabs < e_hi;
+      int32_t c = 0;
+      bool have = false;
+      for (int64_t w0 = e_lo & ~3LL; w0 < e_hi; w0 += 128 * kStreamUnroll) {
+        int4 vals[kStreamUnroll];
+#pragma unroll
+        for (int u = 0; u < kStreamUnroll; ++u) {
+          const int64_t e = w0 + 128 * u + 4 * lane;
+          vals[u] = e < e_hi ? ld_stream_v4(A.col + e) : make_int4(0, 0, 0, 0);
+        }
+        const int64_t off = pabs - w0;
+        const bool mine = want && off >= 0 && off < 128 * kStreamUnroll;
+        if (__any_sync(FULL, mine)) {
+#pragma unroll
+          for (int u = 0; u < kStreamUnroll; ++u) {
+            const int64_t o = off - 128 * u;
+            const bool in_u = mine && o >= 0 && o < 128;
+            if (__any_sync(FULL, in_u)) {
+              const int src = (int)((o >> 2) & 31);
+              const int comp = (int)(o & 3);
+              const int x = __shfl_sync(FULL, vals[u].x, src);
+              const int y = __shfl_sync(FULL, vals[u].y, src);
+              const int z = __shfl_sync(FULL, vals[u].z, src);
+              const int ww = __shfl_sync(FULL, vals[u].w, src);
+              if (in_u) {
+                c = comp == 0 ? x : comp == 1 ? y : comp == 2 ? z : ww;
+                have = true;
+              }
+            }
+          }
+        }
       }
-      sage_row<STREAM>(A, tab, (uint64_t)__shfl_sync(FULL, key, i), d_i,
-                       __shfl_sync(FULL, fp, i), __shfl_sync(FULL, rs, i),
-                       __shfl_sync(FULL, bb, i), lo, hi);
+      if (have) {
+        A.fcol[fp_i + lane] = c;
+        atomicOr(&A.bitmap[b_i * A.nwords + (c >> 5)], 1u << (c & 31));
+      }
     }
   }
 }
@@ -566,6 +558,7 @@ int graph_build_tables(Graph* g, cudaStream_t st) {
 
 // ---------------------------------------------------------- workspace plan
 struct SageWs {
+  int32_t* pidx;
   int32_t* deg;
   int64_t* gstart;
   int64_t* scan_ws;
@@ -577,13 +570,15 @@ struct SageWs {
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
-static SageWs sage_ws_layout(char* base, int64_t k, int64_t n, int64_t r_cap_max) {
+static SageWs sage_ws_layout(char* base, int64_t k, int64_t n, int64_t r_cap_max,
+                             int64_t f_cap_max) {
   SageWs w{};
   const int64_t nwords = (n + 31) / 32;
   const int64_t W = k * nwords;
   const int64_t scan_n = r_cap_max > W ? r_cap_max : W;
   size_t off = 0;
   auto take = [&](size_t bytes) { char* p = base ? base + off : nullptr; off += align_up(bytes); return p; };
+  w.pidx = (int32_t*)take(sizeof(int32_t) * (f_cap_max + 1));
   w.deg = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
   w.gstart = (int64_t*)take(sizeof(int64_t) * (r_cap_max + 1));
   w.scan_ws = (int64_t*)take(sizeof(int64_t) * scan_workspace_elems<int64_t>(scan_n + 1));
@@ -603,25 +598,34 @@ static int64_t sage_rcap_max(int64_t r1_cap, int32_t layers, const int64_t* fano
   return mx;
 }
 
+static int64_t sage_fcap_max(int64_t r1_cap, int32_t layers, const int64_t* fanouts) {
+  int64_t r = r1_cap, mx = 0;
+  for (int32_t l = 0; l < layers; ++l) {
+    r *= fanouts[l];
+    if (r > mx) mx = r;
+  }
+  return mx;
+}
+
 int sage_workspace(const Graph* g, int64_t k, int64_t r1_cap, int32_t layers,
                    const int64_t* fanouts, size_t* bytes) {
-  *bytes = sage_ws_layout(nullptr, k, g->n, sage_rcap_max(r1_cap, layers, fanouts)).bytes;
+  *bytes = sage_ws_layout(nullptr, k, g->n, sage_rcap_max(r1_cap, layers, fanouts),
+                          sage_fcap_max(r1_cap, layers, fanouts)).bytes;
   return GB_OK;
 }
 
-static int sample_grid(bool stream) {
-  static int occ[2] = {0, 0};
-  int& o = occ[stream ? 1 : 0];
-  if (!o) {
-    if (stream)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_sage_sample<true>, kSampleThreads, 0);
-    else
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_sage_sample<false>, kSampleThreads, 0);
-    if (o < 1) o = 1;
-  }
-  int sms = 0;
+template <typename K>
+static int persistent_grid(K kernel, int threads) {
+  int o = 0, sms = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kernel, threads, 0);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  return o * (sms > 0 ? sms : kNumSMs);
+  return (o < 1 ? 1 : o) * (sms > 0 ? sms : kNumSMs);
+}
+
+static int stream_grid() {
+  static int g = 0;
+  if (!g) g = persistent_grid(k_sage_stream, kStreamThreads);
+  return g;
 }
 
 int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d_bverts,
@@ -633,7 +637,7 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
   const int64_t nwords = (g->n + 31) / 32;
   const int64_t W = k * nwords;
   const int64_t rmax = sage_rcap_max(r1_cap, layers, fanouts);
-  SageWs ws = sage_ws_layout((char*)d_ws, k, g->n, rmax);
+  SageWs ws = sage_ws_layout((char*)d_ws, k, g->n, rmax, sage_fcap_max(r1_cap, layers, fanouts));
   if (ws.bytes > ws_bytes) {
     set_error("sage workspace too small: need %zu bytes, got %zu", ws.bytes, ws_bytes);
     return GB_ERR_CAPACITY;
@@ -680,14 +684,22 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     A.rowv = rowv; A.deg = ws.deg; A.fptr = o.fptr; A.gstart = ws.gstart;
     A.brow = brow; A.k = k; A.s = s; A.stride = stride; A.batch_offset = batch_offset;
     A.seed = seed; A.epoch = epoch; A.depth = (uint64_t)d;
-    A.bitmap = ws.bitmap; A.nwords = nwords; A.fcol = o.fcol;
+    A.bitmap = ws.bitmap; A.nwords = nwords; A.fcol = o.fcol; A.pidx = ws.pidx;
+    const int pick_grid = grid_for(r_cap, kPickThreads, 64 * kNumSMs);
     prof_mark(st);
     if (stream)
-      k_sage_sample<true><<<sample_grid(true), kSampleThreads, 0, st>>>(A, R_ptr);
+      k_sage_pick<false><<<pick_grid, kPickThreads, 0, st>>>(A, R_ptr);
     else
-      k_sage_sample<false><<<sample_grid(false), kSampleThreads, 0, st>>>(A, R_ptr);
-    GB_LAUNCH_CHECK("k_sage_sample");
+      k_sage_pick<true><<<pick_grid, kPickThreads, 0, st>>>(A, R_ptr);
+    GB_LAUNCH_CHECK("k_sage_pick");
     prof_mark(st);
+    if (stream) {
+      prof_mark(st);
+      k_sage_stream<<<stream_grid(), kStreamThreads, 0, st>>>(A, R_ptr);
+      GB_LAUNCH_CHECK("k_sage_stream");
+      prof_mark(st);
+      count_launches(1);
+    }
     rc = device_exclusive_scan<int64_t>(ws.d_W, W, PopF{ws.bitmap}, ws.wpre, ws.scan_ws, st);
     if (rc) return rc;
     int64_t* sizes = d_sizes + 3 * l;

@@ -1,0 +1,43 @@
+"""Minimal driver for ncu: build the products-shape graph, run `--warm`
+eager bulks then `--iters` more (same stream).  Kernel order per bulk:
+layer-1, layer-2, layer-3 sample kernels (k_sage_sample<mode>)."""
+
+import argparse
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--mode", default="stream")
+    p.add_argument("--workload", default="products")
+    p.add_argument("--k", type=int, default=64)
+    p.add_argument("--warm", type=int, default=2)
+    p.add_argument("--iters", type=int, default=1)
+    a = p.parse_args()
+    import torch
+
+    from paper_2311_02909_b200 import graphgen
+    from paper_2311_02909_b200.engine import SageBulk
+    from paper_2311_02909_b200.pipeline import make_batches
+
+    n, m, sym = graphgen.SHAPES[a.workload]
+    dg = graphgen.rmat_device_graph(n, m, symmetric=sym, seed=0)
+    batches = make_batches(np.arange(n), 1024, 0, 0)[:a.k]
+    off = np.zeros(a.k + 1, np.int64)
+    off[1:] = np.cumsum([len(b) for b in batches])
+    d_off = torch.as_tensor(off).cuda()
+    d_cat = torch.as_tensor(np.concatenate(batches).astype(np.int32)).cuda()
+    bulk = SageBulk(dg, a.k, int(off[-1]), 1024, (15, 10, 5), mode=a.mode)
+    for _ in range(a.warm + a.iters):
+        bulk.launch(d_off, d_cat, 0, 0, 0)
+    torch.cuda.synchronize()
+    print("sizes", bulk.sizes.cpu().numpy().tolist())
+
+
+if __name__ == "__main__":
+    main()
