@@ -1,6 +1,6 @@
 """Minimal driver for ncu: build the products-shape graph, run `--warm`
 eager bulks then `--iters` more (same stream).  Kernel order per bulk:
-layer-1, layer-2, layer-3 sample kernels (k_sage_sample<mode>)."""
+per layer: prep, scans, k_sage_pick, [k_sage_stream], extraction."""
 
 import argparse
 import os
