@@ -98,6 +98,42 @@ int gb_sage_bulk(const gb_graph* g, int64_t k, const int64_t* d_bptr, const int3
                  gb_sage_layer_out* h_layers, int64_t* d_sizes, void* d_ws, size_t ws_bytes,
                  void* stream);
 
+/* -------------------------------------------------------- LADIES bulk
+ * sample_epoch_bulk with SamplerConfig.kind == LADIES (sampler.py:325-387,
+ * 420-462, 475-483).  Layer-1 rows: the batches, each sorted and distinct
+ * (ladies_seed_matrix), offsets d_qoff[k+1], vertices d_qverts.
+ * Per layer (caller buffers; q_cap >= rows of Q, f_cap >= k*s,
+ * a_cap >= q_cap*s):
+ *   fptr  [k+1]   frontier row offsets; fcol [F] sorted sampled vertices
+ *                 (== col_vertices == sampled_vertices == next layer's Q)
+ *   aptr  [Q+1], acol [nnz]  A_S (one row per Q nonzero, ladies_assemble)
+ *   coloff[k+1]   column offset of each batch's block (all 0 = shared layout)
+ * d_sizes[4*l + {0,1,2,3}] = (A_S rows, F, A_S nnz, A_S cols).
+ * mode GB_LADIES_EXACT replays its_sample_row bit for bit (sequential fp64
+ * cumsum, small graphs); GB_LADIES_RACE draws the same law by an
+ * exponential race (Gumbel top-s) for production sizes. */
+#define GB_LADIES_EXACT 0
+#define GB_LADIES_RACE 1
+
+typedef struct {
+  int64_t* fptr;
+  int32_t* fcol;
+  int64_t* aptr;
+  int32_t* acol;
+  int64_t* coloff;
+  int64_t q_cap;
+  int64_t f_cap;
+  int64_t a_cap;
+} gb_ladies_layer_out;
+
+int gb_ladies_bulk_workspace(const gb_graph* g, int64_t k, int64_t q1_cap, int32_t layers,
+                             const int64_t* h_fanouts, int32_t mode, size_t* h_bytes);
+int gb_ladies_bulk(const gb_graph* g, int64_t k, const int64_t* d_qoff, const int32_t* d_qverts,
+                   int64_t q1_cap, int32_t layers, const int64_t* h_fanouts, uint64_t seed,
+                   uint64_t epoch, int64_t batch_offset, int32_t mode,
+                   gb_ladies_layer_out* h_layers, int64_t* d_sizes, void* d_ws, size_t ws_bytes,
+                   void* stream);
+
 /* ----------------------------------------------------- synthetic inputs
  * R-MAT edge candidates first..first+count (Graph500 quadrant recursion over
  * `scale` levels with probabilities a, b, c; rejected candidates = -1) and

@@ -33,6 +33,16 @@ class SageLayerOut(ctypes.Structure):
     ]
 
 
+class LadiesLayerOut(ctypes.Structure):
+    _fields_ = [
+        ("fptr", _p), ("fcol", _p), ("aptr", _p), ("acol", _p), ("coloff", _p),
+        ("q_cap", _i64), ("f_cap", _i64), ("a_cap", _i64),
+    ]
+
+
+GB_LADIES_EXACT = 0
+GB_LADIES_RACE = 1
+
 # (name, restype, argtypes) — one line per exported symbol of the header
 SIGNATURES = {
     "gb_last_error": (ctypes.c_char_p, []),
@@ -44,6 +54,11 @@ SIGNATURES = {
     "gb_sage_bulk_workspace": (ctypes.c_int, [_p, _i64, _i64, _i32, _p, ctypes.POINTER(ctypes.c_size_t)]),
     "gb_sage_bulk": (ctypes.c_int, [_p, _i64, _p, _p, _i64, _i64, _i32, _p, _u64, _u64, _i64,
                                     _i32, ctypes.POINTER(SageLayerOut), _p, _p, ctypes.c_size_t, _p]),
+    "gb_ladies_bulk_workspace": (ctypes.c_int, [_p, _i64, _i64, _i32, _p, _i32,
+                                                ctypes.POINTER(ctypes.c_size_t)]),
+    "gb_ladies_bulk": (ctypes.c_int, [_p, _i64, _p, _p, _i64, _i32, _p, _u64, _u64, _i64, _i32,
+                                      ctypes.POINTER(LadiesLayerOut), _p, _p, ctypes.c_size_t,
+                                      _p]),
     "gb_rmat_edges": (ctypes.c_int, [_u64, _i32, _i64, _i64, _i64, ctypes.c_double,
                                      ctypes.c_double, ctypes.c_double, _p, _p, _p]),
     "gb_hash64": (ctypes.c_int, [_u64, _p, _i64, _p, _p]),

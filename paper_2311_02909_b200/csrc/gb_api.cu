@@ -167,4 +167,35 @@ int gb_sage_bulk(const gb_graph* g, int64_t k, const int64_t* d_bptr, const int3
                    batch_offset, mode, h_layers, d_sizes, d_ws, ws_bytes, (cudaStream_t)stream);
 }
 
+int gb_ladies_bulk_workspace(const gb_graph* g, int64_t k, int64_t q1_cap, int32_t layers,
+                             const int64_t* h_fanouts, int32_t mode, size_t* h_bytes) {
+  if (!g || !h_bytes || k < 0 || layers < 1 || !h_fanouts) {
+    set_error("ladies workspace: bad arguments");
+    return GB_ERR_CONTRACT;
+  }
+  return ladies_workspace(g, k, q1_cap, layers, h_fanouts, mode, h_bytes);
+}
+
+int gb_ladies_bulk(const gb_graph* g, int64_t k, const int64_t* d_qoff, const int32_t* d_qverts,
+                   int64_t q1_cap, int32_t layers, const int64_t* h_fanouts, uint64_t seed,
+                   uint64_t epoch, int64_t batch_offset, int32_t mode,
+                   gb_ladies_layer_out* h_layers, int64_t* d_sizes, void* d_ws, size_t ws_bytes,
+                   void* stream) {
+  if (!g || k < 0 || layers < 1 || !h_fanouts || !h_layers) {
+    set_error("ladies bulk: bad arguments");
+    return GB_ERR_CONTRACT;
+  }
+  for (int32_t l = 0; l < layers; ++l)
+    if (h_fanouts[l] < 1) {
+      set_error("ladies bulk: sample count must be >= 1");
+      return GB_ERR_CONTRACT;
+    }
+  if (mode != GB_LADIES_EXACT && mode != GB_LADIES_RACE) {
+    set_error("ladies bulk: unknown mode %d", mode);
+    return GB_ERR_CONTRACT;
+  }
+  return ladies_bulk(g, k, d_qoff, d_qverts, q1_cap, layers, h_fanouts, seed, epoch,
+                     batch_offset, mode, h_layers, d_sizes, d_ws, ws_bytes, (cudaStream_t)stream);
+}
+
 }  // extern "C"

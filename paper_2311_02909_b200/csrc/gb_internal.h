@@ -36,5 +36,11 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
               uint64_t seed, uint64_t epoch, int64_t batch_offset, int32_t mode,
               gb_sage_layer_out* L, int64_t* d_sizes, void* d_ws, size_t ws_bytes,
               cudaStream_t st);
+int ladies_workspace(const Graph* g, int64_t k, int64_t q1_cap, int32_t layers,
+                     const int64_t* fanouts, int32_t mode, size_t* bytes);
+int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t* d_qverts,
+                int64_t q1_cap, int32_t layers, const int64_t* fanouts, uint64_t seed,
+                uint64_t epoch, int64_t batch_offset, int32_t mode, gb_ladies_layer_out* L,
+                int64_t* d_sizes, void* d_ws, size_t ws_bytes, cudaStream_t st);
 
 }  // namespace gb

@@ -125,8 +125,89 @@ def sage_epoch(G: Graph, cfg: SamplerConfig, batches, epoch, batch_offset, mode=
     return SampledEpoch(SamplerKind.SAGE, epoch, batches, layers, cfg.layers)
 
 
-def ladies_epoch(G, cfg, batches, epoch, batch_offset):
-    raise NotImplementedError("LADIES device path: see engine_ladies")
+LADIES_MODES = {"exact": _lib.GB_LADIES_EXACT, "race": _lib.GB_LADIES_RACE}
+# auto -> exact replay while its O(s * N) serial cumsum per batch stays small
+LADIES_EXACT_LIMIT = 1 << 26
+
+
+class LadiesBulk:
+    """Reusable device buffers + launcher for LADIES bulks of one shape."""
+
+    def __init__(self, dg, k, q1_cap, fanouts, mode="race"):
+        import torch
+
+        if mode not in LADIES_MODES:
+            raise ContractViolation(f"unknown LADIES mode {mode!r}")
+        self.dg, self.k, self.q1_cap = dg, int(k), int(q1_cap)
+        self.fanouts = tuple(int(s) for s in fanouts)
+        self.mode = mode
+        L = len(self.fanouts)
+        dev = torch.device("cuda")
+        self.out = []
+        self.c_layers = (_lib.LadiesLayerOut * L)()
+        qc = self.q1_cap
+        for l, s in enumerate(self.fanouts):
+            fc, ac = self.k * s, qc * s
+            o = {
+                "fptr": torch.empty(self.k + 1, dtype=torch.int64, device=dev),
+                "fcol": torch.empty(max(fc, 1), dtype=torch.int32, device=dev),
+                "aptr": torch.empty(qc + 1, dtype=torch.int64, device=dev),
+                "acol": torch.empty(max(ac, 1), dtype=torch.int32, device=dev),
+                "coloff": torch.empty(self.k + 1, dtype=torch.int64, device=dev),
+            }
+            self.out.append(o)
+            c = self.c_layers[l]
+            for name in ("fptr", "fcol", "aptr", "acol", "coloff"):
+                setattr(c, name, o[name].data_ptr())
+            c.q_cap, c.f_cap, c.a_cap = qc, fc, ac
+            qc = fc
+        self.h_fanouts = np.ascontiguousarray(self.fanouts, dtype=np.int64)
+        nbytes = ctypes.c_size_t()
+        _lib.check(_lib.lib().gb_ladies_bulk_workspace(
+            dg.handle, self.k, self.q1_cap, L, self.h_fanouts.ctypes.data, LADIES_MODES[mode],
+            ctypes.byref(nbytes)), "gb_ladies_bulk_workspace")
+        self.ws = torch.empty(max(int(nbytes.value), 1), dtype=torch.uint8, device=dev)
+        self.sizes = torch.zeros(4 * L, dtype=torch.int64, device=dev)
+
+    def launch(self, d_qoff, d_qverts, seed, epoch, batch_offset, stream=None):
+        L = len(self.fanouts)
+        _lib.check(_lib.lib().gb_ladies_bulk(
+            self.dg.handle, self.k, _lib.ptr(d_qoff), _lib.ptr(d_qverts), self.q1_cap, L,
+            self.h_fanouts.ctypes.data, int(seed), int(epoch), int(batch_offset),
+            LADIES_MODES[self.mode], self.c_layers, _lib.ptr(self.sizes), _lib.ptr(self.ws),
+            self.ws.numel(), _lib.stream_ptr(stream)), "gb_ladies_bulk")
+
+    def layers(self, d_qoff, d_qverts, sizes=None):
+        if sizes is None:
+            sizes = self.sizes.cpu().numpy()
+        n = self.dg.n
+        out = []
+        qoff, qcol = d_qoff, d_qverts
+        for l in range(len(self.fanouts)):
+            QN, F, A, C = (int(x) for x in sizes[4 * l: 4 * l + 4])
+            o = self.out[l]
+            dev = {
+                "frontier_shape": (self.k, n), "frontier_ptr": o["fptr"],
+                "frontier_col": o["fcol"][:F],
+                "adj_shape": (QN, C), "adj_ptr": o["aptr"][: QN + 1], "adj_col": o["acol"][:A],
+                "rowv_off": qoff, "rowv_cat": qcol[:QN],
+                "colv_off": o["fptr"], "colv_cat": o["fcol"][:F],
+                "sampv_off": o["fptr"], "sampv_cat": o["fcol"][:F],
+            }
+            out.append(LayerSample(l + 1, device=dev, n=n))
+            qoff, qcol = o["fptr"], o["fcol"]
+        return out
+
+
+def ladies_epoch(G, cfg, batches, epoch, batch_offset, mode="auto"):
+    dg = G.device()
+    d_off, d_cat, q1 = upload_batches(batches, G.n, sort_within=True)
+    if mode == "auto":
+        mode = "exact" if G.n * max(cfg.fanouts) <= LADIES_EXACT_LIMIT else "race"
+    bulk = LadiesBulk(dg, len(batches), max(q1, 1), cfg.fanouts, mode=mode)
+    bulk.launch(d_off, d_cat, cfg.seed, epoch, batch_offset)
+    layers = bulk.layers(d_off, d_cat)
+    return SampledEpoch(SamplerKind.LADIES, epoch, batches, layers, cfg.layers)
 
 
 def sample_epoch_generic(G, cfg, batches, epoch, batch_offset, prob_spgemm):

@@ -304,7 +304,7 @@ def global_row_keys(cfg: SamplerConfig, depth, batch_ids, rows_per_batch_actual)
 
 
 def sample_epoch_bulk(G: Graph, cfg: SamplerConfig, batches, epoch=0, batch_offset=0,
-                      prob_spgemm=None, mode="stream") -> SampledEpoch:
+                      prob_spgemm=None, mode="auto") -> SampledEpoch:
     """Sample every layer for k minibatches in one stacked pass on the GPU
     (reference sampler.py:325-387).
 
@@ -321,5 +321,7 @@ def sample_epoch_bulk(G: Graph, cfg: SamplerConfig, batches, epoch=0, batch_offs
     if prob_spgemm is not None:
         return engine.sample_epoch_generic(G, cfg, batches, epoch, batch_offset, prob_spgemm)
     if cfg.kind is SamplerKind.SAGE:
-        return engine.sage_epoch(G, cfg, batches, epoch, batch_offset, mode=mode)
-    return engine.ladies_epoch(G, cfg, batches, epoch, batch_offset)
+        return engine.sage_epoch(G, cfg, batches, epoch, batch_offset,
+                                 mode="stream" if mode in ("auto", None) else mode)
+    return engine.ladies_epoch(G, cfg, batches, epoch, batch_offset,
+                               mode="auto" if mode in ("stream", None) else mode)
