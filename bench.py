@@ -50,6 +50,7 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=15.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-pfree", action="store_true")
+    p.add_argument("--no-ladies", action="store_true")
     return p.parse_args()
 
 
@@ -193,6 +194,64 @@ def cpu_baseline(host_graph, batches, seconds, gpu_layers=None):
     return {"value": kc / dt, "unit": UNIT, "cores": threads, "kind": "port",
             "sample": f"first {kc} of the bulk's minibatches (batch_offset 0), same graph; "
                       f"{dt:.1f} s"}, kc, parity
+
+
+def ladies_bytes(st, k):
+    """SURVEY.md §8(d) LADIES algorithmic bytes per bulk:
+    sum_l 44 nnz(Q) + 8 G + 16 N + 4 |S| + 4 E + 8 k + 16."""
+    return sum(44 * s["Q"] + 8 * s["G"] + 16 * s["N"] + 4 * s["S"] + 4 * s["E"] + 8 * k + 16
+               for s in st)
+
+
+def measure_ladies(args, dg, rank, world, flush, peak):
+    """LADIES b=s=512, L=3, k=64 per GPU on the products-shape graph
+    (exponential-race sampling; exact replay is the small-graph parity mode)."""
+    import torch
+
+    from paper_2311_02909_b200.engine import LadiesBulk
+    from paper_2311_02909_b200.pipeline import make_batches
+
+    k, b, s, L = 64, 512, 512, 3
+    allb = make_batches(np.arange(dg.n), b, seed=0, epoch=0)[:k * world]
+    batches = [np.sort(x) for x in allb[rank * k:(rank + 1) * k]]
+    off = np.zeros(k + 1, np.int64)
+    off[1:] = np.cumsum([len(x) for x in batches])
+    d_off = torch.as_tensor(off).cuda()
+    d_cat = torch.as_tensor(np.concatenate(batches).astype(np.int32)).cuda()
+    bulk = LadiesBulk(dg, k, int(off[-1]), (s,) * L, mode="race")
+    for _ in range(3):
+        bulk.launch(d_off, d_cat, 0, 0, rank * k)
+    torch.cuda.synchronize()
+    steps = max(5, min(args.steps, 20))
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    for i in range(steps):
+        flush.fill_(i)
+        evs[i][0].record()
+        bulk.launch(d_off, d_cat, 0, 0, rank * k)
+        evs[i][1].record()
+    torch.cuda.synchronize()
+    T = float(sum(a.elapsed_time(bb) for a, bb in evs))
+    if world > 1:
+        t = torch.tensor([T], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        T = float(t.item())
+    sizes = bulk.sizes.cpu().numpy()
+    st = []
+    qoff, qcol = d_off, d_cat
+    for li in range(L):
+        QN, F, E, C, N = (int(x) for x in sizes[5 * li:5 * li + 5])
+        rv = qcol[:QN].long()
+        G = int((dg.rowptr[rv + 1] - dg.rowptr[rv]).sum().item())
+        st.append({"Q": QN, "G": G, "N": N, "S": F, "E": E, "cols": C})
+        qoff, qcol = bulk.out[li]["fptr"], bulk.out[li]["fcol"]
+    B = ladies_bytes(st, k)
+    ms = T / steps
+    return {"metric": "sampled minibatches/sec (LADIES 512/layer, 3 layers, k-batch bulk)",
+            "value": world * k * steps / (T / 1e3), "unit": UNIT, "ms_per_step": ms,
+            "config": "products-shape R-MAT, b=s=512, L=3, k=64 per GPU, exponential-race "
+                      "sampling", "layers": st, "bulk_bytes": B,
+            "bulk_gbs": B / (ms / 1e3) / 1e9, "frac_of_peak": B / (ms / 1e3) / 1e9 / peak}
 
 
 # ------------------------------------------------------------------ arms
@@ -383,6 +442,9 @@ def run_ours(args, rank, world, local_rank):
                                       "frac": a2 / peak, "kernel": "k_sage_pick<true>",
                                       "per_layer_ms": km2.mean(axis=0)[:, 0].tolist()}}
         del b2, g2
+    # LADIES, BASELINE configs[2]: same graph, 512 nodes/layer, 3 layers, k=64
+    if not args.no_ladies:
+        line["ladies_cfg3"] = measure_ladies(args, dg, rank, world, flush, peak)
     # end-to-end through the public API (host batches in, host arrays out)
     G = gb.Graph.from_device(dg)
     cfg = gb.SamplerConfig.sage(3, BATCH, FANOUTS, bulk_count=k, seed=0)

@@ -108,7 +108,7 @@ int gb_sage_bulk(const gb_graph* g, int64_t k, const int64_t* d_bptr, const int3
  *                 (== col_vertices == sampled_vertices == next layer's Q)
  *   aptr  [Q+1], acol [nnz]  A_S (one row per Q nonzero, ladies_assemble)
  *   coloff[k+1]   column offset of each batch's block (all 0 = shared layout)
- * d_sizes[4*l + {0,1,2,3}] = (A_S rows, F, A_S nnz, A_S cols).
+ * d_sizes[5*l + {0,1,2,3,4}] = (A_S rows, F, A_S nnz, A_S cols, nnz(P)).
  * mode GB_LADIES_EXACT replays its_sample_row bit for bit (sequential fp64
  * cumsum, small graphs); GB_LADIES_RACE draws the same law by an
  * exponential race (Gumbel top-s) for production sizes. */

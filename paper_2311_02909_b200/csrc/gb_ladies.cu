@@ -30,6 +30,7 @@
 namespace gb {
 
 constexpr int kLadiesThreads = 256;
+constexpr int kLadiesSizes = 5;  // per layer: A_S rows, F, A_S nnz, A_S cols, nnz(P)
 
 __device__ __forceinline__ int64_t last_le(const int64_t* a, int64_t n_plus1, int64_t x) {
   // last b in [0, n) with a[b] <= x, a has n+1 monotone entries
@@ -323,7 +324,9 @@ struct NnzF {
 // shared layout iff every batch took the same count (ladies_assemble)
 __global__ void k_ladies_layout(const int64_t* __restrict__ fptr, int64_t k,
                                 const int64_t* __restrict__ qoff, const int64_t* __restrict__ aptr,
+                                const int64_t* __restrict__ poff,
                                 int64_t* __restrict__ coloff, int64_t* __restrict__ sizes) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) sizes[4] = poff[k];  // nnz(P)
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   bool shared = true;
   for (int64_t i = 1; i < k; ++i)
@@ -483,7 +486,8 @@ int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t*
         qoff, k, qcol, g->rowptr, g->col, n, ws.cnt, nullptr, ws.rcnt, nullptr, nullptr);
     rc = device_exclusive_scan<int64_t>(d_QN, qc, RcntF{ws.rcnt}, o.aptr, ws.scan_ws, st);
     if (rc) return rc;
-    k_ladies_layout<<<1, 1, 0, st>>>(o.fptr, k, qoff, o.aptr, o.coloff, d_sizes + 4 * l);
+    k_ladies_layout<<<1, 1, 0, st>>>(o.fptr, k, qoff, o.aptr, ws.poff, o.coloff,
+                                     d_sizes + kLadiesSizes * l);
     k_ladies_extract<true><<<egrid, kLadiesThreads, 0, st>>>(
         qoff, k, qcol, g->rowptr, g->col, n, ws.cnt, o.coloff, nullptr, o.aptr, o.acol);
     k_ladies_mark<<<mgrid, 256, 0, st>>>(o.fptr, k, n, o.fcol, ws.cnt, 1);

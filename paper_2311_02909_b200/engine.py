@@ -167,7 +167,7 @@ class LadiesBulk:
             dg.handle, self.k, self.q1_cap, L, self.h_fanouts.ctypes.data, LADIES_MODES[mode],
             ctypes.byref(nbytes)), "gb_ladies_bulk_workspace")
         self.ws = torch.empty(max(int(nbytes.value), 1), dtype=torch.uint8, device=dev)
-        self.sizes = torch.zeros(4 * L, dtype=torch.int64, device=dev)
+        self.sizes = torch.zeros(5 * L, dtype=torch.int64, device=dev)
 
     def launch(self, d_qoff, d_qverts, seed, epoch, batch_offset, stream=None):
         L = len(self.fanouts)
@@ -184,7 +184,7 @@ class LadiesBulk:
         out = []
         qoff, qcol = d_qoff, d_qverts
         for l in range(len(self.fanouts)):
-            QN, F, A, C = (int(x) for x in sizes[4 * l: 4 * l + 4])
+            QN, F, A, C = (int(x) for x in sizes[5 * l: 5 * l + 4])
             o = self.out[l]
             dev = {
                 "frontier_shape": (self.k, n), "frontier_ptr": o["fptr"],
