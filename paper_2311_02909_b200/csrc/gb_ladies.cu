@@ -2,27 +2,30 @@
 // sm_100a.  Reference: sample_epoch_bulk LADIES path
 // (pkg/src/gnnbulk/sampler.py:325-387, 420-462, 475-483).
 //
-// Per layer, for the k batches at once:
-//   P = Q^l A        row i = sum of A rows of batch i's vertex set -> counts
-//                    e_v (spgemm sparse.py:233-251 on 0/1 values): dense
-//                    per-batch count vectors fed by a warp per gathered row
-//                    (atomic accumulate), first touches counted per batch.
-//   NORM             w_v = fl(e_v^2 / sum e^2) (norm_rows_ladies
-//                    sparse.py:263-286); the sum is an exact int64 reduce.
-//   SAMPLE           min(s, N_i) distinct columns per batch:
-//                    GB_LADIES_EXACT  — its_sample_row replayed literally
-//                      (sequential fp64 cumsum per draw, searchsorted right,
-//                      clamp, walk back; sampler.py:176-188) with the keyed
-//                      uniforms: bit-exact, O(s N) per batch, small graphs;
-//                    GB_LADIES_RACE   — exponential race / Gumbel top-s:
-//                      key_v = -log(u_v) / e_v^2, the s smallest keys (radix
-//                      select).  Same law as successive sampling without
-//                      replacement; validated statistically.
-//   EXTRACT          A_S = rows of Q^l (in order) x sampled columns: second
-//                    streaming pass over the gathered rows with a per-batch
-//                    rank marker (build_column_extraction sparse.py:430-446,
-//                    ladies_assemble sampler.py:420-434: shared columns when
-//                    every batch took the same count, else block diagonal).
+// Per layer, for the k batches:
+//   P = Q^l A   row i = sum of the A rows of batch i's vertex set: counts
+//               e_v (spgemm sparse.py:233-251 on 0/1 values).  Batches are
+//               processed in groups whose packed 16-bit count vectors stay
+//               L2-resident (e_v <= |Q_i|); warps stream the gathered rows,
+//               merge-path balanced over (rows, entries), and accumulate with
+//               atomics on the packed counters.
+//   NORM        w_v = fl(e_v^2 / sum e^2) (norm_rows_ladies sparse.py:263-286).
+//   SAMPLE      min(s, N_i) distinct columns per batch:
+//               GB_LADIES_EXACT — its_sample_row replayed literally
+//                 (sequential fp64 cumsum per draw, searchsorted right, clamp,
+//                 walk back; sampler.py:176-188) with the keyed uniforms:
+//                 bit-exact, O(s N) serial per batch, small graphs;
+//               GB_LADIES_RACE — exponential race (Gumbel top-s):
+//                 key_v = -log(u_v) / e_v^2, the s smallest keys (multi-CTA
+//                 histogram radix select).  Same law as successive sampling
+//                 without replacement; validated statistically.
+//   EXTRACT     A_S row (batch i, u) = sorted intersection A[u,:] ∩ S_i with
+//               ranks (build_column_extraction sparse.py:430-446,
+//               ladies_assemble sampler.py:420-434): one warp per row with S_i
+//               in shared memory — short rows binary-search S_i per entry,
+//               long (hub) rows binary-search A[u,:] per sampled vertex.
+//               Shared column layout when every batch took the same count,
+//               else block diagonal.
 #include "gb_common.cuh"
 #include "gb_internal.h"
 #include "gb_scan.cuh"
@@ -30,11 +33,15 @@
 namespace gb {
 
 constexpr int kLadiesThreads = 256;
-constexpr int kLadiesSizes = 5;  // per layer: A_S rows, F, A_S nnz, A_S cols, nnz(P)
+constexpr int kLadiesSizes = 5;     // per layer: A_S rows, F, A_S nnz, A_S cols, nnz(P)
+constexpr int kLRowCost = 32;       // merge-path weight of one Q row
+constexpr int kBins = 4096;         // radix-select histogram (12 bits)
+constexpr int kTies = 2048;
+constexpr int64_t kGroupBytes = 64ll << 20;  // packed counters of one group (L2-resident)
+constexpr int kSmaxSmem = 1024;     // S_i staged in shared memory up to this size
 
 __device__ __forceinline__ int64_t last_le(const int64_t* a, int64_t n_plus1, int64_t x) {
-  // last b in [0, n) with a[b] <= x, a has n+1 monotone entries
-  int64_t lo = 0, hi = n_plus1 - 1;
+  int64_t lo = 0, hi = n_plus1 - 1;  // last b in [0, n) with a[b] <= x
   while (hi - lo > 1) {
     const int64_t mid = (lo + hi) >> 1;
     if (a[mid] <= x) lo = mid; else hi = mid;
@@ -42,103 +49,190 @@ __device__ __forceinline__ int64_t last_le(const int64_t* a, int64_t n_plus1, in
   return lo;
 }
 
-// counts: cnt[i * n + v] += 1 for every v in A[u,:], u in Q_i; nnz_b[i]
-// counts first touches (= N_i).  One warp per Q entry.
-__global__ void __launch_bounds__(kLadiesThreads) k_ladies_count(
-    const int64_t* __restrict__ qoff, int64_t k, const int32_t* __restrict__ qcol,
+// ---------------------------------------------------------------- P = Q A
+
+struct QDegF {
+  const int32_t* qcol;
+  const int64_t* rowptr;
+  __device__ int64_t operator()(int64_t q) const {
+    const int32_t u = qcol[q];
+    return rowptr[u + 1] - rowptr[u];
+  }
+};
+
+// Counts for the batches [g0, g1): rows q in [qoff[g0], qoff[g1]), packed
+// uint16 counters cnt16[(i - g0) * n + v]; first touches -> nnz_b[i].
+__global__ void __launch_bounds__(kLadiesThreads) k_lad_count(
+    const int64_t* __restrict__ qoff, int64_t k, int64_t g0, int64_t g1,
+    const int32_t* __restrict__ qcol, const int64_t* __restrict__ qg,
     const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col, int64_t n,
-    int32_t* __restrict__ cnt, int64_t* __restrict__ nnz_b) {
+    uint32_t* __restrict__ cnt32, int64_t* __restrict__ nnz_b) {
   const int lane = lane_id();
-  const int64_t QN = qoff[k];
-  for (int64_t q = global_warp(); q < QN; q += grid_warps()) {
+  const int64_t q0 = qoff[g0], q1 = qoff[g1];
+  if (q1 <= q0) return;
+  const int64_t base = q0 * kLRowCost + qg[q0];
+  const int64_t total = q1 * kLRowCost + qg[q1] - base;
+  const int64_t NW = grid_warps(), w = global_warp();
+  const int64_t share = (total + NW - 1) / NW;
+  const int64_t pa = min(w * share, total) + base, pb = min(w * share + share, total) + base;
+  if (pa >= pb) return;
+  int64_t lo = q0, hi = q1;  // last q with P_q <= pa
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (mid * kLRowCost + qg[mid] <= pa) lo = mid; else hi = mid;
+  }
+  for (int64_t q = lo; q < q1; ++q) {
+    const int64_t pq = q * kLRowCost + qg[q];
+    if (pq >= pb) break;
+    const int64_t d = qg[q + 1] - qg[q];
+    const int64_t e0 = max(pa - pq - kLRowCost, (int64_t)0), e1 = min(pb - pq - kLRowCost, d);
+    if (e0 >= e1) continue;
     const int64_t i = last_le(qoff, k + 1, q);
     const int32_t u = qcol[q];
-    const int64_t a0 = rowptr[u], a1 = rowptr[u + 1];
-    int32_t* ci = cnt + i * n;
-    int64_t first = 0;
-    for (int64_t e = a0 + lane; e < a1; e += 32) {
-      const int32_t v = __ldg(col + e);
-      if (atomicAdd(ci + v, 1) == 0) ++first;
+    const int64_t a0 = rowptr[u];
+    uint32_t* ci = cnt32;
+    const int64_t cb = (i - g0) * n;
+    int first = 0;
+    for (int64_t e = a0 + e0 + lane; e < a0 + e1; e += 32) {
+      const int64_t v = cb + __ldg(col + e);
+      const uint32_t sh = (uint32_t)(v & 1) << 4;
+      const uint32_t old = atomicAdd(ci + (v >> 1), 1u << sh);
+      if (((old >> sh) & 0xffffu) == 0) ++first;
     }
     first = warp_sum(first);
     if (lane == 0 && first) atomicAdd((unsigned long long*)(nnz_b + i), (unsigned long long)first);
   }
 }
 
-// Compaction of the nonzeros of batch i (ascending v): one CTA per batch,
-// block-scan over tiles of its n counters; writes (v, e) at poff[i] and
-// clears the counters.  Also the exact int64 sum of e^2 per batch.
-__global__ void __launch_bounds__(1024) k_ladies_compact(
-    int64_t k, int64_t n, int32_t* __restrict__ cnt, const int64_t* __restrict__ poff,
-    int32_t* __restrict__ pv, int32_t* __restrict__ pe, int64_t* __restrict__ sumsq) {
-  __shared__ int64_t sw[33];
-  for (int64_t i = blockIdx.x; i < k; i += gridDim.x) {
-    int32_t* ci = cnt + i * n;
-    int64_t base = poff[i];
-    int64_t sq = 0;
-    for (int64_t t0 = 0; t0 < n; t0 += blockDim.x) {
-      const int64_t v = t0 + threadIdx.x;
-      const int32_t e = v < n ? ci[v] : 0;
-      int64_t total;
-      const int64_t ex = block_excl_scan<int64_t>(e > 0 ? 1 : 0, sw, total);
-      if (e > 0) {
-        pv[base + ex] = (int32_t)v;
-        pe[base + ex] = e;
-        ci[v] = 0;
-        sq += (int64_t)e * e;
-      }
-      base += total;
-    }
-    int64_t tot;
-    block_excl_scan<int64_t>(sq, sw, tot);
-    if (threadIdx.x == 0) sumsq[i] = tot;
+// Group-local nonzero offsets: gpoff[j] = sum_{g0 <= i < g0 + j} nnz_b[i].
+__global__ void k_lad_gpoff(const int64_t* __restrict__ nnz_b, int64_t g0, int64_t gn,
+                            int64_t* __restrict__ gpoff) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    int64_t acc = 0;
+    for (int64_t j = 0; j < gn; ++j) { gpoff[j] = acc; acc += nnz_b[g0 + j]; }
+    gpoff[gn] = acc;
   }
 }
 
+// Tile-parallel stream compaction of the group's counters in (batch, v)
+// order.  Pass 1: nonzeros per tile.  Pass 2 (after a tile-sum scan): block
+// scan + scatter (v, e) and clear the counters.
+constexpr int kCompTile = 4096;  // counters per tile (256 threads x 16)
+
+__global__ void __launch_bounds__(256) k_lad_compact_count(const uint32_t* __restrict__ cnt32,
+                                                         int64_t words,
+                                                         int64_t* __restrict__ tile_cnt) {
+  __shared__ int64_t sw[33];
+  const int64_t ntiles = (2 * words + kCompTile - 1) / kCompTile;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t w0 = t * (kCompTile / 2) + threadIdx.x * 8;
+    int64_t c = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t wi = w0 + j;
+      if (wi < words) {
+        const uint32_t x = cnt32[wi];
+        c += ((x & 0xffffu) != 0) + ((x >> 16) != 0);
+      }
+    }
+    int64_t total;
+    block_excl_scan<int64_t>(c, sw, total);
+    if (threadIdx.x == 0) tile_cnt[t] = total;
+  }
+}
+
+struct TileF {
+  const int64_t* t;
+  __device__ int64_t operator()(int64_t i) const { return t[i]; }
+};
+
+__global__ void __launch_bounds__(256) k_lad_compact_write(uint32_t* __restrict__ cnt32,
+                                                         int64_t words, int64_t n,
+                                                         const int64_t* __restrict__ tile_off,
+                                                         int32_t* __restrict__ pv,
+                                                         int32_t* __restrict__ pe) {
+  __shared__ int64_t sw[33];
+  const int64_t ntiles = (2 * words + kCompTile - 1) / kCompTile;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t w0 = t * (kCompTile / 2) + threadIdx.x * 8;
+    uint32_t x[8];
+    int64_t c = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t wi = w0 + j;
+      x[j] = wi < words ? cnt32[wi] : 0u;
+      c += ((x[j] & 0xffffu) != 0) + ((x[j] >> 16) != 0);
+    }
+    int64_t total;
+    int64_t o = block_excl_scan<int64_t>(c, sw, total) + tile_off[t];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (!x[j]) continue;
+      const int64_t flat = 2 * (w0 + j);
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t e = (x[j] >> (16 * h)) & 0xffffu;
+        if (e) {
+          pv[o] = (int32_t)((flat + h) % n);
+          pe[o] = (int32_t)e;
+          ++o;
+        }
+      }
+      cnt32[w0 + j] = 0u;
+    }
+  }
+}
+
+// ------------------------------------------------------------- sampling
+
 struct LadiesSampleArgs {
-  const int64_t* poff;   // k+1 offsets of the P rows' nonzeros
+  const int64_t* gpoff;  // group-local offsets of the P rows' nonzeros (gn + 1)
   const int32_t* pv;
   const int32_t* pe;
-  const int64_t* sumsq;
-  int64_t k;
+  int64_t g0, gn;        // batches g0 .. g0+gn-1
   int32_t s;
   int64_t batch_offset;
   uint64_t seed, epoch, depth;
-  double* scratch_w;     // exact mode: weights / cdf scratch (same layout as pv)
-  double* scratch_c;
-  int32_t* sel;          // per batch up to s selected positions (k * s)
-  int64_t* take;         // per batch count
+  double* sw;            // exact: weights, cdf scratch (P layout)
+  double* sc;
+  uint32_t* keys;        // race keys (P layout)
+  int32_t* sel;          // per batch: up to s selected P positions (global batch index * s)
+  int32_t* nsel;         // per batch selected count (atomic)
+  int64_t* take;         // per batch
 };
 
-// Exact replay of its_sample_row: one thread per batch (sequential fp64
-// cumsum is inherently serial; small graphs only).  Writes the selected
-// positions (draw order) into sel[i*s ...].
-__global__ void k_ladies_sample_exact(LadiesSampleArgs A) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A.k;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p0 = A.poff[i], N = A.poff[i + 1] - p0;
+// Exact replay of its_sample_row: one thread per batch.
+__global__ void k_lad_sample_exact(LadiesSampleArgs A) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < A.gn;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = A.g0 + j;
+    const int64_t p0 = A.gpoff[j], N = A.gpoff[j + 1] - p0;
     const int64_t take = N < A.s ? N : A.s;
     A.take[i] = take;
+    A.nsel[i] = (int32_t)take;
     int32_t* sel = A.sel + i * A.s;
     if (N == 0) continue;
     if (take == N) {
-      for (int64_t t = 0; t < N; ++t) sel[t] = (int32_t)t;
+      for (int64_t t = 0; t < N; ++t) sel[t] = (int32_t)(p0 + t);
       continue;
     }
-    double* w = A.scratch_w + p0;
-    double* cdf = A.scratch_c + p0;
-    const double S = (double)A.sumsq[i];
-    for (int64_t j = 0; j < N; ++j) {
-      const double e = (double)A.pe[p0 + j];
-      w[j] = __ddiv_rn(__dmul_rn(e, e), S);
+    double* w = A.sw + p0;
+    double* cdf = A.sc + p0;
+    // norm_rows_ladies: vals = e*e; sum = vals[0] + pairwise(vals[1:]) is
+    // exact for integer values < 2^53, so an int64 sum gives the same double
+    int64_t sq = 0;
+    for (int64_t t = 0; t < N; ++t) sq += (int64_t)A.pe[p0 + t] * A.pe[p0 + t];
+    const double S = (double)sq;
+    for (int64_t t = 0; t < N; ++t) {
+      const double e = (double)A.pe[p0 + t];
+      w[t] = __ddiv_rn(__dmul_rn(e, e), S);
     }
     const uint64_t key = (uint64_t)(A.batch_offset + i);
     int64_t dirty = 0;  // cdf valid below this index
     for (int64_t t = 0; t < take; ++t) {
       double acc = dirty ? cdf[dirty - 1] : 0.0;
-      for (int64_t j = dirty; j < N; ++j) {
-        acc = __dadd_rn(acc, w[j]);
-        cdf[j] = acc;
+      for (int64_t x = dirty; x < N; ++x) {
+        acc = __dadd_rn(acc, w[x]);
+        cdf[x] = acc;
       }
       const double total = cdf[N - 1];
       const double u = uniform53(A.seed, A.epoch, A.depth, key, (uint64_t)t);
@@ -146,64 +240,123 @@ __global__ void k_ladies_sample_exact(LadiesSampleArgs A) {
       int64_t idx = upper_bound(cdf, 0, N, target);
       if (idx >= N) idx = N - 1;
       while (w[idx] == 0.0) --idx;
-      sel[t] = (int32_t)idx;
+      sel[t] = (int32_t)(p0 + idx);
       w[idx] = 0.0;
       dirty = idx;
     }
   }
 }
 
-// Exponential race: the s smallest key_v = -log(u_v) / e_v^2 (ties by
-// position).  Keys are computed once per P nonzero (k_ladies_race_keys);
-// one CTA per batch then radix-selects the take smallest with three
-// histogram passes (12 + 12 + 8 bits of the float key) and resolves exact
-// key ties by position.
-__global__ void k_ladies_race_keys(LadiesSampleArgs A, const int64_t* __restrict__ P_ptr,
-                                   uint32_t* __restrict__ keys) {
-  const int64_t P = *P_ptr;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < P;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = last_le(A.poff, A.k + 1, j);
+// race keys: key = -log(u_v) / e_v^2 as float bits (non-negative floats
+// order like their bit patterns); u_v keyed by (batch key, v) in a domain
+// disjoint from the ITS draws (depth | 2^32).
+__global__ void k_lad_keys(LadiesSampleArgs A) {
+  const int64_t P = A.gpoff[A.gn];
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = last_le(A.gpoff, A.gn + 1, p);
     const double u = uniform53(A.seed, A.epoch, A.depth | (1ULL << 32),
-                               (uint64_t)(A.batch_offset + i), (uint64_t)A.pv[j]);
-    const float e = (float)A.pe[j];
-    const float x = (float)(-log1p(-u)) / (e * e);  // Exp(1) / weight, non-negative
-    keys[j] = __float_as_uint(x);  // non-negative floats order like their bit patterns
+                               (uint64_t)(A.batch_offset + A.g0 + j), (uint64_t)A.pv[p]);
+    const float e = (float)A.pe[p];
+    A.keys[p] = __float_as_uint((float)(-log1p(-u)) / (e * e));
   }
 }
 
-constexpr int kRaceBins = 4096;
-constexpr int kRaceTies = 2048;
-
-__global__ void __launch_bounds__(1024) k_ladies_sample_race(LadiesSampleArgs A,
-                                                           const uint32_t* __restrict__ keys,
-                                                           int32_t* __restrict__ overflow) {
-  __shared__ uint32_t hist[kRaceBins];
-  __shared__ int32_t ties[kRaceTies];
-  __shared__ int s_sel, s_bin, s_acc, s_tie;
-  const int shifts[3] = {20, 8, 0};
-  const int widths[3] = {12, 12, 8};
-  for (int64_t i = blockIdx.x; i < A.k; i += gridDim.x) {
-    const int64_t p0 = A.poff[i], N = A.poff[i + 1] - p0;
-    const int64_t take = N < A.s ? N : A.s;
-    int32_t* sel = A.sel + i * A.s;
-    if (threadIdx.x == 0) A.take[i] = take;
-    if (take == N) {
-      for (int64_t t = threadIdx.x; t < N; t += blockDim.x) sel[t] = (int32_t)t;
-      __syncthreads();
-      continue;
+// histogram of the top 12 key bits per batch (smem-privatised per chunk)
+constexpr int kHistChunk = 8192;
+__global__ void __launch_bounds__(256) k_lad_hist(LadiesSampleArgs A, uint32_t* __restrict__ hist) {
+  __shared__ uint32_t h[kBins];
+  const int64_t P = A.gpoff[A.gn];
+  for (int64_t c0 = (int64_t)blockIdx.x * kHistChunk; c0 < P; c0 += (int64_t)gridDim.x * kHistChunk) {
+    const int64_t c1 = min(c0 + kHistChunk, P);
+    const int64_t j0 = last_le(A.gpoff, A.gn + 1, c0);
+    const int64_t b1 = A.gpoff[j0 + 1];
+    for (int b = threadIdx.x; b < kBins; b += blockDim.x) h[b] = 0;
+    __syncthreads();
+    for (int64_t p = c0 + threadIdx.x; p < c1; p += blockDim.x) {
+      const uint32_t bin = A.keys[p] >> 20;
+      if (p < b1) atomicAdd(&h[bin], 1u);
+      else atomicAdd(&hist[last_le(A.gpoff, A.gn + 1, p) * kBins + bin], 1u);
     }
-    const uint32_t* ki = keys + p0;
-    uint32_t prefix = 0, pmask = 0;
-    int64_t need = take;
-    if (threadIdx.x == 0) s_sel = 0;
-    for (int pass = 0; pass < 3; ++pass) {
+    __syncthreads();
+    for (int b = threadIdx.x; b < kBins; b += blockDim.x)
+      if (h[b]) atomicAdd(&hist[j0 * kBins + b], h[b]);
+    __syncthreads();
+  }
+}
+
+// per batch: take, boundary bin, count strictly below it
+__global__ void k_lad_boundary(LadiesSampleArgs A, const uint32_t* __restrict__ hist,
+                               int32_t* __restrict__ bound) {
+  const int j = blockIdx.x;
+  if (j >= A.gn) return;
+  const int64_t i = A.g0 + j;
+  const int64_t N = A.gpoff[j + 1] - A.gpoff[j];
+  const int64_t take = N < A.s ? N : A.s;
+  if (threadIdx.x == 0) {
+    A.take[i] = take;
+    A.nsel[i] = 0;
+    int64_t acc = 0;
+    int b = 0;
+    if (take < N) {
+      for (; b < kBins; ++b) {
+        if (acc + hist[(int64_t)j * kBins + b] >= take) break;
+        acc += hist[(int64_t)j * kBins + b];
+      }
+    } else {
+      b = kBins;  // everything selected
+    }
+    bound[2 * j] = b;
+    bound[2 * j + 1] = (int32_t)acc;
+  }
+}
+
+// keys strictly below the boundary bin are selected; keys in it become
+// candidates (stored at the batch's P offset)
+__global__ void k_lad_filter(LadiesSampleArgs A, const int32_t* __restrict__ bound,
+                             int32_t* __restrict__ cand, int32_t* __restrict__ ncand) {
+  const int64_t P = A.gpoff[A.gn];
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = last_le(A.gpoff, A.gn + 1, p);
+    const int64_t i = A.g0 + j;
+    const int b = bound[2 * j];
+    const int bin = b == kBins ? -1 : (int)(A.keys[p] >> 20);
+    if (b == kBins || bin < b) {
+      A.sel[i * A.s + atomicAdd(A.nsel + i, 1)] = (int32_t)p;
+    } else if (bin == b) {
+      cand[A.gpoff[j] + atomicAdd(ncand + j, 1)] = (int32_t)p;
+    }
+  }
+}
+
+// one CTA per batch: the need = take - below smallest candidates, two more
+// histogram passes (12 + 8 bits) then ties by position
+__global__ void __launch_bounds__(1024) k_lad_refine(LadiesSampleArgs A,
+                                                   const int32_t* __restrict__ bound,
+                                                   const int32_t* __restrict__ cand,
+                                                   const int32_t* __restrict__ ncand,
+                                                   int32_t* __restrict__ overflow) {
+  __shared__ uint32_t hist[kBins];
+  __shared__ int32_t ties[kTies];
+  __shared__ int s_bin, s_acc, s_tie;
+  const int shifts[2] = {8, 0};
+  const int widths[2] = {12, 8};
+  for (int64_t j = blockIdx.x; j < A.gn; j += gridDim.x) {
+    const int64_t i = A.g0 + j;
+    if (bound[2 * j] == kBins) continue;
+    const int64_t take = A.take[i];
+    int64_t need = take - bound[2 * j + 1];
+    const int32_t* cj = cand + A.gpoff[j];
+    const int m = ncand[j];
+    uint32_t prefix = (uint32_t)bound[2 * j] << 20, pmask = 0xfff00000u;
+    for (int pass = 0; pass < 2; ++pass) {
       const int sh = shifts[pass];
       const uint32_t bm = (1u << widths[pass]) - 1u;
-      for (int b = threadIdx.x; b < kRaceBins; b += blockDim.x) hist[b] = 0;
+      for (int b = threadIdx.x; b < kBins; b += blockDim.x) hist[b] = 0;
       __syncthreads();
-      for (int64_t j = threadIdx.x; j < N; j += blockDim.x) {
-        const uint32_t kk = ki[j];
+      for (int a = threadIdx.x; a < m; a += blockDim.x) {
+        const uint32_t kk = A.keys[cj[a]];
         if ((kk & pmask) == prefix) atomicAdd(&hist[(kk >> sh) & bm], 1u);
       }
       __syncthreads();
@@ -219,92 +372,155 @@ __global__ void __launch_bounds__(1024) k_ladies_sample_race(LadiesSampleArgs A,
       }
       __syncthreads();
       const uint32_t bin = (uint32_t)s_bin;
-      for (int64_t j = threadIdx.x; j < N; j += blockDim.x) {
-        const uint32_t kk = ki[j];
-        if ((kk & pmask) == prefix && ((kk >> sh) & bm) < bin) sel[atomicAdd(&s_sel, 1)] = (int32_t)j;
+      for (int a = threadIdx.x; a < m; a += blockDim.x) {
+        const uint32_t kk = A.keys[cj[a]];
+        if ((kk & pmask) == prefix && ((kk >> sh) & bm) < bin)
+          A.sel[i * A.s + atomicAdd(A.nsel + i, 1)] = cj[a];
       }
       need -= s_acc;
       prefix |= bin << sh;
       pmask |= bm << sh;
       __syncthreads();
     }
-    // remaining `need` picks among keys exactly equal to prefix: smallest positions
     if (threadIdx.x == 0) s_tie = 0;
     __syncthreads();
-    for (int64_t j = threadIdx.x; j < N; j += blockDim.x)
-      if (ki[j] == prefix) {
+    for (int a = threadIdx.x; a < m; a += blockDim.x)
+      if (A.keys[cj[a]] == prefix) {
         const int t = atomicAdd(&s_tie, 1);
-        if (t < kRaceTies) ties[t] = (int32_t)j; else atomicExch(overflow, 1);
+        if (t < kTies) ties[t] = cj[a]; else atomicExch(overflow, 1);
       }
     __syncthreads();
-    const int m = min(s_tie, kRaceTies);
-    const int base = s_sel;
-    for (int a2 = threadIdx.x; a2 < m; a2 += blockDim.x) {
+    const int mt = min(s_tie, kTies);
+    const int base = A.nsel[i];
+    for (int a = threadIdx.x; a < mt; a += blockDim.x) {
       int rank = 0;
-      for (int b2 = 0; b2 < m; ++b2) rank += ties[b2] < ties[a2] ? 1 : 0;
-      if (rank < need) sel[base + rank] = ties[a2];
+      for (int b2 = 0; b2 < mt; ++b2) rank += ties[b2] < ties[a] ? 1 : 0;
+      if (rank < need) A.sel[i * A.s + base + rank] = ties[a];
     }
+    __syncthreads();
+    if (threadIdx.x == 0) A.nsel[i] = (int32_t)take;
     __syncthreads();
   }
 }
 
-// Sort each batch's selected positions ascending (positions ascend with
-// vertex id) and emit the frontier row: fcol[fptr[i] + r] = pv[p0 + pos].
-__global__ void __launch_bounds__(256) k_ladies_emit(const int64_t* __restrict__ poff,
-                                                   const int32_t* __restrict__ pv, int64_t k,
-                                                   int32_t s, const int32_t* __restrict__ sel,
-                                                   const int64_t* __restrict__ fptr,
-                                                   int32_t* __restrict__ fcol) {
-  for (int64_t i = blockIdx.x; i < k; i += gridDim.x) {
-    const int64_t take = fptr[i + 1] - fptr[i];
-    const int32_t* si = sel + i * s;
+// sorted sampled vertices of each batch of the group: Sfix[i*s + r]
+__global__ void __launch_bounds__(256) k_lad_emit(LadiesSampleArgs A, int32_t* __restrict__ Sfix) {
+  for (int64_t j = blockIdx.x; j < A.gn; j += gridDim.x) {
+    const int64_t i = A.g0 + j;
+    const int64_t take = A.take[i];
+    const int32_t* si = A.sel + i * A.s;
     for (int64_t a = threadIdx.x; a < take; a += blockDim.x) {
       const int32_t x = si[a];
       int64_t rank = 0;
       for (int64_t b = 0; b < take; ++b) rank += si[b] < x ? 1 : 0;
-      fcol[fptr[i] + rank] = pv[poff[i] + x];
+      Sfix[i * A.s + rank] = A.pv[x];  // P positions ascend with v inside a batch
     }
   }
 }
 
-// marker[i*n + v] = rank + 1 for the sampled vertices (0 elsewhere)
-__global__ void k_ladies_mark(const int64_t* __restrict__ fptr, int64_t k, int64_t n,
-                              const int32_t* __restrict__ fcol, int32_t* __restrict__ marker,
-                              int32_t clear) {
+__global__ void k_lad_pack_s(const int64_t* __restrict__ fptr, int64_t k, int32_t s,
+                             const int32_t* __restrict__ Sfix, int32_t* __restrict__ fcol) {
   const int64_t F = fptr[k];
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < F;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = last_le(fptr, k + 1, e);
-    marker[i * n + fcol[e]] = clear ? 0 : (int32_t)(e - fptr[i] + 1);
+    fcol[e] = Sfix[i * s + (e - fptr[i])];
   }
 }
 
-// A_S row q (batch i, vertex u = qcol[q]): the marked ranks of A[u,:] in
-// column order.  COUNT pass writes rcnt[q]; WRITE pass fills acol.
-template <bool WRITE>
-__global__ void __launch_bounds__(kLadiesThreads) k_ladies_extract(
+// ------------------------------------------------------------- extraction
+
+// shared layout iff every batch took the same count (ladies_assemble)
+__global__ void k_lad_layout(const int64_t* __restrict__ fptr, int64_t k,
+                             int64_t* __restrict__ coloff, int64_t* __restrict__ sizes) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  bool shared = true;
+  for (int64_t i = 1; i < k; ++i)
+    if (fptr[i + 1] - fptr[i] != fptr[1] - fptr[0]) shared = false;
+  for (int64_t i = 0; i <= k; ++i) coloff[i] = shared ? 0 : fptr[i];
+  sizes[1] = fptr[k];
+  sizes[3] = k == 0 ? 0 : (shared ? fptr[1] - fptr[0] : fptr[k]);
+}
+
+struct RcapF {
+  const int32_t* qcol;
+  const int64_t* rowptr;
+  const int64_t* qoff;
+  const int64_t* fptr;
+  int64_t k;
+  __device__ int64_t operator()(int64_t q) const {
+    const int32_t u = qcol[q];
+    const int64_t d = rowptr[u + 1] - rowptr[u];
+    const int64_t i = last_le(qoff, k + 1, q);
+    const int64_t t = fptr[i + 1] - fptr[i];
+    return d < t ? d : t;
+  }
+};
+
+// one warp per A_S row q: the ranks of A[u,:] ∩ S_i, ascending
+__global__ void __launch_bounds__(kLadiesThreads) k_lad_extract(
     const int64_t* __restrict__ qoff, int64_t k, const int32_t* __restrict__ qcol,
-    const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col, int64_t n,
-    const int32_t* __restrict__ marker, const int64_t* __restrict__ coloff,
-    int32_t* __restrict__ rcnt, const int64_t* __restrict__ aptr, int32_t* __restrict__ acol) {
+    const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+    const int64_t* __restrict__ fptr, const int32_t* __restrict__ fcol,
+    const int64_t* __restrict__ coloff, const int64_t* __restrict__ slot,
+    int32_t* __restrict__ slots, int32_t* __restrict__ rcnt) {
+  __shared__ int32_t sS[kLadiesThreads / 32][kSmaxSmem];
   const unsigned FULL = 0xffffffffu;
-  const int lane = lane_id();
+  const int lane = lane_id(), wib = threadIdx.x >> 5;
   const int64_t QN = qoff[k];
+  int64_t staged = -1;
   for (int64_t q = global_warp(); q < QN; q += grid_warps()) {
     const int64_t i = last_le(qoff, k + 1, q);
-    const int32_t u = qcol[q];
-    const int64_t a0 = rowptr[u], a1 = rowptr[u + 1];
-    const int32_t* mi = marker + i * n;
-    int64_t o = WRITE ? aptr[q] : 0;
-    const int64_t cbase = WRITE ? coloff[i] : 0;
-    for (int64_t e0 = a0; e0 < a1; e0 += 32) {
-      const int64_t e = e0 + lane;
-      const int32_t m = e < a1 ? mi[__ldg(col + e)] : 0;
-      const unsigned bal = __ballot_sync(FULL, m > 0);
-      if (WRITE && m > 0) acol[o + __popc(bal & ((1u << lane) - 1))] = (int32_t)(cbase + m - 1);
-      o += __popc(bal);
+    const int64_t f0 = fptr[i], take = fptr[i + 1] - f0;
+    const bool in_smem = take <= kSmaxSmem;
+    if (in_smem && staged != i) {
+      __syncwarp();
+      for (int64_t r = lane; r < take; r += 32) sS[wib][r] = fcol[f0 + r];
+      __syncwarp();
+      staged = i;
     }
-    if (!WRITE && lane == 0) rcnt[q] = (int32_t)o;
+    const int32_t* S = in_smem ? sS[wib] : fcol + f0;
+    const int32_t u = qcol[q];
+    const int64_t a0 = rowptr[u], d = rowptr[u + 1] - a0;
+    const int64_t cb = coloff[i];
+    int32_t* out = slots + slot[q];
+    int64_t o = 0;
+    if (d <= 16 * take) {
+      // stream A[u,:]; binary search each entry in S_i
+      for (int64_t e0 = 0; e0 < d; e0 += 32) {
+        int rank = -1;
+        if (e0 + lane < d) {
+          const int32_t v = __ldg(col + a0 + e0 + lane);
+          int lo = 0, hi = (int)take;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (S[mid] < v) lo = mid + 1; else hi = mid;
+          }
+          if (lo < take && S[lo] == v) rank = lo;
+        }
+        const unsigned bal = __ballot_sync(FULL, rank >= 0);
+        if (rank >= 0) out[o + __popc(bal & ((1u << lane) - 1))] = (int32_t)(cb + rank);
+        o += __popc(bal);
+      }
+    } else {
+      // hub row: binary search each sampled vertex in A[u,:]
+      for (int64_t r0 = 0; r0 < take; r0 += 32) {
+        bool hit = false;
+        if (r0 + lane < take) {
+          const int32_t v = S[r0 + lane];
+          int64_t lo = 0, hi = d;
+          while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (__ldg(col + a0 + mid) < v) lo = mid + 1; else hi = mid;
+          }
+          hit = lo < d && __ldg(col + a0 + lo) == v;
+        }
+        const unsigned bal = __ballot_sync(FULL, hit);
+        if (hit) out[o + __popc(bal & ((1u << lane) - 1))] = (int32_t)(cb + r0 + lane);
+        o += __popc(bal);
+      }
+    }
+    if (lane == 0) rcnt[q] = (int32_t)o;
   }
 }
 
@@ -316,30 +532,36 @@ struct TakeLF {
   const int64_t* t;
   __device__ int64_t operator()(int64_t i) const { return t[i]; }
 };
-struct NnzF {
-  const int64_t* t;
-  __device__ int64_t operator()(int64_t i) const { return t[i]; }
-};
 
-// shared layout iff every batch took the same count (ladies_assemble)
-__global__ void k_ladies_layout(const int64_t* __restrict__ fptr, int64_t k,
-                                const int64_t* __restrict__ qoff, const int64_t* __restrict__ aptr,
-                                const int64_t* __restrict__ poff,
-                                int64_t* __restrict__ coloff, int64_t* __restrict__ sizes) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) sizes[4] = poff[k];  // nnz(P)
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  bool shared = true;
-  for (int64_t i = 1; i < k; ++i)
-    if (fptr[i + 1] - fptr[i] != fptr[1] - fptr[0]) shared = false;
-  for (int64_t i = 0; i <= k; ++i) coloff[i] = shared ? 0 : fptr[i];
+__global__ void __launch_bounds__(kLadiesThreads) k_lad_pack_a(
+    const int64_t* __restrict__ qoff, int64_t k, const int64_t* __restrict__ slot,
+    const int32_t* __restrict__ slots, const int64_t* __restrict__ aptr,
+    int32_t* __restrict__ acol) {
+  const int lane = lane_id();
   const int64_t QN = qoff[k];
-  sizes[0] = QN;                                              // A_S rows
-  sizes[1] = fptr[k];                                         // F
-  sizes[2] = aptr[QN];                                        // A_S nnz
-  sizes[3] = k == 0 ? 0 : (shared ? fptr[1] - fptr[0] : fptr[k]);  // A_S cols
+  for (int64_t q = global_warp(); q < QN; q += grid_warps()) {
+    const int64_t o = aptr[q], c = aptr[q + 1] - o, s0 = slot[q];
+    for (int64_t x = lane; x < c; x += 32) acol[o + x] = slots[s0 + x];
+  }
 }
 
-static int grid_cap(int64_t n, int threads, int cap) {
+__global__ void k_lad_sizes(const int64_t* __restrict__ qoff, int64_t k,
+                            const int64_t* __restrict__ aptr, const int64_t* __restrict__ nnz_b,
+                            int64_t* __restrict__ sizes) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int64_t QN = qoff[k];
+  int64_t p = 0;
+  for (int64_t i = 0; i < k; ++i) p += nnz_b[i];
+  sizes[0] = QN;
+  sizes[2] = aptr[QN];
+  sizes[4] = p;
+}
+
+__global__ void k_lad_set(int64_t* p, int64_t v) { *p = v; }
+
+// ============================================================== host side
+
+static int gcap(int64_t n, int threads, int cap) {
   int64_t g = (n + threads - 1) / threads;
   if (g < 1) g = 1;
   if (g > cap) g = cap;
@@ -347,80 +569,106 @@ static int grid_cap(int64_t n, int threads, int cap) {
 }
 
 struct LadiesWs {
-  int32_t* cnt;      // k * n
+  uint32_t* cnt32;   // packed uint16 counters of one group
   int64_t* nnz_b;    // k + 1
-  int64_t* poff;     // k + 1
-  int32_t* pv;       // P nnz cap
+  int64_t* gpoff;    // group + 1
+  int32_t* pv;       // group P cap
   int32_t* pe;
   double* sw;        // exact scratch
   double* sc;
-  int64_t* sumsq;    // k
-  uint32_t* keys;    // race keys (P nnz cap)
+  uint32_t* keys;    // race keys
+  int32_t* cand;     // race candidates (P layout)
+  int32_t* ncand;    // group
+  uint32_t* hist;    // group * kBins
+  int32_t* bound;    // group * 2
   int32_t* sel;      // k * s_max
+  int32_t* nsel;     // k
   int64_t* take;     // k
+  int32_t* Sfix;     // k * s_max
+  int64_t* qg;       // Q cap + 1 (degree prefix of Q rows)
+  int64_t* slot;     // Q cap + 1
+  int32_t* slots;    // Q cap * s_max
   int32_t* rcnt;     // Q cap
+  int64_t* tile_off; // compaction tiles + 1
   int64_t* scan_ws;
-  int64_t* d_k;      // device scalar k
+  int64_t* d_scalar; // 4 device scalars (k, words, tiles, ...)
   int32_t* overflow;
   size_t bytes;
 };
 
 static size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
-static LadiesWs ladies_ws_layout(char* base, int64_t k, int64_t n, int64_t p_cap, int64_t q_cap,
-                                 int64_t s_max, bool exact) {
+struct LadiesPlan {
+  int64_t gsize, words, tiles, p_cap, q_cap, s_max;
+};
+
+static LadiesPlan ladies_plan(int64_t k, int64_t n, int64_t q1_cap, int32_t layers,
+                              const int64_t* fanouts) {
+  LadiesPlan p{};
+  p.s_max = 1;
+  p.q_cap = q1_cap;
+  for (int32_t l = 0; l < layers; ++l) {
+    if (fanouts[l] > p.s_max) p.s_max = fanouts[l];
+    if (k * fanouts[l] > p.q_cap) p.q_cap = k * fanouts[l];
+  }
+  p.gsize = n > 0 ? kGroupBytes / (2 * n) : k;
+  if (p.gsize < 1) p.gsize = 1;
+  if (p.gsize > k) p.gsize = k > 0 ? k : 1;
+  p.words = (p.gsize * n + 1) / 2 + 1;
+  p.tiles = (2 * p.words + kCompTile - 1) / kCompTile;
+  p.p_cap = p.gsize * n;
+  return p;
+}
+
+static LadiesWs ladies_ws_layout(char* base, int64_t k, const LadiesPlan& P, bool exact) {
   LadiesWs w{};
   size_t off = 0;
   auto take = [&](size_t bytes) { char* p = base ? base + off : nullptr; off += al(bytes); return p; };
-  w.cnt = (int32_t*)take(sizeof(int32_t) * (size_t)(k * n + 1));
+  w.cnt32 = (uint32_t*)take(sizeof(uint32_t) * P.words);
   w.nnz_b = (int64_t*)take(sizeof(int64_t) * (k + 1));
-  w.poff = (int64_t*)take(sizeof(int64_t) * (k + 1));
-  w.pv = (int32_t*)take(sizeof(int32_t) * (p_cap + 1));
-  w.pe = (int32_t*)take(sizeof(int32_t) * (p_cap + 1));
-  w.sw = (double*)take(exact ? sizeof(double) * (p_cap + 1) : 8);
-  w.sc = (double*)take(exact ? sizeof(double) * (p_cap + 1) : 8);
-  w.sumsq = (int64_t*)take(sizeof(int64_t) * (k + 1));
-  w.keys = (uint32_t*)take(exact ? 8 : sizeof(uint32_t) * (p_cap + 1));
-  w.sel = (int32_t*)take(sizeof(int32_t) * (k * s_max + 1));
+  w.gpoff = (int64_t*)take(sizeof(int64_t) * (P.gsize + 1));
+  w.pv = (int32_t*)take(sizeof(int32_t) * (P.p_cap + 1));
+  w.pe = (int32_t*)take(sizeof(int32_t) * (P.p_cap + 1));
+  w.sw = (double*)take(exact ? sizeof(double) * (P.p_cap + 1) : 8);
+  w.sc = (double*)take(exact ? sizeof(double) * (P.p_cap + 1) : 8);
+  w.keys = (uint32_t*)take(exact ? 8 : sizeof(uint32_t) * (P.p_cap + 1));
+  w.cand = (int32_t*)take(exact ? 8 : sizeof(int32_t) * (P.p_cap + 1));
+  w.ncand = (int32_t*)take(sizeof(int32_t) * (P.gsize + 1));
+  w.hist = (uint32_t*)take(sizeof(uint32_t) * P.gsize * kBins);
+  w.bound = (int32_t*)take(sizeof(int32_t) * 2 * (P.gsize + 1));
+  w.sel = (int32_t*)take(sizeof(int32_t) * (k * P.s_max + 1));
+  w.nsel = (int32_t*)take(sizeof(int32_t) * (k + 1));
   w.take = (int64_t*)take(sizeof(int64_t) * (k + 1));
-  w.rcnt = (int32_t*)take(sizeof(int32_t) * (q_cap + 1));
-  const int64_t sn = q_cap > k ? q_cap : k;
+  w.Sfix = (int32_t*)take(sizeof(int32_t) * (k * P.s_max + 1));
+  w.qg = (int64_t*)take(sizeof(int64_t) * (P.q_cap + 1));
+  w.slot = (int64_t*)take(sizeof(int64_t) * (P.q_cap + 1));
+  w.slots = (int32_t*)take(sizeof(int32_t) * (P.q_cap * P.s_max + 1));
+  w.rcnt = (int32_t*)take(sizeof(int32_t) * (P.q_cap + 1));
+  w.tile_off = (int64_t*)take(sizeof(int64_t) * (P.tiles + 1));
+  int64_t sn = P.q_cap > k ? P.q_cap : k;
+  if (P.tiles > sn) sn = P.tiles;
   w.scan_ws = (int64_t*)take(sizeof(int64_t) * scan_workspace_elems<int64_t>(sn + 1));
-  w.d_k = (int64_t*)take(sizeof(int64_t));
+  w.d_scalar = (int64_t*)take(sizeof(int64_t) * 4);
   w.overflow = (int32_t*)take(sizeof(int32_t));
   w.bytes = off;
   return w;
 }
 
-// P nnz capacity: N_i <= min(n, sum of degrees of Q_i) <= n per batch.
-static int64_t ladies_p_cap(int64_t k, int64_t n) { return k * n; }
-
 int ladies_workspace(const Graph* g, int64_t k, int64_t q1_cap, int32_t layers,
                      const int64_t* fanouts, int32_t mode, size_t* bytes) {
-  int64_t s_max = 1, q_cap = q1_cap;
-  for (int32_t l = 0; l < layers; ++l) {
-    if (fanouts[l] > s_max) s_max = fanouts[l];
-    if (k * fanouts[l] > q_cap) q_cap = k * fanouts[l];
-  }
-  *bytes = ladies_ws_layout(nullptr, k, g->n, ladies_p_cap(k, g->n), q_cap, s_max,
-                            mode == GB_LADIES_EXACT).bytes;
+  const LadiesPlan P = ladies_plan(k, g->n, q1_cap, layers, fanouts);
+  *bytes = ladies_ws_layout(nullptr, k, P, mode == GB_LADIES_EXACT).bytes;
   return GB_OK;
 }
-
-__global__ void k_set_i64_l(int64_t* p, int64_t v) { *p = v; }
 
 int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t* d_qverts,
                 int64_t q1_cap, int32_t layers, const int64_t* fanouts, uint64_t seed,
                 uint64_t epoch, int64_t batch_offset, int32_t mode, gb_ladies_layer_out* L,
                 int64_t* d_sizes, void* d_ws, size_t ws_bytes, cudaStream_t st) {
   const bool exact = mode == GB_LADIES_EXACT;
-  int64_t s_max = 1, q_cap = q1_cap;
-  for (int32_t l = 0; l < layers; ++l) {
-    if (fanouts[l] > s_max) s_max = fanouts[l];
-    if (k * fanouts[l] > q_cap) q_cap = k * fanouts[l];
-  }
   const int64_t n = g->n;
-  LadiesWs ws = ladies_ws_layout((char*)d_ws, k, n, ladies_p_cap(k, n), q_cap, s_max, exact);
+  const LadiesPlan P = ladies_plan(k, n, q1_cap, layers, fanouts);
+  LadiesWs ws = ladies_ws_layout((char*)d_ws, k, P, exact);
   if (ws.bytes > ws_bytes) {
     set_error("ladies workspace too small: need %zu bytes, got %zu", ws.bytes, ws_bytes);
     return GB_ERR_CAPACITY;
@@ -433,13 +681,16 @@ int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t*
     }
     qc = k * fanouts[l];
   }
-  GB_CUDA(cudaMemsetAsync(ws.cnt, 0, sizeof(int32_t) * (size_t)(k * n + 1), st));
-  GB_CUDA(cudaMemsetAsync(ws.overflow, 0, sizeof(int32_t), st));
-  k_set_i64_l<<<1, 1, 0, st>>>(ws.d_k, k);
-  count_launches(1);
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   if (sms <= 0) sms = kNumSMs;
+  int64_t* d_k = ws.d_scalar;
+  int64_t* d_tiles = ws.d_scalar + 1;
+  GB_CUDA(cudaMemsetAsync(ws.cnt32, 0, sizeof(uint32_t) * P.words, st));
+  GB_CUDA(cudaMemsetAsync(ws.overflow, 0, sizeof(int32_t), st));
+  k_lad_set<<<1, 1, 0, st>>>(d_k, k);
+  k_lad_set<<<1, 1, 0, st>>>(d_tiles, P.tiles);
+  count_launches(2);
   qc = q1_cap;
   for (int32_t l = 0; l < layers; ++l) {
     const int32_t s = (int32_t)fanouts[l];
@@ -447,52 +698,69 @@ int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t*
     const int64_t* qoff = l == 0 ? d_qoff : L[l - 1].fptr;
     const int32_t* qcol = l == 0 ? d_qverts : L[l - 1].fcol;
     const int64_t* d_QN = qoff + k;
-    // ---- P = Q A (counts) + first touches
+    int64_t* sizes = d_sizes + kLadiesSizes * l;
+    int rc = device_exclusive_scan<int64_t>(d_QN, qc, QDegF{qcol, g->rowptr}, ws.qg, ws.scan_ws, st);
+    if (rc) return rc;
     GB_CUDA(cudaMemsetAsync(ws.nnz_b, 0, sizeof(int64_t) * (k + 1), st));
-    prof_mark(st);
-    k_ladies_count<<<grid_cap(qc * 32, kLadiesThreads, 16 * sms), kLadiesThreads, 0, st>>>(
-        qoff, k, qcol, g->rowptr, g->col, n, ws.cnt, ws.nnz_b);
-    GB_LAUNCH_CHECK("k_ladies_count");
-    prof_mark(st);
-    int rc = device_exclusive_scan<int64_t>(ws.d_k, k, NnzF{ws.nnz_b}, ws.poff, ws.scan_ws, st);
-    if (rc) return rc;
-    k_ladies_compact<<<(int)(k < 4 * sms ? (k > 0 ? k : 1) : 4 * sms), 1024, 0, st>>>(
-        k, n, ws.cnt, ws.poff, ws.pv, ws.pe, ws.sumsq);
-    GB_LAUNCH_CHECK("k_ladies_compact");
-    // ---- NORM + SAMPLE
-    LadiesSampleArgs A{};
-    A.poff = ws.poff; A.pv = ws.pv; A.pe = ws.pe; A.sumsq = ws.sumsq; A.k = k; A.s = s;
-    A.batch_offset = batch_offset; A.seed = seed; A.epoch = epoch; A.depth = (uint64_t)(l + 1);
-    A.scratch_w = ws.sw; A.scratch_c = ws.sc; A.sel = ws.sel; A.take = ws.take;
-    if (exact)
-      k_ladies_sample_exact<<<grid_cap(k, 32, 4 * sms), 32, 0, st>>>(A);
-    else {
-      k_ladies_race_keys<<<grid_cap(k * n, 256, 32 * sms), 256, 0, st>>>(A, ws.poff + k, ws.keys);
-      k_ladies_sample_race<<<(int)(k < 4 * sms ? (k > 0 ? k : 1) : 4 * sms), 1024, 0, st>>>(
-          A, ws.keys, ws.overflow);
-      count_launches(1);
+    for (int64_t g0 = 0; g0 < k; g0 += P.gsize) {
+      const int64_t g1 = g0 + P.gsize < k ? g0 + P.gsize : k;
+      const int64_t gn = g1 - g0;
+      const int64_t words = (gn * n + 1) / 2;
+      // ---- P = Q A for this group
+      prof_mark(st);
+      k_lad_count<<<4 * sms, kLadiesThreads, 0, st>>>(qoff, k, g0, g1, qcol, ws.qg, g->rowptr,
+                                                      g->col, n, ws.cnt32, ws.nnz_b);
+      GB_LAUNCH_CHECK("k_lad_count");
+      prof_mark(st);
+      k_lad_gpoff<<<1, 1, 0, st>>>(ws.nnz_b, g0, gn, ws.gpoff);
+      k_lad_compact_count<<<gcap(P.tiles, 1, 8 * sms), 256, 0, st>>>(ws.cnt32, words, ws.tile_off);
+      rc = device_exclusive_scan<int64_t>(d_tiles, P.tiles, TileF{ws.tile_off}, ws.tile_off,
+                                          ws.scan_ws, st);
+      if (rc) return rc;
+      k_lad_compact_write<<<gcap(P.tiles, 1, 8 * sms), 256, 0, st>>>(ws.cnt32, words, n,
+                                                                    ws.tile_off, ws.pv, ws.pe);
+      GB_LAUNCH_CHECK("k_lad_compact");
+      // ---- NORM + SAMPLE
+      LadiesSampleArgs A{};
+      A.gpoff = ws.gpoff; A.pv = ws.pv; A.pe = ws.pe; A.g0 = g0; A.gn = gn; A.s = s;
+      A.batch_offset = batch_offset; A.seed = seed; A.epoch = epoch; A.depth = (uint64_t)(l + 1);
+      A.sw = ws.sw; A.sc = ws.sc; A.keys = ws.keys; A.sel = ws.sel; A.nsel = ws.nsel;
+      A.take = ws.take;
+      if (exact) {
+        k_lad_sample_exact<<<gcap(gn, 32, 4 * sms), 32, 0, st>>>(A);
+        count_launches(1);
+      } else {
+        GB_CUDA(cudaMemsetAsync(ws.hist, 0, sizeof(uint32_t) * gn * kBins, st));
+        GB_CUDA(cudaMemsetAsync(ws.ncand, 0, sizeof(int32_t) * (gn + 1), st));
+        k_lad_keys<<<16 * sms, 256, 0, st>>>(A);
+        k_lad_hist<<<4 * sms, 256, 0, st>>>(A, ws.hist);
+        k_lad_boundary<<<(int)gn, 32, 0, st>>>(A, ws.hist, ws.bound);
+        k_lad_filter<<<16 * sms, 256, 0, st>>>(A, ws.bound, ws.cand, ws.ncand);
+        k_lad_refine<<<(int)gn, 1024, 0, st>>>(A, ws.bound, ws.cand, ws.ncand, ws.overflow);
+        count_launches(5);
+      }
+      GB_LAUNCH_CHECK("k_lad_sample");
+      k_lad_emit<<<(int)gn, 256, 0, st>>>(A, ws.Sfix);
+      GB_LAUNCH_CHECK("k_lad_emit");
+      count_launches(6);
     }
-    GB_LAUNCH_CHECK("k_ladies_sample");
-    rc = device_exclusive_scan<int64_t>(ws.d_k, k, TakeLF{ws.take}, o.fptr, ws.scan_ws, st);
+    rc = device_exclusive_scan<int64_t>(d_k, k, TakeLF{ws.take}, o.fptr, ws.scan_ws, st);
     if (rc) return rc;
-    k_ladies_emit<<<(int)(k < 4 * sms ? (k > 0 ? k : 1) : 4 * sms), 256, 0, st>>>(
-        ws.poff, ws.pv, k, s, ws.sel, o.fptr, o.fcol);
-    GB_LAUNCH_CHECK("k_ladies_emit");
+    k_lad_pack_s<<<gcap(k * s, 256, 16 * sms), 256, 0, st>>>(o.fptr, k, s, ws.Sfix, o.fcol);
+    k_lad_layout<<<1, 1, 0, st>>>(o.fptr, k, o.coloff, sizes);
     // ---- EXTRACT A_S = Q_R A Q_C
-    const int mgrid = grid_cap(k * s, 256, 16 * sms);
-    k_ladies_mark<<<mgrid, 256, 0, st>>>(o.fptr, k, n, o.fcol, ws.cnt, 0);
-    const int egrid = grid_cap(qc * 32, kLadiesThreads, 16 * sms);
-    k_ladies_extract<false><<<egrid, kLadiesThreads, 0, st>>>(
-        qoff, k, qcol, g->rowptr, g->col, n, ws.cnt, nullptr, ws.rcnt, nullptr, nullptr);
+    rc = device_exclusive_scan<int64_t>(d_QN, qc, RcapF{qcol, g->rowptr, qoff, o.fptr, k},
+                                        ws.slot, ws.scan_ws, st);
+    if (rc) return rc;
+    k_lad_extract<<<8 * sms, kLadiesThreads, 0, st>>>(qoff, k, qcol, g->rowptr, g->col, o.fptr,
+                                                     o.fcol, o.coloff, ws.slot, ws.slots,
+                                                     ws.rcnt);
     rc = device_exclusive_scan<int64_t>(d_QN, qc, RcntF{ws.rcnt}, o.aptr, ws.scan_ws, st);
     if (rc) return rc;
-    k_ladies_layout<<<1, 1, 0, st>>>(o.fptr, k, qoff, o.aptr, ws.poff, o.coloff,
-                                     d_sizes + kLadiesSizes * l);
-    k_ladies_extract<true><<<egrid, kLadiesThreads, 0, st>>>(
-        qoff, k, qcol, g->rowptr, g->col, n, ws.cnt, o.coloff, nullptr, o.aptr, o.acol);
-    k_ladies_mark<<<mgrid, 256, 0, st>>>(o.fptr, k, n, o.fcol, ws.cnt, 1);
-    GB_LAUNCH_CHECK("k_ladies_extract");
-    count_launches(10);
+    k_lad_pack_a<<<8 * sms, kLadiesThreads, 0, st>>>(qoff, k, ws.slot, ws.slots, o.aptr, o.acol);
+    k_lad_sizes<<<1, 1, 0, st>>>(qoff, k, o.aptr, ws.nnz_b, sizes);
+    GB_LAUNCH_CHECK("k_lad_extract");
+    count_launches(5);
     qc = k * s;
   }
   return GB_OK;
