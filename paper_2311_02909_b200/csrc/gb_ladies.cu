@@ -92,16 +92,12 @@ __global__ void __launch_bounds__(kLadiesThreads) k_lad_count(
     const int64_t a0 = rowptr[u];
     uint32_t* ci = cnt32;
     const int64_t cb = (i - g0) * n;
-    int first = 0;
     for (int64_t e = a0 + e0 + lane; e < a0 + e1; e += 32) {
       const int64_t v = cb + __ldg(col + e);
-      const uint32_t sh = (uint32_t)(v & 1) << 4;
-      const uint32_t old = atomicAdd(ci + (v >> 1), 1u << sh);
-      if (((old >> sh) & 0xffffu) == 0) ++first;
+      atomicAdd(ci + (v >> 1), 1u << ((uint32_t)(v & 1) << 4));  // no return: RED
     }
-    first = warp_sum(first);
-    if (lane == 0 && first) atomicAdd((unsigned long long*)(nnz_b + i), (unsigned long long)first);
   }
+  (void)nnz_b;
 }
 
 // Group-local nonzero offsets: gpoff[j] = sum_{g0 <= i < g0 + j} nnz_b[i].
@@ -119,22 +115,39 @@ __global__ void k_lad_gpoff(const int64_t* __restrict__ nnz_b, int64_t g0, int64
 // scan + scatter (v, e) and clear the counters.
 constexpr int kCompTile = 4096;  // counters per tile (256 threads x 16)
 
+// Also N_i: nonzeros per batch (a thread's 16 counters straddle at most one
+// batch boundary when n >= 16; otherwise counted one by one).
 __global__ void __launch_bounds__(256) k_lad_compact_count(const uint32_t* __restrict__ cnt32,
-                                                         int64_t words,
-                                                         int64_t* __restrict__ tile_cnt) {
+                                                         int64_t words, int64_t n, int64_t g0,
+                                                         int64_t* __restrict__ tile_cnt,
+                                                         int64_t* __restrict__ nnz_b) {
   __shared__ int64_t sw[33];
   const int64_t ntiles = (2 * words + kCompTile - 1) / kCompTile;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int64_t w0 = t * (kCompTile / 2) + threadIdx.x * 8;
     int64_t c = 0;
+    int64_t jcur = (2 * w0) / n, ccur = 0, next = (jcur + 1) * n;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int64_t wi = w0 + j;
       if (wi < words) {
         const uint32_t x = cnt32[wi];
-        c += ((x & 0xffffu) != 0) + ((x >> 16) != 0);
+        for (int h = 0; h < 2; ++h) {
+          if ((x >> (16 * h)) & 0xffffu) {
+            const int64_t f = 2 * wi + h;
+            if (f >= next) {
+              if (ccur) atomicAdd((unsigned long long*)(nnz_b + g0 + jcur), (unsigned long long)ccur);
+              jcur = f / n;
+              next = (jcur + 1) * n;
+              ccur = 0;
+            }
+            ++ccur;
+            ++c;
+          }
+        }
       }
     }
+    if (ccur) atomicAdd((unsigned long long*)(nnz_b + g0 + jcur), (unsigned long long)ccur);
     int64_t total;
     block_excl_scan<int64_t>(c, sw, total);
     if (threadIdx.x == 0) tile_cnt[t] = total;
@@ -146,11 +159,29 @@ struct TileF {
   __device__ int64_t operator()(int64_t i) const { return t[i]; }
 };
 
+// race key of P entry (batch key, v, e): -log(u) / e^2 as float bits
+// (non-negative floats order like their bit patterns); u keyed by
+// (batch key, v) in a domain disjoint from the ITS draws (depth | 2^32).
+struct RaceKey {
+  uint64_t seed, epoch, depth;
+  int64_t key0;  // batch_offset + g0
+  __device__ __forceinline__ uint32_t operator()(int64_t j, int32_t v, uint32_t e) const {
+    const uint64_t w = philox_word(seed, epoch, depth | (1ULL << 32), (uint64_t)(key0 + j),
+                                   (uint64_t)v);
+    const float u = ((float)(w >> 40) + 0.5f) * 0x1.0p-24f;  // (0, 1)
+    const float fe = (float)e;
+    return __float_as_uint(-__logf(u) / (fe * fe));
+  }
+};
+
+// keys != nullptr (race mode): also writes the race key of every nonzero
 __global__ void __launch_bounds__(256) k_lad_compact_write(uint32_t* __restrict__ cnt32,
                                                          int64_t words, int64_t n,
                                                          const int64_t* __restrict__ tile_off,
                                                          int32_t* __restrict__ pv,
-                                                         int32_t* __restrict__ pe) {
+                                                         int32_t* __restrict__ pe,
+                                                         uint32_t* __restrict__ keys,
+                                                         RaceKey rk) {
   __shared__ int64_t sw[33];
   const int64_t ntiles = (2 * words + kCompTile - 1) / kCompTile;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -165,6 +196,7 @@ __global__ void __launch_bounds__(256) k_lad_compact_write(uint32_t* __restrict_
     }
     int64_t total;
     int64_t o = block_excl_scan<int64_t>(c, sw, total) + tile_off[t];
+    int64_t jb = (2 * w0) / n, base = jb * n;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       if (!x[j]) continue;
@@ -172,14 +204,38 @@ __global__ void __launch_bounds__(256) k_lad_compact_write(uint32_t* __restrict_
       for (int h = 0; h < 2; ++h) {
         const uint32_t e = (x[j] >> (16 * h)) & 0xffffu;
         if (e) {
-          pv[o] = (int32_t)((flat + h) % n);
+          int64_t v = flat + h - base;
+          while (v >= n) { ++jb; base += n; v -= n; }
+          pv[o] = (int32_t)v;
           pe[o] = (int32_t)e;
+          if (keys) keys[o] = rk(jb, (int32_t)v, e);
           ++o;
         }
       }
       cnt32[w0 + j] = 0u;
     }
   }
+}
+
+// Block-wide search of the first bin where the running count reaches need:
+// every thread owns kBins / blockDim consecutive bins.  Returns (bin, count
+// strictly below it) through shared memory.
+__device__ __forceinline__ void block_find_bin(const uint32_t* hist, int nbins, int64_t need,
+                                               int64_t* sw, int* s_bin, int* s_acc) {
+  const int per = (nbins + blockDim.x - 1) / blockDim.x;
+  const int b0 = threadIdx.x * per;
+  int64_t c = 0;
+  for (int b = b0; b < b0 + per && b < nbins; ++b) c += hist[b];
+  int64_t total;
+  int64_t acc = block_excl_scan<int64_t>(c, sw, total);
+  if (threadIdx.x == 0 && total < need) { *s_bin = nbins; *s_acc = (int)total; }
+  if (acc < need && acc + c >= need) {
+    for (int b = b0; b < b0 + per && b < nbins; ++b) {
+      if (acc + hist[b] >= need) { *s_bin = b; *s_acc = (int)acc; break; }
+      acc += hist[b];
+    }
+  }
+  __syncthreads();
 }
 
 // ------------------------------------------------------------- sampling
@@ -247,21 +303,6 @@ __global__ void k_lad_sample_exact(LadiesSampleArgs A) {
   }
 }
 
-// race keys: key = -log(u_v) / e_v^2 as float bits (non-negative floats
-// order like their bit patterns); u_v keyed by (batch key, v) in a domain
-// disjoint from the ITS draws (depth | 2^32).
-__global__ void k_lad_keys(LadiesSampleArgs A) {
-  const int64_t P = A.gpoff[A.gn];
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = last_le(A.gpoff, A.gn + 1, p);
-    const double u = uniform53(A.seed, A.epoch, A.depth | (1ULL << 32),
-                               (uint64_t)(A.batch_offset + A.g0 + j), (uint64_t)A.pv[p]);
-    const float e = (float)A.pe[p];
-    A.keys[p] = __float_as_uint((float)(-log1p(-u)) / (e * e));
-  }
-}
-
 // histogram of the top 12 key bits per batch (smem-privatised per chunk)
 constexpr int kHistChunk = 8192;
 __global__ void __launch_bounds__(256) k_lad_hist(LadiesSampleArgs A, uint32_t* __restrict__ hist) {
@@ -286,28 +327,28 @@ __global__ void __launch_bounds__(256) k_lad_hist(LadiesSampleArgs A, uint32_t* 
 }
 
 // per batch: take, boundary bin, count strictly below it
-__global__ void k_lad_boundary(LadiesSampleArgs A, const uint32_t* __restrict__ hist,
-                               int32_t* __restrict__ bound) {
+__global__ void __launch_bounds__(256) k_lad_boundary(LadiesSampleArgs A,
+                                                    const uint32_t* __restrict__ hist,
+                                                    int32_t* __restrict__ bound) {
+  __shared__ int64_t sw[33];
+  __shared__ int s_bin, s_acc;
   const int j = blockIdx.x;
   if (j >= A.gn) return;
   const int64_t i = A.g0 + j;
   const int64_t N = A.gpoff[j + 1] - A.gpoff[j];
   const int64_t take = N < A.s ? N : A.s;
+  if (take < N) {
+    block_find_bin(hist + (int64_t)j * kBins, kBins, take, sw, &s_bin, &s_acc);
+  } else if (threadIdx.x == 0) {
+    s_bin = kBins;  // everything selected
+    s_acc = 0;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
     A.take[i] = take;
     A.nsel[i] = 0;
-    int64_t acc = 0;
-    int b = 0;
-    if (take < N) {
-      for (; b < kBins; ++b) {
-        if (acc + hist[(int64_t)j * kBins + b] >= take) break;
-        acc += hist[(int64_t)j * kBins + b];
-      }
-    } else {
-      b = kBins;  // everything selected
-    }
-    bound[2 * j] = b;
-    bound[2 * j + 1] = (int32_t)acc;
+    bound[2 * j] = s_bin;
+    bound[2 * j + 1] = s_acc;
   }
 }
 
@@ -339,6 +380,7 @@ __global__ void __launch_bounds__(1024) k_lad_refine(LadiesSampleArgs A,
                                                    int32_t* __restrict__ overflow) {
   __shared__ uint32_t hist[kBins];
   __shared__ int32_t ties[kTies];
+  __shared__ int64_t sw[33];
   __shared__ int s_bin, s_acc, s_tie;
   const int shifts[2] = {8, 0};
   const int widths[2] = {12, 8};
@@ -360,17 +402,7 @@ __global__ void __launch_bounds__(1024) k_lad_refine(LadiesSampleArgs A,
         if ((kk & pmask) == prefix) atomicAdd(&hist[(kk >> sh) & bm], 1u);
       }
       __syncthreads();
-      if (threadIdx.x == 0) {
-        int64_t acc = 0;
-        uint32_t b = 0;
-        for (; b <= bm; ++b) {
-          if (acc + hist[b] >= need) break;
-          acc += hist[b];
-        }
-        s_bin = (int)b;
-        s_acc = (int)acc;
-      }
-      __syncthreads();
+      block_find_bin(hist, (int)bm + 1, need, sw, &s_bin, &s_acc);
       const uint32_t bin = (uint32_t)s_bin;
       for (int a = threadIdx.x; a < m; a += blockDim.x) {
         const uint32_t kk = A.keys[cj[a]];
@@ -712,13 +744,15 @@ int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t*
                                                       g->col, n, ws.cnt32, ws.nnz_b);
       GB_LAUNCH_CHECK("k_lad_count");
       prof_mark(st);
+      k_lad_compact_count<<<gcap(P.tiles, 1, 8 * sms), 256, 0, st>>>(ws.cnt32, words, n, g0,
+                                                                    ws.tile_off, ws.nnz_b);
       k_lad_gpoff<<<1, 1, 0, st>>>(ws.nnz_b, g0, gn, ws.gpoff);
-      k_lad_compact_count<<<gcap(P.tiles, 1, 8 * sms), 256, 0, st>>>(ws.cnt32, words, ws.tile_off);
       rc = device_exclusive_scan<int64_t>(d_tiles, P.tiles, TileF{ws.tile_off}, ws.tile_off,
                                           ws.scan_ws, st);
       if (rc) return rc;
-      k_lad_compact_write<<<gcap(P.tiles, 1, 8 * sms), 256, 0, st>>>(ws.cnt32, words, n,
-                                                                    ws.tile_off, ws.pv, ws.pe);
+      const RaceKey rk{seed, epoch, (uint64_t)(l + 1), batch_offset + g0};
+      k_lad_compact_write<<<gcap(P.tiles, 1, 8 * sms), 256, 0, st>>>(
+          ws.cnt32, words, n, ws.tile_off, ws.pv, ws.pe, exact ? nullptr : ws.keys, rk);
       GB_LAUNCH_CHECK("k_lad_compact");
       // ---- NORM + SAMPLE
       LadiesSampleArgs A{};
@@ -732,9 +766,8 @@ int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t*
       } else {
         GB_CUDA(cudaMemsetAsync(ws.hist, 0, sizeof(uint32_t) * gn * kBins, st));
         GB_CUDA(cudaMemsetAsync(ws.ncand, 0, sizeof(int32_t) * (gn + 1), st));
-        k_lad_keys<<<16 * sms, 256, 0, st>>>(A);
         k_lad_hist<<<4 * sms, 256, 0, st>>>(A, ws.hist);
-        k_lad_boundary<<<(int)gn, 32, 0, st>>>(A, ws.hist, ws.bound);
+        k_lad_boundary<<<(int)gn, 256, 0, st>>>(A, ws.hist, ws.bound);
         k_lad_filter<<<16 * sms, 256, 0, st>>>(A, ws.bound, ws.cand, ws.ncand);
         k_lad_refine<<<(int)gn, 1024, 0, st>>>(A, ws.bound, ws.cand, ws.ncand, ws.overflow);
         count_launches(5);
