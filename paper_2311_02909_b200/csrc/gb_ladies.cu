@@ -126,7 +126,11 @@ __global__ void __launch_bounds__(256) k_lad_compact_count(const uint32_t* __res
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int64_t w0 = t * (kCompTile / 2) + threadIdx.x * 8;
     int64_t c = 0;
-    int64_t jcur = (2 * w0) / n, ccur = 0, next = (jcur + 1) * n;
+    // per-thread counts of its (at most two when n >= 16) batches; a third
+    // segment (tiny n) goes straight to memory
+    const int64_t ja = (2 * w0) / n;
+    int64_t next = (ja + 1) * n, jcur = ja;
+    uint32_t ca = 0, cb = 0;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int64_t wi = w0 + j;
@@ -136,18 +140,27 @@ __global__ void __launch_bounds__(256) k_lad_compact_count(const uint32_t* __res
           if ((x >> (16 * h)) & 0xffffu) {
             const int64_t f = 2 * wi + h;
             if (f >= next) {
-              if (ccur) atomicAdd((unsigned long long*)(nnz_b + g0 + jcur), (unsigned long long)ccur);
               jcur = f / n;
               next = (jcur + 1) * n;
-              ccur = 0;
             }
-            ++ccur;
+            if (jcur == ja) ++ca;
+            else if (jcur == ja + 1) ++cb;
+            else atomicAdd((unsigned long long*)(nnz_b + g0 + jcur), 1ull);
             ++c;
           }
         }
       }
     }
-    if (ccur) atomicAdd((unsigned long long*)(nnz_b + g0 + jcur), (unsigned long long)ccur);
+    // warp-aggregate per batch id, one atomic per distinct batch per warp
+    const unsigned FULL = 0xffffffffu;
+    for (int part = 0; part < 2; ++part) {
+      const int64_t jj = ja + part;
+      const uint32_t cc = part ? cb : ca;
+      const unsigned grp = __match_any_sync(FULL, jj);
+      const uint32_t sum = __reduce_add_sync(grp, cc);
+      if (sum && (threadIdx.x & 31) == __ffs(grp) - 1)
+        atomicAdd((unsigned long long*)(nnz_b + g0 + jj), (unsigned long long)sum);
+    }
     int64_t total;
     block_excl_scan<int64_t>(c, sw, total);
     if (threadIdx.x == 0) tile_cnt[t] = total;
@@ -208,7 +221,6 @@ __global__ void __launch_bounds__(256) k_lad_compact_write(uint32_t* __restrict_
           while (v >= n) { ++jb; base += n; v -= n; }
           pv[o] = (int32_t)v;
           pe[o] = (int32_t)e;
-          if (keys) keys[o] = rk(jb, (int32_t)v, e);
           ++o;
         }
       }
@@ -300,6 +312,22 @@ __global__ void k_lad_sample_exact(LadiesSampleArgs A) {
       w[idx] = 0.0;
       dirty = idx;
     }
+  }
+}
+
+// race keys of the group's P entries, one thread per entry
+__global__ void __launch_bounds__(256) k_lad_keys(LadiesSampleArgs A, RaceKey rk) {
+  __shared__ int64_t sp[kSmaxSmem + 1];
+  const bool sm = A.gn + 1 <= kSmaxSmem;
+  if (sm)
+    for (int64_t j = threadIdx.x; j <= A.gn; j += blockDim.x) sp[j] = A.gpoff[j];
+  __syncthreads();
+  const int64_t* gp = sm ? sp : A.gpoff;
+  const int64_t P = gp[A.gn];
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = last_le(gp, A.gn + 1, p);
+    A.keys[p] = rk(j, A.pv[p], (uint32_t)A.pe[p]);
   }
 }
 
@@ -752,7 +780,7 @@ int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t*
       if (rc) return rc;
       const RaceKey rk{seed, epoch, (uint64_t)(l + 1), batch_offset + g0};
       k_lad_compact_write<<<gcap(P.tiles, 1, 8 * sms), 256, 0, st>>>(
-          ws.cnt32, words, n, ws.tile_off, ws.pv, ws.pe, exact ? nullptr : ws.keys, rk);
+          ws.cnt32, words, n, ws.tile_off, ws.pv, ws.pe, nullptr, rk);
       GB_LAUNCH_CHECK("k_lad_compact");
       // ---- NORM + SAMPLE
       LadiesSampleArgs A{};
@@ -766,6 +794,7 @@ int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t*
       } else {
         GB_CUDA(cudaMemsetAsync(ws.hist, 0, sizeof(uint32_t) * gn * kBins, st));
         GB_CUDA(cudaMemsetAsync(ws.ncand, 0, sizeof(int32_t) * (gn + 1), st));
+        k_lad_keys<<<16 * sms, 256, 0, st>>>(A, rk);
         k_lad_hist<<<4 * sms, 256, 0, st>>>(A, ws.hist);
         k_lad_boundary<<<(int)gn, 256, 0, st>>>(A, ws.hist, ws.bound);
         k_lad_filter<<<16 * sms, 256, 0, st>>>(A, ws.bound, ws.cand, ws.ncand);
