@@ -64,6 +64,25 @@ __device__ __forceinline__ double uniform53(uint64_t seed, uint64_t epoch, uint6
   return (double)(philox_word(seed, epoch, depth, row, t) >> 11) * 0x1.0p-53;
 }
 
+// Philox4x32-10 (Random123), used where 24-bit uniforms suffice (race keys)
+__device__ __forceinline__ void philox4x32_10(uint32_t& c0, uint32_t& c1, uint32_t& c2,
+                                              uint32_t& c3, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+  }
+}
+
 // ------------------------------------------------------------ warp utils
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 

@@ -179,9 +179,13 @@ struct RaceKey {
   uint64_t seed, epoch, depth;
   int64_t key0;  // batch_offset + g0
   __device__ __forceinline__ uint32_t operator()(int64_t j, int32_t v, uint32_t e) const {
-    const uint64_t w = philox_word(seed, epoch, depth | (1ULL << 32), (uint64_t)(key0 + j),
-                                   (uint64_t)v);
-    const float u = ((float)(w >> 40) + 0.5f) * 0x1.0p-24f;  // (0, 1)
+    // Philox4x32-10, counter (v, batch key lo/hi, depth), key (seed ^ epoch mix)
+    const uint64_t bk = (uint64_t)(key0 + j);
+    uint32_t c0 = (uint32_t)v, c1 = (uint32_t)bk, c2 = (uint32_t)(bk >> 32),
+             c3 = (uint32_t)depth | 0x80000000u;
+    philox4x32_10(c0, c1, c2, c3, (uint32_t)seed ^ (uint32_t)(seed >> 32),
+                  (uint32_t)epoch ^ (uint32_t)(epoch >> 32) ^ 0x6c616479u);
+    const float u = ((float)(c0 >> 8) + 0.5f) * 0x1.0p-24f;  // (0, 1)
     const float fe = (float)e;
     return __float_as_uint(-__logf(u) / (fe * fe));
   }
