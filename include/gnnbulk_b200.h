@@ -134,6 +134,45 @@ int gb_ladies_bulk(const gb_graph* g, int64_t k, const int64_t* d_qoff, const in
                    gb_ladies_layer_out* h_layers, int64_t* d_sizes, void* d_ws, size_t ws_bytes,
                    void* stream);
 
+/* ------------------------------------------------- generic operators
+ * Device CSR (int64 row offsets, int32 columns, f64 values) operators of
+ * the reference API.  d_m points to the row count on the device (so the
+ * calls can follow device-sized producers); d_scan_ws has
+ * gb_scan_workspace_bytes(m) bytes.
+ *   gb_spgemm_bound  d_ub[m+1] = exclusive prefix of per-row product bounds
+ *   gb_spgemm        C = A B (spgemm, sparse.py:233-251): scipy csr_matmat
+ *                    accumulation order, drop |x| < 1e-12; scratch: gkey /
+ *                    gval 4*ub_total, tmp 1*ub_total, cnt m+1; C capacity
+ *                    ub_total, nnz = d_c_ptr[m]
+ *   gb_csr_add       C = A + B (add, sparse.py:417-427); phase 0 counts and
+ *                    scans d_c_ptr, phase 1 writes
+ *   gb_norm_rows     norm_rows_sage (square=0) / norm_rows_ladies (1)
+ *                    (sparse.py:254-286), numpy add.reduce order; *d_err = 1
+ *                    negative value, 2 zero-mass row
+ *   gb_its_rows      its_sample_row for every row (sampler.py:157-207):
+ *                    picks[r*s + t] in draw order, keyed uniforms or
+ *                    d_inject[r*s + t]; *d_err = 1 non-positive weight */
+size_t gb_scan_workspace_bytes(int64_t max_n);
+int gb_spgemm_bound(int64_t m, const int64_t* d_a_ptr, const int32_t* d_a_col,
+                    const int64_t* d_b_ptr, const int64_t* d_m, int64_t* d_ub, int64_t* d_scan_ws,
+                    void* stream);
+int gb_spgemm(int64_t m, const int64_t* d_m, const int64_t* d_a_ptr, const int32_t* d_a_col,
+              const double* d_a_val, const int64_t* d_b_ptr, const int32_t* d_b_col,
+              const double* d_b_val, const int64_t* d_ub, int64_t ub_total, int32_t* d_gkey,
+              double* d_gval, int32_t* d_tmp_col, double* d_tmp_val, int64_t* d_cnt,
+              int64_t* d_c_ptr, int32_t* d_c_col, double* d_c_val, int64_t* d_scan_ws,
+              void* stream);
+int gb_csr_add(int64_t m, const int64_t* d_m, const int64_t* d_a_ptr, const int32_t* d_a_col,
+               const double* d_a_val, const int64_t* d_b_ptr, const int32_t* d_b_col,
+               const double* d_b_val, int64_t* d_cnt, int64_t* d_c_ptr, int32_t* d_c_col,
+               double* d_c_val, int64_t* d_scan_ws, int32_t phase, void* stream);
+int gb_norm_rows(int64_t m, const int64_t* d_ptr, const double* d_val, int32_t square,
+                 double* d_out, int32_t* d_err, void* stream);
+int gb_its_rows(int64_t m, const int64_t* d_ptr, const double* d_val, int32_t s,
+                const int64_t* d_keys, const double* d_inject, uint64_t seed, uint64_t epoch,
+                uint64_t depth, double* d_w, double* d_cdf, int32_t* d_picks, int32_t* d_take,
+                int32_t* d_err, void* stream);
+
 /* ----------------------------------------------------- synthetic inputs
  * R-MAT edge candidates first..first+count (Graph500 quadrant recursion over
  * `scale` levels with probabilities a, b, c; rejected candidates = -1) and

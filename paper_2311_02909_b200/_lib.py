@@ -59,6 +59,14 @@ SIGNATURES = {
     "gb_ladies_bulk": (ctypes.c_int, [_p, _i64, _p, _p, _i64, _i32, _p, _u64, _u64, _i64, _i32,
                                       ctypes.POINTER(LadiesLayerOut), _p, _p, ctypes.c_size_t,
                                       _p]),
+    "gb_scan_workspace_bytes": (ctypes.c_size_t, [_i64]),
+    "gb_spgemm_bound": (ctypes.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p]),
+    "gb_spgemm": (ctypes.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p, _p, _i64, _p, _p, _p, _p, _p,
+                                 _p, _p, _p, _p, _p]),
+    "gb_csr_add": (ctypes.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _i32, _p]),
+    "gb_norm_rows": (ctypes.c_int, [_i64, _p, _p, _i32, _p, _p, _p]),
+    "gb_its_rows": (ctypes.c_int, [_i64, _p, _p, _i32, _p, _p, _u64, _u64, _u64, _p, _p, _p, _p,
+                                   _p, _p]),
     "gb_rmat_edges": (ctypes.c_int, [_u64, _i32, _i64, _i64, _i64, ctypes.c_double,
                                      ctypes.c_double, ctypes.c_double, _p, _p, _p]),
     "gb_hash64": (ctypes.c_int, [_u64, _p, _i64, _p, _p]),

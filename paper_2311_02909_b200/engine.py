@@ -211,7 +211,50 @@ def ladies_epoch(G, cfg, batches, epoch, batch_offset, mode="auto"):
 
 
 def sample_epoch_generic(G, cfg, batches, epoch, batch_offset, prob_spgemm):
-    raise NotImplementedError("prob_spgemm hook path")
+    """sample_epoch_bulk with a user `prob_spgemm(Q) -> P` hook (reference
+    sampler.py:337-345, 360-379): P is materialised by the hook, then
+    normalised, sampled and extracted by the generic device operators."""
+    from . import ops
+    from . import sampler as smp
+
+    n = G.n
+    batch_ids = [batch_offset + i for i in range(len(batches))]
+    if cfg.kind is SamplerKind.SAGE:
+        Q = smp.sage_seed_matrix(batches, n)
+        rows_actual = [len(b) for b in batches]
+        row_vertices = [np.asarray(b).copy() for b in batches]
+    else:
+        Q = smp.ladies_seed_matrix(batches, n)
+        rows_actual = [1] * len(batches)
+        row_vertices = [np.sort(b) for b in batches]
+    layers = []
+    calls = 0
+    for depth in range(1, cfg.layers + 1):
+        fanout = cfg.fanouts[depth - 1]
+        P = prob_spgemm(Q)
+        calls += 1
+        P = ops.norm_rows_sage(P) if cfg.kind is SamplerKind.SAGE else ops.norm_rows_ladies(P)
+        keys = smp.global_row_keys(cfg, depth, batch_ids, rows_actual)
+        ordered = ops.sample_rows_ordered(P, fanout, epoch, depth, cfg.seed, keys)
+        frontier = ops.frontier_from_rows(ordered, P.n_cols)
+        row_starts = np.cumsum([0] + rows_actual)
+        if cfg.kind is SamplerKind.SAGE:
+            blocks, col_maps, new_rows = smp.sage_batch_blocks(frontier, row_starts)
+            layers.append(smp.build_sage_layer(depth, frontier, blocks, col_maps, row_vertices,
+                                               new_rows))
+            Q = ops.expand_row_extraction(frontier)
+            rows_actual = [len(v) for v in new_rows]
+            row_vertices = new_rows
+        else:
+            QR = ops.expand_row_extraction(Q)
+            AR = ops.spgemm(QR, G.host_adjacency())
+            ar, qc, sampled = smp.ladies_batch_blocks(Q, frontier, AR, n)
+            adjacency = smp.ladies_assemble(ar, qc)
+            layers.append(smp.build_ladies_layer(depth, frontier, adjacency, row_vertices,
+                                                 sampled))
+            Q = frontier
+            row_vertices = sampled
+    return SampledEpoch(cfg.kind, epoch, batches, layers, calls)
 
 
 class BulkSampler:

@@ -289,6 +289,62 @@ class SampledEpoch:
         return True
 
 
+def sage_batch_blocks(frontier, row_starts):
+    """Per-batch node-wise extraction pieces (reference sampler.py:390-406):
+    compacted blocks, global column ids, sampled vertices in row order."""
+    from . import ops
+
+    blocks, col_maps, new_rows = [], [], []
+    for i in range(len(row_starts) - 1):
+        block = frontier.row_slice(int(row_starts[i]), int(row_starts[i + 1]))
+        compacted, col_map = ops.compact_columns(block)
+        blocks.append(compacted)
+        col_maps.append(col_map)
+        new_rows.append(np.asarray(block.col_indices).copy())
+    return blocks, col_maps, new_rows
+
+
+def build_sage_layer(depth, frontier, blocks, col_maps, row_vertices, new_rows):
+    from . import ops
+
+    return LayerSample(depth, frontier, ops.block_diag(blocks),
+                       tuple(np.asarray(v).copy() for v in row_vertices), tuple(col_maps),
+                       tuple(new_rows))
+
+
+def ladies_assemble(ar_blocks, qc_blocks):
+    """Layer-wise extraction (reference sampler.py:420-434): shared columns
+    when every batch sampled the same count, else per-batch diagonal blocks."""
+    from . import ops
+
+    if not qc_blocks:
+        return SparseMatrix.empty(0, 0)
+    if len({b.n_cols for b in qc_blocks}) == 1:
+        return ops.spgemm(ops.block_diag(ar_blocks), ops.vstack(qc_blocks))
+    return ops.block_diag([ops.spgemm(a, q) for a, q in zip(ar_blocks, qc_blocks)])
+
+
+def ladies_batch_blocks(Q, frontier, AR, n):
+    """Per-batch layer-wise extraction pieces (reference sampler.py:437-451)."""
+    from . import ops
+
+    ar_starts = np.concatenate([[0], np.cumsum(Q.row_nnz())])
+    sampled, qc_blocks, ar_blocks = [], [], []
+    for i in range(Q.n_rows):
+        cols = frontier.row_cols(i)
+        sampled.append(np.asarray(cols).copy())
+        qc_blocks.append(ops.build_column_extraction(cols, n))
+        ar_blocks.append(AR.row_slice(int(ar_starts[i]), int(ar_starts[i + 1])))
+    return ar_blocks, qc_blocks, sampled
+
+
+def build_ladies_layer(depth, frontier, adjacency, row_vertices, sampled):
+    return LayerSample(depth, frontier, adjacency,
+                       tuple(np.asarray(v).copy() for v in row_vertices),
+                       tuple(np.asarray(s).copy() for s in sampled),
+                       tuple(np.asarray(s).copy() for s in sampled))
+
+
 def global_row_keys(cfg: SamplerConfig, depth, batch_ids, rows_per_batch_actual):
     """Global row ids of stacked per-batch rows (reference sampler.py:309-322)."""
     stride = cfg.rows_per_batch(depth)
@@ -325,3 +381,30 @@ def sample_epoch_bulk(G: Graph, cfg: SamplerConfig, batches, epoch=0, batch_offs
                                  mode="stream" if mode in ("auto", None) else mode)
     return engine.ladies_epoch(G, cfg, batches, epoch, batch_offset,
                                mode="auto" if mode in ("stream", None) else mode)
+
+
+# -- per-row samplers of the reference sampler.py, on the GPU (ops.py) ----------
+
+
+def its_sample_row(probabilities, s, rng):
+    from .ops import its_sample_row as _f
+
+    return _f(probabilities, s, rng)
+
+
+def sample_rows_ordered(P, s, epoch, layer, seed, row_keys=None):
+    from .ops import sample_rows_ordered as _f
+
+    return _f(P, s, epoch, layer, seed, row_keys)
+
+
+def frontier_from_rows(sampled_rows, n_cols):
+    from .ops import frontier_from_rows as _f
+
+    return _f(sampled_rows, n_cols)
+
+
+def sample_frontier(P, s, epoch, layer, seed, row_keys=None):
+    from .ops import sample_frontier as _f
+
+    return _f(P, s, epoch, layer, seed, row_keys)

@@ -271,3 +271,72 @@ class DeviceGraph:
                 _lib.load().gb_graph_destroy(self.handle)
         except Exception:
             pass
+
+
+# -- the reference sparse.py kernels, computed on the GPU (ops.py) --------------
+
+
+def spgemm(left, right):
+    from .ops import spgemm as _f
+
+    return _f(left, right)
+
+
+def add(left, right):
+    from .ops import add as _f
+
+    return _f(left, right)
+
+
+def norm_rows_sage(P):
+    from .ops import norm_rows_sage as _f
+
+    return _f(P)
+
+
+def norm_rows_ladies(P):
+    from .ops import norm_rows_ladies as _f
+
+    return _f(P)
+
+
+def vstack(blocks, n_cols=None):
+    from .ops import vstack as _f
+
+    return _f(blocks, n_cols)
+
+
+def block_diag(blocks):
+    from .ops import block_diag as _f
+
+    return _f(blocks)
+
+
+def compact_columns(M):
+    from .ops import compact_columns as _f
+
+    return _f(M)
+
+
+def expand_row_extraction(Q):
+    from .ops import expand_row_extraction as _f
+
+    return _f(Q)
+
+
+def column_window(M, lo, hi):
+    from .ops import column_window as _f
+
+    return _f(M, lo, hi)
+
+
+def rows_subset(M, rows):
+    from .ops import rows_subset as _f
+
+    return _f(M, rows)
+
+
+def build_column_extraction(sampled_cols, n):
+    from .ops import build_column_extraction as _f
+
+    return _f(sampled_cols, n)

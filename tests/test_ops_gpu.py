@@ -1,0 +1,140 @@
+"""Generic device operators vs the reference's own outputs (golden fixtures
+from scipy csr_matmat / numpy reduceat, tests/golden/spgemm.npz) and the
+reference's operator tests (pkg/tests/test_sparse.py, test_sampler.py)."""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _gb():
+    import paper_2311_02909_b200 as gb
+
+    return gb
+
+
+@pytest.fixture(scope="module")
+def spg():
+    return dict(np.load(os.path.join(GOLDEN, "spgemm.npz")))
+
+
+def _mat(z, p):
+    gb = _gb()
+    s = z[p + "_shape"]
+    return gb.SparseMatrix(s[0], s[1], z[p + "_ptr"], z[p + "_col"], z[p + "_val"])
+
+
+def test_spgemm_bit_exact_vs_scipy_golden(spg):
+    gb = _gb()
+    for i in range(int(spg["count"])):
+        C = gb.spgemm(_mat(spg, f"c{i}_A"), _mat(spg, f"c{i}_B"))
+        assert C.equals(_mat(spg, f"c{i}_C")), i
+
+
+def test_norm_rows_bit_exact_vs_numpy_golden(spg):
+    gb = _gb()
+    for i in range(int(spg["count"])):
+        P = _mat(spg, f"c{i}_P")
+        assert gb.norm_rows_sage(P).equals(_mat(spg, f"c{i}_NS")), i
+        assert gb.norm_rows_ladies(P).equals(_mat(spg, f"c{i}_NL")), i
+
+
+def test_norm_errors():
+    gb = _gb()
+    with pytest.raises(gb.ContractViolation):
+        gb.norm_rows_sage(gb.SparseMatrix.from_dense(np.array([[1.0, -1.0]])))
+
+
+def test_add_and_cancellation():
+    gb = _gb()
+    a = gb.SparseMatrix.from_dense(np.array([[1.0, 2.0], [0.0, 3.0]]))
+    b = gb.SparseMatrix.from_dense(np.array([[-1.0, 0.5], [4.0, 0.0]]))
+    c = gb.add(a, b)
+    assert c.to_dense().tolist() == [[0.0, 2.5], [4.0, 3.0]]
+    assert c.nnz == 3  # exact cancellation dropped (sparse.py:417-427)
+    with pytest.raises(gb.ContractViolation):
+        gb.add(a, gb.SparseMatrix.identity(3))
+
+
+def test_spgemm_dense_oracle_random():
+    gb = _gb()
+    rng = np.random.default_rng(5)
+    for _ in range(30):
+        m, k, n = (int(x) for x in rng.integers(1, 90, size=3))
+        A = np.where(rng.random((m, k)) < 0.2, rng.integers(1, 65, (m, k)) / 64.0, 0.0)
+        B = np.where(rng.random((k, n)) < 0.2, rng.integers(1, 65, (k, n)) / 64.0, 0.0)
+        C = gb.spgemm(gb.SparseMatrix.from_dense(A), gb.SparseMatrix.from_dense(B))
+        assert np.array_equal(C.to_dense(), A @ B)
+    # a wide row exercising the global-memory hash (bound > 1024 products)
+    A = np.ones((2, 300))
+    B = np.where(rng.random((300, 500)) < 0.05, 1.0, 0.0)
+    C = gb.spgemm(gb.SparseMatrix.from_dense(A), gb.SparseMatrix.from_dense(B))
+    assert np.array_equal(C.to_dense(), A @ B)
+
+
+def test_its_rows_match_reference_golden():
+    from paper_2311_02909_b200 import ops
+
+    z = dict(np.load(os.path.join(GOLDEN, "its_rows.npz")))
+
+    class ListRng:
+        def __init__(self, us):
+            self.us = list(us)
+
+        def random(self):
+            return self.us.pop(0)
+
+    for i in range(0, len(z["deg"]), 7):
+        w = z["w_cat"][z["w_off"][i]:z["w_off"][i + 1]]
+        want = z["picks"][i]
+        want = want[want >= 0]
+        got = ops.its_sample_row(w, int(z["fanout"][i]), ListRng(z["u"][i].tolist()))
+        assert np.array_equal(got, want), i
+
+
+def test_prob_spgemm_hook_matches_fused_path():
+    """sample_epoch_bulk with the reference's prob_spgemm hook (generic
+    device operators) equals the fused device path and the golden."""
+    gb = _gb()
+    for name in ("epoch_rmat10_sage.npz", "epoch_rmat10_ladies.npz", "epoch_fig_ladies.npz"):
+        g, want = O.load_golden(os.path.join(GOLDEN, name))
+        A = gb.SparseMatrix(g["n"], g["n"], g["rowptr"], g["col"], np.ones(len(g["col"])))
+        G = gb.Graph(A)
+        if g["kind"] == "sage":
+            cfg = gb.SamplerConfig.sage(g["layers_cfg"], g["batch_size"], tuple(g["fanouts"]),
+                                        bulk_count=len(g["batches"]), seed=g["seed"])
+        else:
+            cfg = gb.SamplerConfig.ladies(g["layers_cfg"], g["batch_size"], g["fanouts"][0],
+                                          bulk_count=len(g["batches"]), seed=g["seed"])
+        ep = gb.sample_epoch_bulk(G, cfg, g["batches"], epoch=g["epoch"],
+                                  batch_offset=g["batch_offset"],
+                                  prob_spgemm=lambda Q: gb.spgemm(Q, A))
+        assert O.compare_epochs(want, ep.to_arrays()) == [], name
+
+
+def test_structural_helpers():
+    gb = _gb()
+    M = gb.SparseMatrix.from_dense(np.array([[0, 1, 0, 2.0], [3, 0, 0, 0], [0, 0, 0, 4]]))
+    cm, kept = gb.compact_columns(M)
+    assert kept.tolist() == [0, 1, 3] and cm.shape == (3, 3)
+    assert gb.vstack([M, M]).n_rows == 6
+    bd = gb.block_diag([M, M])
+    assert bd.shape == (6, 8) and bd.row_cols(3).tolist() == [4]
+    e = gb.expand_row_extraction(M)
+    assert e.shape == (4, 4) and e.row_cols(3).tolist() == [3]
+    w = gb.column_window(M, 1, 4)
+    assert w.to_dense().tolist() == [[1, 0, 2], [0, 0, 0], [0, 0, 4]]
+    r = gb.rows_subset(M, [2, 0])
+    assert r.row_nnz().tolist() == [2, 0, 1]
+    qc = gb.build_column_extraction([4, 0], 6)
+    assert qc.shape == (6, 2) and qc.row_cols(0).tolist() == [1] and qc.row_cols(4).tolist() == [0]
+    with pytest.raises(gb.ContractViolation):
+        gb.build_column_extraction([1, 1], 6)
+    f = gb.frontier_from_rows([[3, 1], [], [2]], 5)
+    assert f.row_offsets.tolist() == [0, 2, 2, 3] and f.col_indices.tolist() == [1, 3, 2]
