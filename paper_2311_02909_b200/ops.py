@@ -293,7 +293,7 @@ def _stack(blocks, width, diag):
     base, cbase = 0, 0
     for b in blocks:
         ptrs.append(np.asarray(b.row_offsets[1:], np.int64) + base)
-        c = torch.as_tensor(np.asarray(b.col_indices, np.int64)).cuda()
+        c = torch.as_tensor(np.array(b.col_indices, np.int64)).cuda()
         cols.append(c + cbase if diag else c)
         vals.append(np.asarray(b.values))
         base += b.nnz
@@ -306,7 +306,7 @@ def _stack(blocks, width, diag):
 def compact_columns(M: SparseMatrix):
     """Drop empty columns; returns (compacted, column_map) (sparse.py:345-357)."""
     torch = _torch()
-    c = torch.as_tensor(np.asarray(M.col_indices, np.int64)).cuda()
+    c = torch.as_tensor(np.array(M.col_indices, np.int64)).cuda()
     kept = torch.unique(c)
     new = torch.searchsorted(kept, c)
     out = SparseMatrix(M.n_rows, int(kept.numel()), M.row_offsets, new.cpu().numpy(), M.values,
@@ -325,8 +325,8 @@ def column_window(M: SparseMatrix, lo: int, hi: int) -> SparseMatrix:
     torch = _torch()
     if not (0 <= lo <= hi <= M.n_cols):
         raise ContractViolation(f"column window [{lo}, {hi}) out of range")
-    c = torch.as_tensor(np.asarray(M.col_indices, np.int64)).cuda()
-    ptr = torch.as_tensor(np.asarray(M.row_offsets, np.int64)).cuda()
+    c = torch.as_tensor(np.array(M.col_indices, np.int64)).cuda()
+    ptr = torch.as_tensor(np.array(M.row_offsets, np.int64)).cuda()
     keep = (c >= lo) & (c < hi)
     rows = torch.repeat_interleave(torch.arange(M.n_rows, device="cuda"), ptr[1:] - ptr[:-1])
     counts = torch.bincount(rows[keep], minlength=M.n_rows)
@@ -343,7 +343,7 @@ def rows_subset(M: SparseMatrix, rows) -> SparseMatrix:
     r = torch.unique(torch.as_tensor(np.asarray(rows, np.int64)).cuda())
     if r.numel() and (int(r[0]) < 0 or int(r[-1]) >= M.n_rows):
         raise ContractViolation("row id out of range")
-    ptr = torch.as_tensor(np.asarray(M.row_offsets, np.int64)).cuda()
+    ptr = torch.as_tensor(np.array(M.row_offsets, np.int64)).cuda()
     deg = ptr[1:] - ptr[:-1]
     counts = torch.zeros(M.n_rows, dtype=torch.int64, device="cuda")
     counts[r] = deg[r]

@@ -125,7 +125,7 @@ def test_structural_helpers():
     assert kept.tolist() == [0, 1, 3] and cm.shape == (3, 3)
     assert gb.vstack([M, M]).n_rows == 6
     bd = gb.block_diag([M, M])
-    assert bd.shape == (6, 8) and bd.row_cols(3).tolist() == [4]
+    assert bd.shape == (6, 8) and bd.row_cols(3).tolist() == [5, 7]
     e = gb.expand_row_extraction(M)
     assert e.shape == (4, 4) and e.row_cols(3).tolist() == [3]
     w = gb.column_window(M, 1, 4)
