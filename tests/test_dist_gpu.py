@@ -91,7 +91,7 @@ def test_cost_model_band():
     from paper_2311_02909_b200.dist import (CommLedger, ProcessGrid, partition_block_rows,
                                             spgemm_15d_sparsity_aware)
 
-    n, k, b, d = 2**12, 4, 64, 8
+    n, k, b, d = 2**14, 4, 128, 8  # the reference's sizes (test_acceptance.py:204-206)
     G = d_regular(n, d, seed=d)
     rng = np.random.default_rng(d)
     q = gb.sage_seed_matrix(list(rng.permutation(n)[: k * b].reshape(k, b)), n)
