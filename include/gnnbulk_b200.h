@@ -98,6 +98,41 @@ int gb_sage_bulk(const gb_graph* g, int64_t k, const int64_t* d_bptr, const int3
                  gb_sage_layer_out* h_layers, int64_t* d_sizes, void* d_ws, size_t ws_bytes,
                  void* stream);
 
+/* ------------------------------------- SAGE per-layer pieces (1.5D mode)
+ * The distributed executor (one process per GPU) composes a layer from:
+ *   gb_take_scan            fptr = exclusive scan of min(deg[r], s), r < *d_R
+ *   gb_sage_layer_sample    NORM + SAMPLE of the rows with d_deg[r] > 0
+ *                           through the CSR (d_rowptr, d_col) addressed by
+ *                           d_rowv[r] (a local block of fetched A rows);
+ *                           picks land at d_fptr[r] in d_fcol; replay
+ *                           tables of `tables` (built on the global degrees)
+ *   gb_sage_layer_extract   EXTRACT of the completed frontier (after the
+ *                           grid-row exchange): acol, colv, eoff, coloff,
+ *                           sizes (R, F, U) — sage_batch_blocks/block_diag
+ *   gb_gather_rows          sparsity-aware row reply: rows ids[i] - row0 of a
+ *                           CSR block packed at out_off[i] (rows_subset,
+ *                           sparse.py:391-414 / dist.py:357-361)
+ *   gb_gather_features      fp32 feature rows for the all-to-allv of
+ *                           fetch_features (pipeline.py:78-120) */
+int gb_take_scan(int64_t r_cap, const int64_t* d_R, const int32_t* d_deg, int32_t s,
+                 int64_t* d_fptr, int64_t* d_scan_ws, void* stream);
+size_t gb_sage_layer_sample_workspace(int64_t r_cap, int64_t f_cap);
+int gb_sage_layer_sample(const gb_graph* tables, int64_t k, const int64_t* d_brow, int64_t r_cap,
+                         const int32_t* d_rowv, const int32_t* d_deg, const int64_t* d_fptr,
+                         const int64_t* d_rowptr, const int32_t* d_col, int32_t s, int64_t stride,
+                         int64_t batch_offset, uint64_t seed, uint64_t epoch, uint64_t depth,
+                         int32_t mode, int32_t* d_fcol, void* d_ws, size_t ws_bytes,
+                         void* stream);
+size_t gb_sage_layer_extract_workspace(int64_t n, int64_t k);
+int gb_sage_layer_extract(int64_t n, int64_t k, const int64_t* d_brow, const int64_t* d_fptr,
+                          const int32_t* d_fcol, int64_t f_cap, int32_t* d_acol, int32_t* d_colv,
+                          int64_t* d_eoff, int64_t* d_coloff, int64_t* d_sizes, void* d_ws,
+                          size_t ws_bytes, void* stream);
+int gb_gather_rows(int64_t m, const int32_t* d_ids, int64_t row0, const int64_t* d_rowptr,
+                   const int32_t* d_col, const int64_t* d_out_off, int32_t* d_out, void* stream);
+int gb_gather_features(int64_t m, const int32_t* d_ids, int64_t row0, const float* d_H, int64_t f,
+                       float* d_out, void* stream);
+
 /* -------------------------------------------------------- LADIES bulk
  * sample_epoch_bulk with SamplerConfig.kind == LADIES (sampler.py:325-387,
  * 420-462, 475-483).  Layer-1 rows: the batches, each sorted and distinct

@@ -167,6 +167,51 @@ int gb_sage_bulk(const gb_graph* g, int64_t k, const int64_t* d_bptr, const int3
                    batch_offset, mode, h_layers, d_sizes, d_ws, ws_bytes, (cudaStream_t)stream);
 }
 
+size_t gb_sage_layer_sample_workspace(int64_t r_cap, int64_t f_cap) {
+  return sage_layer_sample_ws(r_cap, f_cap);
+}
+
+int gb_sage_layer_sample(const gb_graph* tables, int64_t k, const int64_t* d_brow, int64_t r_cap,
+                         const int32_t* d_rowv, const int32_t* d_deg, const int64_t* d_fptr,
+                         const int64_t* d_rowptr, const int32_t* d_col, int32_t s, int64_t stride,
+                         int64_t batch_offset, uint64_t seed, uint64_t epoch, uint64_t depth,
+                         int32_t mode, int32_t* d_fcol, void* d_ws, size_t ws_bytes,
+                         void* stream) {
+  if (!tables || k < 0 || s < 1 || s > 32 || (mode != GB_SAGE_STREAM && mode != GB_SAGE_PFREE)) {
+    set_error("sage layer sample: bad arguments");
+    return GB_ERR_CONTRACT;
+  }
+  return sage_layer_sample(tables, k, d_brow, r_cap, d_rowv, d_deg, d_fptr, d_rowptr, d_col, s,
+                           stride, batch_offset, seed, epoch, depth, mode, d_fcol, d_ws, ws_bytes,
+                           (cudaStream_t)stream);
+}
+
+size_t gb_sage_layer_extract_workspace(int64_t n, int64_t k) { return sage_layer_extract_ws(n, k); }
+
+int gb_sage_layer_extract(int64_t n, int64_t k, const int64_t* d_brow, const int64_t* d_fptr,
+                          const int32_t* d_fcol, int64_t f_cap, int32_t* d_acol, int32_t* d_colv,
+                          int64_t* d_eoff, int64_t* d_coloff, int64_t* d_sizes, void* d_ws,
+                          size_t ws_bytes, void* stream) {
+  if (n < 0 || k < 0) { set_error("sage extract: bad arguments"); return GB_ERR_CONTRACT; }
+  return sage_layer_extract(n, k, d_brow, d_fptr, d_fcol, f_cap, d_acol, d_colv, d_eoff, d_coloff,
+                            d_sizes, d_ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int gb_take_scan(int64_t r_cap, const int64_t* d_R, const int32_t* d_deg, int32_t s,
+                 int64_t* d_fptr, int64_t* d_scan_ws, void* stream) {
+  return take_scan(r_cap, d_R, d_deg, s, d_fptr, d_scan_ws, (cudaStream_t)stream);
+}
+
+int gb_gather_rows(int64_t m, const int32_t* d_ids, int64_t row0, const int64_t* d_rowptr,
+                   const int32_t* d_col, const int64_t* d_out_off, int32_t* d_out, void* stream) {
+  return gather_rows(m, d_ids, row0, d_rowptr, d_col, d_out_off, d_out, (cudaStream_t)stream);
+}
+
+int gb_gather_features(int64_t m, const int32_t* d_ids, int64_t row0, const float* d_H, int64_t f,
+                       float* d_out, void* stream) {
+  return gather_features(m, d_ids, row0, d_H, f, d_out, (cudaStream_t)stream);
+}
+
 int gb_ladies_bulk_workspace(const gb_graph* g, int64_t k, int64_t q1_cap, int32_t layers,
                              const int64_t* h_fanouts, int32_t mode, size_t* h_bytes) {
   if (!g || !h_bytes || k < 0 || layers < 1 || !h_fanouts) {

@@ -36,6 +36,23 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
               uint64_t seed, uint64_t epoch, int64_t batch_offset, int32_t mode,
               gb_sage_layer_out* L, int64_t* d_sizes, void* d_ws, size_t ws_bytes,
               cudaStream_t st);
+size_t sage_layer_sample_ws(int64_t r_cap, int64_t f_cap);
+int sage_layer_sample(const Graph* tables, int64_t k, const int64_t* brow, int64_t r_cap,
+                      const int32_t* rowv, const int32_t* deg, const int64_t* fptr,
+                      const int64_t* rowptr, const int32_t* col, int32_t s, int64_t stride,
+                      int64_t batch_offset, uint64_t seed, uint64_t epoch, uint64_t depth,
+                      int32_t mode, int32_t* fcol, void* d_ws, size_t ws_bytes, cudaStream_t st);
+size_t sage_layer_extract_ws(int64_t n, int64_t k);
+int sage_layer_extract(int64_t n, int64_t k, const int64_t* brow, const int64_t* fptr,
+                       const int32_t* fcol, int64_t f_cap, int32_t* acol, int32_t* colv,
+                       int64_t* eoff, int64_t* coloff, int64_t* sizes, void* d_ws,
+                       size_t ws_bytes, cudaStream_t st);
+int take_scan(int64_t r_cap, const int64_t* R_ptr, const int32_t* deg, int32_t s, int64_t* fptr,
+              int64_t* scan_ws, cudaStream_t st);
+int gather_rows(int64_t m, const int32_t* ids, int64_t row0, const int64_t* rowptr,
+                const int32_t* col, const int64_t* out_off, int32_t* out, cudaStream_t st);
+int gather_features(int64_t m, const int32_t* ids, int64_t row0, const float* H, int64_t f,
+                    float* out, cudaStream_t st);
 int ladies_workspace(const Graph* g, int64_t k, int64_t q1_cap, int32_t layers,
                      const int64_t* fanouts, int32_t mode, size_t* bytes);
 int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t* d_qverts,

@@ -294,10 +294,10 @@ __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
       const int64_t rs = A.rowptr[A.rowv[r]];
       int32_t cv[kMaxFan];
       for (int t = 0; t < take; ++t) cv[t] = __ldg(A.col + rs + sorted[t]);
-      uint32_t* bm = A.bitmap + bb * A.nwords;
-      for (int t = 0; t < take; ++t) {
-        A.fcol[fp + t] = cv[t];
-        atomicOr(bm + (cv[t] >> 5), 1u << (cv[t] & 31));
+      for (int t = 0; t < take; ++t) A.fcol[fp + t] = cv[t];
+      if (A.bitmap) {
+        uint32_t* bm = A.bitmap + bb * A.nwords;
+        for (int t = 0; t < take; ++t) atomicOr(bm + (cv[t] >> 5), 1u << (cv[t] & 31));
       }
     } else {
       for (int t = 0; t < take; ++t) A.pidx[fp + t] = sorted[t];
@@ -400,7 +400,7 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k_sage_stream(SageArgs A,
       }
       if (have) {
         A.fcol[fp_i + lane] = c;
-        atomicOr(&A.bitmap[b_i * A.nwords + (c >> 5)], 1u << (c & 31));
+        if (A.bitmap) atomicOr(&A.bitmap[b_i * A.nwords + (c >> 5)], 1u << (c & 31));
       }
     }
   }
@@ -716,6 +716,173 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     count_launches(5);  // prep, sample, meta, rank, enumerate
     r_cap = f_cap;
   }
+  return GB_OK;
+}
+
+// ====================================== per-layer pieces (distributed executor)
+
+// eoff[b] = fptr[brow[b]]; then one bit per (batch, picked vertex)
+__global__ void k_sage_eoff(const int64_t* __restrict__ brow, int64_t k,
+                            const int64_t* __restrict__ fptr, int64_t* __restrict__ eoff) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b <= k;
+       b += (int64_t)gridDim.x * blockDim.x)
+    eoff[b] = fptr[brow[b]];
+}
+
+__global__ void k_sage_setbits(const int64_t* __restrict__ eoff, int64_t k,
+                               const int32_t* __restrict__ fcol, uint32_t* __restrict__ bitmap,
+                               int64_t nwords) {
+  const int64_t F = eoff[k];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < F;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = k;
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (eoff[mid] <= e) lo = mid; else hi = mid;
+    }
+    const int32_t v = fcol[e];
+    atomicOr(bitmap + lo * nwords + (v >> 5), 1u << (v & 31));
+  }
+}
+
+size_t sage_layer_sample_ws(int64_t r_cap, int64_t f_cap) {
+  return align_up(sizeof(int32_t) * (f_cap + 1)) + align_up(sizeof(int64_t) * (r_cap + 1)) +
+         align_up(sizeof(int64_t) * scan_workspace_elems<int64_t>(r_cap + 1));
+}
+
+// NORM + SAMPLE of the rows with deg[r] > 0 through the CSR (rowptr, col)
+// addressed by rowv[r]; picks land at fptr[r] (caller-computed).  No bitmap:
+// extraction runs separately once the frontier is complete.
+int sage_layer_sample(const Graph* tables, int64_t k, const int64_t* brow, int64_t r_cap,
+                      const int32_t* rowv, const int32_t* deg, const int64_t* fptr,
+                      const int64_t* rowptr, const int32_t* col, int32_t s, int64_t stride,
+                      int64_t batch_offset, uint64_t seed, uint64_t epoch, uint64_t depth,
+                      int32_t mode, int32_t* fcol, void* d_ws, size_t ws_bytes, cudaStream_t st) {
+  const int64_t f_cap = r_cap * s;
+  if (sage_layer_sample_ws(r_cap, f_cap) > ws_bytes) {
+    set_error("sage layer workspace too small");
+    return GB_ERR_CAPACITY;
+  }
+  char* p = (char*)d_ws;
+  int32_t* pidx = (int32_t*)p;
+  p += align_up(sizeof(int32_t) * (f_cap + 1));
+  int64_t* gstart = (int64_t*)p;
+  p += align_up(sizeof(int64_t) * (r_cap + 1));
+  int64_t* scan_ws = (int64_t*)p;
+  const int64_t* R_ptr = brow + k;
+  const bool stream = mode == GB_SAGE_STREAM;
+  if (stream) {
+    int rc = device_exclusive_scan<int64_t>(R_ptr, r_cap, DegF{deg}, gstart, scan_ws, st);
+    if (rc) return rc;
+  }
+  SageArgs A{};
+  A.rowptr = rowptr; A.col = col;
+  A.deg_slot = tables->deg_slot; A.run_j0 = tables->run_j0; A.run_s0 = tables->run_s0;
+  A.run_d = tables->run_d; A.run_n = tables->run_n;
+  A.rowv = rowv; A.deg = deg; A.fptr = fptr; A.gstart = gstart;
+  A.brow = brow; A.k = k; A.s = s; A.stride = stride; A.batch_offset = batch_offset;
+  A.seed = seed; A.epoch = epoch; A.depth = depth;
+  A.bitmap = nullptr; A.nwords = 0; A.fcol = fcol; A.pidx = pidx;
+  const int pick_grid = grid_for(r_cap, kPickThreads, 64 * kNumSMs);
+  if (stream) {
+    k_sage_pick<false><<<pick_grid, kPickThreads, 0, st>>>(A, R_ptr);
+    k_sage_stream<<<stream_grid(), kStreamThreads, 0, st>>>(A, R_ptr);
+    count_launches(2);
+  } else {
+    k_sage_pick<true><<<pick_grid, kPickThreads, 0, st>>>(A, R_ptr);
+    count_launches(1);
+  }
+  GB_LAUNCH_CHECK("sage_layer_sample");
+  return GB_OK;
+}
+
+size_t sage_layer_extract_ws(int64_t n, int64_t k) {
+  const int64_t W = k * ((n + 31) / 32);
+  return align_up(sizeof(uint32_t) * (W + 1)) + align_up(sizeof(int32_t) * (W + 1)) +
+         align_up(sizeof(int64_t) * scan_workspace_elems<int64_t>(W + 1)) + align_up(8);
+}
+
+// EXTRACT of a complete frontier (fptr, fcol): sage_batch_blocks +
+// block_diag (sampler.py:390-417): acol, colv, eoff, coloff, sizes (R, F, U)
+int sage_layer_extract(int64_t n, int64_t k, const int64_t* brow, const int64_t* fptr,
+                       const int32_t* fcol, int64_t f_cap, int32_t* acol, int32_t* colv,
+                       int64_t* eoff, int64_t* coloff, int64_t* sizes, void* d_ws,
+                       size_t ws_bytes, cudaStream_t st) {
+  if (sage_layer_extract_ws(n, k) > ws_bytes) {
+    set_error("sage extract workspace too small");
+    return GB_ERR_CAPACITY;
+  }
+  const int64_t nwords = (n + 31) / 32, W = k * nwords;
+  char* p = (char*)d_ws;
+  uint32_t* bitmap = (uint32_t*)p;
+  p += align_up(sizeof(uint32_t) * (W + 1));
+  int32_t* wpre = (int32_t*)p;
+  p += align_up(sizeof(int32_t) * (W + 1));
+  int64_t* scan_ws = (int64_t*)p;
+  p += align_up(sizeof(int64_t) * scan_workspace_elems<int64_t>(W + 1));
+  int64_t* d_W = (int64_t*)p;
+  GB_CUDA(cudaMemsetAsync(bitmap, 0, sizeof(uint32_t) * (W + 1), st));
+  k_set_i64<<<1, 1, 0, st>>>(d_W, W);
+  k_sage_eoff<<<grid_for(k + 1, 128, 64), 128, 0, st>>>(brow, k, fptr, eoff);
+  k_sage_setbits<<<grid_for(f_cap, 256, 16 * kNumSMs), 256, 0, st>>>(eoff, k, fcol, bitmap, nwords);
+  GB_LAUNCH_CHECK("k_sage_setbits");
+  int rc = device_exclusive_scan<int64_t>(d_W, W, PopF{bitmap}, wpre, scan_ws, st);
+  if (rc) return rc;
+  k_sage_layer_meta<<<grid_for(k + 1, 128, 64), 128, 0, st>>>(brow, k, fptr, wpre, nwords, eoff,
+                                                               coloff, sizes);
+  k_sage_rank<<<grid_for(f_cap, 256, 16 * kNumSMs), 256, 0, st>>>(sizes + 1, eoff, k, fcol,
+                                                                  bitmap, wpre, nwords, acol);
+  k_sage_enumerate<<<grid_for(W, 256, 16 * kNumSMs), 256, 0, st>>>(W, nwords, bitmap, wpre, colv);
+  GB_LAUNCH_CHECK("sage_layer_extract");
+  count_launches(6);
+  return GB_OK;
+}
+
+int take_scan(int64_t r_cap, const int64_t* R_ptr, const int32_t* deg, int32_t s, int64_t* fptr,
+              int64_t* scan_ws, cudaStream_t st) {
+  return device_exclusive_scan<int64_t>(R_ptr, r_cap, TakeF{deg, s}, fptr, scan_ws, st);
+}
+
+// gather rows `ids` of a CSR block (rows are ids[i] - row0) into a
+// contiguous buffer at out_off[i] (caller-computed from known degrees)
+__global__ void k_gather_rows(int64_t m, const int32_t* __restrict__ ids, int64_t row0,
+                              const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                              const int64_t* __restrict__ out_off, int32_t* __restrict__ out) {
+  const int lane = lane_id();
+  for (int64_t i = global_warp(); i < m; i += grid_warps()) {
+    const int64_t r = ids[i] - row0;
+    const int64_t a = rowptr[r], d = rowptr[r + 1] - a, o = out_off[i];
+    for (int64_t x = lane; x < d; x += 32) out[o + x] = col[a + x];
+  }
+}
+
+int gather_rows(int64_t m, const int32_t* ids, int64_t row0, const int64_t* rowptr,
+                const int32_t* col, const int64_t* out_off, int32_t* out, cudaStream_t st) {
+  if (m == 0) return GB_OK;
+  k_gather_rows<<<grid_for(m * 32, 256, 16 * kNumSMs), 256, 0, st>>>(m, ids, row0, rowptr, col,
+                                                                     out_off, out);
+  GB_LAUNCH_CHECK("k_gather_rows");
+  count_launches(1);
+  return GB_OK;
+}
+
+// dense feature rows: out[i, :] = H[ids[i] - row0, :] (fp32, f columns)
+__global__ void k_gather_feat(int64_t m, const int32_t* __restrict__ ids, int64_t row0,
+                              const float* __restrict__ H, int64_t f, float* __restrict__ out) {
+  const int lane = lane_id();
+  for (int64_t i = global_warp(); i < m; i += grid_warps()) {
+    const float* src = H + (ids[i] - row0) * f;
+    float* dst = out + i * f;
+    for (int64_t x = lane; x < f; x += 32) dst[x] = src[x];
+  }
+}
+
+int gather_features(int64_t m, const int32_t* ids, int64_t row0, const float* H, int64_t f,
+                    float* out, cudaStream_t st) {
+  if (m == 0) return GB_OK;
+  k_gather_feat<<<grid_for(m * 32, 256, 16 * kNumSMs), 256, 0, st>>>(m, ids, row0, H, f, out);
+  GB_LAUNCH_CHECK("k_gather_feat");
+  count_launches(1);
   return GB_OK;
 }
 

@@ -1,0 +1,320 @@
+"""B200 executor of the distributed samplers: one process per GPU.
+
+Replicated mode (cfg4, dist.py:417-429): rank r samples the contiguous batch
+range of group r with the fused device bulk sampler; no communication.
+
+1.5D partitioned mode (cfg5, Alg. 2, dist.py:308-378) for GraphSAGE:
+the grid is p/c rows x c columns (rank = i*c + j); A is split into p/c
+contiguous vertex-range block rows, block i held by the c ranks of grid row
+i; the batches are split into p/c groups, group i sampled by grid row i.
+Per layer, rank (i, j):
+
+  1. row fetch — sparsity aware: for stage q < p/c^2 it asks the owner of
+     block k = j*stages + q, rank (k, j), for exactly the distinct frontier
+     vertices of its group that fall in block k (NnzCols), and receives those
+     A rows (degrees are global metadata, so the reply is just the packed
+     column ids).  P2P send/recv inside the grid column (NCCL over NVLink).
+  2. sample-then-reduce — every frontier row is one-hot, so its P row lives
+     entirely in one block: rank (i, j) samples exactly the rows whose vertex
+     lies in its column's vertex range [V_j, V_{j+1}) from the fetched rows
+     (gb_sage_layer_sample), writing picks at their global frontier
+     positions; an all-reduce (sum) of the frontier inside grid row i
+     assembles the complete frontier.  This replaces the reference's P
+     all-reduce (37-66x larger) by s ids per row.
+  3. extraction on the complete frontier (gb_sage_layer_extract), identical
+     on the c replicas.
+
+The result of grid row i equals the serial bulk of group i (same global
+row keys), so the concatenation over grid rows equals the serial epoch.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from .dist import ProcessGrid, _bounds
+from .errors import ContractViolation
+from .sampler import LayerSample, SampledEpoch, SamplerKind
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def exchange(sends, recv_sizes, group_ranks, dtype, device):
+    """Point-to-point exchange inside a group: sends {peer: tensor},
+    recv_sizes {peer: count}; returns {peer: tensor}.  Grouped isend/irecv
+    (NCCL group on GPUs, gloo on CPU for the host-logic tests)."""
+    import torch.distributed as dist
+
+    torch = _torch()
+    ops, out = [], {}
+    me = dist.get_rank()
+    for peer, n in recv_sizes.items():
+        if peer == me:
+            continue
+        buf = torch.empty(int(n), dtype=dtype, device=device)
+        out[peer] = buf
+        if n:
+            ops.append(dist.P2POp(dist.irecv, buf, peer))
+    for peer, t in sends.items():
+        if peer == me:
+            out[peer] = t
+            continue
+        if t.numel():
+            ops.append(dist.P2POp(dist.isend, t.contiguous(), peer))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    return out
+
+
+def exchange_counts(sends, group_ranks, device):
+    """Every member learns how many elements each peer sends it."""
+    import torch.distributed as dist
+
+    torch = _torch()
+    me = dist.get_rank()
+    cnt_out = {p: torch.tensor([int(sends.get(p, torch.empty(0)).numel())], dtype=torch.int64,
+                               device=device) for p in group_ranks}
+    got = exchange(cnt_out, {p: 1 for p in group_ranks}, group_ranks, torch.int64, device)
+    return {p: int(got[p].item()) if p != me else int(cnt_out[me].item()) for p in group_ranks}
+
+
+class Sage15D:
+    """1.5D partitioned GraphSAGE bulk sampler over real processes.
+
+    full: a DeviceGraph of the whole graph on this GPU — used once to build
+    the global degree array and replay tables and to cut out this rank's
+    block row (a deployment would load only the block and all-gather the
+    degrees; the sampling data path below touches only the local block and
+    fetched rows).
+    """
+
+    def __init__(self, full, grid: ProcessGrid, fanouts, batch_size, mode="pfree",
+                 ledger=None):
+        import torch.distributed as dist
+
+        torch = _torch()
+        if not dist.is_initialized() or dist.get_world_size() != grid.p:
+            raise ContractViolation("Sage15D needs torch.distributed with world_size == grid.p")
+        self.grid, self.fanouts, self.b = grid, tuple(int(s) for s in fanouts), int(batch_size)
+        self.mode, self.ledger = mode, ledger
+        self.rank = dist.get_rank()
+        self.i, self.j = grid.coords(self.rank)
+        self.n = full.n
+        self.tables = full  # replay tables built on the global degree set
+        self.gdeg = (full.rowptr[1:] - full.rowptr[:-1]).to(torch.int32)
+        self.bounds = _bounds(self.n, grid.rows)
+        lo, hi = int(self.bounds[self.i]), int(self.bounds[self.i + 1])
+        a0, a1 = int(full.rowptr[lo].item()), int(full.rowptr[hi].item())
+        self.row0 = lo
+        self.brp = (full.rowptr[lo:hi + 1] - a0).contiguous()
+        self.bcol = full.col[a0:a1].clone()
+        st = grid.stages
+        self.V0 = int(self.bounds[self.j * st])
+        self.V1 = int(self.bounds[(self.j + 1) * st])
+        self.row_groups = [dist.new_group(grid.row_group(r)) for r in range(grid.rows)]
+        self.col_ranks = grid.col_group(self.j)
+        self.row_ranks = grid.row_group(self.i)
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+        self.stats = {"fetch_ids": 0, "fetch_words": 0, "reduce_words": 0}
+
+    # -- step 1: sparsity-aware row fetch ------------------------------------------
+    def fetch_rows(self, U):
+        """A rows of the sorted distinct vertices U (all in this column's
+        range) as a local CSR (rowptr over U, cols)."""
+        torch = _torch()
+        grid, st, L = self.grid, self.grid.stages, _lib.lib()
+        replies = []
+        for q in range(st):
+            kblk = self.j * st + q
+            owner = grid.rank(kblk, self.j)
+            lo, hi = int(self.bounds[kblk]), int(self.bounds[kblk + 1])
+            ids = U[(U >= lo) & (U < hi)].contiguous()
+            sends = {owner: ids}
+            counts = exchange_counts(sends, self.col_ranks, self.dev)
+            reqs = exchange(sends, {p: counts[p] for p in self.col_ranks if self.rank == owner or
+                                    p == self.rank}, self.col_ranks, torch.int32, self.dev)
+            # owner: serve every request of this stage from the local block
+            out = {}
+            if self.rank == owner:
+                for p in self.col_ranks:
+                    rid = reqs.get(p)
+                    if rid is None or rid.numel() == 0:
+                        continue
+                    d = self.gdeg[rid.long()].long()
+                    off = torch.zeros(rid.numel() + 1, dtype=torch.int64, device=self.dev)
+                    off[1:] = torch.cumsum(d, 0)
+                    buf = torch.empty(max(int(off[-1].item()), 1), dtype=torch.int32,
+                                      device=self.dev)
+                    _lib.check(L.gb_gather_rows(rid.numel(), _lib.ptr(rid), self.row0,
+                                                _lib.ptr(self.brp), _lib.ptr(self.bcol),
+                                                _lib.ptr(off), _lib.ptr(buf), _lib.stream_ptr()),
+                               "gb_gather_rows")
+                    out[p] = buf[: int(off[-1].item())]
+                    if self.ledger is not None and p != self.rank and out[p].numel():
+                        self.ledger.charge(self.rank, "row-data", 1, out[p].numel())
+            if self.ledger is not None and owner != self.rank and ids.numel():
+                self.ledger.charge(self.rank, "gather-cols", 1, ids.numel())
+            want = int(self.gdeg[ids.long()].long().sum().item()) if ids.numel() else 0
+            self.stats["fetch_ids"] += ids.numel() if owner != self.rank else 0
+            self.stats["fetch_words"] += want if owner != self.rank else 0
+            got = exchange(out, {owner: want}, self.col_ranks, torch.int32, self.dev)
+            replies.append(got.get(owner, torch.empty(0, dtype=torch.int32, device=self.dev))
+                           if want else torch.empty(0, dtype=torch.int32, device=self.dev))
+        d = self.gdeg[U.long()].long()
+        lrowptr = torch.zeros(U.numel() + 1, dtype=torch.int64, device=self.dev)
+        lrowptr[1:] = torch.cumsum(d, 0)
+        nnz = int(lrowptr[-1].item())
+        lcol = torch.zeros(nnz + _lib.GB_COL_PAD, dtype=torch.int32, device=self.dev)
+        if nnz:
+            lcol[:nnz] = torch.cat(replies)
+        return lrowptr, lcol
+
+    # -- one bulk --------------------------------------------------------------------------
+    def sample(self, group_batches, epoch, batch_offset, seed):
+        """Sample this grid row's group; returns (device layer dicts, sizes)."""
+        import torch.distributed as dist
+
+        torch = _torch()
+        L = _lib.lib()
+        k = len(group_batches)
+        off = np.zeros(k + 1, np.int64)
+        off[1:] = np.cumsum([len(x) for x in group_batches])
+        brow = torch.as_tensor(off).to(self.dev)
+        rowv = torch.as_tensor(np.concatenate(group_batches).astype(np.int32) if k and off[-1]
+                               else np.zeros(1, np.int32)).to(self.dev)
+        R = int(off[-1])
+        stride = self.b
+        layers = []
+        ws_scan = torch.empty(max(L.gb_scan_workspace_bytes(1 + R * int(np.prod(self.fanouts)))
+                                  // 8, 1), dtype=torch.int64, device=self.dev)
+        for l, s in enumerate(self.fanouts):
+            if l:
+                stride *= self.fanouts[l - 1]
+            rv = rowv[:R]
+            deg = self.gdeg[rv.long()] if R else torch.zeros(0, dtype=torch.int32,
+                                                             device=self.dev)
+            fptr = torch.empty(R + 1, dtype=torch.int64, device=self.dev)
+            dR = torch.tensor([R], dtype=torch.int64, device=self.dev)
+            _lib.check(L.gb_take_scan(max(R, 1), _lib.ptr(dR), _lib.ptr(deg if R else None), s,
+                                      _lib.ptr(fptr), _lib.ptr(ws_scan), _lib.stream_ptr()),
+                       "gb_take_scan")
+            F = int(fptr[R].item())
+            mine = (rv >= self.V0) & (rv < self.V1)
+            U = torch.unique(rv[mine])
+            lrowptr, lcol = self.fetch_rows(U)
+            lrow = torch.searchsorted(U, rv).to(torch.int32)
+            deg_mine = torch.where(mine, deg, torch.zeros_like(deg)).contiguous()
+            fcol = torch.zeros(max(F, 1), dtype=torch.int32, device=self.dev)
+            ws = torch.empty(max(L.gb_sage_layer_sample_workspace(max(R, 1), max(R, 1) * s), 1),
+                             dtype=torch.uint8, device=self.dev)
+            mode = _lib.GB_SAGE_STREAM if self.mode == "stream" else _lib.GB_SAGE_PFREE
+            if R:
+                _lib.check(L.gb_sage_layer_sample(
+                    self.tables.handle, k, _lib.ptr(brow), R, _lib.ptr(lrow), _lib.ptr(deg_mine),
+                    _lib.ptr(fptr), _lib.ptr(lrowptr), _lib.ptr(lcol), s, stride, batch_offset,
+                    seed, epoch, l + 1, mode, _lib.ptr(fcol), _lib.ptr(ws), ws.numel(),
+                    _lib.stream_ptr()), "gb_sage_layer_sample")
+            # step 2: sample-then-reduce inside the grid row
+            if self.grid.c > 1 and F:
+                dist.all_reduce(fcol[:F], op=dist.ReduceOp.SUM,
+                                group=self.row_groups[self.i])
+                self.stats["reduce_words"] += F
+                if self.ledger is not None:
+                    self.ledger.charge(self.rank, "all-reduce", 1, F)
+            # step 3: extraction on the complete frontier
+            acol = torch.empty(max(F, 1), dtype=torch.int32, device=self.dev)
+            colv = torch.empty(max(F, 1), dtype=torch.int32, device=self.dev)
+            eoff = torch.empty(k + 1, dtype=torch.int64, device=self.dev)
+            coloff = torch.empty(k + 1, dtype=torch.int64, device=self.dev)
+            sizes = torch.zeros(3, dtype=torch.int64, device=self.dev)
+            xws = torch.empty(max(L.gb_sage_layer_extract_workspace(self.n, k), 1),
+                              dtype=torch.uint8, device=self.dev)
+            _lib.check(L.gb_sage_layer_extract(self.n, k, _lib.ptr(brow), _lib.ptr(fptr),
+                                               _lib.ptr(fcol), max(F, 1), _lib.ptr(acol),
+                                               _lib.ptr(colv), _lib.ptr(eoff), _lib.ptr(coloff),
+                                               _lib.ptr(sizes), _lib.ptr(xws), xws.numel(),
+                                               _lib.stream_ptr()), "gb_sage_layer_extract")
+            U_tot = int(sizes[2].item())
+            layers.append({
+                "frontier_shape": (R, self.n), "frontier_ptr": fptr, "frontier_col": fcol[:F],
+                "adj_shape": (R, U_tot), "adj_ptr": fptr, "adj_col": acol[:F],
+                "rowv_off": brow, "rowv_cat": rowv[:R], "colv_off": coloff,
+                "colv_cat": colv[:U_tot], "sampv_off": eoff, "sampv_cat": fcol[:F],
+            })
+            rowv, brow, R = fcol, eoff, F
+        return layers
+
+
+def sage_epoch_15d(sampler: Sage15D, cfg, batches, epoch=0, batch_offset=0, gather=True):
+    """Distributed SAGE epoch: grid row i samples group i; with gather=True
+    every rank returns the full epoch (groups gathered over the grid column
+    and concatenated — identical to the serial epoch)."""
+    import torch.distributed as dist
+
+    from .dist import merge_epochs
+
+    grid = sampler.grid
+    b = _bounds(len(batches), grid.rows)
+    g0, g1 = int(b[sampler.i]), int(b[sampler.i + 1])
+    mine = sampler.sample([np.asarray(x) for x in batches[g0:g1]], epoch, batch_offset + g0,
+                          cfg.seed)
+    if not gather:
+        return mine
+    local = [{k: (v if isinstance(v, tuple) else v.cpu().numpy()) for k, v in lay.items()}
+             for lay in mine]
+    allp = [None] * grid.p
+    dist.all_gather_object(allp, local)
+    parts = []
+    for i in range(grid.rows):
+        lay = allp[grid.rank(i, 0)]
+        gi = [np.asarray(x) for x in batches[int(b[i]):int(b[i + 1])]]
+        parts.append(SampledEpoch(SamplerKind.SAGE, epoch, gi,
+                                  [LayerSample(d + 1, device=x, n=sampler.n)
+                                   for d, x in enumerate(lay)], cfg.layers))
+    return merge_epochs(SamplerKind.SAGE, epoch, batches, parts, cfg.layers)
+
+
+def fetch_features_nccl(vertices, H_block, row_starts, grid: ProcessGrid, group_col_ranks):
+    """fetch_features (pipeline.py:78-120) over real processes: every rank
+    requests the fp32 feature rows of `vertices` from the replicas in its own
+    grid column (block row owner (r, j)), served by gb_gather_features and
+    delivered by a grouped send/recv all-to-allv.  Returns rows in request
+    order (duplicates fetched per occurrence)."""
+    import torch.distributed as dist
+
+    torch = _torch()
+    me = dist.get_rank()
+    i, j = grid.coords(me)
+    dev = H_block.device
+    f = H_block.shape[1]
+    v = torch.as_tensor(np.asarray(vertices, np.int64)).to(dev)
+    rs = torch.as_tensor(np.asarray(row_starts, np.int64)).to(dev)
+    owner_row = torch.searchsorted(rs, v, right=True) - 1
+    sends, slots = {}, {}
+    for r in range(grid.rows):
+        sel = torch.nonzero(owner_row == r).flatten()
+        sends[grid.rank(r, j)] = v[sel].to(torch.int32)
+        slots[grid.rank(r, j)] = sel
+    counts = exchange_counts(sends, group_col_ranks, dev)
+    reqs = exchange(sends, counts, group_col_ranks, torch.int32, dev)
+    L = _lib.lib()
+    replies = {}
+    for p, ids in reqs.items():
+        buf = torch.empty((ids.numel(), f), dtype=torch.float32, device=dev)
+        _lib.check(L.gb_gather_features(ids.numel(), _lib.ptr(ids), int(row_starts[i]),
+                                        _lib.ptr(H_block), f, _lib.ptr(buf), _lib.stream_ptr()),
+                   "gb_gather_features")
+        replies[p] = buf.flatten()
+    want = {p: sends[p].numel() * f for p in group_col_ranks}
+    got = exchange(replies, want, group_col_ranks, torch.float32, dev)
+    out = torch.empty((v.numel(), f), dtype=torch.float32, device=dev)
+    for p, sel in slots.items():
+        if sel.numel():
+            out[sel] = got[p].view(-1, f)
+    return out

@@ -1,0 +1,72 @@
+"""Multi-GPU parity check of the 1.5D executor (run under torchrun, one
+process per GPU; not collected by pytest):
+
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
+        tests/dist_exec_check.py
+
+For every valid grid (p = N, c with c | p, c^2 <= p, c^2 | p) and both SAGE
+kernel modes: the gathered distributed epoch must equal the serial bulk
+epoch bit for bit; fetch_features over NCCL must equal direct indexing."""
+
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
+    dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
+    import paper_2311_02909_b200 as gb
+    from paper_2311_02909_b200 import graphgen
+    from paper_2311_02909_b200.dist import CommLedger, ProcessGrid, _bounds
+    from paper_2311_02909_b200.dist_exec import Sage15D, fetch_features_nccl, sage_epoch_15d
+
+    dg = graphgen.rmat_device_graph(1 << 14, 200_000, symmetric=True, seed=3)
+    G = gb.Graph.from_device(dg)
+    rng = np.random.default_rng(0)
+    batches = [rng.permutation(dg.n)[:64] for _ in range(8)]
+    cfg = gb.SamplerConfig.sage(3, 64, (15, 10, 5), bulk_count=8, seed=4)
+    serial = gb.sample_epoch_bulk(G, cfg, batches, epoch=1, batch_offset=5)
+    ok = True
+    grids = [(world, c) for c in (1, 2) if world % c == 0 and c * c <= world and world % (c * c) == 0]
+    for p, c in grids:
+        grid = ProcessGrid(p, c)
+        for mode in ("pfree", "stream"):
+            led = CommLedger(p)
+            s = Sage15D(dg, grid, cfg.fanouts, cfg.batch_size, mode=mode, ledger=led)
+            ep = sage_epoch_15d(s, cfg, batches, epoch=1, batch_offset=5)
+            same = serial.equals(ep)
+            ok &= same
+            if rank == 0:
+                print(f"grid ({p},{c}) {mode}: {'PASS' if same else 'FAIL'} stats={s.stats}",
+                      flush=True)
+        # features: replicas of the block rows in every grid column
+        f = 16
+        H = torch.arange(dg.n * f, dtype=torch.float32, device="cuda").view(dg.n, f)
+        rs = _bounds(dg.n, grid.rows)
+        i, j = grid.coords(rank)
+        Hb = H[int(rs[i]):int(rs[i + 1])].contiguous()
+        want = rng.integers(0, dg.n, size=500)
+        got = fetch_features_nccl(want, Hb, rs, grid, grid.col_group(j))
+        same = bool(torch.equal(got, H[torch.as_tensor(want).cuda()]))
+        ok &= same
+        if rank == 0:
+            print(f"grid ({p},{c}) fetch_features: {'PASS' if same else 'FAIL'}", flush=True)
+    t = torch.tensor([1 if ok else 0], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    if rank == 0:
+        print("ALL PASS" if int(t.item()) else "SOME FAILED", flush=True)
+    dist.destroy_process_group()
+    sys.exit(0 if int(t.item()) else 1)
+
+
+if __name__ == "__main__":
+    main()
