@@ -51,6 +51,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-pfree", action="store_true")
     p.add_argument("--no-ladies", action="store_true")
+    p.add_argument("--dist", default="replicated", choices=["replicated", "15d"],
+                   help="multi-GPU mode: replicated graph (cfg4) or 1.5D partitioned (cfg5)")
+    p.add_argument("--c", type=int, default=2, help="1.5D replication factor")
     return p.parse_args()
 
 
@@ -486,6 +489,61 @@ def run_ours(args, rank, world, local_rank):
         print(json.dumps(line), flush=True)
 
 
+def run_15d(args, rank, world, local_rank):
+    """cfg5: GraphSAGE (15,10,5) with the graph 1.5D-partitioned over a
+    (p/c) x c grid: sparsity-aware row fetch inside grid columns (NCCL p2p),
+    sample-then-reduce inside grid rows, k=64 minibatches per grid row."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2311_02909_b200 import graphgen
+    from paper_2311_02909_b200.dist import ProcessGrid
+    from paper_2311_02909_b200.dist_exec import Sage15D
+
+    c = args.c if (world % args.c == 0 and args.c ** 2 <= world and
+                   world % (args.c ** 2) == 0) else 1
+    grid = ProcessGrid(world, c)
+    torch.cuda.set_device(local_rank)
+    n, m, sym = graphgen.SHAPES[args.workload]
+    dg = graphgen.rmat_device_graph(n, m, symmetric=sym, seed=0)
+    k = args.k or default_k(args.workload)
+    allb = make_batches_for(n, k * grid.rows)
+    s = Sage15D(dg, grid, FANOUTS, BATCH, mode=args.mode)
+    i = s.i
+    mine = [np.asarray(x) for x in allb[i * k:(i + 1) * k]]
+    for _ in range(max(args.warmup, 3)):
+        s.sample(mine, 0, i * k, 0)
+    torch.cuda.synchronize()
+    dist.barrier()
+    times = []
+    for _ in range(args.steps):
+        dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        s.sample(mine, 0, i * k, 0)
+        b.record()
+        torch.cuda.synchronize()
+        times.append(a.elapsed_time(b))
+    T = float(np.sum(times))
+    t = torch.tensor([T], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    T = float(t.item())
+    value = k * grid.rows * args.steps / (T / 1e3)
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC + " [1.5D partitioned graph]", "value": value, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": T / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.workload}-shape R-MAT, GraphSAGE (15,10,5), "
+                                   f"b=1024, k={k} per grid row",
+                       "parallelism": f"1.5D grid {grid.rows}x{grid.c} (p={world}, c={grid.c})",
+                       "mode": args.mode},
+            "traffic_rank0": {k2: int(v) for k2, v in s.stats.items()},
+        }), flush=True)
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -500,6 +558,8 @@ def main():
     try:
         if args.impl == "reference":
             run_reference(args, rank, world)
+        elif args.dist == "15d":
+            run_15d(args, rank, world, local_rank)
         else:
             run_ours(args, rank, world, local_rank)
     finally:
