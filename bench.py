@@ -410,6 +410,12 @@ def run_ours(args, rank, world, local_rank):
     pick_avg = kern_ms.mean(axis=0)[:, 0]
     achieved = sum(kb) / (kern_avg.sum() / 1e3) / 1e9
     bulk_bytes = sage_bytes(st)
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath) and args.workload == "products" and k == 64:
+        tk = json.load(open(tpath)).get(dom_kernel := ("k_sage_stream" if args.mode == "stream"
+                                                       else "k_sage_pick<true>"))
+        traffic = tk["bulk_bytes"] if tk else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
@@ -429,7 +435,10 @@ def run_ours(args, rank, world, local_rank):
         "bulk_gbs": bulk_bytes / (total_ms / args.steps / 1e3) / 1e9,
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": None,
+            "frac": achieved / peak, "traffic": traffic,
+            "traffic_note": "dram__bytes_read+write summed over the 3 layer launches of one bulk "
+                            "(ncu --set full, profiles/ncu_traffic.json); achieved/per_layer_bytes "
+                            "aggregate the same 3 launches",
             "kernel": "k_sage_stream" if args.mode == "stream" else "k_sage_pick<true>",
             "pick_kernel_ms": [round(x, 4) for x in pick_avg.tolist()],
             "per_layer_ms": [round(x, 4) for x in kern_avg.tolist()],

@@ -282,6 +282,7 @@ class BulkSampler:
         self.d_off = torch.empty(k + 1, dtype=torch.int64, device="cuda")
         self.d_cat = torch.empty(max(r1, 1), dtype=torch.int32, device="cuda")
         self.h_sizes = torch.empty(3 * cfg.layers, dtype=torch.int64, pin_memory=True)
+        self._pinned = {}
         self.h2d_bytes = 0
         self.d2h_bytes = 0
 
@@ -309,21 +310,39 @@ class BulkSampler:
         layers = self.bulk.layers(self.d_off, self.d_cat, sizes)
         self.d2h_bytes = 8 * sizes.size
         if to_host:
-            host_layers = []
-            pend = []
+            # one D2H copy per distinct device buffer into persistent pinned
+            # staging (frontier/adjacency/sampled arrays alias each other and
+            # the next layer's rows); layer-1 rows are the caller's input.
+            # Host arrays stay valid until the next sample() call.
+            host = {}
+            for layer in layers:
+                for key, v in layer.device.items():
+                    if isinstance(v, tuple):
+                        continue
+                    ident = (v.data_ptr(), v.numel())
+                    if ident in host or v.data_ptr() in (self.d_off.data_ptr(),
+                                                         self.d_cat.data_ptr()):
+                        continue
+                    buf = self._pinned.get(v.data_ptr())
+                    if buf is None or buf.numel() < v.numel():
+                        buf = torch.empty(max(v.numel(), 1), dtype=v.dtype, pin_memory=True)
+                        self._pinned[v.data_ptr()] = buf
+                    buf[: v.numel()].copy_(v, non_blocking=True)
+                    self.d2h_bytes += v.numel() * v.element_size()
+                    host[ident] = buf[: v.numel()]
+            torch.cuda.current_stream().synchronize()
+            out_layers = []
             for layer in layers:
                 h = {}
                 for key, v in layer.device.items():
                     if isinstance(v, tuple):
                         h[key] = v
-                        continue
-                    buf = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
-                    buf.copy_(v, non_blocking=True)
-                    self.d2h_bytes += v.numel() * v.element_size()
-                    pend.append((h, key, buf))
-                host_layers.append((layer.depth, h))
-            torch.cuda.current_stream().synchronize()
-            for h, key, buf in pend:
-                h[key] = buf.numpy()
-            layers = [LayerSample(d, device=h, n=self.G.n) for d, h in host_layers]
+                    elif v.data_ptr() == self.d_off.data_ptr():
+                        h[key] = off
+                    elif v.data_ptr() == self.d_cat.data_ptr():
+                        h[key] = cat[: v.numel()]
+                    else:
+                        h[key] = host[(v.data_ptr(), v.numel())].numpy()
+                out_layers.append(LayerSample(layer.depth, device=h, n=self.G.n))
+            layers = out_layers
         return SampledEpoch(SamplerKind.SAGE, epoch, batches, layers, self.cfg.layers)

@@ -132,3 +132,20 @@ def test_sage_rejects_bad_batches():
         gb.sample_epoch_bulk(G, cfg, [[6]])
     with pytest.raises(gb.ContractViolation):
         gb.sample_epoch_bulk(G, cfg, [[0, 1, 2]])  # longer than batch_size
+
+
+def test_bulk_sampler_public_api_matches():
+    gb = _pkg()
+    from paper_2311_02909_b200.engine import BulkSampler
+
+    g, want = O.load_golden(os.path.join(GOLDEN, "epoch_rmat12_sage.npz"))
+    G = _graph(g["n"], g["rowptr"], g["col"])
+    cfg = gb.SamplerConfig.sage(3, g["batch_size"], tuple(g["fanouts"]),
+                                bulk_count=len(g["batches"]), seed=g["seed"])
+    for mode in MODES:
+        bs = BulkSampler(G, cfg, mode=mode)
+        for _ in range(2):
+            ep = bs.sample(g["batches"], epoch=g["epoch"])
+            assert O.compare_epochs(want, ep.to_arrays()) == []
+        dev = bs.sample(g["batches"], epoch=g["epoch"], to_host=False)
+        assert O.compare_epochs(want, dev.to_arrays()) == []
