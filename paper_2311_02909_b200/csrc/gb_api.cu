@@ -125,6 +125,7 @@ int gb_graph_destroy(gb_graph* g) {
   cudaFree(g->run_s0);
   cudaFree(g->run_d);
   cudaFree(g->run_n);
+  cudaFree(g->run_lower);
   delete g;
   return GB_OK;
 }

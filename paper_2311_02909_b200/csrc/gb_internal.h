@@ -8,6 +8,7 @@
 namespace gb {
 
 constexpr int kMaxRuns = 64;  // replay-table runs per degree (<= 33 + binades observed)
+constexpr int kBinades = 64;  // binade index entries per degree
 
 // Device CSR adjacency + exact-replay tables (opaque gb_graph).
 struct Graph {
@@ -21,6 +22,7 @@ struct Graph {
   double* run_s0 = nullptr;         // [slots * kMaxRuns]
   double* run_d = nullptr;          // [slots * kMaxRuns]
   int32_t* run_n = nullptr;         // [slots]
+  int8_t* run_lower = nullptr;      // [slots * kBinades] binade index
 };
 
 // Launch accounting (gb_launch_counter) and optional CUDA-event marks around

@@ -85,10 +85,13 @@ __device__ __forceinline__ uint64_t binade(double x) {
 // One thread per distinct degree m: walk S[j] = fl(S[j-1] + fl(1/m)),
 // j = 1..m, exactly as numpy's sequential cumsum does, and cut it into runs
 // of constant increment inside one binade.
+// Also the binade index lower[b] = number of runs whose start lies more than
+// b binades below the top run's binade, so the run holding a target value
+// is found in O(1) (gt_first_gt).
 __global__ void k_build_runs(const int32_t* __restrict__ slot_deg, int64_t slots,
                              int32_t* __restrict__ run_j0, double* __restrict__ run_s0,
                              double* __restrict__ run_d, int32_t* __restrict__ run_n,
-                             int32_t* __restrict__ overflow) {
+                             int8_t* __restrict__ run_lower, int32_t* __restrict__ overflow) {
   for (int64_t sl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sl < slots;
        sl += (int64_t)gridDim.x * blockDim.x) {
     const int64_t m = slot_deg[sl];
@@ -119,6 +122,15 @@ __global__ void k_build_runs(const int32_t* __restrict__ slot_deg, int64_t slots
     ++nr;
     if (nr <= kMaxRuns) J[nr] = (int32_t)(m + 1);  // sentinel
     run_n[sl] = nr;
+    if (!bad) {
+      const int64_t top = (int64_t)binade(S0[nr - 1]);
+      int8_t* low = run_lower + sl * kBinades;
+      for (int b = 0; b < kBinades; ++b) {
+        int c = 0;
+        for (int r = 0; r < nr; ++r) c += (top - (int64_t)binade(S0[r]) > b) ? 1 : 0;
+        low[b] = (int8_t)c;
+      }
+    }
     if (bad) atomicExch(overflow, 1);
   }
 }
@@ -153,6 +165,7 @@ struct SageArgs {
   const double* run_s0;
   const double* run_d;
   const int32_t* run_n;
+  const int8_t* run_lower;
   const int32_t* rowv;
   const int32_t* deg;
   const int64_t* fptr;
@@ -197,37 +210,42 @@ __device__ __forceinline__ int64_t batch_of(const int64_t* sb, const int64_t* gb
 }
 
 // Replay table of one degree read through the read-only path (L1-resident:
-// a few KB per hot degree).
+// ~1.4 KB per hot degree) with its binade index.
 struct GTable {
   const int32_t* j0;
   const double* s0;
   const double* d;
+  const int8_t* lower;
   int nr;
+  uint64_t top;  // binade of the last run's start
 };
 
-// S[n], 1 <= n <= m
+// S[n], 1 <= n <= m: n_live is near m, so scan back from the last run
 __device__ __forceinline__ double gt_S(const GTable& t, int64_t n) {
-  int lo = 0, hi = t.nr;  // last run with j0 <= n
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (__ldg(t.j0 + mid) <= n) lo = mid; else hi = mid;
-  }
-  return __dadd_rn(__ldg(t.s0 + lo), __dmul_rn((double)(n - __ldg(t.j0 + lo)), __ldg(t.d + lo)));
+  int r = t.nr - 1;
+  int32_t j0 = __ldg(t.j0 + r);
+  while (j0 > n) j0 = __ldg(t.j0 + --r);
+  return __dadd_rn(__ldg(t.s0 + r), __dmul_rn((double)(n - j0), __ldg(t.d + r)));
 }
 
-// first j >= 1 with S[j] > target (m + 1 when none)
+// first j >= 1 with S[j] > target (m + 1 when none).  The run is located by
+// the binade index (O(1)), the position inside it by a float estimate that
+// the exact fp64 comparisons then correct.
 __device__ __forceinline__ int64_t gt_first_gt(const GTable& t, double target) {
   if (target < __ldg(t.s0)) return 1;
-  int lo = 0, hi = t.nr;  // last run with s0 <= target
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (__ldg(t.s0 + mid) <= target) lo = mid; else hi = mid;
+  const int64_t off = (int64_t)t.top - (int64_t)binade(target);
+  int r = off < 0 ? t.nr : (int)__ldg(t.lower + (off < kBinades ? off : kBinades - 1));
+  // r = first run starting in target's binade or above; step back / forward
+  if (r >= t.nr || __ldg(t.s0 + r) > target) {
+    r = r - 1;
+  } else {
+    while (r + 1 < t.nr && __ldg(t.s0 + r + 1) <= target) ++r;
   }
-  const int64_t j0 = __ldg(t.j0 + lo);
-  const int64_t len = (int64_t)__ldg(t.j0 + lo + 1) - j0;
+  const int64_t j0 = __ldg(t.j0 + r);
+  const int64_t len = (int64_t)__ldg(t.j0 + r + 1) - j0;
   if (len == 1) return j0 + 1;
-  const double s0 = __ldg(t.s0 + lo), d = __ldg(t.d + lo);
-  int64_t q = (int64_t)((target - s0) / d);
+  const double s0 = __ldg(t.s0 + r), d = __ldg(t.d + r);
+  int64_t q = (int64_t)__fdividef((float)(target - s0), (float)d);
   q = q < 0 ? 0 : (q > len - 1 ? len - 1 : q);
   while (q > 0 && __dadd_rn(s0, __dmul_rn((double)q, d)) > target) --q;
   while (q + 1 < len && __dadd_rn(s0, __dmul_rn((double)(q + 1), d)) <= target) ++q;
@@ -239,10 +257,11 @@ __device__ __forceinline__ int64_t gt_first_gt(const GTable& t, double target) {
 // of weight fl(1/deg); target = u * S[n_live]; the draw selects the j-th live
 // entry, j = first j with S[j] > target clamped to n_live — exactly
 // its_sample_row's cumsum/searchsorted/clamp/walk-back (sampler.py:176-188).
-// Picks are kept sorted (frontier_from_rows sorts, sampler.py:216).
+// Picks are kept sorted (frontier_from_rows sorts, sampler.py:216) in
+// registers (MAXF = fanout bucket, fully unrolled).
 // GATHER (P-free): read the picked columns of A directly and finish the row;
 // otherwise write the row-relative indices for the streaming kernel.
-template <bool GATHER>
+template <bool GATHER, int MAXF>
 __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
                                                           const int64_t* __restrict__ R_ptr) {
   __shared__ int64_t s_brow[kBrowSmem];
@@ -257,18 +276,22 @@ __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
     if (deg == 0) continue;  // empty P row (sample_rows_ordered, sampler.py:202-204)
     const int32_t take = min(deg, A.s);
     const int64_t fp = A.fptr[r];
-    int32_t sorted[kMaxFan];
-    if (take == deg) {
-      // exhaustion: every index, no uniform consumed (sampler.py:172-174)
-      for (int t = 0; t < take; ++t) sorted[t] = t;
-    } else {
-      const int64_t bb = batch_of(s_brow, A.brow, A.k, r);
+    const int64_t bb = batch_of(s_brow, A.brow, A.k, r);
+    int32_t sorted[MAXF];
+#pragma unroll
+    for (int q = 0; q < MAXF; ++q) sorted[q] = q;  // exhaustion: every index (sampler.py:172-174)
+    if (take < deg) {
       const int64_t b0 = brow_in_smem ? s_brow[bb] : A.brow[bb];
       // global_row_keys (sampler.py:309-322)
       const uint64_t key = (uint64_t)((A.batch_offset + bb) * A.stride + (r - b0));
       const int32_t slot = __ldg(A.deg_slot + deg);
-      GTable tab{A.run_j0 + (int64_t)slot * (kMaxRuns + 1), A.run_s0 + (int64_t)slot * kMaxRuns,
-                 A.run_d + (int64_t)slot * kMaxRuns, __ldg(A.run_n + slot)};
+      GTable tab;
+      tab.j0 = A.run_j0 + (int64_t)slot * (kMaxRuns + 1);
+      tab.s0 = A.run_s0 + (int64_t)slot * kMaxRuns;
+      tab.d = A.run_d + (int64_t)slot * kMaxRuns;
+      tab.lower = A.run_lower + (int64_t)slot * kBinades;
+      tab.nr = __ldg(A.run_n + slot);
+      tab.top = binade(__ldg(tab.s0 + tab.nr - 1));
       uint64_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;
       for (int t = 0; t < take; ++t) {
         if ((t & 3) == 0) {
@@ -281,28 +304,51 @@ __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
         const double target = __dmul_rn(u, gt_S(tab, n_live));
         int64_t j = gt_first_gt(tab, target);
         if (j > n_live) j = n_live;
-        // j-th live index: skip over the removed (sorted) ones
+        // j-th live index: skip over the removed (sorted) ones, then insert
         int32_t x = (int32_t)(j - 1);
         int i = 0;
-        while (i < t && sorted[i] <= x) { ++x; ++i; }
-        for (int q = t; q > i; --q) sorted[q] = sorted[q - 1];
-        sorted[i] = x;
+#pragma unroll
+        for (int q = 0; q < MAXF; ++q)
+          if (q < t && sorted[q] <= x) { ++x; ++i; }
+#pragma unroll
+        for (int q = MAXF - 1; q > 0; --q)
+          if (q > i && q <= t) sorted[q] = sorted[q - 1];
+#pragma unroll
+        for (int q = 0; q < MAXF; ++q)
+          if (q == i) sorted[q] = x;
       }
     }
     if (GATHER) {
-      const int64_t bb = batch_of(s_brow, A.brow, A.k, r);
       const int64_t rs = A.rowptr[A.rowv[r]];
-      int32_t cv[kMaxFan];
-      for (int t = 0; t < take; ++t) cv[t] = __ldg(A.col + rs + sorted[t]);
-      for (int t = 0; t < take; ++t) A.fcol[fp + t] = cv[t];
+      int32_t cv[MAXF];
+#pragma unroll
+      for (int q = 0; q < MAXF; ++q)
+        if (q < take) cv[q] = __ldg(A.col + rs + sorted[q]);
+#pragma unroll
+      for (int q = 0; q < MAXF; ++q)
+        if (q < take) A.fcol[fp + q] = cv[q];
       if (A.bitmap) {
         uint32_t* bm = A.bitmap + bb * A.nwords;
-        for (int t = 0; t < take; ++t) atomicOr(bm + (cv[t] >> 5), 1u << (cv[t] & 31));
+#pragma unroll
+        for (int q = 0; q < MAXF; ++q)
+          if (q < take) atomicOr(bm + (cv[q] >> 5), 1u << (cv[q] & 31));
       }
     } else {
-      for (int t = 0; t < take; ++t) A.pidx[fp + t] = sorted[t];
+#pragma unroll
+      for (int q = 0; q < MAXF; ++q)
+        if (q < take) A.pidx[fp + q] = sorted[q];
     }
   }
+}
+
+template <bool GATHER>
+static void launch_pick(int grid, const SageArgs& A, const int64_t* R_ptr, cudaStream_t st) {
+  if (A.s <= 8)
+    k_sage_pick<GATHER, 8><<<grid, kPickThreads, 0, st>>>(A, R_ptr);
+  else if (A.s <= 16)
+    k_sage_pick<GATHER, 16><<<grid, kPickThreads, 0, st>>>(A, R_ptr);
+  else
+    k_sage_pick<GATHER, 32><<<grid, kPickThreads, 0, st>>>(A, R_ptr);
 }
 
 // Q^l A with the P row formed on chip: warps stream every A row of the
@@ -527,6 +573,7 @@ int graph_build_tables(Graph* g, cudaStream_t st) {
   GB_CUDA(cudaMalloc(&g->run_s0, sizeof(double) * sl * kMaxRuns));
   GB_CUDA(cudaMalloc(&g->run_d, sizeof(double) * sl * kMaxRuns));
   GB_CUDA(cudaMalloc(&g->run_n, sizeof(int32_t) * sl));
+  GB_CUDA(cudaMalloc(&g->run_lower, sizeof(int8_t) * sl * kBinades));
   int32_t* d_over = nullptr;
   GB_CUDA(cudaMallocAsync(&d_over, sizeof(int32_t), st));
   GB_CUDA(cudaMemsetAsync(d_over, 0, sizeof(int32_t), st));
@@ -536,7 +583,7 @@ int graph_build_tables(Graph* g, cudaStream_t st) {
   if (slots > 0) {
     k_build_runs<<<grid_for(slots, 64, 1 << 20), 64, 0, st>>>(g->slot_deg, slots, g->run_j0,
                                                                g->run_s0, g->run_d, g->run_n,
-                                                               d_over);
+                                                               g->run_lower, d_over);
     GB_LAUNCH_CHECK("k_build_runs");
   }
   int32_t h_over = 0;
@@ -680,7 +727,7 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     SageArgs A{};
     A.rowptr = g->rowptr; A.col = g->col;
     A.deg_slot = g->deg_slot; A.run_j0 = g->run_j0; A.run_s0 = g->run_s0; A.run_d = g->run_d;
-    A.run_n = g->run_n;
+    A.run_n = g->run_n; A.run_lower = g->run_lower;
     A.rowv = rowv; A.deg = ws.deg; A.fptr = o.fptr; A.gstart = ws.gstart;
     A.brow = brow; A.k = k; A.s = s; A.stride = stride; A.batch_offset = batch_offset;
     A.seed = seed; A.epoch = epoch; A.depth = (uint64_t)d;
@@ -688,9 +735,9 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     const int pick_grid = grid_for(r_cap, kPickThreads, 64 * kNumSMs);
     prof_mark(st);
     if (stream)
-      k_sage_pick<false><<<pick_grid, kPickThreads, 0, st>>>(A, R_ptr);
+      launch_pick<false>(pick_grid, A, R_ptr, st);
     else
-      k_sage_pick<true><<<pick_grid, kPickThreads, 0, st>>>(A, R_ptr);
+      launch_pick<true>(pick_grid, A, R_ptr, st);
     GB_LAUNCH_CHECK("k_sage_pick");
     prof_mark(st);
     if (stream) {
@@ -778,18 +825,18 @@ int sage_layer_sample(const Graph* tables, int64_t k, const int64_t* brow, int64
   SageArgs A{};
   A.rowptr = rowptr; A.col = col;
   A.deg_slot = tables->deg_slot; A.run_j0 = tables->run_j0; A.run_s0 = tables->run_s0;
-  A.run_d = tables->run_d; A.run_n = tables->run_n;
+  A.run_d = tables->run_d; A.run_n = tables->run_n; A.run_lower = tables->run_lower;
   A.rowv = rowv; A.deg = deg; A.fptr = fptr; A.gstart = gstart;
   A.brow = brow; A.k = k; A.s = s; A.stride = stride; A.batch_offset = batch_offset;
   A.seed = seed; A.epoch = epoch; A.depth = depth;
   A.bitmap = nullptr; A.nwords = 0; A.fcol = fcol; A.pidx = pidx;
   const int pick_grid = grid_for(r_cap, kPickThreads, 64 * kNumSMs);
   if (stream) {
-    k_sage_pick<false><<<pick_grid, kPickThreads, 0, st>>>(A, R_ptr);
+    launch_pick<false>(pick_grid, A, R_ptr, st);
     k_sage_stream<<<stream_grid(), kStreamThreads, 0, st>>>(A, R_ptr);
     count_launches(2);
   } else {
-    k_sage_pick<true><<<pick_grid, kPickThreads, 0, st>>>(A, R_ptr);
+    launch_pick<true>(pick_grid, A, R_ptr, st);
     count_launches(1);
   }
   GB_LAUNCH_CHECK("sage_layer_sample");
