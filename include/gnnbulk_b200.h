@@ -208,6 +208,31 @@ int gb_its_rows(int64_t m, const int64_t* d_ptr, const double* d_val, int32_t s,
                 uint64_t depth, double* d_w, double* d_cdf, int32_t* d_picks, int32_t* d_take,
                 int32_t* d_err, void* stream);
 
+/* ------------------------------------ LADIES per-layer pieces (1.5D mode)
+ *   gb_ladies_counts       partial P = Q A over the rows with d_qdeg[q] > 0
+ *                          through a local CSR addressed by d_qcol[q]: per
+ *                          batch the sorted (v, e) nonzeros at d_poff[i]
+ *   gb_ladies_race_topk    exponential-race top-s of every batch's (v, e)
+ *                          list: d_take[i], sorted vertices d_Sv[i*s ...] and
+ *                          their race keys d_Sk (for the grid-row merge)
+ *   gb_ladies_extract_rows A_S rows of Q (ranks of A[u,:] ∩ S_i) into the
+ *                          upper-bound slot layout d_slot / d_slots, counts
+ *                          d_rcnt (ladies_assemble, sampler.py:420-434) */
+size_t gb_ladies_counts_workspace(int64_t k, int64_t n, int64_t q_cap);
+int gb_ladies_counts(int64_t k, const int64_t* d_qoff, const int32_t* d_qcol, const int32_t* d_qdeg,
+                     int64_t q_cap, const int64_t* d_rowptr, const int32_t* d_col, int64_t n,
+                     int64_t* d_poff, int32_t* d_pv, int32_t* d_pe, void* d_ws, size_t ws_bytes,
+                     void* stream);
+size_t gb_ladies_race_topk_workspace(int64_t k, int64_t p_cap, int32_t s);
+int gb_ladies_race_topk(int64_t k, const int64_t* d_poff, const int32_t* d_pv, const int32_t* d_pe,
+                        int64_t p_cap, int32_t s, uint64_t seed, uint64_t epoch, uint64_t depth,
+                        int64_t batch_offset, int64_t* d_take, int32_t* d_Sv, uint32_t* d_Sk,
+                        void* d_ws, size_t ws_bytes, void* stream);
+int gb_ladies_extract_rows(int64_t k, const int64_t* d_qoff, const int32_t* d_qcol,
+                           const int64_t* d_rowptr, const int32_t* d_col, const int64_t* d_fptr,
+                           const int32_t* d_fcol, const int64_t* d_coloff, const int64_t* d_slot,
+                           int32_t* d_slots, int32_t* d_rcnt, void* stream);
+
 /* ----------------------------------------------------- synthetic inputs
  * R-MAT edge candidates first..first+count (Graph500 quadrant recursion over
  * `scale` levels with probabilities a, b, c; rejected candidates = -1) and

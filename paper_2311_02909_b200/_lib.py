@@ -59,6 +59,13 @@ SIGNATURES = {
     "gb_ladies_bulk": (ctypes.c_int, [_p, _i64, _p, _p, _i64, _i32, _p, _u64, _u64, _i64, _i32,
                                       ctypes.POINTER(LadiesLayerOut), _p, _p, ctypes.c_size_t,
                                       _p]),
+    "gb_ladies_counts_workspace": (ctypes.c_size_t, [_i64, _i64, _i64]),
+    "gb_ladies_counts": (ctypes.c_int, [_i64, _p, _p, _p, _i64, _p, _p, _i64, _p, _p, _p, _p,
+                                        ctypes.c_size_t, _p]),
+    "gb_ladies_race_topk_workspace": (ctypes.c_size_t, [_i64, _i64, _i32]),
+    "gb_ladies_race_topk": (ctypes.c_int, [_i64, _p, _p, _p, _i64, _i32, _u64, _u64, _u64, _i64,
+                                           _p, _p, _p, _p, ctypes.c_size_t, _p]),
+    "gb_ladies_extract_rows": (ctypes.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p, _p]),
     "gb_take_scan": (ctypes.c_int, [_i64, _p, _p, _i32, _p, _p, _p]),
     "gb_sage_layer_sample_workspace": (ctypes.c_size_t, [_i64, _i64]),
     "gb_sage_layer_sample": (ctypes.c_int, [_p, _i64, _p, _i64, _p, _p, _p, _p, _p, _i32, _i64,

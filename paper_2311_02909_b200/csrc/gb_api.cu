@@ -213,6 +213,40 @@ int gb_gather_features(int64_t m, const int32_t* d_ids, int64_t row0, const floa
   return gather_features(m, d_ids, row0, d_H, f, d_out, (cudaStream_t)stream);
 }
 
+size_t gb_ladies_counts_workspace(int64_t k, int64_t n, int64_t q_cap) {
+  return ladies_counts_ws(k, n, q_cap);
+}
+
+int gb_ladies_counts(int64_t k, const int64_t* d_qoff, const int32_t* d_qcol, const int32_t* d_qdeg,
+                     int64_t q_cap, const int64_t* d_rowptr, const int32_t* d_col, int64_t n,
+                     int64_t* d_poff, int32_t* d_pv, int32_t* d_pe, void* d_ws, size_t ws_bytes,
+                     void* stream) {
+  if (k < 0 || n < 0) { set_error("ladies counts: bad arguments"); return GB_ERR_CONTRACT; }
+  return ladies_counts(k, d_qoff, d_qcol, d_qdeg, q_cap, d_rowptr, d_col, n, d_poff, d_pv, d_pe,
+                       d_ws, ws_bytes, (cudaStream_t)stream);
+}
+
+size_t gb_ladies_race_topk_workspace(int64_t k, int64_t p_cap, int32_t s) {
+  return ladies_race_topk_ws(k, p_cap, s);
+}
+
+int gb_ladies_race_topk(int64_t k, const int64_t* d_poff, const int32_t* d_pv, const int32_t* d_pe,
+                        int64_t p_cap, int32_t s, uint64_t seed, uint64_t epoch, uint64_t depth,
+                        int64_t batch_offset, int64_t* d_take, int32_t* d_Sv, uint32_t* d_Sk,
+                        void* d_ws, size_t ws_bytes, void* stream) {
+  if (k < 0 || s < 1) { set_error("ladies race: bad arguments"); return GB_ERR_CONTRACT; }
+  return ladies_race_topk(k, d_poff, d_pv, d_pe, p_cap, s, seed, epoch, depth, batch_offset,
+                          d_take, d_Sv, d_Sk, d_ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int gb_ladies_extract_rows(int64_t k, const int64_t* d_qoff, const int32_t* d_qcol,
+                           const int64_t* d_rowptr, const int32_t* d_col, const int64_t* d_fptr,
+                           const int32_t* d_fcol, const int64_t* d_coloff, const int64_t* d_slot,
+                           int32_t* d_slots, int32_t* d_rcnt, void* stream) {
+  return ladies_extract_rows(k, d_qoff, d_qcol, d_rowptr, d_col, d_fptr, d_fcol, d_coloff, d_slot,
+                             d_slots, d_rcnt, (cudaStream_t)stream);
+}
+
 int gb_ladies_bulk_workspace(const gb_graph* g, int64_t k, int64_t q1_cap, int32_t layers,
                              const int64_t* h_fanouts, int32_t mode, size_t* h_bytes) {
   if (!g || !h_bytes || k < 0 || layers < 1 || !h_fanouts) {

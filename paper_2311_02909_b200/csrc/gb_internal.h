@@ -55,6 +55,20 @@ int gather_rows(int64_t m, const int32_t* ids, int64_t row0, const int64_t* rowp
                 const int32_t* col, const int64_t* out_off, int32_t* out, cudaStream_t st);
 int gather_features(int64_t m, const int32_t* ids, int64_t row0, const float* H, int64_t f,
                     float* out, cudaStream_t st);
+size_t ladies_counts_ws(int64_t k, int64_t n, int64_t q_cap);
+int ladies_counts(int64_t k, const int64_t* qoff, const int32_t* qcol, const int32_t* qdeg,
+                  int64_t q_cap, const int64_t* rowptr, const int32_t* col, int64_t n,
+                  int64_t* poff, int32_t* pv, int32_t* pe, void* d_ws, size_t ws_bytes,
+                  cudaStream_t st);
+size_t ladies_race_topk_ws(int64_t k, int64_t p_cap, int32_t s);
+int ladies_race_topk(int64_t k, const int64_t* poff, const int32_t* pv, const int32_t* pe,
+                     int64_t p_cap, int32_t s, uint64_t seed, uint64_t epoch, uint64_t depth,
+                     int64_t batch_offset, int64_t* take, int32_t* Sv, uint32_t* Sk, void* d_ws,
+                     size_t ws_bytes, cudaStream_t st);
+int ladies_extract_rows(int64_t k, const int64_t* qoff, const int32_t* qcol,
+                        const int64_t* rowptr, const int32_t* col, const int64_t* fptr,
+                        const int32_t* fcol, const int64_t* coloff, const int64_t* slot,
+                        int32_t* slots, int32_t* rcnt, cudaStream_t st);
 int ladies_workspace(const Graph* g, int64_t k, int64_t q1_cap, int32_t layers,
                      const int64_t* fanouts, int32_t mode, size_t* bytes);
 int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t* d_qverts,

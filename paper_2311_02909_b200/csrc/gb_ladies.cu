@@ -191,15 +191,18 @@ struct RaceKey {
   }
 };
 
-// keys != nullptr (race mode): also writes the race key of every nonzero
+// obase != nullptr: outputs start at *obase (batch groups appended)
 __global__ void __launch_bounds__(256) k_lad_compact_write(uint32_t* __restrict__ cnt32,
                                                          int64_t words, int64_t n,
                                                          const int64_t* __restrict__ tile_off,
                                                          int32_t* __restrict__ pv,
                                                          int32_t* __restrict__ pe,
-                                                         uint32_t* __restrict__ keys,
-                                                         RaceKey rk) {
+                                                         const int64_t* __restrict__ obase) {
   __shared__ int64_t sw[33];
+  if (obase) {
+    pv += *obase;
+    pe += *obase;
+  }
   const int64_t ntiles = (2 * words + kCompTile - 1) / kCompTile;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const int64_t w0 = t * (kCompTile / 2) + threadIdx.x * 8;
@@ -328,7 +331,7 @@ __global__ void __launch_bounds__(256) k_lad_keys(LadiesSampleArgs A, RaceKey rk
   __syncthreads();
   const int64_t* gp = sm ? sp : A.gpoff;
   const int64_t P = gp[A.gn];
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+  for (int64_t p = gp[0] + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
        p += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = last_le(gp, A.gn + 1, p);
     A.keys[p] = rk(j, A.pv[p], (uint32_t)A.pe[p]);
@@ -340,7 +343,8 @@ constexpr int kHistChunk = 8192;
 __global__ void __launch_bounds__(256) k_lad_hist(LadiesSampleArgs A, uint32_t* __restrict__ hist) {
   __shared__ uint32_t h[kBins];
   const int64_t P = A.gpoff[A.gn];
-  for (int64_t c0 = (int64_t)blockIdx.x * kHistChunk; c0 < P; c0 += (int64_t)gridDim.x * kHistChunk) {
+  for (int64_t c0 = A.gpoff[0] + (int64_t)blockIdx.x * kHistChunk; c0 < P;
+       c0 += (int64_t)gridDim.x * kHistChunk) {
     const int64_t c1 = min(c0 + kHistChunk, P);
     const int64_t j0 = last_le(A.gpoff, A.gn + 1, c0);
     const int64_t b1 = A.gpoff[j0 + 1];
@@ -389,7 +393,7 @@ __global__ void __launch_bounds__(256) k_lad_boundary(LadiesSampleArgs A,
 __global__ void k_lad_filter(LadiesSampleArgs A, const int32_t* __restrict__ bound,
                              int32_t* __restrict__ cand, int32_t* __restrict__ ncand) {
   const int64_t P = A.gpoff[A.gn];
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
+  for (int64_t p = A.gpoff[0] + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < P;
        p += (int64_t)gridDim.x * blockDim.x) {
     const int64_t j = last_le(A.gpoff, A.gn + 1, p);
     const int64_t i = A.g0 + j;
@@ -468,7 +472,9 @@ __global__ void __launch_bounds__(1024) k_lad_refine(LadiesSampleArgs A,
 }
 
 // sorted sampled vertices of each batch of the group: Sfix[i*s + r]
-__global__ void __launch_bounds__(256) k_lad_emit(LadiesSampleArgs A, int32_t* __restrict__ Sfix) {
+// (and, for the distributed top-s merge, their race keys Kfix)
+__global__ void __launch_bounds__(256) k_lad_emit(LadiesSampleArgs A, int32_t* __restrict__ Sfix,
+                                                uint32_t* __restrict__ Kfix) {
   for (int64_t j = blockIdx.x; j < A.gn; j += gridDim.x) {
     const int64_t i = A.g0 + j;
     const int64_t take = A.take[i];
@@ -478,6 +484,7 @@ __global__ void __launch_bounds__(256) k_lad_emit(LadiesSampleArgs A, int32_t* _
       int64_t rank = 0;
       for (int64_t b = 0; b < take; ++b) rank += si[b] < x ? 1 : 0;
       Sfix[i * A.s + rank] = A.pv[x];  // P positions ascend with v inside a batch
+      if (Kfix) Kfix[i * A.s + rank] = A.keys[x];
     }
   }
 }
@@ -784,7 +791,7 @@ int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t*
       if (rc) return rc;
       const RaceKey rk{seed, epoch, (uint64_t)(l + 1), batch_offset + g0};
       k_lad_compact_write<<<gcap(P.tiles, 1, 8 * sms), 256, 0, st>>>(
-          ws.cnt32, words, n, ws.tile_off, ws.pv, ws.pe, nullptr, rk);
+          ws.cnt32, words, n, ws.tile_off, ws.pv, ws.pe, nullptr);
       GB_LAUNCH_CHECK("k_lad_compact");
       // ---- NORM + SAMPLE
       LadiesSampleArgs A{};
@@ -806,7 +813,7 @@ int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t*
         count_launches(5);
       }
       GB_LAUNCH_CHECK("k_lad_sample");
-      k_lad_emit<<<(int)gn, 256, 0, st>>>(A, ws.Sfix);
+      k_lad_emit<<<(int)gn, 256, 0, st>>>(A, ws.Sfix, nullptr);
       GB_LAUNCH_CHECK("k_lad_emit");
       count_launches(6);
     }
@@ -829,6 +836,154 @@ int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t*
     count_launches(5);
     qc = k * s;
   }
+  return GB_OK;
+}
+
+// ======================================== pieces of the 1.5D LADIES executor
+
+struct QDegMF {
+  const int32_t* qdeg;
+  __device__ int64_t operator()(int64_t q) const { return qdeg[q]; }
+};
+
+// global offsets of a group's batches: poff[g0 + j + 1] = poff[g0 + j] + nnz
+__global__ void k_lad_poff(const int64_t* __restrict__ nnz_b, int64_t g0, int64_t gn,
+                           int64_t* __restrict__ poff) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    if (g0 == 0) poff[0] = 0;
+    for (int64_t j = 0; j < gn; ++j) poff[g0 + j + 1] = poff[g0 + j] + nnz_b[g0 + j];
+  }
+}
+
+size_t ladies_counts_ws(int64_t k, int64_t n, int64_t q_cap) {
+  int64_t gsize = n > 0 ? kGroupBytes / (2 * n) : k;
+  if (gsize < 1) gsize = 1;
+  if (gsize > k) gsize = k > 0 ? k : 1;
+  const int64_t words = (gsize * n + 1) / 2 + 1;
+  const int64_t tiles = (2 * words + kCompTile - 1) / kCompTile;
+  int64_t sn = q_cap > tiles ? q_cap : tiles;
+  return al(sizeof(uint32_t) * words) + al(sizeof(int64_t) * (k + 1)) +
+         al(sizeof(int64_t) * (q_cap + 1)) + al(sizeof(int64_t) * (tiles + 1)) +
+         al(sizeof(int64_t) * scan_workspace_elems<int64_t>(sn + 1)) + al(sizeof(int64_t) * 4);
+}
+
+// Partial P = Q A over the rows with qdeg[q] > 0, read through the CSR
+// (rowptr, col) addressed by qcol[q]: per batch the sorted (v, e) nonzeros
+// at poff[i] (k + 1 offsets).  Same grouped counters as ladies_bulk.
+int ladies_counts(int64_t k, const int64_t* qoff, const int32_t* qcol, const int32_t* qdeg,
+                  int64_t q_cap, const int64_t* rowptr, const int32_t* col, int64_t n,
+                  int64_t* poff, int32_t* pv, int32_t* pe, void* d_ws, size_t ws_bytes,
+                  cudaStream_t st) {
+  if (ladies_counts_ws(k, n, q_cap) > ws_bytes) {
+    set_error("ladies counts workspace too small");
+    return GB_ERR_CAPACITY;
+  }
+  int64_t gsize = n > 0 ? kGroupBytes / (2 * n) : k;
+  if (gsize < 1) gsize = 1;
+  if (gsize > k) gsize = k > 0 ? k : 1;
+  const int64_t pwords = (gsize * n + 1) / 2 + 1;
+  const int64_t tiles = (2 * pwords + kCompTile - 1) / kCompTile;
+  char* p = (char*)d_ws;
+  auto carve = [&](size_t bytes) { char* r = p; p += al(bytes); return r; };
+  uint32_t* cnt32 = (uint32_t*)carve(sizeof(uint32_t) * pwords);
+  int64_t* nnz_b = (int64_t*)carve(sizeof(int64_t) * (k + 1));
+  int64_t* qg = (int64_t*)carve(sizeof(int64_t) * (q_cap + 1));
+  int64_t* tile_off = (int64_t*)carve(sizeof(int64_t) * (tiles + 1));
+  int64_t sn = q_cap > tiles ? q_cap : tiles;
+  int64_t* scan_ws = (int64_t*)carve(sizeof(int64_t) * scan_workspace_elems<int64_t>(sn + 1));
+  int64_t* d_tiles = (int64_t*)carve(sizeof(int64_t) * 4);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  if (sms <= 0) sms = kNumSMs;
+  GB_CUDA(cudaMemsetAsync(cnt32, 0, sizeof(uint32_t) * pwords, st));
+  GB_CUDA(cudaMemsetAsync(nnz_b, 0, sizeof(int64_t) * (k + 1), st));
+  k_lad_set<<<1, 1, 0, st>>>(d_tiles, tiles);
+  int rc = device_exclusive_scan<int64_t>(qoff + k, q_cap, QDegMF{qdeg}, qg, scan_ws, st);
+  if (rc) return rc;
+  if (k == 0) k_lad_poff<<<1, 1, 0, st>>>(nnz_b, 0, 0, poff);
+  for (int64_t g0 = 0; g0 < k; g0 += gsize) {
+    const int64_t g1 = g0 + gsize < k ? g0 + gsize : k;
+    const int64_t gn = g1 - g0;
+    const int64_t words = (gn * n + 1) / 2;
+    k_lad_count<<<4 * sms, kLadiesThreads, 0, st>>>(qoff, k, g0, g1, qcol, qg, rowptr, col, n,
+                                                    cnt32, nnz_b);
+    k_lad_compact_count<<<gcap(tiles, 1, 8 * sms), 256, 0, st>>>(cnt32, words, n, g0, tile_off,
+                                                                nnz_b);
+    k_lad_poff<<<1, 1, 0, st>>>(nnz_b, g0, gn, poff);
+    rc = device_exclusive_scan<int64_t>(d_tiles, tiles, TileF{tile_off}, tile_off, scan_ws, st);
+    if (rc) return rc;
+    k_lad_compact_write<<<gcap(tiles, 1, 8 * sms), 256, 0, st>>>(cnt32, words, n, tile_off, pv,
+                                                                pe, poff + g0);
+    GB_LAUNCH_CHECK("ladies_counts");
+    count_launches(4);
+  }
+  return GB_OK;
+}
+
+constexpr int64_t kSelGroup = 64;  // batches per race-select pass
+
+size_t ladies_race_topk_ws(int64_t k, int64_t p_cap, int32_t s) {
+  return al(sizeof(uint32_t) * (p_cap + 1)) + al(sizeof(int32_t) * (p_cap + 1)) +
+         al(sizeof(int32_t) * (kSelGroup + 1)) + al(sizeof(uint32_t) * kSelGroup * kBins) +
+         al(sizeof(int32_t) * 2 * (kSelGroup + 1)) + al(sizeof(int32_t) * (k * s + 1)) +
+         al(sizeof(int32_t) * (k + 1)) + al(sizeof(int32_t));
+}
+
+// Exponential-race top-s of every batch's (v, e) list: take[i], the sorted
+// selected vertices Sv[i*s ...] and their keys Sk (for a distributed merge).
+int ladies_race_topk(int64_t k, const int64_t* poff, const int32_t* pv, const int32_t* pe,
+                     int64_t p_cap, int32_t s, uint64_t seed, uint64_t epoch, uint64_t depth,
+                     int64_t batch_offset, int64_t* take, int32_t* Sv, uint32_t* Sk, void* d_ws,
+                     size_t ws_bytes, cudaStream_t st) {
+  if (ladies_race_topk_ws(k, p_cap, s) > ws_bytes) {
+    set_error("ladies race workspace too small");
+    return GB_ERR_CAPACITY;
+  }
+  char* p = (char*)d_ws;
+  auto carve = [&](size_t bytes) { char* r = p; p += al(bytes); return r; };
+  uint32_t* keys = (uint32_t*)carve(sizeof(uint32_t) * (p_cap + 1));
+  int32_t* cand = (int32_t*)carve(sizeof(int32_t) * (p_cap + 1));
+  int32_t* ncand = (int32_t*)carve(sizeof(int32_t) * (kSelGroup + 1));
+  uint32_t* hist = (uint32_t*)carve(sizeof(uint32_t) * kSelGroup * kBins);
+  int32_t* bound = (int32_t*)carve(sizeof(int32_t) * 2 * (kSelGroup + 1));
+  int32_t* sel = (int32_t*)carve(sizeof(int32_t) * (k * s + 1));
+  int32_t* nsel = (int32_t*)carve(sizeof(int32_t) * (k + 1));
+  int32_t* overflow = (int32_t*)carve(sizeof(int32_t));
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  if (sms <= 0) sms = kNumSMs;
+  for (int64_t g0 = 0; g0 < k; g0 += kSelGroup) {
+    const int64_t gn = g0 + kSelGroup < k ? kSelGroup : k - g0;
+    LadiesSampleArgs A{};
+    A.gpoff = poff + g0; A.pv = pv; A.pe = pe; A.g0 = g0; A.gn = gn; A.s = s;
+    A.batch_offset = batch_offset; A.seed = seed; A.epoch = epoch; A.depth = depth;
+    A.keys = keys; A.sel = sel; A.nsel = nsel; A.take = take;
+    const RaceKey rk{seed, epoch, depth, batch_offset + g0};
+    GB_CUDA(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * gn * kBins, st));
+    GB_CUDA(cudaMemsetAsync(ncand, 0, sizeof(int32_t) * (gn + 1), st));
+    k_lad_keys<<<16 * sms, 256, 0, st>>>(A, rk);
+    k_lad_hist<<<4 * sms, 256, 0, st>>>(A, hist);
+    k_lad_boundary<<<(int)gn, 256, 0, st>>>(A, hist, bound);
+    k_lad_filter<<<16 * sms, 256, 0, st>>>(A, bound, cand, ncand);
+    k_lad_refine<<<(int)gn, 1024, 0, st>>>(A, bound, cand, ncand, overflow);
+    k_lad_emit<<<(int)gn, 256, 0, st>>>(A, Sv, Sk);
+    GB_LAUNCH_CHECK("ladies_race_topk");
+    count_launches(6);
+  }
+  return GB_OK;
+}
+
+int ladies_extract_rows(int64_t k, const int64_t* qoff, const int32_t* qcol,
+                        const int64_t* rowptr, const int32_t* col, const int64_t* fptr,
+                        const int32_t* fcol, const int64_t* coloff, const int64_t* slot,
+                        int32_t* slots, int32_t* rcnt, cudaStream_t st) {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  if (sms <= 0) sms = kNumSMs;
+  k_lad_extract<<<8 * sms, kLadiesThreads, 0, st>>>(qoff, k, qcol, rowptr, col, fptr, fcol, coloff,
+                                                   slot, slots, rcnt);
+  GB_LAUNCH_CHECK("ladies_extract_rows");
+  count_launches(1);
   return GB_OK;
 }
 

@@ -251,6 +251,195 @@ class Sage15D:
         return layers
 
 
+class Ladies15D(Sage15D):
+    """1.5D partitioned LADIES (exponential-race sampling) over real processes.
+
+    Per layer, grid row i (k_i batches), replica j:
+      1. row fetch of the batch vertices in column j's range (as SAGE);
+      2. partial P: counts e_v from the fetched rows (gb_ladies_counts);
+      3. sparse merge (reduce-scatter by vertex range over the c replicas):
+         replica m receives every (batch, v, e) with v in its range and sums
+         them, so it owns the exact counts of its vertices;
+      4. local top-s by race key (gb_ladies_race_topk), all-gather of the
+         c*s candidates, final top-s by (key, v) — keys depend only on
+         (batch, v, e), so the result equals the single-GPU race sampler;
+      5. A_S rows for the replica's own Q vertices in the slot layout
+         (gb_ladies_extract_rows), summed over the grid row (C4, dist.py:523).
+    """
+
+    def sample(self, group_batches, epoch, batch_offset, seed):
+        import torch.distributed as dist
+
+        torch = _torch()
+        L = _lib.lib()
+        dev, n, c = self.dev, self.n, self.grid.c
+        k = len(group_batches)
+        rg = self.row_groups[self.i]
+        off = np.zeros(k + 1, np.int64)
+        off[1:] = np.cumsum([len(x) for x in group_batches])
+        qoff = torch.as_tensor(off).to(dev)
+        qcol = torch.as_tensor(np.concatenate([np.sort(np.asarray(x)) for x in group_batches])
+                               .astype(np.int32) if off[-1] else np.zeros(0, np.int32)).to(dev)
+        vr = _bounds(n, c)
+        layers = []
+        for l, s in enumerate(self.fanouts):
+            QN = int(qoff[k].item())
+            qc = qcol[:QN]
+            mine = (qc >= self.V0) & (qc < self.V1)
+            U = torch.unique(qc[mine])
+            lrowptr, lcol = self.fetch_rows(U)
+            nnz = int(lrowptr[-1].item())
+            lrowptr = torch.cat([lrowptr, lrowptr[-1:]])  # dummy empty row U.numel()
+            lrow = torch.searchsorted(U, qc).to(torch.int32)
+            lrow = torch.where(mine, lrow, torch.full_like(lrow, U.numel())).contiguous()
+            qdeg = torch.where(mine, self.gdeg[qc.long()], torch.zeros_like(lrow)).contiguous()
+            # -- partial counts
+            pcap = max(min(k * n, int(qdeg.long().sum().item())), 1)
+            poff = torch.zeros(k + 1, dtype=torch.int64, device=dev)
+            pv = torch.empty(pcap, dtype=torch.int32, device=dev)
+            pe = torch.empty(pcap, dtype=torch.int32, device=dev)
+            ws = torch.empty(max(L.gb_ladies_counts_workspace(k, n, max(QN, 1)), 1),
+                             dtype=torch.uint8, device=dev)
+            _lib.check(L.gb_ladies_counts(k, _lib.ptr(qoff), _lib.ptr(lrow), _lib.ptr(qdeg),
+                                          max(QN, 1), _lib.ptr(lrowptr), _lib.ptr(lcol), n,
+                                          _lib.ptr(poff), _lib.ptr(pv), _lib.ptr(pe),
+                                          _lib.ptr(ws), ws.numel(), _lib.stream_ptr()),
+                       "gb_ladies_counts")
+            P = int(poff[k].item())
+            bid = torch.repeat_interleave(torch.arange(k, device=dev, dtype=torch.int32),
+                                          (poff[1:] - poff[:-1]))
+            trip = torch.stack([bid, pv[:P], pe[:P]], 1)
+            # -- sparse merge: reduce-scatter by vertex range inside the grid row
+            sends = {}
+            for m in range(c):
+                sel = (trip[:, 1] >= int(vr[m])) & (trip[:, 1] < int(vr[m + 1]))
+                sends[self.grid.rank(self.i, m)] = trip[sel].flatten().contiguous()
+            cnts = exchange_counts(sends, self.row_ranks, dev)
+            got = exchange(sends, cnts, self.row_ranks, torch.int32, dev)
+            allt = torch.cat([got[p].view(-1, 3) for p in self.row_ranks if p in got]) \
+                if got else torch.zeros((0, 3), dtype=torch.int32, device=dev)
+            key = allt[:, 0].long() * n + allt[:, 1].long()
+            ukey, inv = torch.unique(key, return_inverse=True)
+            esum = torch.zeros(ukey.numel(), dtype=torch.int64, device=dev)
+            esum.index_add_(0, inv, allt[:, 2].long())
+            mb = (ukey // n)
+            moff = torch.zeros(k + 1, dtype=torch.int64, device=dev)
+            moff[1:] = torch.cumsum(torch.bincount(mb, minlength=k), 0)
+            mv = (ukey % n).to(torch.int32).contiguous()
+            me = esum.to(torch.int32).contiguous()
+            # -- local race top-s, then the grid-row merge of candidates
+            mcap = max(mv.numel(), 1)
+            take = torch.zeros(k, dtype=torch.int64, device=dev)
+            Sv = torch.zeros(max(k * s, 1), dtype=torch.int32, device=dev)
+            Sk = torch.zeros(max(k * s, 1), dtype=torch.int32, device=dev)
+            rws = torch.empty(max(L.gb_ladies_race_topk_workspace(k, mcap, s), 1),
+                              dtype=torch.uint8, device=dev)
+            if k:
+                _lib.check(L.gb_ladies_race_topk(k, _lib.ptr(moff), _lib.ptr(mv), _lib.ptr(me),
+                                                 mcap, s, seed, epoch, l + 1, batch_offset,
+                                                 _lib.ptr(take), _lib.ptr(Sv), _lib.ptr(Sk),
+                                                 _lib.ptr(rws), rws.numel(), _lib.stream_ptr()),
+                           "gb_ladies_race_topk")
+            nb = (moff[1:] - moff[:-1]).clone()
+            if c > 1:
+                dist.all_reduce(nb, group=rg)
+                pack = torch.cat([take, Sv[:k * s].long(), (Sk[:k * s].long() & 0xffffffff)])
+                parts = [torch.empty_like(pack) for _ in range(c)]
+                dist.all_gather(parts, pack, group=rg)
+            else:
+                parts = [torch.cat([take, Sv[:k * s].long(), Sk[:k * s].long() & 0xffffffff])]
+            ct, cv, ck, cb = [], [], [], []
+            for pt in parts:
+                tk = pt[:k]
+                v2 = pt[k:k + k * s].view(k, s)
+                k2 = pt[k + k * s:].view(k, s)
+                valid = torch.arange(s, device=dev)[None, :] < tk[:, None]
+                cv.append(v2[valid])
+                ck.append(k2[valid])
+                cb.append(torch.arange(k, device=dev)[:, None].expand(k, s)[valid])
+            cv, ck, cb = torch.cat(cv), torch.cat(ck), torch.cat(cb)
+            o1 = torch.argsort(cv, stable=True)
+            o2 = torch.argsort((cb[o1] << 32) | ck[o1], stable=True)
+            order = o1[o2]
+            cb, cv = cb[order], cv[order]
+            tk = torch.minimum(nb, torch.full_like(nb, s))
+            first = torch.zeros(k + 1, dtype=torch.int64, device=dev)
+            first[1:] = torch.cumsum(torch.bincount(cb, minlength=k), 0)
+            rank = torch.arange(cb.numel(), device=dev) - first[cb]
+            keep = rank < tk[cb]
+            fb, fv = cb[keep], cv[keep]
+            o3 = torch.argsort((fb << 32) | fv)
+            fcol = fv[o3].to(torch.int32).contiguous()
+            fptr = torch.zeros(k + 1, dtype=torch.int64, device=dev)
+            fptr[1:] = torch.cumsum(tk, 0)
+            F = int(fptr[k].item())
+            # -- extraction of this replica's Q rows, summed over the grid row
+            takes = tk
+            shared = bool((takes == takes[0]).all().item()) if k else True
+            coloff = torch.zeros(k + 1, dtype=torch.int64, device=dev) if shared else fptr.clone()
+            qb = torch.repeat_interleave(torch.arange(k, device=dev), qoff[1:] - qoff[:-1])
+            rcap = torch.minimum(self.gdeg[qc.long()].long(), takes[qb]) if QN else \
+                torch.zeros(0, dtype=torch.int64, device=dev)
+            slot = torch.zeros(QN + 1, dtype=torch.int64, device=dev)
+            slot[1:] = torch.cumsum(rcap, 0)
+            slots = torch.zeros(max(int(slot[-1].item()), 1), dtype=torch.int32, device=dev)
+            rcnt = torch.zeros(max(QN, 1), dtype=torch.int32, device=dev)
+            if QN:
+                _lib.check(L.gb_ladies_extract_rows(k, _lib.ptr(qoff), _lib.ptr(lrow),
+                                                    _lib.ptr(lrowptr), _lib.ptr(lcol),
+                                                    _lib.ptr(fptr), _lib.ptr(fcol),
+                                                    _lib.ptr(coloff), _lib.ptr(slot),
+                                                    _lib.ptr(slots), _lib.ptr(rcnt),
+                                                    _lib.stream_ptr()), "gb_ladies_extract_rows")
+            if c > 1 and QN:
+                dist.all_reduce(slots, group=rg)
+                dist.all_reduce(rcnt, group=rg)
+                self.stats["reduce_words"] += slots.numel() + rcnt.numel()
+            aptr = torch.zeros(QN + 1, dtype=torch.int64, device=dev)
+            aptr[1:] = torch.cumsum(rcnt[:QN].long(), 0)
+            E = int(aptr[-1].item())
+            if E:
+                src = (slot[:-1].repeat_interleave(rcnt[:QN].long()) +
+                       torch.arange(E, device=dev) - aptr[:-1].repeat_interleave(rcnt[:QN].long()))
+                acol = slots[src]
+            else:
+                acol = torch.zeros(0, dtype=torch.int32, device=dev)
+            width = 0 if k == 0 else (int(takes[0].item()) if shared else F)
+            layers.append({
+                "frontier_shape": (k, n), "frontier_ptr": fptr, "frontier_col": fcol,
+                "adj_shape": (QN, width), "adj_ptr": aptr, "adj_col": acol,
+                "rowv_off": qoff, "rowv_cat": qc, "colv_off": fptr, "colv_cat": fcol,
+                "sampv_off": fptr, "sampv_cat": fcol,
+            })
+            del nnz
+            qoff, qcol = fptr, fcol
+        return layers
+
+
+def ladies_epoch_15d(sampler: Ladies15D, cfg, batches, epoch=0, batch_offset=0):
+    """Distributed LADIES epoch over the grid, gathered on every rank."""
+    import torch.distributed as dist
+
+    from .dist import merge_epochs
+
+    grid = sampler.grid
+    b = _bounds(len(batches), grid.rows)
+    g0, g1 = int(b[sampler.i]), int(b[sampler.i + 1])
+    mine = sampler.sample([np.asarray(x) for x in batches[g0:g1]], epoch, batch_offset + g0,
+                          cfg.seed)
+    local = [{k2: (v if isinstance(v, tuple) else v.cpu().numpy()) for k2, v in lay.items()}
+             for lay in mine]
+    allp = [None] * grid.p
+    dist.all_gather_object(allp, local)
+    parts = []
+    for i in range(grid.rows):
+        gi = [np.asarray(x) for x in batches[int(b[i]):int(b[i + 1])]]
+        parts.append(SampledEpoch(SamplerKind.LADIES, epoch, gi,
+                                  [LayerSample(d + 1, device=x, n=sampler.n)
+                                   for d, x in enumerate(allp[grid.rank(i, 0)])], cfg.layers))
+    return merge_epochs(SamplerKind.LADIES, epoch, batches, parts, cfg.layers)
+
+
 def sage_epoch_15d(sampler: Sage15D, cfg, batches, epoch=0, batch_offset=0, gather=True):
     """Distributed SAGE epoch: grid row i samples group i; with gather=True
     every rank returns the full epoch (groups gathered over the grid column

@@ -27,7 +27,8 @@ def main():
     import paper_2311_02909_b200 as gb
     from paper_2311_02909_b200 import graphgen
     from paper_2311_02909_b200.dist import CommLedger, ProcessGrid, _bounds
-    from paper_2311_02909_b200.dist_exec import Sage15D, fetch_features_nccl, sage_epoch_15d
+    from paper_2311_02909_b200.dist_exec import (Ladies15D, Sage15D, fetch_features_nccl,
+                                                 ladies_epoch_15d, sage_epoch_15d)
 
     dg = graphgen.rmat_device_graph(1 << 14, 200_000, symmetric=True, seed=3)
     G = gb.Graph.from_device(dg)
@@ -48,6 +49,16 @@ def main():
             if rank == 0:
                 print(f"grid ({p},{c}) {mode}: {'PASS' if same else 'FAIL'} stats={s.stats}",
                       flush=True)
+        # LADIES (race) on the grid == single-GPU race sampler
+        lcfg = gb.SamplerConfig.ladies(3, 64, 48, bulk_count=8, seed=4)
+        lser = gb.sample_epoch_bulk(G, lcfg, batches, epoch=1, batch_offset=5, mode="race")
+        ls = Ladies15D(dg, grid, lcfg.fanouts, lcfg.batch_size)
+        lep = ladies_epoch_15d(ls, lcfg, batches, epoch=1, batch_offset=5)
+        same = lser.equals(lep)
+        ok &= same
+        if rank == 0:
+            print(f"grid ({p},{c}) ladies race: {'PASS' if same else 'FAIL'} stats={ls.stats}",
+                  flush=True)
         # features: replicas of the block rows in every grid column
         f = 16
         H = torch.arange(dg.n * f, dtype=torch.float32, device="cuda").view(dg.n, f)
