@@ -539,9 +539,34 @@ def run_15d(args, rank, world, local_rank):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     T = float(t.item())
     value = k * grid.rows * args.steps / (T / 1e3)
+    # LADIES (b = s = 512, L = 3) on the same grid, race sampling
+    from paper_2311_02909_b200.dist_exec import Ladies15D
+    from paper_2311_02909_b200.pipeline import make_batches
+
+    lb = make_batches(np.arange(n), 512, seed=0, epoch=0)[:k * grid.rows]
+    lmine = [np.sort(np.asarray(x)) for x in lb[i * k:(i + 1) * k]]
+    ls = Ladies15D(dg, grid, (512,) * 3, 512)
+    for _ in range(2):
+        ls.sample(lmine, 0, i * k, 0)
+    lt = []
+    for _ in range(max(3, min(args.steps, 10))):
+        dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        ls.sample(lmine, 0, i * k, 0)
+        b.record()
+        torch.cuda.synchronize()
+        lt.append(a.elapsed_time(b))
+    LT = torch.tensor([float(np.sum(lt))], device="cuda", dtype=torch.float64)
+    dist.all_reduce(LT, op=dist.ReduceOp.MAX)
+    ladies_value = k * grid.rows * len(lt) / (float(LT.item()) / 1e3)
     if rank == 0:
         print(json.dumps({
             "metric": METRIC + " [1.5D partitioned graph]", "value": value, "unit": UNIT,
+            "ladies_15d": {"value": ladies_value, "unit": UNIT,
+                           "ms_per_step": float(LT.item()) / len(lt),
+                           "config": "LADIES b=s=512, L=3, k per grid row, race sampling"},
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": T / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
