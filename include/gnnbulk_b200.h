@@ -123,6 +123,14 @@ int gb_sage_layer_sample(const gb_graph* tables, int64_t k, const int64_t* d_bro
                          int64_t batch_offset, uint64_t seed, uint64_t epoch, uint64_t depth,
                          int32_t mode, int32_t* d_fcol, void* d_ws, size_t ws_bytes,
                          void* stream);
+/* owner-computes variant: the block owner samples requested rows (local row
+ * d_rowv[r], degree, explicit global row key d_rowkeys[r]) and writes the
+ * sorted picks at d_fptr[r] — only s ids per row cross NVLink */
+int gb_sage_sample_keyed(const gb_graph* tables, int64_t R, const int64_t* d_R,
+                         const int32_t* d_rowv, const int32_t* d_deg, const int64_t* d_fptr,
+                         const int64_t* d_rowkeys, const int64_t* d_rowptr, const int32_t* d_col,
+                         int32_t s, uint64_t seed, uint64_t epoch, uint64_t depth,
+                         int32_t* d_fcol, void* stream);
 size_t gb_sage_layer_extract_workspace(int64_t n, int64_t k);
 int gb_sage_layer_extract(int64_t n, int64_t k, const int64_t* d_brow, const int64_t* d_fptr,
                           const int32_t* d_fcol, int64_t f_cap, int32_t* d_acol, int32_t* d_colv,

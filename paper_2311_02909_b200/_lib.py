@@ -71,6 +71,8 @@ SIGNATURES = {
     "gb_sage_layer_sample": (ctypes.c_int, [_p, _i64, _p, _i64, _p, _p, _p, _p, _p, _i32, _i64,
                                             _i64, _u64, _u64, _u64, _i32, _p, _p, ctypes.c_size_t,
                                             _p]),
+    "gb_sage_sample_keyed": (ctypes.c_int, [_p, _i64, _p, _p, _p, _p, _p, _p, _p, _i32, _u64, _u64,
+                                            _u64, _p, _p]),
     "gb_sage_layer_extract_workspace": (ctypes.c_size_t, [_i64, _i64]),
     "gb_sage_layer_extract": (ctypes.c_int, [_i64, _i64, _p, _p, _p, _i64, _p, _p, _p, _p, _p, _p,
                                              ctypes.c_size_t, _p]),

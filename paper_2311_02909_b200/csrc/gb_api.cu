@@ -187,6 +187,19 @@ int gb_sage_layer_sample(const gb_graph* tables, int64_t k, const int64_t* d_bro
                            (cudaStream_t)stream);
 }
 
+int gb_sage_sample_keyed(const gb_graph* tables, int64_t R, const int64_t* d_R,
+                         const int32_t* d_rowv, const int32_t* d_deg, const int64_t* d_fptr,
+                         const int64_t* d_rowkeys, const int64_t* d_rowptr, const int32_t* d_col,
+                         int32_t s, uint64_t seed, uint64_t epoch, uint64_t depth,
+                         int32_t* d_fcol, void* stream) {
+  if (!tables || R < 0 || s < 1 || s > 32) {
+    set_error("sage keyed sample: bad arguments");
+    return GB_ERR_CONTRACT;
+  }
+  return sage_sample_keyed(tables, R, d_R, d_rowv, d_deg, d_fptr, d_rowkeys, d_rowptr, d_col, s,
+                           seed, epoch, depth, d_fcol, (cudaStream_t)stream);
+}
+
 size_t gb_sage_layer_extract_workspace(int64_t n, int64_t k) { return sage_layer_extract_ws(n, k); }
 
 int gb_sage_layer_extract(int64_t n, int64_t k, const int64_t* d_brow, const int64_t* d_fptr,

@@ -44,6 +44,10 @@ int sage_layer_sample(const Graph* tables, int64_t k, const int64_t* brow, int64
                       const int64_t* rowptr, const int32_t* col, int32_t s, int64_t stride,
                       int64_t batch_offset, uint64_t seed, uint64_t epoch, uint64_t depth,
                       int32_t mode, int32_t* fcol, void* d_ws, size_t ws_bytes, cudaStream_t st);
+int sage_sample_keyed(const Graph* tables, int64_t R, const int64_t* d_R, const int32_t* rowv,
+                      const int32_t* deg, const int64_t* fptr, const int64_t* rowkeys,
+                      const int64_t* rowptr, const int32_t* col, int32_t s, uint64_t seed,
+                      uint64_t epoch, uint64_t depth, int32_t* fcol, cudaStream_t st);
 size_t sage_layer_extract_ws(int64_t n, int64_t k);
 int sage_layer_extract(int64_t n, int64_t k, const int64_t* brow, const int64_t* fptr,
                        const int32_t* fcol, int64_t f_cap, int32_t* acol, int32_t* colv,

@@ -167,6 +167,7 @@ struct SageArgs {
   const int32_t* run_n;
   const int8_t* run_lower;
   const int32_t* rowv;
+  const int64_t* rowkeys;  // optional explicit global row keys (owner-computes 1.5D)
   const int32_t* deg;
   const int64_t* fptr;
   const int64_t* gstart;
@@ -266,7 +267,8 @@ __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
                                                           const int64_t* __restrict__ R_ptr) {
   __shared__ int64_t s_brow[kBrowSmem];
   const int64_t R = *R_ptr;
-  const bool brow_in_smem = A.k + 1 <= kBrowSmem;
+  const bool keyed = A.rowkeys != nullptr;  // explicit keys: no batch structure
+  const bool brow_in_smem = !keyed && A.k + 1 <= kBrowSmem;
   if (brow_in_smem)
     for (int64_t i = threadIdx.x; i <= A.k; i += blockDim.x) s_brow[i] = A.brow[i];
   __syncthreads();
@@ -276,14 +278,19 @@ __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
     if (deg == 0) continue;  // empty P row (sample_rows_ordered, sampler.py:202-204)
     const int32_t take = min(deg, A.s);
     const int64_t fp = A.fptr[r];
-    const int64_t bb = batch_of(s_brow, A.brow, A.k, r);
+    const int64_t bb = keyed ? 0 : batch_of(s_brow, A.brow, A.k, r);
     int32_t sorted[MAXF];
 #pragma unroll
     for (int q = 0; q < MAXF; ++q) sorted[q] = q;  // exhaustion: every index (sampler.py:172-174)
     if (take < deg) {
-      const int64_t b0 = brow_in_smem ? s_brow[bb] : A.brow[bb];
-      // global_row_keys (sampler.py:309-322)
-      const uint64_t key = (uint64_t)((A.batch_offset + bb) * A.stride + (r - b0));
+      // global_row_keys (sampler.py:309-322), or the requester's keys
+      uint64_t key;
+      if (keyed) {
+        key = (uint64_t)A.rowkeys[r];
+      } else {
+        const int64_t b0 = brow_in_smem ? s_brow[bb] : A.brow[bb];
+        key = (uint64_t)((A.batch_offset + bb) * A.stride + (r - b0));
+      }
       const int32_t slot = __ldg(A.deg_slot + deg);
       GTable tab;
       tab.j0 = A.run_j0 + (int64_t)slot * (kMaxRuns + 1);
@@ -840,6 +847,27 @@ int sage_layer_sample(const Graph* tables, int64_t k, const int64_t* brow, int64
     count_launches(1);
   }
   GB_LAUNCH_CHECK("sage_layer_sample");
+  return GB_OK;
+}
+
+// Owner-computes sampling (1.5D): rows given by (local row, degree, global
+// row key, output offset) — the block owner samples requested rows with the
+// requester's keys and returns only the picks.  P-free gather.
+int sage_sample_keyed(const Graph* tables, int64_t R, const int64_t* d_R, const int32_t* rowv,
+                      const int32_t* deg, const int64_t* fptr, const int64_t* rowkeys,
+                      const int64_t* rowptr, const int32_t* col, int32_t s, uint64_t seed,
+                      uint64_t epoch, uint64_t depth, int32_t* fcol, cudaStream_t st) {
+  if (R == 0) return GB_OK;
+  SageArgs A{};
+  A.rowptr = rowptr; A.col = col;
+  A.deg_slot = tables->deg_slot; A.run_j0 = tables->run_j0; A.run_s0 = tables->run_s0;
+  A.run_d = tables->run_d; A.run_n = tables->run_n; A.run_lower = tables->run_lower;
+  A.rowv = rowv; A.rowkeys = rowkeys; A.deg = deg; A.fptr = fptr;
+  A.k = 0; A.s = s; A.seed = seed; A.epoch = epoch; A.depth = depth;
+  A.bitmap = nullptr; A.fcol = fcol;
+  launch_pick<true>(grid_for(R, kPickThreads, 64 * kNumSMs), A, d_R, st);
+  GB_LAUNCH_CHECK("sage_sample_keyed");
+  count_launches(1);
   return GB_OK;
 }
 

@@ -95,7 +95,7 @@ class Sage15D:
     """
 
     def __init__(self, full, grid: ProcessGrid, fanouts, batch_size, mode="pfree",
-                 ledger=None):
+                 ledger=None, fetch="rows"):
         import torch.distributed as dist
 
         torch = _torch()
@@ -103,6 +103,9 @@ class Sage15D:
             raise ContractViolation("Sage15D needs torch.distributed with world_size == grid.p")
         self.grid, self.fanouts, self.b = grid, tuple(int(s) for s in fanouts), int(batch_size)
         self.mode, self.ledger = mode, ledger
+        if fetch not in ("rows", "owner"):
+            raise ContractViolation(f"unknown fetch mode {fetch!r}")
+        self.fetch = fetch  # "rows": Alg. 2 row fetch; "owner": owner samples, returns picks
         self.rank = dist.get_rank()
         self.i, self.j = grid.coords(self.rank)
         self.n = full.n
@@ -175,6 +178,69 @@ class Sage15D:
             lcol[:nnz] = torch.cat(replies)
         return lrowptr, lcol
 
+    # -- step 1+2, owner-computes variant ------------------------------------------------
+    def owner_sample(self, rv, mine, deg, fptr, brow, k, stride, batch_offset, s, seed, epoch,
+                     depth, fcol):
+        """Ship (vertex, global row key) of every row in block k to its owner,
+        which samples it from its local A rows with the same keyed replay
+        (gb_sage_sample_keyed) and returns only the sorted picks."""
+        torch = _torch()
+        L = _lib.lib()
+        grid, st, dev = self.grid, self.grid.stages, self.dev
+        R = rv.numel()
+        ridx = torch.arange(R, device=dev)
+        b = torch.searchsorted(brow, ridx, right=True) - 1
+        keys = (batch_offset + b) * stride + (ridx - brow[b])
+        take_all = torch.minimum(deg.long(), torch.full_like(deg, s).long())
+        for q in range(st):
+            kblk = self.j * st + q
+            owner = grid.rank(kblk, self.j)
+            lo, hi = int(self.bounds[kblk]), int(self.bounds[kblk + 1])
+            sel = torch.nonzero(mine & (rv >= lo) & (rv < hi) & (deg > 0)).flatten()
+            req = torch.stack([rv[sel].long(), keys[sel]], 1).flatten().contiguous()
+            counts = exchange_counts({owner: req}, self.col_ranks, dev)
+            reqs = exchange({owner: req}, {p: counts[p] for p in self.col_ranks
+                                           if self.rank == owner or p == self.rank},
+                            self.col_ranks, torch.int64, dev)
+            replies = {}
+            if self.rank == owner:
+                for p in self.col_ranks:
+                    r = reqs.get(p)
+                    if r is None or r.numel() == 0:
+                        continue
+                    r = r.view(-1, 2)
+                    v = r[:, 0]
+                    d = self.gdeg[v].contiguous()
+                    tk = torch.minimum(d.long(), torch.full_like(d, s).long())
+                    fp = torch.zeros(v.numel() + 1, dtype=torch.int64, device=dev)
+                    fp[1:] = torch.cumsum(tk, 0)
+                    out = torch.empty(max(int(fp[-1].item()), 1), dtype=torch.int32, device=dev)
+                    lrow = (v - self.row0).to(torch.int32).contiguous()
+                    kk = r[:, 1].contiguous()
+                    dR = torch.tensor([v.numel()], dtype=torch.int64, device=dev)
+                    _lib.check(L.gb_sage_sample_keyed(
+                        self.tables.handle, v.numel(), _lib.ptr(dR), _lib.ptr(lrow), _lib.ptr(d),
+                        _lib.ptr(fp), _lib.ptr(kk), _lib.ptr(self.brp), _lib.ptr(self.bcol), s,
+                        seed, epoch, depth, _lib.ptr(out), _lib.stream_ptr()),
+                        "gb_sage_sample_keyed")
+                    replies[p] = out[: int(fp[-1].item())]
+                    if self.ledger is not None and p != self.rank:
+                        self.ledger.charge(self.rank, "row-data", 1, replies[p].numel())
+            tsel = take_all[sel]
+            want = int(tsel.sum().item()) if sel.numel() else 0
+            if owner != self.rank:
+                self.stats["fetch_ids"] += sel.numel()
+                self.stats["fetch_words"] += want + 2 * sel.numel()
+                if self.ledger is not None and sel.numel():
+                    self.ledger.charge(self.rank, "gather-cols", 1, 2 * sel.numel())
+            got = exchange(replies, {owner: want}, self.col_ranks, torch.int32, dev)
+            if want:
+                picks = got[owner]
+                base = torch.repeat_interleave(fptr[sel], tsel)
+                excl = torch.cumsum(tsel, 0) - tsel
+                pos = base + torch.arange(want, device=dev) - torch.repeat_interleave(excl, tsel)
+                fcol[pos] = picks
+
     # -- one bulk --------------------------------------------------------------------------
     def sample(self, group_batches, epoch, batch_offset, seed):
         """Sample this grid row's group; returns (device layer dicts, sizes)."""
@@ -206,20 +272,24 @@ class Sage15D:
                        "gb_take_scan")
             F = int(fptr[R].item())
             mine = (rv >= self.V0) & (rv < self.V1)
-            U = torch.unique(rv[mine])
-            lrowptr, lcol = self.fetch_rows(U)
-            lrow = torch.searchsorted(U, rv).to(torch.int32)
-            deg_mine = torch.where(mine, deg, torch.zeros_like(deg)).contiguous()
             fcol = torch.zeros(max(F, 1), dtype=torch.int32, device=self.dev)
-            ws = torch.empty(max(L.gb_sage_layer_sample_workspace(max(R, 1), max(R, 1) * s), 1),
-                             dtype=torch.uint8, device=self.dev)
-            mode = _lib.GB_SAGE_STREAM if self.mode == "stream" else _lib.GB_SAGE_PFREE
-            if R:
-                _lib.check(L.gb_sage_layer_sample(
-                    self.tables.handle, k, _lib.ptr(brow), R, _lib.ptr(lrow), _lib.ptr(deg_mine),
-                    _lib.ptr(fptr), _lib.ptr(lrowptr), _lib.ptr(lcol), s, stride, batch_offset,
-                    seed, epoch, l + 1, mode, _lib.ptr(fcol), _lib.ptr(ws), ws.numel(),
-                    _lib.stream_ptr()), "gb_sage_layer_sample")
+            if self.fetch == "owner":
+                self.owner_sample(rv, mine, deg, fptr, brow, k, stride, batch_offset, s, seed,
+                                  epoch, l + 1, fcol)
+            else:
+                U = torch.unique(rv[mine])
+                lrowptr, lcol = self.fetch_rows(U)
+                lrow = torch.searchsorted(U, rv).to(torch.int32)
+                deg_mine = torch.where(mine, deg, torch.zeros_like(deg)).contiguous()
+                ws = torch.empty(max(L.gb_sage_layer_sample_workspace(max(R, 1), max(R, 1) * s),
+                                     1), dtype=torch.uint8, device=self.dev)
+                mode = _lib.GB_SAGE_STREAM if self.mode == "stream" else _lib.GB_SAGE_PFREE
+                if R:
+                    _lib.check(L.gb_sage_layer_sample(
+                        self.tables.handle, k, _lib.ptr(brow), R, _lib.ptr(lrow),
+                        _lib.ptr(deg_mine), _lib.ptr(fptr), _lib.ptr(lrowptr), _lib.ptr(lcol), s,
+                        stride, batch_offset, seed, epoch, l + 1, mode, _lib.ptr(fcol),
+                        _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "gb_sage_layer_sample")
             # step 2: sample-then-reduce inside the grid row
             if self.grid.c > 1 and F:
                 dist.all_reduce(fcol[:F], op=dist.ReduceOp.SUM,

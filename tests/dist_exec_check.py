@@ -40,15 +40,15 @@ def main():
     grids = [(world, c) for c in (1, 2) if world % c == 0 and c * c <= world and world % (c * c) == 0]
     for p, c in grids:
         grid = ProcessGrid(p, c)
-        for mode in ("pfree", "stream"):
+        for mode, fetch in (("pfree", "rows"), ("stream", "rows"), ("pfree", "owner")):
             led = CommLedger(p)
-            s = Sage15D(dg, grid, cfg.fanouts, cfg.batch_size, mode=mode, ledger=led)
+            s = Sage15D(dg, grid, cfg.fanouts, cfg.batch_size, mode=mode, ledger=led, fetch=fetch)
             ep = sage_epoch_15d(s, cfg, batches, epoch=1, batch_offset=5)
             same = serial.equals(ep)
             ok &= same
             if rank == 0:
-                print(f"grid ({p},{c}) {mode}: {'PASS' if same else 'FAIL'} stats={s.stats}",
-                      flush=True)
+                print(f"grid ({p},{c}) {mode}/{fetch}: {'PASS' if same else 'FAIL'} "
+                      f"stats={s.stats}", flush=True)
         # LADIES (race) on the grid == single-GPU race sampler
         lcfg = gb.SamplerConfig.ladies(3, 64, 48, bulk_count=8, seed=4)
         lser = gb.sample_epoch_bulk(G, lcfg, batches, epoch=1, batch_offset=5, mode="race")
