@@ -54,6 +54,8 @@ def parse():
     p.add_argument("--dist", default="replicated", choices=["replicated", "15d"],
                    help="multi-GPU mode: replicated graph (cfg4) or 1.5D partitioned (cfg5)")
     p.add_argument("--c", type=int, default=2, help="1.5D replication factor")
+    p.add_argument("--fetch", default="owner", choices=["rows", "owner"],
+                   help="1.5D SAGE: Alg. 2 row fetch, or owner-computes (ship row keys)")
     return p.parse_args()
 
 
@@ -517,7 +519,7 @@ def run_15d(args, rank, world, local_rank):
     dg = graphgen.rmat_device_graph(n, m, symmetric=sym, seed=0)
     k = args.k or default_k(args.workload)
     allb = make_batches_for(n, k * grid.rows)
-    s = Sage15D(dg, grid, FANOUTS, BATCH, mode=args.mode)
+    s = Sage15D(dg, grid, FANOUTS, BATCH, mode=args.mode, fetch=args.fetch)
     i = s.i
     mine = [np.asarray(x) for x in allb[i * k:(i + 1) * k]]
     for _ in range(max(args.warmup, 3)):
@@ -573,7 +575,7 @@ def run_15d(args, rank, world, local_rank):
             "config": {"workload": f"{args.workload}-shape R-MAT, GraphSAGE (15,10,5), "
                                    f"b=1024, k={k} per grid row",
                        "parallelism": f"1.5D grid {grid.rows}x{grid.c} (p={world}, c={grid.c})",
-                       "mode": args.mode},
+                       "mode": args.mode, "fetch": args.fetch},
             "traffic_rank0": {k2: int(v) for k2, v in s.stats.items()},
         }), flush=True)
 
