@@ -40,6 +40,9 @@ extern "C" {
 /* SAGE sample-kernel modes (identical outputs) */
 #define GB_SAGE_STREAM 0 /* Alg. 1: P row formed on chip by streaming A rows */
 #define GB_SAGE_PFREE 1  /* P-free fast path: read only the picked entries  */
+#define GB_SAGE_DEDUP 2  /* Alg. 1 with duplicate-row elimination: every
+                            distinct P row formed on chip once, serving the
+                            picks of all frontier rows that reference it */
 
 const char* gb_last_error(void);
 int gb_version(void);

@@ -22,6 +22,7 @@ GB_ERR_UNSUPPORTED = -4
 GB_COL_PAD = 4
 GB_SAGE_STREAM = 0
 GB_SAGE_PFREE = 1
+GB_SAGE_DEDUP = 2
 
 _i64, _u64, _i32, _p = ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32, ctypes.c_void_p
 

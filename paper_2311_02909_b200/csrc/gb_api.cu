@@ -160,7 +160,7 @@ int gb_sage_bulk(const gb_graph* g, int64_t k, const int64_t* d_bptr, const int3
       set_error("sage bulk: fanout %lld outside [1, 32]", (long long)h_fanouts[l]);
       return h_fanouts[l] < 1 ? GB_ERR_CONTRACT : GB_ERR_UNSUPPORTED;
     }
-  if (mode != GB_SAGE_STREAM && mode != GB_SAGE_PFREE) {
+  if (mode != GB_SAGE_STREAM && mode != GB_SAGE_PFREE && mode != GB_SAGE_DEDUP) {
     set_error("sage bulk: unknown mode %d", mode);
     return GB_ERR_CONTRACT;
   }

@@ -459,6 +459,156 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k_sage_stream(SageArgs A,
   }
 }
 
+// ============================================ deduplicated P rows (GB_SAGE_DEDUP)
+// Frontier rows repeat vertices heavily (hub bias: 3.5M rows over 0.55M
+// distinct vertices in layer 3 at products scale), and identical rows of
+// Q^l give identical rows of P = Q^l A.  Each distinct P row is formed on
+// chip once — the A row streamed through shared memory — and serves the
+// picks of every frontier row that references it.
+
+// one bit per vertex that some row of the layer references
+__global__ void k_dd_mark(const int64_t* __restrict__ R_ptr, const int32_t* __restrict__ rowv,
+                          const int32_t* __restrict__ deg, uint32_t* __restrict__ vbits) {
+  const int64_t R = *R_ptr;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
+       r += (int64_t)gridDim.x * blockDim.x)
+    if (deg[r] > 0) {
+      const int32_t v = rowv[r];
+      atomicOr(vbits + (v >> 5), 1u << (v & 31));
+    }
+}
+
+__device__ __forceinline__ int32_t vrank(const uint32_t* vbits, const int32_t* vpre, int32_t v) {
+  return vpre[v >> 5] + __popc(vbits[v >> 5] & ((1u << (v & 31)) - 1u));
+}
+
+// distinct vertex list (ascending) and its degrees
+__global__ void k_dd_list(int64_t nwords, const uint32_t* __restrict__ vbits,
+                          const int32_t* __restrict__ vpre, const int64_t* __restrict__ rowptr,
+                          int32_t* __restrict__ dv) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nwords;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t x = vbits[i];
+    int32_t o = vpre[i];
+    while (x) {
+      const int bit = __ffs(x) - 1;
+      dv[o++] = (int32_t)(i * 32 + bit);
+      x &= x - 1;
+    }
+  }
+}
+
+// picks per distinct vertex
+__global__ void k_dd_count(const int64_t* __restrict__ R_ptr, const int32_t* __restrict__ rowv,
+                           const int32_t* __restrict__ deg, int32_t s,
+                           const uint32_t* __restrict__ vbits, const int32_t* __restrict__ vpre,
+                           int32_t* __restrict__ gcnt) {
+  const int64_t R = *R_ptr;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t d = deg[r];
+    if (d > 0) atomicAdd(gcnt + vrank(vbits, vpre, rowv[r]), min(d, s));
+  }
+}
+
+struct GcntF {
+  const int32_t* c;
+  __device__ int64_t operator()(int64_t i) const { return c[i]; }
+};
+
+// pick records of every row into its vertex group: (row-relative index,
+// frontier position), packed as idx << 32 | pos
+__global__ void k_dd_scatter(const int64_t* __restrict__ R_ptr, const int32_t* __restrict__ rowv,
+                             const int32_t* __restrict__ deg, int32_t s,
+                             const int64_t* __restrict__ fptr, const int32_t* __restrict__ pidx,
+                             const uint32_t* __restrict__ vbits, const int32_t* __restrict__ vpre,
+                             const int64_t* __restrict__ goff, int32_t* __restrict__ gcur,
+                             uint64_t* __restrict__ pk) {
+  const int64_t R = *R_ptr;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t d = deg[r];
+    if (d <= 0) continue;
+    const int32_t take = min(d, s);
+    const int32_t g = vrank(vbits, vpre, rowv[r]);
+    const int64_t base = goff[g] + atomicAdd(gcur + g, take);
+    const int64_t fp = fptr[r];
+    for (int t = 0; t < take; ++t)
+      pk[base + t] = ((uint64_t)(uint32_t)pidx[fp + t] << 32) | (uint64_t)(fp + t);
+  }
+}
+
+constexpr int kDdWarpChunk = 1024;  // entries staged per warp (small groups)
+constexpr int kDdCtaChunk = 8192;   // entries staged per CTA (large groups)
+constexpr int kDdThreads = 256;
+
+__device__ __forceinline__ void dd_emit(int32_t c, uint64_t rec, const int64_t* eo, int64_t k,
+                                        int32_t* fcol, uint32_t* bitmap, int64_t nwords) {
+  const int64_t pos = (int64_t)(rec & 0xffffffffu);
+  fcol[pos] = c;
+  int64_t lo = 0, hi = k;  // batch of the frontier position
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (eo[mid] <= pos) lo = mid; else hi = mid;
+  }
+  atomicOr(bitmap + lo * nwords + (c >> 5), 1u << (c & 31));
+}
+
+// Stream every distinct A row once and serve its picks.  LARGE = false:
+// one warp per group of degree <= kDdWarpChunk; LARGE = true: one CTA per
+// larger group, kDdCtaChunk entries staged per step.
+template <bool LARGE>
+__global__ void __launch_bounds__(kDdThreads) k_dd_stream(
+    const int64_t* __restrict__ D_ptr, const int32_t* __restrict__ dv,
+    const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+    const int64_t* __restrict__ goff, const uint64_t* __restrict__ pk,
+    const int64_t* __restrict__ eoff, int64_t k, int32_t* __restrict__ fcol,
+    uint32_t* __restrict__ bitmap, int64_t nwords) {
+  constexpr int kChunk = LARGE ? kDdCtaChunk : kDdWarpChunk;
+  constexpr int kSlots = LARGE ? 1 : kDdThreads / 32;
+  __shared__ __align__(16) int32_t sbuf[kSlots][kChunk + 4];
+  __shared__ int64_t s_eoff[kBrowSmem];
+  const bool esm = k + 1 <= kBrowSmem;
+  if (esm)
+    for (int64_t i = threadIdx.x; i <= k; i += blockDim.x) s_eoff[i] = eoff[i];
+  __syncthreads();
+  const int64_t* eo = esm ? s_eoff : eoff;
+  const int64_t D = *D_ptr;
+  const int lane = lane_id();
+  const int tid = LARGE ? threadIdx.x : lane;
+  const int nthr = LARGE ? blockDim.x : 32;
+  int32_t* buf = sbuf[LARGE ? 0 : (threadIdx.x >> 5)];
+  const int64_t first = LARGE ? blockIdx.x : global_warp();
+  const int64_t step = LARGE ? gridDim.x : grid_warps();
+  for (int64_t g = first; g < D; g += step) {
+    const int32_t v = dv[g];
+    const int64_t a0 = rowptr[v], d = rowptr[v + 1] - a0;
+    if ((d > kDdWarpChunk) != LARGE) continue;
+    const int64_t p0 = goff[g], p1 = goff[g + 1];
+    for (int64_t c0 = 0; c0 < d; c0 += kChunk) {
+      const int64_t c1 = min(c0 + (int64_t)kChunk, d);
+      // stage entries [c0, c1) of A row v (16-B aligned vector loads)
+      const int64_t e0 = a0 + c0, e1 = a0 + c1;
+      const int64_t al0 = e0 & ~3LL;
+      for (int64_t e = al0 + 4 * tid; e < e1; e += 4 * nthr) {
+        const int4 x = ld_stream_v4(col + e);
+        const int64_t o = e - e0;  // may be -3..-1 for the aligned head
+        if (o + 0 >= 0 && e + 0 < e1) buf[o + 0] = x.x;
+        if (o + 1 >= 0 && e + 1 < e1) buf[o + 1] = x.y;
+        if (o + 2 >= 0 && e + 2 < e1) buf[o + 2] = x.z;
+        if (o + 3 >= 0 && e + 3 < e1) buf[o + 3] = x.w;
+      }
+      if (LARGE) __syncthreads(); else __syncwarp();
+      for (int64_t p = p0 + tid; p < p1; p += nthr) {
+        const uint64_t rec = pk[p];
+        const int64_t idx = (int64_t)(rec >> 32);
+        if (idx >= c0 && idx < c1) dd_emit(buf[idx - c0], rec, eo, k, fcol, bitmap, nwords);
+      }
+      if (LARGE) __syncthreads(); else __syncwarp();
+    }
+  }
+}
+
 // ============================================================== extraction
 
 struct PopF {
@@ -619,6 +769,15 @@ struct SageWs {
   uint32_t* bitmap;
   int32_t* wpre;
   int64_t* d_W;
+  // dedup mode
+  uint32_t* vbits;   // one bit per vertex
+  int32_t* vpre;     // popcount prefix of vbits
+  int64_t* d_nw;     // device scalars: nwords, D
+  int32_t* dv;       // distinct vertices
+  int32_t* gcnt;     // picks per distinct vertex
+  int32_t* gcur;
+  int64_t* goff;
+  uint64_t* pk;      // pick records grouped by vertex
   size_t bytes;
 };
 
@@ -629,7 +788,8 @@ static SageWs sage_ws_layout(char* base, int64_t k, int64_t n, int64_t r_cap_max
   SageWs w{};
   const int64_t nwords = (n + 31) / 32;
   const int64_t W = k * nwords;
-  const int64_t scan_n = r_cap_max > W ? r_cap_max : W;
+  int64_t scan_n = r_cap_max > W ? r_cap_max : W;
+  if (nwords > scan_n) scan_n = nwords;
   size_t off = 0;
   auto take = [&](size_t bytes) { char* p = base ? base + off : nullptr; off += align_up(bytes); return p; };
   w.pidx = (int32_t*)take(sizeof(int32_t) * (f_cap_max + 1));
@@ -639,8 +799,72 @@ static SageWs sage_ws_layout(char* base, int64_t k, int64_t n, int64_t r_cap_max
   w.bitmap = (uint32_t*)take(sizeof(uint32_t) * (W + 1));
   w.wpre = (int32_t*)take(sizeof(int32_t) * (W + 1));
   w.d_W = (int64_t*)take(sizeof(int64_t));
+  w.vbits = (uint32_t*)take(sizeof(uint32_t) * (nwords + 1));
+  w.vpre = (int32_t*)take(sizeof(int32_t) * (nwords + 1));
+  w.d_nw = (int64_t*)take(sizeof(int64_t) * 2);
+  w.dv = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
+  w.gcnt = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
+  w.gcur = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
+  w.goff = (int64_t*)take(sizeof(int64_t) * (r_cap_max + 1));
+  w.pk = (uint64_t*)take(sizeof(uint64_t) * (f_cap_max + 1));
   w.bytes = off;
   return w;
+}
+
+__global__ void k_sage_eoff(const int64_t* __restrict__ brow, int64_t k,
+                            const int64_t* __restrict__ fptr, int64_t* __restrict__ eoff);
+
+template <typename K>
+static int persistent_grid(K kernel, int threads);
+
+__global__ void k_i32_to_i64(const int32_t* __restrict__ src, int64_t* __restrict__ dst) {
+  *dst = *src;
+}
+
+struct VPopF {
+  const uint32_t* b;
+  __device__ int64_t operator()(int64_t i) const { return __popc(b[i]); }
+};
+
+// Dedup stream step of one layer (pidx from k_sage_pick<false> in place).
+static int dedup_stream(const Graph* g, SageWs& ws, const int64_t* R_ptr, const int32_t* rowv,
+                        const int64_t* brow, int64_t k, int32_t s, int64_t r_cap,
+                        gb_sage_layer_out& o, int64_t nwords, cudaStream_t st) {
+  const int64_t gw = 16 * kNumSMs;
+  GB_CUDA(cudaMemsetAsync(ws.vbits, 0, sizeof(uint32_t) * (nwords + 1), st));
+  GB_CUDA(cudaMemsetAsync(ws.gcnt, 0, sizeof(int32_t) * (r_cap + 1), st));
+  GB_CUDA(cudaMemsetAsync(ws.gcur, 0, sizeof(int32_t) * (r_cap + 1), st));
+  k_sage_eoff<<<grid_for(k + 1, 128, 64), 128, 0, st>>>(brow, k, o.fptr, o.eoff);
+  k_dd_mark<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, ws.vbits);
+  int rc = device_exclusive_scan<int64_t>(ws.d_nw, nwords, VPopF{ws.vbits}, ws.vpre, ws.scan_ws,
+                                          st);
+  if (rc) return rc;
+  k_i32_to_i64<<<1, 1, 0, st>>>(ws.vpre + nwords, ws.d_nw + 1);
+  k_dd_list<<<grid_for(nwords, 256, gw), 256, 0, st>>>(nwords, ws.vbits, ws.vpre, g->rowptr, ws.dv);
+  k_dd_count<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, s, ws.vbits, ws.vpre,
+                                                      ws.gcnt);
+  rc = device_exclusive_scan<int64_t>(ws.d_nw + 1, r_cap, GcntF{ws.gcnt}, ws.goff, ws.scan_ws, st);
+  if (rc) return rc;
+  k_dd_scatter<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, s, o.fptr, ws.pidx,
+                                                        ws.vbits, ws.vpre, ws.goff, ws.gcur,
+                                                        ws.pk);
+  GB_LAUNCH_CHECK("dedup prepare");
+  static int grid_small = 0, grid_large = 0;
+  if (!grid_small) {
+    grid_small = persistent_grid(k_dd_stream<false>, kDdThreads);
+    grid_large = persistent_grid(k_dd_stream<true>, kDdThreads);
+  }
+  prof_mark(st);
+  k_dd_stream<false><<<grid_small, kDdThreads, 0, st>>>(ws.d_nw + 1, ws.dv, g->rowptr, g->col,
+                                                       ws.goff, ws.pk, o.eoff, k, o.fcol,
+                                                       ws.bitmap, nwords);
+  k_dd_stream<true><<<grid_large, kDdThreads, 0, st>>>(ws.d_nw + 1, ws.dv, g->rowptr, g->col,
+                                                      ws.goff, ws.pk, o.eoff, k, o.fcol,
+                                                      ws.bitmap, nwords);
+  prof_mark(st);
+  GB_LAUNCH_CHECK("k_dd_stream");
+  count_launches(11);
+  return GB_OK;
 }
 
 static int64_t sage_rcap_max(int64_t r1_cap, int32_t layers, const int64_t* fanouts) {
@@ -688,6 +912,7 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
               gb_sage_layer_out* L, int64_t* d_sizes, void* d_ws, size_t ws_bytes,
               cudaStream_t st) {
   const bool stream = mode == GB_SAGE_STREAM;
+  const bool dedup = mode == GB_SAGE_DEDUP;
   const int64_t nwords = (g->n + 31) / 32;
   const int64_t W = k * nwords;
   const int64_t rmax = sage_rcap_max(r1_cap, layers, fanouts);
@@ -712,7 +937,8 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
   }
   GB_CUDA(cudaMemsetAsync(ws.bitmap, 0, sizeof(uint32_t) * (W + 1), st));
   k_set_i64<<<1, 1, 0, st>>>(ws.d_W, W);
-  count_launches(1);
+  k_set_i64<<<1, 1, 0, st>>>(ws.d_nw, nwords);
+  count_launches(2);
   int64_t stride = batch_size;
   r_cap = r1_cap;
   for (int32_t l = 0; l < layers; ++l) {
@@ -741,7 +967,7 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     A.bitmap = ws.bitmap; A.nwords = nwords; A.fcol = o.fcol; A.pidx = ws.pidx;
     const int pick_grid = grid_for(r_cap, kPickThreads, 64 * kNumSMs);
     prof_mark(st);
-    if (stream)
+    if (stream || dedup)
       launch_pick<false>(pick_grid, A, R_ptr, st);
     else
       launch_pick<true>(pick_grid, A, R_ptr, st);
@@ -753,6 +979,10 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
       GB_LAUNCH_CHECK("k_sage_stream");
       prof_mark(st);
       count_launches(1);
+    }
+    if (dedup) {
+      rc = dedup_stream(g, ws, R_ptr, rowv, brow, k, s, r_cap, o, nwords, st);
+      if (rc) return rc;
     }
     rc = device_exclusive_scan<int64_t>(ws.d_W, W, PopF{ws.bitmap}, ws.wpre, ws.scan_ws, st);
     if (rc) return rc;

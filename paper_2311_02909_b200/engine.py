@@ -19,7 +19,8 @@ from .errors import ContractViolation
 from .sampler import LayerSample, SampledEpoch, SamplerConfig, SamplerKind, _flatten_batches
 from .sparse import Graph
 
-MODES = {"stream": _lib.GB_SAGE_STREAM, "pfree": _lib.GB_SAGE_PFREE}
+MODES = {"stream": _lib.GB_SAGE_STREAM, "pfree": _lib.GB_SAGE_PFREE,
+         "dedup": _lib.GB_SAGE_DEDUP}
 
 
 def sage_caps(r1_cap, fanouts):

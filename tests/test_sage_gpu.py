@@ -15,7 +15,7 @@ from oracle.philox import uniforms as np_uniforms
 
 pytestmark = pytest.mark.gpu
 
-MODES = ("stream", "pfree")
+MODES = ("stream", "pfree", "dedup")
 
 
 def _pkg():
