@@ -46,7 +46,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--workload", default="products", choices=["products", "cfg1", "papers"])
     p.add_argument("--k", type=int, default=None, help="minibatches per bulk per GPU")
-    p.add_argument("--mode", default="stream", choices=["stream", "pfree"])
+    p.add_argument("--mode", default="dedup", choices=["dedup", "stream", "pfree"])
     p.add_argument("--cpu-seconds", type=float, default=15.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-pfree", action="store_true")
@@ -131,8 +131,10 @@ def layer_stats(bulk, dg, sizes):
         else:
             rv = bulk.out[l - 1]["fcol"][:R].long()
         G = int((dg.rowptr[rv + 1] - dg.rowptr[rv]).sum().item()) if R else 0
-        out.append({"R": R, "G": G, "F": F, "U": U})
-        del rv
+        uv = torch.unique(rv) if R else rv
+        Gd = int((dg.rowptr[uv + 1] - dg.rowptr[uv]).sum().item()) if R else 0
+        out.append({"R": R, "G": G, "F": F, "U": U, "D": int(uv.numel()), "G_distinct": Gd})
+        del rv, uv
     del rowv
     torch.cuda.synchronize()
     return out
@@ -153,6 +155,10 @@ def kernel_bytes(s, kernel):
                                    row, col read 4 + write 4 per pick."""
     if kernel == "stream":
         return 32 * s["R"] + 4 * s["G"] + 8 * s["F"]
+    if kernel == "dedup":
+        # k_dd_stream: per distinct row vertex 4 + row_ptr 8 + offsets 8, 4 per
+        # entry of every DISTINCT row, pick record 8 + col 4 + batch bit 4
+        return 20 * s["D"] + 4 * s["G_distinct"] + 16 * s["F"]
     if kernel == "pick":
         return 12 * s["R"] + 4 * s["F"]
     return 24 * s["R"] + 8 * s["F"]
@@ -382,7 +388,7 @@ def run_ours(args, rank, world, local_rank):
         clocks = clk.stop()
         step_ms = [a.elapsed_time(b) for a, b in evs]
         # sample-kernel durations (events around each launch, same stream)
-        ppl = 2 if mode == "stream" else 1
+        ppl = 1 if mode == "pfree" else 2
         cap = ppl * len(FANOUTS) * 4
         lib.gb_profile_begin(2 * cap)
         for i in range(4):
@@ -406,8 +412,8 @@ def run_ours(args, rank, world, local_rank):
     peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(REPO, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    dom = "stream" if args.mode == "stream" else "pfree"
-    kb = [kernel_bytes(s, dom) for s in st]
+    KERNEL = {"stream": "k_sage_stream", "dedup": "k_dd_stream", "pfree": "k_sage_pick<true>"}
+    kb = [kernel_bytes(s, args.mode) for s in st]
     kern_avg = kern_ms.mean(axis=0)[:, -1]  # dominant kernel, per layer
     pick_avg = kern_ms.mean(axis=0)[:, 0]
     achieved = sum(kb) / (kern_avg.sum() / 1e3) / 1e9
@@ -415,8 +421,7 @@ def run_ours(args, rank, world, local_rank):
     traffic = None
     tpath = os.path.join(REPO, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath) and args.workload == "products" and k == 64:
-        tk = json.load(open(tpath)).get(dom_kernel := ("k_sage_stream" if args.mode == "stream"
-                                                       else "k_sage_pick<true>"))
+        tk = json.load(open(tpath)).get(KERNEL[args.mode])
         traffic = tk["bulk_bytes"] if tk else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -441,29 +446,32 @@ def run_ours(args, rank, world, local_rank):
             "traffic_note": "dram__bytes_read+write summed over the 3 layer launches of one bulk "
                             "(ncu --set full, profiles/ncu_traffic.json); achieved/per_layer_bytes "
                             "aggregate the same 3 launches",
-            "kernel": "k_sage_stream" if args.mode == "stream" else "k_sage_pick<true>",
+            "kernel": KERNEL[args.mode],
             "pick_kernel_ms": [round(x, 4) for x in pick_avg.tolist()],
             "per_layer_ms": [round(x, 4) for x in kern_avg.tolist()],
             "per_layer_bytes": kb, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)",
             "kernel_share_of_step": float(kern_avg.sum() / (total_ms / args.steps)),
         },
     }
-    # P-free exact fast path, same workload
-    if not args.no_pfree and args.mode == "stream":
-        b2, sm2, _, km2, sz2, lpb2, g2 = measure("pfree")
+    # the other SAGE kernel modes on the same workload (identical outputs)
+    for other in ("stream", "pfree") if not args.no_pfree else ():
+        if other == args.mode:
+            continue
+        b2, sm2, _, km2, sz2, lpb2, g2 = measure(other)
         t2 = float(np.sum(sm2))
         if world > 1:
             t = torch.tensor([t2], device=dev, dtype=torch.float64)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             t2 = float(t.item())
-        kb2 = [kernel_bytes(s, "pfree") for s in st]
-        a2 = sum(kb2) / (km2.mean(axis=0)[:, 0].sum() / 1e3) / 1e9
-        same = bool(np.array_equal(sz2, sizes))
-        line["pfree"] = {"value": world * k * args.steps / (t2 / 1e3), "unit": UNIT,
-                         "ms_per_step": t2 / args.steps, "same_sizes_as_stream": same,
-                         "roofline": {"achieved": a2, "peak": peak, "unit": "GB/s",
-                                      "frac": a2 / peak, "kernel": "k_sage_pick<true>",
-                                      "per_layer_ms": km2.mean(axis=0)[:, 0].tolist()}}
+        kb2 = [kernel_bytes(s, other) for s in st]
+        km = km2.mean(axis=0)[:, -1]
+        a2 = sum(kb2) / (km.sum() / 1e3) / 1e9
+        line[other] = {"value": world * k * args.steps / (t2 / 1e3), "unit": UNIT,
+                       "ms_per_step": t2 / args.steps,
+                       "same_sizes": bool(np.array_equal(sz2, sizes)),
+                       "roofline": {"achieved": a2, "peak": peak, "unit": "GB/s",
+                                    "frac": a2 / peak, "kernel": KERNEL[other],
+                                    "per_layer_ms": km.tolist(), "per_layer_bytes": kb2}}
         del b2, g2
     # LADIES, BASELINE configs[2]: same graph, 512 nodes/layer, 3 layers, k=64
     if not args.no_ladies:
