@@ -538,9 +538,11 @@ __global__ void k_dd_scatter(const int64_t* __restrict__ R_ptr, const int32_t* _
   }
 }
 
-constexpr int kDdWarpChunk = 1024;  // entries staged per warp (small groups)
-constexpr int kDdCtaChunk = 8192;   // entries staged per CTA (large groups)
-constexpr int kDdThreads = 256;
+constexpr int kDdWarpChunk = 1024;   // entries staged per warp (small groups)
+constexpr int kDdCtaChunk = 49152;   // entries staged per CTA (large groups): 192 KB
+constexpr int kDdThreads = 256;      // small-group kernel
+constexpr int kDdCtaThreads = 1024;  // large-group kernel
+constexpr int kDdUnroll = 4;         // 16-B loads in flight per thread while staging
 
 __device__ __forceinline__ void dd_emit(int32_t c, uint64_t rec, const int64_t* eo, int64_t k,
                                         int32_t* fcol, uint32_t* bitmap, int64_t nwords) {
@@ -558,15 +560,15 @@ __device__ __forceinline__ void dd_emit(int32_t c, uint64_t rec, const int64_t* 
 // one warp per group of degree <= kDdWarpChunk; LARGE = true: one CTA per
 // larger group, kDdCtaChunk entries staged per step.
 template <bool LARGE>
-__global__ void __launch_bounds__(kDdThreads) k_dd_stream(
+__global__ void __launch_bounds__(LARGE ? kDdCtaThreads : kDdThreads) k_dd_stream(
     const int64_t* __restrict__ D_ptr, const int32_t* __restrict__ dv,
     const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
     const int64_t* __restrict__ goff, const uint64_t* __restrict__ pk,
     const int64_t* __restrict__ eoff, int64_t k, int32_t* __restrict__ fcol,
     uint32_t* __restrict__ bitmap, int64_t nwords) {
   constexpr int kChunk = LARGE ? kDdCtaChunk : kDdWarpChunk;
-  constexpr int kSlots = LARGE ? 1 : kDdThreads / 32;
-  __shared__ __align__(16) int32_t sbuf[kSlots][kChunk + 4];
+  constexpr int kSlotLen = kChunk + 4;
+  extern __shared__ __align__(16) int32_t sdyn[];  // [slots][kSlotLen]
   __shared__ int64_t s_eoff[kBrowSmem];
   const bool esm = k + 1 <= kBrowSmem;
   if (esm)
@@ -577,7 +579,7 @@ __global__ void __launch_bounds__(kDdThreads) k_dd_stream(
   const int lane = lane_id();
   const int tid = LARGE ? threadIdx.x : lane;
   const int nthr = LARGE ? blockDim.x : 32;
-  int32_t* buf = sbuf[LARGE ? 0 : (threadIdx.x >> 5)];
+  int32_t* buf = sdyn + (LARGE ? 0 : (threadIdx.x >> 5) * kSlotLen);
   const int64_t first = LARGE ? blockIdx.x : global_warp();
   const int64_t step = LARGE ? gridDim.x : grid_warps();
   for (int64_t g = first; g < D; g += step) {
@@ -587,16 +589,26 @@ __global__ void __launch_bounds__(kDdThreads) k_dd_stream(
     const int64_t p0 = goff[g], p1 = goff[g + 1];
     for (int64_t c0 = 0; c0 < d; c0 += kChunk) {
       const int64_t c1 = min(c0 + (int64_t)kChunk, d);
-      // stage entries [c0, c1) of A row v (16-B aligned vector loads)
+      // stage entries [c0, c1) of A row v: the P row on chip (16-B aligned
+      // vector loads, kDdUnroll in flight per thread)
       const int64_t e0 = a0 + c0, e1 = a0 + c1;
       const int64_t al0 = e0 & ~3LL;
-      for (int64_t e = al0 + 4 * tid; e < e1; e += 4 * nthr) {
-        const int4 x = ld_stream_v4(col + e);
-        const int64_t o = e - e0;  // may be -3..-1 for the aligned head
-        if (o + 0 >= 0 && e + 0 < e1) buf[o + 0] = x.x;
-        if (o + 1 >= 0 && e + 1 < e1) buf[o + 1] = x.y;
-        if (o + 2 >= 0 && e + 2 < e1) buf[o + 2] = x.z;
-        if (o + 3 >= 0 && e + 3 < e1) buf[o + 3] = x.w;
+      for (int64_t eb = al0 + 4 * tid; eb < e1; eb += 4 * nthr * kDdUnroll) {
+        int4 x[kDdUnroll];
+#pragma unroll
+        for (int u = 0; u < kDdUnroll; ++u) {
+          const int64_t e = eb + 4 * nthr * u;
+          x[u] = e < e1 ? ld_stream_v4(col + e) : make_int4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < kDdUnroll; ++u) {
+          const int64_t e = eb + 4 * nthr * u;
+          const int64_t o = e - e0;  // may be -3..-1 for the aligned head
+          if (o + 0 >= 0 && e + 0 < e1) buf[o + 0] = x[u].x;
+          if (o + 1 >= 0 && e + 1 < e1) buf[o + 1] = x[u].y;
+          if (o + 2 >= 0 && e + 2 < e1) buf[o + 2] = x[u].z;
+          if (o + 3 >= 0 && e + 3 < e1) buf[o + 3] = x[u].w;
+        }
       }
       if (LARGE) __syncthreads(); else __syncwarp();
       for (int64_t p = p0 + tid; p < p1; p += nthr) {
@@ -850,17 +862,25 @@ static int dedup_stream(const Graph* g, SageWs& ws, const int64_t* R_ptr, const 
                                                         ws.pk);
   GB_LAUNCH_CHECK("dedup prepare");
   static int grid_small = 0, grid_large = 0;
+  const size_t smem_small = sizeof(int32_t) * (kDdWarpChunk + 4) * (kDdThreads / 32);
+  const size_t smem_large = sizeof(int32_t) * (kDdCtaChunk + 4);
   if (!grid_small) {
-    grid_small = persistent_grid(k_dd_stream<false>, kDdThreads);
-    grid_large = persistent_grid(k_dd_stream<true>, kDdThreads);
+    cudaFuncSetAttribute(k_dd_stream<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem_large);
+    int o1 = 0, o2 = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_dd_stream<false>, kDdThreads, smem_small);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_dd_stream<true>, kDdCtaThreads,
+                                                  smem_large);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    if (sms <= 0) sms = kNumSMs;
+    grid_small = (o1 > 0 ? o1 : 1) * sms;
+    grid_large = (o2 > 0 ? o2 : 1) * sms;
   }
   prof_mark(st);
-  k_dd_stream<false><<<grid_small, kDdThreads, 0, st>>>(ws.d_nw + 1, ws.dv, g->rowptr, g->col,
-                                                       ws.goff, ws.pk, o.eoff, k, o.fcol,
-                                                       ws.bitmap, nwords);
-  k_dd_stream<true><<<grid_large, kDdThreads, 0, st>>>(ws.d_nw + 1, ws.dv, g->rowptr, g->col,
-                                                      ws.goff, ws.pk, o.eoff, k, o.fcol,
-                                                      ws.bitmap, nwords);
+  k_dd_stream<false><<<grid_small, kDdThreads, smem_small, st>>>(
+      ws.d_nw + 1, ws.dv, g->rowptr, g->col, ws.goff, ws.pk, o.eoff, k, o.fcol, ws.bitmap, nwords);
+  k_dd_stream<true><<<grid_large, kDdCtaThreads, smem_large, st>>>(
+      ws.d_nw + 1, ws.dv, g->rowptr, g->col, ws.goff, ws.pk, o.eoff, k, o.fcol, ws.bitmap, nwords);
   prof_mark(st);
   GB_LAUNCH_CHECK("k_dd_stream");
   count_launches(11);
