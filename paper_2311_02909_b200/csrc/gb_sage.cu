@@ -538,11 +538,16 @@ __global__ void k_dd_scatter(const int64_t* __restrict__ R_ptr, const int32_t* _
   }
 }
 
-constexpr int kDdWarpChunk = 1024;   // entries staged per warp (small groups)
-constexpr int kDdCtaChunk = 49152;   // entries staged per CTA (large groups): 192 KB
-constexpr int kDdThreads = 256;      // small-group kernel
-constexpr int kDdCtaThreads = 1024;  // large-group kernel
-constexpr int kDdUnroll = 4;         // 16-B loads in flight per thread while staging
+// Size tiers of distinct rows (degree d): 0 warp per row (d <= 1K, 4 KB
+// stage), 1 CTA-256 per row (d <= 8K, 32 KB stage), 2 CTA-1024 per row
+// (hubs, 192 KB stage, <= 4 passes over the row's picks at products scale).
+constexpr int kDdThreads = 256;
+constexpr int kDdUnroll = 4;  // 16-B loads in flight per thread while staging
+template <int T> struct DdTier;
+template <> struct DdTier<0> { static constexpr int kChunk = 1024, kThreads = 256, kLo = 0, kHi = 1024; static constexpr bool kWarp = true; };
+template <> struct DdTier<1> { static constexpr int kChunk = 8192, kThreads = 256, kLo = 1024, kHi = 8192; static constexpr bool kWarp = false; };
+template <> struct DdTier<2> { static constexpr int kChunk = 49152, kThreads = 1024, kLo = 8192, kHi = 0x7fffffff; static constexpr bool kWarp = false; };
+constexpr int kDdWarpChunk = 1024;
 
 __device__ __forceinline__ void dd_emit(int32_t c, uint64_t rec, const int64_t* eo, int64_t k,
                                         int32_t* fcol, uint32_t* bitmap, int64_t nwords) {
@@ -556,17 +561,18 @@ __device__ __forceinline__ void dd_emit(int32_t c, uint64_t rec, const int64_t* 
   atomicOr(bitmap + lo * nwords + (c >> 5), 1u << (c & 31));
 }
 
-// Stream every distinct A row once and serve its picks.  LARGE = false:
-// one warp per group of degree <= kDdWarpChunk; LARGE = true: one CTA per
+// Stream every distinct A row once and serve its picks; TIER selects the
+// row sizes handled and warp / CTA granularity.
 // larger group, kDdCtaChunk entries staged per step.
-template <bool LARGE>
-__global__ void __launch_bounds__(LARGE ? kDdCtaThreads : kDdThreads) k_dd_stream(
+template <int TIER>
+__global__ void __launch_bounds__(DdTier<TIER>::kThreads) k_dd_stream(
     const int64_t* __restrict__ D_ptr, const int32_t* __restrict__ dv,
     const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
     const int64_t* __restrict__ goff, const uint64_t* __restrict__ pk,
     const int64_t* __restrict__ eoff, int64_t k, int32_t* __restrict__ fcol,
     uint32_t* __restrict__ bitmap, int64_t nwords) {
-  constexpr int kChunk = LARGE ? kDdCtaChunk : kDdWarpChunk;
+  constexpr bool LARGE = !DdTier<TIER>::kWarp;
+  constexpr int kChunk = DdTier<TIER>::kChunk;
   constexpr int kSlotLen = kChunk + 4;
   extern __shared__ __align__(16) int32_t sdyn[];  // [slots][kSlotLen]
   __shared__ int64_t s_eoff[kBrowSmem];
@@ -585,7 +591,7 @@ __global__ void __launch_bounds__(LARGE ? kDdCtaThreads : kDdThreads) k_dd_strea
   for (int64_t g = first; g < D; g += step) {
     const int32_t v = dv[g];
     const int64_t a0 = rowptr[v], d = rowptr[v + 1] - a0;
-    if ((d > kDdWarpChunk) != LARGE) continue;
+    if (d <= DdTier<TIER>::kLo || d > DdTier<TIER>::kHi) continue;
     const int64_t p0 = goff[g], p1 = goff[g + 1];
     for (int64_t c0 = 0; c0 < d; c0 += kChunk) {
       const int64_t c1 = min(c0 + (int64_t)kChunk, d);
@@ -838,6 +844,26 @@ struct VPopF {
   __device__ int64_t operator()(int64_t i) const { return __popc(b[i]); }
 };
 
+template <int T>
+static int launch_dd(SageWs& ws, const Graph* g, gb_sage_layer_out& o, int64_t k, int64_t nwords,
+                     cudaStream_t st) {
+  using Tr = DdTier<T>;
+  const size_t smem = sizeof(int32_t) * (Tr::kChunk + 4) * (Tr::kWarp ? Tr::kThreads / 32 : 1);
+  static int grid = 0;
+  if (!grid) {
+    cudaFuncSetAttribute(k_dd_stream<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int occ = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dd_stream<T>, Tr::kThreads, smem);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    grid = (occ > 0 ? occ : 1) * (sms > 0 ? sms : kNumSMs);
+  }
+  k_dd_stream<T><<<grid, Tr::kThreads, smem, st>>>(ws.d_nw + 1, ws.dv, g->rowptr, g->col,
+                                                    ws.goff, ws.pk, o.eoff, k, o.fcol, ws.bitmap,
+                                                    nwords);
+  GB_LAUNCH_CHECK("k_dd_stream");
+  return GB_OK;
+}
+
 // Dedup stream step of one layer (pidx from k_sage_pick<false> in place).
 static int dedup_stream(const Graph* g, SageWs& ws, const int64_t* R_ptr, const int32_t* rowv,
                         const int64_t* brow, int64_t k, int32_t s, int64_t r_cap,
@@ -861,29 +887,14 @@ static int dedup_stream(const Graph* g, SageWs& ws, const int64_t* R_ptr, const 
                                                         ws.vbits, ws.vpre, ws.goff, ws.gcur,
                                                         ws.pk);
   GB_LAUNCH_CHECK("dedup prepare");
-  static int grid_small = 0, grid_large = 0;
-  const size_t smem_small = sizeof(int32_t) * (kDdWarpChunk + 4) * (kDdThreads / 32);
-  const size_t smem_large = sizeof(int32_t) * (kDdCtaChunk + 4);
-  if (!grid_small) {
-    cudaFuncSetAttribute(k_dd_stream<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem_large);
-    int o1 = 0, o2 = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_dd_stream<false>, kDdThreads, smem_small);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_dd_stream<true>, kDdCtaThreads,
-                                                  smem_large);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    if (sms <= 0) sms = kNumSMs;
-    grid_small = (o1 > 0 ? o1 : 1) * sms;
-    grid_large = (o2 > 0 ? o2 : 1) * sms;
-  }
   prof_mark(st);
-  k_dd_stream<false><<<grid_small, kDdThreads, smem_small, st>>>(
-      ws.d_nw + 1, ws.dv, g->rowptr, g->col, ws.goff, ws.pk, o.eoff, k, o.fcol, ws.bitmap, nwords);
-  k_dd_stream<true><<<grid_large, kDdCtaThreads, smem_large, st>>>(
-      ws.d_nw + 1, ws.dv, g->rowptr, g->col, ws.goff, ws.pk, o.eoff, k, o.fcol, ws.bitmap, nwords);
+  int rc2 = launch_dd<0>(ws, g, o, k, nwords, st);
+  if (!rc2) rc2 = launch_dd<1>(ws, g, o, k, nwords, st);
+  if (!rc2) rc2 = launch_dd<2>(ws, g, o, k, nwords, st);
+  if (rc2) return rc2;
   prof_mark(st);
   GB_LAUNCH_CHECK("k_dd_stream");
-  count_launches(11);
+  count_launches(12);
   return GB_OK;
 }
 
