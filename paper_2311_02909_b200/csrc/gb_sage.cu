@@ -544,9 +544,33 @@ __global__ void k_dd_scatter(const int64_t* __restrict__ R_ptr, const int32_t* _
 constexpr int kDdThreads = 256;
 constexpr int kDdUnroll = 4;  // 16-B loads in flight per thread while staging
 template <int T> struct DdTier;
-template <> struct DdTier<0> { static constexpr int kChunk = 1024, kThreads = 256, kLo = 0, kHi = 1024; static constexpr bool kWarp = true; };
-template <> struct DdTier<1> { static constexpr int kChunk = 8192, kThreads = 256, kLo = 1024, kHi = 8192; static constexpr bool kWarp = false; };
-template <> struct DdTier<2> { static constexpr int kChunk = 49152, kThreads = 1024, kLo = 8192, kHi = 0x7fffffff; static constexpr bool kWarp = false; };
+template <> struct DdTier<0> {
+  static constexpr int kChunk = 1024, kThreads = 256, kLo = 0, kHi = 1024, kPicks = 0;
+  static constexpr bool kWarp = true;
+};
+template <> struct DdTier<1> {
+  static constexpr int kChunk = 8192, kThreads = 256, kLo = 1024, kHi = 8192, kPicks = 2048;
+  static constexpr bool kWarp = false;
+};
+template <> struct DdTier<2> {
+  static constexpr int kChunk = 49152, kThreads = 1024, kLo = 8192, kHi = 0x7fffffff, kPicks = 8192;
+  static constexpr bool kWarp = false;
+};
+
+// work items of a CTA tier: ceil(picks / kPicks) per distinct row of the tier
+template <int T>
+struct ItemF {
+  const int32_t* dv;
+  const int64_t* rowptr;
+  const int64_t* goff;
+  __device__ int64_t operator()(int64_t g) const {
+    const int32_t v = dv[g];
+    const int64_t d = rowptr[v + 1] - rowptr[v];
+    if (d <= DdTier<T>::kLo || d > DdTier<T>::kHi) return 0;
+    const int64_t p = goff[g + 1] - goff[g];
+    return (p + DdTier<T>::kPicks - 1) / DdTier<T>::kPicks;
+  }
+};
 constexpr int kDdWarpChunk = 1024;
 
 __device__ __forceinline__ void dd_emit(int32_t c, uint64_t rec, const int64_t* eo, int64_t k,
@@ -570,7 +594,7 @@ __global__ void __launch_bounds__(DdTier<TIER>::kThreads) k_dd_stream(
     const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
     const int64_t* __restrict__ goff, const uint64_t* __restrict__ pk,
     const int64_t* __restrict__ eoff, int64_t k, int32_t* __restrict__ fcol,
-    uint32_t* __restrict__ bitmap, int64_t nwords) {
+    uint32_t* __restrict__ bitmap, int64_t nwords, const int64_t* __restrict__ ioff) {
   constexpr bool LARGE = !DdTier<TIER>::kWarp;
   constexpr int kChunk = DdTier<TIER>::kChunk;
   constexpr int kSlotLen = kChunk + 4;
@@ -588,11 +612,27 @@ __global__ void __launch_bounds__(DdTier<TIER>::kThreads) k_dd_stream(
   int32_t* buf = sdyn + (LARGE ? 0 : (threadIdx.x >> 5) * kSlotLen);
   const int64_t first = LARGE ? blockIdx.x : global_warp();
   const int64_t step = LARGE ? gridDim.x : grid_warps();
-  for (int64_t g = first; g < D; g += step) {
+  // warp tier: one distinct row per warp; CTA tiers: work items of at most
+  // kPicks picks of one row (item prefix ioff over the rows of the tier)
+  const int64_t nitems = LARGE ? ioff[D] : D;
+  for (int64_t it = first; it < nitems; it += step) {
+    int64_t g = it, p0, p1;
+    if (LARGE) {
+      int64_t lo = 0, hi = D;  // last g with ioff[g] <= it
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (ioff[mid] <= it) lo = mid; else hi = mid;
+      }
+      g = lo;
+      p0 = goff[g] + (it - ioff[g]) * DdTier<TIER>::kPicks;
+      p1 = min(p0 + (int64_t)DdTier<TIER>::kPicks, goff[g + 1]);
+    } else {
+      p0 = goff[g];
+      p1 = goff[g + 1];
+    }
     const int32_t v = dv[g];
     const int64_t a0 = rowptr[v], d = rowptr[v + 1] - a0;
     if (d <= DdTier<TIER>::kLo || d > DdTier<TIER>::kHi) continue;
-    const int64_t p0 = goff[g], p1 = goff[g + 1];
     for (int64_t c0 = 0; c0 < d; c0 += kChunk) {
       const int64_t c1 = min(c0 + (int64_t)kChunk, d);
       // stage entries [c0, c1) of A row v: the P row on chip (16-B aligned
@@ -796,6 +836,8 @@ struct SageWs {
   int32_t* gcur;
   int64_t* goff;
   uint64_t* pk;      // pick records grouped by vertex
+  int64_t* ioff1;    // work-item prefixes of the CTA tiers
+  int64_t* ioff2;
   size_t bytes;
 };
 
@@ -825,6 +867,8 @@ static SageWs sage_ws_layout(char* base, int64_t k, int64_t n, int64_t r_cap_max
   w.gcur = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
   w.goff = (int64_t*)take(sizeof(int64_t) * (r_cap_max + 1));
   w.pk = (uint64_t*)take(sizeof(uint64_t) * (f_cap_max + 1));
+  w.ioff1 = (int64_t*)take(sizeof(int64_t) * (r_cap_max + 1));
+  w.ioff2 = (int64_t*)take(sizeof(int64_t) * (r_cap_max + 1));
   w.bytes = off;
   return w;
 }
@@ -846,7 +890,7 @@ struct VPopF {
 
 template <int T>
 static int launch_dd(SageWs& ws, const Graph* g, gb_sage_layer_out& o, int64_t k, int64_t nwords,
-                     cudaStream_t st) {
+                     int64_t r_cap, cudaStream_t st) {
   using Tr = DdTier<T>;
   const size_t smem = sizeof(int32_t) * (Tr::kChunk + 4) * (Tr::kWarp ? Tr::kThreads / 32 : 1);
   static int grid = 0;
@@ -857,9 +901,16 @@ static int launch_dd(SageWs& ws, const Graph* g, gb_sage_layer_out& o, int64_t k
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     grid = (occ > 0 ? occ : 1) * (sms > 0 ? sms : kNumSMs);
   }
+  int64_t* ioff = nullptr;
+  if (!Tr::kWarp) {
+    ioff = T == 1 ? ws.ioff1 : ws.ioff2;
+    int rc = device_exclusive_scan<int64_t>(ws.d_nw + 1, r_cap, ItemF<T>{ws.dv, g->rowptr, ws.goff},
+                                            ioff, ws.scan_ws, st);
+    if (rc) return rc;
+  }
   k_dd_stream<T><<<grid, Tr::kThreads, smem, st>>>(ws.d_nw + 1, ws.dv, g->rowptr, g->col,
                                                     ws.goff, ws.pk, o.eoff, k, o.fcol, ws.bitmap,
-                                                    nwords);
+                                                    nwords, ioff);
   GB_LAUNCH_CHECK("k_dd_stream");
   return GB_OK;
 }
@@ -888,9 +939,9 @@ static int dedup_stream(const Graph* g, SageWs& ws, const int64_t* R_ptr, const 
                                                         ws.pk);
   GB_LAUNCH_CHECK("dedup prepare");
   prof_mark(st);
-  int rc2 = launch_dd<0>(ws, g, o, k, nwords, st);
-  if (!rc2) rc2 = launch_dd<1>(ws, g, o, k, nwords, st);
-  if (!rc2) rc2 = launch_dd<2>(ws, g, o, k, nwords, st);
+  int rc2 = launch_dd<0>(ws, g, o, k, nwords, r_cap, st);
+  if (!rc2) rc2 = launch_dd<1>(ws, g, o, k, nwords, r_cap, st);
+  if (!rc2) rc2 = launch_dd<2>(ws, g, o, k, nwords, r_cap, st);
   if (rc2) return rc2;
   prof_mark(st);
   GB_LAUNCH_CHECK("k_dd_stream");
