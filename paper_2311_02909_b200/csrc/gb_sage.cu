@@ -523,7 +523,8 @@ __global__ void k_dd_scatter(const int64_t* __restrict__ R_ptr, const int32_t* _
                              const int64_t* __restrict__ fptr, const int32_t* __restrict__ pidx,
                              const uint32_t* __restrict__ vbits, const int32_t* __restrict__ vpre,
                              const int64_t* __restrict__ goff, int32_t* __restrict__ gcur,
-                             uint64_t* __restrict__ pk) {
+                             uint64_t* __restrict__ pk, int32_t* __restrict__ pkb,
+                             const int64_t* __restrict__ brow, int64_t k) {
   const int64_t R = *R_ptr;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
        r += (int64_t)gridDim.x * blockDim.x) {
@@ -533,8 +534,15 @@ __global__ void k_dd_scatter(const int64_t* __restrict__ R_ptr, const int32_t* _
     const int32_t g = vrank(vbits, vpre, rowv[r]);
     const int64_t base = goff[g] + atomicAdd(gcur + g, take);
     const int64_t fp = fptr[r];
-    for (int t = 0; t < take; ++t)
+    int64_t lo = 0, hi = k;  // batch of row r (carried with the picks)
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (__ldg(brow + mid) <= r) lo = mid; else hi = mid;
+    }
+    for (int t = 0; t < take; ++t) {
       pk[base + t] = ((uint64_t)(uint32_t)pidx[fp + t] << 32) | (uint64_t)(fp + t);
+      pkb[base + t] = (int32_t)lo;
+    }
   }
 }
 
@@ -573,38 +581,25 @@ struct ItemF {
 };
 constexpr int kDdWarpChunk = 1024;
 
-__device__ __forceinline__ void dd_emit(int32_t c, uint64_t rec, const int64_t* eo, int64_t k,
-                                        int32_t* fcol, uint32_t* bitmap, int64_t nwords) {
-  const int64_t pos = (int64_t)(rec & 0xffffffffu);
-  fcol[pos] = c;
-  int64_t lo = 0, hi = k;  // batch of the frontier position
-  while (hi - lo > 1) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (eo[mid] <= pos) lo = mid; else hi = mid;
-  }
-  atomicOr(bitmap + lo * nwords + (c >> 5), 1u << (c & 31));
+__device__ __forceinline__ void dd_emit(int32_t c, uint64_t rec, int32_t batch, int32_t* fcol,
+                                        uint32_t* bitmap, int64_t nwords) {
+  fcol[(int64_t)(rec & 0xffffffffu)] = c;
+  atomicOr(bitmap + (int64_t)batch * nwords + (c >> 5), 1u << (c & 31));
 }
 
 // Stream every distinct A row once and serve its picks; TIER selects the
 // row sizes handled and warp / CTA granularity.
-// larger group, kDdCtaChunk entries staged per step.
 template <int TIER>
 __global__ void __launch_bounds__(DdTier<TIER>::kThreads) k_dd_stream(
     const int64_t* __restrict__ D_ptr, const int32_t* __restrict__ dv,
     const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
     const int64_t* __restrict__ goff, const uint64_t* __restrict__ pk,
-    const int64_t* __restrict__ eoff, int64_t k, int32_t* __restrict__ fcol,
+    const int32_t* __restrict__ pkb, int32_t* __restrict__ fcol,
     uint32_t* __restrict__ bitmap, int64_t nwords, const int64_t* __restrict__ ioff) {
   constexpr bool LARGE = !DdTier<TIER>::kWarp;
   constexpr int kChunk = DdTier<TIER>::kChunk;
   constexpr int kSlotLen = kChunk + 4;
   extern __shared__ __align__(16) int32_t sdyn[];  // [slots][kSlotLen]
-  __shared__ int64_t s_eoff[kBrowSmem];
-  const bool esm = k + 1 <= kBrowSmem;
-  if (esm)
-    for (int64_t i = threadIdx.x; i <= k; i += blockDim.x) s_eoff[i] = eoff[i];
-  __syncthreads();
-  const int64_t* eo = esm ? s_eoff : eoff;
   const int64_t D = *D_ptr;
   const int lane = lane_id();
   const int tid = LARGE ? threadIdx.x : lane;
@@ -660,7 +655,7 @@ __global__ void __launch_bounds__(DdTier<TIER>::kThreads) k_dd_stream(
       for (int64_t p = p0 + tid; p < p1; p += nthr) {
         const uint64_t rec = pk[p];
         const int64_t idx = (int64_t)(rec >> 32);
-        if (idx >= c0 && idx < c1) dd_emit(buf[idx - c0], rec, eo, k, fcol, bitmap, nwords);
+        if (idx >= c0 && idx < c1) dd_emit(buf[idx - c0], rec, pkb[p], fcol, bitmap, nwords);
       }
       if (LARGE) __syncthreads(); else __syncwarp();
     }
@@ -707,12 +702,18 @@ __global__ void k_sage_rank(const int64_t* __restrict__ F_ptr, const int64_t* __
   __syncthreads();
   const int64_t F = *F_ptr;
   const int64_t* eo = sm ? s_eoff : eoff;
+  int64_t lo = -1;  // batch of e: binary search once, then walk forward (e increases)
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < F;
        e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t lo = 0, hi = k;
-    while (hi - lo > 1) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (eo[mid] <= e) lo = mid; else hi = mid;
+    if (lo < 0) {
+      int64_t a = 0, b = k;
+      while (b - a > 1) {
+        const int64_t mid = (a + b) >> 1;
+        if (eo[mid] <= e) a = mid; else b = mid;
+      }
+      lo = a;
+    } else {
+      while (lo + 1 < k && eo[lo + 1] <= e) ++lo;
     }
     const int32_t v = fcol[e];
     const int64_t wi = lo * nwords + (v >> 5);
@@ -836,6 +837,7 @@ struct SageWs {
   int32_t* gcur;
   int64_t* goff;
   uint64_t* pk;      // pick records grouped by vertex
+  int32_t* pkb;      // batch of each pick record
   int64_t* ioff1;    // work-item prefixes of the CTA tiers
   int64_t* ioff2;
   size_t bytes;
@@ -867,6 +869,7 @@ static SageWs sage_ws_layout(char* base, int64_t k, int64_t n, int64_t r_cap_max
   w.gcur = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
   w.goff = (int64_t*)take(sizeof(int64_t) * (r_cap_max + 1));
   w.pk = (uint64_t*)take(sizeof(uint64_t) * (f_cap_max + 1));
+  w.pkb = (int32_t*)take(sizeof(int32_t) * (f_cap_max + 1));
   w.ioff1 = (int64_t*)take(sizeof(int64_t) * (r_cap_max + 1));
   w.ioff2 = (int64_t*)take(sizeof(int64_t) * (r_cap_max + 1));
   w.bytes = off;
@@ -909,7 +912,7 @@ static int launch_dd(SageWs& ws, const Graph* g, gb_sage_layer_out& o, int64_t k
     if (rc) return rc;
   }
   k_dd_stream<T><<<grid, Tr::kThreads, smem, st>>>(ws.d_nw + 1, ws.dv, g->rowptr, g->col,
-                                                    ws.goff, ws.pk, o.eoff, k, o.fcol, ws.bitmap,
+                                                    ws.goff, ws.pk, ws.pkb, o.fcol, ws.bitmap,
                                                     nwords, ioff);
   GB_LAUNCH_CHECK("k_dd_stream");
   return GB_OK;
@@ -936,7 +939,7 @@ static int dedup_stream(const Graph* g, SageWs& ws, const int64_t* R_ptr, const 
   if (rc) return rc;
   k_dd_scatter<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, s, o.fptr, ws.pidx,
                                                         ws.vbits, ws.vpre, ws.goff, ws.gcur,
-                                                        ws.pk);
+                                                        ws.pk, ws.pkb, brow, k);
   GB_LAUNCH_CHECK("dedup prepare");
   prof_mark(st);
   int rc2 = launch_dd<0>(ws, g, o, k, nwords, r_cap, st);
