@@ -181,7 +181,18 @@ struct SageArgs {
   int64_t nwords;
   int32_t* fcol;         // frontier columns (output)
   int32_t* pidx;         // stream mode: row-relative pick indices (scratch)
+  // dedup mode: pick records grouped by distinct row vertex
+  const uint32_t* vbits;
+  const int32_t* vpre;
+  const int64_t* goff;
+  int32_t* gcur;
+  uint64_t* pk;
+  int32_t* pkb;
 };
+
+__device__ __forceinline__ int32_t vrank(const uint32_t* vbits, const int32_t* vpre, int32_t v) {
+  return vpre[v >> 5] + __popc(vbits[v >> 5] & ((1u << (v & 31)) - 1u));
+}
 
 constexpr int kPickThreads = 128;
 constexpr int kStreamThreads = 256;
@@ -260,9 +271,10 @@ __device__ __forceinline__ int64_t gt_first_gt(const GTable& t, double target) {
 // its_sample_row's cumsum/searchsorted/clamp/walk-back (sampler.py:176-188).
 // Picks are kept sorted (frontier_from_rows sorts, sampler.py:216) in
 // registers (MAXF = fanout bucket, fully unrolled).
-// GATHER (P-free): read the picked columns of A directly and finish the row;
-// otherwise write the row-relative indices for the streaming kernel.
-template <bool GATHER, int MAXF>
+// OUT 1 (P-free): read the picked columns of A directly and finish the row;
+// OUT 0: write the row-relative indices for the row-streaming kernel;
+// OUT 2 (dedup): write pick records straight into the row's vertex group.
+template <int OUT, int MAXF>
 __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
                                                           const int64_t* __restrict__ R_ptr) {
   __shared__ int64_t s_brow[kBrowSmem];
@@ -325,7 +337,7 @@ __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
           if (q == i) sorted[q] = x;
       }
     }
-    if (GATHER) {
+    if (OUT == 1) {
       const int64_t rs = A.rowptr[A.rowv[r]];
       int32_t cv[MAXF];
 #pragma unroll
@@ -340,6 +352,15 @@ __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
         for (int q = 0; q < MAXF; ++q)
           if (q < take) atomicOr(bm + (cv[q] >> 5), 1u << (cv[q] & 31));
       }
+    } else if (OUT == 2) {
+      const int32_t g = vrank(A.vbits, A.vpre, A.rowv[r]);
+      const int64_t base = A.goff[g] + atomicAdd(A.gcur + g, take);
+#pragma unroll
+      for (int q = 0; q < MAXF; ++q)
+        if (q < take) {
+          A.pk[base + q] = ((uint64_t)(uint32_t)sorted[q] << 32) | (uint64_t)(fp + q);
+          A.pkb[base + q] = (int32_t)bb;
+        }
     } else {
 #pragma unroll
       for (int q = 0; q < MAXF; ++q)
@@ -348,14 +369,14 @@ __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
   }
 }
 
-template <bool GATHER>
+template <int OUT>
 static void launch_pick(int grid, const SageArgs& A, const int64_t* R_ptr, cudaStream_t st) {
   if (A.s <= 8)
-    k_sage_pick<GATHER, 8><<<grid, kPickThreads, 0, st>>>(A, R_ptr);
+    k_sage_pick<OUT, 8><<<grid, kPickThreads, 0, st>>>(A, R_ptr);
   else if (A.s <= 16)
-    k_sage_pick<GATHER, 16><<<grid, kPickThreads, 0, st>>>(A, R_ptr);
+    k_sage_pick<OUT, 16><<<grid, kPickThreads, 0, st>>>(A, R_ptr);
   else
-    k_sage_pick<GATHER, 32><<<grid, kPickThreads, 0, st>>>(A, R_ptr);
+    k_sage_pick<OUT, 32><<<grid, kPickThreads, 0, st>>>(A, R_ptr);
 }
 
 // Q^l A with the P row formed on chip: warps stream every A row of the
@@ -476,10 +497,6 @@ __global__ void k_dd_mark(const int64_t* __restrict__ R_ptr, const int32_t* __re
       const int32_t v = rowv[r];
       atomicOr(vbits + (v >> 5), 1u << (v & 31));
     }
-}
-
-__device__ __forceinline__ int32_t vrank(const uint32_t* vbits, const int32_t* vpre, int32_t v) {
-  return vpre[v >> 5] + __popc(vbits[v >> 5] & ((1u << (v & 31)) - 1u));
 }
 
 // distinct vertex list (ascending) and its degrees
@@ -919,14 +936,15 @@ static int launch_dd(SageWs& ws, const Graph* g, gb_sage_layer_out& o, int64_t k
 }
 
 // Dedup stream step of one layer (pidx from k_sage_pick<false> in place).
-static int dedup_stream(const Graph* g, SageWs& ws, const int64_t* R_ptr, const int32_t* rowv,
-                        const int64_t* brow, int64_t k, int32_t s, int64_t r_cap,
-                        gb_sage_layer_out& o, int64_t nwords, cudaStream_t st) {
+// Dedup step 1 (before the pick kernel): distinct row vertices, picks per
+// vertex (from the degrees alone) and the group offsets the pick kernel
+// writes its records into.
+static int dedup_prepare(const Graph* g, SageWs& ws, const int64_t* R_ptr, const int32_t* rowv,
+                         int32_t s, int64_t r_cap, int64_t nwords, cudaStream_t st) {
   const int64_t gw = 16 * kNumSMs;
   GB_CUDA(cudaMemsetAsync(ws.vbits, 0, sizeof(uint32_t) * (nwords + 1), st));
   GB_CUDA(cudaMemsetAsync(ws.gcnt, 0, sizeof(int32_t) * (r_cap + 1), st));
   GB_CUDA(cudaMemsetAsync(ws.gcur, 0, sizeof(int32_t) * (r_cap + 1), st));
-  k_sage_eoff<<<grid_for(k + 1, 128, 64), 128, 0, st>>>(brow, k, o.fptr, o.eoff);
   k_dd_mark<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, ws.vbits);
   int rc = device_exclusive_scan<int64_t>(ws.d_nw, nwords, VPopF{ws.vbits}, ws.vpre, ws.scan_ws,
                                           st);
@@ -937,18 +955,22 @@ static int dedup_stream(const Graph* g, SageWs& ws, const int64_t* R_ptr, const 
                                                       ws.gcnt);
   rc = device_exclusive_scan<int64_t>(ws.d_nw + 1, r_cap, GcntF{ws.gcnt}, ws.goff, ws.scan_ws, st);
   if (rc) return rc;
-  k_dd_scatter<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, s, o.fptr, ws.pidx,
-                                                        ws.vbits, ws.vpre, ws.goff, ws.gcur,
-                                                        ws.pk, ws.pkb, brow, k);
   GB_LAUNCH_CHECK("dedup prepare");
+  count_launches(5);
+  return GB_OK;
+}
+
+// Dedup step 2 (after the pick kernel wrote the grouped records): stream
+// every distinct row once, in three size tiers.
+static int dedup_stream(const Graph* g, SageWs& ws, gb_sage_layer_out& o, int64_t k,
+                        int64_t r_cap, int64_t nwords, cudaStream_t st) {
   prof_mark(st);
-  int rc2 = launch_dd<0>(ws, g, o, k, nwords, r_cap, st);
-  if (!rc2) rc2 = launch_dd<1>(ws, g, o, k, nwords, r_cap, st);
-  if (!rc2) rc2 = launch_dd<2>(ws, g, o, k, nwords, r_cap, st);
-  if (rc2) return rc2;
+  int rc = launch_dd<0>(ws, g, o, k, nwords, r_cap, st);
+  if (!rc) rc = launch_dd<1>(ws, g, o, k, nwords, r_cap, st);
+  if (!rc) rc = launch_dd<2>(ws, g, o, k, nwords, r_cap, st);
+  if (rc) return rc;
   prof_mark(st);
-  GB_LAUNCH_CHECK("k_dd_stream");
-  count_launches(12);
+  count_launches(5);
   return GB_OK;
 }
 
@@ -1051,11 +1073,19 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     A.seed = seed; A.epoch = epoch; A.depth = (uint64_t)d;
     A.bitmap = ws.bitmap; A.nwords = nwords; A.fcol = o.fcol; A.pidx = ws.pidx;
     const int pick_grid = grid_for(r_cap, kPickThreads, 64 * kNumSMs);
+    if (dedup) {
+      rc = dedup_prepare(g, ws, R_ptr, rowv, s, r_cap, nwords, st);
+      if (rc) return rc;
+      A.vbits = ws.vbits; A.vpre = ws.vpre; A.goff = ws.goff; A.gcur = ws.gcur;
+      A.pk = ws.pk; A.pkb = ws.pkb;
+    }
     prof_mark(st);
-    if (stream || dedup)
-      launch_pick<false>(pick_grid, A, R_ptr, st);
+    if (dedup)
+      launch_pick<2>(pick_grid, A, R_ptr, st);
+    else if (stream)
+      launch_pick<0>(pick_grid, A, R_ptr, st);
     else
-      launch_pick<true>(pick_grid, A, R_ptr, st);
+      launch_pick<1>(pick_grid, A, R_ptr, st);
     GB_LAUNCH_CHECK("k_sage_pick");
     prof_mark(st);
     if (stream) {
@@ -1066,7 +1096,7 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
       count_launches(1);
     }
     if (dedup) {
-      rc = dedup_stream(g, ws, R_ptr, rowv, brow, k, s, r_cap, o, nwords, st);
+      rc = dedup_stream(g, ws, o, k, r_cap, nwords, st);
       if (rc) return rc;
     }
     rc = device_exclusive_scan<int64_t>(ws.d_W, W, PopF{ws.bitmap}, ws.wpre, ws.scan_ws, st);
@@ -1154,11 +1184,11 @@ int sage_layer_sample(const Graph* tables, int64_t k, const int64_t* brow, int64
   A.bitmap = nullptr; A.nwords = 0; A.fcol = fcol; A.pidx = pidx;
   const int pick_grid = grid_for(r_cap, kPickThreads, 64 * kNumSMs);
   if (stream) {
-    launch_pick<false>(pick_grid, A, R_ptr, st);
+    launch_pick<0>(pick_grid, A, R_ptr, st);
     k_sage_stream<<<stream_grid(), kStreamThreads, 0, st>>>(A, R_ptr);
     count_launches(2);
   } else {
-    launch_pick<true>(pick_grid, A, R_ptr, st);
+    launch_pick<1>(pick_grid, A, R_ptr, st);
     count_launches(1);
   }
   GB_LAUNCH_CHECK("sage_layer_sample");
@@ -1180,7 +1210,7 @@ int sage_sample_keyed(const Graph* tables, int64_t R, const int64_t* d_R, const 
   A.rowv = rowv; A.rowkeys = rowkeys; A.deg = deg; A.fptr = fptr;
   A.k = 0; A.s = s; A.seed = seed; A.epoch = epoch; A.depth = depth;
   A.bitmap = nullptr; A.fcol = fcol;
-  launch_pick<true>(grid_for(R, kPickThreads, 64 * kNumSMs), A, d_R, st);
+  launch_pick<1>(grid_for(R, kPickThreads, 64 * kNumSMs), A, d_R, st);
   GB_LAUNCH_CHECK("sage_sample_keyed");
   count_launches(1);
   return GB_OK;
