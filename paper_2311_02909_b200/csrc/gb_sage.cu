@@ -354,7 +354,15 @@ __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
       }
     } else if (OUT == 2) {
       const int32_t g = vrank(A.vbits, A.vpre, A.rowv[r]);
-      const int64_t base = A.goff[g] + atomicAdd(A.gcur + g, take);
+      // rows of one vertex have the same degree, hence the same take:
+      // one cursor atomic per vertex per warp (hub groups are hot)
+      const unsigned act = __activemask();
+      const unsigned peers = __match_any_sync(act, g);
+      const int lane = lane_id(), leader = __ffs(peers) - 1;
+      int32_t cur = 0;
+      if (lane == leader) cur = atomicAdd(A.gcur + g, take * __popc(peers));
+      cur = __shfl_sync(peers, cur, leader);
+      const int64_t base = A.goff[g] + cur + take * __popc(peers & ((1u << lane) - 1u));
 #pragma unroll
       for (int q = 0; q < MAXF; ++q)
         if (q < take) {
@@ -524,7 +532,12 @@ __global__ void k_dd_count(const int64_t* __restrict__ R_ptr, const int32_t* __r
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
        r += (int64_t)gridDim.x * blockDim.x) {
     const int32_t d = deg[r];
-    if (d > 0) atomicAdd(gcnt + vrank(vbits, vpre, rowv[r]), min(d, s));
+    if (d > 0) {
+      const int32_t g = vrank(vbits, vpre, rowv[r]);
+      const unsigned act = __activemask();
+      const unsigned peers = __match_any_sync(act, g);  // same vertex -> same take
+      if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(gcnt + g, min(d, s) * __popc(peers));
+    }
   }
 }
 
