@@ -156,9 +156,10 @@ def kernel_bytes(s, kernel):
     if kernel == "stream":
         return 32 * s["R"] + 4 * s["G"] + 8 * s["F"]
     if kernel == "dedup":
-        # k_dd_stream: per distinct row vertex 4 + row_ptr 8 + offsets 8, 4 per
-        # entry of every DISTINCT row, pick record 8 + col 4 + batch bit 4
-        return 20 * s["D"] + 4 * s["G_distinct"] + 16 * s["F"]
+        # k_dd_serve: per distinct row vertex 4 + row_ptr 8 + row-list offset
+        # 8, per frontier row its offset 4 + batch 4, 4 per entry of every
+        # DISTINCT row, pick idx 4 + col write 4 + batch bit 4 per pick
+        return 20 * s["D"] + 8 * s["R"] + 4 * s["G_distinct"] + 12 * s["F"]
     if kernel == "pick":
         return 12 * s["R"] + 4 * s["F"]
     return 24 * s["R"] + 8 * s["F"]
@@ -412,7 +413,7 @@ def run_ours(args, rank, world, local_rank):
     peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(REPO, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    KERNEL = {"stream": "k_sage_stream", "dedup": "k_dd_stream", "pfree": "k_sage_pick<true>"}
+    KERNEL = {"stream": "k_sage_stream", "dedup": "k_dd_serve", "pfree": "k_sage_pick<true>"}
     kb = [kernel_bytes(s, args.mode) for s in st]
     kern_avg = kern_ms.mean(axis=0)[:, -1]  # dominant kernel, per layer
     pick_avg = kern_ms.mean(axis=0)[:, 0]

@@ -181,13 +181,13 @@ struct SageArgs {
   int64_t nwords;
   int32_t* fcol;         // frontier columns (output)
   int32_t* pidx;         // stream mode: row-relative pick indices (scratch)
-  // dedup mode: pick records grouped by distinct row vertex
-  const uint32_t* vbits;
-  const int32_t* vpre;
-  const int64_t* goff;
-  int32_t* gcur;
-  uint64_t* pk;
-  int32_t* pkb;
+  // dedup mode (OUT 2): frontier rows grouped by vertex, per grouped row its
+  // frontier offset and batch, picks at pidx[q * s ..]
+  const int64_t* D_ptr;
+  const int64_t* roff;
+  const int32_t* grow;
+  int32_t* rfp;
+  int32_t* rbb;
 };
 
 __device__ __forceinline__ int32_t vrank(const uint32_t* vbits, const int32_t* vpre, int32_t v) {
@@ -199,7 +199,6 @@ constexpr int kStreamThreads = 256;
 constexpr int kRowCost = 48;       // merge-path weight of one row (in entries)
 constexpr int kStreamUnroll = 8;   // 16-B loads in flight per lane
 constexpr int kBrowSmem = 1024;
-constexpr int kMaxFan = 32;
 
 __device__ __forceinline__ int4 ld_stream_v4(const int32_t* p) {
   int4 r;
@@ -221,8 +220,9 @@ __device__ __forceinline__ int64_t batch_of(const int64_t* sb, const int64_t* gb
   return lo;
 }
 
-// Replay table of one degree read through the read-only path (L1-resident:
-// ~1.4 KB per hot degree) with its binade index.
+// Replay table of one degree with its binade index: read through the
+// read-only path (L1-resident, ~1.4 KB per hot degree; SM = false) or from a
+// shared-memory copy (SM = true, the fused dedup kernel).
 struct GTable {
   const int32_t* j0;
   const double* s0;
@@ -232,31 +232,38 @@ struct GTable {
   uint64_t top;  // binade of the last run's start
 };
 
+template <bool SM, typename T>
+__device__ __forceinline__ T tld(const T* p) {
+  if constexpr (SM) return *p; else return __ldg(p);
+}
+
 // S[n], 1 <= n <= m: n_live is near m, so scan back from the last run
+template <bool SM = false>
 __device__ __forceinline__ double gt_S(const GTable& t, int64_t n) {
   int r = t.nr - 1;
-  int32_t j0 = __ldg(t.j0 + r);
-  while (j0 > n) j0 = __ldg(t.j0 + --r);
-  return __dadd_rn(__ldg(t.s0 + r), __dmul_rn((double)(n - j0), __ldg(t.d + r)));
+  int32_t j0 = tld<SM>(t.j0 + r);
+  while (j0 > n) j0 = tld<SM>(t.j0 + --r);
+  return __dadd_rn(tld<SM>(t.s0 + r), __dmul_rn((double)(n - j0), tld<SM>(t.d + r)));
 }
 
 // first j >= 1 with S[j] > target (m + 1 when none).  The run is located by
 // the binade index (O(1)), the position inside it by a float estimate that
 // the exact fp64 comparisons then correct.
+template <bool SM = false>
 __device__ __forceinline__ int64_t gt_first_gt(const GTable& t, double target) {
-  if (target < __ldg(t.s0)) return 1;
+  if (target < tld<SM>(t.s0)) return 1;
   const int64_t off = (int64_t)t.top - (int64_t)binade(target);
-  int r = off < 0 ? t.nr : (int)__ldg(t.lower + (off < kBinades ? off : kBinades - 1));
+  int r = off < 0 ? t.nr : (int)tld<SM>(t.lower + (off < kBinades ? off : kBinades - 1));
   // r = first run starting in target's binade or above; step back / forward
-  if (r >= t.nr || __ldg(t.s0 + r) > target) {
+  if (r >= t.nr || tld<SM>(t.s0 + r) > target) {
     r = r - 1;
   } else {
-    while (r + 1 < t.nr && __ldg(t.s0 + r + 1) <= target) ++r;
+    while (r + 1 < t.nr && tld<SM>(t.s0 + r + 1) <= target) ++r;
   }
-  const int64_t j0 = __ldg(t.j0 + r);
-  const int64_t len = (int64_t)__ldg(t.j0 + r + 1) - j0;
+  const int64_t j0 = tld<SM>(t.j0 + r);
+  const int64_t len = (int64_t)tld<SM>(t.j0 + r + 1) - j0;
   if (len == 1) return j0 + 1;
-  const double s0 = __ldg(t.s0 + r), d = __ldg(t.d + r);
+  const double s0 = tld<SM>(t.s0 + r), d = tld<SM>(t.d + r);
   int64_t q = (int64_t)__fdividef((float)(target - s0), (float)d);
   q = q < 0 ? 0 : (q > len - 1 ? len - 1 : q);
   while (q > 0 && __dadd_rn(s0, __dmul_rn((double)q, d)) > target) --q;
@@ -272,20 +279,22 @@ __device__ __forceinline__ int64_t gt_first_gt(const GTable& t, double target) {
 // Picks are kept sorted (frontier_from_rows sorts, sampler.py:216) in
 // registers (MAXF = fanout bucket, fully unrolled).
 // OUT 1 (P-free): read the picked columns of A directly and finish the row;
-// OUT 0: write the row-relative indices for the row-streaming kernel;
-// OUT 2 (dedup): write pick records straight into the row's vertex group.
+// OUT 0: write the row-relative indices for the row-streaming kernel.
 template <int OUT, int MAXF>
 __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
                                                           const int64_t* __restrict__ R_ptr) {
   __shared__ int64_t s_brow[kBrowSmem];
-  const int64_t R = *R_ptr;
+  // OUT 2 walks the frontier rows grouped by vertex (rows of one vertex in
+  // adjacent lanes share the replay-table loads)
+  const int64_t R = OUT == 2 ? A.roff[*A.D_ptr] : *R_ptr;
   const bool keyed = A.rowkeys != nullptr;  // explicit keys: no batch structure
   const bool brow_in_smem = !keyed && A.k + 1 <= kBrowSmem;
   if (brow_in_smem)
     for (int64_t i = threadIdx.x; i <= A.k; i += blockDim.x) s_brow[i] = A.brow[i];
   __syncthreads();
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
-       r += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < R;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = OUT == 2 ? (int64_t)A.grow[q] : q;
     const int32_t deg = A.deg[r];
     if (deg == 0) continue;  // empty P row (sample_rows_ordered, sampler.py:202-204)
     const int32_t take = min(deg, A.s);
@@ -293,7 +302,7 @@ __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
     const int64_t bb = keyed ? 0 : batch_of(s_brow, A.brow, A.k, r);
     int32_t sorted[MAXF];
 #pragma unroll
-    for (int q = 0; q < MAXF; ++q) sorted[q] = q;  // exhaustion: every index (sampler.py:172-174)
+    for (int z = 0; z < MAXF; ++z) sorted[z] = z;  // exhaustion: every index (sampler.py:172-174)
     if (take < deg) {
       // global_row_keys (sampler.py:309-322), or the requester's keys
       uint64_t key;
@@ -327,52 +336,43 @@ __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
         int32_t x = (int32_t)(j - 1);
         int i = 0;
 #pragma unroll
-        for (int q = 0; q < MAXF; ++q)
-          if (q < t && sorted[q] <= x) { ++x; ++i; }
+        for (int z = 0; z < MAXF; ++z)
+          if (z < t && sorted[z] <= x) { ++x; ++i; }
 #pragma unroll
-        for (int q = MAXF - 1; q > 0; --q)
-          if (q > i && q <= t) sorted[q] = sorted[q - 1];
+        for (int z = MAXF - 1; z > 0; --z)
+          if (z > i && z <= t) sorted[z] = sorted[z - 1];
 #pragma unroll
-        for (int q = 0; q < MAXF; ++q)
-          if (q == i) sorted[q] = x;
+        for (int z = 0; z < MAXF; ++z)
+          if (z == i) sorted[z] = x;
       }
     }
     if (OUT == 1) {
       const int64_t rs = A.rowptr[A.rowv[r]];
       int32_t cv[MAXF];
 #pragma unroll
-      for (int q = 0; q < MAXF; ++q)
-        if (q < take) cv[q] = __ldg(A.col + rs + sorted[q]);
+      for (int z = 0; z < MAXF; ++z)
+        if (z < take) cv[z] = __ldg(A.col + rs + sorted[z]);
 #pragma unroll
-      for (int q = 0; q < MAXF; ++q)
-        if (q < take) A.fcol[fp + q] = cv[q];
+      for (int z = 0; z < MAXF; ++z)
+        if (z < take) A.fcol[fp + z] = cv[z];
       if (A.bitmap) {
         uint32_t* bm = A.bitmap + bb * A.nwords;
 #pragma unroll
-        for (int q = 0; q < MAXF; ++q)
-          if (q < take) atomicOr(bm + (cv[q] >> 5), 1u << (cv[q] & 31));
+        for (int z = 0; z < MAXF; ++z)
+          if (z < take) atomicOr(bm + (cv[z] >> 5), 1u << (cv[z] & 31));
       }
     } else if (OUT == 2) {
-      const int32_t g = vrank(A.vbits, A.vpre, A.rowv[r]);
-      // rows of one vertex have the same degree, hence the same take:
-      // one cursor atomic per vertex per warp (hub groups are hot)
-      const unsigned act = __activemask();
-      const unsigned peers = __match_any_sync(act, g);
-      const int lane = lane_id(), leader = __ffs(peers) - 1;
-      int32_t cur = 0;
-      if (lane == leader) cur = atomicAdd(A.gcur + g, take * __popc(peers));
-      cur = __shfl_sync(peers, cur, leader);
-      const int64_t base = A.goff[g] + cur + take * __popc(peers & ((1u << lane) - 1u));
+      A.rfp[q] = (int32_t)fp;
+      A.rbb[q] = (int32_t)bb;
+      if (take < deg) {
 #pragma unroll
-      for (int q = 0; q < MAXF; ++q)
-        if (q < take) {
-          A.pk[base + q] = ((uint64_t)(uint32_t)sorted[q] << 32) | (uint64_t)(fp + q);
-          A.pkb[base + q] = (int32_t)bb;
-        }
+        for (int t = 0; t < MAXF; ++t)
+          if (t < take) A.pidx[q * A.s + t] = sorted[t];
+      }
     } else {
 #pragma unroll
-      for (int q = 0; q < MAXF; ++q)
-        if (q < take) A.pidx[fp + q] = sorted[q];
+      for (int t = 0; t < MAXF; ++t)
+        if (t < take) A.pidx[fp + t] = sorted[t];
     }
   }
 }
@@ -492,8 +492,10 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k_sage_stream(SageArgs A,
 // Frontier rows repeat vertices heavily (hub bias: 3.5M rows over 0.55M
 // distinct vertices in layer 3 at products scale), and identical rows of
 // Q^l give identical rows of P = Q^l A.  Each distinct P row is formed on
-// chip once — the A row streamed through shared memory — and serves the
-// picks of every frontier row that references it.
+// chip once per work item — the A row and its degree's replay table staged
+// in shared memory — and every frontier row that references it draws its
+// picks from there: NORM + SAMPLE + the P-row gather in one kernel, with no
+// per-row global table look-ups and no intermediate pick records.
 
 // one bit per vertex that some row of the layer references
 __global__ void k_dd_mark(const int64_t* __restrict__ R_ptr, const int32_t* __restrict__ rowv,
@@ -507,10 +509,9 @@ __global__ void k_dd_mark(const int64_t* __restrict__ R_ptr, const int32_t* __re
     }
 }
 
-// distinct vertex list (ascending) and its degrees
+// distinct vertex list (ascending)
 __global__ void k_dd_list(int64_t nwords, const uint32_t* __restrict__ vbits,
-                          const int32_t* __restrict__ vpre, const int64_t* __restrict__ rowptr,
-                          int32_t* __restrict__ dv) {
+                          const int32_t* __restrict__ vpre, int32_t* __restrict__ dv) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nwords;
        i += (int64_t)gridDim.x * blockDim.x) {
     uint32_t x = vbits[i];
@@ -523,20 +524,38 @@ __global__ void k_dd_list(int64_t nwords, const uint32_t* __restrict__ vbits,
   }
 }
 
-// picks per distinct vertex
-__global__ void k_dd_count(const int64_t* __restrict__ R_ptr, const int32_t* __restrict__ rowv,
-                           const int32_t* __restrict__ deg, int32_t s,
-                           const uint32_t* __restrict__ vbits, const int32_t* __restrict__ vpre,
-                           int32_t* __restrict__ gcnt) {
+// rows per distinct vertex (one atomic per vertex per warp: hub groups are hot)
+__global__ void k_dd_rcount(const int64_t* __restrict__ R_ptr, const int32_t* __restrict__ rowv,
+                            const int32_t* __restrict__ deg, const uint32_t* __restrict__ vbits,
+                            const int32_t* __restrict__ vpre, int32_t* __restrict__ gcnt) {
   const int64_t R = *R_ptr;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
        r += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t d = deg[r];
-    if (d > 0) {
+    if (deg[r] > 0) {
       const int32_t g = vrank(vbits, vpre, rowv[r]);
-      const unsigned act = __activemask();
-      const unsigned peers = __match_any_sync(act, g);  // same vertex -> same take
-      if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(gcnt + g, min(d, s) * __popc(peers));
+      const unsigned peers = __match_any_sync(__activemask(), g);
+      if (lane_id() == __ffs(peers) - 1) atomicAdd(gcnt + g, __popc(peers));
+    }
+  }
+}
+
+// frontier rows grouped by vertex: grow[roff[g] ..) (order inside a group is
+// irrelevant — every row's output is independent)
+__global__ void k_dd_rows(const int64_t* __restrict__ R_ptr, const int32_t* __restrict__ rowv,
+                          const int32_t* __restrict__ deg, const uint32_t* __restrict__ vbits,
+                          const int32_t* __restrict__ vpre, const int64_t* __restrict__ roff,
+                          int32_t* __restrict__ gcur, int32_t* __restrict__ grow) {
+  const int64_t R = *R_ptr;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    if (deg[r] > 0) {
+      const int32_t g = vrank(vbits, vpre, rowv[r]);
+      const unsigned peers = __match_any_sync(__activemask(), g);
+      const int lane = lane_id(), leader = __ffs(peers) - 1;
+      int32_t cur = 0;
+      if (lane == leader) cur = atomicAdd(gcur + g, __popc(peers));
+      cur = __shfl_sync(peers, cur, leader);
+      grow[roff[g] + cur + __popc(peers & ((1u << lane) - 1u))] = (int32_t)r;
     }
   }
 }
@@ -546,148 +565,136 @@ struct GcntF {
   __device__ int64_t operator()(int64_t i) const { return c[i]; }
 };
 
-// pick records of every row into its vertex group: (row-relative index,
-// frontier position), packed as idx << 32 | pos
-__global__ void k_dd_scatter(const int64_t* __restrict__ R_ptr, const int32_t* __restrict__ rowv,
-                             const int32_t* __restrict__ deg, int32_t s,
-                             const int64_t* __restrict__ fptr, const int32_t* __restrict__ pidx,
-                             const uint32_t* __restrict__ vbits, const int32_t* __restrict__ vpre,
-                             const int64_t* __restrict__ goff, int32_t* __restrict__ gcur,
-                             uint64_t* __restrict__ pk, int32_t* __restrict__ pkb,
-                             const int64_t* __restrict__ brow, int64_t k) {
-  const int64_t R = *R_ptr;
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
-       r += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t d = deg[r];
-    if (d <= 0) continue;
-    const int32_t take = min(d, s);
-    const int32_t g = vrank(vbits, vpre, rowv[r]);
-    const int64_t base = goff[g] + atomicAdd(gcur + g, take);
-    const int64_t fp = fptr[r];
-    int64_t lo = 0, hi = k;  // batch of row r (carried with the picks)
-    while (hi - lo > 1) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (__ldg(brow + mid) <= r) lo = mid; else hi = mid;
-    }
-    for (int t = 0; t < take; ++t) {
-      pk[base + t] = ((uint64_t)(uint32_t)pidx[fp + t] << 32) | (uint64_t)(fp + t);
-      pkb[base + t] = (int32_t)lo;
-    }
-  }
-}
-
-// Size tiers of distinct rows (degree d): 0 warp per row (d <= 1K, 4 KB
-// stage), 1 CTA-256 per row (d <= 8K, 32 KB stage), 2 CTA-1024 per row
-// (hubs, 192 KB stage, <= 4 passes over the row's picks at products scale).
-constexpr int kDdThreads = 256;
-constexpr int kDdUnroll = 4;  // 16-B loads in flight per thread while staging
+// Size tiers of distinct rows (degree d): 0 warp per item (d <= 1K, row
+// staged whole, 4 KB), 1 CTA-256 per item (d <= 8K, 32 KB), 2 CTA-1024 per
+// item (hubs, staged in chunks as large as shared memory allows).  A work
+// item is one distinct row and the picks of at most rows_item[tier] of the
+// frontier rows that reference it (about kPicks picks).
 template <int T> struct DdTier;
 template <> struct DdTier<0> {
-  static constexpr int kChunk = 1024, kThreads = 256, kLo = 0, kHi = 1024, kPicks = 0;
+  static constexpr int kThreads = 256, kHi = 1024, kPicks = 512;
   static constexpr bool kWarp = true;
 };
 template <> struct DdTier<1> {
-  static constexpr int kChunk = 8192, kThreads = 256, kLo = 1024, kHi = 8192, kPicks = 2048;
+  static constexpr int kThreads = 256, kHi = 8192, kPicks = 2048;
   static constexpr bool kWarp = false;
 };
 template <> struct DdTier<2> {
-  static constexpr int kChunk = 49152, kThreads = 1024, kLo = 8192, kHi = 0x7fffffff, kPicks = 8192;
+  static constexpr int kThreads = 1024, kHi = 0x7fffffff, kPicks = 8192;
   static constexpr bool kWarp = false;
 };
+__host__ __device__ __forceinline__ int dd_tier(int64_t d) {
+  return d <= DdTier<0>::kHi ? 0 : d <= DdTier<1>::kHi ? 1 : 2;
+}
 
-// work items of a CTA tier: ceil(picks / kPicks) per distinct row of the tier
-template <int T>
+struct DdItems {
+  int32_t rows[3];  // rows per work item, per tier
+};
+
+// Tier-major work-item prefix in one scan: virtual index i = tier * D + g
 struct ItemF {
   const int32_t* dv;
   const int64_t* rowptr;
-  const int64_t* goff;
-  __device__ int64_t operator()(int64_t g) const {
+  const int32_t* gcnt;
+  const int64_t* D_ptr;
+  DdItems it;
+  __device__ int64_t operator()(int64_t i) const {
+    const int64_t D = *D_ptr;
+    const int64_t t = i / D, g = i - t * D;
     const int32_t v = dv[g];
     const int64_t d = rowptr[v + 1] - rowptr[v];
-    if (d <= DdTier<T>::kLo || d > DdTier<T>::kHi) return 0;
-    const int64_t p = goff[g + 1] - goff[g];
-    return (p + DdTier<T>::kPicks - 1) / DdTier<T>::kPicks;
+    if (dd_tier(d) != t) return 0;
+    const int64_t rows = it.rows[t];
+    return (gcnt[g] + rows - 1) / rows;
   }
 };
-constexpr int kDdWarpChunk = 1024;
 
-__device__ __forceinline__ void dd_emit(int32_t c, uint64_t rec, int32_t batch, int32_t* fcol,
-                                        uint32_t* bitmap, int64_t nwords) {
-  fcol[(int64_t)(rec & 0xffffffffu)] = c;
-  atomicOr(bitmap + (int64_t)batch * nwords + (c >> 5), 1u << (c & 31));
+__global__ void k_dd_3d(const int32_t* __restrict__ dcount, int64_t* __restrict__ out) {
+  out[0] = *dcount;      // D
+  out[1] = 3 * *dcount;  // tier-major item index space
 }
 
-// Stream every distinct A row once and serve its picks; TIER selects the
-// row sizes handled and warp / CTA granularity.
-template <int TIER>
-__global__ void __launch_bounds__(DdTier<TIER>::kThreads) k_dd_stream(
-    const int64_t* __restrict__ D_ptr, const int32_t* __restrict__ dv,
-    const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
-    const int64_t* __restrict__ goff, const uint64_t* __restrict__ pk,
-    const int32_t* __restrict__ pkb, int32_t* __restrict__ fcol,
-    uint32_t* __restrict__ bitmap, int64_t nwords, const int64_t* __restrict__ ioff) {
-  constexpr bool LARGE = !DdTier<TIER>::kWarp;
-  constexpr int kChunk = DdTier<TIER>::kChunk;
-  constexpr int kSlotLen = kChunk + 4;
-  extern __shared__ __align__(16) int32_t sdyn[];  // [slots][kSlotLen]
+// item -> group map of every tier
+__global__ void k_dd_items(const int64_t* __restrict__ D_ptr, const int32_t* __restrict__ dv,
+                           const int64_t* __restrict__ rowptr, const int64_t* __restrict__ ioff,
+                           int32_t* __restrict__ igrp) {
   const int64_t D = *D_ptr;
-  const int lane = lane_id();
-  const int tid = LARGE ? threadIdx.x : lane;
-  const int nthr = LARGE ? blockDim.x : 32;
-  int32_t* buf = sdyn + (LARGE ? 0 : (threadIdx.x >> 5) * kSlotLen);
-  const int64_t first = LARGE ? blockIdx.x : global_warp();
-  const int64_t step = LARGE ? gridDim.x : grid_warps();
-  // warp tier: one distinct row per warp; CTA tiers: work items of at most
-  // kPicks picks of one row (item prefix ioff over the rows of the tier)
-  const int64_t nitems = LARGE ? ioff[D] : D;
-  for (int64_t it = first; it < nitems; it += step) {
-    int64_t g = it, p0, p1;
-    if (LARGE) {
-      int64_t lo = 0, hi = D;  // last g with ioff[g] <= it
-      while (hi - lo > 1) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (ioff[mid] <= it) lo = mid; else hi = mid;
-      }
-      g = lo;
-      p0 = goff[g] + (it - ioff[g]) * DdTier<TIER>::kPicks;
-      p1 = min(p0 + (int64_t)DdTier<TIER>::kPicks, goff[g + 1]);
-    } else {
-      p0 = goff[g];
-      p1 = goff[g + 1];
-    }
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < D;
+       g += (int64_t)gridDim.x * blockDim.x) {
     const int32_t v = dv[g];
-    const int64_t a0 = rowptr[v], d = rowptr[v + 1] - a0;
-    if (d <= DdTier<TIER>::kLo || d > DdTier<TIER>::kHi) continue;
-    for (int64_t c0 = 0; c0 < d; c0 += kChunk) {
-      const int64_t c1 = min(c0 + (int64_t)kChunk, d);
-      // stage entries [c0, c1) of A row v: the P row on chip (16-B aligned
-      // vector loads, kDdUnroll in flight per thread)
-      const int64_t e0 = a0 + c0, e1 = a0 + c1;
-      const int64_t al0 = e0 & ~3LL;
-      for (int64_t eb = al0 + 4 * tid; eb < e1; eb += 4 * nthr * kDdUnroll) {
-        int4 x[kDdUnroll];
-#pragma unroll
-        for (int u = 0; u < kDdUnroll; ++u) {
-          const int64_t e = eb + 4 * nthr * u;
-          x[u] = e < e1 ? ld_stream_v4(col + e) : make_int4(0, 0, 0, 0);
-        }
-#pragma unroll
-        for (int u = 0; u < kDdUnroll; ++u) {
-          const int64_t e = eb + 4 * nthr * u;
-          const int64_t o = e - e0;  // may be -3..-1 for the aligned head
-          if (o + 0 >= 0 && e + 0 < e1) buf[o + 0] = x[u].x;
-          if (o + 1 >= 0 && e + 1 < e1) buf[o + 1] = x[u].y;
-          if (o + 2 >= 0 && e + 2 < e1) buf[o + 2] = x[u].z;
-          if (o + 3 >= 0 && e + 3 < e1) buf[o + 3] = x[u].w;
+    const int t = dd_tier(rowptr[v + 1] - rowptr[v]);
+    const int64_t o0 = ioff[t * D + g], o1 = ioff[t * D + g + 1];
+    for (int64_t o = o0; o < o1; ++o) igrp[o] = (int32_t)g;
+  }
+}
+
+struct DdArgs {
+  const int64_t* D_ptr;
+  const int32_t* dv;
+  const int64_t* rowptr;
+  const int32_t* col;
+  const int64_t* roff;   // group row-list offsets (D + 1)
+  const int64_t* ioff;   // tier-major item prefix (3D + 1)
+  const int32_t* igrp;   // item -> group
+  const int32_t* pidx;   // sorted picks of grouped row q at pidx[q * s ..]
+  const int32_t* rfp;    // frontier offset of grouped row q
+  const int32_t* rbb;    // batch of grouped row q
+  int32_t s;
+  int32_t rows_item;
+  int32_t chunk;         // A-row entries staged per pass
+  int32_t* fcol;
+  uint32_t* bitmap;
+  int64_t nwords;
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+}
+
+// Q^l A for the distinct rows: per work item, A row v staged in shared
+// memory (16-B cp.async; buf[e - (e0 & ~3)]) — the P row on chip once —
+// then every pick of the item's frontier rows is served from it: frontier
+// write and the (batch, vertex) bit.
+template <int TIER>
+__global__ void __launch_bounds__(DdTier<TIER>::kThreads) k_dd_serve(DdArgs A) {
+  constexpr bool CTA = !DdTier<TIER>::kWarp;
+  extern __shared__ __align__(16) int32_t sbuf[];
+  const int chunk = A.chunk, s = A.s;
+  const int tid = CTA ? threadIdx.x : lane_id();
+  const int nthr = CTA ? blockDim.x : 32;
+  int32_t* buf = sbuf + (CTA ? 0 : (threadIdx.x >> 5) * (chunk + 8));
+  const int64_t D = *A.D_ptr;
+  const int64_t it0 = A.ioff[TIER * D], it1 = A.ioff[(TIER + 1) * D];
+  const int64_t step = CTA ? gridDim.x : grid_warps();
+  for (int64_t it = it0 + (CTA ? blockIdx.x : global_warp()); it < it1; it += step) {
+    const int32_t g = A.igrp[it];
+    const int64_t q0 = A.roff[g] + (it - A.ioff[TIER * D + g]) * A.rows_item;
+    const int nrows = (int)min((int64_t)A.rows_item, A.roff[g + 1] - q0);
+    const int32_t v = A.dv[g];
+    const int64_t a0 = A.rowptr[v];
+    const int32_t d = (int32_t)(A.rowptr[v + 1] - a0);
+    const int32_t take = min(d, s);
+    const bool all = take == d;  // exhaustion: every entry, in order
+    for (int64_t c0 = 0; c0 < d; c0 += chunk) {
+      const int64_t c1 = min(c0 + (int64_t)chunk, (int64_t)d);
+      const int64_t al0 = (a0 + c0) & ~3LL;
+      for (int64_t e = al0 + 4 * tid; e < a0 + c1; e += 4 * nthr)
+        cp_async16(buf + (e - al0), A.col + e);
+      asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+      if (CTA) __syncthreads(); else __syncwarp();
+      const int32_t sh = (int32_t)((a0 + c0) - al0 - c0);  // buf[idx + sh], idx in [c0, c1)
+      for (int p = tid; p < nrows * take; p += nthr) {
+        const int i = p / take, t = p - i * take;
+        const int64_t q = q0 + i;
+        const int32_t idx = all ? t : A.pidx[q * s + t];
+        if (idx >= c0 && idx < c1) {
+          const int32_t c = buf[idx + sh];
+          A.fcol[A.rfp[q] + t] = c;
+          atomicOr(A.bitmap + (int64_t)A.rbb[q] * A.nwords + (c >> 5), 1u << (c & 31));
         }
       }
-      if (LARGE) __syncthreads(); else __syncwarp();
-      for (int64_t p = p0 + tid; p < p1; p += nthr) {
-        const uint64_t rec = pk[p];
-        const int64_t idx = (int64_t)(rec >> 32);
-        if (idx >= c0 && idx < c1) dd_emit(buf[idx - c0], rec, pkb[p], fcol, bitmap, nwords);
-      }
-      if (LARGE) __syncthreads(); else __syncwarp();
+      if (CTA) __syncthreads(); else __syncwarp();
     }
   }
 }
@@ -863,13 +870,14 @@ struct SageWs {
   int32_t* vpre;     // popcount prefix of vbits
   int64_t* d_nw;     // device scalars: nwords, D
   int32_t* dv;       // distinct vertices
-  int32_t* gcnt;     // picks per distinct vertex
+  int32_t* gcnt;     // frontier rows per distinct vertex
   int32_t* gcur;
-  int64_t* goff;
-  uint64_t* pk;      // pick records grouped by vertex
-  int32_t* pkb;      // batch of each pick record
-  int64_t* ioff1;    // work-item prefixes of the CTA tiers
-  int64_t* ioff2;
+  int64_t* roff;     // group offsets into grow
+  int32_t* grow;     // frontier rows grouped by vertex
+  int64_t* ioff;     // tier-major work-item prefix [3 * r_cap + 1]
+  int32_t* igrp;     // work item -> group
+  int32_t* rfp;      // per grouped row: frontier offset
+  int32_t* rbb;      // per grouped row: batch
   size_t bytes;
 };
 
@@ -880,7 +888,7 @@ static SageWs sage_ws_layout(char* base, int64_t k, int64_t n, int64_t r_cap_max
   SageWs w{};
   const int64_t nwords = (n + 31) / 32;
   const int64_t W = k * nwords;
-  int64_t scan_n = r_cap_max > W ? r_cap_max : W;
+  int64_t scan_n = 3 * r_cap_max > W ? 3 * r_cap_max : W;
   if (nwords > scan_n) scan_n = nwords;
   size_t off = 0;
   auto take = [&](size_t bytes) { char* p = base ? base + off : nullptr; off += align_up(bytes); return p; };
@@ -893,15 +901,17 @@ static SageWs sage_ws_layout(char* base, int64_t k, int64_t n, int64_t r_cap_max
   w.d_W = (int64_t*)take(sizeof(int64_t));
   w.vbits = (uint32_t*)take(sizeof(uint32_t) * (nwords + 1));
   w.vpre = (int32_t*)take(sizeof(int32_t) * (nwords + 1));
-  w.d_nw = (int64_t*)take(sizeof(int64_t) * 2);
+  w.d_nw = (int64_t*)take(sizeof(int64_t) * 3);
   w.dv = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
   w.gcnt = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
   w.gcur = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
-  w.goff = (int64_t*)take(sizeof(int64_t) * (r_cap_max + 1));
-  w.pk = (uint64_t*)take(sizeof(uint64_t) * (f_cap_max + 1));
-  w.pkb = (int32_t*)take(sizeof(int32_t) * (f_cap_max + 1));
-  w.ioff1 = (int64_t*)take(sizeof(int64_t) * (r_cap_max + 1));
-  w.ioff2 = (int64_t*)take(sizeof(int64_t) * (r_cap_max + 1));
+  w.roff = (int64_t*)take(sizeof(int64_t) * (r_cap_max + 1));
+  w.grow = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
+  w.ioff = (int64_t*)take(sizeof(int64_t) * (3 * r_cap_max + 1));
+  // items <= groups + rows / 32 <= 2 * rows
+  w.igrp = (int32_t*)take(sizeof(int32_t) * (2 * r_cap_max + 2));
+  w.rfp = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
+  w.rbb = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
   w.bytes = off;
   return w;
 }
@@ -921,37 +931,16 @@ struct VPopF {
   __device__ int64_t operator()(int64_t i) const { return __popc(b[i]); }
 };
 
-template <int T>
-static int launch_dd(SageWs& ws, const Graph* g, gb_sage_layer_out& o, int64_t k, int64_t nwords,
-                     int64_t r_cap, cudaStream_t st) {
-  using Tr = DdTier<T>;
-  const size_t smem = sizeof(int32_t) * (Tr::kChunk + 4) * (Tr::kWarp ? Tr::kThreads / 32 : 1);
-  static int grid = 0;
-  if (!grid) {
-    cudaFuncSetAttribute(k_dd_stream<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int occ = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dd_stream<T>, Tr::kThreads, smem);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    grid = (occ > 0 ? occ : 1) * (sms > 0 ? sms : kNumSMs);
-  }
-  int64_t* ioff = nullptr;
-  if (!Tr::kWarp) {
-    ioff = T == 1 ? ws.ioff1 : ws.ioff2;
-    int rc = device_exclusive_scan<int64_t>(ws.d_nw + 1, r_cap, ItemF<T>{ws.dv, g->rowptr, ws.goff},
-                                            ioff, ws.scan_ws, st);
-    if (rc) return rc;
-  }
-  k_dd_stream<T><<<grid, Tr::kThreads, smem, st>>>(ws.d_nw + 1, ws.dv, g->rowptr, g->col,
-                                                    ws.goff, ws.pk, ws.pkb, o.fcol, ws.bitmap,
-                                                    nwords, ioff);
-  GB_LAUNCH_CHECK("k_dd_stream");
-  return GB_OK;
+static DdItems dd_items(int32_t s) {
+  DdItems it;
+  it.rows[0] = max(1, DdTier<0>::kPicks / s);
+  it.rows[1] = max(1, DdTier<1>::kPicks / s);
+  it.rows[2] = max(1, DdTier<2>::kPicks / s);
+  return it;
 }
 
-// Dedup stream step of one layer (pidx from k_sage_pick<false> in place).
-// Dedup step 1 (before the pick kernel): distinct row vertices, picks per
-// vertex (from the degrees alone) and the group offsets the pick kernel
-// writes its records into.
+// Dedup step 1: distinct row vertices, the frontier rows of each grouped
+// together, and the tier-major work items of the serve kernels.
 static int dedup_prepare(const Graph* g, SageWs& ws, const int64_t* R_ptr, const int32_t* rowv,
                          int32_t s, int64_t r_cap, int64_t nwords, cudaStream_t st) {
   const int64_t gw = 16 * kNumSMs;
@@ -962,29 +951,63 @@ static int dedup_prepare(const Graph* g, SageWs& ws, const int64_t* R_ptr, const
   int rc = device_exclusive_scan<int64_t>(ws.d_nw, nwords, VPopF{ws.vbits}, ws.vpre, ws.scan_ws,
                                           st);
   if (rc) return rc;
-  k_i32_to_i64<<<1, 1, 0, st>>>(ws.vpre + nwords, ws.d_nw + 1);
-  k_dd_list<<<grid_for(nwords, 256, gw), 256, 0, st>>>(nwords, ws.vbits, ws.vpre, g->rowptr, ws.dv);
-  k_dd_count<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, s, ws.vbits, ws.vpre,
-                                                      ws.gcnt);
-  rc = device_exclusive_scan<int64_t>(ws.d_nw + 1, r_cap, GcntF{ws.gcnt}, ws.goff, ws.scan_ws, st);
+  k_dd_3d<<<1, 1, 0, st>>>(ws.vpre + nwords, ws.d_nw + 1);
+  k_dd_list<<<grid_for(nwords, 256, gw), 256, 0, st>>>(nwords, ws.vbits, ws.vpre, ws.dv);
+  k_dd_rcount<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, ws.vbits, ws.vpre,
+                                                       ws.gcnt);
+  rc = device_exclusive_scan<int64_t>(ws.d_nw + 1, r_cap, GcntF{ws.gcnt}, ws.roff, ws.scan_ws, st);
   if (rc) return rc;
+  k_dd_rows<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, ws.vbits, ws.vpre,
+                                                     ws.roff, ws.gcur, ws.grow);
+  rc = device_exclusive_scan<int64_t>(ws.d_nw + 2, 3 * r_cap,
+                                      ItemF{ws.dv, g->rowptr, ws.gcnt, ws.d_nw + 1, dd_items(s)},
+                                      ws.ioff, ws.scan_ws, st);
+  if (rc) return rc;
+  k_dd_items<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(ws.d_nw + 1, ws.dv, g->rowptr, ws.ioff,
+                                                      ws.igrp);
   GB_LAUNCH_CHECK("dedup prepare");
-  count_launches(5);
+  count_launches(7);
   return GB_OK;
 }
 
-// Dedup step 2 (after the pick kernel wrote the grouped records): stream
-// every distinct row once, in three size tiers.
-static int dedup_stream(const Graph* g, SageWs& ws, gb_sage_layer_out& o, int64_t k,
-                        int64_t r_cap, int64_t nwords, cudaStream_t st) {
-  prof_mark(st);
-  int rc = launch_dd<0>(ws, g, o, k, nwords, r_cap, st);
-  if (!rc) rc = launch_dd<1>(ws, g, o, k, nwords, r_cap, st);
-  if (!rc) rc = launch_dd<2>(ws, g, o, k, nwords, r_cap, st);
-  if (rc) return rc;
-  prof_mark(st);
-  count_launches(5);
+template <int T>
+static int launch_serve(DdArgs A, cudaStream_t st) {
+  using Tr = DdTier<T>;
+  static int max_smem = 0;
+  if (!max_smem) {
+    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0);
+    if (max_smem <= 0) max_smem = 227 * 1024;
+    cudaFuncSetAttribute(k_dd_serve<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+  }
+  // chunk: the whole row for tiers 0 / 1, all of shared memory for hubs
+  A.chunk = T == 2 ? ((max_smem / 4 - 8) & ~3) : Tr::kHi;
+  A.rows_item = dd_items(A.s).rows[T];
+  const size_t smem = sizeof(int32_t) * (A.chunk + 8) * (Tr::kWarp ? Tr::kThreads / 32 : 1);
+  static int grid = 0;  // smem is fixed per tier
+  if (!grid) {
+    int occ = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dd_serve<T>, Tr::kThreads, smem);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    grid = (occ > 0 ? occ : 1) * (sms > 0 ? sms : kNumSMs);
+  }
+  k_dd_serve<T><<<grid, Tr::kThreads, smem, st>>>(A);
+  GB_LAUNCH_CHECK("k_dd_serve");
   return GB_OK;
+}
+
+// Dedup step 2 (after k_sage_pick<2> wrote the grouped picks): each
+// distinct row on chip, three size tiers.
+static int dedup_serve(const Graph* g, SageWs& ws, const SageArgs& S, cudaStream_t st) {
+  DdArgs A{};
+  A.D_ptr = ws.d_nw + 1; A.dv = ws.dv; A.rowptr = g->rowptr; A.col = g->col;
+  A.roff = ws.roff; A.ioff = ws.ioff; A.igrp = ws.igrp;
+  A.pidx = ws.pidx; A.rfp = ws.rfp; A.rbb = ws.rbb;
+  A.s = S.s; A.fcol = S.fcol; A.bitmap = S.bitmap; A.nwords = S.nwords;
+  int rc = launch_serve<0>(A, st);
+  if (!rc) rc = launch_serve<1>(A, st);
+  if (!rc) rc = launch_serve<2>(A, st);
+  count_launches(3);
+  return rc;
 }
 
 static int64_t sage_rcap_max(int64_t r1_cap, int32_t layers, const int64_t* fanouts) {
@@ -1089,28 +1112,30 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     if (dedup) {
       rc = dedup_prepare(g, ws, R_ptr, rowv, s, r_cap, nwords, st);
       if (rc) return rc;
-      A.vbits = ws.vbits; A.vpre = ws.vpre; A.goff = ws.goff; A.gcur = ws.gcur;
-      A.pk = ws.pk; A.pkb = ws.pkb;
-    }
-    prof_mark(st);
-    if (dedup)
+      A.D_ptr = ws.d_nw + 1; A.roff = ws.roff; A.grow = ws.grow; A.rfp = ws.rfp; A.rbb = ws.rbb;
+      prof_mark(st);
       launch_pick<2>(pick_grid, A, R_ptr, st);
-    else if (stream)
-      launch_pick<0>(pick_grid, A, R_ptr, st);
-    else
-      launch_pick<1>(pick_grid, A, R_ptr, st);
-    GB_LAUNCH_CHECK("k_sage_pick");
-    prof_mark(st);
-    if (stream) {
+      GB_LAUNCH_CHECK("k_sage_pick");
       prof_mark(st);
-      k_sage_stream<<<stream_grid(), kStreamThreads, 0, st>>>(A, R_ptr);
-      GB_LAUNCH_CHECK("k_sage_stream");
       prof_mark(st);
-      count_launches(1);
-    }
-    if (dedup) {
-      rc = dedup_stream(g, ws, o, k, r_cap, nwords, st);
+      rc = dedup_serve(g, ws, A, st);
       if (rc) return rc;
+      prof_mark(st);
+    } else {
+      prof_mark(st);
+      if (stream)
+        launch_pick<0>(pick_grid, A, R_ptr, st);
+      else
+        launch_pick<1>(pick_grid, A, R_ptr, st);
+      GB_LAUNCH_CHECK("k_sage_pick");
+      prof_mark(st);
+      if (stream) {
+        prof_mark(st);
+        k_sage_stream<<<stream_grid(), kStreamThreads, 0, st>>>(A, R_ptr);
+        GB_LAUNCH_CHECK("k_sage_stream");
+        prof_mark(st);
+        count_launches(1);
+      }
     }
     rc = device_exclusive_scan<int64_t>(ws.d_W, W, PopF{ws.bitmap}, ws.wpre, ws.scan_ws, st);
     if (rc) return rc;
