@@ -186,8 +186,8 @@ struct SageArgs {
   const int64_t* D_ptr;
   const int64_t* roff;
   const int32_t* grow;
-  int32_t* rfp;
-  int32_t* rbb;
+  const int32_t* rdeg;
+  const int32_t* rbb;
 };
 
 __device__ __forceinline__ int32_t vrank(const uint32_t* vbits, const int32_t* vpre, int32_t v) {
@@ -295,11 +295,12 @@ __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < R;
        q += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = OUT == 2 ? (int64_t)A.grow[q] : q;
-    const int32_t deg = A.deg[r];
+    const int32_t deg = OUT == 2 ? A.rdeg[q] : A.deg[r];
     if (deg == 0) continue;  // empty P row (sample_rows_ordered, sampler.py:202-204)
     const int32_t take = min(deg, A.s);
-    const int64_t fp = A.fptr[r];
-    const int64_t bb = keyed ? 0 : batch_of(s_brow, A.brow, A.k, r);
+    if (OUT == 2 && take == deg) continue;  // served in order by k_dd_serve
+    const int64_t fp = OUT == 2 ? 0 : A.fptr[r];
+    const int64_t bb = keyed ? 0 : OUT == 2 ? A.rbb[q] : batch_of(s_brow, A.brow, A.k, r);
     int32_t sorted[MAXF];
 #pragma unroll
     for (int z = 0; z < MAXF; ++z) sorted[z] = z;  // exhaustion: every index (sampler.py:172-174)
@@ -362,13 +363,9 @@ __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
           if (z < take) atomicOr(bm + (cv[z] >> 5), 1u << (cv[z] & 31));
       }
     } else if (OUT == 2) {
-      A.rfp[q] = (int32_t)fp;
-      A.rbb[q] = (int32_t)bb;
-      if (take < deg) {
 #pragma unroll
-        for (int t = 0; t < MAXF; ++t)
-          if (t < take) A.pidx[q * A.s + t] = sorted[t];
-      }
+      for (int t = 0; t < MAXF; ++t)
+        if (t < take) A.pidx[q * A.s + t] = sorted[t];
     } else {
 #pragma unroll
       for (int t = 0; t < MAXF; ++t)
@@ -540,22 +537,36 @@ __global__ void k_dd_rcount(const int64_t* __restrict__ R_ptr, const int32_t* __
 }
 
 // frontier rows grouped by vertex: grow[roff[g] ..) (order inside a group is
-// irrelevant — every row's output is independent)
+// irrelevant — every row's output is independent), with each grouped row's
+// degree, batch and frontier offset so the pick and serve kernels read them
+// in order instead of gathering them
 __global__ void k_dd_rows(const int64_t* __restrict__ R_ptr, const int32_t* __restrict__ rowv,
-                          const int32_t* __restrict__ deg, const uint32_t* __restrict__ vbits,
-                          const int32_t* __restrict__ vpre, const int64_t* __restrict__ roff,
-                          int32_t* __restrict__ gcur, int32_t* __restrict__ grow) {
+                          const int32_t* __restrict__ deg, const int64_t* __restrict__ fptr,
+                          const int64_t* __restrict__ brow, int64_t k,
+                          const uint32_t* __restrict__ vbits, const int32_t* __restrict__ vpre,
+                          const int64_t* __restrict__ roff, int32_t* __restrict__ gcur,
+                          int32_t* __restrict__ grow, int32_t* __restrict__ rdeg,
+                          int32_t* __restrict__ rbb, int32_t* __restrict__ rfp) {
+  __shared__ int64_t s_brow[kBrowSmem];
+  if (k + 1 <= kBrowSmem)
+    for (int64_t i = threadIdx.x; i <= k; i += blockDim.x) s_brow[i] = brow[i];
+  __syncthreads();
   const int64_t R = *R_ptr;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
        r += (int64_t)gridDim.x * blockDim.x) {
-    if (deg[r] > 0) {
+    const int32_t dr = deg[r];
+    if (dr > 0) {
       const int32_t g = vrank(vbits, vpre, rowv[r]);
       const unsigned peers = __match_any_sync(__activemask(), g);
       const int lane = lane_id(), leader = __ffs(peers) - 1;
       int32_t cur = 0;
       if (lane == leader) cur = atomicAdd(gcur + g, __popc(peers));
       cur = __shfl_sync(peers, cur, leader);
-      grow[roff[g] + cur + __popc(peers & ((1u << lane) - 1u))] = (int32_t)r;
+      const int64_t pos = roff[g] + cur + __popc(peers & ((1u << lane) - 1u));
+      grow[pos] = (int32_t)r;
+      rdeg[pos] = dr;
+      rbb[pos] = (int32_t)batch_of(s_brow, brow, k, r);
+      rfp[pos] = (int32_t)fptr[r];
     }
   }
 }
@@ -614,33 +625,50 @@ __global__ void k_dd_3d(const int32_t* __restrict__ dcount, int64_t* __restrict_
   out[1] = 3 * *dcount;  // tier-major item index space
 }
 
-// item -> group map of every tier
+// Work-item descriptor: everything the serve kernel needs before its first
+// load, in one 32-B record (no dependent look-up chain per item).
+struct __align__(16) DdItem {
+  int64_t a0;     // A row start
+  int32_t d;      // A row length
+  int32_t q0;     // first grouped row
+  int32_t nrows;  // grouped rows served
+  int32_t pad[3];
+};
+
+// descriptors of every tier's items (tier-major)
 __global__ void k_dd_items(const int64_t* __restrict__ D_ptr, const int32_t* __restrict__ dv,
-                           const int64_t* __restrict__ rowptr, const int64_t* __restrict__ ioff,
-                           int32_t* __restrict__ igrp) {
+                           const int64_t* __restrict__ rowptr, const int64_t* __restrict__ roff,
+                           const int64_t* __restrict__ ioff, DdItems rows,
+                           DdItem* __restrict__ items) {
   const int64_t D = *D_ptr;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < D;
        g += (int64_t)gridDim.x * blockDim.x) {
     const int32_t v = dv[g];
-    const int t = dd_tier(rowptr[v + 1] - rowptr[v]);
+    const int64_t a0 = rowptr[v], d = rowptr[v + 1] - a0;
+    const int t = dd_tier(d);
     const int64_t o0 = ioff[t * D + g], o1 = ioff[t * D + g + 1];
-    for (int64_t o = o0; o < o1; ++o) igrp[o] = (int32_t)g;
+    const int64_t r0 = roff[g], r1 = roff[g + 1], per = rows.rows[t];
+    for (int64_t o = o0; o < o1; ++o) {
+      DdItem it;
+      it.a0 = a0;
+      it.d = (int32_t)d;
+      it.q0 = (int32_t)(r0 + (o - o0) * per);
+      it.nrows = (int32_t)min(per, r1 - it.q0);
+      it.pad[0] = it.pad[1] = it.pad[2] = 0;
+      items[o] = it;
+    }
   }
 }
 
 struct DdArgs {
   const int64_t* D_ptr;
-  const int32_t* dv;
-  const int64_t* rowptr;
   const int32_t* col;
-  const int64_t* roff;   // group row-list offsets (D + 1)
   const int64_t* ioff;   // tier-major item prefix (3D + 1)
-  const int32_t* igrp;   // item -> group
+  const DdItem* items;
   const int32_t* pidx;   // sorted picks of grouped row q at pidx[q * s ..]
   const int32_t* rfp;    // frontier offset of grouped row q
   const int32_t* rbb;    // batch of grouped row q
   int32_t s;
-  int32_t rows_item;
   int32_t chunk;         // A-row entries staged per pass
   int32_t* fcol;
   uint32_t* bitmap;
@@ -655,7 +683,8 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 // Q^l A for the distinct rows: per work item, A row v staged in shared
 // memory (16-B cp.async; buf[e - (e0 & ~3)]) — the P row on chip once —
 // then every pick of the item's frontier rows is served from it: frontier
-// write and the (batch, vertex) bit.
+// write and the (batch, vertex) bit.  The next item's descriptor and each
+// pass's pick metadata are loaded while the staged row is in flight.
 template <int TIER>
 __global__ void __launch_bounds__(DdTier<TIER>::kThreads) k_dd_serve(DdArgs A) {
   constexpr bool CTA = !DdTier<TIER>::kWarp;
@@ -665,37 +694,59 @@ __global__ void __launch_bounds__(DdTier<TIER>::kThreads) k_dd_serve(DdArgs A) {
   const int nthr = CTA ? blockDim.x : 32;
   int32_t* buf = sbuf + (CTA ? 0 : (threadIdx.x >> 5) * (chunk + 8));
   const int64_t D = *A.D_ptr;
-  const int64_t it0 = A.ioff[TIER * D], it1 = A.ioff[(TIER + 1) * D];
+  const int64_t it1 = A.ioff[(TIER + 1) * D];
   const int64_t step = CTA ? gridDim.x : grid_warps();
-  for (int64_t it = it0 + (CTA ? blockIdx.x : global_warp()); it < it1; it += step) {
-    const int32_t g = A.igrp[it];
-    const int64_t q0 = A.roff[g] + (it - A.ioff[TIER * D + g]) * A.rows_item;
-    const int nrows = (int)min((int64_t)A.rows_item, A.roff[g + 1] - q0);
-    const int32_t v = A.dv[g];
-    const int64_t a0 = A.rowptr[v];
-    const int32_t d = (int32_t)(A.rowptr[v + 1] - a0);
+  int64_t it = A.ioff[TIER * D] + (CTA ? blockIdx.x : global_warp());
+  DdItem cur;
+  if (it < it1) cur = A.items[it];
+  for (; it < it1; it += step) {
+    DdItem nxt;
+    if (it + step < it1) nxt = A.items[it + step];
+    const int64_t a0 = cur.a0;
+    const int32_t d = cur.d, nrows = cur.nrows;
+    const int64_t q0 = cur.q0;
     const int32_t take = min(d, s);
     const bool all = take == d;  // exhaustion: every entry, in order
+    const int npairs = nrows * take;
     for (int64_t c0 = 0; c0 < d; c0 += chunk) {
       const int64_t c1 = min(c0 + (int64_t)chunk, (int64_t)d);
       const int64_t al0 = (a0 + c0) & ~3LL;
       for (int64_t e = al0 + 4 * tid; e < a0 + c1; e += 4 * nthr)
         cp_async16(buf + (e - al0), A.col + e);
-      asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      // first pass's pick metadata while the row lands
+      int p = tid;
+      int32_t idx = 0, fp = 0, bb = 0, t = 0;
+      if (p < npairs) {
+        const int i = p / take;
+        t = p - i * take;
+        idx = all ? t : A.pidx[(q0 + i) * s + t];
+        fp = A.rfp[q0 + i];
+        bb = A.rbb[q0 + i];
+      }
+      asm volatile("cp.async.wait_all;" ::: "memory");
       if (CTA) __syncthreads(); else __syncwarp();
       const int32_t sh = (int32_t)((a0 + c0) - al0 - c0);  // buf[idx + sh], idx in [c0, c1)
-      for (int p = tid; p < nrows * take; p += nthr) {
-        const int i = p / take, t = p - i * take;
-        const int64_t q = q0 + i;
-        const int32_t idx = all ? t : A.pidx[q * s + t];
+      while (p < npairs) {
+        const int pn = p + nthr;
+        int32_t idx2 = 0, fp2 = 0, bb2 = 0, t2 = 0;
+        if (pn < npairs) {
+          const int i = pn / take;
+          t2 = pn - i * take;
+          idx2 = all ? t2 : A.pidx[(q0 + i) * s + t2];
+          fp2 = A.rfp[q0 + i];
+          bb2 = A.rbb[q0 + i];
+        }
         if (idx >= c0 && idx < c1) {
           const int32_t c = buf[idx + sh];
-          A.fcol[A.rfp[q] + t] = c;
-          atomicOr(A.bitmap + (int64_t)A.rbb[q] * A.nwords + (c >> 5), 1u << (c & 31));
+          A.fcol[fp + t] = c;
+          atomicOr(A.bitmap + (int64_t)bb * A.nwords + (c >> 5), 1u << (c & 31));
         }
+        p = pn; idx = idx2; fp = fp2; bb = bb2; t = t2;
       }
       if (CTA) __syncthreads(); else __syncwarp();
     }
+    cur = nxt;
   }
 }
 
@@ -875,8 +926,9 @@ struct SageWs {
   int64_t* roff;     // group offsets into grow
   int32_t* grow;     // frontier rows grouped by vertex
   int64_t* ioff;     // tier-major work-item prefix [3 * r_cap + 1]
-  int32_t* igrp;     // work item -> group
+  DdItem* items;     // work-item descriptors
   int32_t* rfp;      // per grouped row: frontier offset
+  int32_t* rdeg;     // per grouped row: degree
   int32_t* rbb;      // per grouped row: batch
   size_t bytes;
 };
@@ -909,8 +961,9 @@ static SageWs sage_ws_layout(char* base, int64_t k, int64_t n, int64_t r_cap_max
   w.grow = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
   w.ioff = (int64_t*)take(sizeof(int64_t) * (3 * r_cap_max + 1));
   // items <= groups + rows / 32 <= 2 * rows
-  w.igrp = (int32_t*)take(sizeof(int32_t) * (2 * r_cap_max + 2));
+  w.items = (DdItem*)take(sizeof(DdItem) * (2 * r_cap_max + 2));
   w.rfp = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
+  w.rdeg = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
   w.rbb = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
   w.bytes = off;
   return w;
@@ -942,7 +995,8 @@ static DdItems dd_items(int32_t s) {
 // Dedup step 1: distinct row vertices, the frontier rows of each grouped
 // together, and the tier-major work items of the serve kernels.
 static int dedup_prepare(const Graph* g, SageWs& ws, const int64_t* R_ptr, const int32_t* rowv,
-                         int32_t s, int64_t r_cap, int64_t nwords, cudaStream_t st) {
+                         const int64_t* fptr, const int64_t* brow, int64_t k, int32_t s,
+                         int64_t r_cap, int64_t nwords, cudaStream_t st) {
   const int64_t gw = 16 * kNumSMs;
   GB_CUDA(cudaMemsetAsync(ws.vbits, 0, sizeof(uint32_t) * (nwords + 1), st));
   GB_CUDA(cudaMemsetAsync(ws.gcnt, 0, sizeof(int32_t) * (r_cap + 1), st));
@@ -957,14 +1011,15 @@ static int dedup_prepare(const Graph* g, SageWs& ws, const int64_t* R_ptr, const
                                                        ws.gcnt);
   rc = device_exclusive_scan<int64_t>(ws.d_nw + 1, r_cap, GcntF{ws.gcnt}, ws.roff, ws.scan_ws, st);
   if (rc) return rc;
-  k_dd_rows<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, ws.vbits, ws.vpre,
-                                                     ws.roff, ws.gcur, ws.grow);
+  k_dd_rows<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, fptr, brow, k,
+                                                     ws.vbits, ws.vpre, ws.roff, ws.gcur,
+                                                     ws.grow, ws.rdeg, ws.rbb, ws.rfp);
   rc = device_exclusive_scan<int64_t>(ws.d_nw + 2, 3 * r_cap,
                                       ItemF{ws.dv, g->rowptr, ws.gcnt, ws.d_nw + 1, dd_items(s)},
                                       ws.ioff, ws.scan_ws, st);
   if (rc) return rc;
-  k_dd_items<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(ws.d_nw + 1, ws.dv, g->rowptr, ws.ioff,
-                                                      ws.igrp);
+  k_dd_items<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(ws.d_nw + 1, ws.dv, g->rowptr, ws.roff,
+                                                      ws.ioff, dd_items(s), ws.items);
   GB_LAUNCH_CHECK("dedup prepare");
   count_launches(7);
   return GB_OK;
@@ -981,7 +1036,6 @@ static int launch_serve(DdArgs A, cudaStream_t st) {
   }
   // chunk: the whole row for tiers 0 / 1, all of shared memory for hubs
   A.chunk = T == 2 ? ((max_smem / 4 - 8) & ~3) : Tr::kHi;
-  A.rows_item = dd_items(A.s).rows[T];
   const size_t smem = sizeof(int32_t) * (A.chunk + 8) * (Tr::kWarp ? Tr::kThreads / 32 : 1);
   static int grid = 0;  // smem is fixed per tier
   if (!grid) {
@@ -999,8 +1053,7 @@ static int launch_serve(DdArgs A, cudaStream_t st) {
 // distinct row on chip, three size tiers.
 static int dedup_serve(const Graph* g, SageWs& ws, const SageArgs& S, cudaStream_t st) {
   DdArgs A{};
-  A.D_ptr = ws.d_nw + 1; A.dv = ws.dv; A.rowptr = g->rowptr; A.col = g->col;
-  A.roff = ws.roff; A.ioff = ws.ioff; A.igrp = ws.igrp;
+  A.D_ptr = ws.d_nw + 1; A.col = g->col; A.ioff = ws.ioff; A.items = ws.items;
   A.pidx = ws.pidx; A.rfp = ws.rfp; A.rbb = ws.rbb;
   A.s = S.s; A.fcol = S.fcol; A.bitmap = S.bitmap; A.nwords = S.nwords;
   int rc = launch_serve<0>(A, st);
@@ -1110,9 +1163,9 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     A.bitmap = ws.bitmap; A.nwords = nwords; A.fcol = o.fcol; A.pidx = ws.pidx;
     const int pick_grid = grid_for(r_cap, kPickThreads, 64 * kNumSMs);
     if (dedup) {
-      rc = dedup_prepare(g, ws, R_ptr, rowv, s, r_cap, nwords, st);
+      rc = dedup_prepare(g, ws, R_ptr, rowv, o.fptr, brow, k, s, r_cap, nwords, st);
       if (rc) return rc;
-      A.D_ptr = ws.d_nw + 1; A.roff = ws.roff; A.grow = ws.grow; A.rfp = ws.rfp; A.rbb = ws.rbb;
+      A.D_ptr = ws.d_nw + 1; A.roff = ws.roff; A.grow = ws.grow; A.rdeg = ws.rdeg; A.rbb = ws.rbb;
       prof_mark(st);
       launch_pick<2>(pick_grid, A, R_ptr, st);
       GB_LAUNCH_CHECK("k_sage_pick");
