@@ -185,9 +185,7 @@ struct SageArgs {
   // frontier offset and batch, picks at pidx[q * s ..]
   const int64_t* D_ptr;
   const int64_t* roff;
-  const int32_t* grow;
-  const int32_t* rdeg;
-  const int32_t* rbb;
+  const int4* rrec;
 };
 
 __device__ __forceinline__ int32_t vrank(const uint32_t* vbits, const int32_t* vpre, int32_t v) {
@@ -294,13 +292,15 @@ __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
   __syncthreads();
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < R;
        q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = OUT == 2 ? (int64_t)A.grow[q] : q;
-    const int32_t deg = OUT == 2 ? A.rdeg[q] : A.deg[r];
+    int4 rec = make_int4(0, 0, 0, 0);
+    if (OUT == 2) rec = A.rrec[q];
+    const int64_t r = OUT == 2 ? (int64_t)rec.x : q;
+    const int32_t deg = OUT == 2 ? rec.y : A.deg[r];
     if (deg == 0) continue;  // empty P row (sample_rows_ordered, sampler.py:202-204)
     const int32_t take = min(deg, A.s);
     if (OUT == 2 && take == deg) continue;  // served in order by k_dd_serve
     const int64_t fp = OUT == 2 ? 0 : A.fptr[r];
-    const int64_t bb = keyed ? 0 : OUT == 2 ? A.rbb[q] : batch_of(s_brow, A.brow, A.k, r);
+    const int64_t bb = keyed ? 0 : OUT == 2 ? (int64_t)rec.z : batch_of(s_brow, A.brow, A.k, r);
     int32_t sorted[MAXF];
 #pragma unroll
     for (int z = 0; z < MAXF; ++z) sorted[z] = z;  // exhaustion: every index (sampler.py:172-174)
@@ -506,16 +506,19 @@ __global__ void k_dd_mark(const int64_t* __restrict__ R_ptr, const int32_t* __re
     }
 }
 
-// distinct vertex list (ascending)
+// distinct vertex list (ascending) and degrees
 __global__ void k_dd_list(int64_t nwords, const uint32_t* __restrict__ vbits,
-                          const int32_t* __restrict__ vpre, int32_t* __restrict__ dv) {
+                          const int32_t* __restrict__ vpre, const int64_t* __restrict__ rowptr,
+                          int32_t* __restrict__ dv, int32_t* __restrict__ ddeg) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nwords;
        i += (int64_t)gridDim.x * blockDim.x) {
     uint32_t x = vbits[i];
     int32_t o = vpre[i];
     while (x) {
       const int bit = __ffs(x) - 1;
-      dv[o++] = (int32_t)(i * 32 + bit);
+      const int32_t v = (int32_t)(i * 32 + bit);
+      dv[o] = v;
+      ddeg[o++] = (int32_t)(rowptr[v + 1] - rowptr[v]);
       x &= x - 1;
     }
   }
@@ -536,17 +539,16 @@ __global__ void k_dd_rcount(const int64_t* __restrict__ R_ptr, const int32_t* __
   }
 }
 
-// frontier rows grouped by vertex: grow[roff[g] ..) (order inside a group is
-// irrelevant — every row's output is independent), with each grouped row's
-// degree, batch and frontier offset so the pick and serve kernels read them
-// in order instead of gathering them
+// frontier rows grouped by vertex: rrec[roff[g] ..) = (row, degree, batch,
+// frontier offset) — order inside a group is irrelevant, every row's output
+// is independent; the pick and serve kernels read the records in order
+// instead of gathering them
 __global__ void k_dd_rows(const int64_t* __restrict__ R_ptr, const int32_t* __restrict__ rowv,
                           const int32_t* __restrict__ deg, const int64_t* __restrict__ fptr,
                           const int64_t* __restrict__ brow, int64_t k,
                           const uint32_t* __restrict__ vbits, const int32_t* __restrict__ vpre,
                           const int64_t* __restrict__ roff, int32_t* __restrict__ gcur,
-                          int32_t* __restrict__ grow, int32_t* __restrict__ rdeg,
-                          int32_t* __restrict__ rbb, int32_t* __restrict__ rfp) {
+                          int4* __restrict__ rrec) {
   __shared__ int64_t s_brow[kBrowSmem];
   if (k + 1 <= kBrowSmem)
     for (int64_t i = threadIdx.x; i <= k; i += blockDim.x) s_brow[i] = brow[i];
@@ -563,10 +565,8 @@ __global__ void k_dd_rows(const int64_t* __restrict__ R_ptr, const int32_t* __re
       if (lane == leader) cur = atomicAdd(gcur + g, __popc(peers));
       cur = __shfl_sync(peers, cur, leader);
       const int64_t pos = roff[g] + cur + __popc(peers & ((1u << lane) - 1u));
-      grow[pos] = (int32_t)r;
-      rdeg[pos] = dr;
-      rbb[pos] = (int32_t)batch_of(s_brow, brow, k, r);
-      rfp[pos] = (int32_t)fptr[r];
+      rrec[pos] = make_int4((int32_t)r, dr, (int32_t)batch_of(s_brow, brow, k, r),
+                            (int32_t)fptr[r]);
     }
   }
 }
@@ -604,17 +604,14 @@ struct DdItems {
 
 // Tier-major work-item prefix in one scan: virtual index i = tier * D + g
 struct ItemF {
-  const int32_t* dv;
-  const int64_t* rowptr;
+  const int32_t* ddeg;
   const int32_t* gcnt;
   const int64_t* D_ptr;
   DdItems it;
   __device__ int64_t operator()(int64_t i) const {
     const int64_t D = *D_ptr;
-    const int64_t t = i / D, g = i - t * D;
-    const int32_t v = dv[g];
-    const int64_t d = rowptr[v + 1] - rowptr[v];
-    if (dd_tier(d) != t) return 0;
+    const int64_t t = i >= D ? (i >= 2 * D ? 2 : 1) : 0, g = i - t * D;
+    if (dd_tier(ddeg[g]) != t) return 0;
     const int64_t rows = it.rows[t];
     return (gcnt[g] + rows - 1) / rows;
   }
@@ -637,14 +634,13 @@ struct __align__(16) DdItem {
 
 // descriptors of every tier's items (tier-major)
 __global__ void k_dd_items(const int64_t* __restrict__ D_ptr, const int32_t* __restrict__ dv,
-                           const int64_t* __restrict__ rowptr, const int64_t* __restrict__ roff,
+                           const int32_t* __restrict__ ddeg, const int64_t* __restrict__ rowptr, const int64_t* __restrict__ roff,
                            const int64_t* __restrict__ ioff, DdItems rows,
                            DdItem* __restrict__ items) {
   const int64_t D = *D_ptr;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < D;
        g += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t v = dv[g];
-    const int64_t a0 = rowptr[v], d = rowptr[v + 1] - a0;
+    const int64_t a0 = rowptr[dv[g]], d = ddeg[g];
     const int t = dd_tier(d);
     const int64_t o0 = ioff[t * D + g], o1 = ioff[t * D + g + 1];
     const int64_t r0 = roff[g], r1 = roff[g + 1], per = rows.rows[t];
@@ -666,8 +662,7 @@ struct DdArgs {
   const int64_t* ioff;   // tier-major item prefix (3D + 1)
   const DdItem* items;
   const int32_t* pidx;   // sorted picks of grouped row q at pidx[q * s ..]
-  const int32_t* rfp;    // frontier offset of grouped row q
-  const int32_t* rbb;    // batch of grouped row q
+  const int2* rbf;       // (batch, frontier offset) of grouped row q at [2q + 1]
   int32_t s;
   int32_t chunk;         // A-row entries staged per pass
   int32_t* fcol;
@@ -721,8 +716,9 @@ __global__ void __launch_bounds__(DdTier<TIER>::kThreads) k_dd_serve(DdArgs A) {
         const int i = p / take;
         t = p - i * take;
         idx = all ? t : A.pidx[(q0 + i) * s + t];
-        fp = A.rfp[q0 + i];
-        bb = A.rbb[q0 + i];
+        const int2 bf = A.rbf[2 * (q0 + i) + 1];
+        bb = bf.x;
+        fp = bf.y;
       }
       asm volatile("cp.async.wait_all;" ::: "memory");
       if (CTA) __syncthreads(); else __syncwarp();
@@ -734,8 +730,9 @@ __global__ void __launch_bounds__(DdTier<TIER>::kThreads) k_dd_serve(DdArgs A) {
           const int i = pn / take;
           t2 = pn - i * take;
           idx2 = all ? t2 : A.pidx[(q0 + i) * s + t2];
-          fp2 = A.rfp[q0 + i];
-          bb2 = A.rbb[q0 + i];
+          const int2 bf = A.rbf[2 * (q0 + i) + 1];
+          bb2 = bf.x;
+          fp2 = bf.y;
         }
         if (idx >= c0 && idx < c1) {
           const int32_t c = buf[idx + sh];
@@ -783,6 +780,7 @@ __global__ void k_sage_rank(const int64_t* __restrict__ F_ptr, const int64_t* __
                             int64_t k, const int32_t* __restrict__ fcol,
                             const uint32_t* __restrict__ bitmap, const int32_t* __restrict__ wpre,
                             int64_t nwords, int32_t* __restrict__ acol) {
+  constexpr int U = 4;  // entries per thread per pass: 2U independent gathers in flight
   __shared__ int64_t s_eoff[kBrowSmem];
   const bool sm = k + 1 <= kBrowSmem;
   if (sm)
@@ -790,23 +788,31 @@ __global__ void k_sage_rank(const int64_t* __restrict__ F_ptr, const int64_t* __
   __syncthreads();
   const int64_t F = *F_ptr;
   const int64_t* eo = sm ? s_eoff : eoff;
-  int64_t lo = -1;  // batch of e: binary search once, then walk forward (e increases)
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < F;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    if (lo < 0) {
-      int64_t a = 0, b = k;
+  const int64_t S = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e0 < F; e0 += U * S) {
+    int32_t v[U];
+    int64_t wi[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = e0 + u * S < F ? fcol[e0 + u * S] : 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t e = e0 + u * S;
+      int64_t a = 0, b = k;  // batch of e: last b with eoff[b] <= e
       while (b - a > 1) {
         const int64_t mid = (a + b) >> 1;
         if (eo[mid] <= e) a = mid; else b = mid;
       }
-      lo = a;
-    } else {
-      while (lo + 1 < k && eo[lo + 1] <= e) ++lo;
+      wi[u] = a * nwords + (v[u] >> 5);
     }
-    const int32_t v = fcol[e];
-    const int64_t wi = lo * nwords + (v >> 5);
-    const uint32_t mask = (1u << (v & 31)) - 1u;
-    acol[e] = wpre[wi] + __popc(bitmap[wi] & mask);
+    uint32_t bm[U];
+    int32_t wp[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (e0 + u * S < F) { bm[u] = bitmap[wi[u]]; wp[u] = wpre[wi[u]]; }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (e0 + u * S < F)
+        acol[e0 + u * S] = wp[u] + __popc(bm[u] & ((1u << (v[u] & 31)) - 1u));
   }
 }
 
@@ -923,13 +929,11 @@ struct SageWs {
   int32_t* dv;       // distinct vertices
   int32_t* gcnt;     // frontier rows per distinct vertex
   int32_t* gcur;
-  int64_t* roff;     // group offsets into grow
-  int32_t* grow;     // frontier rows grouped by vertex
+  int64_t* roff;     // group offsets into rrec
   int64_t* ioff;     // tier-major work-item prefix [3 * r_cap + 1]
   DdItem* items;     // work-item descriptors
-  int32_t* rfp;      // per grouped row: frontier offset
-  int32_t* rdeg;     // per grouped row: degree
-  int32_t* rbb;      // per grouped row: batch
+  int4* rrec;        // per grouped row: (row, degree, batch, frontier offset)
+  int32_t* ddeg;     // degree per distinct vertex
   size_t bytes;
 };
 
@@ -958,13 +962,11 @@ static SageWs sage_ws_layout(char* base, int64_t k, int64_t n, int64_t r_cap_max
   w.gcnt = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
   w.gcur = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
   w.roff = (int64_t*)take(sizeof(int64_t) * (r_cap_max + 1));
-  w.grow = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
   w.ioff = (int64_t*)take(sizeof(int64_t) * (3 * r_cap_max + 1));
   // items <= groups + rows / 32 <= 2 * rows
   w.items = (DdItem*)take(sizeof(DdItem) * (2 * r_cap_max + 2));
-  w.rfp = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
-  w.rdeg = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
-  w.rbb = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
+  w.rrec = (int4*)take(sizeof(int4) * (r_cap_max + 1));
+  w.ddeg = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
   w.bytes = off;
   return w;
 }
@@ -1006,19 +1008,20 @@ static int dedup_prepare(const Graph* g, SageWs& ws, const int64_t* R_ptr, const
                                           st);
   if (rc) return rc;
   k_dd_3d<<<1, 1, 0, st>>>(ws.vpre + nwords, ws.d_nw + 1);
-  k_dd_list<<<grid_for(nwords, 256, gw), 256, 0, st>>>(nwords, ws.vbits, ws.vpre, ws.dv);
+  k_dd_list<<<grid_for(nwords, 256, gw), 256, 0, st>>>(nwords, ws.vbits, ws.vpre, g->rowptr,
+                                                      ws.dv, ws.ddeg);
   k_dd_rcount<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, ws.vbits, ws.vpre,
                                                        ws.gcnt);
   rc = device_exclusive_scan<int64_t>(ws.d_nw + 1, r_cap, GcntF{ws.gcnt}, ws.roff, ws.scan_ws, st);
   if (rc) return rc;
   k_dd_rows<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, fptr, brow, k,
                                                      ws.vbits, ws.vpre, ws.roff, ws.gcur,
-                                                     ws.grow, ws.rdeg, ws.rbb, ws.rfp);
+                                                     ws.rrec);
   rc = device_exclusive_scan<int64_t>(ws.d_nw + 2, 3 * r_cap,
-                                      ItemF{ws.dv, g->rowptr, ws.gcnt, ws.d_nw + 1, dd_items(s)},
+                                      ItemF{ws.ddeg, ws.gcnt, ws.d_nw + 1, dd_items(s)},
                                       ws.ioff, ws.scan_ws, st);
   if (rc) return rc;
-  k_dd_items<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(ws.d_nw + 1, ws.dv, g->rowptr, ws.roff,
+  k_dd_items<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(ws.d_nw + 1, ws.dv, ws.ddeg, g->rowptr, ws.roff,
                                                       ws.ioff, dd_items(s), ws.items);
   GB_LAUNCH_CHECK("dedup prepare");
   count_launches(7);
@@ -1054,7 +1057,7 @@ static int launch_serve(DdArgs A, cudaStream_t st) {
 static int dedup_serve(const Graph* g, SageWs& ws, const SageArgs& S, cudaStream_t st) {
   DdArgs A{};
   A.D_ptr = ws.d_nw + 1; A.col = g->col; A.ioff = ws.ioff; A.items = ws.items;
-  A.pidx = ws.pidx; A.rfp = ws.rfp; A.rbb = ws.rbb;
+  A.pidx = ws.pidx; A.rbf = (const int2*)ws.rrec;
   A.s = S.s; A.fcol = S.fcol; A.bitmap = S.bitmap; A.nwords = S.nwords;
   int rc = launch_serve<0>(A, st);
   if (!rc) rc = launch_serve<1>(A, st);
@@ -1165,7 +1168,7 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     if (dedup) {
       rc = dedup_prepare(g, ws, R_ptr, rowv, o.fptr, brow, k, s, r_cap, nwords, st);
       if (rc) return rc;
-      A.D_ptr = ws.d_nw + 1; A.roff = ws.roff; A.grow = ws.grow; A.rdeg = ws.rdeg; A.rbb = ws.rbb;
+      A.D_ptr = ws.d_nw + 1; A.roff = ws.roff; A.rrec = ws.rrec;
       prof_mark(st);
       launch_pick<2>(pick_grid, A, R_ptr, st);
       GB_LAUNCH_CHECK("k_sage_pick");
