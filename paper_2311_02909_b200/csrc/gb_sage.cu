@@ -340,11 +340,9 @@ __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
         for (int z = 0; z < MAXF; ++z)
           if (z < t && sorted[z] <= x) { ++x; ++i; }
 #pragma unroll
-        for (int z = MAXF - 1; z > 0; --z)
-          if (z > i && z <= t) sorted[z] = sorted[z - 1];
-#pragma unroll
-        for (int z = 0; z < MAXF; ++z)
-          if (z == i) sorted[z] = x;
+        for (int z = MAXF - 1; z > 0; --z)  // shift up and insert in one pass
+          sorted[z] = (z > i && z <= t) ? sorted[z - 1] : (z == i ? x : sorted[z]);
+        if (i == 0) sorted[0] = x;
       }
     }
     if (OUT == 1) {
@@ -376,8 +374,12 @@ __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
 
 template <int OUT>
 static void launch_pick(int grid, const SageArgs& A, const int64_t* R_ptr, cudaStream_t st) {
-  if (A.s <= 8)
+  if (A.s <= 5)
+    k_sage_pick<OUT, 5><<<grid, kPickThreads, 0, st>>>(A, R_ptr);
+  else if (A.s <= 8)
     k_sage_pick<OUT, 8><<<grid, kPickThreads, 0, st>>>(A, R_ptr);
+  else if (A.s <= 10)
+    k_sage_pick<OUT, 10><<<grid, kPickThreads, 0, st>>>(A, R_ptr);
   else if (A.s <= 16)
     k_sage_pick<OUT, 16><<<grid, kPickThreads, 0, st>>>(A, R_ptr);
   else
@@ -780,39 +782,47 @@ __global__ void k_sage_rank(const int64_t* __restrict__ F_ptr, const int64_t* __
                             int64_t k, const int32_t* __restrict__ fcol,
                             const uint32_t* __restrict__ bitmap, const int32_t* __restrict__ wpre,
                             int64_t nwords, int32_t* __restrict__ acol) {
-  constexpr int U = 4;  // entries per thread per pass: 2U independent gathers in flight
-  __shared__ int64_t s_eoff[kBrowSmem];
+  // F < 2^31 and k * nwords < 2^31 (checked by the host): 32-bit indexing.
+  // U entries per thread per pass (coalesced, 2U independent gathers in
+  // flight); batch by binary search for the first, a forward walk for the rest
+  constexpr int U = 4;
+  __shared__ int32_t s_eoff[kBrowSmem];
   const bool sm = k + 1 <= kBrowSmem;
   if (sm)
-    for (int64_t i = threadIdx.x; i <= k; i += blockDim.x) s_eoff[i] = eoff[i];
+    for (int i = threadIdx.x; i <= k; i += blockDim.x) s_eoff[i] = (int32_t)eoff[i];
   __syncthreads();
-  const int64_t F = *F_ptr;
-  const int64_t* eo = sm ? s_eoff : eoff;
-  const int64_t S = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e0 < F; e0 += U * S) {
-    int32_t v[U];
-    int64_t wi[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) v[u] = e0 + u * S < F ? fcol[e0 + u * S] : 0;
+  const int32_t F = (int32_t)*F_ptr;
+  const int32_t K = (int32_t)k, NW = (int32_t)nwords;
+  auto eo = [&](int32_t i) { return sm ? s_eoff[i] : (int32_t)eoff[i]; };
+  for (int32_t e0 = blockIdx.x * blockDim.x * U + threadIdx.x; e0 < F;
+       e0 += gridDim.x * blockDim.x * U) {
+    int32_t v[U], wi[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t e = e0 + u * S;
-      int64_t a = 0, b = k;  // batch of e: last b with eoff[b] <= e
-      while (b - a > 1) {
-        const int64_t mid = (a + b) >> 1;
-        if (eo[mid] <= e) a = mid; else b = mid;
-      }
-      wi[u] = a * nwords + (v[u] >> 5);
+      const int32_t e = e0 + u * (int32_t)blockDim.x;
+      v[u] = e < F ? fcol[e] : 0;
+    }
+    int32_t a = 0, b = K;  // last batch with eoff <= e0
+    while (b - a > 1) {
+      const int32_t mid = (a + b) >> 1;
+      if (eo(mid) <= e0) a = mid; else b = mid;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int32_t e = e0 + u * (int32_t)blockDim.x;
+      while (a + 1 < K && eo(a + 1) <= e) ++a;
+      wi[u] = a * NW + (v[u] >> 5);
     }
     uint32_t bm[U];
     int32_t wp[U];
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (e0 + u * S < F) { bm[u] = bitmap[wi[u]]; wp[u] = wpre[wi[u]]; }
+      if (e0 + u * (int32_t)blockDim.x < F) { bm[u] = bitmap[wi[u]]; wp[u] = wpre[wi[u]]; }
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (e0 + u * S < F)
-        acol[e0 + u * S] = wp[u] + __popc(bm[u] & ((1u << (v[u] & 31)) - 1u));
+    for (int u = 0; u < U; ++u) {
+      const int32_t e = e0 + u * (int32_t)blockDim.x;
+      if (e < F) acol[e] = wp[u] + __popc(bm[u] & ((1u << (v[u] & 31)) - 1u));
+    }
   }
 }
 
@@ -1114,6 +1124,11 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
   const bool dedup = mode == GB_SAGE_DEDUP;
   const int64_t nwords = (g->n + 31) / 32;
   const int64_t W = k * nwords;
+  if (W >= ((int64_t)1 << 31)) {
+    set_error("bulk: k * ceil(n / 32) = %lld (batch, vertex) words exceeds int32 indexing",
+              (long long)W);
+    return GB_ERR_UNSUPPORTED;
+  }
   const int64_t rmax = sage_rcap_max(r1_cap, layers, fanouts);
   SageWs ws = sage_ws_layout((char*)d_ws, k, g->n, rmax, sage_fcap_max(r1_cap, layers, fanouts));
   if (ws.bytes > ws_bytes) {
@@ -1327,6 +1342,10 @@ int sage_layer_extract(int64_t n, int64_t k, const int64_t* brow, const int64_t*
     return GB_ERR_CAPACITY;
   }
   const int64_t nwords = (n + 31) / 32, W = k * nwords;
+  if (W >= ((int64_t)1 << 31) || f_cap >= ((int64_t)1 << 31)) {
+    set_error("extract: k * ceil(n / 32) and the entry bound must stay below 2^31");
+    return GB_ERR_UNSUPPORTED;
+  }
   char* p = (char*)d_ws;
   uint32_t* bitmap = (uint32_t*)p;
   p += align_up(sizeof(uint32_t) * (W + 1));
