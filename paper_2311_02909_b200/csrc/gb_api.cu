@@ -32,6 +32,47 @@ void prof_mark(cudaStream_t st) {
   cudaEventRecord(g_prof.ev[g_prof.used++], st);
 }
 
+// Side streams for independent launches inside one step (fork / join by
+// events, so it also works under CUDA graph capture), per device.
+struct Fork {
+  cudaStream_t s[kForkStreams];
+  cudaEvent_t ev[kForkStreams + 1];
+  bool ready = false;
+};
+static Fork g_fork[16];
+
+cudaStream_t fork_begin(cudaStream_t st, int n) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Fork& f = g_fork[dev & 15];
+  if (!f.ready) {
+    for (int i = 0; i < kForkStreams; ++i)
+      cudaStreamCreateWithFlags(&f.s[i], cudaStreamNonBlocking);
+    for (int i = 0; i <= kForkStreams; ++i)
+      cudaEventCreateWithFlags(&f.ev[i], cudaEventDisableTiming);
+    f.ready = true;
+  }
+  cudaEventRecord(f.ev[kForkStreams], st);
+  for (int i = 0; i < n && i < kForkStreams; ++i) cudaStreamWaitEvent(f.s[i], f.ev[kForkStreams], 0);
+  return f.s[0];
+}
+
+cudaStream_t fork_stream(int i) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return g_fork[dev & 15].s[i];
+}
+
+void fork_join(cudaStream_t st, int n) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Fork& f = g_fork[dev & 15];
+  for (int i = 0; i < n && i < kForkStreams; ++i) {
+    cudaEventRecord(f.ev[i], f.s[i]);
+    cudaStreamWaitEvent(st, f.ev[i], 0);
+  }
+}
+
 int cuda_status(cudaError_t e, const char* what) {
   set_error("CUDA error in %s: %s", what, cudaGetErrorString(e));
   return GB_ERR_CUDA;

@@ -30,6 +30,13 @@ struct Graph {
 void count_launches(int n);
 void prof_mark(cudaStream_t st);
 
+// Fork n <= kForkStreams side streams off st (they wait for st's work so
+// far), launch on fork_stream(i), then fork_join makes st wait for them.
+constexpr int kForkStreams = 2;
+cudaStream_t fork_begin(cudaStream_t st, int n);
+cudaStream_t fork_stream(int i);
+void fork_join(cudaStream_t st, int n);
+
 int graph_build_tables(Graph* g, cudaStream_t st);
 int sage_workspace(const Graph* g, int64_t k, int64_t r1_cap, int32_t layers,
                    const int64_t* fanouts, size_t* bytes);

@@ -1069,9 +1069,13 @@ static int dedup_serve(const Graph* g, SageWs& ws, const SageArgs& S, cudaStream
   A.D_ptr = ws.d_nw + 1; A.col = g->col; A.ioff = ws.ioff; A.items = ws.items;
   A.pidx = ws.pidx; A.rbf = (const int2*)ws.rrec;
   A.s = S.s; A.fcol = S.fcol; A.bitmap = S.bitmap; A.nwords = S.nwords;
+  // the tiers touch disjoint frontier entries (and commutative bitmap ORs):
+  // run them concurrently so each tier's tail overlaps the others
+  fork_begin(st, 2);
   int rc = launch_serve<0>(A, st);
-  if (!rc) rc = launch_serve<1>(A, st);
-  if (!rc) rc = launch_serve<2>(A, st);
+  if (!rc) rc = launch_serve<1>(A, fork_stream(0));
+  if (!rc) rc = launch_serve<2>(A, fork_stream(1));
+  fork_join(st, 2);
   count_launches(3);
   return rc;
 }
