@@ -157,9 +157,12 @@ int gb_gather_features(int64_t m, const int32_t* d_ids, int64_t row0, const floa
  * d_sizes[5*l + {0,1,2,3,4}] = (A_S rows, F, A_S nnz, A_S cols, nnz(P)).
  * mode GB_LADIES_EXACT replays its_sample_row bit for bit (sequential fp64
  * cumsum, small graphs); GB_LADIES_RACE draws the same law by an
- * exponential race (Gumbel top-s) for production sizes. */
+ * exponential race (Gumbel top-s) for production sizes, counting P by
+ * column tiles in shared memory; GB_LADIES_RACE_DENSE is the same race over
+ * dense per-batch counters (identical output; kept as a cross-check). */
 #define GB_LADIES_EXACT 0
 #define GB_LADIES_RACE 1
+#define GB_LADIES_RACE_DENSE 2
 
 typedef struct {
   int64_t* fptr;

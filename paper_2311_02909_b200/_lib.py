@@ -43,6 +43,7 @@ class LadiesLayerOut(ctypes.Structure):
 
 GB_LADIES_EXACT = 0
 GB_LADIES_RACE = 1
+GB_LADIES_RACE_DENSE = 2
 
 # (name, restype, argtypes) — one line per exported symbol of the header
 SIGNATURES = {

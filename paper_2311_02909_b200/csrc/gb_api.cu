@@ -324,7 +324,7 @@ int gb_ladies_bulk(const gb_graph* g, int64_t k, const int64_t* d_qoff, const in
       set_error("ladies bulk: sample count must be >= 1");
       return GB_ERR_CONTRACT;
     }
-  if (mode != GB_LADIES_EXACT && mode != GB_LADIES_RACE) {
+  if (mode != GB_LADIES_EXACT && mode != GB_LADIES_RACE && mode != GB_LADIES_RACE_DENSE) {
     set_error("ladies bulk: unknown mode %d", mode);
     return GB_ERR_CONTRACT;
   }

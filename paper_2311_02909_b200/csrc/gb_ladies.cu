@@ -236,6 +236,227 @@ __global__ void __launch_bounds__(256) k_lad_compact_write(uint32_t* __restrict_
   }
 }
 
+// ------------------------------------------- P = Q A by column tiles (race)
+// GB_LADIES_RACE does not need the dense per-batch counter vectors: one CTA
+// per (batch, column tile) counts e_v for its tile in shared memory, then
+// compacts the tile's nonzeros straight into the P layout with their race
+// keys and key histogram.  Tiles are at most kLTileW columns wide and cut by
+// degree mass (columns near hubs are narrow) so CTAs carry similar work;
+// CTAs take (batch, tile) tickets in order and chain their output offsets by
+// decoupled look-back, so P comes out in (batch, v) order in one pass.
+constexpr int kLTileW = 32768;      // columns per tile (64 KB of 16-bit counters)
+constexpr int kLTileThreads = 512;
+constexpr int kLMassTiles = 64;     // extra cuts by degree mass
+
+// cut before v when v is a multiple of kLTileW or crosses a mass quantile
+struct CutF {
+  const int64_t* rowptr;
+  int64_t n, mass;
+  __device__ int64_t operator()(int64_t v) const {
+    if (v == 0 || v >= n) return 0;
+    return (v % kLTileW == 0) || (rowptr[v] / mass != rowptr[v - 1] / mass) ? 1 : 0;
+  }
+};
+
+// tb[0] = 0, tb[c] = the c-th cut, tb[ntiles] = n; *ntiles
+__global__ void k_lad_tiles(const int64_t* __restrict__ rowptr, int64_t n, int64_t mass,
+                            const int64_t* __restrict__ cpre, int32_t* __restrict__ tb,
+                            int64_t* __restrict__ ntiles) {
+  const CutF f{rowptr, n, mass};
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    if (v == 0) tb[0] = 0;
+    if (v == n) {
+      tb[cpre[n] + 1] = (int32_t)n;
+      *ntiles = cpre[n] + 1;
+    }
+    if (v < n && f(v)) tb[cpre[v] + 1] = (int32_t)v;
+  }
+}
+
+// first index in col[a, b) with col >= x: 32-ary warp search
+__device__ __forceinline__ int64_t warp_lower_bound(const int32_t* __restrict__ col, int64_t a,
+                                                    int64_t b, int32_t x) {
+  const int lane = lane_id();
+  const unsigned FULL = 0xffffffffu;
+  while (b - a > 32) {
+    const int64_t step = (b - a + 31) >> 5;
+    const int64_t p = a + (int64_t)lane * step;
+    const bool lt = p < b && __ldg(col + p) < x;
+    const int c = __popc(__ballot_sync(FULL, lt));  // lanes 0..c-1 below x
+    if (c == 0) return a;
+    a = a + (int64_t)(c - 1) * step + 1;
+    const int64_t nb = a - 1 + step;
+    if (nb < b) b = nb;
+  }
+  const int64_t p = a + lane;
+  const bool lt = p < b && __ldg(col + p) < x;
+  return a + __popc(__ballot_sync(FULL, lt));
+}
+
+struct LadTileArgs {
+  const int64_t* qoff;     // batch row offsets (k + 1)
+  const int32_t* qcol;
+  const int64_t* rowptr;
+  const int32_t* col;
+  const int32_t* tb;       // tile bounds (ntiles + 1)
+  const int64_t* ntiles;
+  int64_t n;
+  int64_t g0, gn;          // batches of this group
+  RaceKey rk;
+  unsigned long long* ticket;
+  int32_t* pv;             // P columns: batch j, tile t at slot j * n + tb[t]
+  uint32_t* keys;          // race keys, same slots
+  int32_t* tcnt;           // nonzeros of (j, t), gn * ntiles
+  uint32_t* hist;          // gn * kBins key histograms
+  int64_t* nnz_b;          // nonzeros per batch
+};
+
+constexpr int kLTileRun = 8;      // consecutive tiles per ticket (row cursors carried over)
+constexpr int kLRowsSmem = 1024;  // rows whose cursors fit in shared memory
+
+// One ticket = batch j and a run of kLTileRun consecutive column tiles.  Per
+// tile: counts in shared memory (warp per A row, from the row's cursor, which
+// the scan leaves at the first column past the tile), then a warp-balanced
+// compaction of the nonzeros into the tile's slot with their race keys.
+__global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
+  extern __shared__ uint32_t s_cnt[];               // kLTileW / 2 packed 16-bit counters
+  uint32_t* s_h = s_cnt + kLTileW / 2;               // kBins
+  int64_t* s_ra = (int64_t*)(s_h + kBins);           // row start, kLRowsSmem
+  int32_t* s_rl = (int32_t*)(s_ra + kLRowsSmem);     // row length
+  int32_t* s_rc = s_rl + kLRowsSmem;                 // row cursor (relative)
+  __shared__ int32_t s_wcnt[kLTileThreads / 32 + 1];
+  __shared__ int64_t s_ticket;
+  __shared__ unsigned long long s_nnz;
+  const unsigned FULL = 0xffffffffu;
+  const int lane = lane_id(), warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int64_t ntiles = *A.ntiles;
+  const int64_t nruns = (ntiles + kLTileRun - 1) / kLTileRun;
+  const int64_t nt = A.gn * nruns;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      s_ticket = (int64_t)atomicAdd(A.ticket, 1ull);
+      s_nnz = 0;
+    }
+    for (int b = threadIdx.x; b < kBins; b += blockDim.x) s_h[b] = 0;
+    __syncthreads();
+    const int64_t ticket = s_ticket;
+    if (ticket >= nt) return;
+    const int64_t j = ticket / nruns, run = ticket - j * nruns;
+    const int64_t t0 = run * kLTileRun, t1 = min(t0 + kLTileRun, ntiles);
+    const int64_t q0 = A.qoff[A.g0 + j], q1 = A.qoff[A.g0 + j + 1];
+    const bool cur = q1 - q0 <= kLRowsSmem;
+    if (cur) {
+      // cursors at the run's first column (a 32-ary search per row)
+      const int32_t vs = A.tb[t0];
+      for (int64_t q = q0 + warp; q < q1; q += nwarps) {
+        const int32_t u = A.qcol[q];
+        const int64_t a = A.rowptr[u], b = A.rowptr[u + 1];
+        int64_t e0 = a;
+        if (vs > 0 && a < b && __ldg(A.col + a) < vs) e0 = warp_lower_bound(A.col, a, b, vs);
+        if (lane == 0) {
+          s_ra[q - q0] = a;
+          s_rl[q - q0] = (int32_t)(b - a);
+          s_rc[q - q0] = (int32_t)(e0 - a);
+        }
+      }
+    }
+    for (int64_t t = t0; t < t1; ++t) {
+      const int32_t v0 = A.tb[t], v1 = A.tb[t + 1];
+      const int nw2 = (v1 - v0 + 1) >> 1;
+      for (int w = threadIdx.x; w < nw2; w += blockDim.x) s_cnt[w] = 0;
+      __syncthreads();
+      // ---- e_v for v in [v0, v1)
+      for (int64_t q = q0 + warp; q < q1; q += nwarps) {
+        int64_t a, b, e0;
+        if (cur) {
+          a = s_ra[q - q0];
+          b = a + s_rl[q - q0];
+          e0 = a + s_rc[q - q0];
+        } else {
+          const int32_t u = A.qcol[q];
+          a = A.rowptr[u];
+          b = A.rowptr[u + 1];
+          e0 = a < b && __ldg(A.col + a) < v0 ? warp_lower_bound(A.col, a, b, v0) : a;
+        }
+        if (e0 >= b) continue;
+        for (int64_t e = e0 + lane;; e += 32) {
+          const int32_t c = e < b ? __ldg(A.col + e) : 0x7fffffff;
+          const bool in = c < v1;
+          if (in) atomicAdd(s_cnt + ((c - v0) >> 1), 1u << (((c - v0) & 1) << 4));
+          const unsigned out = __ballot_sync(FULL, !in);
+          if (out) {
+            if (cur && lane == 0) s_rc[q - q0] = (int32_t)(e - lane - a + __ffs(out) - 1);
+            break;
+          }
+        }
+      }
+      __syncthreads();
+      // ---- compaction: warp w owns words [w * chunk, ...), counted then written
+      const int chunk = (nw2 + nwarps - 1) / nwarps;
+      const int wa = warp * chunk, wb = min(wa + chunk, nw2);
+      int c = 0;
+      for (int w = wa + lane; w < wb; w += 32) {
+        const uint32_t x = s_cnt[w];
+        c += ((x & 0xffffu) != 0) + ((x >> 16) != 0);
+      }
+      c = warp_sum(c);
+      if (lane == 0) s_wcnt[warp] = c;
+      __syncthreads();
+      int base = 0, total = 0;
+      for (int w = 0; w < nwarps; ++w) {
+        const int x = s_wcnt[w];
+        base += w < warp ? x : 0;
+        total += x;
+      }
+      const int64_t slot = j * A.n + v0;
+      for (int w0 = wa; w0 < wb; w0 += 32) {
+        const int w = w0 + lane;
+        const uint32_t x = w < wb ? s_cnt[w] : 0u;
+        const int m = ((x & 0xffffu) != 0) + ((x >> 16) != 0);
+        int inc = m;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(FULL, inc, o);
+          if (lane >= o) inc += y;
+        }
+        int o = base + inc - m;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const uint32_t e = (x >> (16 * h)) & 0xffffu;
+          if (e) {
+            const int32_t v = v0 + 2 * w + h;
+            const uint32_t key = A.rk(j, v, e);
+            A.pv[slot + o] = v;
+            A.keys[slot + o] = key;
+            atomicAdd(s_h + (key >> 20), 1u);
+            ++o;
+          }
+        }
+        base += __shfl_sync(FULL, inc, 31);
+      }
+      if (threadIdx.x == 0) {
+        A.tcnt[j * ntiles + t] = total;
+        s_nnz += (unsigned long long)total;
+      }
+      __syncthreads();  // counters reused by the next tile
+    }
+    uint32_t* hj = A.hist + j * kBins;
+    for (int b = threadIdx.x; b < kBins; b += blockDim.x)
+      if (s_h[b]) atomicAdd(hj + b, s_h[b]);
+    if (threadIdx.x == 0 && s_nnz)
+      atomicAdd((unsigned long long*)(A.nnz_b + A.g0 + j), s_nnz);
+    __syncthreads();
+  }
+}
+
+// tiled P layout: every batch's slots start at j * n
+__global__ void k_lad_slot_off(int64_t gn, int64_t n, int64_t* __restrict__ gpoff) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j <= gn;
+       j += (int64_t)gridDim.x * blockDim.x)
+    gpoff[j] = j * n;
+}
+
 // Block-wide search of the first bin where the running count reaches need:
 // every thread owns kBins / blockDim consecutive bins.  Returns (bin, count
 // strictly below it) through shared memory.
@@ -273,6 +494,7 @@ struct LadiesSampleArgs {
   int32_t* sel;          // per batch: up to s selected P positions (global batch index * s)
   int32_t* nsel;         // per batch selected count (atomic)
   int64_t* take;         // per batch
+  const int64_t* nnzb;   // tiled layout: nonzeros per batch (P rows have slot gaps)
 };
 
 // Exact replay of its_sample_row: one thread per batch.
@@ -371,7 +593,7 @@ __global__ void __launch_bounds__(256) k_lad_boundary(LadiesSampleArgs A,
   const int j = blockIdx.x;
   if (j >= A.gn) return;
   const int64_t i = A.g0 + j;
-  const int64_t N = A.gpoff[j + 1] - A.gpoff[j];
+  const int64_t N = A.nnzb ? A.nnzb[i] : A.gpoff[j + 1] - A.gpoff[j];
   const int64_t take = N < A.s ? N : A.s;
   if (take < N) {
     block_find_bin(hist + (int64_t)j * kBins, kBins, take, sw, &s_bin, &s_acc);
@@ -403,6 +625,33 @@ __global__ void k_lad_filter(LadiesSampleArgs A, const int32_t* __restrict__ bou
       A.sel[i * A.s + atomicAdd(A.nsel + i, 1)] = (int32_t)p;
     } else if (bin == b) {
       cand[A.gpoff[j] + atomicAdd(ncand + j, 1)] = (int32_t)p;
+    }
+  }
+}
+
+// k_lad_filter over the tiled layout: one CTA per (batch, tile) slot
+__global__ void __launch_bounds__(256) k_lad_filter_tiles(LadiesSampleArgs A,
+                                                        const int32_t* __restrict__ tb,
+                                                        const int64_t* __restrict__ ntiles_p,
+                                                        int64_t n, const int32_t* __restrict__ tcnt,
+                                                        const int32_t* __restrict__ bound,
+                                                        int32_t* __restrict__ cand,
+                                                        int32_t* __restrict__ ncand) {
+  const int64_t ntiles = *ntiles_p;
+  for (int64_t pr = blockIdx.x; pr < A.gn * ntiles; pr += gridDim.x) {
+    const int32_t cnt = tcnt[pr];
+    if (!cnt) continue;
+    const int64_t j = pr / ntiles, t = pr - j * ntiles;
+    const int64_t i = A.g0 + j;
+    const int64_t slot = j * n + tb[t];
+    const int b = bound[2 * j];
+    for (int x = threadIdx.x; x < cnt; x += blockDim.x) {
+      const int64_t p = slot + x;
+      const int bin = b == kBins ? -1 : (int)(A.keys[p] >> 20);
+      if (b == kBins || bin < b)
+        A.sel[i * A.s + atomicAdd(A.nsel + i, 1)] = (int32_t)p;
+      else if (bin == b)
+        cand[A.gpoff[j] + atomicAdd(ncand + j, 1)] = (int32_t)p;
     }
   }
 }
@@ -662,8 +911,14 @@ struct LadiesWs {
   int32_t* rcnt;     // Q cap
   int64_t* tile_off; // compaction tiles + 1
   int64_t* scan_ws;
-  int64_t* d_scalar; // 4 device scalars (k, words, tiles, ...)
+  int64_t* d_scalar; // 4 device scalars (k, words, tiles, n)
   int32_t* overflow;
+  // race mode, column tiles
+  int32_t* tb;       // tile bounds (ntiles_max + 1)
+  int64_t* cpre;     // cut prefix (n + 1)
+  int64_t* ntiles;   // device scalar
+  unsigned long long* tst;  // tile ticket
+  int32_t* tcnt;     // nonzeros per (batch, tile), gsize * ntiles_max
   size_t bytes;
 };
 
@@ -671,23 +926,31 @@ static size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct LadiesPlan {
   int64_t gsize, words, tiles, p_cap, q_cap, s_max;
+  bool tiled;          // race mode: column-tile counting, no dense counters
+  int64_t ntiles_max;  // column tiles
+  int64_t n;
 };
 
+constexpr int64_t kTiledGroupBytes = 2ll << 30;  // P layout (v, key, candidate) of one group
+
 static LadiesPlan ladies_plan(int64_t k, int64_t n, int64_t q1_cap, int32_t layers,
-                              const int64_t* fanouts) {
+                              const int64_t* fanouts, int32_t mode) {
   LadiesPlan p{};
+  p.n = n;
+  p.tiled = mode == GB_LADIES_RACE;
   p.s_max = 1;
   p.q_cap = q1_cap;
   for (int32_t l = 0; l < layers; ++l) {
     if (fanouts[l] > p.s_max) p.s_max = fanouts[l];
     if (k * fanouts[l] > p.q_cap) p.q_cap = k * fanouts[l];
   }
-  p.gsize = n > 0 ? kGroupBytes / (2 * n) : k;
+  p.gsize = n > 0 ? (p.tiled ? kTiledGroupBytes / (12 * n) : kGroupBytes / (2 * n)) : k;
   if (p.gsize < 1) p.gsize = 1;
   if (p.gsize > k) p.gsize = k > 0 ? k : 1;
-  p.words = (p.gsize * n + 1) / 2 + 1;
-  p.tiles = (2 * p.words + kCompTile - 1) / kCompTile;
+  p.words = p.tiled ? 1 : (p.gsize * n + 1) / 2 + 1;
+  p.tiles = p.tiled ? 1 : (2 * p.words + kCompTile - 1) / kCompTile;
   p.p_cap = p.gsize * n;
+  p.ntiles_max = p.tiled ? n / kLTileW + kLMassTiles + 2 : 1;
   return p;
 }
 
@@ -699,7 +962,7 @@ static LadiesWs ladies_ws_layout(char* base, int64_t k, const LadiesPlan& P, boo
   w.nnz_b = (int64_t*)take(sizeof(int64_t) * (k + 1));
   w.gpoff = (int64_t*)take(sizeof(int64_t) * (P.gsize + 1));
   w.pv = (int32_t*)take(sizeof(int32_t) * (P.p_cap + 1));
-  w.pe = (int32_t*)take(sizeof(int32_t) * (P.p_cap + 1));
+  w.pe = (int32_t*)take(P.tiled ? 8 : sizeof(int32_t) * (P.p_cap + 1));  // counts: exact only
   w.sw = (double*)take(exact ? sizeof(double) * (P.p_cap + 1) : 8);
   w.sc = (double*)take(exact ? sizeof(double) * (P.p_cap + 1) : 8);
   w.keys = (uint32_t*)take(exact ? 8 : sizeof(uint32_t) * (P.p_cap + 1));
@@ -718,16 +981,22 @@ static LadiesWs ladies_ws_layout(char* base, int64_t k, const LadiesPlan& P, boo
   w.tile_off = (int64_t*)take(sizeof(int64_t) * (P.tiles + 1));
   int64_t sn = P.q_cap > k ? P.q_cap : k;
   if (P.tiles > sn) sn = P.tiles;
+  if (P.tiled && P.n + 1 > sn) sn = P.n + 1;
   w.scan_ws = (int64_t*)take(sizeof(int64_t) * scan_workspace_elems<int64_t>(sn + 1));
   w.d_scalar = (int64_t*)take(sizeof(int64_t) * 4);
   w.overflow = (int32_t*)take(sizeof(int32_t));
+  w.tb = (int32_t*)take(sizeof(int32_t) * (P.ntiles_max + 1));
+  w.cpre = (int64_t*)take(P.tiled ? sizeof(int64_t) * (P.n + 2) : 8);
+  w.ntiles = (int64_t*)take(sizeof(int64_t));
+  w.tst = (unsigned long long*)take(sizeof(unsigned long long) * 2);
+  w.tcnt = (int32_t*)take(sizeof(int32_t) * (P.gsize * P.ntiles_max + 1));
   w.bytes = off;
   return w;
 }
 
 int ladies_workspace(const Graph* g, int64_t k, int64_t q1_cap, int32_t layers,
                      const int64_t* fanouts, int32_t mode, size_t* bytes) {
-  const LadiesPlan P = ladies_plan(k, g->n, q1_cap, layers, fanouts);
+  const LadiesPlan P = ladies_plan(k, g->n, q1_cap, layers, fanouts, mode);
   *bytes = ladies_ws_layout(nullptr, k, P, mode == GB_LADIES_EXACT).bytes;
   return GB_OK;
 }
@@ -738,7 +1007,7 @@ int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t*
                 int64_t* d_sizes, void* d_ws, size_t ws_bytes, cudaStream_t st) {
   const bool exact = mode == GB_LADIES_EXACT;
   const int64_t n = g->n;
-  const LadiesPlan P = ladies_plan(k, n, q1_cap, layers, fanouts);
+  const LadiesPlan P = ladies_plan(k, n, q1_cap, layers, fanouts, mode);
   LadiesWs ws = ladies_ws_layout((char*)d_ws, k, P, exact);
   if (ws.bytes > ws_bytes) {
     set_error("ladies workspace too small: need %zu bytes, got %zu", ws.bytes, ws_bytes);
@@ -762,6 +1031,32 @@ int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t*
   k_lad_set<<<1, 1, 0, st>>>(d_k, k);
   k_lad_set<<<1, 1, 0, st>>>(d_tiles, P.tiles);
   count_launches(2);
+  int tile_grid = 0;
+  const size_t tile_smem = sizeof(uint32_t) * (kLTileW / 2 + kBins) +
+                           (sizeof(int64_t) + 2 * sizeof(int32_t)) * kLRowsSmem;
+  if (P.tiled) {
+    // column tiles of this graph: cuts every kLTileW columns and at
+    // kLMassTiles quantiles of the degree mass
+    int64_t* d_n = ws.d_scalar + 3;
+    k_lad_set<<<1, 1, 0, st>>>(d_n, n);
+    const int64_t mass = g->nnz / kLMassTiles + 1;
+    int rc = device_exclusive_scan<int64_t>(d_n, n, CutF{g->rowptr, n, mass}, ws.cpre, ws.scan_ws,
+                                            st);
+    if (rc) return rc;
+    k_lad_tiles<<<gcap(n + 1, 256, 16 * sms), 256, 0, st>>>(g->rowptr, n, mass, ws.cpre, ws.tb,
+                                                          ws.ntiles);
+    GB_LAUNCH_CHECK("k_lad_tiles");
+    static int s_grid = 0;
+    if (!s_grid) {
+      cudaFuncSetAttribute(k_lad_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)tile_smem);
+      int occ = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lad_tile, kLTileThreads, tile_smem);
+      s_grid = (occ > 0 ? occ : 1) * sms;
+    }
+    tile_grid = s_grid;
+    count_launches(2);
+  }
   qc = q1_cap;
   for (int32_t l = 0; l < layers; ++l) {
     const int32_t s = (int32_t)fanouts[l];
@@ -770,47 +1065,73 @@ int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t*
     const int32_t* qcol = l == 0 ? d_qverts : L[l - 1].fcol;
     const int64_t* d_QN = qoff + k;
     int64_t* sizes = d_sizes + kLadiesSizes * l;
-    int rc = device_exclusive_scan<int64_t>(d_QN, qc, QDegF{qcol, g->rowptr}, ws.qg, ws.scan_ws, st);
-    if (rc) return rc;
+    int rc = GB_OK;
+    if (!P.tiled) {
+      rc = device_exclusive_scan<int64_t>(d_QN, qc, QDegF{qcol, g->rowptr}, ws.qg, ws.scan_ws, st);
+      if (rc) return rc;
+    }
     GB_CUDA(cudaMemsetAsync(ws.nnz_b, 0, sizeof(int64_t) * (k + 1), st));
     for (int64_t g0 = 0; g0 < k; g0 += P.gsize) {
       const int64_t g1 = g0 + P.gsize < k ? g0 + P.gsize : k;
       const int64_t gn = g1 - g0;
       const int64_t words = (gn * n + 1) / 2;
-      // ---- P = Q A for this group
-      prof_mark(st);
-      k_lad_count<<<4 * sms, kLadiesThreads, 0, st>>>(qoff, k, g0, g1, qcol, ws.qg, g->rowptr,
-                                                      g->col, n, ws.cnt32, ws.nnz_b);
-      GB_LAUNCH_CHECK("k_lad_count");
-      prof_mark(st);
-      k_lad_compact_count<<<gcap(P.tiles, 1, 8 * sms), 256, 0, st>>>(ws.cnt32, words, n, g0,
-                                                                    ws.tile_off, ws.nnz_b);
-      k_lad_gpoff<<<1, 1, 0, st>>>(ws.nnz_b, g0, gn, ws.gpoff);
-      rc = device_exclusive_scan<int64_t>(d_tiles, P.tiles, TileF{ws.tile_off}, ws.tile_off,
-                                          ws.scan_ws, st);
-      if (rc) return rc;
       const RaceKey rk{seed, epoch, (uint64_t)(l + 1), batch_offset + g0};
-      k_lad_compact_write<<<gcap(P.tiles, 1, 8 * sms), 256, 0, st>>>(
-          ws.cnt32, words, n, ws.tile_off, ws.pv, ws.pe, nullptr);
-      GB_LAUNCH_CHECK("k_lad_compact");
+      if (P.tiled) {
+        // ---- P = Q A, race keys and key histograms for this group, one pass
+        GB_CUDA(cudaMemsetAsync(ws.tst, 0, sizeof(unsigned long long), st));
+        GB_CUDA(cudaMemsetAsync(ws.hist, 0, sizeof(uint32_t) * gn * kBins, st));
+        LadTileArgs T{};
+        T.qoff = qoff; T.qcol = qcol; T.rowptr = g->rowptr; T.col = g->col; T.tb = ws.tb;
+        T.ntiles = ws.ntiles; T.n = n; T.g0 = g0; T.gn = gn; T.rk = rk; T.ticket = ws.tst;
+        T.pv = ws.pv; T.keys = ws.keys; T.tcnt = ws.tcnt; T.hist = ws.hist; T.nnz_b = ws.nnz_b;
+        prof_mark(st);
+        k_lad_tile<<<tile_grid, kLTileThreads, tile_smem, st>>>(T);
+        GB_LAUNCH_CHECK("k_lad_tile");
+        prof_mark(st);
+        k_lad_slot_off<<<gcap(gn + 1, 128, 64), 128, 0, st>>>(gn, n, ws.gpoff);
+        count_launches(2);
+      } else {
+        // ---- P = Q A for this group
+        prof_mark(st);
+        k_lad_count<<<4 * sms, kLadiesThreads, 0, st>>>(qoff, k, g0, g1, qcol, ws.qg, g->rowptr,
+                                                        g->col, n, ws.cnt32, ws.nnz_b);
+        GB_LAUNCH_CHECK("k_lad_count");
+        prof_mark(st);
+        k_lad_compact_count<<<gcap(P.tiles, 1, 8 * sms), 256, 0, st>>>(ws.cnt32, words, n, g0,
+                                                                      ws.tile_off, ws.nnz_b);
+        k_lad_gpoff<<<1, 1, 0, st>>>(ws.nnz_b, g0, gn, ws.gpoff);
+        rc = device_exclusive_scan<int64_t>(d_tiles, P.tiles, TileF{ws.tile_off}, ws.tile_off,
+                                            ws.scan_ws, st);
+        if (rc) return rc;
+        k_lad_compact_write<<<gcap(P.tiles, 1, 8 * sms), 256, 0, st>>>(
+            ws.cnt32, words, n, ws.tile_off, ws.pv, ws.pe, nullptr);
+        GB_LAUNCH_CHECK("k_lad_compact");
+      }
       // ---- NORM + SAMPLE
       LadiesSampleArgs A{};
       A.gpoff = ws.gpoff; A.pv = ws.pv; A.pe = ws.pe; A.g0 = g0; A.gn = gn; A.s = s;
       A.batch_offset = batch_offset; A.seed = seed; A.epoch = epoch; A.depth = (uint64_t)(l + 1);
       A.sw = ws.sw; A.sc = ws.sc; A.keys = ws.keys; A.sel = ws.sel; A.nsel = ws.nsel;
       A.take = ws.take;
+      A.nnzb = P.tiled ? ws.nnz_b : nullptr;
       if (exact) {
         k_lad_sample_exact<<<gcap(gn, 32, 4 * sms), 32, 0, st>>>(A);
         count_launches(1);
       } else {
-        GB_CUDA(cudaMemsetAsync(ws.hist, 0, sizeof(uint32_t) * gn * kBins, st));
         GB_CUDA(cudaMemsetAsync(ws.ncand, 0, sizeof(int32_t) * (gn + 1), st));
-        k_lad_keys<<<16 * sms, 256, 0, st>>>(A, rk);
-        k_lad_hist<<<4 * sms, 256, 0, st>>>(A, ws.hist);
+        if (!P.tiled) {
+          GB_CUDA(cudaMemsetAsync(ws.hist, 0, sizeof(uint32_t) * gn * kBins, st));
+          k_lad_keys<<<16 * sms, 256, 0, st>>>(A, rk);
+          k_lad_hist<<<4 * sms, 256, 0, st>>>(A, ws.hist);
+        }
         k_lad_boundary<<<(int)gn, 256, 0, st>>>(A, ws.hist, ws.bound);
-        k_lad_filter<<<16 * sms, 256, 0, st>>>(A, ws.bound, ws.cand, ws.ncand);
+        if (P.tiled)
+          k_lad_filter_tiles<<<16 * sms, 256, 0, st>>>(A, ws.tb, ws.ntiles, n, ws.tcnt, ws.bound,
+                                                       ws.cand, ws.ncand);
+        else
+          k_lad_filter<<<16 * sms, 256, 0, st>>>(A, ws.bound, ws.cand, ws.ncand);
         k_lad_refine<<<(int)gn, 1024, 0, st>>>(A, ws.bound, ws.cand, ws.ncand, ws.overflow);
-        count_launches(5);
+        count_launches(P.tiled ? 3 : 5);
       }
       GB_LAUNCH_CHECK("k_lad_sample");
       k_lad_emit<<<(int)gn, 256, 0, st>>>(A, ws.Sfix, nullptr);

@@ -126,7 +126,8 @@ def sage_epoch(G: Graph, cfg: SamplerConfig, batches, epoch, batch_offset, mode=
     return SampledEpoch(SamplerKind.SAGE, epoch, batches, layers, cfg.layers)
 
 
-LADIES_MODES = {"exact": _lib.GB_LADIES_EXACT, "race": _lib.GB_LADIES_RACE}
+LADIES_MODES = {"exact": _lib.GB_LADIES_EXACT, "race": _lib.GB_LADIES_RACE,
+                "race_dense": _lib.GB_LADIES_RACE_DENSE}
 # auto -> exact replay while its O(s * N) serial cumsum per batch stays small
 LADIES_EXACT_LIMIT = 1 << 26
 

@@ -142,3 +142,22 @@ def test_ladies_race_structure_matches_exact_shapes():
                 for e in range(ptr[r], ptr[r + 1]):
                     c = lay["adj_col"][e] + (c0 if shared else 0)
                     assert (int(rows[r]), int(cols[c])) in A
+
+
+@pytest.mark.parametrize("scale,edges,k,b,layers,s", [(16, 300000, 24, 256, 2, 128),
+                                                      (12, 30000, 5, 64, 3, 48),
+                                                      (5, 60, 3, 4, 2, 3)])
+def test_ladies_race_tiled_equals_dense(scale, edges, k, b, layers, s):
+    """The column-tile race (shared-memory counts, one pass) selects exactly
+    what the dense-counter race selects: same keys, same (key, v) order."""
+    gb = _gb()
+    from test_sage_gpu import _rmat
+
+    rng = np.random.default_rng(scale)
+    n, rowptr, col = _rmat(scale, edges, seed=scale)
+    G = _graph(n, rowptr, col)
+    batches = [np.sort(rng.permutation(n)[: rng.integers(1, b + 1)]) for _ in range(k)]
+    cfg = gb.SamplerConfig.ladies(layers, b, s, bulk_count=k, seed=3)
+    tiled = gb.sample_epoch_bulk(G, cfg, batches, mode="race", epoch=2, batch_offset=7)
+    dense = gb.sample_epoch_bulk(G, cfg, batches, mode="race_dense", epoch=2, batch_offset=7)
+    assert O.compare_epochs(dense.to_arrays(), tiled.to_arrays()) == []
