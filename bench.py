@@ -473,6 +473,11 @@ def run_ours(args, rank, world, local_rank):
                        "roofline": {"achieved": a2, "peak": peak, "unit": "GB/s",
                                     "frac": a2 / peak, "kernel": KERNEL[other],
                                     "per_layer_ms": km.tolist(), "per_layer_bytes": kb2}}
+        if other == "stream":
+            line[other]["roofline"]["note"] = (
+                "algorithmic bytes stream every frontier row's A row, duplicates included; "
+                "repeated hub rows are served by the 126 MB L2, so achieved can exceed the "
+                "HBM peak (DRAM traffic: profiles/ncu_traffic.json k_sage_stream)")
         del b2, g2
     # LADIES, BASELINE configs[2]: same graph, 512 nodes/layer, 3 layers, k=64
     if not args.no_ladies:
