@@ -36,37 +36,47 @@ void prof_mark(cudaStream_t st) {
 // events, so it also works under CUDA graph capture), per device.
 struct Fork {
   cudaStream_t s[kForkStreams];
-  cudaEvent_t ev[kForkStreams + 1];
+  cudaEvent_t ev[kForkStreams + 2];
+  cudaEvent_t ring[kEventRing];
   bool ready = false;
 };
 static Fork g_fork[16];
 
-cudaStream_t fork_begin(cudaStream_t st, int n) {
+static Fork& fork_state() {
   int dev = 0;
   cudaGetDevice(&dev);
   Fork& f = g_fork[dev & 15];
   if (!f.ready) {
     for (int i = 0; i < kForkStreams; ++i)
       cudaStreamCreateWithFlags(&f.s[i], cudaStreamNonBlocking);
-    for (int i = 0; i <= kForkStreams; ++i)
+    for (int i = 0; i < kForkStreams + 2; ++i)
       cudaEventCreateWithFlags(&f.ev[i], cudaEventDisableTiming);
+    for (int i = 0; i < kEventRing; ++i)
+      cudaEventCreateWithFlags(&f.ring[i], cudaEventDisableTiming);
     f.ready = true;
   }
+  return f;
+}
+
+void stream_wait(cudaStream_t waiter, cudaStream_t src) {
+  Fork& f = fork_state();
+  cudaEventRecord(f.ev[kForkStreams + 1], src);
+  cudaStreamWaitEvent(waiter, f.ev[kForkStreams + 1], 0);
+}
+
+cudaEvent_t ring_event(int i) { return fork_state().ring[((i % kEventRing) + kEventRing) % kEventRing]; }
+
+cudaStream_t fork_begin(cudaStream_t st, int n) {
+  Fork& f = fork_state();
   cudaEventRecord(f.ev[kForkStreams], st);
   for (int i = 0; i < n && i < kForkStreams; ++i) cudaStreamWaitEvent(f.s[i], f.ev[kForkStreams], 0);
   return f.s[0];
 }
 
-cudaStream_t fork_stream(int i) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  return g_fork[dev & 15].s[i];
-}
+cudaStream_t fork_stream(int i) { return fork_state().s[i]; }
 
 void fork_join(cudaStream_t st, int n) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  Fork& f = g_fork[dev & 15];
+  Fork& f = fork_state();
   for (int i = 0; i < n && i < kForkStreams; ++i) {
     cudaEventRecord(f.ev[i], f.s[i]);
     cudaStreamWaitEvent(st, f.ev[i], 0);

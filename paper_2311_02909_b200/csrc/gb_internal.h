@@ -32,10 +32,15 @@ void prof_mark(cudaStream_t st);
 
 // Fork n <= kForkStreams side streams off st (they wait for st's work so
 // far), launch on fork_stream(i), then fork_join makes st wait for them.
-constexpr int kForkStreams = 2;
+constexpr int kForkStreams = 3;
 cudaStream_t fork_begin(cudaStream_t st, int n);
 cudaStream_t fork_stream(int i);
 void fork_join(cudaStream_t st, int n);
+// waiter continues only after src's work enqueued so far
+void stream_wait(cudaStream_t waiter, cudaStream_t src);
+// per-device event ring for ordering across streams (i mod kEventRing)
+constexpr int kEventRing = 8;
+cudaEvent_t ring_event(int i);
 
 int graph_build_tables(Graph* g, cudaStream_t st);
 int sage_workspace(const Graph* g, int64_t k, int64_t r1_cap, int32_t layers,

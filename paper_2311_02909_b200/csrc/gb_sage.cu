@@ -775,6 +775,22 @@ __global__ void k_sage_layer_meta(const int64_t* __restrict__ brow, int64_t k,
   }
 }
 
+// coloff and sizes only (eoff already written on the sampling stream)
+__global__ void k_sage_layer_cols(const int64_t* __restrict__ brow, int64_t k,
+                                  const int64_t* __restrict__ fptr,
+                                  const int32_t* __restrict__ wpre, int64_t nwords,
+                                  int64_t* __restrict__ coloff, int64_t* __restrict__ sizes) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b <= k;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    coloff[b] = wpre[b * nwords];
+    if (b == k) {
+      sizes[0] = brow[k];
+      sizes[1] = fptr[brow[k]];
+      sizes[2] = wpre[k * nwords];
+    }
+  }
+}
+
 // acol[e] = block-diagonal column of frontier entry e:
 //   coloff[batch] + rank of fcol[e] among the batch's sorted unique columns
 // (compact_columns sparse.py:352-357 + block_diag sparse.py:321-342)
@@ -929,8 +945,11 @@ struct SageWs {
   int32_t* deg;
   int64_t* gstart;
   int64_t* scan_ws;
-  uint32_t* bitmap;
-  int32_t* wpre;
+  uint32_t* bitmap;   // (batch, vertex) bits and their popcount prefix, two sets:
+  int32_t* wpre;      // layer l's extraction overlaps layer l + 1's sampling
+  uint32_t* bitmap2;
+  int32_t* wpre2;
+  int64_t* scan_ws2;  // scans of the extraction stream
   int64_t* d_W;
   // dedup mode
   uint32_t* vbits;   // one bit per vertex
@@ -964,6 +983,9 @@ static SageWs sage_ws_layout(char* base, int64_t k, int64_t n, int64_t r_cap_max
   w.scan_ws = (int64_t*)take(sizeof(int64_t) * scan_workspace_elems<int64_t>(scan_n + 1));
   w.bitmap = (uint32_t*)take(sizeof(uint32_t) * (W + 1));
   w.wpre = (int32_t*)take(sizeof(int32_t) * (W + 1));
+  w.bitmap2 = (uint32_t*)take(sizeof(uint32_t) * (W + 1));
+  w.wpre2 = (int32_t*)take(sizeof(int32_t) * (W + 1));
+  w.scan_ws2 = (int64_t*)take(sizeof(int64_t) * scan_workspace_elems<int64_t>(W + 1));
   w.d_W = (int64_t*)take(sizeof(int64_t));
   w.vbits = (uint32_t*)take(sizeof(uint32_t) * (nwords + 1));
   w.vpre = (int32_t*)take(sizeof(int32_t) * (nwords + 1));
@@ -1154,9 +1176,14 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     r_cap = f_cap;
   }
   GB_CUDA(cudaMemsetAsync(ws.bitmap, 0, sizeof(uint32_t) * (W + 1), st));
+  GB_CUDA(cudaMemsetAsync(ws.bitmap2, 0, sizeof(uint32_t) * (W + 1), st));
   k_set_i64<<<1, 1, 0, st>>>(ws.d_W, W);
   k_set_i64<<<1, 1, 0, st>>>(ws.d_nw, nwords);
   count_launches(2);
+  // extraction of layer l (popcount scan, rank, enumerate) runs on a side
+  // stream while layer l + 1 samples; layer l + 2 reuses layer l's bitmap
+  // only after that extraction (ring events) — graph-capturable
+  const cudaStream_t xs = fork_stream(2);
   int64_t stride = batch_size;
   r_cap = r1_cap;
   for (int32_t l = 0; l < layers; ++l) {
@@ -1167,6 +1194,9 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     const int64_t* brow = l == 0 ? d_bptr : L[l - 1].eoff;
     const int64_t* R_ptr = brow + k;
     const int32_t s = (int32_t)fanouts[l];
+    uint32_t* bm = (l & 1) ? ws.bitmap2 : ws.bitmap;
+    int32_t* wp = (l & 1) ? ws.wpre2 : ws.wpre;
+    if (l >= 2) GB_CUDA(cudaStreamWaitEvent(st, ring_event(l - 2), 0));
     k_sage_prep<<<grid_for(r_cap, 256, 16 * kNumSMs), 256, 0, st>>>(R_ptr, rowv, g->rowptr, ws.deg);
     GB_LAUNCH_CHECK("k_sage_prep");
     int rc = device_exclusive_scan<int64_t>(R_ptr, r_cap, TakeF{ws.deg, s}, o.fptr, ws.scan_ws, st);
@@ -1182,7 +1212,7 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     A.rowv = rowv; A.deg = ws.deg; A.fptr = o.fptr; A.gstart = ws.gstart;
     A.brow = brow; A.k = k; A.s = s; A.stride = stride; A.batch_offset = batch_offset;
     A.seed = seed; A.epoch = epoch; A.depth = (uint64_t)d;
-    A.bitmap = ws.bitmap; A.nwords = nwords; A.fcol = o.fcol; A.pidx = ws.pidx;
+    A.bitmap = bm; A.nwords = nwords; A.fcol = o.fcol; A.pidx = ws.pidx;
     const int pick_grid = grid_for(r_cap, kPickThreads, 64 * kNumSMs);
     if (dedup) {
       rc = dedup_prepare(g, ws, R_ptr, rowv, o.fptr, brow, k, s, r_cap, nwords, st);
@@ -1212,22 +1242,27 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
         count_launches(1);
       }
     }
-    rc = device_exclusive_scan<int64_t>(ws.d_W, W, PopF{ws.bitmap}, ws.wpre, ws.scan_ws, st);
+    // next layer's batch row offsets, on the sampling stream
+    k_sage_eoff<<<grid_for(k + 1, 128, 64), 128, 0, st>>>(brow, k, o.fptr, o.eoff);
+    GB_LAUNCH_CHECK("k_sage_eoff");
+    stream_wait(xs, st);
+    rc = device_exclusive_scan<int64_t>(ws.d_W, W, PopF{bm}, wp, ws.scan_ws2, xs);
     if (rc) return rc;
     int64_t* sizes = d_sizes + 3 * l;
-    k_sage_layer_meta<<<grid_for(k + 1, 128, 64), 128, 0, st>>>(brow, k, o.fptr, ws.wpre, nwords,
-                                                                 o.eoff, o.coloff, sizes);
-    GB_LAUNCH_CHECK("k_sage_layer_meta");
+    k_sage_layer_cols<<<grid_for(k + 1, 128, 64), 128, 0, xs>>>(brow, k, o.fptr, wp, nwords,
+                                                                 o.coloff, sizes);
+    GB_LAUNCH_CHECK("k_sage_layer_cols");
     const int64_t f_cap = r_cap * s;
-    k_sage_rank<<<grid_for(f_cap, 256, 16 * kNumSMs), 256, 0, st>>>(
-        sizes + 1, o.eoff, k, o.fcol, ws.bitmap, ws.wpre, nwords, o.acol);
+    k_sage_rank<<<grid_for(f_cap, 256, 16 * kNumSMs), 256, 0, xs>>>(
+        sizes + 1, o.eoff, k, o.fcol, bm, wp, nwords, o.acol);
     GB_LAUNCH_CHECK("k_sage_rank");
-    k_sage_enumerate<<<grid_for(W, 256, 16 * kNumSMs), 256, 0, st>>>(W, nwords, ws.bitmap, ws.wpre,
-                                                                       o.colv);
+    k_sage_enumerate<<<grid_for(W, 256, 16 * kNumSMs), 256, 0, xs>>>(W, nwords, bm, wp, o.colv);
     GB_LAUNCH_CHECK("k_sage_enumerate");
-    count_launches(5);  // prep, sample, meta, rank, enumerate
+    GB_CUDA(cudaEventRecord(ring_event(l), xs));
+    count_launches(6);  // prep, sample, eoff, cols, rank, enumerate
     r_cap = f_cap;
   }
+  stream_wait(st, xs);
   return GB_OK;
 }
 
