@@ -533,7 +533,9 @@ def run_15d(args, rank, world, local_rank):
     dg = graphgen.rmat_device_graph(n, m, symmetric=sym, seed=0)
     k = args.k or default_k(args.workload)
     allb = make_batches_for(n, k * grid.rows)
-    s = Sage15D(dg, grid, FANOUTS, BATCH, mode=args.mode, fetch=args.fetch)
+    # the grid samples row by row at the owner: stream or P-free kernels
+    m15 = "stream" if args.mode == "stream" else "pfree"
+    s = Sage15D(dg, grid, FANOUTS, BATCH, mode=m15, fetch=args.fetch)
     i = s.i
     mine = [np.asarray(x) for x in allb[i * k:(i + 1) * k]]
     for _ in range(max(args.warmup, 3)):
@@ -589,7 +591,7 @@ def run_15d(args, rank, world, local_rank):
             "config": {"workload": f"{args.workload}-shape R-MAT, GraphSAGE (15,10,5), "
                                    f"b=1024, k={k} per grid row",
                        "parallelism": f"1.5D grid {grid.rows}x{grid.c} (p={world}, c={grid.c})",
-                       "mode": args.mode, "fetch": args.fetch},
+                       "mode": m15, "fetch": args.fetch},
             "traffic_rank0": {k2: int(v) for k2, v in s.stats.items()},
         }), flush=True)
 
