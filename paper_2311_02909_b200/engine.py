@@ -276,75 +276,150 @@ class BulkSampler:
             raise ContractViolation("BulkSampler currently drives the SAGE path")
         self.G, self.cfg, self.mode = G, cfg, mode
         self.dg = G.device()
-        k = cfg.bulk_count
-        r1 = int(max_batch_vertices or k * cfg.batch_size)
-        self.bulk = SageBulk(self.dg, k, r1, cfg.batch_size, cfg.fanouts, mode=mode)
-        self.h_off = torch.empty(k + 1, dtype=torch.int64, pin_memory=True)
-        self.h_cat = torch.empty(max(r1, 1), dtype=torch.int32, pin_memory=True)
-        self.d_off = torch.empty(k + 1, dtype=torch.int64, device="cuda")
-        self.d_cat = torch.empty(max(r1, 1), dtype=torch.int32, device="cuda")
-        self.h_sizes = torch.empty(3 * cfg.layers, dtype=torch.int64, pin_memory=True)
+        self.r1 = int(max_batch_vertices or cfg.bulk_count * cfg.batch_size)
         self._pinned = {}
+        self._slots = [self._new_slot()]
+        self._copy_stream = torch.cuda.Stream()
         self.h2d_bytes = 0
         self.d2h_bytes = 0
 
-    def sample(self, batches, epoch=0, batch_offset=0, to_host=True) -> SampledEpoch:
+    def _new_slot(self):
+        """Device buffers + pinned input staging of one in-flight bulk."""
         import torch
 
+        k, r1, cfg = self.cfg.bulk_count, self.r1, self.cfg
+        return {
+            "bulk": SageBulk(self.dg, k, r1, cfg.batch_size, cfg.fanouts, mode=self.mode),
+            "h_off": torch.empty(k + 1, dtype=torch.int64, pin_memory=True),
+            "h_cat": torch.empty(max(r1, 1), dtype=torch.int32, pin_memory=True),
+            "d_off": torch.empty(k + 1, dtype=torch.int64, device="cuda"),
+            "d_cat": torch.empty(max(r1, 1), dtype=torch.int32, device="cuda"),
+            "h_sizes": torch.empty(3 * cfg.layers, dtype=torch.int64, pin_memory=True),
+            "copied": None,
+        }
+
+    @property
+    def bulk(self):
+        return self._slots[0]["bulk"]
+
+    def _upload(self, slot, batches):
         k = self.cfg.bulk_count
         if len(batches) != k:
             raise ContractViolation(f"BulkSampler built for {k} batches, got {len(batches)}")
         cat, off = _flatten_batches(batches, self.G.n)
         if k and int(np.max(np.diff(off))) > self.cfg.batch_size:
             raise ContractViolation("actual rows exceed the nominal stride")
-        if cat.size > self.h_cat.numel():
+        if cat.size > slot["h_cat"].numel():
             raise ContractViolation("more batch vertices than the sampler was built for")
         r1 = int(off[-1])
-        self.h_off.numpy()[:] = off
-        self.h_cat.numpy()[:r1] = cat
-        self.d_off.copy_(self.h_off, non_blocking=True)
-        self.d_cat[:r1].copy_(self.h_cat[:r1], non_blocking=True)
+        slot["h_off"].numpy()[:] = off
+        slot["h_cat"].numpy()[:r1] = cat
+        slot["d_off"].copy_(slot["h_off"], non_blocking=True)
+        slot["d_cat"][:r1].copy_(slot["h_cat"][:r1], non_blocking=True)
         self.h2d_bytes = 8 * (k + 1) + 4 * r1
-        self.bulk.launch(self.d_off, self.d_cat, self.cfg.seed, epoch, batch_offset)
-        self.h_sizes.copy_(self.bulk.sizes, non_blocking=True)
+        return cat, off
+
+    def _stage(self, slot, layers):
+        """One D2H copy per distinct device buffer into persistent pinned
+        staging on the current stream (frontier/adjacency/sampled arrays
+        alias each other and the next layer's rows; layer-1 rows are the
+        caller's input)."""
+        import torch
+
+        host = {}
+        nbytes = 0
+        for layer in layers:
+            for key, v in layer.device.items():
+                if isinstance(v, tuple):
+                    continue
+                ident = (v.data_ptr(), v.numel())
+                if ident in host or v.data_ptr() in (slot["d_off"].data_ptr(),
+                                                     slot["d_cat"].data_ptr()):
+                    continue
+                buf = self._pinned.get(v.data_ptr())
+                if buf is None or buf.numel() < v.numel():
+                    buf = torch.empty(max(v.numel(), 1), dtype=v.dtype, pin_memory=True)
+                    self._pinned[v.data_ptr()] = buf
+                buf[: v.numel()].copy_(v, non_blocking=True)
+                nbytes += v.numel() * v.element_size()
+                host[ident] = buf[: v.numel()]
+        return host, nbytes
+
+    def _host_epoch(self, slot, layers, host, batches, cat, off, epoch):
+        out_layers = []
+        for layer in layers:
+            h = {}
+            for key, v in layer.device.items():
+                if isinstance(v, tuple):
+                    h[key] = v
+                elif v.data_ptr() == slot["d_off"].data_ptr():
+                    h[key] = off
+                elif v.data_ptr() == slot["d_cat"].data_ptr():
+                    h[key] = cat[: v.numel()]
+                else:
+                    h[key] = host[(v.data_ptr(), v.numel())].numpy()
+            out_layers.append(LayerSample(layer.depth, device=h, n=self.G.n))
+        return SampledEpoch(SamplerKind.SAGE, epoch, batches, out_layers, self.cfg.layers)
+
+    def sample(self, batches, epoch=0, batch_offset=0, to_host=True) -> SampledEpoch:
+        import torch
+
+        slot = self._slots[0]
+        cat, off = self._upload(slot, batches)
+        slot["bulk"].launch(slot["d_off"], slot["d_cat"], self.cfg.seed, epoch, batch_offset)
+        slot["h_sizes"].copy_(slot["bulk"].sizes, non_blocking=True)
         torch.cuda.current_stream().synchronize()
-        sizes = self.h_sizes.numpy().copy()
-        layers = self.bulk.layers(self.d_off, self.d_cat, sizes)
+        sizes = slot["h_sizes"].numpy().copy()
+        layers = slot["bulk"].layers(slot["d_off"], slot["d_cat"], sizes)
         self.d2h_bytes = 8 * sizes.size
-        if to_host:
-            # one D2H copy per distinct device buffer into persistent pinned
-            # staging (frontier/adjacency/sampled arrays alias each other and
-            # the next layer's rows); layer-1 rows are the caller's input.
-            # Host arrays stay valid until the next sample() call.
-            host = {}
-            for layer in layers:
-                for key, v in layer.device.items():
-                    if isinstance(v, tuple):
-                        continue
-                    ident = (v.data_ptr(), v.numel())
-                    if ident in host or v.data_ptr() in (self.d_off.data_ptr(),
-                                                         self.d_cat.data_ptr()):
-                        continue
-                    buf = self._pinned.get(v.data_ptr())
-                    if buf is None or buf.numel() < v.numel():
-                        buf = torch.empty(max(v.numel(), 1), dtype=v.dtype, pin_memory=True)
-                        self._pinned[v.data_ptr()] = buf
-                    buf[: v.numel()].copy_(v, non_blocking=True)
-                    self.d2h_bytes += v.numel() * v.element_size()
-                    host[ident] = buf[: v.numel()]
-            torch.cuda.current_stream().synchronize()
-            out_layers = []
-            for layer in layers:
-                h = {}
-                for key, v in layer.device.items():
-                    if isinstance(v, tuple):
-                        h[key] = v
-                    elif v.data_ptr() == self.d_off.data_ptr():
-                        h[key] = off
-                    elif v.data_ptr() == self.d_cat.data_ptr():
-                        h[key] = cat[: v.numel()]
-                    else:
-                        h[key] = host[(v.data_ptr(), v.numel())].numpy()
-                out_layers.append(LayerSample(layer.depth, device=h, n=self.G.n))
-            layers = out_layers
-        return SampledEpoch(SamplerKind.SAGE, epoch, batches, layers, self.cfg.layers)
+        if not to_host:
+            return SampledEpoch(SamplerKind.SAGE, epoch, batches, layers, self.cfg.layers)
+        # Host arrays stay valid until the next sample() call.
+        host, nbytes = self._stage(slot, layers)
+        self.d2h_bytes += nbytes
+        torch.cuda.current_stream().synchronize()
+        return self._host_epoch(slot, layers, host, batches, cat, off, epoch)
+
+    def sample_stream(self, jobs, epoch=0):
+        """Generator over `jobs` (an iterable of (batches, batch_offset)):
+        yields each bulk's host SampledEpoch, with the device->host copy of
+        bulk j (side stream) overlapping the sampling of bulk j + 1 (two
+        device buffer sets alternate).  Same results as sample(); host arrays
+        of a yielded epoch stay valid until the generator is advanced twice.
+        """
+        import torch
+
+        if len(self._slots) < 2:
+            self._slots.append(self._new_slot())
+        cs = torch.cuda.current_stream()
+        xs = self._copy_stream
+        pend = None
+        j = 0
+        for batches, boff in jobs:
+            slot = self._slots[j % 2]
+            if slot["copied"] is not None:
+                cs.wait_event(slot["copied"])  # its previous bulk left the device
+            cat, off = self._upload(slot, batches)
+            slot["bulk"].launch(slot["d_off"], slot["d_cat"], self.cfg.seed, epoch, boff)
+            slot["h_sizes"].copy_(slot["bulk"].sizes, non_blocking=True)
+            done = torch.cuda.Event()
+            done.record(cs)
+            done.synchronize()  # sizes of bulk j (bulk j - 1 is still copying)
+            sizes = slot["h_sizes"].numpy().copy()
+            layers = slot["bulk"].layers(slot["d_off"], slot["d_cat"], sizes)
+            xs.wait_event(done)
+            with torch.cuda.stream(xs):
+                host, nbytes = self._stage(slot, layers)
+            slot["copied"] = torch.cuda.Event()
+            slot["copied"].record(xs)
+            self.d2h_bytes = 8 * sizes.size + nbytes
+            if pend is not None:
+                pslot, players, phost, pb, pcat, poff = pend
+                pslot["copied"].synchronize()
+                yield self._host_epoch(pslot, players, phost, pb, pcat, poff, epoch)
+            pend = (slot, layers, host, batches, cat, off)
+            j += 1
+        if pend is not None:
+            pslot, players, phost, pb, pcat, poff = pend
+            pslot["copied"].synchronize()
+            yield self._host_epoch(pslot, players, phost, pb, pcat, poff, epoch)

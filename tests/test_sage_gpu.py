@@ -149,3 +149,26 @@ def test_bulk_sampler_public_api_matches():
             assert O.compare_epochs(want, ep.to_arrays()) == []
         dev = bs.sample(g["batches"], epoch=g["epoch"], to_host=False)
         assert O.compare_epochs(want, dev.to_arrays()) == []
+
+
+def test_bulk_sampler_stream_matches_single_calls():
+    """sample_stream (copy of bulk j overlapping bulk j+1) returns exactly
+    what one sample() call per bulk returns."""
+    gb = _pkg()
+    from paper_2311_02909_b200.engine import BulkSampler
+
+    rng = np.random.default_rng(5)
+    n, rowptr, col = _rmat(13, 60000, seed=5)
+    G = _graph(n, rowptr, col)
+    cfg = gb.SamplerConfig.sage(3, 64, (15, 10, 5), bulk_count=4, seed=11)
+    jobs = [([rng.permutation(n)[: rng.integers(1, 65)] for _ in range(4)], 4 * j)
+            for j in range(5)]
+    want = []
+    for mode in ("dedup", "pfree"):
+        bs = BulkSampler(G, cfg, mode=mode)
+        for batches, boff in jobs:
+            want.append(bs.sample(batches, epoch=2, batch_offset=boff).to_arrays())
+        got = [ep.to_arrays() for ep in bs.sample_stream(jobs, epoch=2)]
+        assert len(got) == len(jobs)
+        for g, w in zip(got, want[-len(jobs):]):
+            assert O.compare_epochs(w, g) == []
