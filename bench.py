@@ -51,6 +51,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-pfree", action="store_true")
     p.add_argument("--no-ladies", action="store_true")
+    p.add_argument("--no-aggregation", action="store_true")
     p.add_argument("--dist", default="replicated", choices=["replicated", "15d"],
                    help="multi-GPU mode: replicated graph (cfg4) or 1.5D partitioned (cfg5)")
     p.add_argument("--c", type=int, default=2, help="1.5D replication factor")
@@ -213,6 +214,48 @@ def ladies_bytes(st, k):
     sum_l 44 nnz(Q) + 8 G + 16 N + 4 |S| + 4 E + 8 k + 16."""
     return sum(44 * s["Q"] + 8 * s["G"] + 16 * s["N"] + 4 * s["S"] + 4 * s["E"] + 8 * k + 16
                for s in st)
+
+
+def measure_aggregation(bulk, d_off, d_cat, sizes, st, n, k, peak, f=128):
+    """feature fetch of the deepest col_vertices and the
+    aggregation chain of the whole bulk (pipeline.propagate_bulk: Y = A^l X
+    per layer + first-occurrence carry), fp32 features of width f, random
+    H in HBM.  Algorithmic bytes: every gathered X row read once, every Y /
+    X row written once."""
+    import torch
+
+    from paper_2311_02909_b200.pipeline import _gather_rows, propagate_bulk
+    from paper_2311_02909_b200.sampler import SampledEpoch, SamplerKind
+
+    layers = bulk.layers(d_off, d_cat, sizes)
+    ep = SampledEpoch(SamplerKind.SAGE, 0, list(range(k)), layers, len(layers))
+    H = torch.rand((n, f), device="cuda")
+    colv = layers[-1].device["colv_cat"]
+
+    def run():
+        return propagate_bulk(ep, _gather_rows(colv, H))
+
+    for _ in range(2):
+        run()
+    torch.cuda.synchronize()
+    reps = 5
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        run()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / reps
+    row = 4 * f
+    byt = 2 * st[-1]["U"] * row  # fetch: read + write
+    for li, s_ in enumerate(st):
+        byt += s_["F"] * row + s_["R"] * row  # gathered X rows + Y rows
+        if li > 0:
+            byt += 2 * st[li - 1]["U"] * row  # carry to the shallower layer
+    del H
+    return {"ms_per_bulk": ms, "f": f, "dtype": "f32", "bytes_per_bulk": byt,
+            "gb_s": byt / (ms / 1e3) / 1e9, "frac_of_peak": byt / (ms / 1e3) / 1e9 / peak,
+            "api": "pipeline.propagate_bulk after the device fetch of layers[-1].col_vertices"}
 
 
 def measure_ladies(args, dg, rank, world, flush, peak):
@@ -413,6 +456,8 @@ def run_ours(args, rank, world, local_rank):
     peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(REPO, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
     peak = float(peaks.get("hbm_gbs", 6650.0))
+    agg = measure_aggregation(bulk, d_off, d_cat, sizes, st, n, k, peak) \
+        if not args.no_aggregation else None
     KERNEL = {"stream": "k_sage_stream", "dedup": "k_dd_serve", "pfree": "k_sage_pick<true>"}
     kb = [kernel_bytes(s, args.mode) for s in st]
     kern_avg = kern_ms.mean(axis=0)[:, -1]  # dominant kernel, per layer
@@ -436,6 +481,7 @@ def run_ours(args, rank, world, local_rank):
             "parallelism": f"replicated x{world}", "graph_build_s": round(t_graph, 2),
         },
         "gpu_launches": lpb * args.steps,
+        **({"aggregation": agg} if agg else {}),
         "clocks": clocks,
         "layers": st,
         "edges_per_s": world * sum(s["G"] for s in st) * args.steps / (total_ms / 1e3),

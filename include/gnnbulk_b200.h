@@ -144,6 +144,23 @@ int gb_gather_rows(int64_t m, const int32_t* d_ids, int64_t row0, const int64_t*
 int gb_gather_features(int64_t m, const int32_t* d_ids, int64_t row0, const float* d_H, int64_t f,
                        float* d_out, void* stream);
 
+/* ------------------------------------------ epoch pipeline aggregation
+ * Replaces forward_aggregate (pipeline.py:123-130) and the layer-to-layer
+ * carry of _propagate_batch (pipeline.py:280-305) for a whole bulk.
+ *   gb_spmm_rows        Y[r, :] = sum_e X[col[e] + shift[b(r)], :] over the
+ *                       stacked sampled adjacency (values 1.0), fp32; b(r)
+ *                       from d_row_batch[k+1] (rows of batch b); d_shift may
+ *                       be NULL (block-diagonal columns address X directly)
+ *   gb_first_occurrence first[j] = smallest entry e with column index j
+ *                       (col[e] + shift[b(e)], batch offsets d_entry_batch),
+ *                       or e itself when d_colidx is NULL; unset = INT32_MAX */
+int gb_spmm_rows(int64_t R, const int64_t* d_rowptr, const int32_t* d_col,
+                 const int64_t* d_row_batch, const int64_t* d_shift, int64_t k, const float* d_X,
+                 int64_t f, float* d_Y, void* stream);
+int gb_first_occurrence(int64_t F, const int32_t* d_colidx, const int64_t* d_entry_batch,
+                        const int64_t* d_shift, int64_t k, int64_t ncols, int32_t* d_first,
+                        void* stream);
+
 /* -------------------------------------------------------- LADIES bulk
  * sample_epoch_bulk with SamplerConfig.kind == LADIES (sampler.py:325-387,
  * 420-462, 475-483).  Layer-1 rows: the batches, each sorted and distinct

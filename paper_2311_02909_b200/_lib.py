@@ -80,6 +80,8 @@ SIGNATURES = {
                                              ctypes.c_size_t, _p]),
     "gb_gather_rows": (ctypes.c_int, [_i64, _p, _i64, _p, _p, _p, _p, _p]),
     "gb_gather_features": (ctypes.c_int, [_i64, _p, _i64, _p, _i64, _p, _p]),
+    "gb_spmm_rows": (ctypes.c_int, [_i64, _p, _p, _p, _p, _i64, _p, _i64, _p, _p]),
+    "gb_first_occurrence": (ctypes.c_int, [_i64, _p, _p, _p, _i64, _i64, _p, _p]),
     "gb_scan_workspace_bytes": (ctypes.c_size_t, [_i64]),
     "gb_spgemm_bound": (ctypes.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p]),
     "gb_spgemm": (ctypes.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p, _p, _i64, _p, _p, _p, _p, _p,

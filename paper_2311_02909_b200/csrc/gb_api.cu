@@ -277,6 +277,27 @@ int gb_gather_features(int64_t m, const int32_t* d_ids, int64_t row0, const floa
   return gather_features(m, d_ids, row0, d_H, f, d_out, (cudaStream_t)stream);
 }
 
+int gb_spmm_rows(int64_t R, const int64_t* d_rowptr, const int32_t* d_col,
+                 const int64_t* d_row_batch, const int64_t* d_shift, int64_t k, const float* d_X,
+                 int64_t f, float* d_Y, void* stream) {
+  if (R < 0 || f < 0 || k < 0 || (d_shift && !d_row_batch)) {
+    set_error("spmm_rows: bad arguments");
+    return GB_ERR_CONTRACT;
+  }
+  return spmm_rows(R, d_rowptr, d_col, d_row_batch, d_shift, k, d_X, f, d_Y, (cudaStream_t)stream);
+}
+
+int gb_first_occurrence(int64_t F, const int32_t* d_colidx, const int64_t* d_entry_batch,
+                        const int64_t* d_shift, int64_t k, int64_t ncols, int32_t* d_first,
+                        void* stream) {
+  if (F < 0 || ncols < 0 || F >= ((int64_t)1 << 31) || (d_shift && !d_entry_batch)) {
+    set_error("first_occurrence: bad arguments");
+    return GB_ERR_CONTRACT;
+  }
+  return first_occurrence(F, d_colidx, d_entry_batch, d_shift, k, ncols, d_first,
+                          (cudaStream_t)stream);
+}
+
 size_t gb_ladies_counts_workspace(int64_t k, int64_t n, int64_t q_cap) {
   return ladies_counts_ws(k, n, q_cap);
 }

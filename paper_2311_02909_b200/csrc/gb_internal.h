@@ -43,6 +43,11 @@ constexpr int kEventRing = 8;
 cudaEvent_t ring_event(int i);
 
 int graph_build_tables(Graph* g, cudaStream_t st);
+int spmm_rows(int64_t R, const int64_t* rowptr, const int32_t* col, const int64_t* rowb,
+              const int64_t* shift, int64_t k, const float* X, int64_t f, float* Y,
+              cudaStream_t st);
+int first_occurrence(int64_t F, const int32_t* colidx, const int64_t* eb, const int64_t* shift,
+                     int64_t k, int64_t ncols, int32_t* first, cudaStream_t st);
 int sage_workspace(const Graph* g, int64_t k, int64_t r1_cap, int32_t layers,
                    const int64_t* fanouts, size_t* bytes);
 int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d_bverts,

@@ -84,3 +84,25 @@ def test_make_batches_matches_reference_recipe():
         np.random.SeedSequence([1, 0x6261746368, 2]))).permutation(10)
     assert [x.tolist() for x in b] == [order[0:4].tolist(), order[4:8].tolist(),
                                        order[8:].tolist()]
+
+
+def test_epoch_plan_and_trainers_match_reference_rules():
+    from oracle import pipeline_ref as PR
+    from paper_2311_02909_b200.dist import ProcessGrid
+    from paper_2311_02909_b200.pipeline import EpochPlan, _trainer_of_batch
+
+    plan = EpochPlan.build(10, 4)
+    assert plan.chunks == ((0, 4), (4, 8), (8, 10)) and plan.rounds == 3
+    assert EpochPlan.build(0, 3).chunks == ()
+    import pytest
+    from paper_2311_02909_b200 import ContractViolation
+
+    with pytest.raises(ContractViolation):
+        EpochPlan.build(5, 0)
+    for p, c in [(1, 1), (4, 1), (4, 2), (8, 2)]:
+        grid = ProcessGrid(p, c)
+        for size in (1, 3, 8, 13):
+            for local in range(size):
+                for mode, rep in (("replicated", True), ("partitioned", False)):
+                    assert _trainer_of_batch(local, size, grid, mode) == \
+                        PR.trainer_of_batch(local, size, p, grid.rows, c, rep)
