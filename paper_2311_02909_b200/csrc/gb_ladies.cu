@@ -314,6 +314,7 @@ struct LadTileArgs {
 
 constexpr int kLTileRun = 8;      // consecutive tiles per ticket (row cursors carried over)
 constexpr int kLRowsSmem = 1024;  // rows whose cursors fit in shared memory
+constexpr int kLUnroll = 4;       // 32-entry loads in flight per row
 
 // One ticket = batch j and a run of kLTileRun consecutive column tiles.  Per
 // tile: counts in shared memory (warp per A row, from the row's cursor, which
@@ -380,14 +381,25 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
           e0 = a < b && __ldg(A.col + a) < v0 ? warp_lower_bound(A.col, a, b, v0) : a;
         }
         if (e0 >= b) continue;
-        for (int64_t e = e0 + lane;; e += 32) {
-          const int32_t c = e < b ? __ldg(A.col + e) : 0x7fffffff;
-          const bool in = c < v1;
-          if (in) atomicAdd(s_cnt + ((c - v0) >> 1), 1u << (((c - v0) & 1) << 4));
-          const unsigned out = __ballot_sync(FULL, !in);
-          if (out) {
-            if (cur && lane == 0) s_rc[q - q0] = (int32_t)(e - lane - a + __ffs(out) - 1);
-            break;
+        // kLUnroll 32-entry steps per round: all loads in flight
+        bool done = false;
+        for (int64_t e = e0 + lane; !done; e += 32 * kLUnroll) {
+          int32_t cv[kLUnroll];
+#pragma unroll
+          for (int u = 0; u < kLUnroll; ++u)
+            cv[u] = e + 32 * u < b ? __ldg(A.col + e + 32 * u) : 0x7fffffff;
+#pragma unroll
+          for (int u = 0; u < kLUnroll; ++u) {
+            if (done) break;
+            const int32_t c = cv[u];
+            const bool in = c < v1;
+            if (in) atomicAdd(s_cnt + ((c - v0) >> 1), 1u << (((c - v0) & 1) << 4));
+            const unsigned out = __ballot_sync(FULL, !in);
+            if (out) {
+              if (cur && lane == 0)
+                s_rc[q - q0] = (int32_t)(e + 32 * u - lane - a + __ffs(out) - 1);
+              done = true;
+            }
           }
         }
       }
