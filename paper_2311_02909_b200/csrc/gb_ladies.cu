@@ -856,6 +856,109 @@ __global__ void __launch_bounds__(kLadiesThreads) k_lad_extract(
   }
 }
 
+// A_S rows by hashing: CTA per (batch i, chunk of kXRows rows of Q_i); S_i
+// goes into a shared-memory hash (vertex -> rank, 2·kSmaxSmem slots) once
+// per item, then every A row of the chunk is streamed once (coalesced,
+// kXUnroll loads in flight per lane) and probed — no per-entry binary search,
+// hub rows read sequentially instead of searched per sampled vertex.  Hits
+// come out in row order (ascending v), i.e. the sorted intersection.
+constexpr int kXRows = 64;
+constexpr int kXSlots = 2 * kSmaxSmem;  // 2048
+constexpr int kXUnroll = 4;
+
+__device__ __forceinline__ uint32_t xhash(int32_t v) {
+  return ((uint32_t)v * 0x9E3779B1u) >> (32 - 11);  // kXSlots = 2^11
+}
+
+__global__ void __launch_bounds__(kLadiesThreads) k_lad_extract_hash(
+    const int64_t* __restrict__ qoff, int64_t k, int64_t chunks, const int32_t* __restrict__ qcol,
+    const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+    const int64_t* __restrict__ fptr, const int32_t* __restrict__ fcol,
+    const int64_t* __restrict__ coloff, const int64_t* __restrict__ slot,
+    int32_t* __restrict__ slots, int32_t* __restrict__ rcnt) {
+  __shared__ int32_t hkey[kXSlots];
+  __shared__ int16_t hval[kXSlots];
+  __shared__ int32_t sS[kSmaxSmem];
+  __shared__ int s_next;
+  const unsigned FULL = 0xffffffffu;
+  const int lane = lane_id();
+  for (int64_t item = blockIdx.x; item < k * chunks; item += gridDim.x) {
+    const int64_t i = item / chunks, c = item - i * chunks;
+    const int64_t q0 = qoff[i] + c * kXRows, q1 = min(q0 + kXRows, qoff[i + 1]);
+    if (q0 >= q1) continue;  // uniform over the CTA
+    const int64_t f0 = fptr[i], take = fptr[i + 1] - f0;
+    for (int x = threadIdx.x; x < kXSlots; x += blockDim.x) hkey[x] = -1;
+    if (threadIdx.x == 0) s_next = 0;
+    __syncthreads();
+    for (int64_t r = threadIdx.x; r < take; r += blockDim.x) {
+      const int32_t v = fcol[f0 + r];
+      sS[r] = v;
+      uint32_t h = xhash(v);
+      while (atomicCAS(&hkey[h], -1, v) != -1) h = (h + 1) & (kXSlots - 1);
+      hval[h] = (int16_t)r;
+    }
+    __syncthreads();
+    const int64_t cb = coloff[i];
+    for (;;) {
+      int r = 0;
+      if (lane == 0) r = atomicAdd(&s_next, 1);
+      r = __shfl_sync(FULL, r, 0);
+      const int64_t q = q0 + r;
+      if (q >= q1) break;
+      const int32_t u = qcol[q];
+      const int64_t a0 = rowptr[u], d = rowptr[u + 1] - a0;
+      int32_t* out = slots + slot[q];
+      int64_t o = 0;
+      if (d > 16 * take) {
+        // hub row: search each sampled vertex in A[u,:] (sorted)
+        for (int64_t r0 = 0; r0 < take; r0 += 32) {
+          bool hit = false;
+          if (r0 + lane < take) {
+            const int32_t v = sS[r0 + lane];
+            int64_t lo = 0, hi = d;
+            while (lo < hi) {
+              const int64_t mid = (lo + hi) >> 1;
+              if (__ldg(col + a0 + mid) < v) lo = mid + 1; else hi = mid;
+            }
+            hit = lo < d && __ldg(col + a0 + lo) == v;
+          }
+          const unsigned bal = __ballot_sync(FULL, hit);
+          if (hit) out[o + __popc(bal & ((1u << lane) - 1))] = (int32_t)(cb + r0 + lane);
+          o += __popc(bal);
+        }
+        if (lane == 0) rcnt[q] = (int32_t)o;
+        continue;
+      }
+      for (int64_t e0 = 0; e0 < d; e0 += 32 * kXUnroll) {
+        int32_t vv[kXUnroll];
+#pragma unroll
+        for (int w = 0; w < kXUnroll; ++w) {
+          const int64_t e = e0 + 32 * w + lane;
+          vv[w] = e < d ? __ldg(col + a0 + e) : -1;
+        }
+#pragma unroll
+        for (int w = 0; w < kXUnroll; ++w) {
+          int rank = -1;
+          const int32_t v = vv[w];
+          if (v >= 0) {
+            uint32_t h = xhash(v);
+            int32_t kk;
+            while ((kk = hkey[h]) != -1) {
+              if (kk == v) { rank = hval[h]; break; }
+              h = (h + 1) & (kXSlots - 1);
+            }
+          }
+          const unsigned bal = __ballot_sync(FULL, rank >= 0);
+          if (rank >= 0) out[o + __popc(bal & ((1u << lane) - 1))] = (int32_t)(cb + rank);
+          o += __popc(bal);
+        }
+      }
+      if (lane == 0) rcnt[q] = (int32_t)o;
+    }
+    __syncthreads();  // hash reused by the next item
+  }
+}
+
 struct RcntF {
   const int32_t* r;
   __device__ int64_t operator()(int64_t i) const { return r[i]; }
@@ -1158,9 +1261,18 @@ int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t*
     rc = device_exclusive_scan<int64_t>(d_QN, qc, RcapF{qcol, g->rowptr, qoff, o.fptr, k},
                                         ws.slot, ws.scan_ws, st);
     if (rc) return rc;
-    k_lad_extract<<<8 * sms, kLadiesThreads, 0, st>>>(qoff, k, qcol, g->rowptr, g->col, o.fptr,
-                                                     o.fcol, o.coloff, ws.slot, ws.slots,
-                                                     ws.rcnt);
+    if (s <= kSmaxSmem) {
+      // rows per batch: the batch sizes (layer 1, bounded by the Q rows) or s
+      const int64_t rows_max = l == 0 ? q1_cap : fanouts[l - 1];
+      const int64_t chunks = (rows_max + kXRows - 1) / kXRows;
+      k_lad_extract_hash<<<gcap(k * chunks, 1, 8 * sms), kLadiesThreads, 0, st>>>(
+          qoff, k, chunks, qcol, g->rowptr, g->col, o.fptr, o.fcol, o.coloff, ws.slot, ws.slots,
+          ws.rcnt);
+    } else {
+      k_lad_extract<<<8 * sms, kLadiesThreads, 0, st>>>(qoff, k, qcol, g->rowptr, g->col, o.fptr,
+                                                       o.fcol, o.coloff, ws.slot, ws.slots,
+                                                       ws.rcnt);
+    }
     rc = device_exclusive_scan<int64_t>(d_QN, qc, RcntF{ws.rcnt}, o.aptr, ws.scan_ws, st);
     if (rc) return rc;
     k_lad_pack_a<<<8 * sms, kLadiesThreads, 0, st>>>(qoff, k, ws.slot, ws.slots, o.aptr, o.acol);
