@@ -327,6 +327,7 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
   int32_t* s_rl = (int32_t*)(s_ra + kLRowsSmem);     // row length
   int32_t* s_rc = s_rl + kLRowsSmem;                 // row cursor (relative)
   __shared__ int32_t s_wcnt[kLTileThreads / 32 + 1];
+  __shared__ uint32_t s_stage[kLTileThreads / 32 * 64];
   __shared__ int64_t s_ticket;
   __shared__ unsigned long long s_nnz;
   const unsigned FULL = 0xffffffffu;
@@ -422,6 +423,9 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
         total += x;
       }
       const int64_t slot = j * A.n + v0;
+      // nonzeros of 32 words -> the warp's staging buffer (<= 64), then the
+      // keys with all lanes busy and coalesced slot writes
+      uint32_t* stg = s_stage + warp * 64;
       for (int w0 = wa; w0 < wb; w0 += 32) {
         const int w = w0 + lane;
         const uint32_t x = w < wb ? s_cnt[w] : 0u;
@@ -432,20 +436,24 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
           const int y = __shfl_up_sync(FULL, inc, o);
           if (lane >= o) inc += y;
         }
-        int o = base + inc - m;
+        int o = inc - m;
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const uint32_t e = (x >> (16 * h)) & 0xffffu;
-          if (e) {
-            const int32_t v = v0 + 2 * w + h;
-            const uint32_t key = A.rk(j, v, e);
-            A.pv[slot + o] = v;
-            A.keys[slot + o] = key;
-            atomicAdd(s_h + (key >> 20), 1u);
-            ++o;
-          }
+          if (e) stg[o++] = ((uint32_t)(2 * w + h) << 16) | e;  // (tile offset, count)
         }
-        base += __shfl_sync(FULL, inc, 31);
+        const int cnt = __shfl_sync(FULL, inc, 31);
+        __syncwarp();
+        for (int p = lane; p < cnt; p += 32) {
+          const uint32_t rec = stg[p];
+          const int32_t v = v0 + (int32_t)(rec >> 16);
+          const uint32_t key = A.rk(j, v, rec & 0xffffu);
+          A.pv[slot + base + p] = v;
+          A.keys[slot + base + p] = key;
+          atomicAdd(s_h + (key >> 20), 1u);
+        }
+        __syncwarp();
+        base += cnt;
       }
       if (threadIdx.x == 0) {
         A.tcnt[j * ntiles + t] = total;
