@@ -137,13 +137,18 @@ __global__ void k_build_runs(const int32_t* __restrict__ slot_deg, int64_t slots
 
 // ============================================================ layer kernels
 
+// degrees of the layer's rows; vbits != nullptr (dedup): also one bit per
+// vertex that some nonempty row references
 __global__ void k_sage_prep(const int64_t* __restrict__ R_ptr, const int32_t* __restrict__ rowv,
-                            const int64_t* __restrict__ rowptr, int32_t* __restrict__ deg) {
+                            const int64_t* __restrict__ rowptr, int32_t* __restrict__ deg,
+                            uint32_t* __restrict__ vbits) {
   const int64_t R = *R_ptr;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
        r += (int64_t)gridDim.x * blockDim.x) {
     const int32_t v = rowv[r];
-    deg[r] = (int32_t)(rowptr[v + 1] - rowptr[v]);
+    const int32_t d = (int32_t)(rowptr[v + 1] - rowptr[v]);
+    deg[r] = d;
+    if (vbits && d > 0) atomicOr(vbits + (v >> 5), 1u << (v & 31));
   }
 }
 
@@ -495,18 +500,6 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k_sage_stream(SageArgs A,
 // in shared memory — and every frontier row that references it draws its
 // picks from there: NORM + SAMPLE + the P-row gather in one kernel, with no
 // per-row global table look-ups and no intermediate pick records.
-
-// one bit per vertex that some row of the layer references
-__global__ void k_dd_mark(const int64_t* __restrict__ R_ptr, const int32_t* __restrict__ rowv,
-                          const int32_t* __restrict__ deg, uint32_t* __restrict__ vbits) {
-  const int64_t R = *R_ptr;
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
-       r += (int64_t)gridDim.x * blockDim.x)
-    if (deg[r] > 0) {
-      const int32_t v = rowv[r];
-      atomicOr(vbits + (v >> 5), 1u << (v & 31));
-    }
-}
 
 // distinct vertex list (ascending) and degrees
 __global__ void k_dd_list(int64_t nwords, const uint32_t* __restrict__ vbits,
@@ -1032,10 +1025,11 @@ static int dedup_prepare(const Graph* g, SageWs& ws, const int64_t* R_ptr, const
                          const int64_t* fptr, const int64_t* brow, int64_t k, int32_t s,
                          int64_t r_cap, int64_t nwords, cudaStream_t st) {
   const int64_t gw = 16 * kNumSMs;
-  GB_CUDA(cudaMemsetAsync(ws.vbits, 0, sizeof(uint32_t) * (nwords + 1), st));
-  GB_CUDA(cudaMemsetAsync(ws.gcnt, 0, sizeof(int32_t) * (r_cap + 1), st));
-  GB_CUDA(cudaMemsetAsync(ws.gcur, 0, sizeof(int32_t) * (r_cap + 1), st));
-  k_dd_mark<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, ws.vbits);
+  // (vertex bitmap already marked by k_sage_prep)
+  // distinct row vertices D <= min(rows, n): group arrays sized by that
+  const int64_t dcap = r_cap < g->n ? r_cap : g->n;
+  GB_CUDA(cudaMemsetAsync(ws.gcnt, 0, sizeof(int32_t) * (dcap + 1), st));
+  GB_CUDA(cudaMemsetAsync(ws.gcur, 0, sizeof(int32_t) * (dcap + 1), st));
   int rc = device_exclusive_scan<int64_t>(ws.d_nw, nwords, VPopF{ws.vbits}, ws.vpre, ws.scan_ws,
                                           st);
   if (rc) return rc;
@@ -1044,19 +1038,19 @@ static int dedup_prepare(const Graph* g, SageWs& ws, const int64_t* R_ptr, const
                                                       ws.dv, ws.ddeg);
   k_dd_rcount<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, ws.vbits, ws.vpre,
                                                        ws.gcnt);
-  rc = device_exclusive_scan<int64_t>(ws.d_nw + 1, r_cap, GcntF{ws.gcnt}, ws.roff, ws.scan_ws, st);
+  rc = device_exclusive_scan<int64_t>(ws.d_nw + 1, dcap, GcntF{ws.gcnt}, ws.roff, ws.scan_ws, st);
   if (rc) return rc;
   k_dd_rows<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, fptr, brow, k,
                                                      ws.vbits, ws.vpre, ws.roff, ws.gcur,
                                                      ws.rrec);
-  rc = device_exclusive_scan<int64_t>(ws.d_nw + 2, 3 * r_cap,
+  rc = device_exclusive_scan<int64_t>(ws.d_nw + 2, 3 * dcap,
                                       ItemF{ws.ddeg, ws.gcnt, ws.d_nw + 1, dd_items(s)},
                                       ws.ioff, ws.scan_ws, st);
   if (rc) return rc;
-  k_dd_items<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(ws.d_nw + 1, ws.dv, ws.ddeg, g->rowptr, ws.roff,
+  k_dd_items<<<grid_for(dcap, 256, gw), 256, 0, st>>>(ws.d_nw + 1, ws.dv, ws.ddeg, g->rowptr, ws.roff,
                                                       ws.ioff, dd_items(s), ws.items);
   GB_LAUNCH_CHECK("dedup prepare");
-  count_launches(7);
+  count_launches(6);
   return GB_OK;
 }
 
@@ -1197,7 +1191,9 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     uint32_t* bm = (l & 1) ? ws.bitmap2 : ws.bitmap;
     int32_t* wp = (l & 1) ? ws.wpre2 : ws.wpre;
     if (l >= 2) GB_CUDA(cudaStreamWaitEvent(st, ring_event(l - 2), 0));
-    k_sage_prep<<<grid_for(r_cap, 256, 16 * kNumSMs), 256, 0, st>>>(R_ptr, rowv, g->rowptr, ws.deg);
+    if (dedup) GB_CUDA(cudaMemsetAsync(ws.vbits, 0, sizeof(uint32_t) * (nwords + 1), st));
+    k_sage_prep<<<grid_for(r_cap, 256, 16 * kNumSMs), 256, 0, st>>>(R_ptr, rowv, g->rowptr, ws.deg,
+                                                                     dedup ? ws.vbits : nullptr);
     GB_LAUNCH_CHECK("k_sage_prep");
     int rc = device_exclusive_scan<int64_t>(R_ptr, r_cap, TakeF{ws.deg, s}, o.fptr, ws.scan_ws, st);
     if (rc) return rc;
