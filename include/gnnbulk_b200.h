@@ -160,6 +160,15 @@ int gb_spmm_rows(int64_t R, const int64_t* d_rowptr, const int32_t* d_col,
 int gb_first_occurrence(int64_t F, const int32_t* d_colidx, const int64_t* d_entry_batch,
                         const int64_t* d_shift, int64_t k, int64_t ncols, int32_t* d_first,
                         void* stream);
+/* Segmented copy of the distributed executor (placing picks returned by the
+ * block owner into the frontier, dist.py:357-361 reply handling; packing
+ * slot-layout A_S rows, dist.py:523-541):
+ * d_dst[d_dst_off[row_i] + t] = d_src[d_src_off[i] + t], t < len_i, with
+ * row_i = d_rows[i] (identity if NULL), len_i = d_lens[i] (or
+ * d_src_off[i+1] - d_src_off[i] if NULL). */
+int gb_segment_copy(int64_t m, const int64_t* d_rows, const int64_t* d_src_off,
+                    const int32_t* d_lens, const int32_t* d_src, const int64_t* d_dst_off,
+                    int32_t* d_dst, void* stream);
 
 /* -------------------------------------------------------- LADIES bulk
  * sample_epoch_bulk with SamplerConfig.kind == LADIES (sampler.py:325-387,

@@ -82,6 +82,7 @@ SIGNATURES = {
     "gb_gather_features": (ctypes.c_int, [_i64, _p, _i64, _p, _i64, _p, _p]),
     "gb_spmm_rows": (ctypes.c_int, [_i64, _p, _p, _p, _p, _i64, _p, _i64, _p, _p]),
     "gb_first_occurrence": (ctypes.c_int, [_i64, _p, _p, _p, _i64, _i64, _p, _p]),
+    "gb_segment_copy": (ctypes.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p]),
     "gb_scan_workspace_bytes": (ctypes.c_size_t, [_i64]),
     "gb_spgemm_bound": (ctypes.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p]),
     "gb_spgemm": (ctypes.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p, _p, _i64, _p, _p, _p, _p, _p,

@@ -114,4 +114,30 @@ int first_occurrence(int64_t F, const int32_t* colidx, const int64_t* eb, const 
   return GB_OK;
 }
 
+// dst[dst_off[row_i] + t] = src[src_off[i] + t] for t < len_i, warp per
+// segment; row_i = rows[i] (identity when rows == nullptr), len_i = lens[i]
+// or src_off[i + 1] - src_off[i].  Places the picks returned by block owners
+// and packs slot-layout rows in the distributed executor.
+__global__ void k_segment_copy(int64_t m, const int64_t* __restrict__ rows,
+                               const int64_t* __restrict__ src_off,
+                               const int32_t* __restrict__ lens, const int32_t* __restrict__ src,
+                               const int64_t* __restrict__ dst_off, int32_t* __restrict__ dst) {
+  const int lane = lane_id();
+  for (int64_t i = global_warp(); i < m; i += grid_warps()) {
+    const int64_t s0 = src_off[i];
+    const int64_t len = lens ? (int64_t)lens[i] : src_off[i + 1] - s0;
+    const int64_t d0 = dst_off[rows ? rows[i] : i];
+    for (int64_t t = lane; t < len; t += 32) dst[d0 + t] = src[s0 + t];
+  }
+}
+
+int segment_copy(int64_t m, const int64_t* rows, const int64_t* src_off, const int32_t* lens,
+                 const int32_t* src, const int64_t* dst_off, int32_t* dst, cudaStream_t st) {
+  if (m == 0) return GB_OK;
+  k_segment_copy<<<agg_grid(m * 32, 256), 256, 0, st>>>(m, rows, src_off, lens, src, dst_off, dst);
+  GB_LAUNCH_CHECK("k_segment_copy");
+  count_launches(1);
+  return GB_OK;
+}
+
 }  // namespace gb

@@ -287,6 +287,16 @@ int gb_spmm_rows(int64_t R, const int64_t* d_rowptr, const int32_t* d_col,
   return spmm_rows(R, d_rowptr, d_col, d_row_batch, d_shift, k, d_X, f, d_Y, (cudaStream_t)stream);
 }
 
+int gb_segment_copy(int64_t m, const int64_t* d_rows, const int64_t* d_src_off,
+                    const int32_t* d_lens, const int32_t* d_src, const int64_t* d_dst_off,
+                    int32_t* d_dst, void* stream) {
+  if (m < 0 || (m > 0 && (!d_src_off || !d_src || !d_dst_off || !d_dst))) {
+    set_error("segment_copy: bad arguments");
+    return GB_ERR_CONTRACT;
+  }
+  return segment_copy(m, d_rows, d_src_off, d_lens, d_src, d_dst_off, d_dst, (cudaStream_t)stream);
+}
+
 int gb_first_occurrence(int64_t F, const int32_t* d_colidx, const int64_t* d_entry_batch,
                         const int64_t* d_shift, int64_t k, int64_t ncols, int32_t* d_first,
                         void* stream) {

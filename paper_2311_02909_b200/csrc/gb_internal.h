@@ -46,6 +46,8 @@ int graph_build_tables(Graph* g, cudaStream_t st);
 int spmm_rows(int64_t R, const int64_t* rowptr, const int32_t* col, const int64_t* rowb,
               const int64_t* shift, int64_t k, const float* X, int64_t f, float* Y,
               cudaStream_t st);
+int segment_copy(int64_t m, const int64_t* rows, const int64_t* src_off, const int32_t* lens,
+                 const int32_t* src, const int64_t* dst_off, int32_t* dst, cudaStream_t st);
 int first_occurrence(int64_t F, const int32_t* colidx, const int64_t* eb, const int64_t* shift,
                      int64_t k, int64_t ncols, int32_t* first, cudaStream_t st);
 int sage_workspace(const Graph* g, int64_t k, int64_t r1_cap, int32_t layers,

@@ -235,11 +235,13 @@ class Sage15D:
                     self.ledger.charge(self.rank, "gather-cols", 1, 2 * sel.numel())
             got = exchange(replies, {owner: want}, self.col_ranks, torch.int32, dev)
             if want:
-                picks = got[owner]
-                base = torch.repeat_interleave(fptr[sel], tsel)
-                excl = torch.cumsum(tsel, 0) - tsel
-                pos = base + torch.arange(want, device=dev) - torch.repeat_interleave(excl, tsel)
-                fcol[pos] = picks
+                # each selected row's picks into its frontier slot
+                soff = torch.zeros(sel.numel() + 1, dtype=torch.int64, device=dev)
+                soff[1:] = torch.cumsum(tsel, 0)
+                _lib.check(L.gb_segment_copy(sel.numel(), _lib.ptr(sel.contiguous()),
+                                             _lib.ptr(soff), None, _lib.ptr(got[owner]),
+                                             _lib.ptr(fptr), _lib.ptr(fcol), _lib.stream_ptr()),
+                           "gb_segment_copy")
 
     # -- one bulk --------------------------------------------------------------------------
     def sample(self, group_batches, epoch, batch_offset, seed):
@@ -468,12 +470,12 @@ class Ladies15D(Sage15D):
             aptr = torch.zeros(QN + 1, dtype=torch.int64, device=dev)
             aptr[1:] = torch.cumsum(rcnt[:QN].long(), 0)
             E = int(aptr[-1].item())
+            acol = torch.zeros(max(E, 1), dtype=torch.int32, device=dev)
             if E:
-                src = (slot[:-1].repeat_interleave(rcnt[:QN].long()) +
-                       torch.arange(E, device=dev) - aptr[:-1].repeat_interleave(rcnt[:QN].long()))
-                acol = slots[src]
-            else:
-                acol = torch.zeros(0, dtype=torch.int32, device=dev)
+                _lib.check(L.gb_segment_copy(QN, None, _lib.ptr(slot), _lib.ptr(rcnt),
+                                             _lib.ptr(slots), _lib.ptr(aptr), _lib.ptr(acol),
+                                             _lib.stream_ptr()), "gb_segment_copy")
+            acol = acol[:E]
             width = 0 if k == 0 else (int(takes[0].item()) if shared else F)
             layers.append({
                 "frontier_shape": (k, n), "frontier_ptr": fptr, "frontier_col": fcol,
