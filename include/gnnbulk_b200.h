@@ -252,6 +252,9 @@ int gb_its_rows(int64_t m, const int64_t* d_ptr, const double* d_val, int32_t s,
  *   gb_ladies_counts       partial P = Q A over the rows with d_qdeg[q] > 0
  *                          through a local CSR addressed by d_qcol[q]: per
  *                          batch the sorted (v, e) nonzeros at d_poff[i]
+ *   gb_ladies_merge_counts sum of partial (batch, v, e) int32 triples d_trip
+ *                          [3m] for v in [v0, v0 + nloc) (the sparse merge of
+ *                          the grid row): per batch the sorted (v, e) at d_poff
  *   gb_ladies_race_topk    exponential-race top-s of every batch's (v, e)
  *                          list: d_take[i], sorted vertices d_Sv[i*s ...] and
  *                          their race keys d_Sk (for the grid-row merge)
@@ -263,6 +266,10 @@ int gb_ladies_counts(int64_t k, const int64_t* d_qoff, const int32_t* d_qcol, co
                      int64_t q_cap, const int64_t* d_rowptr, const int32_t* d_col, int64_t n,
                      int64_t* d_poff, int32_t* d_pv, int32_t* d_pe, void* d_ws, size_t ws_bytes,
                      void* stream);
+size_t gb_ladies_merge_counts_workspace(int64_t k, int64_t nloc);
+int gb_ladies_merge_counts(int64_t k, int64_t m, const int32_t* d_trip, int64_t v0, int64_t nloc,
+                           int64_t* d_poff, int32_t* d_pv, int32_t* d_pe, void* d_ws,
+                           size_t ws_bytes, void* stream);
 size_t gb_ladies_race_topk_workspace(int64_t k, int64_t p_cap, int32_t s);
 int gb_ladies_race_topk(int64_t k, const int64_t* d_poff, const int32_t* d_pv, const int32_t* d_pe,
                         int64_t p_cap, int32_t s, uint64_t seed, uint64_t epoch, uint64_t depth,

@@ -321,6 +321,21 @@ int gb_ladies_counts(int64_t k, const int64_t* d_qoff, const int32_t* d_qcol, co
                        d_ws, ws_bytes, (cudaStream_t)stream);
 }
 
+size_t gb_ladies_merge_counts_workspace(int64_t k, int64_t nloc) {
+  return ladies_merge_ws(k, nloc);
+}
+
+int gb_ladies_merge_counts(int64_t k, int64_t m, const int32_t* d_trip, int64_t v0, int64_t nloc,
+                           int64_t* d_poff, int32_t* d_pv, int32_t* d_pe, void* d_ws,
+                           size_t ws_bytes, void* stream) {
+  if (k < 0 || m < 0 || v0 < 0 || nloc < 0) {
+    set_error("ladies merge: bad arguments");
+    return GB_ERR_CONTRACT;
+  }
+  return ladies_merge_counts(k, m, d_trip, v0, nloc, d_poff, d_pv, d_pe, d_ws, ws_bytes,
+                             (cudaStream_t)stream);
+}
+
 size_t gb_ladies_race_topk_workspace(int64_t k, int64_t p_cap, int32_t s) {
   return ladies_race_topk_ws(k, p_cap, s);
 }

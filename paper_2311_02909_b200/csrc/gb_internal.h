@@ -79,6 +79,10 @@ int gather_rows(int64_t m, const int32_t* ids, int64_t row0, const int64_t* rowp
 int gather_features(int64_t m, const int32_t* ids, int64_t row0, const float* H, int64_t f,
                     float* out, cudaStream_t st);
 size_t ladies_counts_ws(int64_t k, int64_t n, int64_t q_cap);
+size_t ladies_merge_ws(int64_t k, int64_t nloc);
+int ladies_merge_counts(int64_t k, int64_t m, const int32_t* trip, int64_t v0, int64_t nloc,
+                        int64_t* poff, int32_t* pv, int32_t* pe, void* d_ws, size_t ws_bytes,
+                        cudaStream_t st);
 int ladies_counts(int64_t k, const int64_t* qoff, const int32_t* qcol, const int32_t* qdeg,
                   int64_t q_cap, const int64_t* rowptr, const int32_t* col, int64_t n,
                   int64_t* poff, int32_t* pv, int32_t* pe, void* d_ws, size_t ws_bytes,

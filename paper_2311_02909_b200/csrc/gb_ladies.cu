@@ -197,7 +197,8 @@ __global__ void __launch_bounds__(256) k_lad_compact_write(uint32_t* __restrict_
                                                          const int64_t* __restrict__ tile_off,
                                                          int32_t* __restrict__ pv,
                                                          int32_t* __restrict__ pe,
-                                                         const int64_t* __restrict__ obase) {
+                                                         const int64_t* __restrict__ obase,
+                                                         int32_t vbase = 0) {
   __shared__ int64_t sw[33];
   if (obase) {
     pv += *obase;
@@ -226,7 +227,7 @@ __global__ void __launch_bounds__(256) k_lad_compact_write(uint32_t* __restrict_
         if (e) {
           int64_t v = flat + h - base;
           while (v >= n) { ++jb; base += n; v -= n; }
-          pv[o] = (int32_t)v;
+          pv[o] = (int32_t)v + vbase;
           pe[o] = (int32_t)e;
           ++o;
         }
@@ -1369,6 +1370,70 @@ int ladies_counts(int64_t k, const int64_t* qoff, const int32_t* qcol, const int
                                                                 pe, poff + g0);
     GB_LAUNCH_CHECK("ladies_counts");
     count_launches(4);
+  }
+  return GB_OK;
+}
+
+// Sum of partial (batch, v, e) triples for the vertex range [v0, v0 + nloc)
+// (the sparse merge of the 1.5D LADIES counts): RED adds into the grouped
+// packed 16-bit counters, then the same compaction as ladies_counts.
+__global__ void k_lad_merge_add(int64_t m, const int32_t* __restrict__ trip, int64_t g0,
+                                int64_t g1, int64_t v0, int64_t nloc,
+                                uint32_t* __restrict__ cnt32) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = trip[3 * t];
+    if (b < g0 || b >= g1) continue;
+    const int64_t idx = (b - g0) * nloc + (trip[3 * t + 1] - v0);
+    atomicAdd(cnt32 + (idx >> 1), (uint32_t)trip[3 * t + 2] << ((uint32_t)(idx & 1) << 4));
+  }
+}
+
+size_t ladies_merge_ws(int64_t k, int64_t nloc) { return ladies_counts_ws(k, nloc, 1); }
+
+int ladies_merge_counts(int64_t k, int64_t m, const int32_t* trip, int64_t v0, int64_t nloc,
+                        int64_t* poff, int32_t* pv, int32_t* pe, void* d_ws, size_t ws_bytes,
+                        cudaStream_t st) {
+  if (ladies_merge_ws(k, nloc) > ws_bytes) {
+    set_error("ladies merge workspace too small");
+    return GB_ERR_CAPACITY;
+  }
+  int64_t gsize = nloc > 0 ? kGroupBytes / (2 * nloc) : k;
+  if (gsize < 1) gsize = 1;
+  if (gsize > k) gsize = k > 0 ? k : 1;
+  const int64_t pwords = (gsize * nloc + 1) / 2 + 1;
+  const int64_t tiles = (2 * pwords + kCompTile - 1) / kCompTile;
+  char* p = (char*)d_ws;
+  auto carve = [&](size_t bytes) { char* r = p; p += al(bytes); return r; };
+  uint32_t* cnt32 = (uint32_t*)carve(sizeof(uint32_t) * pwords);
+  int64_t* nnz_b = (int64_t*)carve(sizeof(int64_t) * (k + 1));
+  carve(sizeof(int64_t) * 2);  // (q rows of ladies_counts_ws: unused here)
+  int64_t* tile_off = (int64_t*)carve(sizeof(int64_t) * (tiles + 1));
+  const int64_t sn = tiles > 1 ? tiles : 1;
+  int64_t* scan_ws = (int64_t*)carve(sizeof(int64_t) * scan_workspace_elems<int64_t>(sn + 1));
+  int64_t* d_tiles = (int64_t*)carve(sizeof(int64_t) * 4);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  if (sms <= 0) sms = kNumSMs;
+  GB_CUDA(cudaMemsetAsync(cnt32, 0, sizeof(uint32_t) * pwords, st));
+  GB_CUDA(cudaMemsetAsync(nnz_b, 0, sizeof(int64_t) * (k + 1), st));
+  k_lad_set<<<1, 1, 0, st>>>(d_tiles, tiles);
+  if (k == 0) k_lad_poff<<<1, 1, 0, st>>>(nnz_b, 0, 0, poff);
+  for (int64_t g0 = 0; g0 < k; g0 += gsize) {
+    const int64_t g1 = g0 + gsize < k ? g0 + gsize : k;
+    const int64_t gn = g1 - g0;
+    const int64_t words = (gn * nloc + 1) / 2;
+    if (m > 0)
+      k_lad_merge_add<<<gcap(m, 256, 16 * sms), 256, 0, st>>>(m, trip, g0, g1, v0, nloc, cnt32);
+    k_lad_compact_count<<<gcap(tiles, 1, 8 * sms), 256, 0, st>>>(cnt32, words, nloc, g0,
+                                                                tile_off, nnz_b);
+    k_lad_poff<<<1, 1, 0, st>>>(nnz_b, g0, gn, poff);
+    int rc = device_exclusive_scan<int64_t>(d_tiles, tiles, TileF{tile_off}, tile_off, scan_ws, st);
+    if (rc) return rc;
+    k_lad_compact_write<<<gcap(tiles, 1, 8 * sms), 256, 0, st>>>(cnt32, words, nloc, tile_off, pv,
+                                                                pe, poff + g0, (int32_t)v0);
+    GB_LAUNCH_CHECK("ladies_merge_counts");
+    count_launches(5);
   }
   return GB_OK;
 }

@@ -390,15 +390,19 @@ class Ladies15D(Sage15D):
             got = exchange(sends, cnts, self.row_ranks, torch.int32, dev)
             allt = torch.cat([got[p].view(-1, 3) for p in self.row_ranks if p in got]) \
                 if got else torch.zeros((0, 3), dtype=torch.int32, device=dev)
-            key = allt[:, 0].long() * n + allt[:, 1].long()
-            ukey, inv = torch.unique(key, return_inverse=True)
-            esum = torch.zeros(ukey.numel(), dtype=torch.int64, device=dev)
-            esum.index_add_(0, inv, allt[:, 2].long())
-            mb = (ukey // n)
+            # sum the partials of this replica's vertex range on the device
+            v0, v1 = int(vr[self.j]), int(vr[self.j + 1])
+            allt = allt.contiguous()
+            mcnt = allt.shape[0]
             moff = torch.zeros(k + 1, dtype=torch.int64, device=dev)
-            moff[1:] = torch.cumsum(torch.bincount(mb, minlength=k), 0)
-            mv = (ukey % n).to(torch.int32).contiguous()
-            me = esum.to(torch.int32).contiguous()
+            mv = torch.empty(max(mcnt, 1), dtype=torch.int32, device=dev)
+            me = torch.empty(max(mcnt, 1), dtype=torch.int32, device=dev)
+            mws = torch.empty(max(L.gb_ladies_merge_counts_workspace(k, v1 - v0), 1),
+                              dtype=torch.uint8, device=dev)
+            _lib.check(L.gb_ladies_merge_counts(k, mcnt, _lib.ptr(allt), v0, v1 - v0,
+                                                _lib.ptr(moff), _lib.ptr(mv), _lib.ptr(me),
+                                                _lib.ptr(mws), mws.numel(), _lib.stream_ptr()),
+                       "gb_ladies_merge_counts")
             # -- local race top-s, then the grid-row merge of candidates
             mcap = max(mv.numel(), 1)
             take = torch.zeros(k, dtype=torch.int64, device=dev)

@@ -15,6 +15,7 @@ def main():
     ap.add_argument("--workload", default="products")
     ap.add_argument("--k", type=int, default=64)
     ap.add_argument("--fetch", default="owner")
+    ap.add_argument("--sampler", default="sage", choices=["sage", "ladies"])
     a = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -25,15 +26,20 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
     from paper_2311_02909_b200 import graphgen
     from paper_2311_02909_b200.dist import ProcessGrid
-    from paper_2311_02909_b200.dist_exec import Sage15D
+    from paper_2311_02909_b200.dist_exec import Ladies15D, Sage15D
     from paper_2311_02909_b200.pipeline import make_batches
 
     grid = ProcessGrid(world, a.c)
     n, m, sym = graphgen.SHAPES[a.workload]
     dg = graphgen.rmat_device_graph(n, m, symmetric=sym, seed=0)
-    allb = make_batches(np.arange(n), 1024, 0, 0)[:a.k * grid.rows]
-    s = Sage15D(dg, grid, (15, 10, 5), 1024, mode="pfree", fetch=a.fetch)
-    mine = [np.asarray(x) for x in allb[s.i * a.k:(s.i + 1) * a.k]]
+    if a.sampler == "sage":
+        allb = make_batches(np.arange(n), 1024, 0, 0)[:a.k * grid.rows]
+        s = Sage15D(dg, grid, (15, 10, 5), 1024, mode="pfree", fetch=a.fetch)
+        mine = [np.asarray(x) for x in allb[s.i * a.k:(s.i + 1) * a.k]]
+    else:
+        allb = make_batches(np.arange(n), 512, 0, 0)[:a.k * grid.rows]
+        s = Ladies15D(dg, grid, (512,) * 3, 512)
+        mine = [np.sort(np.asarray(x)) for x in allb[s.i * a.k:(s.i + 1) * a.k]]
     for _ in range(3):
         s.sample(mine, 0, s.i * a.k, 0)
     torch.cuda.synchronize()
