@@ -1050,7 +1050,7 @@ static int dedup_prepare(const Graph* g, SageWs& ws, const int64_t* R_ptr, const
   k_dd_items<<<grid_for(dcap, 256, gw), 256, 0, st>>>(ws.d_nw + 1, ws.dv, ws.ddeg, g->rowptr, ws.roff,
                                                       ws.ioff, dd_items(s), ws.items);
   GB_LAUNCH_CHECK("dedup prepare");
-  count_launches(6);
+  count_launches(5);  // 3d, list, rcount, rows, items (scans count themselves)
   return GB_OK;
 }
 
