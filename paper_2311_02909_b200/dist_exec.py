@@ -125,6 +125,22 @@ class Sage15D:
         self.row_ranks = grid.row_group(self.i)
         self.dev = torch.device("cuda", torch.cuda.current_device())
         self.stats = {"fetch_ids": 0, "fetch_words": 0, "reduce_words": 0}
+        # per-phase wall time (ms, host clock around device-synchronised
+        # phases) when profile is set: the α–β cost-model check
+        self.profile = False
+        self.phase_ms = {"fetch": 0.0, "reduce": 0.0}
+
+    def _phase(self, name, t0):
+        import time
+
+        torch = _torch()
+        if not self.profile:
+            return time.perf_counter()
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        if name:
+            self.phase_ms[name] += 1e3 * (t1 - t0)
+        return t1
 
     # -- step 1: sparsity-aware row fetch ------------------------------------------
     def fetch_rows(self, U):
@@ -280,7 +296,9 @@ class Sage15D:
                                   epoch, l + 1, fcol)
             else:
                 U = torch.unique(rv[mine])
+                t0 = self._phase(None, 0.0)
                 lrowptr, lcol = self.fetch_rows(U)
+                self._phase("fetch", t0)
                 lrow = torch.searchsorted(U, rv).to(torch.int32)
                 deg_mine = torch.where(mine, deg, torch.zeros_like(deg)).contiguous()
                 ws = torch.empty(max(L.gb_sage_layer_sample_workspace(max(R, 1), max(R, 1) * s),
@@ -294,8 +312,10 @@ class Sage15D:
                         _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "gb_sage_layer_sample")
             # step 2: sample-then-reduce inside the grid row
             if self.grid.c > 1 and F:
+                t0 = self._phase(None, 0.0)
                 dist.all_reduce(fcol[:F], op=dist.ReduceOp.SUM,
                                 group=self.row_groups[self.i])
+                self._phase("reduce", t0)
                 self.stats["reduce_words"] += F
                 if self.ledger is not None:
                     self.ledger.charge(self.rank, "all-reduce", 1, F)
