@@ -327,6 +327,9 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
   int64_t* s_ra = (int64_t*)(s_h + kBins);           // row start, kLRowsSmem
   int32_t* s_rl = (int32_t*)(s_ra + kLRowsSmem);     // row length
   int32_t* s_rc = s_rl + kLRowsSmem;                 // row cursor (relative)
+  int32_t* s_nv = s_rc + kLRowsSmem;                 // column at the cursor (INT32_MAX: done)
+  int16_t* s_act = (int16_t*)(s_nv + kLRowsSmem);    // rows with entries in the tile
+  __shared__ int s_nact;
   __shared__ int32_t s_wcnt[kLTileThreads / 32 + 1];
   __shared__ uint32_t s_stage[kLTileThreads / 32 * 64];
   __shared__ int64_t s_ticket;
@@ -336,6 +339,7 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
   const int64_t ntiles = *A.ntiles;
   const int64_t nruns = (ntiles + kLTileRun - 1) / kLTileRun;
   const int64_t nt = A.gn * nruns;
+  for (int w = threadIdx.x; w < kLTileW / 2; w += blockDim.x) s_cnt[w] = 0;
   for (;;) {
     if (threadIdx.x == 0) {
       s_ticket = (int64_t)atomicAdd(A.ticket, 1ull);
@@ -361,16 +365,28 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
           s_ra[q - q0] = a;
           s_rl[q - q0] = (int32_t)(b - a);
           s_rc[q - q0] = (int32_t)(e0 - a);
+          s_nv[q - q0] = e0 < b ? __ldg(A.col + e0) : 0x7fffffff;
         }
       }
     }
     for (int64_t t = t0; t < t1; ++t) {
       const int32_t v0 = A.tb[t], v1 = A.tb[t + 1];
       const int nw2 = (v1 - v0 + 1) >> 1;
-      for (int w = threadIdx.x; w < nw2; w += blockDim.x) s_cnt[w] = 0;
+      // counters are zero here: cleared once at start, then by the compaction
+      if (threadIdx.x == 0) s_nact = 0;
       __syncthreads();
+      // rows whose next column falls in this tile (cursor mode): tiles a
+      // row has no entries in cost one shared-memory read
+      int nact = (int)(q1 - q0);
+      if (cur) {
+        for (int r = threadIdx.x; r < q1 - q0; r += blockDim.x)
+          if (s_nv[r] < v1) s_act[atomicAdd(&s_nact, 1)] = (int16_t)r;
+        __syncthreads();
+        nact = s_nact;
+      }
       // ---- e_v for v in [v0, v1)
-      for (int64_t q = q0 + warp; q < q1; q += nwarps) {
+      for (int ai = warp; ai < nact; ai += nwarps) {
+        const int64_t q = q0 + (cur ? (int64_t)s_act[ai] : (int64_t)ai);
         int64_t a, b, e0;
         if (cur) {
           a = s_ra[q - q0];
@@ -398,8 +414,12 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
             if (in) atomicAdd(s_cnt + ((c - v0) >> 1), 1u << (((c - v0) & 1) << 4));
             const unsigned out = __ballot_sync(FULL, !in);
             if (out) {
-              if (cur && lane == 0)
-                s_rc[q - q0] = (int32_t)(e + 32 * u - lane - a + __ffs(out) - 1);
+              const int src = __ffs(out) - 1;
+              const int32_t nv = __shfl_sync(FULL, c, src);  // next column (or INT32_MAX)
+              if (cur && lane == 0) {
+                s_rc[q - q0] = (int32_t)(e + 32 * u - lane - a + src);
+                s_nv[q - q0] = nv;
+              }
               done = true;
             }
           }
@@ -430,6 +450,7 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
       for (int w0 = wa; w0 < wb; w0 += 32) {
         const int w = w0 + lane;
         const uint32_t x = w < wb ? s_cnt[w] : 0u;
+        if (x) s_cnt[w] = 0;  // ready for the next tile
         const int m = ((x & 0xffffu) != 0) + ((x >> 16) != 0);
         int inc = m;
 #pragma unroll
@@ -1055,7 +1076,7 @@ struct LadiesPlan {
   int64_t n;
 };
 
-constexpr int64_t kTiledGroupBytes = 2ll << 30;  // P layout (v, key, candidate) of one group
+constexpr int64_t kTiledGroupBytes = 16ll << 30;  // P layout (v, key, candidate) of one group
 
 static LadiesPlan ladies_plan(int64_t k, int64_t n, int64_t q1_cap, int32_t layers,
                               const int64_t* fanouts, int32_t mode) {
@@ -1157,7 +1178,8 @@ int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t*
   count_launches(2);
   int tile_grid = 0;
   const size_t tile_smem = sizeof(uint32_t) * (kLTileW / 2 + kBins) +
-                           (sizeof(int64_t) + 2 * sizeof(int32_t)) * kLRowsSmem;
+                           (sizeof(int64_t) + 3 * sizeof(int32_t) + sizeof(int16_t)) *
+                               kLRowsSmem;
   if (P.tiled) {
     // column tiles of this graph: cuts every kLTileW columns and at
     // kLMassTiles quantiles of the degree mass
