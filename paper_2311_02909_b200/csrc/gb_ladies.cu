@@ -316,6 +316,7 @@ struct LadTileArgs {
 constexpr int kLTileRun = 8;      // consecutive tiles per ticket (row cursors carried over)
 constexpr int kLRowsSmem = 1024;  // rows whose cursors fit in shared memory
 constexpr int kLUnroll = 4;       // 32-entry loads in flight per row
+constexpr int kLList = 2048;      // touched offsets remembered per tile (sparse compaction)
 
 // One ticket = batch j and a run of kLTileRun consecutive column tiles.  Per
 // tile: counts in shared memory (warp per A row, from the row's cursor, which
@@ -329,7 +330,8 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
   int32_t* s_rc = s_rl + kLRowsSmem;                 // row cursor (relative)
   int32_t* s_nv = s_rc + kLRowsSmem;                 // column at the cursor (INT32_MAX: done)
   int16_t* s_act = (int16_t*)(s_nv + kLRowsSmem);    // rows with entries in the tile
-  __shared__ int s_nact;
+  __shared__ int s_nact, s_lcnt, s_emit;
+  __shared__ uint16_t s_list[kLList];               // column offsets touched (sparse tiles)
   __shared__ int32_t s_wcnt[kLTileThreads / 32 + 1];
   __shared__ uint32_t s_stage[kLTileThreads / 32 * 64];
   __shared__ int64_t s_ticket;
@@ -373,7 +375,11 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
       const int32_t v0 = A.tb[t], v1 = A.tb[t + 1];
       const int nw2 = (v1 - v0 + 1) >> 1;
       // counters are zero here: cleared once at start, then by the compaction
-      if (threadIdx.x == 0) s_nact = 0;
+      if (threadIdx.x == 0) {
+        s_nact = 0;
+        s_lcnt = 0;
+        s_emit = 0;
+      }
       __syncthreads();
       // rows whose next column falls in this tile (cursor mode): tiles a
       // row has no entries in cost one shared-memory read
@@ -413,6 +419,16 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
             const bool in = c < v1;
             if (in) atomicAdd(s_cnt + ((c - v0) >> 1), 1u << (((c - v0) & 1) << 4));
             const unsigned out = __ballot_sync(FULL, !in);
+            // sparse tiles: remember the touched offsets while they fit (a
+            // count past kLList, even by skipped appends, marks the tile dense)
+            const int lc = __shfl_sync(FULL, s_lcnt, 0);
+            if (lc <= kLList && ~out) {
+              const unsigned m = ~out;
+              int lb = 0;
+              if (lane == 0) lb = atomicAdd(&s_lcnt, __popc(m));
+              lb = __shfl_sync(FULL, lb, 0) + __popc(m & ((1u << lane) - 1u));
+              if (in && lb < kLList) s_list[lb] = (uint16_t)(c - v0);
+            }
             if (out) {
               const int src = __ffs(out) - 1;
               const int32_t nv = __shfl_sync(FULL, c, src);  // next column (or INT32_MAX)
@@ -426,6 +442,28 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
         }
       }
       __syncthreads();
+      const int64_t slot = j * A.n + v0;
+      int total = 0;
+      const int lcnt = s_lcnt;
+      if (lcnt <= kLList) {
+        // ---- sparse compaction: each touched counter read-and-cleared once
+        for (int i = threadIdx.x; i < lcnt; i += blockDim.x) {
+          const int off = s_list[i];
+          const int sh = (off & 1) << 4;
+          const uint32_t old = atomicAnd(s_cnt + (off >> 1), ~(0xffffu << sh));
+          const uint32_t e = (old >> sh) & 0xffffu;
+          if (e) {
+            const int pos = atomicAdd(&s_emit, 1);
+            const int32_t v = v0 + off;
+            const uint32_t key = A.rk(j, v, e);
+            A.pv[slot + pos] = v;
+            A.keys[slot + pos] = key;
+            atomicAdd(s_h + (key >> 20), 1u);
+          }
+        }
+        __syncthreads();
+        total = s_emit;
+      } else {
       // ---- compaction: warp w owns words [w * chunk, ...), counted then written
       const int chunk = (nw2 + nwarps - 1) / nwarps;
       const int wa = warp * chunk, wb = min(wa + chunk, nw2);
@@ -437,13 +475,12 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
       c = warp_sum(c);
       if (lane == 0) s_wcnt[warp] = c;
       __syncthreads();
-      int base = 0, total = 0;
+      int base = 0;
       for (int w = 0; w < nwarps; ++w) {
         const int x = s_wcnt[w];
         base += w < warp ? x : 0;
         total += x;
       }
-      const int64_t slot = j * A.n + v0;
       // nonzeros of 32 words -> the warp's staging buffer (<= 64), then the
       // keys with all lanes busy and coalesced slot writes
       uint32_t* stg = s_stage + warp * 64;
@@ -476,6 +513,7 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
         }
         __syncwarp();
         base += cnt;
+      }
       }
       if (threadIdx.x == 0) {
         A.tcnt[j * ntiles + t] = total;
@@ -753,7 +791,9 @@ __global__ void __launch_bounds__(1024) k_lad_refine(LadiesSampleArgs A,
     const int base = A.nsel[i];
     for (int a = threadIdx.x; a < mt; a += blockDim.x) {
       int rank = 0;
-      for (int b2 = 0; b2 < mt; ++b2) rank += ties[b2] < ties[a] ? 1 : 0;
+      // ties by vertex (slot order need not follow v)
+      const int32_t va = A.pv[ties[a]];
+      for (int b2 = 0; b2 < mt; ++b2) rank += A.pv[ties[b2]] < va ? 1 : 0;
       if (rank < need) A.sel[i * A.s + base + rank] = ties[a];
     }
     __syncthreads();
@@ -772,9 +812,10 @@ __global__ void __launch_bounds__(256) k_lad_emit(LadiesSampleArgs A, int32_t* _
     const int32_t* si = A.sel + i * A.s;
     for (int64_t a = threadIdx.x; a < take; a += blockDim.x) {
       const int32_t x = si[a];
-      int64_t rank = 0;
-      for (int64_t b = 0; b < take; ++b) rank += si[b] < x ? 1 : 0;
-      Sfix[i * A.s + rank] = A.pv[x];  // P positions ascend with v inside a batch
+      const int32_t vx = A.pv[x];
+      int64_t rank = 0;  // by vertex: slot order need not follow v
+      for (int64_t b = 0; b < take; ++b) rank += A.pv[si[b]] < vx ? 1 : 0;
+      Sfix[i * A.s + rank] = vx;
       if (Kfix) Kfix[i * A.s + rank] = A.keys[x];
     }
   }
