@@ -55,8 +55,9 @@ def parse():
     p.add_argument("--dist", default="replicated", choices=["replicated", "15d"],
                    help="multi-GPU mode: replicated graph (cfg4) or 1.5D partitioned (cfg5)")
     p.add_argument("--c", type=int, default=2, help="1.5D replication factor")
-    p.add_argument("--fetch", default="owner", choices=["rows", "owner"],
-                   help="1.5D SAGE: Alg. 2 row fetch, or owner-computes (ship row keys)")
+    p.add_argument("--fetch", default="p2p", choices=["rows", "owner", "p2p"],
+                   help="1.5D SAGE: Alg. 2 row fetch, owner-computes over NCCL (ship row "
+                        "keys), or owner sampling over peer memory (fused, default)")
     return p.parse_args()
 
 

@@ -248,6 +248,25 @@ int gb_its_rows(int64_t m, const int64_t* d_ptr, const double* d_val, int32_t s,
                 uint64_t depth, double* d_w, double* d_cdf, int32_t* d_picks, int32_t* d_take,
                 int32_t* d_err, void* stream);
 
+/* Owner sampling over peer memory (1.5D SAGE, fused exchange): for each of
+ * ngroups requesting grid rows g, read its frontier rows h_rows[g] (R =
+ * h_brow[g][k]), batch offsets h_brow[g] (k+1) and frontier offsets
+ * h_fptr[g] directly from that rank's memory (P2P), keep the rows whose
+ * vertex is in [lo, hi) (this rank's block, CSR d_brp / d_bcol over the
+ * block's rows), sample them with keys (h_boff[g] + batch) * stride + row,
+ * and store the picks into h_dst[g * ndst + m] + fptr (the frontiers of the
+ * grid row's ndst replicas, P2P).  Replaces the request / reply messages of
+ * the owner-computes variant and the grid-row all-reduce (dist.py:349-378,
+ * 469-484).  Host arrays of device pointers; caller brackets the call with
+ * device barriers over the participating ranks. */
+size_t gb_sage_owner_p2p_workspace(int64_t r_cap);
+int gb_sage_owner_p2p(const gb_graph* tables, int64_t ngroups, const int32_t* const* h_rows,
+                      const int64_t* const* h_brow, const int64_t* const* h_fptr,
+                      const int64_t* h_boff, int64_t k, int64_t r_cap, int32_t ndst,
+                      int32_t* const* h_dst, int64_t lo, int64_t hi, const int64_t* d_brp,
+                      const int32_t* d_bcol, int32_t s, int64_t stride, uint64_t seed,
+                      uint64_t epoch, uint64_t depth, void* d_ws, size_t ws_bytes, void* stream);
+
 /* ------------------------------------ LADIES per-layer pieces (1.5D mode)
  *   gb_ladies_counts       partial P = Q A over the rows with d_qdeg[q] > 0
  *                          through a local CSR addressed by d_qcol[q]: per

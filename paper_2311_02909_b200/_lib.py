@@ -86,6 +86,10 @@ SIGNATURES = {
     "gb_spmm_rows": (ctypes.c_int, [_i64, _p, _p, _p, _p, _i64, _p, _i64, _p, _p]),
     "gb_first_occurrence": (ctypes.c_int, [_i64, _p, _p, _p, _i64, _i64, _p, _p]),
     "gb_segment_copy": (ctypes.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p]),
+    "gb_sage_owner_p2p_workspace": (ctypes.c_size_t, [_i64]),
+    "gb_sage_owner_p2p": (ctypes.c_int, [_p, _i64, _p, _p, _p, _p, _i64, _i64, _i32, _p, _i64,
+                                         _i64, _p, _p, _i32, _i64, _u64, _u64, _u64, _p,
+                                         ctypes.c_size_t, _p]),
     "gb_scan_workspace_bytes": (ctypes.c_size_t, [_i64]),
     "gb_spgemm_bound": (ctypes.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p]),
     "gb_spgemm": (ctypes.c_int, [_i64, _p, _p, _p, _p, _p, _p, _p, _p, _i64, _p, _p, _p, _p, _p,

@@ -287,6 +287,24 @@ int gb_spmm_rows(int64_t R, const int64_t* d_rowptr, const int32_t* d_col,
   return spmm_rows(R, d_rowptr, d_col, d_row_batch, d_shift, k, d_X, f, d_Y, (cudaStream_t)stream);
 }
 
+size_t gb_sage_owner_p2p_workspace(int64_t r_cap) { return sage_owner_p2p_ws(r_cap); }
+
+int gb_sage_owner_p2p(const gb_graph* tables, int64_t ngroups, const int32_t* const* h_rows,
+                      const int64_t* const* h_brow, const int64_t* const* h_fptr,
+                      const int64_t* h_boff, int64_t k, int64_t r_cap, int32_t ndst,
+                      int32_t* const* h_dst, int64_t lo, int64_t hi, const int64_t* d_brp,
+                      const int32_t* d_bcol, int32_t s, int64_t stride, uint64_t seed,
+                      uint64_t epoch, uint64_t depth, void* d_ws, size_t ws_bytes, void* stream) {
+  if (!tables || ngroups < 0 || k < 1 || r_cap < 0 || lo < 0 || hi < lo || s < 1 || s > 32 ||
+      (ngroups && (!h_rows || !h_brow || !h_fptr || !h_boff || !h_dst))) {
+    set_error("owner p2p: bad arguments");
+    return GB_ERR_CONTRACT;
+  }
+  return sage_owner_p2p(tables, ngroups, h_rows, h_brow, h_fptr, h_boff, k, r_cap, ndst, h_dst, lo,
+                        hi, d_brp, d_bcol, s, stride, seed, epoch, depth, d_ws, ws_bytes,
+                        (cudaStream_t)stream);
+}
+
 int gb_segment_copy(int64_t m, const int64_t* d_rows, const int64_t* d_src_off,
                     const int32_t* d_lens, const int32_t* d_src, const int64_t* d_dst_off,
                     int32_t* d_dst, void* stream) {

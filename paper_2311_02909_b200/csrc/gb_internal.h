@@ -48,6 +48,13 @@ int spmm_rows(int64_t R, const int64_t* rowptr, const int32_t* col, const int64_
               cudaStream_t st);
 int segment_copy(int64_t m, const int64_t* rows, const int64_t* src_off, const int32_t* lens,
                  const int32_t* src, const int64_t* dst_off, int32_t* dst, cudaStream_t st);
+size_t sage_owner_p2p_ws(int64_t r_cap);
+int sage_owner_p2p(const Graph* tables, int64_t ngroups, const int32_t* const* rows,
+                   const int64_t* const* brow, const int64_t* const* fptr, const int64_t* boff,
+                   int64_t k, int64_t r_cap, int32_t ndst, int32_t* const* dst, int64_t lo,
+                   int64_t hi, const int64_t* brp, const int32_t* bcol, int32_t s, int64_t stride,
+                   uint64_t seed, uint64_t epoch, uint64_t depth, void* d_ws, size_t ws_bytes,
+                   cudaStream_t st);
 int first_occurrence(int64_t F, const int32_t* colidx, const int64_t* eb, const int64_t* shift,
                      int64_t k, int64_t ncols, int32_t* first, cudaStream_t st);
 int sage_workspace(const Graph* g, int64_t k, int64_t r1_cap, int32_t layers,

@@ -191,6 +191,9 @@ struct SageArgs {
   const int64_t* D_ptr;
   const int64_t* roff;
   const int4* rrec;
+  // P-free (OUT 1) extra destinations: peer frontiers written over NVLink
+  int32_t* dst[8];
+  int ndst;
 };
 
 __device__ __forceinline__ int32_t vrank(const uint32_t* vbits, const int32_t* vpre, int32_t v) {
@@ -356,9 +359,17 @@ __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
 #pragma unroll
       for (int z = 0; z < MAXF; ++z)
         if (z < take) cv[z] = __ldg(A.col + rs + sorted[z]);
+      if (A.fcol) {
 #pragma unroll
-      for (int z = 0; z < MAXF; ++z)
-        if (z < take) A.fcol[fp + z] = cv[z];
+        for (int z = 0; z < MAXF; ++z)
+          if (z < take) A.fcol[fp + z] = cv[z];
+      }
+      for (int m = 0; m < A.ndst; ++m) {
+        int32_t* d = A.dst[m] + fp;
+#pragma unroll
+        for (int z = 0; z < MAXF; ++z)
+          if (z < take) d[z] = cv[z];
+      }
       if (A.bitmap) {
         uint32_t* bm = A.bitmap + bb * A.nwords;
 #pragma unroll
@@ -1357,6 +1368,97 @@ int sage_sample_keyed(const Graph* tables, int64_t R, const int64_t* d_R, const 
   launch_pick<1>(grid_for(R, kPickThreads, 64 * kNumSMs), A, d_R, st);
   GB_LAUNCH_CHECK("sage_sample_keyed");
   count_launches(1);
+  return GB_OK;
+}
+
+// ------------------------------------------ owner sampling over peer memory
+// 1.5D owner-computes with the exchange fused into the kernels: the owner of
+// a block reads the requesting grid row's frontier, batch offsets and
+// frontier offsets straight from that rank's memory (P2P loads over NVLink),
+// keeps the rows whose vertex lies in its block, samples them from its local
+// block with the requester's keys, and stores the picks into the frontier of
+// every replica of that grid row (P2P stores) — no request / reply messages
+// and no all-reduce.  Caller brackets it with device barriers.
+
+// rows of a requester whose vertex lies in [lo, hi): block-local row,
+// degree, global row key and frontier offset (order arbitrary)
+__global__ void k_p2p_rows(const int32_t* __restrict__ rows, const int64_t* __restrict__ brow,
+                           const int64_t* __restrict__ fptr, int64_t k, int64_t boff,
+                           int64_t stride, int64_t lo, int64_t hi,
+                           const int64_t* __restrict__ brp, int32_t* __restrict__ lrow,
+                           int32_t* __restrict__ ldeg, int64_t* __restrict__ lkey,
+                           int64_t* __restrict__ lpos, int64_t* __restrict__ count) {
+  __shared__ int64_t s_brow[kBrowSmem];
+  if (k + 1 <= kBrowSmem)
+    for (int64_t i = threadIdx.x; i <= k; i += blockDim.x) s_brow[i] = brow[i];
+  __syncthreads();
+  const int64_t R = brow[k];
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = rows[r];
+    if (v < lo || v >= hi) continue;
+    const int64_t lr = v - lo;
+    const int32_t d = (int32_t)(brp[lr + 1] - brp[lr]);
+    if (d == 0) continue;
+    const int64_t b = batch_of(s_brow, brow, k, r);
+    const int64_t b0 = k + 1 <= kBrowSmem ? s_brow[b] : brow[b];
+    const unsigned peers = __activemask();
+    const int lane = lane_id(), leader = __ffs(peers) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd((unsigned long long*)count, (unsigned long long)__popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    const int64_t o = (int64_t)base + __popc(peers & ((1u << lane) - 1u));
+    lrow[o] = (int32_t)lr;
+    ldeg[o] = d;
+    lkey[o] = (boff + b) * stride + (r - b0);
+    lpos[o] = fptr[r];
+  }
+}
+
+size_t sage_owner_p2p_ws(int64_t r_cap) {
+  return 2 * align_up(sizeof(int32_t) * (r_cap + 1)) + 2 * align_up(sizeof(int64_t) * (r_cap + 1)) +
+         align_up(sizeof(int64_t) * 2);
+}
+
+int sage_owner_p2p(const Graph* tables, int64_t ngroups, const int32_t* const* rows,
+                   const int64_t* const* brow, const int64_t* const* fptr, const int64_t* boff,
+                   int64_t k, int64_t r_cap, int32_t ndst, int32_t* const* dst, int64_t lo,
+                   int64_t hi, const int64_t* brp, const int32_t* bcol, int32_t s, int64_t stride,
+                   uint64_t seed, uint64_t epoch, uint64_t depth, void* d_ws, size_t ws_bytes,
+                   cudaStream_t st) {
+  if (sage_owner_p2p_ws(r_cap) > ws_bytes) {
+    set_error("owner p2p workspace too small");
+    return GB_ERR_CAPACITY;
+  }
+  if (ndst < 1 || ndst > 8) {
+    set_error("owner p2p: 1..8 destination frontiers per grid row");
+    return GB_ERR_UNSUPPORTED;
+  }
+  char* p = (char*)d_ws;
+  auto carve = [&](size_t bytes) { char* r = p; p += align_up(bytes); return r; };
+  int32_t* lrow = (int32_t*)carve(sizeof(int32_t) * (r_cap + 1));
+  int32_t* ldeg = (int32_t*)carve(sizeof(int32_t) * (r_cap + 1));
+  int64_t* lkey = (int64_t*)carve(sizeof(int64_t) * (r_cap + 1));
+  int64_t* lpos = (int64_t*)carve(sizeof(int64_t) * (r_cap + 1));
+  int64_t* count = (int64_t*)carve(sizeof(int64_t) * 2);
+  for (int64_t g = 0; g < ngroups; ++g) {
+    GB_CUDA(cudaMemsetAsync(count, 0, sizeof(int64_t), st));
+    k_p2p_rows<<<grid_for(r_cap, 256, 16 * kNumSMs), 256, 0, st>>>(
+        rows[g], brow[g], fptr[g], k, boff[g], stride, lo, hi, brp, lrow, ldeg, lkey, lpos, count);
+    GB_LAUNCH_CHECK("k_p2p_rows");
+    SageArgs A{};
+    A.rowptr = brp; A.col = bcol;
+    A.deg_slot = tables->deg_slot; A.run_j0 = tables->run_j0; A.run_s0 = tables->run_s0;
+    A.run_d = tables->run_d; A.run_n = tables->run_n; A.run_lower = tables->run_lower;
+    A.rowv = lrow; A.rowkeys = lkey; A.deg = ldeg; A.fptr = lpos;
+    A.k = 0; A.s = s; A.seed = seed; A.epoch = epoch; A.depth = depth;
+    A.bitmap = nullptr; A.fcol = nullptr;
+    A.ndst = ndst;
+    for (int m = 0; m < ndst; ++m) A.dst[m] = dst[g * ndst + m];
+    launch_pick<1>(grid_for(r_cap, kPickThreads, 64 * kNumSMs), A, count, st);
+    GB_LAUNCH_CHECK("owner p2p pick");
+    count_launches(2);
+  }
   return GB_OK;
 }
 

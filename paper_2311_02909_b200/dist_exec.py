@@ -103,9 +103,12 @@ class Sage15D:
             raise ContractViolation("Sage15D needs torch.distributed with world_size == grid.p")
         self.grid, self.fanouts, self.b = grid, tuple(int(s) for s in fanouts), int(batch_size)
         self.mode, self.ledger = mode, ledger
-        if fetch not in ("rows", "owner"):
+        if fetch not in ("rows", "owner", "p2p"):
             raise ContractViolation(f"unknown fetch mode {fetch!r}")
-        self.fetch = fetch  # "rows": Alg. 2 row fetch; "owner": owner samples, returns picks
+        # "rows": Alg. 2 row fetch; "owner": owner samples, returns picks;
+        # "p2p": owner reads requests from and writes picks into peer memory
+        self.fetch = fetch
+        self._p2p = None
         self.rank = dist.get_rank()
         self.i, self.j = grid.coords(self.rank)
         self.n = full.n
@@ -259,9 +262,148 @@ class Sage15D:
                                              _lib.ptr(fptr), _lib.ptr(fcol), _lib.stream_ptr()),
                            "gb_segment_copy")
 
+    # -- owner sampling over peer memory ----------------------------------------------------
+    def _p2p_buffers(self, k):
+        """Symmetric-memory frontiers of every layer (same sizes on all ranks):
+        rows / batch offsets / frontier offsets / picks, rendezvoused once."""
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+
+        torch = _torch()
+        if self._p2p is not None and self._p2p["k"] == k:
+            return self._p2p
+        grp = dist.group.WORLD.group_name
+
+        def sym(numel, dtype):
+            t = symm_mem.empty(max(int(numel), 1), dtype=dtype, device=self.dev)
+            t.zero_()
+            return t, symm_mem.rendezvous(t, grp)
+
+        r = k * self.b
+        bufs = {"k": k, "layers": []}
+        rows, rows_h = sym(r + _lib.GB_COL_PAD, torch.int32)
+        brow, brow_h = sym(k + 1, torch.int64)
+        for s in self.fanouts:
+            fptr, fptr_h = sym(r + 1, torch.int64)
+            fcol, fcol_h = sym(r * s + _lib.GB_COL_PAD, torch.int32)
+            nbrow, nbrow_h = sym(k + 1, torch.int64)
+            bufs["layers"].append({"cap": r, "rows": rows, "rows_h": rows_h, "brow": brow,
+                                   "brow_h": brow_h, "fptr": fptr, "fptr_h": fptr_h,
+                                   "fcol": fcol, "fcol_h": fcol_h})
+            rows, rows_h, brow, brow_h = fcol, fcol_h, nbrow, nbrow_h
+            r *= s
+        bufs["barrier"] = bufs["layers"][0]["brow_h"]
+        L = _lib.lib()
+        bufs["ws"] = torch.empty(max(L.gb_sage_owner_p2p_workspace(r), 1), dtype=torch.uint8,
+                                 device=self.dev)
+        self._p2p = bufs
+        return bufs
+
+    def sample_p2p(self, group_batches, epoch, batch_offset, seed):
+        """1.5D SAGE with the owner exchange fused into the sampling kernels
+        (gb_sage_owner_p2p): per layer, publish rows / offsets, barrier, every
+        block owner samples the rows of its block for all grid rows of its
+        column straight out of their memory and stores the picks into every
+        replica's frontier, barrier, extraction.  No NCCL messages and no
+        host synchronisation inside the bulk."""
+        import ctypes
+
+        import torch.distributed as dist
+
+        torch = _torch()
+        L = _lib.lib()
+        grid, st, c = self.grid, self.grid.stages, self.grid.c
+        k = len(group_batches)
+        bufs = self._p2p_buffers(k)
+        off = np.zeros(k + 1, np.int64)
+        off[1:] = np.cumsum([len(x) for x in group_batches])
+        lay0 = bufs["layers"][0]
+        if off[-1] > lay0["cap"]:
+            raise ContractViolation("more batch vertices than the p2p buffers hold")
+        lay0["brow"][: k + 1].copy_(torch.as_tensor(off))
+        if off[-1]:
+            lay0["rows"][: int(off[-1])].copy_(torch.as_tensor(
+                np.concatenate(group_batches).astype(np.int32)))
+        # batch offsets of every rank (keys of the rows an owner samples) and
+        # the equal-group check the symmetric buffers rely on
+        boffs = torch.zeros(grid.p + 1, dtype=torch.int64, device=self.dev)
+        boffs[self.rank] = batch_offset
+        boffs[grid.p] = k
+        kmax = boffs[grid.p:].clone()
+        dist.all_reduce(boffs)
+        dist.all_reduce(kmax, op=dist.ReduceOp.MAX)
+        boffs, kmax = boffs.tolist(), int(kmax.item())
+        if boffs[grid.p] != k * grid.p or kmax != k:
+            raise ContractViolation("fetch='p2p' needs the same number of batches on every grid row")
+        owner = self.j * st <= self.i < (self.j + 1) * st
+        lo, hi = int(self.bounds[self.i]), int(self.bounds[self.i + 1])
+        req = [grid.rank(g, self.j) for g in range(grid.rows)]
+        P = ctypes.c_void_p
+        barrier = bufs["barrier"]
+        layers, stride = [], self.b
+        xws = torch.empty(max(L.gb_sage_layer_extract_workspace(self.n, k), 1), dtype=torch.uint8,
+                          device=self.dev)
+        ws_scan = None
+        for l, s in enumerate(self.fanouts):
+            if l:
+                stride *= self.fanouts[l - 1]
+            lay = bufs["layers"][l]
+            cap = lay["cap"]
+            deg = self.gdeg[lay["rows"][:cap].long()].contiguous()
+            if ws_scan is None or ws_scan.numel() * 8 < L.gb_scan_workspace_bytes(cap + 1):
+                ws_scan = torch.empty(max(L.gb_scan_workspace_bytes(cap + 1) // 8, 1),
+                                      dtype=torch.int64, device=self.dev)
+            _lib.check(L.gb_take_scan(cap, _lib.ptr(lay["brow"][k:]), _lib.ptr(deg), s,
+                                      _lib.ptr(lay["fptr"]), _lib.ptr(ws_scan),
+                                      _lib.stream_ptr()), "gb_take_scan")
+            barrier.barrier(channel=0)  # rows, offsets and frontier offsets published
+            if owner:
+                ng = len(req)
+                rows = (P * ng)(*[lay["rows_h"].buffer_ptrs[r] for r in req])
+                brow = (P * ng)(*[lay["brow_h"].buffer_ptrs[r] for r in req])
+                fptr = (P * ng)(*[lay["fptr_h"].buffer_ptrs[r] for r in req])
+                boff = (ctypes.c_int64 * ng)(*[boffs[r] for r in req])
+                dst = (P * (ng * c))(*[lay["fcol_h"].buffer_ptrs[grid.rank(g, m)]
+                                       for g in range(grid.rows) for m in range(c)])
+                ws = bufs["ws"]
+                _lib.check(L.gb_sage_owner_p2p(
+                    self.tables.handle, ng, rows, brow, fptr, boff, k, cap, c, dst, lo, hi,
+                    _lib.ptr(self.brp), _lib.ptr(self.bcol), s, stride, seed, epoch, l + 1,
+                    _lib.ptr(ws), ws.numel(), _lib.stream_ptr()), "gb_sage_owner_p2p")
+            barrier.barrier(channel=0)  # every pick stored
+            nxt = bufs["layers"][l + 1]["brow"] if l + 1 < len(self.fanouts) else \
+                torch.empty(k + 1, dtype=torch.int64, device=self.dev)
+            F_cap = cap * s
+            acol = torch.empty(F_cap, dtype=torch.int32, device=self.dev)
+            colv = torch.empty(F_cap, dtype=torch.int32, device=self.dev)
+            coloff = torch.empty(k + 1, dtype=torch.int64, device=self.dev)
+            sizes = torch.zeros(3, dtype=torch.int64, device=self.dev)
+            _lib.check(L.gb_sage_layer_extract(self.n, k, _lib.ptr(lay["brow"]),
+                                               _lib.ptr(lay["fptr"]), _lib.ptr(lay["fcol"]),
+                                               F_cap, _lib.ptr(acol), _lib.ptr(colv),
+                                               _lib.ptr(nxt), _lib.ptr(coloff), _lib.ptr(sizes),
+                                               _lib.ptr(xws), xws.numel(), _lib.stream_ptr()),
+                       "gb_sage_layer_extract")
+            layers.append((lay, acol, colv, coloff, nxt, sizes))
+        # one host read of the sizes for the reference-shaped views
+        sz = torch.stack([x[5] for x in layers]).cpu().numpy()
+        out = []
+        for (lay, acol, colv, coloff, nxt, _), (R, F, U) in zip(layers, sz):
+            R, F, U = int(R), int(F), int(U)
+            out.append({
+                "frontier_shape": (R, self.n), "frontier_ptr": lay["fptr"][: R + 1],
+                "frontier_col": lay["fcol"][:F], "adj_shape": (R, U),
+                "adj_ptr": lay["fptr"][: R + 1], "adj_col": acol[:F],
+                "rowv_off": lay["brow"][: k + 1], "rowv_cat": lay["rows"][:R],
+                "colv_off": coloff, "colv_cat": colv[:U], "sampv_off": nxt, "sampv_cat":
+                lay["fcol"][:F]})
+        return out
+
     # -- one bulk --------------------------------------------------------------------------
     def sample(self, group_batches, epoch, batch_offset, seed):
         """Sample this grid row's group; returns (device layer dicts, sizes)."""
+        if self.fetch == "p2p":
+            return self.sample_p2p(group_batches, epoch, batch_offset, seed)
         import torch.distributed as dist
 
         torch = _torch()

@@ -40,7 +40,8 @@ def main():
     grids = [(world, c) for c in (1, 2) if world % c == 0 and c * c <= world and world % (c * c) == 0]
     for p, c in grids:
         grid = ProcessGrid(p, c)
-        for mode, fetch in (("pfree", "rows"), ("stream", "rows"), ("pfree", "owner")):
+        for mode, fetch in (("pfree", "rows"), ("stream", "rows"), ("pfree", "owner"),
+                            ("pfree", "p2p")):
             led = CommLedger(p)
             s = Sage15D(dg, grid, cfg.fanouts, cfg.batch_size, mode=mode, ledger=led, fetch=fetch)
             ep = sage_epoch_15d(s, cfg, batches, epoch=1, batch_offset=5)
