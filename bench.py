@@ -618,6 +618,39 @@ def run_15d(args, rank, world, local_rank):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     T = float(t.item())
     value = k * grid.rows * args.steps / (T / 1e3)
+    # feature fetch of the bulk's deepest col_vertices (f = 128, fp32): the
+    # NCCL all-to-allv against the gather fused over peer memory
+    from paper_2311_02909_b200.dist_exec import (PeerFeatures, fetch_features_nccl,
+                                                 fetch_features_p2p)
+
+    lay = s.sample(mine, 0, i * k, 0)[-1]
+    verts = lay["colv_cat"].cpu().numpy()
+    rs = np.linspace(0, n, grid.rows + 1).astype(np.int64)
+    fdim = 128
+    Hb = torch.rand((int(rs[s.i + 1] - rs[s.i]), fdim), device="cuda")
+    peer = PeerFeatures(Hb, rs, grid)
+    ftimes = {}
+    for name, fn in (("nccl", lambda: fetch_features_nccl(verts, Hb, rs, grid,
+                                                           grid.col_group(s.j))),
+                     ("p2p", lambda: fetch_features_p2p(verts, peer))):
+        fn()
+        torch.cuda.synchronize()
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(5):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        tt = torch.tensor([a.elapsed_time(b) / 5], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ftimes[name] = float(tt.item())
+    fetch_line = {"rows": int(verts.size), "f": fdim, "dtype": "f32",
+                  "ms_nccl": ftimes["nccl"], "ms_p2p": ftimes["p2p"],
+                  "gb_s_p2p": verts.size * fdim * 4 / (ftimes["p2p"] / 1e3) / 1e9,
+                  "api": "dist_exec.fetch_features_p2p vs fetch_features_nccl"}
+    peer.handle.barrier(channel=0)
+    del peer, Hb
     # LADIES (b = s = 512, L = 3) on the same grid, race sampling
     from paper_2311_02909_b200.dist_exec import Ladies15D
     from paper_2311_02909_b200.pipeline import make_batches
@@ -654,6 +687,7 @@ def run_15d(args, rank, world, local_rank):
                        "parallelism": f"1.5D grid {grid.rows}x{grid.c} (p={world}, c={grid.c})",
                        "mode": m15, "fetch": args.fetch},
             "traffic_rank0": {k2: int(v) for k2, v in s.stats.items()},
+            "feature_fetch_rank0_group": fetch_line,
         }), flush=True)
 
 

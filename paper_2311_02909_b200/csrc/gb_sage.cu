@@ -1537,20 +1537,50 @@ int gather_rows(int64_t m, const int32_t* ids, int64_t row0, const int64_t* rowp
 }
 
 // dense feature rows: out[i, :] = H[ids[i] - row0, :] (fp32, f columns)
+// rows of H (fp32, f wide) for ids: a warp moves kGU rows per step with all
+// their loads issued first (16-B vectors when f % 4 == 0 and aligned), so a
+// remote (peer-memory) H keeps several NVLink requests in flight per warp
+constexpr int kGU = 4;
+template <bool V4>
 __global__ void k_gather_feat(int64_t m, const int32_t* __restrict__ ids, int64_t row0,
                               const float* __restrict__ H, int64_t f, float* __restrict__ out) {
   const int lane = lane_id();
-  for (int64_t i = global_warp(); i < m; i += grid_warps()) {
-    const float* src = H + (ids[i] - row0) * f;
-    float* dst = out + i * f;
-    for (int64_t x = lane; x < f; x += 32) dst[x] = src[x];
+  constexpr int W = V4 ? 128 : 32;
+  for (int64_t i0 = global_warp() * (int64_t)kGU; i0 < m; i0 += (int64_t)grid_warps() * kGU) {
+    int64_t src[kGU];
+#pragma unroll
+    for (int u = 0; u < kGU; ++u) src[u] = i0 + u < m ? ((int64_t)ids[i0 + u] - row0) * f : -1;
+    for (int64_t f0 = 0; f0 < f; f0 += W) {
+      const int64_t x = f0 + (V4 ? 4 * lane : lane);
+      float4 v[kGU];
+#pragma unroll
+      for (int u = 0; u < kGU; ++u) {
+        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (src[u] >= 0 && x < f) {
+          if (V4) v[u] = __ldg((const float4*)(H + src[u] + x));
+          else v[u].x = __ldg(H + src[u] + x);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kGU; ++u)
+        if (src[u] >= 0 && x < f) {
+          float* d = out + (i0 + u) * f + x;
+          if (V4) *(float4*)d = v[u];
+          else *d = v[u].x;
+        }
+    }
   }
 }
 
 int gather_features(int64_t m, const int32_t* ids, int64_t row0, const float* H, int64_t f,
                     float* out, cudaStream_t st) {
   if (m == 0) return GB_OK;
-  k_gather_feat<<<grid_for(m * 32, 256, 16 * kNumSMs), 256, 0, st>>>(m, ids, row0, H, f, out);
+  const bool v4 = f % 4 == 0 && (uintptr_t)H % 16 == 0 && (uintptr_t)out % 16 == 0;
+  const int grid = grid_for((m + kGU - 1) / kGU * 32, 256, 16 * kNumSMs);
+  if (v4)
+    k_gather_feat<true><<<grid, 256, 0, st>>>(m, ids, row0, H, f, out);
+  else
+    k_gather_feat<false><<<grid, 256, 0, st>>>(m, ids, row0, H, f, out);
   GB_LAUNCH_CHECK("k_gather_feat");
   count_launches(1);
   return GB_OK;

@@ -30,6 +30,8 @@ row keys), so the concatenation over grid rows equals the serial epoch.
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 
 from . import _lib
@@ -744,4 +746,58 @@ def fetch_features_nccl(vertices, H_block, row_starts, grid: ProcessGrid, group_
     for p, sel in slots.items():
         if sel.numel():
             out[sel] = got[p].view(-1, f)
+    return out
+
+
+class PeerFeatures:
+    """Feature block rows in symmetric memory: block i (rows row_starts[i] ..
+    row_starts[i+1]) on every rank of grid row i, padded to the largest block
+    so every rank allocates the same size (torch symmetric memory,
+    rendezvoused once over the world group)."""
+
+    def __init__(self, H_block, row_starts, grid: ProcessGrid):
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+
+        torch = _torch()
+        self.grid = grid
+        self.row_starts = np.asarray(row_starts, np.int64)
+        self.f = int(H_block.shape[1])
+        rows = int(np.max(np.diff(self.row_starts)))
+        self.buf = symm_mem.empty(max(rows, 1) * self.f, dtype=torch.float32,
+                                  device=H_block.device)
+        self.buf[: H_block.numel()].copy_(H_block.flatten())
+        self.handle = symm_mem.rendezvous(self.buf, dist.group.WORLD.group_name)
+        self.handle.barrier(channel=0)
+
+
+def fetch_features_p2p(vertices, peer: PeerFeatures):
+    """fetch_features (pipeline.py:78-120) with the all-to-allv fused into
+    the gather: the requester reads each feature row straight out of the
+    block owner's memory in its own grid column (P2P loads over NVLink,
+    gb_gather_features on the peer pointer) — no request / reply messages.
+    Returns rows in request order (duplicates per occurrence)."""
+    import torch.distributed as dist
+
+    torch = _torch()
+    grid, f = peer.grid, peer.f
+    me = dist.get_rank()
+    _, j = grid.coords(me)
+    dev = peer.buf.device
+    v = torch.as_tensor(np.asarray(vertices, np.int64)).to(dev)
+    rs = torch.as_tensor(peer.row_starts).to(dev)
+    owner_row = torch.searchsorted(rs, v, right=True) - 1
+    out = torch.empty((v.numel(), f), dtype=torch.float32, device=dev)
+    L = _lib.lib()
+    for r in range(grid.rows):
+        sel = torch.nonzero(owner_row == r).flatten()
+        if sel.numel() == 0:
+            continue
+        ids = v[sel].to(torch.int32).contiguous()
+        rows = torch.empty((ids.numel(), f), dtype=torch.float32, device=dev)
+        src = peer.handle.buffer_ptrs[grid.rank(r, j)]
+        _lib.check(L.gb_gather_features(ids.numel(), _lib.ptr(ids), int(peer.row_starts[r]),
+                                        ctypes.c_void_p(src), f, _lib.ptr(rows),
+                                        _lib.stream_ptr()), "gb_gather_features")
+        out[sel] = rows
     return out

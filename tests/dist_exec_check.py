@@ -27,7 +27,8 @@ def main():
     import paper_2311_02909_b200 as gb
     from paper_2311_02909_b200 import graphgen
     from paper_2311_02909_b200.dist import CommLedger, ProcessGrid, _bounds
-    from paper_2311_02909_b200.dist_exec import (Ladies15D, Sage15D, fetch_features_nccl,
+    from paper_2311_02909_b200.dist_exec import (Ladies15D, PeerFeatures, Sage15D,
+                                                 fetch_features_nccl, fetch_features_p2p,
                                                  ladies_epoch_15d, sage_epoch_15d)
 
     dg = graphgen.rmat_device_graph(1 << 14, 200_000, symmetric=True, seed=3)
@@ -72,6 +73,14 @@ def main():
         ok &= same
         if rank == 0:
             print(f"grid ({p},{c}) fetch_features: {'PASS' if same else 'FAIL'}", flush=True)
+        peer = PeerFeatures(Hb, rs, grid)
+        got = fetch_features_p2p(want, peer)
+        torch.cuda.synchronize()
+        same = bool(torch.equal(got, H[torch.as_tensor(want).cuda()]))
+        ok &= same
+        if rank == 0:
+            print(f"grid ({p},{c}) fetch_features p2p: {'PASS' if same else 'FAIL'}", flush=True)
+        peer.handle.barrier(channel=0)
     t = torch.tensor([1 if ok else 0], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MIN)
     if rank == 0:
