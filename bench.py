@@ -657,7 +657,7 @@ def run_15d(args, rank, world, local_rank):
 
     lb = make_batches(np.arange(n), 512, seed=0, epoch=0)[:k * grid.rows]
     lmine = [np.sort(np.asarray(x)) for x in lb[i * k:(i + 1) * k]]
-    ls = Ladies15D(dg, grid, (512,) * 3, 512)
+    ls = Ladies15D(dg, grid, (512,) * 3, 512, fetch="p2p" if args.fetch == "p2p" else "rows")
     for _ in range(2):
         ls.sample(lmine, 0, i * k, 0)
     lt = []

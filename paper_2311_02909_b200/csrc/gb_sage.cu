@@ -1522,7 +1522,15 @@ __global__ void k_gather_rows(int64_t m, const int32_t* __restrict__ ids, int64_
   for (int64_t i = global_warp(); i < m; i += grid_warps()) {
     const int64_t r = ids[i] - row0;
     const int64_t a = rowptr[r], d = rowptr[r + 1] - a, o = out_off[i];
-    for (int64_t x = lane; x < d; x += 32) out[o + x] = col[a + x];
+    // four loads in flight per lane (the block may live in a peer's memory)
+    for (int64_t x = lane; x < d; x += 128) {
+      int32_t v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = x + 32 * u < d ? col[a + x + 32 * u] : 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (x + 32 * u < d) out[o + x + 32 * u] = v[u];
+    }
   }
 }
 

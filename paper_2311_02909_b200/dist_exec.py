@@ -148,10 +148,66 @@ class Sage15D:
         return t1
 
     # -- step 1: sparsity-aware row fetch ------------------------------------------
+    def _peer_block(self):
+        """This rank's block CSR in symmetric memory (padded to the largest
+        block of any rank), so requesters read rows straight out of it."""
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+
+        torch = _torch()
+        if getattr(self, "_pblk", None) is not None:
+            return self._pblk
+        sz = torch.tensor([self.brp.numel(), self.bcol.numel()], dtype=torch.int64,
+                          device=self.dev)
+        dist.all_reduce(sz, op=dist.ReduceOp.MAX)
+        nr, nc = (int(x) for x in sz.tolist())
+        grp = dist.group.WORLD.group_name
+        rp = symm_mem.empty(max(nr, 1), dtype=torch.int64, device=self.dev)
+        cl = symm_mem.empty(max(nc, 1) + _lib.GB_COL_PAD, dtype=torch.int32, device=self.dev)
+        rp[: self.brp.numel()].copy_(self.brp)
+        cl[: self.bcol.numel()].copy_(self.bcol)
+        self._pblk = {"rp": rp, "rp_h": symm_mem.rendezvous(rp, grp), "cl": cl,
+                      "cl_h": symm_mem.rendezvous(cl, grp)}
+        self._pblk["rp_h"].barrier(channel=0)
+        return self._pblk
+
+    def fetch_rows_p2p(self, U):
+        """fetch_rows with the messages replaced by peer reads: the A rows of
+        U are gathered straight from each block owner's CSR in symmetric
+        memory (gb_gather_rows on the peer pointers).  Same local CSR."""
+        torch = _torch()
+        L = _lib.lib()
+        pb = self._peer_block()
+        grid, st = self.grid, self.grid.stages
+        d = self.gdeg[U.long()].long()
+        lrowptr = torch.zeros(U.numel() + 1, dtype=torch.int64, device=self.dev)
+        lrowptr[1:] = torch.cumsum(d, 0)
+        nnz = int(lrowptr[-1].item())
+        lcol = torch.zeros(nnz + _lib.GB_COL_PAD, dtype=torch.int32, device=self.dev)
+        for q in range(st):
+            kblk = self.j * st + q
+            owner = grid.rank(kblk, self.j)
+            lo, hi = int(self.bounds[kblk]), int(self.bounds[kblk + 1])
+            sel = torch.nonzero((U >= lo) & (U < hi)).flatten()
+            if sel.numel() == 0:
+                continue
+            ids = U[sel].to(torch.int32).contiguous()
+            offs = lrowptr[sel].contiguous()
+            _lib.check(L.gb_gather_rows(ids.numel(), _lib.ptr(ids), lo,
+                                        ctypes.c_void_p(pb["rp_h"].buffer_ptrs[owner]),
+                                        ctypes.c_void_p(pb["cl_h"].buffer_ptrs[owner]),
+                                        _lib.ptr(offs), _lib.ptr(lcol), _lib.stream_ptr()),
+                       "gb_gather_rows")
+            if owner != self.rank:
+                self.stats["fetch_ids"] += ids.numel()
+        return lrowptr, lcol
+
     def fetch_rows(self, U):
         """A rows of the sorted distinct vertices U (all in this column's
         range) as a local CSR (rowptr over U, cols)."""
         torch = _torch()
+        if self.fetch == "p2p":
+            return self.fetch_rows_p2p(U)
         grid, st, L = self.grid, self.grid.stages, _lib.lib()
         replies = []
         for q in range(st):

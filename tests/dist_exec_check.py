@@ -54,13 +54,14 @@ def main():
         # LADIES (race) on the grid == single-GPU race sampler
         lcfg = gb.SamplerConfig.ladies(3, 64, 48, bulk_count=8, seed=4)
         lser = gb.sample_epoch_bulk(G, lcfg, batches, epoch=1, batch_offset=5, mode="race")
-        ls = Ladies15D(dg, grid, lcfg.fanouts, lcfg.batch_size)
-        lep = ladies_epoch_15d(ls, lcfg, batches, epoch=1, batch_offset=5)
-        same = lser.equals(lep)
-        ok &= same
-        if rank == 0:
-            print(f"grid ({p},{c}) ladies race: {'PASS' if same else 'FAIL'} stats={ls.stats}",
-                  flush=True)
+        for lf in ("rows", "p2p"):
+            ls = Ladies15D(dg, grid, lcfg.fanouts, lcfg.batch_size, fetch=lf)
+            lep = ladies_epoch_15d(ls, lcfg, batches, epoch=1, batch_offset=5)
+            same = lser.equals(lep)
+            ok &= same
+            if rank == 0:
+                print(f"grid ({p},{c}) ladies race/{lf}: {'PASS' if same else 'FAIL'} "
+                      f"stats={ls.stats}", flush=True)
         # features: replicas of the block rows in every grid column
         f = 16
         H = torch.arange(dg.n * f, dtype=torch.float32, device="cuda").view(dg.n, f)
