@@ -180,7 +180,9 @@ int gb_segment_copy(int64_t m, const int64_t* d_rows, const int64_t* d_src_off,
  *                 (== col_vertices == sampled_vertices == next layer's Q)
  *   aptr  [Q+1], acol [nnz]  A_S (one row per Q nonzero, ladies_assemble)
  *   coloff[k+1]   column offset of each batch's block (all 0 = shared layout)
- * d_sizes[5*l + {0,1,2,3,4}] = (A_S rows, F, A_S nnz, A_S cols, nnz(P)).
+ * d_sizes[5*l + {0,1,2,3,4}] = (A_S rows, F, A_S nnz, A_S cols, nnz(P)); a
+ * negative last entry reports a capacity overflow inside the bulk (-1: race
+ * tie list of more than 2048 equal keys).
  * mode GB_LADIES_EXACT replays its_sample_row bit for bit (sequential fp64
  * cumsum, small graphs); GB_LADIES_RACE draws the same law by an
  * exponential race (Gumbel top-s) for production sizes, counting P by

@@ -1065,6 +1065,10 @@ __global__ void k_lad_sizes(const int64_t* __restrict__ qoff, int64_t k,
 
 __global__ void k_lad_set(int64_t* p, int64_t v) { *p = v; }
 
+__global__ void k_lad_flag(const int32_t* __restrict__ overflow, int64_t* __restrict__ size) {
+  if (*overflow) *size = -(int64_t)*overflow;
+}
+
 // ============================================================== host side
 
 static int gcap(int64_t n, int threads, int cap) {
@@ -1353,6 +1357,10 @@ int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t*
     count_launches(5);
     qc = k * s;
   }
+  // capacity overflow anywhere in the bulk (race tie list): the last layer's
+  // nnz(P) size becomes -flag for the caller
+  k_lad_flag<<<1, 1, 0, st>>>(ws.overflow, d_sizes + kLadiesSizes * (layers - 1) + 4);
+  count_launches(1);
   return GB_OK;
 }
 

@@ -182,6 +182,9 @@ class LadiesBulk:
     def layers(self, d_qoff, d_qverts, sizes=None):
         if sizes is None:
             sizes = self.sizes.cpu().numpy()
+        if len(sizes) and sizes[-1] < 0:
+            raise RuntimeError(f"LADIES bulk capacity overflow (code {-int(sizes[-1])}: "
+                               "race tie list)")
         n = self.dg.n
         out = []
         qoff, qcol = d_qoff, d_qverts
