@@ -41,7 +41,7 @@ BATCH = 1024
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--steps", type=int, default=100)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--workload", default="products", choices=["products", "cfg1", "papers"])
@@ -84,6 +84,17 @@ class ClockSampler:
                  "-lms", "100"], stdout=self.fh, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+            return
+        # nvidia-smi takes a while to come up: start timing only once it
+        # writes, so the timed region is covered by samples
+        import time as _t
+
+        t0 = _t.time()
+        while _t.time() - t0 < 5.0:
+            self.fh.flush()
+            if os.path.getsize(self.path) > 0:
+                break
+            _t.sleep(0.02)
 
     def stop(self):
         if self.proc is None:
