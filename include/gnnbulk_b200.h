@@ -287,6 +287,18 @@ int gb_ladies_counts(int64_t k, const int64_t* d_qoff, const int32_t* d_qcol, co
                      int64_t q_cap, const int64_t* d_rowptr, const int32_t* d_col, int64_t n,
                      int64_t* d_poff, int32_t* d_pv, int32_t* d_pe, void* d_ws, size_t ws_bytes,
                      void* stream);
+/* One LADIES race layer over a local row source (1.5D batch slices): Q's
+ * rows as a CSR d_lrowptr / d_lcol (global column ids, e.g. gathered from
+ * the block owners' memory), Q given as local row indices d_qrow under the
+ * batch offsets d_qoff; keys use layer index `depth`.  Output and workspace
+ * as gb_ladies_bulk with layers = 1 (gb_ladies_bulk_workspace(g, k, q_cap,
+ * 1, &s, mode)); the graph g supplies the column count and degree prefix. */
+int gb_ladies_layer_rows(const gb_graph* g, int64_t k, const int64_t* d_qoff,
+                         const int32_t* d_qrow, int64_t q_cap, const int64_t* d_lrowptr,
+                         const int32_t* d_lcol, int64_t s, uint64_t seed, uint64_t epoch,
+                         int32_t depth, int64_t batch_offset, int32_t mode,
+                         gb_ladies_layer_out* h_layer, int64_t* d_sizes, void* d_ws,
+                         size_t ws_bytes, void* stream);
 size_t gb_ladies_merge_counts_workspace(int64_t k, int64_t nloc);
 int gb_ladies_merge_counts(int64_t k, int64_t m, const int32_t* d_trip, int64_t v0, int64_t nloc,
                            int64_t* d_poff, int32_t* d_pv, int32_t* d_pe, void* d_ws,

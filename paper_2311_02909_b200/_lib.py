@@ -64,6 +64,8 @@ SIGNATURES = {
     "gb_ladies_counts_workspace": (ctypes.c_size_t, [_i64, _i64, _i64]),
     "gb_ladies_counts": (ctypes.c_int, [_i64, _p, _p, _p, _i64, _p, _p, _i64, _p, _p, _p, _p,
                                         ctypes.c_size_t, _p]),
+    "gb_ladies_layer_rows": (ctypes.c_int, [_p, _i64, _p, _p, _i64, _p, _p, _i64, _u64, _u64,
+                                            _i32, _i64, _i32, _p, _p, _p, ctypes.c_size_t, _p]),
     "gb_ladies_merge_counts_workspace": (ctypes.c_size_t, [_i64, _i64]),
     "gb_ladies_merge_counts": (ctypes.c_int, [_i64, _i64, _p, _i64, _i64, _p, _p, _p, _p,
                                               ctypes.c_size_t, _p]),

@@ -406,4 +406,23 @@ int gb_ladies_bulk(const gb_graph* g, int64_t k, const int64_t* d_qoff, const in
                      batch_offset, mode, h_layers, d_sizes, d_ws, ws_bytes, (cudaStream_t)stream);
 }
 
+int gb_ladies_layer_rows(const gb_graph* g, int64_t k, const int64_t* d_qoff,
+                         const int32_t* d_qrow, int64_t q_cap, const int64_t* d_lrowptr,
+                         const int32_t* d_lcol, int64_t s, uint64_t seed, uint64_t epoch,
+                         int32_t depth, int64_t batch_offset, int32_t mode,
+                         gb_ladies_layer_out* h_layer, int64_t* d_sizes, void* d_ws,
+                         size_t ws_bytes, void* stream) {
+  if (!g || k < 0 || s < 1 || depth < 1 || !h_layer || !d_lrowptr || !d_lcol || !d_qrow) {
+    set_error("ladies layer rows: bad arguments");
+    return GB_ERR_CONTRACT;
+  }
+  if (mode != GB_LADIES_RACE && mode != GB_LADIES_RACE_DENSE) {
+    set_error("ladies layer rows: race modes only");
+    return GB_ERR_CONTRACT;
+  }
+  const LadiesRows src{d_lrowptr, d_lcol, d_qrow, depth};
+  return ladies_bulk(g, k, d_qoff, nullptr, q_cap, 1, &s, seed, epoch, batch_offset, mode,
+                     h_layer, d_sizes, d_ws, ws_bytes, (cudaStream_t)stream, &src);
+}
+
 }  // extern "C"

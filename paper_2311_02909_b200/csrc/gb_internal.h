@@ -105,9 +105,18 @@ int ladies_extract_rows(int64_t k, const int64_t* qoff, const int32_t* qcol,
                         int32_t* slots, int32_t* rcnt, cudaStream_t st);
 int ladies_workspace(const Graph* g, int64_t k, int64_t q1_cap, int32_t layers,
                      const int64_t* fanouts, int32_t mode, size_t* bytes);
+// local row source for one LADIES layer: Q's rows as a CSR with global
+// column ids, Q given as local row indices qrow[q]
+struct LadiesRows {
+  const int64_t* rowptr;
+  const int32_t* col;
+  const int32_t* qrow;
+  int32_t depth;  // layer index of the keys (1-based)
+};
 int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t* d_qverts,
                 int64_t q1_cap, int32_t layers, const int64_t* fanouts, uint64_t seed,
                 uint64_t epoch, int64_t batch_offset, int32_t mode, gb_ladies_layer_out* L,
-                int64_t* d_sizes, void* d_ws, size_t ws_bytes, cudaStream_t st);
+                int64_t* d_sizes, void* d_ws, size_t ws_bytes, cudaStream_t st,
+                const LadiesRows* src = nullptr);
 
 }  // namespace gb

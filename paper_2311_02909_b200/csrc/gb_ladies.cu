@@ -1194,9 +1194,18 @@ int ladies_workspace(const Graph* g, int64_t k, int64_t q1_cap, int32_t layers,
 int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t* d_qverts,
                 int64_t q1_cap, int32_t layers, const int64_t* fanouts, uint64_t seed,
                 uint64_t epoch, int64_t batch_offset, int32_t mode, gb_ladies_layer_out* L,
-                int64_t* d_sizes, void* d_ws, size_t ws_bytes, cudaStream_t st) {
+                int64_t* d_sizes, void* d_ws, size_t ws_bytes, cudaStream_t st,
+                const LadiesRows* src) {
   const bool exact = mode == GB_LADIES_EXACT;
   const int64_t n = g->n;
+  // rows of Q: the graph's, or (one layer) a local CSR of the Q rows with
+  // global column ids, Q given as local row indices (1.5D batch slices)
+  if (src && layers != 1) {
+    set_error("ladies: a local row source serves exactly one layer");
+    return GB_ERR_CONTRACT;
+  }
+  const int64_t* RP = src ? src->rowptr : g->rowptr;
+  const int32_t* CL = src ? src->col : g->col;
   const LadiesPlan P = ladies_plan(k, n, q1_cap, layers, fanouts, mode);
   LadiesWs ws = ladies_ws_layout((char*)d_ws, k, P, exact);
   if (ws.bytes > ws_bytes) {
@@ -1253,12 +1262,12 @@ int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t*
     const int32_t s = (int32_t)fanouts[l];
     gb_ladies_layer_out& o = L[l];
     const int64_t* qoff = l == 0 ? d_qoff : L[l - 1].fptr;
-    const int32_t* qcol = l == 0 ? d_qverts : L[l - 1].fcol;
+    const int32_t* qcol = l == 0 ? (src ? src->qrow : d_qverts) : L[l - 1].fcol;
     const int64_t* d_QN = qoff + k;
     int64_t* sizes = d_sizes + kLadiesSizes * l;
     int rc = GB_OK;
     if (!P.tiled) {
-      rc = device_exclusive_scan<int64_t>(d_QN, qc, QDegF{qcol, g->rowptr}, ws.qg, ws.scan_ws, st);
+      rc = device_exclusive_scan<int64_t>(d_QN, qc, QDegF{qcol, RP}, ws.qg, ws.scan_ws, st);
       if (rc) return rc;
     }
     GB_CUDA(cudaMemsetAsync(ws.nnz_b, 0, sizeof(int64_t) * (k + 1), st));
@@ -1266,13 +1275,14 @@ int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t*
       const int64_t g1 = g0 + P.gsize < k ? g0 + P.gsize : k;
       const int64_t gn = g1 - g0;
       const int64_t words = (gn * n + 1) / 2;
-      const RaceKey rk{seed, epoch, (uint64_t)(l + 1), batch_offset + g0};
+      const uint64_t depth = src ? (uint64_t)src->depth : (uint64_t)(l + 1);
+      const RaceKey rk{seed, epoch, depth, batch_offset + g0};
       if (P.tiled) {
         // ---- P = Q A, race keys and key histograms for this group, one pass
         GB_CUDA(cudaMemsetAsync(ws.tst, 0, sizeof(unsigned long long), st));
         GB_CUDA(cudaMemsetAsync(ws.hist, 0, sizeof(uint32_t) * gn * kBins, st));
         LadTileArgs T{};
-        T.qoff = qoff; T.qcol = qcol; T.rowptr = g->rowptr; T.col = g->col; T.tb = ws.tb;
+        T.qoff = qoff; T.qcol = qcol; T.rowptr = RP; T.col = CL; T.tb = ws.tb;
         T.ntiles = ws.ntiles; T.n = n; T.g0 = g0; T.gn = gn; T.rk = rk; T.ticket = ws.tst;
         T.pv = ws.pv; T.keys = ws.keys; T.tcnt = ws.tcnt; T.hist = ws.hist; T.nnz_b = ws.nnz_b;
         prof_mark(st);
@@ -1284,8 +1294,8 @@ int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t*
       } else {
         // ---- P = Q A for this group
         prof_mark(st);
-        k_lad_count<<<4 * sms, kLadiesThreads, 0, st>>>(qoff, k, g0, g1, qcol, ws.qg, g->rowptr,
-                                                        g->col, n, ws.cnt32, ws.nnz_b);
+        k_lad_count<<<4 * sms, kLadiesThreads, 0, st>>>(qoff, k, g0, g1, qcol, ws.qg, RP, CL, n,
+                                                        ws.cnt32, ws.nnz_b);
         GB_LAUNCH_CHECK("k_lad_count");
         prof_mark(st);
         k_lad_compact_count<<<gcap(P.tiles, 1, 8 * sms), 256, 0, st>>>(ws.cnt32, words, n, g0,
@@ -1301,7 +1311,7 @@ int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t*
       // ---- NORM + SAMPLE
       LadiesSampleArgs A{};
       A.gpoff = ws.gpoff; A.pv = ws.pv; A.pe = ws.pe; A.g0 = g0; A.gn = gn; A.s = s;
-      A.batch_offset = batch_offset; A.seed = seed; A.epoch = epoch; A.depth = (uint64_t)(l + 1);
+      A.batch_offset = batch_offset; A.seed = seed; A.epoch = epoch; A.depth = depth;
       A.sw = ws.sw; A.sc = ws.sc; A.keys = ws.keys; A.sel = ws.sel; A.nsel = ws.nsel;
       A.take = ws.take;
       A.nnzb = P.tiled ? ws.nnz_b : nullptr;
@@ -1334,7 +1344,7 @@ int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t*
     k_lad_pack_s<<<gcap(k * s, 256, 16 * sms), 256, 0, st>>>(o.fptr, k, s, ws.Sfix, o.fcol);
     k_lad_layout<<<1, 1, 0, st>>>(o.fptr, k, o.coloff, sizes);
     // ---- EXTRACT A_S = Q_R A Q_C
-    rc = device_exclusive_scan<int64_t>(d_QN, qc, RcapF{qcol, g->rowptr, qoff, o.fptr, k},
+    rc = device_exclusive_scan<int64_t>(d_QN, qc, RcapF{qcol, RP, qoff, o.fptr, k},
                                         ws.slot, ws.scan_ws, st);
     if (rc) return rc;
     if (s <= kSmaxSmem) {
@@ -1342,10 +1352,10 @@ int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t*
       const int64_t rows_max = l == 0 ? q1_cap : fanouts[l - 1];
       const int64_t chunks = (rows_max + kXRows - 1) / kXRows;
       k_lad_extract_hash<<<gcap(k * chunks, 1, 8 * sms), kLadiesThreads, 0, st>>>(
-          qoff, k, chunks, qcol, g->rowptr, g->col, o.fptr, o.fcol, o.coloff, ws.slot, ws.slots,
+          qoff, k, chunks, qcol, RP, CL, o.fptr, o.fcol, o.coloff, ws.slot, ws.slots,
           ws.rcnt);
     } else {
-      k_lad_extract<<<8 * sms, kLadiesThreads, 0, st>>>(qoff, k, qcol, g->rowptr, g->col, o.fptr,
+      k_lad_extract<<<8 * sms, kLadiesThreads, 0, st>>>(qoff, k, qcol, RP, CL, o.fptr,
                                                        o.fcol, o.coloff, ws.slot, ws.slots,
                                                        ws.rcnt);
     }

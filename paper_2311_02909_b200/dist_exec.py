@@ -202,6 +202,35 @@ class Sage15D:
                 self.stats["fetch_ids"] += ids.numel()
         return lrowptr, lcol
 
+    def fetch_rows_any(self, U):
+        """A rows of any sorted distinct vertices U from their block owners'
+        memory (grid row b, this rank's column: every replica of a grid row
+        holds its block), as a local CSR — peer reads, no messages."""
+        torch = _torch()
+        L = _lib.lib()
+        pb = self._peer_block()
+        d = self.gdeg[U.long()].long()
+        lrowptr = torch.zeros(U.numel() + 1, dtype=torch.int64, device=self.dev)
+        lrowptr[1:] = torch.cumsum(d, 0)
+        nnz = int(lrowptr[-1].item())
+        lcol = torch.zeros(nnz + _lib.GB_COL_PAD, dtype=torch.int32, device=self.dev)
+        for b in range(self.grid.rows):
+            owner = self.grid.rank(b, self.j)
+            lo, hi = int(self.bounds[b]), int(self.bounds[b + 1])
+            sel = torch.nonzero((U >= lo) & (U < hi)).flatten()
+            if sel.numel() == 0:
+                continue
+            ids = U[sel].to(torch.int32).contiguous()
+            offs = lrowptr[sel].contiguous()
+            _lib.check(L.gb_gather_rows(ids.numel(), _lib.ptr(ids), lo,
+                                        ctypes.c_void_p(pb["rp_h"].buffer_ptrs[owner]),
+                                        ctypes.c_void_p(pb["cl_h"].buffer_ptrs[owner]),
+                                        _lib.ptr(offs), _lib.ptr(lcol), _lib.stream_ptr()),
+                       "gb_gather_rows")
+            if owner != self.rank:
+                self.stats["fetch_ids"] += ids.numel()
+        return lrowptr, lcol
+
     def fetch_rows(self, U):
         """A rows of the sorted distinct vertices U (all in this column's
         range) as a local CSR (rowptr over U, cols)."""
@@ -544,6 +573,71 @@ class Sage15D:
 
 
 class Ladies15D(Sage15D):
+    def batch_slice(self, k):
+        """fetch="p2p": this replica's share [j0, j1) of its grid row's k
+        batches."""
+        b = _bounds(k, self.grid.c)
+        return int(b[self.j]), int(b[self.j + 1])
+
+    def sample_p2p(self, group_batches, epoch, batch_offset, seed):
+        """1.5D LADIES with the replicas of a grid row splitting its batches:
+        each layer gathers the A rows of its Q straight from the block
+        owners' memory (peer reads) and runs the single-GPU race layer on them
+        (gb_ladies_layer_rows: column tiles in shared memory, keys, radix
+        select, extraction).  The partial-count merge and candidate exchange
+        of the message-based variant disappear: every sampled set is complete
+        where it is computed."""
+        torch = _torch()
+        L = _lib.lib()
+        dev, n = self.dev, self.n
+        j0, j1 = self.batch_slice(len(group_batches))
+        mine = group_batches[j0:j1]
+        k = len(mine)
+        off = np.zeros(k + 1, np.int64)
+        off[1:] = np.cumsum([len(x) for x in mine])
+        qoff = torch.as_tensor(off).to(dev)
+        qcol = torch.as_tensor(np.concatenate([np.sort(np.asarray(x)) for x in mine])
+                               .astype(np.int32) if off[-1] else np.zeros(1, np.int32)).to(dev)
+        layers = []
+        for l, s in enumerate(self.fanouts):
+            QN = int(qoff[k].item()) if k else 0
+            qc = qcol[:QN]
+            U = torch.unique(qc)
+            lrowptr, lcol = self.fetch_rows_any(U)
+            lrow = torch.searchsorted(U, qc).to(torch.int32).contiguous()
+            qcap = max(QN, 1)
+            o = {"fptr": torch.zeros(k + 1, dtype=torch.int64, device=dev),
+                 "fcol": torch.zeros(max(k * s, 1), dtype=torch.int32, device=dev),
+                 "aptr": torch.zeros(qcap + 1, dtype=torch.int64, device=dev),
+                 "acol": torch.zeros(qcap * s, dtype=torch.int32, device=dev),
+                 "coloff": torch.zeros(k + 1, dtype=torch.int64, device=dev)}
+            out = _lib.LadiesLayerOut()
+            for name in ("fptr", "fcol", "aptr", "acol", "coloff"):
+                setattr(out, name, o[name].data_ptr())
+            out.q_cap, out.f_cap, out.a_cap = qcap, max(k * s, 1), qcap * s
+            sizes = torch.zeros(5, dtype=torch.int64, device=dev)
+            fan = (ctypes.c_int64 * 1)(s)
+            wsb = ctypes.c_size_t()
+            _lib.check(L.gb_ladies_bulk_workspace(self.tables.handle, max(k, 1), qcap, 1, fan,
+                                                  _lib.GB_LADIES_RACE, ctypes.byref(wsb)),
+                       "gb_ladies_bulk_workspace")
+            ws = torch.empty(max(int(wsb.value), 1), dtype=torch.uint8, device=dev)
+            if k:
+                _lib.check(L.gb_ladies_layer_rows(
+                    self.tables.handle, k, _lib.ptr(qoff), _lib.ptr(lrow), qcap, _lib.ptr(lrowptr),
+                    _lib.ptr(lcol), s, seed, epoch, l + 1, batch_offset + j0,
+                    _lib.GB_LADIES_RACE, ctypes.byref(out), _lib.ptr(sizes), _lib.ptr(ws),
+                    ws.numel(), _lib.stream_ptr()), "gb_ladies_layer_rows")
+            R, F, A, C = (int(x) for x in sizes.tolist()[:4])
+            layers.append({
+                "frontier_shape": (k, n), "frontier_ptr": o["fptr"], "frontier_col": o["fcol"][:F],
+                "adj_shape": (QN, C), "adj_ptr": o["aptr"][: QN + 1], "adj_col": o["acol"][:A],
+                "rowv_off": qoff, "rowv_cat": qc,
+                "colv_off": o["fptr"], "colv_cat": o["fcol"][:F],
+                "sampv_off": o["fptr"], "sampv_cat": o["fcol"][:F]})
+            qoff, qcol = o["fptr"], o["fcol"]
+        return layers
+
     """1.5D partitioned LADIES (exponential-race sampling) over real processes.
 
     Per layer, grid row i (k_i batches), replica j:
@@ -562,6 +656,8 @@ class Ladies15D(Sage15D):
     def sample(self, group_batches, epoch, batch_offset, seed):
         import torch.distributed as dist
 
+        if self.fetch == "p2p":
+            return self.sample_p2p(group_batches, epoch, batch_offset, seed)
         torch = _torch()
         L = _lib.lib()
         dev, n, c = self.dev, self.n, self.grid.c
@@ -730,6 +826,16 @@ def ladies_epoch_15d(sampler: Ladies15D, cfg, batches, epoch=0, batch_offset=0):
     parts = []
     for i in range(grid.rows):
         gi = [np.asarray(x) for x in batches[int(b[i]):int(b[i + 1])]]
+        if sampler.fetch == "p2p":  # the grid row's batches split over its replicas
+            cb = _bounds(len(gi), grid.c)
+            for j in range(grid.c):
+                if int(cb[j + 1]) == int(cb[j]):
+                    continue
+                parts.append(SampledEpoch(SamplerKind.LADIES, epoch, gi[int(cb[j]):int(cb[j + 1])],
+                                          [LayerSample(d + 1, device=x, n=sampler.n)
+                                           for d, x in enumerate(allp[grid.rank(i, j)])],
+                                          cfg.layers))
+            continue
         parts.append(SampledEpoch(SamplerKind.LADIES, epoch, gi,
                                   [LayerSample(d + 1, device=x, n=sampler.n)
                                    for d, x in enumerate(allp[grid.rank(i, 0)])], cfg.layers))
