@@ -1195,6 +1195,10 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     const int32_t d = l + 1;
     if (l > 0) stride *= fanouts[l - 1];
     gb_sage_layer_out& o = L[l];
+    // layer 1's rows are the batch vertices, all distinct: the duplicate-row
+    // pass has nothing to merge there, every P row is streamed on chip once
+    const bool ldedup = dedup && l > 0;
+    const bool lstream = stream || (dedup && l == 0);
     const int32_t* rowv = l == 0 ? d_bverts : L[l - 1].fcol;
     const int64_t* brow = l == 0 ? d_bptr : L[l - 1].eoff;
     const int64_t* R_ptr = brow + k;
@@ -1202,13 +1206,13 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     uint32_t* bm = (l & 1) ? ws.bitmap2 : ws.bitmap;
     int32_t* wp = (l & 1) ? ws.wpre2 : ws.wpre;
     if (l >= 2) GB_CUDA(cudaStreamWaitEvent(st, ring_event(l - 2), 0));
-    if (dedup) GB_CUDA(cudaMemsetAsync(ws.vbits, 0, sizeof(uint32_t) * (nwords + 1), st));
+    if (ldedup) GB_CUDA(cudaMemsetAsync(ws.vbits, 0, sizeof(uint32_t) * (nwords + 1), st));
     k_sage_prep<<<grid_for(r_cap, 256, 16 * kNumSMs), 256, 0, st>>>(R_ptr, rowv, g->rowptr, ws.deg,
-                                                                     dedup ? ws.vbits : nullptr);
+                                                                     ldedup ? ws.vbits : nullptr);
     GB_LAUNCH_CHECK("k_sage_prep");
     int rc = device_exclusive_scan<int64_t>(R_ptr, r_cap, TakeF{ws.deg, s}, o.fptr, ws.scan_ws, st);
     if (rc) return rc;
-    if (stream) {
+    if (lstream) {
       rc = device_exclusive_scan<int64_t>(R_ptr, r_cap, DegF{ws.deg}, ws.gstart, ws.scan_ws, st);
       if (rc) return rc;
     }
@@ -1221,7 +1225,7 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     A.seed = seed; A.epoch = epoch; A.depth = (uint64_t)d;
     A.bitmap = bm; A.nwords = nwords; A.fcol = o.fcol; A.pidx = ws.pidx;
     const int pick_grid = grid_for(r_cap, kPickThreads, 64 * kNumSMs);
-    if (dedup) {
+    if (ldedup) {
       rc = dedup_prepare(g, ws, R_ptr, rowv, o.fptr, brow, k, s, r_cap, nwords, st);
       if (rc) return rc;
       A.D_ptr = ws.d_nw + 1; A.roff = ws.roff; A.rrec = ws.rrec;
@@ -1235,13 +1239,13 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
       prof_mark(st);
     } else {
       prof_mark(st);
-      if (stream)
+      if (lstream)
         launch_pick<0>(pick_grid, A, R_ptr, st);
       else
         launch_pick<1>(pick_grid, A, R_ptr, st);
       GB_LAUNCH_CHECK("k_sage_pick");
       prof_mark(st);
-      if (stream) {
+      if (lstream) {
         prof_mark(st);
         k_sage_stream<<<stream_grid(), kStreamThreads, 0, st>>>(A, R_ptr);
         GB_LAUNCH_CHECK("k_sage_stream");
