@@ -55,9 +55,11 @@ def parse():
     p.add_argument("--dist", default="replicated", choices=["replicated", "15d"],
                    help="multi-GPU mode: replicated graph (cfg4) or 1.5D partitioned (cfg5)")
     p.add_argument("--c", type=int, default=2, help="1.5D replication factor")
-    p.add_argument("--fetch", default="p2p", choices=["rows", "owner", "p2p"],
-                   help="1.5D SAGE: Alg. 2 row fetch, owner-computes over NCCL (ship row "
-                        "keys), or owner sampling over peer memory (fused, default)")
+    p.add_argument("--fetch", default="auto", choices=["auto", "rows", "owner", "p2p", "split"],
+                   help="1.5D SAGE: Alg. 2 row fetch / owner-computes over NCCL, owner "
+                        "sampling over peer memory (p2p), replicas splitting the batches "
+                        "with rows read from peer memory (split); auto = split if c > 1 "
+                        "else p2p")
     return p.parse_args()
 
 
@@ -608,7 +610,10 @@ def run_15d(args, rank, world, local_rank):
     k = args.k or default_k(args.workload)
     allb = make_batches_for(n, k * grid.rows)
     # the grid samples row by row at the owner: stream or P-free kernels
-    m15 = "stream" if args.mode == "stream" else "pfree"
+    # auto: replicas split the batches (c > 1), else owner sampling over peer memory
+    fetch = args.fetch if args.fetch != "auto" else ("split" if c > 1 else "p2p")
+    args.fetch = fetch
+    m15 = "dedup" if fetch == "split" else ("stream" if args.mode == "stream" else "pfree")
     s = Sage15D(dg, grid, FANOUTS, BATCH, mode=m15, fetch=args.fetch)
     i = s.i
     mine = [np.asarray(x) for x in allb[i * k:(i + 1) * k]]
@@ -670,7 +675,8 @@ def run_15d(args, rank, world, local_rank):
 
     lb = make_batches(np.arange(n), 512, seed=0, epoch=0)[:k * grid.rows]
     lmine = [np.sort(np.asarray(x)) for x in lb[i * k:(i + 1) * k]]
-    ls = Ladies15D(dg, grid, (512,) * 3, 512, fetch="p2p" if args.fetch == "p2p" else "rows")
+    ls = Ladies15D(dg, grid, (512,) * 3, 512,
+                   fetch="p2p" if args.fetch in ("p2p", "split") else "rows")
     for _ in range(2):
         ls.sample(lmine, 0, i * k, 0)
     lt = []

@@ -287,6 +287,20 @@ int gb_ladies_counts(int64_t k, const int64_t* d_qoff, const int32_t* d_qcol, co
                      int64_t q_cap, const int64_t* d_rowptr, const int32_t* d_col, int64_t n,
                      int64_t* d_poff, int32_t* d_pv, int32_t* d_pe, void* d_ws, size_t ws_bytes,
                      void* stream);
+/* gb_sage_bulk (dedup mode) over rows held in other GPUs' memory (1.5D
+ * batch split): the graph g supplies degrees and replay tables; the A rows of
+ * block b (vertices [d_bounds[b], d_bounds[b+1])) are read from CSR
+ * d_brp[b] / d_bcol[b] (device arrays of peer pointers, e.g. symmetric
+ * memory) — the distinct rows are staged straight from the owners' memory
+ * by the serve kernels (P2P cp.async over NVLink).  Same outputs as
+ * gb_sage_bulk. */
+int gb_sage_bulk_peer(const gb_graph* g, int64_t k, const int64_t* d_bptr,
+                      const int32_t* d_bverts, int64_t r1_cap, int64_t batch_size, int32_t layers,
+                      const int64_t* h_fanouts, uint64_t seed, uint64_t epoch,
+                      int64_t batch_offset, gb_sage_layer_out* h_layers, int64_t* d_sizes,
+                      void* d_ws, size_t ws_bytes, int32_t nblk, const int64_t* d_bounds,
+                      const int64_t* const* d_brp, const int32_t* const* d_bcol, void* stream);
+
 /* One LADIES race layer over a local row source (1.5D batch slices): Q's
  * rows as a CSR d_lrowptr / d_lcol (global column ids, e.g. gathered from
  * the block owners' memory), Q given as local row indices d_qrow under the

@@ -56,6 +56,9 @@ SIGNATURES = {
     "gb_sage_bulk_workspace": (ctypes.c_int, [_p, _i64, _i64, _i32, _p, ctypes.POINTER(ctypes.c_size_t)]),
     "gb_sage_bulk": (ctypes.c_int, [_p, _i64, _p, _p, _i64, _i64, _i32, _p, _u64, _u64, _i64,
                                     _i32, ctypes.POINTER(SageLayerOut), _p, _p, ctypes.c_size_t, _p]),
+    "gb_sage_bulk_peer": (ctypes.c_int, [_p, _i64, _p, _p, _i64, _i64, _i32, _p, _u64, _u64,
+                                         _i64, ctypes.POINTER(SageLayerOut), _p, _p,
+                                         ctypes.c_size_t, _i32, _p, _p, _p, _p]),
     "gb_ladies_bulk_workspace": (ctypes.c_int, [_p, _i64, _i64, _i32, _p, _i32,
                                                 ctypes.POINTER(ctypes.c_size_t)]),
     "gb_ladies_bulk": (ctypes.c_int, [_p, _i64, _p, _p, _i64, _i32, _p, _u64, _u64, _i64, _i32,

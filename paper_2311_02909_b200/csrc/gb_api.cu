@@ -219,6 +219,31 @@ int gb_sage_bulk(const gb_graph* g, int64_t k, const int64_t* d_bptr, const int3
                    batch_offset, mode, h_layers, d_sizes, d_ws, ws_bytes, (cudaStream_t)stream);
 }
 
+int gb_sage_bulk_peer(const gb_graph* g, int64_t k, const int64_t* d_bptr,
+                      const int32_t* d_bverts, int64_t r1_cap, int64_t batch_size, int32_t layers,
+                      const int64_t* h_fanouts, uint64_t seed, uint64_t epoch,
+                      int64_t batch_offset, gb_sage_layer_out* h_layers, int64_t* d_sizes,
+                      void* d_ws, size_t ws_bytes, int32_t nblk, const int64_t* d_bounds,
+                      const int64_t* const* d_brp, const int32_t* const* d_bcol, void* stream) {
+  if (nblk < 1 || !d_bounds || !d_brp || !d_bcol) {
+    set_error("sage bulk peer: need the block table");
+    return GB_ERR_CONTRACT;
+  }
+  if (!g || k < 0 || layers < 1 || batch_size < 1 || !h_fanouts || !h_layers) {
+    set_error("sage bulk: bad arguments");
+    return GB_ERR_CONTRACT;
+  }
+  for (int32_t l = 0; l < layers; ++l)
+    if (h_fanouts[l] < 1 || h_fanouts[l] > 32) {
+      set_error("sage bulk: fanout %lld outside [1, 32]", (long long)h_fanouts[l]);
+      return h_fanouts[l] < 1 ? GB_ERR_CONTRACT : GB_ERR_UNSUPPORTED;
+    }
+  const PeerRowsHost peer{nblk, d_bounds, d_brp, d_bcol};
+  return sage_bulk(g, k, d_bptr, d_bverts, r1_cap, batch_size, layers, h_fanouts, seed, epoch,
+                   batch_offset, GB_SAGE_DEDUP, h_layers, d_sizes, d_ws, ws_bytes,
+                   (cudaStream_t)stream, &peer);
+}
+
 size_t gb_sage_layer_sample_workspace(int64_t r_cap, int64_t f_cap) {
   return sage_layer_sample_ws(r_cap, f_cap);
 }

@@ -59,11 +59,19 @@ int first_occurrence(int64_t F, const int32_t* colidx, const int64_t* eb, const 
                      int64_t k, int64_t ncols, int32_t* first, cudaStream_t st);
 int sage_workspace(const Graph* g, int64_t k, int64_t r1_cap, int32_t layers,
                    const int64_t* fanouts, size_t* bytes);
+// rows held by peers (1.5D batch split): device arrays of the block bounds
+// (nblk + 1) and of the blocks' CSR pointers in their owners' memory
+struct PeerRowsHost {
+  int nblk;
+  const int64_t* bounds;
+  const int64_t* const* brp;
+  const int32_t* const* bcol;
+};
 int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d_bverts,
               int64_t r1_cap, int64_t batch_size, int32_t layers, const int64_t* fanouts,
               uint64_t seed, uint64_t epoch, int64_t batch_offset, int32_t mode,
               gb_sage_layer_out* L, int64_t* d_sizes, void* d_ws, size_t ws_bytes,
-              cudaStream_t st);
+              cudaStream_t st, const PeerRowsHost* peer = nullptr);
 size_t sage_layer_sample_ws(int64_t r_cap, int64_t f_cap);
 int sage_layer_sample(const Graph* tables, int64_t k, const int64_t* brow, int64_t r_cap,
                       const int32_t* rowv, const int32_t* deg, const int64_t* fptr,

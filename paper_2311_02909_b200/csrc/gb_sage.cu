@@ -638,15 +638,37 @@ struct __align__(16) DdItem {
   int32_t pad[3];
 };
 
+// row source of the 1.5D batch-split mode: rows of block b (vertices
+// [bounds[b], bounds[b+1])) live in a peer's memory as CSR brp[b] / bcol[b]
+struct PeerRows {
+  int nblk;
+  const int64_t* bounds;
+  const int64_t* const* brp;
+  const int32_t* const* bcol;
+};
+
 // descriptors of every tier's items (tier-major)
+// a0: index of the row's first entry in the graph's column array, or with a
+// peer row source the row's address in its block owner's memory / 4 (the
+// serve kernel then addresses rows from a null base)
 __global__ void k_dd_items(const int64_t* __restrict__ D_ptr, const int32_t* __restrict__ dv,
                            const int32_t* __restrict__ ddeg, const int64_t* __restrict__ rowptr, const int64_t* __restrict__ roff,
                            const int64_t* __restrict__ ioff, DdItems rows,
-                           DdItem* __restrict__ items) {
+                           DdItem* __restrict__ items, PeerRows peer) {
   const int64_t D = *D_ptr;
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < D;
        g += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t a0 = rowptr[dv[g]], d = ddeg[g];
+    const int32_t v = dv[g];
+    int64_t a0;
+    if (peer.nblk) {
+      int b = 0;
+      while (b + 1 < peer.nblk && peer.bounds[b + 1] <= v) ++b;
+      const int64_t* brp = peer.brp[b];
+      a0 = ((int64_t)(uintptr_t)(peer.bcol[b] + brp[v - peer.bounds[b]])) >> 2;
+    } else {
+      a0 = rowptr[v];
+    }
+    const int64_t d = ddeg[g];
     const int t = dd_tier(d);
     const int64_t o0 = ioff[t * D + g], o1 = ioff[t * D + g + 1];
     const int64_t r0 = roff[g], r1 = roff[g + 1], per = rows.rows[t];
@@ -663,7 +685,7 @@ __global__ void k_dd_items(const int64_t* __restrict__ D_ptr, const int32_t* __r
 }
 
 struct DdArgs {
-  const int64_t* D_ptr;
+  const int64_t* D_ptr;  // (col == nullptr: item a0 is an address / 4, peer rows)
   const int32_t* col;
   const int64_t* ioff;   // tier-major item prefix (3D + 1)
   const DdItem* items;
@@ -1034,7 +1056,7 @@ static DdItems dd_items(int32_t s) {
 // together, and the tier-major work items of the serve kernels.
 static int dedup_prepare(const Graph* g, SageWs& ws, const int64_t* R_ptr, const int32_t* rowv,
                          const int64_t* fptr, const int64_t* brow, int64_t k, int32_t s,
-                         int64_t r_cap, int64_t nwords, cudaStream_t st) {
+                         int64_t r_cap, int64_t nwords, const PeerRows& peer, cudaStream_t st) {
   const int64_t gw = 16 * kNumSMs;
   // (vertex bitmap already marked by k_sage_prep)
   // distinct row vertices D <= min(rows, n): group arrays sized by that
@@ -1059,7 +1081,7 @@ static int dedup_prepare(const Graph* g, SageWs& ws, const int64_t* R_ptr, const
                                       ws.ioff, ws.scan_ws, st);
   if (rc) return rc;
   k_dd_items<<<grid_for(dcap, 256, gw), 256, 0, st>>>(ws.d_nw + 1, ws.dv, ws.ddeg, g->rowptr, ws.roff,
-                                                      ws.ioff, dd_items(s), ws.items);
+                                                      ws.ioff, dd_items(s), ws.items, peer);
   GB_LAUNCH_CHECK("dedup prepare");
   count_launches(5);  // 3d, list, rcount, rows, items (scans count themselves)
   return GB_OK;
@@ -1091,9 +1113,11 @@ static int launch_serve(DdArgs A, cudaStream_t st) {
 
 // Dedup step 2 (after k_sage_pick<2> wrote the grouped picks): each
 // distinct row on chip, three size tiers.
-static int dedup_serve(const Graph* g, SageWs& ws, const SageArgs& S, cudaStream_t st) {
+static int dedup_serve(const Graph* g, SageWs& ws, const SageArgs& S, bool peer_rows,
+                       cudaStream_t st) {
   DdArgs A{};
-  A.D_ptr = ws.d_nw + 1; A.col = g->col; A.ioff = ws.ioff; A.items = ws.items;
+  A.D_ptr = ws.d_nw + 1; A.col = peer_rows ? nullptr : g->col; A.ioff = ws.ioff;
+  A.items = ws.items;
   A.pidx = ws.pidx; A.rbf = (const int2*)ws.rrec;
   A.s = S.s; A.fcol = S.fcol; A.bitmap = S.bitmap; A.nwords = S.nwords;
   // the tiers touch disjoint frontier entries (and commutative bitmap ORs):
@@ -1150,9 +1174,17 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
               int64_t r1_cap, int64_t batch_size, int32_t layers, const int64_t* fanouts,
               uint64_t seed, uint64_t epoch, int64_t batch_offset, int32_t mode,
               gb_sage_layer_out* L, int64_t* d_sizes, void* d_ws, size_t ws_bytes,
-              cudaStream_t st) {
+              cudaStream_t st, const PeerRowsHost* peer_host) {
   const bool stream = mode == GB_SAGE_STREAM;
   const bool dedup = mode == GB_SAGE_DEDUP;
+  PeerRows peer{0, nullptr, nullptr, nullptr};
+  if (peer_host) {
+    if (!dedup) {
+      set_error("sage bulk: peer rows need the dedup mode");
+      return GB_ERR_UNSUPPORTED;
+    }
+    peer = PeerRows{peer_host->nblk, peer_host->bounds, peer_host->brp, peer_host->bcol};
+  }
   const int64_t nwords = (g->n + 31) / 32;
   const int64_t W = k * nwords;
   if (W >= ((int64_t)1 << 31)) {
@@ -1197,8 +1229,8 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     gb_sage_layer_out& o = L[l];
     // layer 1's rows are the batch vertices, all distinct: the duplicate-row
     // pass has nothing to merge there, every P row is streamed on chip once
-    const bool ldedup = dedup && l > 0;
-    const bool lstream = stream || (dedup && l == 0);
+    const bool ldedup = dedup && (l > 0 || peer.nblk);
+    const bool lstream = stream || (dedup && !ldedup);
     const int32_t* rowv = l == 0 ? d_bverts : L[l - 1].fcol;
     const int64_t* brow = l == 0 ? d_bptr : L[l - 1].eoff;
     const int64_t* R_ptr = brow + k;
@@ -1226,7 +1258,7 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     A.bitmap = bm; A.nwords = nwords; A.fcol = o.fcol; A.pidx = ws.pidx;
     const int pick_grid = grid_for(r_cap, kPickThreads, 64 * kNumSMs);
     if (ldedup) {
-      rc = dedup_prepare(g, ws, R_ptr, rowv, o.fptr, brow, k, s, r_cap, nwords, st);
+      rc = dedup_prepare(g, ws, R_ptr, rowv, o.fptr, brow, k, s, r_cap, nwords, peer, st);
       if (rc) return rc;
       A.D_ptr = ws.d_nw + 1; A.roff = ws.roff; A.rrec = ws.rrec;
       prof_mark(st);
@@ -1234,7 +1266,7 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
       GB_LAUNCH_CHECK("k_sage_pick");
       prof_mark(st);
       prof_mark(st);
-      rc = dedup_serve(g, ws, A, st);
+      rc = dedup_serve(g, ws, A, peer.nblk > 0, st);
       if (rc) return rc;
       prof_mark(st);
     } else {

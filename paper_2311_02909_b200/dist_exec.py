@@ -105,10 +105,12 @@ class Sage15D:
             raise ContractViolation("Sage15D needs torch.distributed with world_size == grid.p")
         self.grid, self.fanouts, self.b = grid, tuple(int(s) for s in fanouts), int(batch_size)
         self.mode, self.ledger = mode, ledger
-        if fetch not in ("rows", "owner", "p2p"):
+        if fetch not in ("rows", "owner", "p2p", "split"):
             raise ContractViolation(f"unknown fetch mode {fetch!r}")
         # "rows": Alg. 2 row fetch; "owner": owner samples, returns picks;
-        # "p2p": owner reads requests from and writes picks into peer memory
+        # "p2p": owner reads requests from and writes picks into peer memory;
+        # "split": the grid row's replicas split its batches and run the
+        # single-GPU dedup bulk on rows read from the owners' memory
         self.fetch = fetch
         self._p2p = None
         self.rank = dist.get_rank()
@@ -486,11 +488,63 @@ class Sage15D:
                 lay["fcol"][:F]})
         return out
 
+    # -- batch split over the replicas, rows from peer memory ----------------------------
+    def batch_slice(self, k):
+        """This replica's share [j0, j1) of its grid row's k batches."""
+        b = _bounds(k, self.grid.c)
+        return int(b[self.j]), int(b[self.j + 1])
+
+    def _peer_table(self):
+        """Device block table of the peer row source: bounds and the CSR
+        pointers of every block in the owner of this rank's column."""
+        torch = _torch()
+        if getattr(self, "_ptab", None) is None:
+            pb = self._peer_block()
+            owners = [self.grid.rank(b, self.j) for b in range(self.grid.rows)]
+            self._ptab = (
+                torch.as_tensor(np.asarray(self.bounds, np.int64)).to(self.dev),
+                torch.tensor([pb["rp_h"].buffer_ptrs[o] for o in owners], dtype=torch.int64,
+                             device=self.dev),
+                torch.tensor([pb["cl_h"].buffer_ptrs[o] for o in owners], dtype=torch.int64,
+                             device=self.dev))
+        return self._ptab
+
+    def sample_split(self, group_batches, epoch, batch_offset, seed):
+        """1.5D SAGE with the grid row's batches split over its c replicas:
+        each runs the single-GPU bulk (dedup Alg. 1: pick in vertex-group
+        order, distinct rows staged on chip) with every distinct A row read
+        straight from its block owner's memory by the serve kernels.  No
+        messages; outputs are this replica's batch slice."""
+        from .engine import SageBulk
+
+        torch = _torch()
+        j0, j1 = self.batch_slice(len(group_batches))
+        mine = [np.asarray(x) for x in group_batches[j0:j1]]
+        k = len(mine)
+        off = np.zeros(k + 1, np.int64)
+        off[1:] = np.cumsum([len(x) for x in mine])
+        r1 = max(int(off[-1]), 1)
+        key = (k, r1)
+        if getattr(self, "_split_bulk", None) is None or self._split_key != key:
+            self._split_bulk = SageBulk(self.tables, max(k, 1), max(k * self.b, r1), self.b,
+                                        self.fanouts, mode="dedup")
+            self._split_key = key
+        d_off = torch.as_tensor(off).to(self.dev)
+        d_cat = torch.as_tensor(np.concatenate(mine).astype(np.int32) if off[-1]
+                                else np.zeros(1, np.int32)).to(self.dev)
+        if not k:
+            return []
+        bulk = self._split_bulk
+        bulk.launch_peer(d_off, d_cat, seed, epoch, batch_offset + j0, self._peer_table())
+        return [ls.device for ls in bulk.layers(d_off, d_cat)]
+
     # -- one bulk --------------------------------------------------------------------------
     def sample(self, group_batches, epoch, batch_offset, seed):
         """Sample this grid row's group; returns (device layer dicts, sizes)."""
         if self.fetch == "p2p":
             return self.sample_p2p(group_batches, epoch, batch_offset, seed)
+        if self.fetch == "split":
+            return self.sample_split(group_batches, epoch, batch_offset, seed)
         import torch.distributed as dist
 
         torch = _torch()
@@ -573,12 +627,6 @@ class Sage15D:
 
 
 class Ladies15D(Sage15D):
-    def batch_slice(self, k):
-        """fetch="p2p": this replica's share [j0, j1) of its grid row's k
-        batches."""
-        b = _bounds(k, self.grid.c)
-        return int(b[self.j]), int(b[self.j + 1])
-
     def sample_p2p(self, group_batches, epoch, batch_offset, seed):
         """1.5D LADIES with the replicas of a grid row splitting its batches:
         each layer gathers the A rows of its Q straight from the block
@@ -863,8 +911,18 @@ def sage_epoch_15d(sampler: Sage15D, cfg, batches, epoch=0, batch_offset=0, gath
     dist.all_gather_object(allp, local)
     parts = []
     for i in range(grid.rows):
-        lay = allp[grid.rank(i, 0)]
         gi = [np.asarray(x) for x in batches[int(b[i]):int(b[i + 1])]]
+        if sampler.fetch == "split":  # the grid row's batches split over its replicas
+            cb = _bounds(len(gi), grid.c)
+            for j in range(grid.c):
+                if int(cb[j + 1]) == int(cb[j]):
+                    continue
+                parts.append(SampledEpoch(SamplerKind.SAGE, epoch, gi[int(cb[j]):int(cb[j + 1])],
+                                          [LayerSample(d + 1, device=x, n=sampler.n)
+                                           for d, x in enumerate(allp[grid.rank(i, j)])],
+                                          cfg.layers))
+            continue
+        lay = allp[grid.rank(i, 0)]
         parts.append(SampledEpoch(SamplerKind.SAGE, epoch, gi,
                                   [LayerSample(d + 1, device=x, n=sampler.n)
                                    for d, x in enumerate(lay)], cfg.layers))

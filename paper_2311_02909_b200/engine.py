@@ -71,6 +71,19 @@ class SageBulk:
         self.ws = torch.empty(max(int(nbytes.value), 1), dtype=torch.uint8, device=dev)
         self.sizes = torch.zeros(3 * L, dtype=torch.int64, device=dev)
 
+    def launch_peer(self, d_bptr, d_bverts, seed, epoch, batch_offset, peer, stream=None):
+        """The bulk (dedup mode) with the A rows read from their owners'
+        memory: peer = (bounds int64[nblk + 1], brp pointers, bcol pointers)
+        as device tensors (gb_sage_bulk_peer)."""
+        bounds, brp, bcol = peer
+        L = len(self.fanouts)
+        _lib.check(_lib.lib().gb_sage_bulk_peer(
+            self.dg.handle, self.k, _lib.ptr(d_bptr), _lib.ptr(d_bverts), self.r1_cap,
+            self.batch_size, L, self.h_fanouts.ctypes.data, int(seed), int(epoch),
+            int(batch_offset), self.c_layers, _lib.ptr(self.sizes), _lib.ptr(self.ws),
+            self.ws.numel(), int(bounds.numel() - 1), _lib.ptr(bounds), _lib.ptr(brp),
+            _lib.ptr(bcol), _lib.stream_ptr(stream)), "gb_sage_bulk_peer")
+
     def launch(self, d_bptr, d_bverts, seed, epoch, batch_offset, stream=None):
         """Enqueue the whole bulk (all layers) on `stream`; no host sync."""
         L = len(self.fanouts)

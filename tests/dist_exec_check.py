@@ -42,7 +42,7 @@ def main():
     for p, c in grids:
         grid = ProcessGrid(p, c)
         for mode, fetch in (("pfree", "rows"), ("stream", "rows"), ("pfree", "owner"),
-                            ("pfree", "p2p")):
+                            ("pfree", "p2p"), ("dedup", "split")):
             led = CommLedger(p)
             s = Sage15D(dg, grid, cfg.fanouts, cfg.batch_size, mode=mode, ledger=led, fetch=fetch)
             ep = sage_epoch_15d(s, cfg, batches, epoch=1, batch_offset=5)
