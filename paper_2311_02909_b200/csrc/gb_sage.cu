@@ -868,6 +868,104 @@ __global__ void k_sage_rank(const int64_t* __restrict__ F_ptr, const int64_t* __
   }
 }
 
+// Sector-granular extraction (the bulk path): batch rows of the bitmap are
+// padded to whole 8-word (32-B) sectors and the scan runs over sectors, so a
+// rank is one prefix load plus one sector load, and the scan is 8x shorter.
+struct SecPopF {
+  const uint4* sec;  // 2 uint4 per sector
+  __device__ int64_t operator()(int64_t i) const {
+    const uint4 a = sec[2 * i], b = sec[2 * i + 1];
+    return __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w) + __popc(b.x) + __popc(b.y) +
+           __popc(b.z) + __popc(b.w);
+  }
+};
+
+__device__ __forceinline__ int32_t sector_rank(const uint4 a, const uint4 b, int32_t bit) {
+  // set bits before position bit (0..255) of the sector
+  const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  const int wi = bit >> 5;
+  int32_t r = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t m = j < wi ? 0xffffffffu : (j == wi ? (1u << (bit & 31)) - 1u : 0u);
+    r += __popc(w[j] & m);
+  }
+  return r;
+}
+
+// acol[e] = spre[batch sector] + rank inside the sector (same contract as
+// k_sage_rank; compact_columns sparse.py:352-357 + block_diag :321-342)
+__global__ void k_sage_rank8(const int64_t* __restrict__ F_ptr, const int64_t* __restrict__ eoff,
+                             int64_t k, const int32_t* __restrict__ fcol,
+                             const uint4* __restrict__ sec, const int32_t* __restrict__ spre,
+                             int64_t nsec, int32_t* __restrict__ acol) {
+  constexpr int U = 4;
+  __shared__ int32_t s_eoff[kBrowSmem];
+  const bool sm = k + 1 <= kBrowSmem;
+  if (sm)
+    for (int i = threadIdx.x; i <= k; i += blockDim.x) s_eoff[i] = (int32_t)eoff[i];
+  __syncthreads();
+  const int32_t F = (int32_t)*F_ptr;
+  const int32_t K = (int32_t)k, NS = (int32_t)nsec;
+  auto eo = [&](int32_t i) { return sm ? s_eoff[i] : (int32_t)eoff[i]; };
+  for (int32_t e0 = blockIdx.x * blockDim.x * U + threadIdx.x; e0 < F;
+       e0 += gridDim.x * blockDim.x * U) {
+    int32_t v[U], si[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int32_t e = e0 + u * (int32_t)blockDim.x;
+      v[u] = e < F ? fcol[e] : 0;
+    }
+    int32_t a = 0, b = K;
+    while (b - a > 1) {
+      const int32_t mid = (a + b) >> 1;
+      if (eo(mid) <= e0) a = mid; else b = mid;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int32_t e = e0 + u * (int32_t)blockDim.x;
+      while (a + 1 < K && eo(a + 1) <= e) ++a;
+      si[u] = a * NS + (v[u] >> 8);
+    }
+    uint4 lo[U], hi[U];
+    int32_t sp[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (e0 + u * (int32_t)blockDim.x < F) {
+        lo[u] = sec[2 * si[u]]; hi[u] = sec[2 * si[u] + 1]; sp[u] = spre[si[u]];
+      }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int32_t e = e0 + u * (int32_t)blockDim.x;
+      if (e < F) acol[e] = sp[u] + sector_rank(lo[u], hi[u], v[u] & 255);
+    }
+  }
+}
+
+// col_vertices from the sector bitmap, thread per sector; clears the map
+__global__ void k_sage_enumerate8(int64_t NSt, int64_t nsec, uint4* __restrict__ sec,
+                                  const int32_t* __restrict__ spre, int32_t* __restrict__ colv) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < NSt;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 a = sec[2 * i], b = sec[2 * i + 1];
+    if (!(a.x | a.y | a.z | a.w | b.x | b.y | b.z | b.w)) continue;
+    const int64_t bt = i / nsec;
+    const int32_t vb = (int32_t)((i - bt * nsec) << 8);
+    const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    int32_t o = spre[i];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint32_t x = w[j];
+      while (x) {
+        colv[o++] = vb + 32 * j + __ffs(x) - 1;
+        x &= x - 1;
+      }
+    }
+    sec[2 * i] = make_uint4(0, 0, 0, 0);
+    sec[2 * i + 1] = make_uint4(0, 0, 0, 0);
+  }
+}
+
 // col_vertices: enumerate set bits in (batch, vertex) order; clears the map.
 __global__ void k_sage_enumerate(int64_t W, int64_t nwords, uint32_t* __restrict__ bitmap,
                                  const int32_t* __restrict__ wpre, int32_t* __restrict__ colv) {
@@ -998,7 +1096,7 @@ static SageWs sage_ws_layout(char* base, int64_t k, int64_t n, int64_t r_cap_max
                              int64_t f_cap_max) {
   SageWs w{};
   const int64_t nwords = (n + 31) / 32;
-  const int64_t W = k * nwords;
+  const int64_t W = k * ((nwords + 7) & ~(int64_t)7);  // sector-padded batch rows
   int64_t scan_n = 3 * r_cap_max > W ? 3 * r_cap_max : W;
   if (nwords > scan_n) scan_n = nwords;
   size_t off = 0;
@@ -1007,9 +1105,9 @@ static SageWs sage_ws_layout(char* base, int64_t k, int64_t n, int64_t r_cap_max
   w.deg = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
   w.gstart = (int64_t*)take(sizeof(int64_t) * (r_cap_max + 1));
   w.scan_ws = (int64_t*)take(sizeof(int64_t) * scan_workspace_elems<int64_t>(scan_n + 1));
-  w.bitmap = (uint32_t*)take(sizeof(uint32_t) * (W + 1));
+  w.bitmap = (uint32_t*)take(sizeof(uint32_t) * (W + 8));
   w.wpre = (int32_t*)take(sizeof(int32_t) * (W + 1));
-  w.bitmap2 = (uint32_t*)take(sizeof(uint32_t) * (W + 1));
+  w.bitmap2 = (uint32_t*)take(sizeof(uint32_t) * (W + 8));
   w.wpre2 = (int32_t*)take(sizeof(int32_t) * (W + 1));
   w.scan_ws2 = (int64_t*)take(sizeof(int64_t) * scan_workspace_elems<int64_t>(W + 1));
   w.d_W = (int64_t*)take(sizeof(int64_t));
@@ -1186,7 +1284,10 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     peer = PeerRows{peer_host->nblk, peer_host->bounds, peer_host->brp, peer_host->bcol};
   }
   const int64_t nwords = (g->n + 31) / 32;
-  const int64_t W = k * nwords;
+  // (batch, vertex) bitmaps: batch rows padded to whole 32-B sectors so the
+  // extraction ranks and enumerates a sector per load (k_sage_rank8)
+  const int64_t nw8 = (nwords + 7) & ~(int64_t)7;
+  const int64_t W = k * nw8, NS = W / 8;
   if (W >= ((int64_t)1 << 31)) {
     set_error("bulk: k * ceil(n / 32) = %lld (batch, vertex) words exceeds int32 indexing",
               (long long)W);
@@ -1212,9 +1313,9 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     }
     r_cap = f_cap;
   }
-  GB_CUDA(cudaMemsetAsync(ws.bitmap, 0, sizeof(uint32_t) * (W + 1), st));
-  GB_CUDA(cudaMemsetAsync(ws.bitmap2, 0, sizeof(uint32_t) * (W + 1), st));
-  k_set_i64<<<1, 1, 0, st>>>(ws.d_W, W);
+  GB_CUDA(cudaMemsetAsync(ws.bitmap, 0, sizeof(uint32_t) * (W + 8), st));
+  GB_CUDA(cudaMemsetAsync(ws.bitmap2, 0, sizeof(uint32_t) * (W + 8), st));
+  k_set_i64<<<1, 1, 0, st>>>(ws.d_W, NS);
   k_set_i64<<<1, 1, 0, st>>>(ws.d_nw, nwords);
   count_launches(2);
   // extraction of layer l (popcount scan, rank, enumerate) runs on a side
@@ -1255,7 +1356,7 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     A.rowv = rowv; A.deg = ws.deg; A.fptr = o.fptr; A.gstart = ws.gstart;
     A.brow = brow; A.k = k; A.s = s; A.stride = stride; A.batch_offset = batch_offset;
     A.seed = seed; A.epoch = epoch; A.depth = (uint64_t)d;
-    A.bitmap = bm; A.nwords = nwords; A.fcol = o.fcol; A.pidx = ws.pidx;
+    A.bitmap = bm; A.nwords = nw8; A.fcol = o.fcol; A.pidx = ws.pidx;
     const int pick_grid = grid_for(r_cap, kPickThreads, 64 * kNumSMs);
     if (ldedup) {
       rc = dedup_prepare(g, ws, R_ptr, rowv, o.fptr, brow, k, s, r_cap, nwords, peer, st);
@@ -1289,18 +1390,21 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     k_sage_eoff<<<grid_for(k + 1, 128, 64), 128, 0, st>>>(brow, k, o.fptr, o.eoff);
     GB_LAUNCH_CHECK("k_sage_eoff");
     stream_wait(xs, st);
-    rc = device_exclusive_scan<int64_t>(ws.d_W, W, PopF{bm}, wp, ws.scan_ws2, xs);
+    // wp = popcount prefix per 8-word sector
+    rc = device_exclusive_scan<int64_t>(ws.d_W, NS, SecPopF{(const uint4*)bm}, wp, ws.scan_ws2,
+                                        xs);
     if (rc) return rc;
     int64_t* sizes = d_sizes + 3 * l;
-    k_sage_layer_cols<<<grid_for(k + 1, 128, 64), 128, 0, xs>>>(brow, k, o.fptr, wp, nwords,
+    k_sage_layer_cols<<<grid_for(k + 1, 128, 64), 128, 0, xs>>>(brow, k, o.fptr, wp, nw8 / 8,
                                                                  o.coloff, sizes);
     GB_LAUNCH_CHECK("k_sage_layer_cols");
     const int64_t f_cap = r_cap * s;
-    k_sage_rank<<<grid_for(f_cap, 256, 16 * kNumSMs), 256, 0, xs>>>(
-        sizes + 1, o.eoff, k, o.fcol, bm, wp, nwords, o.acol);
-    GB_LAUNCH_CHECK("k_sage_rank");
-    k_sage_enumerate<<<grid_for(W, 256, 16 * kNumSMs), 256, 0, xs>>>(W, nwords, bm, wp, o.colv);
-    GB_LAUNCH_CHECK("k_sage_enumerate");
+    k_sage_rank8<<<grid_for(f_cap, 256, 16 * kNumSMs), 256, 0, xs>>>(
+        sizes + 1, o.eoff, k, o.fcol, (const uint4*)bm, wp, nw8 / 8, o.acol);
+    GB_LAUNCH_CHECK("k_sage_rank8");
+    k_sage_enumerate8<<<grid_for(NS, 256, 16 * kNumSMs), 256, 0, xs>>>(NS, nw8 / 8, (uint4*)bm,
+                                                                       wp, o.colv);
+    GB_LAUNCH_CHECK("k_sage_enumerate8");
     GB_CUDA(cudaEventRecord(ring_event(l), xs));
     count_launches(6);  // prep, sample, eoff, cols, rank, enumerate
     r_cap = f_cap;

@@ -172,3 +172,55 @@ def test_bulk_sampler_stream_matches_single_calls():
         assert len(got) == len(jobs)
         for g, w in zip(got, want[-len(jobs):]):
             assert O.compare_epochs(w, g) == []
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_sage_inclusion_two_thirds(mode):
+    """A degree-3 vertex with s = 2 keeps each neighbour with probability 2/3
+    (reference test_acceptance.py:80-84), over many minibatches of the
+    production Philox stream (distinct keys per batch)."""
+    from scipy import stats
+
+    gb = _pkg()
+    G = gb.Graph.from_edges(4, [0, 0, 0, 1, 2, 3], [1, 2, 3, 0, 0, 0])
+    trials = 30000
+    cfg = gb.SamplerConfig.sage(1, 1, (2,), bulk_count=trials, seed=123)
+    ep = gb.sample_epoch_bulk(G, cfg, [[0]] * trials, mode=mode)
+    a = ep.layers[0].to_arrays()
+    cat, off = a["sampv_cat"], a["sampv_off"]
+    assert np.all(np.diff(off) == 2)
+    counts = np.bincount(cat, minlength=4)[1:]
+    assert counts.sum() == 2 * trials
+    assert stats.chisquare(counts, f_exp=np.full(3, 2 * trials / 3)).pvalue > 0.01
+    pairs = np.bincount((cat.reshape(-1, 2) - 1) @ np.array([3, 1]), minlength=9)
+    assert stats.chisquare(pairs[[1, 2, 5]], f_exp=np.full(3, trials / 3)).pvalue > 0.01
+
+
+def test_sage_per_edge_inclusion_law():
+    """Per-edge inclusion min(s, d) / d for every row of a random graph
+    (SURVEY.md §8c statistical parity, SAGE): one-layer bulks over many
+    epochs, chi-square per vertex on the neighbour counts."""
+    from scipy import stats
+
+    gb = _pkg()
+    rng = np.random.default_rng(8)
+    n, rowptr, col = _rmat(9, 3000, seed=8)
+    G = _graph(n, rowptr, col)
+    deg = np.diff(rowptr)
+    verts = np.flatnonzero((deg > 6) & (deg <= 40))[:24]
+    s, epochs = 5, 400
+    cfg = gb.SamplerConfig.sage(1, len(verts), (s,), bulk_count=1, seed=3)
+    hits = {int(v): np.zeros(deg[v]) for v in verts}
+    for e in range(epochs):
+        ep = gb.sample_epoch_bulk(G, cfg, [verts], epoch=e, mode="dedup")
+        fr = ep.layers[0].frontier
+        fp, fc = fr.row_offsets, fr.col_indices
+        for i, v in enumerate(verts):
+            nb = col[rowptr[v]: rowptr[v + 1]]
+            got = fc[fp[i]: fp[i + 1]]
+            assert got.size == s
+            hits[int(v)][np.searchsorted(nb, got)] += 1
+    pv = [stats.chisquare(h, f_exp=np.full(h.size, epochs * s / h.size)).pvalue
+          for h in hits.values()]
+    # 24 independent tests at 1%: allow one rejection
+    assert sum(p < 0.01 for p in pv) <= 1
