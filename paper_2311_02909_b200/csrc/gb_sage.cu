@@ -703,6 +703,87 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
 }
 
+// Warp tier (rows of at most kHi entries, whole row per item): the warp's
+// buffer holds two rows at opposite ends when they fit, so the next item's
+// row is in flight (cp.async group) while the current one is served.
+__device__ __forceinline__ int dd_row_len(int64_t a0, int32_t d) {
+  return (int)(((a0 + d) - (a0 & ~3LL) + 3) & ~3LL);  // staged entries, 16-B granules
+}
+
+__device__ __forceinline__ void dd_stage_row(int32_t* dst, const int32_t* col, int64_t a0,
+                                             int32_t d, int lane) {
+  const int64_t al0 = a0 & ~3LL;
+  for (int64_t e = al0 + 4 * lane; e < a0 + d; e += 128) cp_async16(dst + (e - al0), col + e);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+__device__ void dd_serve_warp(const DdArgs& A, int32_t* buf, int B) {
+  // 32-bit indexing: frontier entries, grouped rows * s and k * nwords are
+  // all < 2^31 (host checks); p / take by a multiply-high (p < 2^16)
+  const int lane = lane_id(), s = A.s;
+  const uint32_t NW = (uint32_t)A.nwords;
+  const int64_t D = *A.D_ptr;
+  const int64_t it1 = A.ioff[D];
+  const int64_t step = grid_warps();
+  int64_t it = A.ioff[0] + global_warp();
+  if (it >= it1) return;
+  DdItem cur = A.items[it];
+  int cb = 0;  // buffer offset of the current row
+  dd_stage_row(buf, A.col, cur.a0, cur.d, lane);
+  DdItem nxt;
+  if (it + step < it1) nxt = A.items[it + step];
+  for (; it < it1; it += step) {
+    const bool has_nxt = it + step < it1;
+    DdItem nn;
+    if (it + 2 * step < it1) nn = A.items[it + 2 * step];
+    // prefetch the next row into the free end of the buffer when it fits
+    int nb = -1;
+    if (has_nxt) {
+      const int lc = dd_row_len(cur.a0, cur.d), ln = dd_row_len(nxt.a0, nxt.d);
+      nb = ln <= cb ? 0 : (cb + lc + ln <= B ? B - ln : -1);
+      if (nb >= 0) dd_stage_row(buf + nb, A.col, nxt.a0, nxt.d, lane);
+    }
+    const int32_t d = cur.d, take = min(d, s);
+    const bool all = take == d;
+    const int npairs = cur.nrows * take;
+    const uint32_t magic = 0xffffffffu / (uint32_t)take + 1u;  // ceil(2^32 / take), take > 1
+    const int32_t q0 = cur.q0;
+    auto meta = [&](int p, int32_t& idx, int32_t& fp, int32_t& bb, int32_t& t) {
+      const int i = take == 1 ? p : (int)__umulhi((uint32_t)p, magic);
+      t = p - i * take;
+      idx = all ? t : A.pidx[(q0 + i) * s + t];
+      const int2 bf = A.rbf[2 * (q0 + i) + 1];
+      bb = bf.x;
+      fp = bf.y;
+    };
+    int p = lane;
+    int32_t idx = 0, fp = 0, bb = 0, t = 0;
+    if (p < npairs) meta(p, idx, fp, bb, t);
+    if (nb >= 0) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+    const int32_t* row = buf + cb + (int32_t)(cur.a0 & 3);
+    while (p < npairs) {
+      const int pn = p + 32;
+      int32_t idx2 = 0, fp2 = 0, bb2 = 0, t2 = 0;
+      if (pn < npairs) meta(pn, idx2, fp2, bb2, t2);
+      const int32_t c = row[idx];
+      A.fcol[(uint32_t)(fp + t)] = c;
+      atomicOr(A.bitmap + ((uint32_t)bb * NW + ((uint32_t)c >> 5)), 1u << (c & 31));
+      p = pn; idx = idx2; fp = fp2; bb = bb2; t = t2;
+    }
+    __syncwarp();  // the current row's space is free
+    if (has_nxt && nb < 0) {
+      nb = 0;
+      dd_stage_row(buf, A.col, nxt.a0, nxt.d, lane);
+    }
+    cur = nxt;
+    cb = nb;
+    nxt = nn;
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
 // Q^l A for the distinct rows: per work item, A row v staged in shared
 // memory (16-B cp.async; buf[e - (e0 & ~3)]) — the P row on chip once —
 // then every pick of the item's frontier rows is served from it: frontier
@@ -712,6 +793,10 @@ template <int TIER>
 __global__ void __launch_bounds__(DdTier<TIER>::kThreads) k_dd_serve(DdArgs A) {
   constexpr bool CTA = !DdTier<TIER>::kWarp;
   extern __shared__ __align__(16) int32_t sbuf[];
+  if constexpr (!CTA) {
+    dd_serve_warp(A, sbuf + (threadIdx.x >> 5) * (A.chunk + 8), A.chunk + 8);
+    return;
+  }
   const int chunk = A.chunk, s = A.s;
   const int tid = CTA ? threadIdx.x : lane_id();
   const int nthr = CTA ? blockDim.x : 32;
