@@ -703,85 +703,106 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
 }
 
-// Warp tier (rows of at most kHi entries, whole row per item): the warp's
-// buffer holds two rows at opposite ends when they fit, so the next item's
-// row is in flight (cp.async group) while the current one is served.
+// staged entries of an A row (16-B granules from the aligned start)
 __device__ __forceinline__ int dd_row_len(int64_t a0, int32_t d) {
-  return (int)(((a0 + d) - (a0 & ~3LL) + 3) & ~3LL);  // staged entries, 16-B granules
+  return (int)(((a0 + d) - (a0 & ~3LL) + 3) & ~3LL);
 }
 
-__device__ __forceinline__ void dd_stage_row(int32_t* dst, const int32_t* col, int64_t a0,
-                                             int32_t d, int lane) {
-  const int64_t al0 = a0 & ~3LL;
-  for (int64_t e = al0 + 4 * lane; e < a0 + d; e += 128) cp_async16(dst + (e - al0), col + e);
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
+// Warp tier, batched: a warp takes 32 consecutive work items (one
+// descriptor per lane), packs as many of their rows as fit into its buffer
+// (one cp.async group), and serves all their picks lane-parallel — pair p
+// of the group finds its item by a search over the per-warp group table.
+// Per-item latency chains and instruction overhead are amortised over the
+// group (layer-3 tier-0 items carry ~12 picks each).
+constexpr int kGrpInts = 6 * 33;
 
-__device__ void dd_serve_warp(const DdArgs& A, int32_t* buf, int B) {
+__device__ void dd_serve_warp(const DdArgs& A, int32_t* buf, int B, int32_t* gi) {
+  int32_t* g_pst = gi;            // pair start per item (+ sentinel)
+  int32_t* g_rof = gi + 33;       // row base in buf (16-B alignment shift included)
+  int32_t* g_q0 = gi + 66;        // first grouped row
+  int32_t* g_tk = gi + 99;        // take, negated when take == d (every entry)
+  uint32_t* g_mg = (uint32_t*)(gi + 132);  // ceil(2^32 / take)
   // 32-bit indexing: frontier entries, grouped rows * s and k * nwords are
-  // all < 2^31 (host checks); p / take by a multiply-high (p < 2^16)
+  // all < 2^31 (host checks)
   const int lane = lane_id(), s = A.s;
   const uint32_t NW = (uint32_t)A.nwords;
   const int64_t D = *A.D_ptr;
-  const int64_t it1 = A.ioff[D];
-  const int64_t step = grid_warps();
-  int64_t it = A.ioff[0] + global_warp();
-  if (it >= it1) return;
-  DdItem cur = A.items[it];
-  int cb = 0;  // buffer offset of the current row
-  dd_stage_row(buf, A.col, cur.a0, cur.d, lane);
-  DdItem nxt;
-  if (it + step < it1) nxt = A.items[it + step];
-  for (; it < it1; it += step) {
-    const bool has_nxt = it + step < it1;
-    DdItem nn;
-    if (it + 2 * step < it1) nn = A.items[it + 2 * step];
-    // prefetch the next row into the free end of the buffer when it fits
-    int nb = -1;
-    if (has_nxt) {
-      const int lc = dd_row_len(cur.a0, cur.d), ln = dd_row_len(nxt.a0, nxt.d);
-      nb = ln <= cb ? 0 : (cb + lc + ln <= B ? B - ln : -1);
-      if (nb >= 0) dd_stage_row(buf + nb, A.col, nxt.a0, nxt.d, lane);
+  const int64_t i0 = A.ioff[0], it1 = A.ioff[D];
+  const int64_t nblk = (it1 - i0 + 31) / 32;
+  for (int64_t blk = global_warp(); blk < nblk; blk += grid_warps()) {
+    const int64_t it = i0 + blk * 32 + lane;
+    const int nitems = (int)min((int64_t)32, it1 - (i0 + blk * 32));
+    DdItem c{};
+    const bool valid = lane < nitems;
+    if (valid) c = A.items[it];
+    const int len = valid ? dd_row_len(c.a0, c.d) : 0;
+    const int take = valid ? min(c.d, s) : 0;
+    const int np = valid ? c.nrows * take : 0;
+    for (int j0 = 0; j0 < nitems;) {
+      // sub-group [j0, j1): rows packed while they fit (always at least one)
+      const int lz = lane >= j0 ? len : 0;
+      const int incl = warp_incl_scan(lz);
+      const unsigned fit = __ballot_sync(0xffffffffu, lane >= j0 && lane < nitems && incl <= B);
+      const int j1 = fit ? 32 - __clz(fit) : j0 + 1;
+      const bool in = lane >= j0 && lane < j1;
+      const int pz = in ? np : 0;
+      const int pinc = warp_incl_scan(pz);
+      const int P = __shfl_sync(0xffffffffu, pinc, j1 - 1);
+      if (in) {
+        const int j = lane - j0;
+        g_pst[j] = pinc - pz;
+        g_rof[j] = incl - lz + (int)(c.a0 & 3);
+        g_q0[j] = c.q0;
+        g_tk[j] = take == c.d ? -take : take;
+        g_mg[j] = 0xffffffffu / (uint32_t)take + 1u;
+      }
+      if (lane == 0) g_pst[j1 - j0] = P;
+      for (int j = j0; j < j1; ++j) {
+        const int64_t a0 = __shfl_sync(0xffffffffu, c.a0, j);
+        const int32_t d = __shfl_sync(0xffffffffu, c.d, j);
+        const int o = __shfl_sync(0xffffffffu, incl - lz, j);
+        const int64_t al0 = a0 & ~3LL;
+        for (int64_t e = al0 + 4 * lane; e < a0 + d; e += 128)
+          cp_async16(buf + o + (int)(e - al0), A.col + e);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      __syncwarp();
+      const int ng = j1 - j0;
+      auto meta = [&](int p, int32_t& idx, int32_t& fp, int32_t& bb, int32_t& t, int32_t& ro) {
+        int lo = 0, hi = ng;
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (g_pst[mid] <= p) lo = mid; else hi = mid;
+        }
+        const int tk = g_tk[lo], tkn = tk < 0 ? -tk : tk;
+        const int r = p - g_pst[lo];
+        const int i = tkn == 1 ? r : (int)__umulhi((uint32_t)r, g_mg[lo]);
+        t = r - i * tkn;
+        const int q = g_q0[lo] + i;
+        idx = tk < 0 ? t : A.pidx[q * s + t];
+        const int2 bf = A.rbf[2 * q + 1];
+        bb = bf.x;
+        fp = bf.y;
+        ro = g_rof[lo];
+      };
+      int32_t idx = 0, fp = 0, bb = 0, t = 0, ro = 0;
+      if (lane < P) meta(lane, idx, fp, bb, t, ro);
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      __syncwarp();
+      for (int p0 = 0; p0 < P; p0 += 32) {
+        int32_t idx2 = 0, fp2 = 0, bb2 = 0, t2 = 0, ro2 = 0;
+        if (p0 + 32 + lane < P) meta(p0 + 32 + lane, idx2, fp2, bb2, t2, ro2);
+        if (p0 + lane < P) {
+          const int32_t cv = buf[ro + idx];
+          A.fcol[(uint32_t)(fp + t)] = cv;
+          atomicOr(A.bitmap + ((uint32_t)bb * NW + ((uint32_t)cv >> 5)), 1u << (cv & 31));
+        }
+        idx = idx2; fp = fp2; bb = bb2; t = t2; ro = ro2;
+      }
+      __syncwarp();  // buffer and group table free
+      j0 = j1;
     }
-    const int32_t d = cur.d, take = min(d, s);
-    const bool all = take == d;
-    const int npairs = cur.nrows * take;
-    const uint32_t magic = 0xffffffffu / (uint32_t)take + 1u;  // ceil(2^32 / take), take > 1
-    const int32_t q0 = cur.q0;
-    auto meta = [&](int p, int32_t& idx, int32_t& fp, int32_t& bb, int32_t& t) {
-      const int i = take == 1 ? p : (int)__umulhi((uint32_t)p, magic);
-      t = p - i * take;
-      idx = all ? t : A.pidx[(q0 + i) * s + t];
-      const int2 bf = A.rbf[2 * (q0 + i) + 1];
-      bb = bf.x;
-      fp = bf.y;
-    };
-    int p = lane;
-    int32_t idx = 0, fp = 0, bb = 0, t = 0;
-    if (p < npairs) meta(p, idx, fp, bb, t);
-    if (nb >= 0) asm volatile("cp.async.wait_group 1;" ::: "memory");
-    else asm volatile("cp.async.wait_group 0;" ::: "memory");
-    __syncwarp();
-    const int32_t* row = buf + cb + (int32_t)(cur.a0 & 3);
-    while (p < npairs) {
-      const int pn = p + 32;
-      int32_t idx2 = 0, fp2 = 0, bb2 = 0, t2 = 0;
-      if (pn < npairs) meta(pn, idx2, fp2, bb2, t2);
-      const int32_t c = row[idx];
-      A.fcol[(uint32_t)(fp + t)] = c;
-      atomicOr(A.bitmap + ((uint32_t)bb * NW + ((uint32_t)c >> 5)), 1u << (c & 31));
-      p = pn; idx = idx2; fp = fp2; bb = bb2; t = t2;
-    }
-    __syncwarp();  // the current row's space is free
-    if (has_nxt && nb < 0) {
-      nb = 0;
-      dd_stage_row(buf, A.col, nxt.a0, nxt.d, lane);
-    }
-    cur = nxt;
-    cb = nb;
-    nxt = nn;
   }
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 // Q^l A for the distinct rows: per work item, A row v staged in shared
@@ -794,7 +815,9 @@ __global__ void __launch_bounds__(DdTier<TIER>::kThreads) k_dd_serve(DdArgs A) {
   constexpr bool CTA = !DdTier<TIER>::kWarp;
   extern __shared__ __align__(16) int32_t sbuf[];
   if constexpr (!CTA) {
-    dd_serve_warp(A, sbuf + (threadIdx.x >> 5) * (A.chunk + 8), A.chunk + 8);
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    dd_serve_warp(A, sbuf + w * (A.chunk + 8), A.chunk + 8,
+                  sbuf + nw * (A.chunk + 8) + w * kGrpInts);
     return;
   }
   const int chunk = A.chunk, s = A.s;
@@ -1281,7 +1304,8 @@ static int launch_serve(DdArgs A, cudaStream_t st) {
   }
   // chunk: the whole row for tiers 0 / 1, all of shared memory for hubs
   A.chunk = T == 2 ? ((max_smem / 4 - 8) & ~3) : Tr::kHi;
-  const size_t smem = sizeof(int32_t) * (A.chunk + 8) * (Tr::kWarp ? Tr::kThreads / 32 : 1);
+  const size_t smem = sizeof(int32_t) * (A.chunk + 8 + (Tr::kWarp ? kGrpInts : 0)) *
+                      (Tr::kWarp ? Tr::kThreads / 32 : 1);
   static int grid = 0;  // smem is fixed per tier
   if (!grid) {
     int occ = 0, sms = 0;
