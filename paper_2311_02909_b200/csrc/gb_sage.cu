@@ -200,6 +200,14 @@ __device__ __forceinline__ int32_t vrank(const uint32_t* vbits, const int32_t* v
   return vpre[v >> 5] + __popc(vbits[v >> 5] & ((1u << (v & 31)) - 1u));
 }
 
+// (batch, vertex) bitmap of the bulk: each 32-B sector holds 7 bit words
+// (224 vertices) and, after the extraction scan, their batch-row prefix in
+// word 7 — a rank is one sector load.  Word of vertex v in a batch row:
+__device__ __forceinline__ uint32_t pk_word(int32_t v) {
+  const uint32_t w = (uint32_t)v >> 5;
+  return w + w / 7u;
+}
+
 constexpr int kPickThreads = 128;
 constexpr int kStreamThreads = 256;
 constexpr int kRowCost = 48;       // merge-path weight of one row (in entries)
@@ -374,7 +382,7 @@ __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
         uint32_t* bm = A.bitmap + bb * A.nwords;
 #pragma unroll
         for (int z = 0; z < MAXF; ++z)
-          if (z < take) atomicOr(bm + (cv[z] >> 5), 1u << (cv[z] & 31));
+          if (z < take) atomicOr(bm + pk_word(cv[z]), 1u << (cv[z] & 31));
       }
     } else if (OUT == 2) {
 #pragma unroll
@@ -497,7 +505,7 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k_sage_stream(SageArgs A,
       }
       if (have) {
         A.fcol[fp_i + lane] = c;
-        if (A.bitmap) atomicOr(&A.bitmap[b_i * A.nwords + (c >> 5)], 1u << (c & 31));
+        if (A.bitmap) atomicOr(&A.bitmap[b_i * A.nwords + pk_word(c)], 1u << (c & 31));
       }
     }
   }
@@ -795,7 +803,7 @@ __device__ void dd_serve_warp(const DdArgs& A, int32_t* buf, int B, int32_t* gi)
         if (p0 + lane < P) {
           const int32_t cv = buf[ro + idx];
           A.fcol[(uint32_t)(fp + t)] = cv;
-          atomicOr(A.bitmap + ((uint32_t)bb * NW + ((uint32_t)cv >> 5)), 1u << (cv & 31));
+          atomicOr(A.bitmap + ((uint32_t)bb * NW + pk_word(cv)), 1u << (cv & 31));
         }
         idx = idx2; fp = fp2; bb = bb2; t = t2; ro = ro2;
       }
@@ -873,7 +881,7 @@ __global__ void __launch_bounds__(DdTier<TIER>::kThreads) k_dd_serve(DdArgs A) {
         if (idx >= c0 && idx < c1) {
           const int32_t c = buf[idx + sh];
           A.fcol[fp + t] = c;
-          atomicOr(A.bitmap + (int64_t)bb * A.nwords + (c >> 5), 1u << (c & 31));
+          atomicOr(A.bitmap + (int64_t)bb * A.nwords + pk_word(c), 1u << (c & 31));
         }
         p = pn; idx = idx2; fp = fp2; bb = bb2; t = t2;
       }
@@ -976,37 +984,24 @@ __global__ void k_sage_rank(const int64_t* __restrict__ F_ptr, const int64_t* __
   }
 }
 
-// Sector-granular extraction (the bulk path): batch rows of the bitmap are
-// padded to whole 8-word (32-B) sectors and the scan runs over sectors, so a
-// rank is one prefix load plus one sector load, and the scan is 8x shorter.
+// Sector-granular extraction (the bulk path, pk_word layout): the scan
+// runs over sectors and writes each sector's prefix into its word 7, so a
+// rank and an enumeration step are one 32-B sector load each.
 struct SecPopF {
   const uint4* sec;  // 2 uint4 per sector
   __device__ int64_t operator()(int64_t i) const {
     const uint4 a = sec[2 * i], b = sec[2 * i + 1];
     return __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w) + __popc(b.x) + __popc(b.y) +
-           __popc(b.z) + __popc(b.w);
+           __popc(b.z);
   }
 };
 
-__device__ __forceinline__ int32_t sector_rank(const uint4 a, const uint4 b, int32_t bit) {
-  // set bits before position bit (0..255) of the sector
-  const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-  const int wi = bit >> 5;
-  int32_t r = 0;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const uint32_t m = j < wi ? 0xffffffffu : (j == wi ? (1u << (bit & 31)) - 1u : 0u);
-    r += __popc(w[j] & m);
-  }
-  return r;
-}
-
-// acol[e] = spre[batch sector] + rank inside the sector (same contract as
+// acol[e] = sector prefix + rank inside the sector (same contract as
 // k_sage_rank; compact_columns sparse.py:352-357 + block_diag :321-342)
 __global__ void k_sage_rank8(const int64_t* __restrict__ F_ptr, const int64_t* __restrict__ eoff,
                              int64_t k, const int32_t* __restrict__ fcol,
-                             const uint4* __restrict__ sec, const int32_t* __restrict__ spre,
-                             int64_t nsec, int32_t* __restrict__ acol) {
+                             const uint4* __restrict__ sec, int64_t nsec,
+                             int32_t* __restrict__ acol) {
   constexpr int U = 4;
   __shared__ int32_t s_eoff[kBrowSmem];
   const bool sm = k + 1 <= kBrowSmem;
@@ -1018,7 +1013,7 @@ __global__ void k_sage_rank8(const int64_t* __restrict__ F_ptr, const int64_t* _
   auto eo = [&](int32_t i) { return sm ? s_eoff[i] : (int32_t)eoff[i]; };
   for (int32_t e0 = blockIdx.x * blockDim.x * U + threadIdx.x; e0 < F;
        e0 += gridDim.x * blockDim.x * U) {
-    int32_t v[U], si[U];
+    int32_t v[U], si[U], wi[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int32_t e = e0 + u * (int32_t)blockDim.x;
@@ -1033,36 +1028,46 @@ __global__ void k_sage_rank8(const int64_t* __restrict__ F_ptr, const int64_t* _
     for (int u = 0; u < U; ++u) {
       const int32_t e = e0 + u * (int32_t)blockDim.x;
       while (a + 1 < K && eo(a + 1) <= e) ++a;
-      si[u] = a * NS + (v[u] >> 8);
+      const uint32_t w = (uint32_t)v[u] >> 5, q = w / 7u;
+      si[u] = a * NS + (int32_t)q;
+      wi[u] = (int32_t)(w - 7u * q);
     }
     uint4 lo[U], hi[U];
-    int32_t sp[U];
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (e0 + u * (int32_t)blockDim.x < F) {
-        lo[u] = sec[2 * si[u]]; hi[u] = sec[2 * si[u] + 1]; sp[u] = spre[si[u]];
-      }
+      if (e0 + u * (int32_t)blockDim.x < F) { lo[u] = sec[2 * si[u]]; hi[u] = sec[2 * si[u] + 1]; }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int32_t e = e0 + u * (int32_t)blockDim.x;
-      if (e < F) acol[e] = sp[u] + sector_rank(lo[u], hi[u], v[u] & 255);
+      if (e < F) {
+        const uint32_t x[7] = {lo[u].x, lo[u].y, lo[u].z, lo[u].w, hi[u].x, hi[u].y, hi[u].z};
+        int32_t r = (int32_t)hi[u].w;
+#pragma unroll
+        for (int j = 0; j < 7; ++j) {
+          const uint32_t m = j < wi[u] ? 0xffffffffu
+                                       : (j == wi[u] ? (1u << (v[u] & 31)) - 1u : 0u);
+          r += __popc(x[j] & m);
+        }
+        acol[e] = r;
+      }
     }
   }
 }
 
-// col_vertices from the sector bitmap, thread per sector; clears the map
+// col_vertices from the sector bitmap, thread per sector; clears the bits
+// (word 7 is rewritten by the next scan)
 __global__ void k_sage_enumerate8(int64_t NSt, int64_t nsec, uint4* __restrict__ sec,
-                                  const int32_t* __restrict__ spre, int32_t* __restrict__ colv) {
+                                  int32_t* __restrict__ colv) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < NSt;
        i += (int64_t)gridDim.x * blockDim.x) {
     const uint4 a = sec[2 * i], b = sec[2 * i + 1];
-    if (!(a.x | a.y | a.z | a.w | b.x | b.y | b.z | b.w)) continue;
+    if (!(a.x | a.y | a.z | a.w | b.x | b.y | b.z)) continue;
     const int64_t bt = i / nsec;
-    const int32_t vb = (int32_t)((i - bt * nsec) << 8);
-    const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-    int32_t o = spre[i];
+    const int32_t vb = (int32_t)((i - bt * nsec) * 224);
+    const uint32_t w[7] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z};
+    int32_t o = (int32_t)b.w;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < 7; ++j) {
       uint32_t x = w[j];
       while (x) {
         colv[o++] = vb + 32 * j + __ffs(x) - 1;
@@ -1204,7 +1209,7 @@ static SageWs sage_ws_layout(char* base, int64_t k, int64_t n, int64_t r_cap_max
                              int64_t f_cap_max) {
   SageWs w{};
   const int64_t nwords = (n + 31) / 32;
-  const int64_t W = k * ((nwords + 7) & ~(int64_t)7);  // sector-padded batch rows
+  const int64_t W = k * 8 * ((nwords + 6) / 7);  // pk_word sectors per batch row
   int64_t scan_n = 3 * r_cap_max > W ? 3 * r_cap_max : W;
   if (nwords > scan_n) scan_n = nwords;
   size_t off = 0;
@@ -1393,9 +1398,8 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     peer = PeerRows{peer_host->nblk, peer_host->bounds, peer_host->brp, peer_host->bcol};
   }
   const int64_t nwords = (g->n + 31) / 32;
-  // (batch, vertex) bitmaps: batch rows padded to whole 32-B sectors so the
-  // extraction ranks and enumerates a sector per load (k_sage_rank8)
-  const int64_t nw8 = (nwords + 7) & ~(int64_t)7;
+  // (batch, vertex) bitmaps in pk_word sectors (7 bit words + prefix word)
+  const int64_t nw8 = 8 * ((nwords + 6) / 7);
   const int64_t W = k * nw8, NS = W / 8;
   if (W >= ((int64_t)1 << 31)) {
     set_error("bulk: k * ceil(n / 32) = %lld (batch, vertex) words exceeds int32 indexing",
@@ -1446,7 +1450,6 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     const int64_t* R_ptr = brow + k;
     const int32_t s = (int32_t)fanouts[l];
     uint32_t* bm = (l & 1) ? ws.bitmap2 : ws.bitmap;
-    int32_t* wp = (l & 1) ? ws.wpre2 : ws.wpre;
     if (l >= 2) GB_CUDA(cudaStreamWaitEvent(st, ring_event(l - 2), 0));
     if (ldedup) GB_CUDA(cudaMemsetAsync(ws.vbits, 0, sizeof(uint32_t) * (nwords + 1), st));
     k_sage_prep<<<grid_for(r_cap, 256, 16 * kNumSMs), 256, 0, st>>>(R_ptr, rowv, g->rowptr, ws.deg,
@@ -1499,20 +1502,21 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     k_sage_eoff<<<grid_for(k + 1, 128, 64), 128, 0, st>>>(brow, k, o.fptr, o.eoff);
     GB_LAUNCH_CHECK("k_sage_eoff");
     stream_wait(xs, st);
-    // wp = popcount prefix per 8-word sector
-    rc = device_exclusive_scan<int64_t>(ws.d_W, NS, SecPopF{(const uint4*)bm}, wp, ws.scan_ws2,
-                                        xs);
+    // popcount prefix of each sector into its word 7 (total after the last)
+    int32_t* spre = (int32_t*)bm + 7;
+    rc = device_exclusive_scan<int64_t, 8>(ws.d_W, NS, SecPopF{(const uint4*)bm}, spre,
+                                           ws.scan_ws2, xs);
     if (rc) return rc;
     int64_t* sizes = d_sizes + 3 * l;
-    k_sage_layer_cols<<<grid_for(k + 1, 128, 64), 128, 0, xs>>>(brow, k, o.fptr, wp, nw8 / 8,
+    k_sage_layer_cols<<<grid_for(k + 1, 128, 64), 128, 0, xs>>>(brow, k, o.fptr, spre, nw8,
                                                                  o.coloff, sizes);
     GB_LAUNCH_CHECK("k_sage_layer_cols");
     const int64_t f_cap = r_cap * s;
     k_sage_rank8<<<grid_for(f_cap, 256, 16 * kNumSMs), 256, 0, xs>>>(
-        sizes + 1, o.eoff, k, o.fcol, (const uint4*)bm, wp, nw8 / 8, o.acol);
+        sizes + 1, o.eoff, k, o.fcol, (const uint4*)bm, nw8 / 8, o.acol);
     GB_LAUNCH_CHECK("k_sage_rank8");
     k_sage_enumerate8<<<grid_for(NS, 256, 16 * kNumSMs), 256, 0, xs>>>(NS, nw8 / 8, (uint4*)bm,
-                                                                       wp, o.colv);
+                                                                       o.colv);
     GB_LAUNCH_CHECK("k_sage_enumerate8");
     GB_CUDA(cudaEventRecord(ring_event(l), xs));
     count_launches(6);  // prep, sample, eoff, cols, rank, enumerate

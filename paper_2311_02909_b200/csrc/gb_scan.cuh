@@ -53,7 +53,7 @@ __device__ __forceinline__ void st_store(unsigned long long* p, unsigned long lo
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-template <typename OutT, typename F>
+template <typename OutT, typename F, int STRIDE = 1>
 __global__ void __launch_bounds__(kScanThreads) scan_single_pass(const int64_t* n_ptr, F f,
                                                                  OutT* out,
                                                                  unsigned long long* st) {
@@ -107,10 +107,10 @@ __global__ void __launch_bounds__(kScanThreads) scan_single_pass(const int64_t* 
     ex += s_prefix;
 #pragma unroll
     for (int i = 0; i < kScanItems; ++i) {
-      if (base + i < n) out[base + i] = (OutT)ex;
+      if (base + i < n) out[(base + i) * STRIDE] = (OutT)ex;
       ex += vals[i];
     }
-    if (tile == ntiles - 1 && threadIdx.x == 0) out[n] = (OutT)(s_prefix + total);
+    if (tile == ntiles - 1 && threadIdx.x == 0) out[n * STRIDE] = (OutT)(s_prefix + total);
     __syncthreads();  // s_tile / s_prefix reuse
   }
 }
@@ -122,14 +122,16 @@ inline size_t scan_workspace_elems(int64_t max_n) {
 }
 
 // out[0..n) = exclusive prefix of f(0..n), out[n] = total; n = *d_n <= max_n.
-template <typename T, typename OutT, typename F>
+// STRIDE > 1: element i lands at out[i * STRIDE] (prefixes interleaved with
+// the data they count).
+template <typename T, int STRIDE = 1, typename OutT, typename F>
 inline int device_exclusive_scan(const int64_t* d_n, int64_t max_n, F f, OutT* out, T* ws,
                                  cudaStream_t st) {
   static_assert(sizeof(T) == 8, "64-bit scan workspace");
   const int64_t max_tiles = (max_n + kScanTile - 1) / kScanTile;
   const int grid = (int)(max_tiles < 8 * kNumSMs ? (max_tiles > 0 ? max_tiles : 1) : 8 * kNumSMs);
   GB_CUDA(cudaMemsetAsync(ws, 0, sizeof(unsigned long long) * (max_tiles + 1), st));
-  scan_single_pass<OutT, F><<<grid, kScanThreads, 0, st>>>(d_n, f, out,
+  scan_single_pass<OutT, F, STRIDE><<<grid, kScanThreads, 0, st>>>(d_n, f, out,
                                                            (unsigned long long*)ws);
   GB_LAUNCH_CHECK("device_exclusive_scan");
   count_launches(1);
