@@ -538,18 +538,14 @@ __global__ void k_dd_list(int64_t nwords, const uint32_t* __restrict__ vbits,
   }
 }
 
-// rows per distinct vertex (one atomic per vertex per warp: hub groups are hot)
+// rows per distinct vertex
 __global__ void k_dd_rcount(const int64_t* __restrict__ R_ptr, const int32_t* __restrict__ rowv,
                             const int32_t* __restrict__ deg, const uint32_t* __restrict__ vbits,
                             const int32_t* __restrict__ vpre, int32_t* __restrict__ gcnt) {
   const int64_t R = *R_ptr;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
        r += (int64_t)gridDim.x * blockDim.x) {
-    if (deg[r] > 0) {
-      const int32_t g = vrank(vbits, vpre, rowv[r]);
-      const unsigned peers = __match_any_sync(__activemask(), g);
-      if (lane_id() == __ffs(peers) - 1) atomicAdd(gcnt + g, __popc(peers));
-    }
+    if (deg[r] > 0) atomicAdd(gcnt + vrank(vbits, vpre, rowv[r]), 1);
   }
 }
 
@@ -573,12 +569,7 @@ __global__ void k_dd_rows(const int64_t* __restrict__ R_ptr, const int32_t* __re
     const int32_t dr = deg[r];
     if (dr > 0) {
       const int32_t g = vrank(vbits, vpre, rowv[r]);
-      const unsigned peers = __match_any_sync(__activemask(), g);
-      const int lane = lane_id(), leader = __ffs(peers) - 1;
-      int32_t cur = 0;
-      if (lane == leader) cur = atomicAdd(gcur + g, __popc(peers));
-      cur = __shfl_sync(peers, cur, leader);
-      const int64_t pos = roff[g] + cur + __popc(peers & ((1u << lane) - 1u));
+      const int64_t pos = roff[g] + atomicAdd(gcur + g, 1);
       rrec[pos] = make_int4((int32_t)r, dr, (int32_t)batch_of(s_brow, brow, k, r),
                             (int32_t)fptr[r]);
     }
