@@ -723,6 +723,10 @@ def main():
         import torch
         import torch.distributed as dist
 
+        # the NCCL version banner (NCCL_DEBUG=VERSION) would land on stdout
+        # ahead of the one JSON line
+        if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+            os.environ["NCCL_DEBUG"] = "WARN"
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
