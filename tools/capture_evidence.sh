@@ -13,15 +13,18 @@ python tools/profile_bulk.py --sampler ladies > $O/ev_pb_ladies.log 2>&1 || exit
 # launch lists (one warm bulk + one measured bulk)
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/ev_launches_dedup.csv \
     python tools/profile_bulk.py --mode dedup --warm 1 > $O/ev_ncu_a.log 2>&1
+ncu --cache-control none --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file $O/ev_launches_dedup_warm.csv python tools/profile_bulk.py --mode dedup --warm 1 \
+    > $O/ev_ncu_a2.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/ev_launches_ladies.csv \
     python tools/profile_bulk.py --sampler ladies --warm 1 > $O/ev_ncu_b.log 2>&1
-# DRAM traffic of every serve / pick launch of the second bulk
+# DRAM traffic of every stream / serve / pick launch of the second bulk
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
-    --csv -k "regex:k_dd_serve|k_sage_pick" --launch-skip 12 --launch-count 12 \
+    --csv -k "regex:k_dd_serve|k_sage_pick|k_sage_stream" --launch-skip 10 --launch-count 10 \
     --log-file $O/ev_traffic_dedup.csv python tools/profile_bulk.py --mode dedup --warm 1 > $O/ev_ncu_c.log 2>&1
 # full captures: layer 3 of the dedup bulk, layer 2 of the LADIES bulk
 ncu --set full --clock-control none --import-source on \
-    -k "regex:k_dd_serve|k_sage_pick|k_sage_rank|k_dd_rows" --launch-skip 30 --launch-count 6 \
+    -k "regex:k_dd_serve|k_sage_pick|k_sage_rank8|k_dd_rows" --launch-skip 22 --launch-count 6 \
     -o $O/ev_dedup_full python tools/profile_bulk.py --mode dedup --warm 1 > $O/ev_ncu_d.log 2>&1
 ncu --set full --clock-control none --import-source on -k "regex:k_lad_tile$|k_lad_extract" \
     --launch-skip 8 --launch-count 2 -o $O/ev_ladies_full \

@@ -1,0 +1,58 @@
+"""Refresh profiles/ncu_traffic.json (k_dd_serve, k_sage_pick<2>) from an
+ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum CSV of the dedup
+bulk's stream / serve / pick launches (tools/capture_evidence.sh, one bulk:
+layer 1 streams its rows, layers 2 and 3 run the three serve tiers).
+
+usage: traffic_json.py TRAFFIC.csv [SOURCE_NOTE]"""
+import collections
+import csv
+import json
+import os
+import sys
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def main():
+    path = sys.argv[1]
+    note = sys.argv[2] if len(sys.argv) > 2 else os.path.basename(path)
+    rows = [r for r in csv.reader(open(path)) if r]
+    i = [k for k, r in enumerate(rows) if r[0] == "ID"][0]
+    h = rows[i]
+    kn, mn, mv, idc = (h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"),
+                       h.index("ID"))
+    per = collections.OrderedDict()  # launch id -> (name, bytes)
+    for r in rows[i + 1:]:
+        if r[mn] not in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            continue
+        name = r[kn].split("(")[0].replace("void ", "").replace("gb::", "")
+        b = float(r[mv].replace(",", ""))
+        nm, acc = per.get(r[idc], (name, 0.0))
+        per[r[idc]] = (nm, acc + b)
+    serve, pick = [], []
+    l1 = 0.0
+    cur = None
+    for name, b in per.values():
+        if name.startswith("k_sage_stream"):
+            l1 = b  # layer 1 of the dedup bulk streams its (all distinct) rows
+        elif name.startswith("k_sage_pick<2"):
+            pick.append(b)
+            cur = 0.0
+            serve.append(cur)
+        elif name.startswith("k_dd_serve") and serve:
+            serve[-1] += b
+    out_path = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    d = json.load(open(out_path))
+    # the bench's dedup roofline covers layer 1's k_sage_stream + the serves
+    d["k_dd_serve"] = {"per_layer_bytes": [l1] + serve, "bulk_bytes": l1 + sum(serve),
+                       "source": note + " (ncu --metrics dram__bytes_read.sum,"
+                       "dram__bytes_write.sum; layer 1: k_sage_stream, layers 2-3: the 3 "
+                       "serve tier launches)"}
+    d["k_sage_pick<2>"] = {"per_layer_bytes": [0.0] + pick, "bulk_bytes": sum(pick),
+                           "source": "same capture"}
+    json.dump(d, open(out_path, "w"), indent=1)
+    print(json.dumps({k: d[k] for k in ("k_dd_serve", "k_sage_pick<2>")}, indent=1))
+
+
+if __name__ == "__main__":
+    main()
