@@ -391,6 +391,74 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
         nact = s_nact;
       }
       // ---- e_v for v in [v0, v1)
+      // cursor mode: the first kLUnroll x 32 entries of the warp's next row
+      // are loaded while the current row is counted (two rows in flight)
+      if (cur) {
+        auto row_at = [&](int ai, int64_t& q, int64_t& a, int64_t& b, int64_t& e0) {
+          q = q0 + (int64_t)s_act[ai];
+          a = s_ra[q - q0];
+          b = a + s_rl[q - q0];
+          e0 = a + s_rc[q - q0];
+        };
+        int64_t qn = 0, an = 0, bn = 0, e0n = 0;
+        int32_t cvn[kLUnroll];
+        if (warp < nact) {
+          row_at(warp, qn, an, bn, e0n);
+#pragma unroll
+          for (int u = 0; u < kLUnroll; ++u) {
+            const int64_t e = e0n + lane + 32 * u;
+            cvn[u] = e < bn ? __ldg(A.col + e) : 0x7fffffff;
+          }
+        }
+        for (int ai = warp; ai < nact; ai += nwarps) {
+          const int64_t q = qn, a = an, b = bn, e0 = e0n;
+          int32_t cv[kLUnroll];
+#pragma unroll
+          for (int u = 0; u < kLUnroll; ++u) cv[u] = cvn[u];
+          if (ai + nwarps < nact) {
+            row_at(ai + nwarps, qn, an, bn, e0n);
+#pragma unroll
+            for (int u = 0; u < kLUnroll; ++u) {
+              const int64_t e = e0n + lane + 32 * u;
+              cvn[u] = e < bn ? __ldg(A.col + e) : 0x7fffffff;
+            }
+          }
+          bool done = false;
+          for (int64_t e = e0 + lane;; e += 32 * kLUnroll) {
+            if (e != e0 + lane) {
+#pragma unroll
+              for (int u = 0; u < kLUnroll; ++u)
+                cv[u] = e + 32 * u < b ? __ldg(A.col + e + 32 * u) : 0x7fffffff;
+            }
+#pragma unroll
+            for (int u = 0; u < kLUnroll; ++u) {
+              if (done) break;
+              const int32_t c = cv[u];
+              const bool in = c < v1;
+              if (in) atomicAdd(s_cnt + ((c - v0) >> 1), 1u << (((c - v0) & 1) << 4));
+              const unsigned out = __ballot_sync(FULL, !in);
+              const int lc = __shfl_sync(FULL, s_lcnt, 0);
+              if (lc <= kLList && ~out) {
+                const unsigned m = ~out;
+                int lb = 0;
+                if (lane == 0) lb = atomicAdd(&s_lcnt, __popc(m));
+                lb = __shfl_sync(FULL, lb, 0) + __popc(m & ((1u << lane) - 1u));
+                if (in && lb < kLList) s_list[lb] = (uint16_t)(c - v0);
+              }
+              if (out) {
+                const int src = __ffs(out) - 1;
+                const int32_t nv = __shfl_sync(FULL, c, src);
+                if (lane == 0) {
+                  s_rc[q - q0] = (int32_t)(e + 32 * u - lane - a + src);
+                  s_nv[q - q0] = nv;
+                }
+                done = true;
+              }
+            }
+            if (done) break;
+          }
+        }
+      } else
       for (int ai = warp; ai < nact; ai += nwarps) {
         const int64_t q = q0 + (cur ? (int64_t)s_act[ai] : (int64_t)ai);
         int64_t a, b, e0;
