@@ -987,6 +987,13 @@ struct SecPopF {
   }
 };
 
+// (1 << bits) - 1, all ones for bits >= 32 (one BMSK)
+__device__ __forceinline__ uint32_t low_mask(int32_t bits) {
+  uint32_t m;
+  asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(m) : "r"(bits));
+  return m;
+}
+
 // acol[e] = sector prefix + rank inside the sector (same contract as
 // k_sage_rank; compact_columns sparse.py:352-357 + block_diag :321-342)
 __global__ void k_sage_rank8(const int64_t* __restrict__ F_ptr, const int64_t* __restrict__ eoff,
@@ -1019,9 +1026,9 @@ __global__ void k_sage_rank8(const int64_t* __restrict__ F_ptr, const int64_t* _
     for (int u = 0; u < U; ++u) {
       const int32_t e = e0 + u * (int32_t)blockDim.x;
       while (a + 1 < K && eo(a + 1) <= e) ++a;
-      const uint32_t w = (uint32_t)v[u] >> 5, q = w / 7u;
+      const uint32_t q = ((uint32_t)v[u] >> 5) / 7u;
       si[u] = a * NS + (int32_t)q;
-      wi[u] = (int32_t)(w - 7u * q);
+      wi[u] = v[u] - 224 * (int32_t)q;  // bit position inside the sector
     }
     uint4 lo[U], hi[U];
 #pragma unroll
@@ -1034,11 +1041,7 @@ __global__ void k_sage_rank8(const int64_t* __restrict__ F_ptr, const int64_t* _
         const uint32_t x[7] = {lo[u].x, lo[u].y, lo[u].z, lo[u].w, hi[u].x, hi[u].y, hi[u].z};
         int32_t r = (int32_t)hi[u].w;
 #pragma unroll
-        for (int j = 0; j < 7; ++j) {
-          const uint32_t m = j < wi[u] ? 0xffffffffu
-                                       : (j == wi[u] ? (1u << (v[u] & 31)) - 1u : 0u);
-          r += __popc(x[j] & m);
-        }
+        for (int j = 0; j < 7; ++j) r += __popc(x[j] & low_mask(max(wi[u] - 32 * j, 0)));
         acol[e] = r;
       }
     }

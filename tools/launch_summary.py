@@ -14,12 +14,18 @@ def main():
     scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "ns": 1e-3, "us": 1.0, "ms": 1e3}
     seq = [(r[kn].split("(")[0].replace("void ", ""),
             float(r[val].replace(",", "")) * scale.get(r[unit], 1.0)) for r in data]
-    start = [k for k, (n, _) in enumerate(seq) if first in n][0]
-    bulk = seq[start:]
-    per = len(bulk) // nb
+    # the last bulk starts at the last run of consecutive FIRST_KERNEL launches
+    hits = [k for k, (n, _) in enumerate(seq) if first in n]
+    starts = [k for i, k in enumerate(hits) if i == 0 or hits[i - 1] != k - 1]
+    if len(starts) >= nb:
+        last = seq[starts[-1]:]
+    else:  # markers absent per bulk: split evenly
+        bulk = seq[hits[0]:]
+        last = bulk[-(len(bulk) // nb):]
+    per = len(last)
     agg = collections.OrderedDict()
     cnt = collections.Counter()
-    for n, v in bulk[-per:]:
+    for n, v in last:
         agg[n] = agg.get(n, 0.0) + v
         cnt[n] += 1
     T = sum(agg.values())
