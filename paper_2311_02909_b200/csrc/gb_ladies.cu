@@ -1005,6 +1005,8 @@ constexpr int kXRows = 64;
 constexpr int kXSlots = 2 * kSmaxSmem;  // 2048
 constexpr int kXUnroll = 4;
 
+constexpr int kXSearch = 8;  // hub-row binary searches in flight per lane
+
 __device__ __forceinline__ uint32_t xhash(int32_t v) {
   return ((uint32_t)v * 0x9E3779B1u) >> (32 - 11);  // kXSlots = 2^11
 }
@@ -1049,21 +1051,46 @@ __global__ void __launch_bounds__(kLadiesThreads) k_lad_extract_hash(
       int32_t* out = slots + slot[q];
       int64_t o = 0;
       if (d > 16 * take) {
-        // hub row: search each sampled vertex in A[u,:] (sorted)
-        for (int64_t r0 = 0; r0 < take; r0 += 32) {
-          bool hit = false;
-          if (r0 + lane < take) {
-            const int32_t v = sS[r0 + lane];
-            int64_t lo = 0, hi = d;
-            while (lo < hi) {
-              const int64_t mid = (lo + hi) >> 1;
-              if (__ldg(col + a0 + mid) < v) lo = mid + 1; else hi = mid;
-            }
-            hit = lo < d && __ldg(col + a0 + lo) == v;
+        // hub row: search each sampled vertex in A[u,:] (sorted), kXSearch
+        // searches per lane in lock-step so their loads are in flight together
+        // (log2 d round trips per kXSearch * 32 sampled vertices)
+        const int nsteps = 32 - __clz((int)d);
+        for (int64_t r0 = 0; r0 < take; r0 += 32 * kXSearch) {
+          int32_t v[kXSearch], lo[kXSearch], hi[kXSearch];
+#pragma unroll
+          for (int j = 0; j < kXSearch; ++j) {
+            const int64_t r = r0 + 32 * j + lane;
+            v[j] = r < take ? sS[r] : 0;
+            lo[j] = 0;
+            hi[j] = r < take ? (int32_t)d : 0;
           }
-          const unsigned bal = __ballot_sync(FULL, hit);
-          if (hit) out[o + __popc(bal & ((1u << lane) - 1))] = (int32_t)(cb + r0 + lane);
-          o += __popc(bal);
+          for (int step = 0; step < nsteps; ++step) {
+            int32_t cm[kXSearch];
+#pragma unroll
+            for (int j = 0; j < kXSearch; ++j)
+              cm[j] = lo[j] < hi[j] ? __ldg(col + a0 + ((lo[j] + hi[j]) >> 1)) : 0;
+#pragma unroll
+            for (int j = 0; j < kXSearch; ++j) {
+              if (lo[j] < hi[j]) {
+                const int32_t mid = (lo[j] + hi[j]) >> 1;
+                if (cm[j] < v[j]) lo[j] = mid + 1; else hi[j] = mid;
+              }
+            }
+          }
+          int32_t at[kXSearch];
+#pragma unroll
+          for (int j = 0; j < kXSearch; ++j) {
+            const int64_t r = r0 + 32 * j + lane;
+            at[j] = r < take && lo[j] < d ? __ldg(col + a0 + lo[j]) : -1;
+          }
+#pragma unroll
+          for (int j = 0; j < kXSearch; ++j) {
+            const int64_t r = r0 + 32 * j + lane;
+            const bool hit = r < take && at[j] == v[j];
+            const unsigned bal = __ballot_sync(FULL, hit);
+            if (hit) out[o + __popc(bal & ((1u << lane) - 1))] = (int32_t)(cb + r);
+            o += __popc(bal);
+          }
         }
         if (lane == 0) rcnt[q] = (int32_t)o;
         continue;
