@@ -1050,7 +1050,7 @@ __global__ void __launch_bounds__(kLadiesThreads) k_lad_extract_hash(
       const int64_t a0 = rowptr[u], d = rowptr[u + 1] - a0;
       int32_t* out = slots + slot[q];
       int64_t o = 0;
-      if (d > 16 * take) {
+      if (d > 4 * take) {
         // hub row: search each sampled vertex in A[u,:] (sorted), kXSearch
         // searches per lane in lock-step so their loads are in flight together
         // (log2 d round trips per kXSearch * 32 sampled vertices)
