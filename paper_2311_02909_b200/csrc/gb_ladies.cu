@@ -356,19 +356,21 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
     const int64_t q0 = A.qoff[A.g0 + j], q1 = A.qoff[A.g0 + j + 1];
     const bool cur = q1 - q0 <= kLRowsSmem;
     if (cur) {
-      // cursors at the run's first column (a 32-ary search per row)
+      // cursors at the run's first column: a binary search per row, one row
+      // per thread, so all rows' searches are in flight together
       const int32_t vs = A.tb[t0];
-      for (int64_t q = q0 + warp; q < q1; q += nwarps) {
+      for (int64_t q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
         const int32_t u = A.qcol[q];
         const int64_t a = A.rowptr[u], b = A.rowptr[u + 1];
-        int64_t e0 = a;
-        if (vs > 0 && a < b && __ldg(A.col + a) < vs) e0 = warp_lower_bound(A.col, a, b, vs);
-        if (lane == 0) {
-          s_ra[q - q0] = a;
-          s_rl[q - q0] = (int32_t)(b - a);
-          s_rc[q - q0] = (int32_t)(e0 - a);
-          s_nv[q - q0] = e0 < b ? __ldg(A.col + e0) : 0x7fffffff;
+        int64_t lo = a, hi = vs > 0 ? b : a;
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (__ldg(A.col + mid) < vs) lo = mid + 1; else hi = mid;
         }
+        s_ra[q - q0] = a;
+        s_rl[q - q0] = (int32_t)(b - a);
+        s_rc[q - q0] = (int32_t)(lo - a);
+        s_nv[q - q0] = lo < b ? __ldg(A.col + lo) : 0x7fffffff;
       }
     }
     for (int64_t t = t0; t < t1; ++t) {
