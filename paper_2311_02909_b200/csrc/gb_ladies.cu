@@ -313,7 +313,7 @@ struct LadTileArgs {
   int64_t* nnz_b;          // nonzeros per batch
 };
 
-constexpr int kLTileRun = 8;      // consecutive tiles per ticket (row cursors carried over)
+constexpr int kLTileRun = 16;     // consecutive tiles per ticket (row cursors carried over)
 constexpr int kLRowsSmem = 1024;  // rows whose cursors fit in shared memory
 constexpr int kLUnroll = 4;       // 32-entry loads in flight per row
 constexpr int kLList = 2048;      // touched offsets remembered per tile (sparse compaction)
