@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
   int32_t* s_rc = s_rl + kLRowsSmem;                 // row cursor (relative)
   int32_t* s_nv = s_rc + kLRowsSmem;                 // column at the cursor (INT32_MAX: done)
   int16_t* s_act = (int16_t*)(s_nv + kLRowsSmem);    // rows with entries in the tile
-  __shared__ int s_nact, s_lcnt, s_emit;
+  __shared__ int s_nact, s_lcnt, s_emit, s_rnext;
   __shared__ uint16_t s_list[kLList];               // column offsets touched (sparse tiles)
   __shared__ int32_t s_wcnt[kLTileThreads / 32 + 1];
   __shared__ uint32_t s_stage[kLTileThreads / 32 * 64];
@@ -381,6 +381,7 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
         s_nact = 0;
         s_lcnt = 0;
         s_emit = 0;
+        s_rnext = 0;
       }
       __syncthreads();
       // rows whose next column falls in this tile (cursor mode): tiles a
@@ -402,23 +403,31 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
           b = a + s_rl[q - q0];
           e0 = a + s_rc[q - q0];
         };
+        // rows taken dynamically (segment lengths vary widely per tile)
+        auto grab = [&]() {
+          int x = 0;
+          if (lane == 0) x = atomicAdd(&s_rnext, 1);
+          return __shfl_sync(FULL, x, 0);
+        };
         int64_t qn = 0, an = 0, bn = 0, e0n = 0;
         int32_t cvn[kLUnroll];
-        if (warp < nact) {
-          row_at(warp, qn, an, bn, e0n);
+        int ai = grab();
+        if (ai < nact) {
+          row_at(ai, qn, an, bn, e0n);
 #pragma unroll
           for (int u = 0; u < kLUnroll; ++u) {
             const int64_t e = e0n + lane + 32 * u;
             cvn[u] = e < bn ? __ldg(A.col + e) : 0x7fffffff;
           }
         }
-        for (int ai = warp; ai < nact; ai += nwarps) {
+        while (ai < nact) {
           const int64_t q = qn, a = an, b = bn, e0 = e0n;
           int32_t cv[kLUnroll];
 #pragma unroll
           for (int u = 0; u < kLUnroll; ++u) cv[u] = cvn[u];
-          if (ai + nwarps < nact) {
-            row_at(ai + nwarps, qn, an, bn, e0n);
+          const int anext = grab();
+          if (anext < nact) {
+            row_at(anext, qn, an, bn, e0n);
 #pragma unroll
             for (int u = 0; u < kLUnroll; ++u) {
               const int64_t e = e0n + lane + 32 * u;
@@ -459,6 +468,7 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
             }
             if (done) break;
           }
+          ai = anext;
         }
       } else
       for (int ai = warp; ai < nact; ai += nwarps) {
