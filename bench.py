@@ -380,7 +380,7 @@ def run_reference(args, rank, world):
                          "sample": f"{kc} minibatches per step of the {k}-minibatch bulk"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def run_ours(args, rank, world, local_rank):
@@ -587,7 +587,7 @@ def run_ours(args, rank, world, local_rank):
         line["cpu_baseline"] = cb
         line["parity_full_size"] = f"{parity} on the first {kc} of {k} minibatches vs oracle"
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
 
 
 def run_15d(args, rank, world, local_rank):
@@ -697,7 +697,7 @@ def run_15d(args, rank, world, local_rank):
     dist.all_reduce(LT, op=dist.ReduceOp.MAX)
     ladies_value = k * grid.rows * len(lt) / (float(LT.item()) / 1e3)
     if rank == 0:
-        print(json.dumps({
+        emit({
             "metric": METRIC + " [1.5D partitioned graph]", "value": value, "unit": UNIT,
             "ladies_15d": {"value": ladies_value, "unit": UNIT,
                            "ms_per_step": float(LT.item()) / len(lt),
@@ -711,10 +711,24 @@ def run_15d(args, rank, world, local_rank):
                        "mode": m15, "fetch": args.fetch},
             "traffic_rank0": {k2: int(v) for k2, v in s.stats.items()},
             "feature_fetch_rank0_group": fetch_line,
-        }), flush=True)
+        })
+
+
+_JSON_FD = None  # the process's real stdout; fd 1 itself is pointed at stderr
+
+
+def emit(obj):
+    """Write the one JSON line to the real stdout (everything else a library
+    prints to stdout -- e.g. the NCCL version banner under torchrun -- has
+    been sent to stderr by main())."""
+    os.write(_JSON_FD if _JSON_FD is not None else 1, (json.dumps(obj) + "\n").encode())
 
 
 def main():
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -723,10 +737,6 @@ def main():
         import torch
         import torch.distributed as dist
 
-        # the NCCL version banner (NCCL_DEBUG=VERSION) would land on stdout
-        # ahead of the one JSON line
-        if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
-            os.environ["NCCL_DEBUG"] = "WARN"
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
