@@ -317,6 +317,8 @@ constexpr int kLTileRun = 16;     // consecutive tiles per ticket (row cursors c
 constexpr int kLRowsSmem = 1024;  // rows whose cursors fit in shared memory
 constexpr int kLUnroll = 4;       // 32-entry loads in flight per row
 constexpr int kLList = 2048;      // touched offsets remembered per tile (sparse compaction)
+constexpr int kLShort = 8;        // expected entries per tile below which a row is "short"
+constexpr int kLShortRows = 4;    // short rows per warp step (8 lanes each)
 
 // One ticket = batch j and a run of kLTileRun consecutive column tiles.  Per
 // tile: counts in shared memory (warp per A row, from the row's cursor, which
@@ -330,7 +332,7 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
   int32_t* s_rc = s_rl + kLRowsSmem;                 // row cursor (relative)
   int32_t* s_nv = s_rc + kLRowsSmem;                 // column at the cursor (INT32_MAX: done)
   int16_t* s_act = (int16_t*)(s_nv + kLRowsSmem);    // rows with entries in the tile
-  __shared__ int s_nact, s_lcnt, s_emit, s_rnext;
+  __shared__ int s_nact, s_lcnt, s_emit, s_rnext, s_nshort, s_snext;
   __shared__ uint16_t s_list[kLList];               // column offsets touched (sparse tiles)
   __shared__ int32_t s_wcnt[kLTileThreads / 32 + 1];
   __shared__ uint32_t s_stage[kLTileThreads / 32 * 64];
@@ -382,16 +384,28 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
         s_lcnt = 0;
         s_emit = 0;
         s_rnext = 0;
+        s_nshort = 0;
+        s_snext = 0;
       }
       __syncthreads();
       // rows whose next column falls in this tile (cursor mode): tiles a
       // row has no entries in cost one shared-memory read
-      int nact = (int)(q1 - q0);
+      // Rows expected to hold few entries in the tile (deg * width / n <
+      // kLShort, columns are spread uniformly by the relabel) are listed from
+      // the back and counted kLShortRows per warp, 8 lanes each.
+      int nact = (int)(q1 - q0), nshort = 0;
       if (cur) {
+        const int64_t wn = (int64_t)(v1 - v0);
         for (int r = threadIdx.x; r < q1 - q0; r += blockDim.x)
-          if (s_nv[r] < v1) s_act[atomicAdd(&s_nact, 1)] = (int16_t)r;
+          if (s_nv[r] < v1) {
+            if ((int64_t)s_rl[r] * wn < (int64_t)kLShort * A.n)
+              s_act[kLRowsSmem - 1 - atomicAdd(&s_nshort, 1)] = (int16_t)r;
+            else
+              s_act[atomicAdd(&s_nact, 1)] = (int16_t)r;
+          }
         __syncthreads();
         nact = s_nact;
+        nshort = s_nshort;
       }
       // ---- e_v for v in [v0, v1)
       // cursor mode: the first kLUnroll x 32 entries of the warp's next row
@@ -469,6 +483,50 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
             if (done) break;
           }
           ai = anext;
+        }
+        // short rows: kLShortRows rows per warp step, 8 lanes (one 32-B
+        // sector of columns) per row per step
+        const int g = lane >> 3, sl = lane & 7;
+        for (;;) {
+          int base = 0;
+          if (lane == 0) base = atomicAdd(&s_snext, kLShortRows);
+          base = __shfl_sync(FULL, base, 0);
+          if (base >= nshort) break;
+          const int si = base + g;
+          bool gdone = si >= nshort;
+          int64_t q = q0, a = 0, b = 0, e = 0;
+          if (!gdone) {
+            q = q0 + (int64_t)s_act[kLRowsSmem - 1 - si];
+            a = s_ra[q - q0];
+            b = a + s_rl[q - q0];
+            e = a + s_rc[q - q0] + sl;
+          }
+          for (;;) {
+            const int32_t c = !gdone && e < b ? __ldg(A.col + e) : 0x7fffffff;
+            const bool in = !gdone && c < v1;
+            if (in) atomicAdd(s_cnt + ((c - v0) >> 1), 1u << (((c - v0) & 1) << 4));
+            const unsigned inb = __ballot_sync(FULL, in);
+            const int lc = __shfl_sync(FULL, s_lcnt, 0);
+            if (lc <= kLList && inb) {
+              int lb = 0;
+              if (lane == 0) lb = atomicAdd(&s_lcnt, __popc(inb));
+              lb = __shfl_sync(FULL, lb, 0) + __popc(inb & ((1u << lane) - 1u));
+              if (in && lb < kLList) s_list[lb] = (uint16_t)(c - v0);
+            }
+            const unsigned outb = __ballot_sync(FULL, !gdone && !in);
+            const unsigned gout = (outb >> (8 * g)) & 0xffu;
+            const int src = gout ? __ffs(gout) - 1 : 0;
+            const int32_t nv = __shfl_sync(FULL, c, 8 * g + src);  // next column
+            if (gout) {
+              if (sl == 0) {
+                s_rc[q - q0] = (int32_t)(e - a + src);
+                s_nv[q - q0] = nv;
+              }
+              gdone = true;
+            }
+            e += 8;
+            if (__all_sync(FULL, gdone)) break;
+          }
         }
       } else
       for (int ai = warp; ai < nact; ai += nwarps) {
