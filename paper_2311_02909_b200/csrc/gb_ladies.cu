@@ -317,7 +317,7 @@ constexpr int kLTileRun = 16;     // consecutive tiles per ticket (row cursors c
 constexpr int kLRowsSmem = 1024;  // rows whose cursors fit in shared memory
 constexpr int kLUnroll = 4;       // 32-entry loads in flight per row
 constexpr int kLList = 2048;      // touched offsets remembered per tile (sparse compaction)
-constexpr int kLShort = 8;        // expected entries per tile below which a row is "short"
+constexpr int kLShort = 16;       // expected entries per tile below which a row is "short"
 constexpr int kLShortRows = 4;    // short rows per warp step (8 lanes each)
 
 // One ticket = batch j and a run of kLTileRun consecutive column tiles.  Per
