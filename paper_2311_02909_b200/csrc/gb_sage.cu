@@ -251,15 +251,6 @@ __device__ __forceinline__ T tld(const T* p) {
   if constexpr (SM) return *p; else return __ldg(p);
 }
 
-// S[n], 1 <= n <= m: n_live is near m, so scan back from the last run
-template <bool SM = false>
-__device__ __forceinline__ double gt_S(const GTable& t, int64_t n) {
-  int r = t.nr - 1;
-  int32_t j0 = tld<SM>(t.j0 + r);
-  while (j0 > n) j0 = tld<SM>(t.j0 + --r);
-  return __dadd_rn(tld<SM>(t.s0 + r), __dmul_rn((double)(n - j0), tld<SM>(t.d + r)));
-}
-
 // first j >= 1 with S[j] > target (m + 1 when none).  The run is located by
 // the binade index (O(1)), the position inside it by a float estimate that
 // the exact fp64 comparisons then correct.
@@ -336,7 +327,12 @@ __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
       tab.d = A.run_d + (int64_t)slot * kMaxRuns;
       tab.lower = A.run_lower + (int64_t)slot * kBinades;
       tab.nr = __ldg(A.run_n + slot);
-      tab.top = binade(__ldg(tab.s0 + tab.nr - 1));
+      // S[n_live] run cursor: n_live only falls, so the run of S[n_live] is
+      // carried across draws and its (j0, s0, d) reloaded only when it moves
+      int rS = tab.nr - 1;
+      int32_t j0S = __ldg(tab.j0 + rS);
+      double s0S = __ldg(tab.s0 + rS), dS = __ldg(tab.d + rS);
+      tab.top = binade(s0S);
       uint64_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;
       for (int t = 0; t < take; ++t) {
         if ((t & 3) == 0) {
@@ -346,7 +342,13 @@ __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
         const uint64_t w = (t & 3) == 0 ? w0 : (t & 3) == 1 ? w1 : (t & 3) == 2 ? w2 : w3;
         const double u = (double)(w >> 11) * 0x1.0p-53;
         const int64_t n_live = deg - t;
-        const double target = __dmul_rn(u, gt_S(tab, n_live));
+        if (j0S > n_live) {
+          do j0S = __ldg(tab.j0 + --rS); while (j0S > n_live);
+          s0S = __ldg(tab.s0 + rS);
+          dS = __ldg(tab.d + rS);
+        }
+        const double target =
+            __dmul_rn(u, __dadd_rn(s0S, __dmul_rn((double)(n_live - j0S), dS)));
         int64_t j = gt_first_gt(tab, target);
         if (j > n_live) j = n_live;
         // j-th live index: skip over the removed (sorted) ones, then insert
