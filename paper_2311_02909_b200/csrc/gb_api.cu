@@ -173,8 +173,7 @@ int gb_graph_destroy(gb_graph* g) {
   cudaFree(g->deg_slot);
   cudaFree(g->slot_deg);
   cudaFree(g->run_j0);
-  cudaFree(g->run_s0);
-  cudaFree(g->run_d);
+  cudaFree(g->run_sd);
   cudaFree(g->run_n);
   cudaFree(g->run_lower);
   delete g;

@@ -19,8 +19,7 @@ struct Graph {
   int32_t* deg_slot = nullptr;      // [max_deg + 1] -> table slot or -1
   int32_t* slot_deg = nullptr;      // [slots]
   int32_t* run_j0 = nullptr;        // [slots * (kMaxRuns + 1)]
-  double* run_s0 = nullptr;         // [slots * kMaxRuns]
-  double* run_d = nullptr;          // [slots * kMaxRuns]
+  double2* run_sd = nullptr;        // [slots * kMaxRuns] (run start S, increment)
   int32_t* run_n = nullptr;         // [slots]
   int8_t* run_lower = nullptr;      // [slots * kBinades] binade index
 };

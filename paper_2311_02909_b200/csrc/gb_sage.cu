@@ -89,16 +89,15 @@ __device__ __forceinline__ uint64_t binade(double x) {
 // b binades below the top run's binade, so the run holding a target value
 // is found in O(1) (gt_first_gt).
 __global__ void k_build_runs(const int32_t* __restrict__ slot_deg, int64_t slots,
-                             int32_t* __restrict__ run_j0, double* __restrict__ run_s0,
-                             double* __restrict__ run_d, int32_t* __restrict__ run_n,
+                             int32_t* __restrict__ run_j0, double2* __restrict__ run_sd,
+                             int32_t* __restrict__ run_n,
                              int8_t* __restrict__ run_lower, int32_t* __restrict__ overflow) {
   for (int64_t sl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sl < slots;
        sl += (int64_t)gridDim.x * blockDim.x) {
     const int64_t m = slot_deg[sl];
     const double w = 1.0 / (double)m;
     int32_t* J = run_j0 + sl * (kMaxRuns + 1);
-    double* S0 = run_s0 + sl * kMaxRuns;
-    double* D = run_d + sl * kMaxRuns;
+    double2* SD = run_sd + sl * kMaxRuns;
     int nr = 0;
     int64_t j0 = 1, len = 1;
     double s0 = w, d = 0.0, S = w;
@@ -112,22 +111,22 @@ __global__ void k_build_runs(const int32_t* __restrict__ slot_deg, int64_t slots
       } else if (len >= 2 && step == d && binade(S2) == binade(s0)) {
         ++len;
       } else {
-        if (nr < kMaxRuns) { J[nr] = (int32_t)j0; S0[nr] = s0; D[nr] = d; } else bad = true;
+        if (nr < kMaxRuns) { J[nr] = (int32_t)j0; SD[nr] = make_double2(s0, d); } else bad = true;
         ++nr;
         j0 = j; s0 = S2; len = 1; d = 0.0;
       }
       S = S2;
     }
-    if (nr < kMaxRuns) { J[nr] = (int32_t)j0; S0[nr] = s0; D[nr] = d; } else bad = true;
+    if (nr < kMaxRuns) { J[nr] = (int32_t)j0; SD[nr] = make_double2(s0, d); } else bad = true;
     ++nr;
     if (nr <= kMaxRuns) J[nr] = (int32_t)(m + 1);  // sentinel
     run_n[sl] = nr;
     if (!bad) {
-      const int64_t top = (int64_t)binade(S0[nr - 1]);
+      const int64_t top = (int64_t)binade(SD[nr - 1].x);
       int8_t* low = run_lower + sl * kBinades;
       for (int b = 0; b < kBinades; ++b) {
         int c = 0;
-        for (int r = 0; r < nr; ++r) c += (top - (int64_t)binade(S0[r]) > b) ? 1 : 0;
+        for (int r = 0; r < nr; ++r) c += (top - (int64_t)binade(SD[r].x) > b) ? 1 : 0;
         low[b] = (int8_t)c;
       }
     }
@@ -167,8 +166,7 @@ struct SageArgs {
   const int32_t* col;
   const int32_t* deg_slot;
   const int32_t* run_j0;
-  const double* run_s0;
-  const double* run_d;
+  const double2* run_sd;  // (run start S, increment) per run
   const int32_t* run_n;
   const int8_t* run_lower;
   const int32_t* rowv;
@@ -239,36 +237,31 @@ __device__ __forceinline__ int64_t batch_of(const int64_t* sb, const int64_t* gb
 // shared-memory copy (SM = true, the fused dedup kernel).
 struct GTable {
   const int32_t* j0;
-  const double* s0;
-  const double* d;
+  const double2* sd;  // (run start S, increment)
   const int8_t* lower;
   int nr;
   uint64_t top;  // binade of the last run's start
 };
 
-template <bool SM, typename T>
-__device__ __forceinline__ T tld(const T* p) {
-  if constexpr (SM) return *p; else return __ldg(p);
-}
-
 // first j >= 1 with S[j] > target (m + 1 when none).  The run is located by
 // the binade index (O(1)), the position inside it by a float estimate that
 // the exact fp64 comparisons then correct.
-template <bool SM = false>
 __device__ __forceinline__ int64_t gt_first_gt(const GTable& t, double target) {
-  if (target < tld<SM>(t.s0)) return 1;
+  if (target < __ldg(&t.sd->x)) return 1;
   const int64_t off = (int64_t)t.top - (int64_t)binade(target);
-  int r = off < 0 ? t.nr : (int)tld<SM>(t.lower + (off < kBinades ? off : kBinades - 1));
+  int r = off < 0 ? t.nr : (int)__ldg(t.lower + (off < kBinades ? off : kBinades - 1));
   // r = first run starting in target's binade or above; step back / forward
-  if (r >= t.nr || tld<SM>(t.s0 + r) > target) {
-    r = r - 1;
+  double2 sd;
+  if (r >= t.nr || (sd = __ldg(t.sd + r)).x > target) {
+    sd = __ldg(t.sd + --r);
   } else {
-    while (r + 1 < t.nr && tld<SM>(t.s0 + r + 1) <= target) ++r;
+    double2 nx;
+    while (r + 1 < t.nr && (nx = __ldg(t.sd + r + 1)).x <= target) { ++r; sd = nx; }
   }
-  const int64_t j0 = tld<SM>(t.j0 + r);
-  const int64_t len = (int64_t)tld<SM>(t.j0 + r + 1) - j0;
+  const int64_t j0 = __ldg(t.j0 + r);
+  const int64_t len = (int64_t)__ldg(t.j0 + r + 1) - j0;
   if (len == 1) return j0 + 1;
-  const double s0 = tld<SM>(t.s0 + r), d = tld<SM>(t.d + r);
+  const double s0 = sd.x, d = sd.y;
   int64_t q = (int64_t)__fdividef((float)(target - s0), (float)d);
   q = q < 0 ? 0 : (q > len - 1 ? len - 1 : q);
   while (q > 0 && __dadd_rn(s0, __dmul_rn((double)q, d)) > target) --q;
@@ -323,16 +316,15 @@ __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
       const int32_t slot = __ldg(A.deg_slot + deg);
       GTable tab;
       tab.j0 = A.run_j0 + (int64_t)slot * (kMaxRuns + 1);
-      tab.s0 = A.run_s0 + (int64_t)slot * kMaxRuns;
-      tab.d = A.run_d + (int64_t)slot * kMaxRuns;
+      tab.sd = A.run_sd + (int64_t)slot * kMaxRuns;
       tab.lower = A.run_lower + (int64_t)slot * kBinades;
       tab.nr = __ldg(A.run_n + slot);
       // S[n_live] run cursor: n_live only falls, so the run of S[n_live] is
       // carried across draws and its (j0, s0, d) reloaded only when it moves
       int rS = tab.nr - 1;
       int32_t j0S = __ldg(tab.j0 + rS);
-      double s0S = __ldg(tab.s0 + rS), dS = __ldg(tab.d + rS);
-      tab.top = binade(s0S);
+      double2 sdS = __ldg(tab.sd + rS);
+      tab.top = binade(sdS.x);
       uint64_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;
       for (int t = 0; t < take; ++t) {
         if ((t & 3) == 0) {
@@ -344,11 +336,10 @@ __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
         const int64_t n_live = deg - t;
         if (j0S > n_live) {
           do j0S = __ldg(tab.j0 + --rS); while (j0S > n_live);
-          s0S = __ldg(tab.s0 + rS);
-          dS = __ldg(tab.d + rS);
+          sdS = __ldg(tab.sd + rS);
         }
         const double target =
-            __dmul_rn(u, __dadd_rn(s0S, __dmul_rn((double)(n_live - j0S), dS)));
+            __dmul_rn(u, __dadd_rn(sdS.x, __dmul_rn((double)(n_live - j0S), sdS.y)));
         int64_t j = gt_first_gt(tab, target);
         if (j > n_live) j = n_live;
         // j-th live index: skip over the removed (sorted) ones, then insert
@@ -1139,8 +1130,7 @@ int graph_build_tables(Graph* g, cudaStream_t st) {
   const int64_t sl = slots > 0 ? slots : 1;
   GB_CUDA(cudaMalloc(&g->slot_deg, sizeof(int32_t) * sl));
   GB_CUDA(cudaMalloc(&g->run_j0, sizeof(int32_t) * sl * (kMaxRuns + 1)));
-  GB_CUDA(cudaMalloc(&g->run_s0, sizeof(double) * sl * kMaxRuns));
-  GB_CUDA(cudaMalloc(&g->run_d, sizeof(double) * sl * kMaxRuns));
+  GB_CUDA(cudaMalloc(&g->run_sd, sizeof(double2) * sl * kMaxRuns));
   GB_CUDA(cudaMalloc(&g->run_n, sizeof(int32_t) * sl));
   GB_CUDA(cudaMalloc(&g->run_lower, sizeof(int8_t) * sl * kBinades));
   int32_t* d_over = nullptr;
@@ -1151,7 +1141,7 @@ int graph_build_tables(Graph* g, cudaStream_t st) {
   GB_LAUNCH_CHECK("k_degree_slots");
   if (slots > 0) {
     k_build_runs<<<grid_for(slots, 64, 1 << 20), 64, 0, st>>>(g->slot_deg, slots, g->run_j0,
-                                                               g->run_s0, g->run_d, g->run_n,
+                                                               g->run_sd, g->run_n,
                                                                g->run_lower, d_over);
     GB_LAUNCH_CHECK("k_build_runs");
   }
@@ -1459,7 +1449,7 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     }
     SageArgs A{};
     A.rowptr = g->rowptr; A.col = g->col;
-    A.deg_slot = g->deg_slot; A.run_j0 = g->run_j0; A.run_s0 = g->run_s0; A.run_d = g->run_d;
+    A.deg_slot = g->deg_slot; A.run_j0 = g->run_j0; A.run_sd = g->run_sd;
     A.run_n = g->run_n; A.run_lower = g->run_lower;
     A.rowv = rowv; A.deg = ws.deg; A.fptr = o.fptr; A.gstart = ws.gstart;
     A.brow = brow; A.k = k; A.s = s; A.stride = stride; A.batch_offset = batch_offset;
@@ -1580,8 +1570,8 @@ int sage_layer_sample(const Graph* tables, int64_t k, const int64_t* brow, int64
   }
   SageArgs A{};
   A.rowptr = rowptr; A.col = col;
-  A.deg_slot = tables->deg_slot; A.run_j0 = tables->run_j0; A.run_s0 = tables->run_s0;
-  A.run_d = tables->run_d; A.run_n = tables->run_n; A.run_lower = tables->run_lower;
+  A.deg_slot = tables->deg_slot; A.run_j0 = tables->run_j0; A.run_sd = tables->run_sd;
+  A.run_n = tables->run_n; A.run_lower = tables->run_lower;
   A.rowv = rowv; A.deg = deg; A.fptr = fptr; A.gstart = gstart;
   A.brow = brow; A.k = k; A.s = s; A.stride = stride; A.batch_offset = batch_offset;
   A.seed = seed; A.epoch = epoch; A.depth = depth;
@@ -1609,8 +1599,8 @@ int sage_sample_keyed(const Graph* tables, int64_t R, const int64_t* d_R, const 
   if (R == 0) return GB_OK;
   SageArgs A{};
   A.rowptr = rowptr; A.col = col;
-  A.deg_slot = tables->deg_slot; A.run_j0 = tables->run_j0; A.run_s0 = tables->run_s0;
-  A.run_d = tables->run_d; A.run_n = tables->run_n; A.run_lower = tables->run_lower;
+  A.deg_slot = tables->deg_slot; A.run_j0 = tables->run_j0; A.run_sd = tables->run_sd;
+  A.run_n = tables->run_n; A.run_lower = tables->run_lower;
   A.rowv = rowv; A.rowkeys = rowkeys; A.deg = deg; A.fptr = fptr;
   A.k = 0; A.s = s; A.seed = seed; A.epoch = epoch; A.depth = depth;
   A.bitmap = nullptr; A.fcol = fcol;
@@ -1697,8 +1687,8 @@ int sage_owner_p2p(const Graph* tables, int64_t ngroups, const int32_t* const* r
     GB_LAUNCH_CHECK("k_p2p_rows");
     SageArgs A{};
     A.rowptr = brp; A.col = bcol;
-    A.deg_slot = tables->deg_slot; A.run_j0 = tables->run_j0; A.run_s0 = tables->run_s0;
-    A.run_d = tables->run_d; A.run_n = tables->run_n; A.run_lower = tables->run_lower;
+    A.deg_slot = tables->deg_slot; A.run_j0 = tables->run_j0; A.run_sd = tables->run_sd;
+    A.run_n = tables->run_n; A.run_lower = tables->run_lower;
     A.rowv = lrow; A.rowkeys = lkey; A.deg = ldeg; A.fptr = lpos;
     A.k = 0; A.s = s; A.seed = seed; A.epoch = epoch; A.depth = depth;
     A.bitmap = nullptr; A.fcol = nullptr;
