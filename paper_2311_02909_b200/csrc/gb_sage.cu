@@ -531,14 +531,19 @@ __global__ void k_dd_list(int64_t nwords, const uint32_t* __restrict__ vbits,
   }
 }
 
-// rows per distinct vertex
+// rows per distinct vertex; each row keeps its group and its slot in the
+// group, so the grouping pass needs no second atomic
 __global__ void k_dd_rcount(const int64_t* __restrict__ R_ptr, const int32_t* __restrict__ rowv,
                             const int32_t* __restrict__ deg, const uint32_t* __restrict__ vbits,
-                            const int32_t* __restrict__ vpre, int32_t* __restrict__ gcnt) {
+                            const int32_t* __restrict__ vpre, int32_t* __restrict__ gcnt,
+                            int2* __restrict__ rslot) {
   const int64_t R = *R_ptr;
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
        r += (int64_t)gridDim.x * blockDim.x) {
-    if (deg[r] > 0) atomicAdd(gcnt + vrank(vbits, vpre, rowv[r]), 1);
+    if (deg[r] > 0) {
+      const int32_t g = vrank(vbits, vpre, rowv[r]);
+      rslot[r] = make_int2(g, atomicAdd(gcnt + g, 1));
+    }
   }
 }
 
@@ -549,8 +554,7 @@ __global__ void k_dd_rcount(const int64_t* __restrict__ R_ptr, const int32_t* __
 __global__ void k_dd_rows(const int64_t* __restrict__ R_ptr, const int32_t* __restrict__ rowv,
                           const int32_t* __restrict__ deg, const int64_t* __restrict__ fptr,
                           const int64_t* __restrict__ brow, int64_t k,
-                          const uint32_t* __restrict__ vbits, const int32_t* __restrict__ vpre,
-                          const int64_t* __restrict__ roff, int32_t* __restrict__ gcur,
+                          const int2* __restrict__ rslot, const int64_t* __restrict__ roff,
                           int4* __restrict__ rrec) {
   __shared__ int64_t s_brow[kBrowSmem];
   if (k + 1 <= kBrowSmem)
@@ -561,8 +565,8 @@ __global__ void k_dd_rows(const int64_t* __restrict__ R_ptr, const int32_t* __re
        r += (int64_t)gridDim.x * blockDim.x) {
     const int32_t dr = deg[r];
     if (dr > 0) {
-      const int32_t g = vrank(vbits, vpre, rowv[r]);
-      const int64_t pos = roff[g] + atomicAdd(gcur + g, 1);
+      const int2 gs = rslot[r];
+      const int64_t pos = roff[gs.x] + gs.y;
       rrec[pos] = make_int4((int32_t)r, dr, (int32_t)batch_of(s_brow, brow, k, r),
                             (int32_t)fptr[r]);
     }
@@ -1180,7 +1184,7 @@ struct SageWs {
   int64_t* d_nw;     // device scalars: nwords, D
   int32_t* dv;       // distinct vertices
   int32_t* gcnt;     // frontier rows per distinct vertex
-  int32_t* gcur;
+  int2* rslot;       // per frontier row: (group, slot in the group)
   int64_t* roff;     // group offsets into rrec
   int64_t* ioff;     // tier-major work-item prefix [3 * r_cap + 1]
   DdItem* items;     // work-item descriptors
@@ -1215,7 +1219,7 @@ static SageWs sage_ws_layout(char* base, int64_t k, int64_t n, int64_t r_cap_max
   w.d_nw = (int64_t*)take(sizeof(int64_t) * 3);
   w.dv = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
   w.gcnt = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
-  w.gcur = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
+  w.rslot = (int2*)take(sizeof(int2) * (r_cap_max + 1));
   w.roff = (int64_t*)take(sizeof(int64_t) * (r_cap_max + 1));
   w.ioff = (int64_t*)take(sizeof(int64_t) * (3 * r_cap_max + 1));
   // items <= groups + rows / 32 <= 2 * rows
@@ -1259,7 +1263,6 @@ static int dedup_prepare(const Graph* g, SageWs& ws, const int64_t* R_ptr, const
   // distinct row vertices D <= min(rows, n): group arrays sized by that
   const int64_t dcap = r_cap < g->n ? r_cap : g->n;
   GB_CUDA(cudaMemsetAsync(ws.gcnt, 0, sizeof(int32_t) * (dcap + 1), st));
-  GB_CUDA(cudaMemsetAsync(ws.gcur, 0, sizeof(int32_t) * (dcap + 1), st));
   int rc = device_exclusive_scan<int64_t>(ws.d_nw, nwords, VPopF{ws.vbits}, ws.vpre, ws.scan_ws,
                                           st);
   if (rc) return rc;
@@ -1267,12 +1270,11 @@ static int dedup_prepare(const Graph* g, SageWs& ws, const int64_t* R_ptr, const
   k_dd_list<<<grid_for(nwords, 256, gw), 256, 0, st>>>(nwords, ws.vbits, ws.vpre, g->rowptr,
                                                       ws.dv, ws.ddeg);
   k_dd_rcount<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, ws.vbits, ws.vpre,
-                                                       ws.gcnt);
+                                                       ws.gcnt, ws.rslot);
   rc = device_exclusive_scan<int64_t>(ws.d_nw + 1, dcap, GcntF{ws.gcnt}, ws.roff, ws.scan_ws, st);
   if (rc) return rc;
   k_dd_rows<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, fptr, brow, k,
-                                                     ws.vbits, ws.vpre, ws.roff, ws.gcur,
-                                                     ws.rrec);
+                                                     ws.rslot, ws.roff, ws.rrec);
   rc = device_exclusive_scan<int64_t>(ws.d_nw + 2, 3 * dcap,
                                       ItemF{ws.ddeg, ws.gcnt, ws.d_nw + 1, dd_items(s)},
                                       ws.ioff, ws.scan_ws, st);
