@@ -604,21 +604,6 @@ struct DdItems {
   int32_t rows[3];  // rows per work item, per tier
 };
 
-// Tier-major work-item prefix in one scan: virtual index i = tier * D + g
-struct ItemF {
-  const int32_t* ddeg;
-  const int32_t* gcnt;
-  const int64_t* D_ptr;
-  DdItems it;
-  __device__ int64_t operator()(int64_t i) const {
-    const int64_t D = *D_ptr;
-    const int64_t t = i >= D ? (i >= 2 * D ? 2 : 1) : 0, g = i - t * D;
-    if (dd_tier(ddeg[g]) != t) return 0;
-    const int64_t rows = it.rows[t];
-    return (gcnt[g] + rows - 1) / rows;
-  }
-};
-
 __global__ void k_dd_3d(const int32_t* __restrict__ dcount, int64_t* __restrict__ out) {
   out[0] = *dcount;      // D
   out[1] = 3 * *dcount;  // tier-major item index space
@@ -643,47 +628,83 @@ struct PeerRows {
   const int32_t* const* bcol;
 };
 
-// descriptors of every tier's items (tier-major)
+// descriptors of every tier's items: tier t's items live in region
+// [t * icap, t * icap + tcnt[t]); a block reserves its items of each tier with
+// one atomic per tier (item order inside a tier is free — every frontier
+// row's output is independent), so no prefix pass over the groups is needed
 // a0: index of the row's first entry in the graph's column array, or with a
 // peer row source the row's address in its block owner's memory / 4 (the
 // serve kernel then addresses rows from a null base)
-__global__ void k_dd_items(const int64_t* __restrict__ D_ptr, const int32_t* __restrict__ dv,
-                           const int32_t* __restrict__ ddeg, const int64_t* __restrict__ rowptr, const int64_t* __restrict__ roff,
-                           const int64_t* __restrict__ ioff, DdItems rows,
-                           DdItem* __restrict__ items, PeerRows peer) {
+constexpr int kItemThreads = 256;
+__global__ void __launch_bounds__(kItemThreads) k_dd_items(
+    const int64_t* __restrict__ D_ptr, const int32_t* __restrict__ dv,
+    const int32_t* __restrict__ ddeg, const int32_t* __restrict__ gcnt,
+    const int64_t* __restrict__ rowptr, const int64_t* __restrict__ roff, DdItems rows,
+    int64_t icap, unsigned long long* __restrict__ tcnt, DdItem* __restrict__ items,
+    PeerRows peer) {
+  __shared__ int32_t s_wsum[3][kItemThreads / 32];
+  __shared__ int64_t s_base[3];
   const int64_t D = *D_ptr;
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < D;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t v = dv[g];
-    int64_t a0;
-    if (peer.nblk) {
-      int b = 0;
-      while (b + 1 < peer.nblk && peer.bounds[b + 1] <= v) ++b;
-      const int64_t* brp = peer.brp[b];
-      a0 = ((int64_t)(uintptr_t)(peer.bcol[b] + brp[v - peer.bounds[b]])) >> 2;
-    } else {
-      a0 = rowptr[v];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int64_t g0 = blockIdx.x * (int64_t)kItemThreads; g0 < D;
+       g0 += (int64_t)gridDim.x * kItemThreads) {
+    const int64_t g = g0 + threadIdx.x;
+    int t = 0, n = 0;
+    int64_t d = 0;
+    if (g < D) {
+      d = ddeg[g];
+      t = dd_tier(d);
+      n = (gcnt[g] + rows.rows[t] - 1) / rows.rows[t];
     }
-    const int64_t d = ddeg[g];
-    const int t = dd_tier(d);
-    const int64_t o0 = ioff[t * D + g], o1 = ioff[t * D + g + 1];
-    const int64_t r0 = roff[g], r1 = roff[g + 1], per = rows.rows[t];
-    for (int64_t o = o0; o < o1; ++o) {
-      DdItem it;
-      it.a0 = a0;
-      it.d = (int32_t)d;
-      it.q0 = (int32_t)(r0 + (o - o0) * per);
-      it.nrows = (int32_t)min(per, r1 - it.q0);
-      it.pad[0] = it.pad[1] = it.pad[2] = 0;
-      items[o] = it;
+    // per-tier exclusive offsets inside the block
+    int incl[3];
+#pragma unroll
+    for (int z = 0; z < 3; ++z) {
+      incl[z] = warp_incl_scan(t == z ? n : 0);
+      if (lane == 31) s_wsum[z][wid] = incl[z];
     }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+      int tot = 0;
+      for (int w = 0; w < kItemThreads / 32; ++w) tot += s_wsum[threadIdx.x][w];
+      s_base[threadIdx.x] =
+          tot ? (int64_t)atomicAdd(tcnt + threadIdx.x, (unsigned long long)tot) : 0;
+    }
+    __syncthreads();
+    if (n) {
+      int64_t o0 = s_base[t] + incl[t] - n;
+      for (int w = 0; w < wid; ++w) o0 += s_wsum[t][w];
+      o0 += (int64_t)t * icap;
+      const int32_t v = dv[g];
+      int64_t a0;
+      if (peer.nblk) {
+        int b = 0;
+        while (b + 1 < peer.nblk && peer.bounds[b + 1] <= v) ++b;
+        const int64_t* brp = peer.brp[b];
+        a0 = ((int64_t)(uintptr_t)(peer.bcol[b] + brp[v - peer.bounds[b]])) >> 2;
+      } else {
+        a0 = rowptr[v];
+      }
+      const int64_t r0 = roff[g], r1 = roff[g + 1], per = rows.rows[t];
+      for (int o = 0; o < n; ++o) {
+        DdItem it;
+        it.a0 = a0;
+        it.d = (int32_t)d;
+        it.q0 = (int32_t)(r0 + o * per);
+        it.nrows = (int32_t)min(per, r1 - it.q0);
+        it.pad[0] = it.pad[1] = it.pad[2] = 0;
+        items[o0 + o] = it;
+      }
+    }
+    __syncthreads();  // s_wsum / s_base reused by the next round
   }
 }
 
 struct DdArgs {
   const int64_t* D_ptr;  // (col == nullptr: item a0 is an address / 4, peer rows)
   const int32_t* col;
-  const int64_t* ioff;   // tier-major item prefix (3D + 1)
+  const unsigned long long* tcnt;  // items per tier; tier t's at [t * icap, ..)
+  int64_t icap;
   const DdItem* items;
   const int32_t* pidx;   // sorted picks of grouped row q at pidx[q * s ..]
   const int2* rbf;       // (batch, frontier offset) of grouped row q at [2q + 1]
@@ -723,7 +744,8 @@ __device__ void dd_serve_warp(const DdArgs& A, int32_t* buf, int B, int32_t* gi)
   const int lane = lane_id(), s = A.s;
   const uint32_t NW = (uint32_t)A.nwords;
   const int64_t D = *A.D_ptr;
-  const int64_t i0 = A.ioff[0], it1 = A.ioff[D];
+  const int64_t i0 = 0, it1 = (int64_t)A.tcnt[0];
+  (void)D;
   const int64_t nblk = (it1 - i0 + 31) / 32;
   for (int64_t blk = global_warp(); blk < nblk; blk += grid_warps()) {
     const int64_t it = i0 + blk * 32 + lane;
@@ -821,9 +843,10 @@ __global__ void __launch_bounds__(DdTier<TIER>::kThreads) k_dd_serve(DdArgs A) {
   const int nthr = CTA ? blockDim.x : 32;
   int32_t* buf = sbuf + (CTA ? 0 : (threadIdx.x >> 5) * (chunk + 8));
   const int64_t D = *A.D_ptr;
-  const int64_t it1 = A.ioff[(TIER + 1) * D];
+  const int64_t it1 = TIER * A.icap + (int64_t)A.tcnt[TIER];
+  (void)D;
   const int64_t step = CTA ? gridDim.x : grid_warps();
-  int64_t it = A.ioff[TIER * D] + (CTA ? blockIdx.x : global_warp());
+  int64_t it = TIER * A.icap + (CTA ? blockIdx.x : global_warp());
   DdItem cur;
   if (it < it1) cur = A.items[it];
   for (; it < it1; it += step) {
@@ -1186,7 +1209,8 @@ struct SageWs {
   int32_t* gcnt;     // frontier rows per distinct vertex
   int2* rslot;       // per frontier row: (group, slot in the group)
   int64_t* roff;     // group offsets into rrec
-  int64_t* ioff;     // tier-major work-item prefix [3 * r_cap + 1]
+  unsigned long long* tcnt;  // work items per tier [3]
+  int64_t icap;      // work-item capacity per tier
   DdItem* items;     // work-item descriptors
   int4* rrec;        // per grouped row: (row, degree, batch, frontier offset)
   int32_t* ddeg;     // degree per distinct vertex
@@ -1221,9 +1245,10 @@ static SageWs sage_ws_layout(char* base, int64_t k, int64_t n, int64_t r_cap_max
   w.gcnt = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
   w.rslot = (int2*)take(sizeof(int2) * (r_cap_max + 1));
   w.roff = (int64_t*)take(sizeof(int64_t) * (r_cap_max + 1));
-  w.ioff = (int64_t*)take(sizeof(int64_t) * (3 * r_cap_max + 1));
-  // items <= groups + rows / 32 <= 2 * rows
-  w.items = (DdItem*)take(sizeof(DdItem) * (2 * r_cap_max + 2));
+  w.tcnt = (unsigned long long*)take(sizeof(unsigned long long) * 4);
+  // items <= groups + rows / 32 <= 2 * rows, per tier region
+  w.icap = 2 * r_cap_max + 2;
+  w.items = (DdItem*)take(sizeof(DdItem) * 3 * w.icap);
   w.rrec = (int4*)take(sizeof(int4) * (r_cap_max + 1));
   w.ddeg = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
   w.bytes = off;
@@ -1275,12 +1300,10 @@ static int dedup_prepare(const Graph* g, SageWs& ws, const int64_t* R_ptr, const
   if (rc) return rc;
   k_dd_rows<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, fptr, brow, k,
                                                      ws.rslot, ws.roff, ws.rrec);
-  rc = device_exclusive_scan<int64_t>(ws.d_nw + 2, 3 * dcap,
-                                      ItemF{ws.ddeg, ws.gcnt, ws.d_nw + 1, dd_items(s)},
-                                      ws.ioff, ws.scan_ws, st);
-  if (rc) return rc;
-  k_dd_items<<<grid_for(dcap, 256, gw), 256, 0, st>>>(ws.d_nw + 1, ws.dv, ws.ddeg, g->rowptr, ws.roff,
-                                                      ws.ioff, dd_items(s), ws.items, peer);
+  GB_CUDA(cudaMemsetAsync(ws.tcnt, 0, sizeof(unsigned long long) * 4, st));
+  k_dd_items<<<grid_for(dcap, kItemThreads, gw), kItemThreads, 0, st>>>(
+      ws.d_nw + 1, ws.dv, ws.ddeg, ws.gcnt, g->rowptr, ws.roff, dd_items(s), ws.icap, ws.tcnt,
+      ws.items, peer);
   GB_LAUNCH_CHECK("dedup prepare");
   count_launches(5);  // 3d, list, rcount, rows, items (scans count themselves)
   return GB_OK;
@@ -1316,7 +1339,7 @@ static int launch_serve(DdArgs A, cudaStream_t st) {
 static int dedup_serve(const Graph* g, SageWs& ws, const SageArgs& S, bool peer_rows,
                        cudaStream_t st) {
   DdArgs A{};
-  A.D_ptr = ws.d_nw + 1; A.col = peer_rows ? nullptr : g->col; A.ioff = ws.ioff;
+  A.D_ptr = ws.d_nw + 1; A.col = peer_rows ? nullptr : g->col; A.tcnt = ws.tcnt; A.icap = ws.icap;
   A.items = ws.items;
   A.pidx = ws.pidx; A.rbf = (const int2*)ws.rrec;
   A.s = S.s; A.fcol = S.fcol; A.bitmap = S.bitmap; A.nwords = S.nwords;
