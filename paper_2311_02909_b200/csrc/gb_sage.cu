@@ -187,7 +187,7 @@ struct SageArgs {
   // dedup mode (OUT 2): frontier rows grouped by vertex, per grouped row its
   // frontier offset and batch, picks at pidx[q * s ..]
   const int64_t* D_ptr;
-  const int64_t* roff;
+  const unsigned long long* grows;  // grouped rows in total (dedup)
   const int4* rrec;
   // P-free (OUT 1) extra destinations: peer frontiers written over NVLink
   int32_t* dst[8];
@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
   __shared__ int64_t s_brow[kBrowSmem];
   // OUT 2 walks the frontier rows grouped by vertex (rows of one vertex in
   // adjacent lanes share the replay-table loads)
-  const int64_t R = OUT == 2 ? A.roff[*A.D_ptr] : *R_ptr;
+  const int64_t R = OUT == 2 ? (int64_t)*A.grows : *R_ptr;
   const bool keyed = A.rowkeys != nullptr;  // explicit keys: no batch structure
   const bool brow_in_smem = !keyed && A.k + 1 <= kBrowSmem;
   if (brow_in_smem)
@@ -573,10 +573,6 @@ __global__ void k_dd_rows(const int64_t* __restrict__ R_ptr, const int32_t* __re
   }
 }
 
-struct GcntF {
-  const int32_t* c;
-  __device__ int64_t operator()(int64_t i) const { return c[i]; }
-};
 
 // Size tiers of distinct rows (degree d): 0 warp per item (d <= 1K, row
 // staged whole, 4 KB), 1 CTA-256 per item (d <= 8K, 32 KB), 2 CTA-1024 per
@@ -639,32 +635,33 @@ constexpr int kItemThreads = 256;
 __global__ void __launch_bounds__(kItemThreads) k_dd_items(
     const int64_t* __restrict__ D_ptr, const int32_t* __restrict__ dv,
     const int32_t* __restrict__ ddeg, const int32_t* __restrict__ gcnt,
-    const int64_t* __restrict__ rowptr, const int64_t* __restrict__ roff, DdItems rows,
+    const int64_t* __restrict__ rowptr, int64_t* __restrict__ roff, DdItems rows,
     int64_t icap, unsigned long long* __restrict__ tcnt, DdItem* __restrict__ items,
     PeerRows peer) {
-  __shared__ int32_t s_wsum[3][kItemThreads / 32];
-  __shared__ int64_t s_base[3];
+  __shared__ int32_t s_wsum[4][kItemThreads / 32];
+  __shared__ int64_t s_base[4];
   const int64_t D = *D_ptr;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int64_t g0 = blockIdx.x * (int64_t)kItemThreads; g0 < D;
        g0 += (int64_t)gridDim.x * kItemThreads) {
     const int64_t g = g0 + threadIdx.x;
-    int t = 0, n = 0;
+    int t = 0, n = 0, gc = 0;
     int64_t d = 0;
     if (g < D) {
       d = ddeg[g];
       t = dd_tier(d);
-      n = (gcnt[g] + rows.rows[t] - 1) / rows.rows[t];
+      gc = gcnt[g];
+      n = (gc + rows.rows[t] - 1) / rows.rows[t];
     }
-    // per-tier exclusive offsets inside the block
-    int incl[3];
+    // per-tier item offsets and the group's row range (z = 3) inside the block
+    int incl[4];
 #pragma unroll
-    for (int z = 0; z < 3; ++z) {
-      incl[z] = warp_incl_scan(t == z ? n : 0);
+    for (int z = 0; z < 4; ++z) {
+      incl[z] = warp_incl_scan(z == 3 ? gc : t == z ? n : 0);
       if (lane == 31) s_wsum[z][wid] = incl[z];
     }
     __syncthreads();
-    if (threadIdx.x < 3) {
+    if (threadIdx.x < 4) {
       int tot = 0;
       for (int w = 0; w < kItemThreads / 32; ++w) tot += s_wsum[threadIdx.x][w];
       s_base[threadIdx.x] =
@@ -672,9 +669,10 @@ __global__ void __launch_bounds__(kItemThreads) k_dd_items(
     }
     __syncthreads();
     if (n) {
-      int64_t o0 = s_base[t] + incl[t] - n;
-      for (int w = 0; w < wid; ++w) o0 += s_wsum[t][w];
+      int64_t o0 = s_base[t] + incl[t] - n, r0 = s_base[3] + incl[3] - gc;
+      for (int w = 0; w < wid; ++w) { o0 += s_wsum[t][w]; r0 += s_wsum[3][w]; }
       o0 += (int64_t)t * icap;
+      roff[g] = r0;
       const int32_t v = dv[g];
       int64_t a0;
       if (peer.nblk) {
@@ -685,7 +683,7 @@ __global__ void __launch_bounds__(kItemThreads) k_dd_items(
       } else {
         a0 = rowptr[v];
       }
-      const int64_t r0 = roff[g], r1 = roff[g + 1], per = rows.rows[t];
+      const int64_t r1 = r0 + gc, per = rows.rows[t];
       for (int o = 0; o < n; ++o) {
         DdItem it;
         it.a0 = a0;
@@ -1209,7 +1207,7 @@ struct SageWs {
   int32_t* gcnt;     // frontier rows per distinct vertex
   int2* rslot;       // per frontier row: (group, slot in the group)
   int64_t* roff;     // group offsets into rrec
-  unsigned long long* tcnt;  // work items per tier [3]
+  unsigned long long* tcnt;  // work items per tier [3], then grouped rows in total
   int64_t icap;      // work-item capacity per tier
   DdItem* items;     // work-item descriptors
   int4* rrec;        // per grouped row: (row, degree, batch, frontier offset)
@@ -1296,14 +1294,14 @@ static int dedup_prepare(const Graph* g, SageWs& ws, const int64_t* R_ptr, const
                                                       ws.dv, ws.ddeg);
   k_dd_rcount<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, ws.vbits, ws.vpre,
                                                        ws.gcnt, ws.rslot);
-  rc = device_exclusive_scan<int64_t>(ws.d_nw + 1, dcap, GcntF{ws.gcnt}, ws.roff, ws.scan_ws, st);
-  if (rc) return rc;
-  k_dd_rows<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, fptr, brow, k,
-                                                     ws.rslot, ws.roff, ws.rrec);
+  // work items and each group's row range (roff) in one pass, then the
+  // grouped row records
   GB_CUDA(cudaMemsetAsync(ws.tcnt, 0, sizeof(unsigned long long) * 4, st));
   k_dd_items<<<grid_for(dcap, kItemThreads, gw), kItemThreads, 0, st>>>(
       ws.d_nw + 1, ws.dv, ws.ddeg, ws.gcnt, g->rowptr, ws.roff, dd_items(s), ws.icap, ws.tcnt,
       ws.items, peer);
+  k_dd_rows<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, fptr, brow, k,
+                                                     ws.rslot, ws.roff, ws.rrec);
   GB_LAUNCH_CHECK("dedup prepare");
   count_launches(5);  // 3d, list, rcount, rows, items (scans count themselves)
   return GB_OK;
@@ -1484,7 +1482,7 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     if (ldedup) {
       rc = dedup_prepare(g, ws, R_ptr, rowv, o.fptr, brow, k, s, r_cap, nwords, peer, st);
       if (rc) return rc;
-      A.D_ptr = ws.d_nw + 1; A.roff = ws.roff; A.rrec = ws.rrec;
+      A.D_ptr = ws.d_nw + 1; A.grows = ws.tcnt + 3; A.rrec = ws.rrec;
       prof_mark(st);
       launch_pick<2>(pick_grid, A, R_ptr, st);
       GB_LAUNCH_CHECK("k_sage_pick");
