@@ -339,18 +339,18 @@ def run_reference(args, rank, world):
     host cores, rank 0 only, same graph/batches/metric."""
     if rank != 0:
         return
-    import torch
+    from oracle import oracle as O
+    from paper_2311_02909_b200.graphgen import SHAPES
 
-    from paper_2311_02909_b200 import graphgen
-
-    n, m, sym = graphgen.SHAPES[args.workload]
-    dg = graphgen.rmat_device_graph(n, m, symmetric=sym, seed=0)  # input generation only
-    host = (n, dg.rowptr.cpu().numpy(), dg.col[:dg.nnz].cpu().numpy())
-    del dg
-    torch.cuda.empty_cache()
+    # the same graph the GPU arm builds (gb_rmat_graph), restated on the host
+    # (oracle/csrc/gen.c): the reference arm never loads the product library
+    n, m, sym = SHAPES[args.workload]
+    t0 = time.perf_counter()
+    rowptr, col = O.rmat_graph(n, m, symmetric=sym, seed=0)
+    t_graph = time.perf_counter() - t0
+    host = (n, rowptr, col)
     k = args.k or default_k(args.workload)
     batches = make_batches_for(n, k)
-    from oracle import oracle as O
 
     threads = os.cpu_count() or 1
     t0 = time.perf_counter()
@@ -375,7 +375,8 @@ def run_reference(args, rank, world):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": f"{args.workload}-shape R-MAT, GraphSAGE (15,10,5), b=1024",
-                   "k_per_step": kc, "n": n, "nnz": int(len(host[2]))},
+                   "k_per_step": kc, "n": n, "nnz": int(len(host[2])),
+                   "graph": f"oracle/csrc/gen.c host build, {t_graph:.1f} s (no product library)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"{kc} minibatches per step of the {k}-minibatch bulk"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

@@ -337,6 +337,35 @@ int gb_rmat_edges(uint64_t seed, int32_t scale, int64_t n, int64_t first, int64_
                   double a, double b, double c, int64_t* d_src, int64_t* d_dst, void* stream);
 int gb_hash64(uint64_t seed, const int64_t* d_x, int64_t count, int64_t* d_out, void* stream);
 
+/* ---------------------------------------------------------- ingestion
+ * gb_csr_from_edges — Graph.from_edges (sparse.py:211-216) =
+ * SparseMatrix.from_coo(n, n, src, dst, ones, dedup="first")
+ * (sparse.py:82-103) on the device: COO (int64 ids) -> canonical CSR
+ * (rowptr int64[n+1], col int32, sorted and distinct per row), by a stable
+ * LSD radix sort of the packed (src, dst) keys.  d_col needs m + GB_COL_PAD
+ * entries; the padding is zeroed.  Ids outside [0, n) -> GB_ERR_CONTRACT
+ * ("row/column index out of range", sparse.py:93-96).  Synchronises
+ * `stream` (returns the distinct edge count in *h_nnz). */
+size_t gb_csr_from_edges_workspace(int64_t n, int64_t m);
+int gb_csr_from_edges(int64_t n, int64_t m, const int64_t* d_src, const int64_t* d_dst,
+                      int64_t* d_rowptr, int32_t* d_col, int64_t* h_nnz, void* d_ws,
+                      size_t ws_bytes, void* stream);
+
+/* gb_rmat_graph — the synthetic OGB-shaped graphs of SURVEY.md §8(d) (the
+ * canonical recipe of Appendix B with counter-based draws): `candidates`
+ * R-MAT draws (Philox keyed by the draw index; ids >= n and self loops
+ * rejected; (min, max) pairs when symmetric), the first m distinct pairs in
+ * draw order, vertices relabelled by the rank of a keyed hash, reverse edges
+ * added when symmetric, CSR built as above.  h_info = (nnz, distinct pairs
+ * among the candidates); GB_ERR_CAPACITY when fewer than m distinct pairs
+ * were drawn (retry with more candidates).  col_cap >= (symmetric ? 2m : m)
+ * + GB_COL_PAD.  Synchronises `stream`.  oracle/csrc/gen.c is the host
+ * restatement (bit-identical CSR). */
+size_t gb_rmat_graph_workspace(int64_t n, int64_t m, int32_t symmetric, int64_t candidates);
+int gb_rmat_graph(uint64_t seed, int64_t n, int64_t m, int32_t symmetric, double a, double b,
+                  double c, int64_t candidates, int64_t* d_rowptr, int32_t* d_col,
+                  int64_t col_cap, int64_t* h_info, void* d_ws, size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------------- instrumentation
  * gb_launch_counter: kernels this host thread has launched through the
  * library (optionally reset).  gb_profile_begin/end: CUDA events recorded

@@ -78,8 +78,31 @@ def lib():
         L.orc_its_sample_row.argtypes = [p, i64, i64, p, p]
         L.orc_segment_sum.restype = ctypes.c_double
         L.orc_segment_sum.argtypes = [p, i64]
+        L.orc_rmat_graph.restype = i64
+        L.orc_rmat_graph.argtypes = [u64, i64, i64, ctypes.c_int, ctypes.c_double,
+                                     ctypes.c_double, ctypes.c_double,
+                                     ctypes.POINTER(ctypes.POINTER(ctypes.c_int64)),
+                                     ctypes.POINTER(ctypes.POINTER(ctypes.c_int32))]
+        L.orc_free.argtypes = [p]
         _LIB = L
     return _LIB
+
+
+def rmat_graph(n, m, symmetric=True, seed=0, a=0.57, b=0.19, c=0.19):
+    """Host restatement of the library's synthetic graph (gb_rmat_graph,
+    oracle/csrc/gen.c): (rowptr int64[n+1], col int32[nnz])."""
+    L = lib()
+    rp = ctypes.POINTER(ctypes.c_int64)()
+    cp = ctypes.POINTER(ctypes.c_int32)()
+    nnz = L.orc_rmat_graph(int(seed), int(n), int(m), int(bool(symmetric)), a, b, c,
+                           ctypes.byref(rp), ctypes.byref(cp))
+    if nnz < 0:
+        raise MemoryError("oracle rmat_graph: allocation failed")
+    rowptr = np.ctypeslib.as_array(rp, shape=(int(n) + 1,)).copy()
+    col = np.ctypeslib.as_array(cp, shape=(max(int(nnz), 1),))[: int(nnz)].copy()
+    L.orc_free(ctypes.cast(rp, ctypes.c_void_p))
+    L.orc_free(ctypes.cast(cp, ctypes.c_void_p))
+    return rowptr, col
 
 
 def _arr(ptr, n, dtype):

@@ -106,6 +106,13 @@ SIGNATURES = {
     "gb_rmat_edges": (ctypes.c_int, [_u64, _i32, _i64, _i64, _i64, ctypes.c_double,
                                      ctypes.c_double, ctypes.c_double, _p, _p, _p]),
     "gb_hash64": (ctypes.c_int, [_u64, _p, _i64, _p, _p]),
+    "gb_csr_from_edges_workspace": (ctypes.c_size_t, [_i64, _i64]),
+    "gb_csr_from_edges": (ctypes.c_int, [_i64, _i64, _p, _p, _p, _p, ctypes.POINTER(_i64), _p,
+                                         ctypes.c_size_t, _p]),
+    "gb_rmat_graph_workspace": (ctypes.c_size_t, [_i64, _i64, _i32, _i64]),
+    "gb_rmat_graph": (ctypes.c_int, [_u64, _i64, _i64, _i32, ctypes.c_double, ctypes.c_double,
+                                     ctypes.c_double, _i64, _p, _p, _i64, _p, _p, ctypes.c_size_t,
+                                     _p]),
     "gb_launch_counter": (ctypes.c_int64, [_i32]),
     "gb_profile_begin": (ctypes.c_int, [_i32]),
     "gb_profile_end": (ctypes.c_int, [_p, _i32, _p]),

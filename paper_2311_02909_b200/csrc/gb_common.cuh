@@ -83,6 +83,18 @@ __device__ __forceinline__ void philox4x32_10(uint32_t& c0, uint32_t& c1, uint32
   }
 }
 
+// Exp(1) variate E = -log(1 - V) from a 32-bit word x, V = (x + 1/2) 2^-32.
+// The race selects the SMALLEST keys E / e^2, so E must be accurate in
+// relative terms near 0: V is formed exactly (relative rounding 2^-24 at
+// most) and E = -log1p(-V) there; the upper half uses 1 - V formed exactly
+// from the complement, so neither branch cancels.  Accurate libm log1pf /
+// logf (a few ulp), never the __logf intrinsic (absolute error ~2^-21,
+// which near the selection boundary is a large fraction of E).
+__device__ __forceinline__ float race_exp(uint32_t x) {
+  if (x < 0x80000000u) return -log1pf(-(((float)x + 0.5f) * 0x1.0p-32f));
+  return -logf(((float)(0xffffffffu - x) + 0.5f) * 0x1.0p-32f);
+}
+
 // ------------------------------------------------------------ warp utils
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 

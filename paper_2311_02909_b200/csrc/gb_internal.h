@@ -42,6 +42,14 @@ constexpr int kEventRing = 8;
 cudaEvent_t ring_event(int i);
 
 int graph_build_tables(Graph* g, cudaStream_t st);
+// device COO -> CSR (gb_csr.cu)
+int bits_for(int64_t n);
+size_t radix_sort_ws(int64_t m);
+int radix_sort(uint64_t* keys, uint64_t* alt, uint32_t* vals, uint32_t* valt, int64_t m,
+               int bits, void* ws, size_t ws_bytes, bool* in_alt, cudaStream_t st);
+size_t csr_from_keys_ws(int64_t n, int64_t m);
+int csr_from_keys(uint64_t* keys, int64_t m, uint64_t end, int sb, int64_t n, int64_t* rowptr,
+                  int32_t* col, int64_t** d_nnz, void* ws, size_t ws_bytes, cudaStream_t st);
 int spmm_rows(int64_t R, const int64_t* rowptr, const int32_t* col, const int64_t* rowb,
               const int64_t* shift, int64_t k, const float* X, int64_t f, float* Y,
               cudaStream_t st);

@@ -16,7 +16,7 @@
 //                 walk back; sampler.py:176-188) with the keyed uniforms:
 //                 bit-exact, O(s N) serial per batch, small graphs;
 //               GB_LADIES_RACE — exponential race (Gumbel top-s):
-//                 key_v = -log(u_v) / e_v^2, the s smallest keys (multi-CTA
+//                 key_v = E_v / e_v^2, E_v ~ Exp(1), the s smallest keys (multi-CTA
 //                 histogram radix select).  Same law as successive sampling
 //                 without replacement; validated statistically.
 //   EXTRACT     A_S row (batch i, u) = sorted intersection A[u,:] ∩ S_i with
@@ -172,9 +172,11 @@ struct TileF {
   __device__ int64_t operator()(int64_t i) const { return t[i]; }
 };
 
-// race key of P entry (batch key, v, e): -log(u) / e^2 as float bits
-// (non-negative floats order like their bit patterns); u keyed by
-// (batch key, v) in a domain disjoint from the ITS draws (depth | 2^32).
+// race key of P entry (batch key, v, e): E / e^2 as float bits, E ~ Exp(1)
+// from a full 32-bit Philox word (race_exp: accurate in relative terms near
+// 0, where the s smallest keys are decided); non-negative floats order like
+// their bit patterns; keyed by (batch key, v) in a domain disjoint from the
+// ITS draws (depth | 2^31).  Equal keys are ordered by vertex id.
 struct RaceKey {
   uint64_t seed, epoch, depth;
   int64_t key0;  // batch_offset + g0
@@ -185,9 +187,7 @@ struct RaceKey {
              c3 = (uint32_t)depth | 0x80000000u;
     philox4x32_10(c0, c1, c2, c3, (uint32_t)seed ^ (uint32_t)(seed >> 32),
                   (uint32_t)epoch ^ (uint32_t)(epoch >> 32) ^ 0x6c616479u);
-    const float u = ((float)(c0 >> 8) + 0.5f) * 0x1.0p-24f;  // (0, 1)
-    const float fe = (float)e;
-    return __float_as_uint(-__logf(u) / (fe * fe));
+    return __float_as_uint(race_exp(c0) / ((float)e * (float)e));
   }
 };
 
@@ -922,7 +922,7 @@ __global__ void __launch_bounds__(1024) k_lad_refine(LadiesSampleArgs A,
     for (int a = threadIdx.x; a < m; a += blockDim.x)
       if (A.keys[cj[a]] == prefix) {
         const int t = atomicAdd(&s_tie, 1);
-        if (t < kTies) ties[t] = cj[a]; else atomicExch(overflow, 1);
+        if (t < kTies) ties[t] = cj[a]; else atomicOr(overflow, 1);
       }
     __syncthreads();
     const int mt = min(s_tie, kTies);
@@ -1234,6 +1234,17 @@ __global__ void k_lad_flag(const int32_t* __restrict__ overflow, int64_t* __rest
   if (*overflow) *size = -(int64_t)*overflow;
 }
 
+// counts e_v <= |Q_i| live in packed 16-bit counters: a batch of more than
+// 65535 rows is flagged (code 2) instead of silently carrying into the
+// neighbouring counter (fanouts are checked on the host)
+constexpr int64_t kMaxCount16 = 65535;
+__global__ void k_lad_qcheck(const int64_t* __restrict__ qoff, int64_t k,
+                             int32_t* __restrict__ overflow) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (qoff[i + 1] - qoff[i] > kMaxCount16) atomicOr(overflow, 2);
+}
+
 // ============================================================== host side
 
 static int gcap(int64_t n, int threads, int cap) {
@@ -1379,6 +1390,11 @@ int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t*
   }
   int64_t qc = q1_cap;
   for (int32_t l = 0; l < layers; ++l) {
+    if (fanouts[l] < 1 || fanouts[l] > kMaxCount16) {
+      set_error("ladies layer %d: fanout %lld outside 1..%lld (16-bit counts)", (int)l + 1,
+                (long long)fanouts[l], (long long)kMaxCount16);
+      return GB_ERR_UNSUPPORTED;
+    }
     if (L[l].q_cap < qc || L[l].f_cap < k * fanouts[l] || L[l].a_cap < qc * fanouts[l]) {
       set_error("ladies layer %d output too small", (int)l + 1);
       return GB_ERR_CAPACITY;
@@ -1394,7 +1410,8 @@ int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t*
   GB_CUDA(cudaMemsetAsync(ws.overflow, 0, sizeof(int32_t), st));
   k_lad_set<<<1, 1, 0, st>>>(d_k, k);
   k_lad_set<<<1, 1, 0, st>>>(d_tiles, P.tiles);
-  count_launches(2);
+  k_lad_qcheck<<<gcap(k, 256, 64), 256, 0, st>>>(d_qoff, k, ws.overflow);
+  count_launches(3);
   int tile_grid = 0;
   const size_t tile_smem = sizeof(uint32_t) * (kLTileW / 2 + kBins) +
                            (sizeof(int64_t) + 3 * sizeof(int32_t) + sizeof(int16_t)) *

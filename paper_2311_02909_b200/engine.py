@@ -35,7 +35,7 @@ def sage_caps(r1_cap, fanouts):
 class SageBulk:
     """Reusable device buffers + launcher for SAGE bulks of one shape."""
 
-    def __init__(self, dg, k, r1_cap, batch_size, fanouts, mode="stream"):
+    def __init__(self, dg, k, r1_cap, batch_size, fanouts, mode="dedup"):
         import torch
 
         self.dg, self.k, self.r1_cap = dg, int(k), int(r1_cap)
@@ -130,7 +130,7 @@ def upload_batches(batches, n, batch_size=None, sort_within=False):
     return d_off, d_cat, int(off[-1])
 
 
-def sage_epoch(G: Graph, cfg: SamplerConfig, batches, epoch, batch_offset, mode="stream"):
+def sage_epoch(G: Graph, cfg: SamplerConfig, batches, epoch, batch_offset, mode="dedup"):
     dg = G.device()
     d_off, d_cat, r1 = upload_batches(batches, G.n, cfg.batch_size)
     bulk = SageBulk(dg, len(batches), max(r1, 1), cfg.batch_size, cfg.fanouts, mode=mode)
@@ -196,8 +196,11 @@ class LadiesBulk:
         if sizes is None:
             sizes = self.sizes.cpu().numpy()
         if len(sizes) and sizes[-1] < 0:
-            raise RuntimeError(f"LADIES bulk capacity overflow (code {-int(sizes[-1])}: "
-                               "race tie list)")
+            code = -int(sizes[-1])
+            if code & 2:
+                raise ContractViolation("LADIES batch with more than 65535 vertices: counts "
+                                        "are kept in 16-bit counters")
+            raise RuntimeError(f"LADIES bulk capacity overflow (code {code}: race tie list)")
         n = self.dg.n
         out = []
         qoff, qcol = d_qoff, d_qverts
@@ -285,7 +288,7 @@ class BulkSampler:
     host numpy arrays).  With `to_host=False` the results stay in HBM.
     """
 
-    def __init__(self, G: Graph, cfg: SamplerConfig, max_batch_vertices=None, mode="stream"):
+    def __init__(self, G: Graph, cfg: SamplerConfig, max_batch_vertices=None, mode="dedup"):
         import torch
 
         if cfg.kind is not SamplerKind.SAGE:

@@ -2,20 +2,17 @@
 
 Canonical recipe: Graph500 R-MAT (a, b, c) =
 (0.57, 0.19, 0.19) over scale = ceil(log2 n) levels, reject ids >= n and self
-loops, keep m unique (undirected) pairs, random relabel, symmetrise
-(papers shape stays directed), sorted de-duplicated CSR.  Candidates come
-from the library's Philox-driven R-MAT kernel (gb_rmat_edges) and the
-relabelling from its keyed hash (gb_hash64), so every device produces the
-same graph; sorting/de-duplication uses torch on the device (plumbing).
+loops, keep the first m distinct (undirected) pairs in draw order, random
+relabel, symmetrise (papers shape stays directed), sorted de-duplicated CSR.
+Everything runs in the library (`gb_rmat_graph`: Philox-keyed candidates,
+radix sorts, scans); `oracle/csrc/gen.c` builds the identical CSR on the host.
 
-Difference from the host recipe: when more than m unique pairs were drawn,
-the m kept are the ones with the smallest keyed hash (a deterministic
-uniform subset) instead of the first m in draw order.
+Difference from the host recipe: draws come from Philox keyed by the draw
+index (parallel, identical on every device) instead of one sequential
+PCG64 stream, and the relabelling permutation is the rank of a keyed hash.
 """
 
 from __future__ import annotations
-
-import math
 
 from . import _lib
 from .sparse import DeviceGraph, Graph
@@ -28,74 +25,35 @@ SHAPES = {
 }
 
 
-def _rmat_candidates(seed, scale, n, first, count, a, b, c):
-    import torch
-
-    src = torch.empty(count, dtype=torch.int64, device="cuda")
-    dst = torch.empty(count, dtype=torch.int64, device="cuda")
-    _lib.check(_lib.lib().gb_rmat_edges(seed, scale, n, first, count, a, b, c, _lib.ptr(src),
-                                        _lib.ptr(dst), _lib.stream_ptr()), "gb_rmat_edges")
-    return src, dst
-
-
-def _hash(seed, x):
-    import torch
-
-    out = torch.empty_like(x)
-    _lib.check(_lib.lib().gb_hash64(seed, _lib.ptr(x), x.numel(), _lib.ptr(out),
-                                    _lib.stream_ptr()), "gb_hash64")
-    return out
-
-
 def rmat_device_graph(n, m, symmetric=True, seed=0, a=0.57, b=0.19, c=0.19) -> DeviceGraph:
-    """R-MAT graph with exactly m unique pairs (2m directed entries when
-    symmetric), entirely on the current CUDA device."""
+    """R-MAT graph with exactly m distinct pairs (2m directed entries when
+    symmetric), built on the current CUDA device."""
+    import ctypes
+
     import torch
 
     n, m = int(n), int(m)
-    scale = max(1, math.ceil(math.log2(n)))
-    keys = torch.empty(0, dtype=torch.int64, device="cuda")
-    first = 0
-    while keys.numel() < m:
-        need = m - keys.numel()
-        count = int(need * 1.35) + 4096
-        src, dst = _rmat_candidates(seed, scale, n, first, count, a, b, c)
-        first += count
-        ok = src >= 0
-        src, dst = src[ok], dst[ok]
-        if symmetric:
-            src, dst = torch.minimum(src, dst), torch.maximum(src, dst)
-        new = src * n + dst
-        del src, dst, ok
-        keys = torch.unique(torch.cat([keys, new]))
-        del new
-    if keys.numel() > m:
-        order = torch.argsort(_hash(seed + 1, keys))[:m]
-        keys = keys[order]
-        del order
-    # random relabel: label[v] = rank of hash(v)
-    ids = torch.arange(n, dtype=torch.int64, device="cuda")
-    perm = torch.argsort(_hash(seed + 2, ids))
-    label = torch.empty_like(perm)
-    label[perm] = ids
-    del perm, ids
-    u = label[keys // n]
-    v = label[keys % n]
-    del keys, label
-    if symmetric:
-        u, v = torch.cat([u, v]), torch.cat([v, u])
-    key = torch.sort(u * n + v).values
-    del u, v
-    src = key // n
-    rowptr = torch.zeros(n + 1, dtype=torch.int64, device="cuda")
-    rowptr[1:] = torch.cumsum(torch.bincount(src, minlength=n), 0)
-    del src
-    nnz = key.numel()
-    col = torch.zeros(nnz + _lib.GB_COL_PAD, dtype=torch.int32, device="cuda")
-    col[:nnz] = (key % n).to(torch.int32)
-    del key
+    E = 2 * m if symmetric else m
+    L = _lib.lib()
+    cand = int(m * 1.3) + 4096
+    rowptr = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    col = torch.empty(E + _lib.GB_COL_PAD, dtype=torch.int32, device="cuda")
+    info = (ctypes.c_int64 * 2)()
+    while True:
+        nbytes = L.gb_rmat_graph_workspace(n, m, int(bool(symmetric)), cand)
+        ws = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device="cuda")
+        rc = L.gb_rmat_graph(seed, n, m, int(bool(symmetric)), a, b, c, cand, _lib.ptr(rowptr),
+                             _lib.ptr(col), col.numel(), info, _lib.ptr(ws), ws.numel(),
+                             _lib.stream_ptr())
+        del ws
+        if rc == _lib.GB_ERR_CAPACITY and info[1] < m:
+            # too few distinct pairs among the candidates: draw more
+            cand = int(cand * m / max(int(info[1]), 1) * 1.05) + 4096
+            continue
+        _lib.check(rc, "gb_rmat_graph")
+        break
     torch.cuda.synchronize()
-    return DeviceGraph(n, rowptr, col, nnz)
+    return DeviceGraph(n, rowptr, col, int(info[0]))
 
 
 def synthetic_graph(shape="products", seed=0) -> Graph:

@@ -368,8 +368,11 @@ def sample_epoch_bulk(G: Graph, cfg: SamplerConfig, batches, epoch=0, batch_offs
     chunks).  prob_spgemm: the reference's hook to substitute the probability
     multiply; when given, P is materialised through it and normalised and
     sampled by the generic device kernels (ops.py), otherwise the fused
-    device path runs.  mode: "stream" (Alg. 1, P row formed on chip) or
-    "pfree" (P-free exact fast path); outputs are identical.
+    device path runs.  mode (SAGE): "dedup" (default; Alg. 1 with every
+    distinct P row formed on chip once), "stream" (Alg. 1, every P row
+    streamed) or "pfree" (P-free exact fast path); LADIES: "race" / "exact"
+    ("auto" picks exact replay on small graphs).  Outputs of the SAGE modes
+    are identical.
     """
     from . import engine
 
@@ -378,9 +381,9 @@ def sample_epoch_bulk(G: Graph, cfg: SamplerConfig, batches, epoch=0, batch_offs
         return engine.sample_epoch_generic(G, cfg, batches, epoch, batch_offset, prob_spgemm)
     if cfg.kind is SamplerKind.SAGE:
         return engine.sage_epoch(G, cfg, batches, epoch, batch_offset,
-                                 mode="stream" if mode in ("auto", None) else mode)
+                                 mode="dedup" if mode in ("auto", None) else mode)
     return engine.ladies_epoch(G, cfg, batches, epoch, batch_offset,
-                               mode="auto" if mode in ("stream", None) else mode)
+                               mode="auto" if mode in ("dedup", "stream", None) else mode)
 
 
 # -- per-row samplers of the reference sampler.py, on the GPU (ops.py) ----------

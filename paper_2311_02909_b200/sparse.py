@@ -168,46 +168,57 @@ class SparseMatrix:
 class Graph:
     """Unweighted graph as an n x n 0/1 adjacency (reference `sparse.py:194-227`).
 
-    The device copy (`device()`) is created on first use and cached.
+    `from_edges` builds the CSR on the device (`gb_csr_from_edges`); the host
+    `adjacency` SparseMatrix is materialised from the device copy on first
+    access, and the device copy (`device()`) from a host adjacency on first
+    use.
     """
 
-    __slots__ = ("adjacency", "n", "_dev")
+    __slots__ = ("_adj", "n", "_dev")
 
     def __init__(self, adjacency: SparseMatrix):
         if adjacency.n_rows != adjacency.n_cols:
             raise ContractViolation("adjacency matrix must be square")
         if adjacency.nnz and not np.all(adjacency.values == 1.0):
             raise ContractViolation("adjacency values must all equal 1.0")
-        self.adjacency = adjacency
+        self._adj = adjacency
         self.n = adjacency.n_rows
         self._dev = None
 
     @classmethod
     def from_edges(cls, n, sources, targets):
-        src = np.asarray(sources, dtype=INDEX_DTYPE)
-        dst = np.asarray(targets, dtype=INDEX_DTYPE)
-        return cls(SparseMatrix.from_coo(n, n, src, dst, np.ones(src.shape[0]), dedup="first"))
+        """Edge list -> Graph, duplicates collapsed (sparse.py:211-216), the
+        CSR built on the device."""
+        src = np.asarray(sources, dtype=INDEX_DTYPE).ravel()
+        dst = np.asarray(targets, dtype=INDEX_DTYPE).ravel()
+        if src.shape != dst.shape:
+            raise ContractViolation("sources and targets differ in length")
+        return cls.from_device(DeviceGraph.from_edges(int(n), src, dst))
 
     @classmethod
     def from_device(cls, dev: "DeviceGraph"):
-        """Wrap a graph that only lives on the device (e.g. GPU R-MAT)."""
+        """Wrap a graph that lives on the device (device ingestion, R-MAT)."""
         g = cls.__new__(cls)
         g._dev = dev
         g.n = dev.n
-        g.adjacency = None
+        g._adj = None
         return g
 
+    @property
+    def adjacency(self) -> SparseMatrix:
+        return self.host_adjacency()
+
     def host_adjacency(self) -> SparseMatrix:
-        if self.adjacency is None:
+        if self._adj is None:
             rowptr = self._dev.rowptr.cpu().numpy()
-            col = self._dev.col[: self._dev.nnz].cpu().numpy()
-            self.adjacency = SparseMatrix(self.n, self.n, rowptr, col,
-                                          np.ones(col.shape[0]), validate=False)
-        return self.adjacency
+            col = self._dev.col[: self._dev.nnz].cpu().numpy().astype(INDEX_DTYPE)
+            self._adj = SparseMatrix(self.n, self.n, rowptr, col, np.ones(col.shape[0]),
+                                     validate=False)
+        return self._adj
 
     def device(self) -> "DeviceGraph":
         if self._dev is None:
-            A = self.adjacency
+            A = self._adj
             self._dev = DeviceGraph.upload(self.n, A.row_offsets, A.col_indices)
         return self._dev
 
@@ -220,7 +231,7 @@ class Graph:
         return bool(i < len(cols) and cols[i] == v)
 
     def __repr__(self):
-        nnz = self.adjacency.nnz if self.adjacency is not None else self._dev.nnz
+        nnz = self._adj.nnz if self._adj is not None else self._dev.nnz
         return f"Graph(n={self.n}, edges={nnz})"
 
 
@@ -258,6 +269,32 @@ class DeviceGraph:
         if nnz:
             d_col[:nnz] = torch.as_tensor(np.asarray(col, dtype=np.int32)).cuda()
         return cls(n, d_ptr, d_col, nnz)
+
+    @classmethod
+    def from_edges(cls, n, src, dst):
+        """COO (host int64 arrays) -> device CSR by the library's radix sort
+        and duplicate collapse (gb_csr_from_edges)."""
+        import ctypes
+
+        import torch
+
+        from . import _lib
+
+        if n < 1:
+            raise ContractViolation("graph needs at least one vertex")
+        L = _lib.lib()
+        m = int(src.shape[0])
+        d_src = torch.as_tensor(src).cuda()
+        d_dst = torch.as_tensor(dst).cuda()
+        rowptr = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+        col = torch.zeros(m + _lib.GB_COL_PAD, dtype=torch.int32, device="cuda")
+        ws = torch.empty(max(int(L.gb_csr_from_edges_workspace(n, m)), 1), dtype=torch.uint8,
+                         device="cuda")
+        nnz = ctypes.c_int64()
+        _lib.check(L.gb_csr_from_edges(n, m, _lib.ptr(d_src), _lib.ptr(d_dst), _lib.ptr(rowptr),
+                                       _lib.ptr(col), ctypes.byref(nnz), _lib.ptr(ws),
+                                       ws.numel(), _lib.stream_ptr()), "gb_csr_from_edges")
+        return cls(n, rowptr, col, int(nnz.value))
 
     @classmethod
     def from_tensors(cls, n, rowptr, col_padded, nnz):

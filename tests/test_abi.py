@@ -54,7 +54,9 @@ def test_compute_entry_points_fail_loudly_without_cuda():
         pytest.skip("GPU present")
     import paper_2311_02909_b200 as gb
 
-    G = gb.Graph.from_edges(4, [0, 1], [1, 0])
+    with pytest.raises(RuntimeError):
+        gb.Graph.from_edges(4, [0, 1], [1, 0])  # device ingestion, no host fallback
+    G = gb.Graph(gb.SparseMatrix(4, 4, [0, 1, 2, 2, 2], [1, 0], [1.0, 1.0]))
     cfg = gb.SamplerConfig.sage(1, 2, 2)
     with pytest.raises(RuntimeError):
         gb.sample_epoch_bulk(G, cfg, [[0, 1]])

@@ -163,3 +163,70 @@ def test_ladies_race_tiled_equals_dense(scale, edges, k, b, layers, s):
     tiled = gb.sample_epoch_bulk(G, cfg, batches, mode="race", epoch=2, batch_offset=7)
     dense = gb.sample_epoch_bulk(G, cfg, batches, mode="race_dense", epoch=2, batch_offset=7)
     assert O.compare_epochs(dense.to_arrays(), tiled.to_arrays()) == []
+
+
+def _inclusion_table(race, exact, e, min_cell=20):
+    """2 x C contingency table of inclusion counts: vertices expected to be
+    picked often are their own cells, the rest pooled by count e_v (weight
+    class), classes merged upward until every cell holds >= min_cell."""
+    tot = race + exact
+    own = tot >= 4 * min_cell
+    cells_r, cells_x = list(race[own]), list(exact[own])
+    rest = ~own & (e > 0)
+    classes = np.unique(e[rest])
+    acc_r = acc_x = 0
+    for c in classes:
+        m = rest & (e == c)
+        acc_r += int(race[m].sum())
+        acc_x += int(exact[m].sum())
+        if acc_r >= min_cell and acc_x >= min_cell:
+            cells_r.append(acc_r)
+            cells_x.append(acc_x)
+            acc_r = acc_x = 0
+    if acc_r or acc_x:
+        cells_r[-1] += acc_r
+        cells_x[-1] += acc_x
+    return np.array([cells_r, cells_x], dtype=np.float64)
+
+
+@pytest.mark.parametrize("bias", ["uniform", "degree"])
+def test_ladies_race_inclusion_law_at_scale(bias):
+    """Production race (column tiles, E/e^2 keys) against the bit-exact
+    replay of its_sample_row (sampler.py:157-189, bit-exact with the
+    reference goldens above) at a cfg3-like size: one P row with >= 10^5
+    candidates, s = 512 draws, hundreds of independent repetitions (the same
+    batch repeated across the bulk: keys differ per batch index).  Per-vertex
+    inclusion frequencies (hub vertices as their own cells, the rest pooled
+    by weight class e_v) must agree by a chi-square contingency test at 1%.
+    'degree' draws the batch by degree (hub-biased, like layers >= 2 of a
+    LADIES bulk): heavy-tailed counts e_v."""
+    gb = _gb()
+    from test_sage_gpu import _rmat
+
+    n, rowptr, col = _rmat(18, 1_200_000, seed=18)
+    G = _graph(n, rowptr, col)
+    rng = np.random.default_rng(31 if bias == "uniform" else 32)
+    deg = np.diff(rowptr)
+    b, s, k = (32768 if bias == "uniform" else 8192), 512, 128
+    p = None if bias == "uniform" else deg / deg.sum()
+    batch = np.sort(rng.choice(n, b, replace=False, p=p))
+    e = np.bincount(np.concatenate([col[rowptr[u]:rowptr[u + 1]] for u in batch]), minlength=n)
+    assert (e > 0).sum() >= 100_000
+    cfg = gb.SamplerConfig.ladies(1, b, s, bulk_count=k, seed=11)
+
+    def counts(mode, bulks, epoch0):
+        c = np.zeros(n, np.int64)
+        for ep in range(epoch0, epoch0 + bulks):
+            lay = gb.sample_epoch_bulk(G, cfg, [batch] * k, epoch=ep, mode=mode).to_arrays()[0]
+            assert np.all(np.diff(lay["sampv_off"]) == s)
+            c += np.bincount(lay["sampv_cat"], minlength=n)
+        return c
+
+    race = counts("race", 6, 100)
+    exact = counts("exact", 3, 200)
+    assert race.sum() == 6 * k * s and exact.sum() == 3 * k * s
+    assert np.all(race[e == 0] == 0) and np.all(exact[e == 0] == 0)
+    table = _inclusion_table(race, exact, e)
+    assert table.shape[1] >= 20
+    chi2, pval, dof, _ = stats.chi2_contingency(table)
+    assert pval > 0.01, (chi2, dof, pval)
