@@ -365,6 +365,15 @@ size_t gb_rmat_graph_workspace(int64_t n, int64_t m, int32_t symmetric, int64_t 
 int gb_rmat_graph(uint64_t seed, int64_t n, int64_t m, int32_t symmetric, double a, double b,
                   double c, int64_t candidates, int64_t* d_rowptr, int32_t* d_col,
                   int64_t col_cap, int64_t* h_info, void* d_ws, size_t ws_bytes, void* stream);
+/* gb_rmat_block — rows [row_lo, row_hi) of the same graph as a block CSR
+ * (local rows, global column ids): the 1.5D partition's block row
+ * (partition_block_rows, dist.py:200-214) built without the other blocks
+ * resident.  The candidate selection is global (transient workspace);
+ * GB_ERR_CAPACITY with h_info[0] = block edges when col_cap is too small. */
+int gb_rmat_block(uint64_t seed, int64_t n, int64_t m, int32_t symmetric, double a, double b,
+                  double c, int64_t candidates, int64_t row_lo, int64_t row_hi,
+                  int64_t* d_rowptr, int32_t* d_col, int64_t col_cap, int64_t* h_info,
+                  void* d_ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------- instrumentation
  * gb_launch_counter: kernels this host thread has launched through the

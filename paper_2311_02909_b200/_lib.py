@@ -113,6 +113,9 @@ SIGNATURES = {
     "gb_rmat_graph": (ctypes.c_int, [_u64, _i64, _i64, _i32, ctypes.c_double, ctypes.c_double,
                                      ctypes.c_double, _i64, _p, _p, _i64, _p, _p, ctypes.c_size_t,
                                      _p]),
+    "gb_rmat_block": (ctypes.c_int, [_u64, _i64, _i64, _i32, ctypes.c_double, ctypes.c_double,
+                                     ctypes.c_double, _i64, _i64, _i64, _p, _p, _i64, _p, _p,
+                                     ctypes.c_size_t, _p]),
     "gb_launch_counter": (ctypes.c_int64, [_i32]),
     "gb_profile_begin": (ctypes.c_int, [_i32]),
     "gb_profile_end": (ctypes.c_int, [_p, _i32, _p]),

@@ -206,9 +206,9 @@ int gb_sage_bulk(const gb_graph* g, int64_t k, const int64_t* d_bptr, const int3
     return GB_ERR_CONTRACT;
   }
   for (int32_t l = 0; l < layers; ++l)
-    if (h_fanouts[l] < 1 || h_fanouts[l] > 32) {
-      set_error("sage bulk: fanout %lld outside [1, 32]", (long long)h_fanouts[l]);
-      return h_fanouts[l] < 1 ? GB_ERR_CONTRACT : GB_ERR_UNSUPPORTED;
+    if (h_fanouts[l] < 1) {
+      set_error("sage bulk: fanout %lld < 1", (long long)h_fanouts[l]);
+      return GB_ERR_CONTRACT;
     }
   if (mode != GB_SAGE_STREAM && mode != GB_SAGE_PFREE && mode != GB_SAGE_DEDUP) {
     set_error("sage bulk: unknown mode %d", mode);

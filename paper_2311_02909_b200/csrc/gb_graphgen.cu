@@ -118,20 +118,38 @@ struct MarkF {
 
 // the first m distinct pairs in draw order, relabelled, as CSR keys (and
 // their reverses at [m, 2m) when symmetric)
+// Block mode (row_hi > row_lo): an edge whose relabelled source lies outside
+// [row_lo, row_hi) becomes ~0 (dropped by the CSR build), kept sources are
+// shifted to block-local rows; *kept counts the block's edges.
 __global__ void k_emit_pairs(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals,
                              int64_t C, uint64_t end, const uint32_t* __restrict__ rank,
                              int64_t m, int sb, const int32_t* __restrict__ label,
-                             int32_t symmetric, uint64_t* __restrict__ out) {
+                             int32_t symmetric, int64_t row_lo, int64_t row_hi,
+                             uint64_t* __restrict__ out, unsigned long long* __restrict__ kept) {
   const uint64_t mask = (1ull << sb) - 1ull;
+  const bool block = row_hi > row_lo;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < C;
        i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t x = keys[i];
     if (x >= end || (i > 0 && x == keys[i - 1])) continue;
     const int64_t r = rank[vals[i]];
     if (r >= m) continue;
-    const uint64_t lu = (uint64_t)label[x >> sb], lv = (uint64_t)label[x & mask];
-    out[r] = (lu << sb) | lv;
-    if (symmetric) out[m + r] = (lv << sb) | lu;
+    const int64_t lu = label[x >> sb], lv = label[x & mask];
+    if (!block) {
+      out[r] = ((uint64_t)lu << sb) | (uint64_t)lv;
+      if (symmetric) out[m + r] = ((uint64_t)lv << sb) | (uint64_t)lu;
+      continue;
+    }
+    int nk = 0;
+    const bool ku = lu >= row_lo && lu < row_hi;
+    out[r] = ku ? ((uint64_t)(lu - row_lo) << sb) | (uint64_t)lv : ~0ull;
+    nk += ku;
+    if (symmetric) {
+      const bool kv = lv >= row_lo && lv < row_hi;
+      out[m + r] = kv ? ((uint64_t)(lv - row_lo) << sb) | (uint64_t)lu : ~0ull;
+      nk += kv;
+    }
+    if (nk) atomicAdd(kept, (unsigned long long)nk);
   }
 }
 
@@ -202,13 +220,20 @@ size_t gb_rmat_graph_workspace(int64_t n, int64_t m, int32_t symmetric, int64_t 
   return gen_layout(n, m, symmetric, candidates).bytes;
 }
 
-int gb_rmat_graph(uint64_t seed, int64_t n, int64_t m, int32_t symmetric, double a, double b,
-                  double c, int64_t candidates, int64_t* d_rowptr, int32_t* d_col,
-                  int64_t col_cap, int64_t* h_info, void* d_ws, size_t ws_bytes, void* stream) {
+static int rmat_graph(uint64_t seed, int64_t n, int64_t m, int32_t symmetric, double a, double b,
+                      double c, int64_t candidates, int64_t row_lo, int64_t row_hi,
+                      int64_t* d_rowptr, int32_t* d_col, int64_t col_cap, int64_t* h_info,
+                      void* d_ws, size_t ws_bytes, void* stream) {
   const int64_t E = symmetric ? 2 * m : m;
+  const bool block = row_hi > row_lo;
+  if (block && (row_lo < 0 || row_hi > n)) {
+    set_error("rmat block: rows [%lld, %lld) outside [0, n)", (long long)row_lo,
+              (long long)row_hi);
+    return GB_ERR_CONTRACT;
+  }
   if (n < 2 || n >= ((int64_t)1 << 31) || m < 0 || candidates < 0 ||
       candidates >= ((int64_t)1 << 32) || a < 0 || b < 0 || c < 0 || a + b + c > 1.0 ||
-      !d_rowptr || !d_col || !h_info || col_cap < E + GB_COL_PAD) {
+      !d_rowptr || !d_col || !h_info || (!block && col_cap < E + GB_COL_PAD)) {
     set_error("rmat graph: bad arguments");
     return GB_ERR_CONTRACT;
   }
@@ -277,12 +302,26 @@ int gb_rmat_graph(uint64_t seed, int64_t n, int64_t m, int32_t symmetric, double
               (long long)C, (long long)U, (long long)m);
     return GB_ERR_CAPACITY;
   }
-  k_emit_pairs<<<grid(C), 256, 0, st>>>(sk, sv, C, end, rank, m, sb, label, symmetric, keysB);
+  unsigned long long* kept = (unsigned long long*)(scal + 1);
+  GB_CUDA(cudaMemsetAsync(kept, 0, sizeof(unsigned long long), st));
+  k_emit_pairs<<<grid(C), 256, 0, st>>>(sk, sv, C, end, rank, m, sb, label, symmetric, row_lo,
+                                        row_hi, keysB, kept);
   GB_LAUNCH_CHECK("k_emit_pairs");
   count_launches(4);
+  if (block) {
+    unsigned long long h_kept = 0;
+    GB_CUDA(cudaMemcpyAsync(&h_kept, kept, sizeof(h_kept), cudaMemcpyDeviceToHost, st));
+    GB_CUDA(cudaStreamSynchronize(st));
+    if ((int64_t)h_kept + GB_COL_PAD > col_cap) {
+      h_info[0] = (int64_t)h_kept;
+      set_error("rmat block: %lld edges need col_cap >= %lld", (long long)h_kept,
+                (long long)h_kept + GB_COL_PAD);
+      return GB_ERR_CAPACITY;
+    }
+  }
   int64_t* d_nnz = nullptr;
-  rc = csr_from_keys(keysB, E, ~0ull, sb, n, d_rowptr, d_col, &d_nnz, w + L.keysA,
-                     ws_bytes - L.keysA, st);
+  rc = csr_from_keys(keysB, E, ~0ull, sb, block ? row_hi - row_lo : n, d_rowptr, d_col, &d_nnz,
+                     w + L.keysA, ws_bytes - L.keysA, st);
   if (rc) return rc;
   int64_t nnz = 0;
   GB_CUDA(cudaMemcpyAsync(&nnz, d_nnz, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -291,6 +330,25 @@ int gb_rmat_graph(uint64_t seed, int64_t n, int64_t m, int32_t symmetric, double
   GB_CUDA(cudaStreamSynchronize(st));
   h_info[0] = nnz;
   return GB_OK;
+}
+
+int gb_rmat_graph(uint64_t seed, int64_t n, int64_t m, int32_t symmetric, double a, double b,
+                  double c, int64_t candidates, int64_t* d_rowptr, int32_t* d_col,
+                  int64_t col_cap, int64_t* h_info, void* d_ws, size_t ws_bytes, void* stream) {
+  return rmat_graph(seed, n, m, symmetric, a, b, c, candidates, 0, 0, d_rowptr, d_col, col_cap,
+                    h_info, d_ws, ws_bytes, stream);
+}
+
+int gb_rmat_block(uint64_t seed, int64_t n, int64_t m, int32_t symmetric, double a, double b,
+                  double c, int64_t candidates, int64_t row_lo, int64_t row_hi,
+                  int64_t* d_rowptr, int32_t* d_col, int64_t col_cap, int64_t* h_info,
+                  void* d_ws, size_t ws_bytes, void* stream) {
+  if (row_hi <= row_lo) {
+    set_error("rmat block: empty row range");
+    return GB_ERR_CONTRACT;
+  }
+  return rmat_graph(seed, n, m, symmetric, a, b, c, candidates, row_lo, row_hi, d_rowptr, d_col,
+                    col_cap, h_info, d_ws, ws_bytes, stream);
 }
 
 }  // extern "C"

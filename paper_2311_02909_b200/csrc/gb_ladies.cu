@@ -1401,8 +1401,9 @@ int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t*
     }
     qc = k * fanouts[l];
   }
-  int sms = 0;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  int sms = 0, cur_dev = 0;
+  cudaGetDevice(&cur_dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cur_dev);
   if (sms <= 0) sms = kNumSMs;
   int64_t* d_k = ws.d_scalar;
   int64_t* d_tiles = ws.d_scalar + 1;
@@ -1428,15 +1429,19 @@ int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t*
     k_lad_tiles<<<gcap(n + 1, 256, 16 * sms), 256, 0, st>>>(g->rowptr, n, mass, ws.cpre, ws.tb,
                                                           ws.ntiles);
     GB_LAUNCH_CHECK("k_lad_tiles");
-    static int s_grid = 0;
-    if (!s_grid) {
+    // the smem attribute and the occupancy are per device
+    static int s_grid[16] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int& grid_dev = s_grid[dev < 16 ? dev : 0];
+    if (!grid_dev) {
       cudaFuncSetAttribute(k_lad_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)tile_smem);
       int occ = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_lad_tile, kLTileThreads, tile_smem);
-      s_grid = (occ > 0 ? occ : 1) * sms;
+      grid_dev = (occ > 0 ? occ : 1) * sms;
     }
-    tile_grid = s_grid;
+    tile_grid = grid_dev;
     count_launches(2);
   }
   qc = q1_cap;

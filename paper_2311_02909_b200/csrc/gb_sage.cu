@@ -269,38 +269,90 @@ __device__ __forceinline__ int64_t gt_first_gt(const GTable& t, double target) {
   return j0 + q + 1;
 }
 
-// NORM + SAMPLE, one thread per P row.  Draw t of row r uses
-// u = uniform53(seed, epoch, depth, key_r, t); n_live = deg - t live entries
-// of weight fl(1/deg); target = u * S[n_live]; the draw selects the j-th live
-// entry, j = first j with S[j] > target clamped to n_live — exactly
-// its_sample_row's cumsum/searchsorted/clamp/walk-back (sampler.py:176-188).
-// Picks are kept sorted (frontier_from_rows sorts, sampler.py:216) in
-// registers (MAXF = fanout bucket, fully unrolled).
+// Per-degree replay tables of the graph (gb_graph_create).
+struct SageTabs {
+  const int32_t* deg_slot;
+  const int32_t* run_j0;
+  const double2* run_sd;
+  const int32_t* run_n;
+  const int8_t* run_lower;
+};
+
+// NORM + SAMPLE of one P row: draw t uses u = uniform53(seed, epoch, depth,
+// key, t); n_live = deg - t live entries of weight fl(1/deg); target =
+// u * S[n_live]; the draw selects the j-th live entry, j = first j with
+// S[j] > target clamped to n_live — exactly its_sample_row's
+// cumsum/searchsorted/clamp/walk-back (sampler.py:176-188).  The picks are
+// kept sorted (frontier_from_rows sorts, sampler.py:216) in registers (MAXF
+// = fanout bucket, fully unrolled).  Requires take < deg (exhausted rows
+// take every index, sampler.py:172-174, and consume no uniform).
+template <int MAXF>
+__device__ __forceinline__ void sage_draws(const SageTabs& T, uint64_t key, int32_t deg,
+                                           int32_t take, uint64_t seed, uint64_t epoch,
+                                           uint64_t depth, int32_t (&sorted)[MAXF]) {
+  const int32_t slot = __ldg(T.deg_slot + deg);
+  GTable tab;
+  tab.j0 = T.run_j0 + (int64_t)slot * (kMaxRuns + 1);
+  tab.sd = T.run_sd + (int64_t)slot * kMaxRuns;
+  tab.lower = T.run_lower + (int64_t)slot * kBinades;
+  tab.nr = __ldg(T.run_n + slot);
+  // S[n_live] run cursor: n_live only falls, so the run of S[n_live] is
+  // carried across draws and its (j0, s0, d) reloaded only when it moves
+  int rS = tab.nr - 1;
+  int32_t j0S = __ldg(tab.j0 + rS);
+  double2 sdS = __ldg(tab.sd + rS);
+  tab.top = binade(sdS.x);
+  uint64_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;
+  for (int t = 0; t < take; ++t) {
+    if ((t & 3) == 0) {
+      w0 = key; w1 = depth; w2 = (uint64_t)(t >> 2); w3 = 0;
+      philox4x64_10(w0, w1, w2, w3, seed, epoch);
+    }
+    const uint64_t w = (t & 3) == 0 ? w0 : (t & 3) == 1 ? w1 : (t & 3) == 2 ? w2 : w3;
+    const double u = (double)(w >> 11) * 0x1.0p-53;
+    const int64_t n_live = deg - t;
+    if (j0S > n_live) {
+      do j0S = __ldg(tab.j0 + --rS); while (j0S > n_live);
+      sdS = __ldg(tab.sd + rS);
+    }
+    const double target =
+        __dmul_rn(u, __dadd_rn(sdS.x, __dmul_rn((double)(n_live - j0S), sdS.y)));
+    int64_t j = gt_first_gt(tab, target);
+    if (j > n_live) j = n_live;
+    // j-th live index: skip over the removed (sorted) ones, then insert
+    int32_t x = (int32_t)(j - 1);
+    int i = 0;
+#pragma unroll
+    for (int z = 0; z < MAXF; ++z)
+      if (z < t && sorted[z] <= x) { ++x; ++i; }
+#pragma unroll
+    for (int z = MAXF - 1; z > 0; --z)  // shift up and insert in one pass
+      sorted[z] = (z > i && z <= t) ? sorted[z - 1] : (z == i ? x : sorted[z]);
+    if (i == 0) sorted[0] = x;
+  }
+}
+
+// NORM + SAMPLE, one thread per P row (sage_draws).
 // OUT 1 (P-free): read the picked columns of A directly and finish the row;
 // OUT 0: write the row-relative indices for the row-streaming kernel.
 template <int OUT, int MAXF>
 __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
                                                           const int64_t* __restrict__ R_ptr) {
   __shared__ int64_t s_brow[kBrowSmem];
-  // OUT 2 walks the frontier rows grouped by vertex (rows of one vertex in
-  // adjacent lanes share the replay-table loads)
-  const int64_t R = OUT == 2 ? (int64_t)*A.grows : *R_ptr;
+  const int64_t R = *R_ptr;
   const bool keyed = A.rowkeys != nullptr;  // explicit keys: no batch structure
   const bool brow_in_smem = !keyed && A.k + 1 <= kBrowSmem;
   if (brow_in_smem)
     for (int64_t i = threadIdx.x; i <= A.k; i += blockDim.x) s_brow[i] = A.brow[i];
   __syncthreads();
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < R;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    int4 rec = make_int4(0, 0, 0, 0);
-    if (OUT == 2) rec = A.rrec[q];
-    const int64_t r = OUT == 2 ? (int64_t)rec.x : q;
-    const int32_t deg = OUT == 2 ? rec.y : A.deg[r];
+  const SageTabs T{A.deg_slot, A.run_j0, A.run_sd, A.run_n, A.run_lower};
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t deg = A.deg[r];
     if (deg == 0) continue;  // empty P row (sample_rows_ordered, sampler.py:202-204)
     const int32_t take = min(deg, A.s);
-    if (OUT == 2 && take == deg) continue;  // served in order by k_dd_serve
-    const int64_t fp = OUT == 2 ? 0 : A.fptr[r];
-    const int64_t bb = keyed ? 0 : OUT == 2 ? (int64_t)rec.z : batch_of(s_brow, A.brow, A.k, r);
+    const int64_t fp = A.fptr[r];
+    const int64_t bb = keyed ? 0 : batch_of(s_brow, A.brow, A.k, r);
     int32_t sorted[MAXF];
 #pragma unroll
     for (int z = 0; z < MAXF; ++z) sorted[z] = z;  // exhaustion: every index (sampler.py:172-174)
@@ -313,46 +365,7 @@ __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
         const int64_t b0 = brow_in_smem ? s_brow[bb] : A.brow[bb];
         key = (uint64_t)((A.batch_offset + bb) * A.stride + (r - b0));
       }
-      const int32_t slot = __ldg(A.deg_slot + deg);
-      GTable tab;
-      tab.j0 = A.run_j0 + (int64_t)slot * (kMaxRuns + 1);
-      tab.sd = A.run_sd + (int64_t)slot * kMaxRuns;
-      tab.lower = A.run_lower + (int64_t)slot * kBinades;
-      tab.nr = __ldg(A.run_n + slot);
-      // S[n_live] run cursor: n_live only falls, so the run of S[n_live] is
-      // carried across draws and its (j0, s0, d) reloaded only when it moves
-      int rS = tab.nr - 1;
-      int32_t j0S = __ldg(tab.j0 + rS);
-      double2 sdS = __ldg(tab.sd + rS);
-      tab.top = binade(sdS.x);
-      uint64_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;
-      for (int t = 0; t < take; ++t) {
-        if ((t & 3) == 0) {
-          w0 = key; w1 = A.depth; w2 = (uint64_t)(t >> 2); w3 = 0;
-          philox4x64_10(w0, w1, w2, w3, A.seed, A.epoch);
-        }
-        const uint64_t w = (t & 3) == 0 ? w0 : (t & 3) == 1 ? w1 : (t & 3) == 2 ? w2 : w3;
-        const double u = (double)(w >> 11) * 0x1.0p-53;
-        const int64_t n_live = deg - t;
-        if (j0S > n_live) {
-          do j0S = __ldg(tab.j0 + --rS); while (j0S > n_live);
-          sdS = __ldg(tab.sd + rS);
-        }
-        const double target =
-            __dmul_rn(u, __dadd_rn(sdS.x, __dmul_rn((double)(n_live - j0S), sdS.y)));
-        int64_t j = gt_first_gt(tab, target);
-        if (j > n_live) j = n_live;
-        // j-th live index: skip over the removed (sorted) ones, then insert
-        int32_t x = (int32_t)(j - 1);
-        int i = 0;
-#pragma unroll
-        for (int z = 0; z < MAXF; ++z)
-          if (z < t && sorted[z] <= x) { ++x; ++i; }
-#pragma unroll
-        for (int z = MAXF - 1; z > 0; --z)  // shift up and insert in one pass
-          sorted[z] = (z > i && z <= t) ? sorted[z - 1] : (z == i ? x : sorted[z]);
-        if (i == 0) sorted[0] = x;
-      }
+      sage_draws<MAXF>(T, key, deg, take, A.seed, A.epoch, A.depth, sorted);
     }
     if (OUT == 1) {
       const int64_t rs = A.rowptr[A.rowv[r]];
@@ -377,10 +390,6 @@ __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
         for (int z = 0; z < MAXF; ++z)
           if (z < take) atomicOr(bm + pk_word(cv[z]), 1u << (cv[z] & 31));
       }
-    } else if (OUT == 2) {
-#pragma unroll
-      for (int t = 0; t < MAXF; ++t)
-        if (t < take) A.pidx[q * A.s + t] = sorted[t];
     } else {
 #pragma unroll
       for (int t = 0; t < MAXF; ++t)
@@ -508,107 +517,66 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k_sage_stream(SageArgs A,
 // Frontier rows repeat vertices heavily (hub bias: 3.5M rows over 0.55M
 // distinct vertices in layer 3 at products scale), and identical rows of
 // Q^l give identical rows of P = Q^l A.  Each distinct P row is formed on
-// chip once per work item — the A row and its degree's replay table staged
-// in shared memory — and every frontier row that references it draws its
-// picks from there: NORM + SAMPLE + the P-row gather in one kernel, with no
-// per-row global table look-ups and no intermediate pick records.
+// chip once per work item — the A row staged in shared memory by a TMA bulk
+// copy (cp.async.bulk + mbarrier) — and the NORM + SAMPLE of every frontier
+// row that references it runs in the same kernel while the row lands, its
+// picks served from shared memory: no intermediate pick records.
+//
+// Grouping (three passes over the layer's rows, no vertex bitmap):
+//   k_grp_count  degree of each row; rows per vertex counted in a per-vertex
+//                counter (the row keeps its slot); a vertex's first row
+//                appends it to the distinct list
+//   k_grp_items  per distinct vertex: its work items (tier by degree) and its
+//                rows' range, reserved by block-aggregated atomics (item and
+//                row order are free: every frontier row is independent);
+//                clears the counter for the next layer
+//   k_grp_rows   16-B record (key lo, key hi, frontier offset, batch) of each
+//                row at its group's range + slot
 
-// distinct vertex list (ascending) and degrees
-__global__ void k_dd_list(int64_t nwords, const uint32_t* __restrict__ vbits,
-                          const int32_t* __restrict__ vpre, const int64_t* __restrict__ rowptr,
-                          int32_t* __restrict__ dv, int32_t* __restrict__ ddeg) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nwords;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t x = vbits[i];
-    int32_t o = vpre[i];
-    while (x) {
-      const int bit = __ffs(x) - 1;
-      const int32_t v = (int32_t)(i * 32 + bit);
-      dv[o] = v;
-      ddeg[o++] = (int32_t)(rowptr[v + 1] - rowptr[v]);
-      x &= x - 1;
-    }
-  }
-}
-
-// rows per distinct vertex; each row keeps its group and its slot in the
-// group, so the grouping pass needs no second atomic
-__global__ void k_dd_rcount(const int64_t* __restrict__ R_ptr, const int32_t* __restrict__ rowv,
-                            const int32_t* __restrict__ deg, const uint32_t* __restrict__ vbits,
-                            const int32_t* __restrict__ vpre, int32_t* __restrict__ gcnt,
-                            int2* __restrict__ rslot) {
+__global__ void k_grp_count(const int64_t* __restrict__ R_ptr, const int32_t* __restrict__ rowv,
+                            const int64_t* __restrict__ rowptr, int32_t* __restrict__ deg,
+                            int32_t* __restrict__ vcnt, int32_t* __restrict__ rslot,
+                            int32_t* __restrict__ dv, unsigned long long* __restrict__ dcount) {
   const int64_t R = *R_ptr;
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
-       r += (int64_t)gridDim.x * blockDim.x) {
-    if (deg[r] > 0) {
-      const int32_t g = vrank(vbits, vpre, rowv[r]);
-      rslot[r] = make_int2(g, atomicAdd(gcnt + g, 1));
+  const int lane = lane_id();
+  for (int64_t r0 = (int64_t)global_warp() * 32; r0 < R; r0 += (int64_t)grid_warps() * 32) {
+    const int64_t r = r0 + lane;
+    int32_t v = -1, d = 0, slot = -1;
+    if (r < R) {
+      v = rowv[r];
+      d = (int32_t)(rowptr[v + 1] - rowptr[v]);
+      deg[r] = d;
+      if (d > 0) slot = atomicAdd(vcnt + v, 1);
+      rslot[r] = slot;
+    }
+    const unsigned first = __ballot_sync(0xffffffffu, slot == 0);
+    if (first) {
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(dcount, (unsigned long long)__popc(first));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (slot == 0) dv[base + __popc(first & ((1u << lane) - 1u))] = v;
     }
   }
 }
 
-// frontier rows grouped by vertex: rrec[roff[g] ..) = (row, degree, batch,
-// frontier offset) — order inside a group is irrelevant, every row's output
-// is independent; the pick and serve kernels read the records in order
-// instead of gathering them
-__global__ void k_dd_rows(const int64_t* __restrict__ R_ptr, const int32_t* __restrict__ rowv,
-                          const int32_t* __restrict__ deg, const int64_t* __restrict__ fptr,
-                          const int64_t* __restrict__ brow, int64_t k,
-                          const int2* __restrict__ rslot, const int64_t* __restrict__ roff,
-                          int4* __restrict__ rrec) {
-  __shared__ int64_t s_brow[kBrowSmem];
-  if (k + 1 <= kBrowSmem)
-    for (int64_t i = threadIdx.x; i <= k; i += blockDim.x) s_brow[i] = brow[i];
-  __syncthreads();
-  const int64_t R = *R_ptr;
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
-       r += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t dr = deg[r];
-    if (dr > 0) {
-      const int2 gs = rslot[r];
-      const int64_t pos = roff[gs.x] + gs.y;
-      rrec[pos] = make_int4((int32_t)r, dr, (int32_t)batch_of(s_brow, brow, k, r),
-                            (int32_t)fptr[r]);
-    }
-  }
+// Work tiers by row degree d: A (d <= kTierAHi) staged whole, many rows per
+// CTA batch (k_dd_batch); B (hubs) staged in chunks, one CTA per item
+// (k_dd_hub).  An item serves at most rows_item(d) frontier rows.
+constexpr int kTierAHi = 8192;
+constexpr int kBatchThreads = 256;
+constexpr int kBatchBuf = kTierAHi + 8;  // ints: one whole tier-A row + alignment
+constexpr int kHubThreads = 1024;
+
+__host__ __device__ __forceinline__ int32_t rows_item(int64_t d, int32_t s) {
+  const int32_t p = d <= 1024 ? 512 : d <= kTierAHi ? 2048 : 8192;
+  const int32_t r = p / s;
+  return r < 1 ? 1 : (d > kTierAHi && r > kHubThreads ? kHubThreads : r);
 }
 
-
-// Size tiers of distinct rows (degree d): 0 warp per item (d <= 1K, row
-// staged whole, 4 KB), 1 CTA-256 per item (d <= 8K, 32 KB), 2 CTA-1024 per
-// item (hubs, staged in chunks as large as shared memory allows).  A work
-// item is one distinct row and the picks of at most rows_item[tier] of the
-// frontier rows that reference it (about kPicks picks).
-template <int T> struct DdTier;
-template <> struct DdTier<0> {
-  static constexpr int kThreads = 256, kHi = 1024, kPicks = 512;
-  static constexpr bool kWarp = true;
-};
-template <> struct DdTier<1> {
-  static constexpr int kThreads = 256, kHi = 8192, kPicks = 2048;
-  static constexpr bool kWarp = false;
-};
-template <> struct DdTier<2> {
-  static constexpr int kThreads = 1024, kHi = 0x7fffffff, kPicks = 8192;
-  static constexpr bool kWarp = false;
-};
-__host__ __device__ __forceinline__ int dd_tier(int64_t d) {
-  return d <= DdTier<0>::kHi ? 0 : d <= DdTier<1>::kHi ? 1 : 2;
-}
-
-struct DdItems {
-  int32_t rows[3];  // rows per work item, per tier
-};
-
-__global__ void k_dd_3d(const int32_t* __restrict__ dcount, int64_t* __restrict__ out) {
-  out[0] = *dcount;      // D
-  out[1] = 3 * *dcount;  // tier-major item index space
-}
-
-// Work-item descriptor: everything the serve kernel needs before its first
-// load, in one 32-B record (no dependent look-up chain per item).
+// Work-item descriptor: everything the serve kernels need before the first
+// load, in one 32-B record.
 struct __align__(16) DdItem {
-  int64_t a0;     // A row start
+  int64_t a0;     // A row start (index into col, or peer address / 4)
   int32_t d;      // A row length
   int32_t q0;     // first grouped row
   int32_t nrows;  // grouped rows served
@@ -624,44 +592,42 @@ struct PeerRows {
   const int32_t* const* bcol;
 };
 
-// descriptors of every tier's items: tier t's items live in region
-// [t * icap, t * icap + tcnt[t]); a block reserves its items of each tier with
-// one atomic per tier (item order inside a tier is free — every frontier
-// row's output is independent), so no prefix pass over the groups is needed
-// a0: index of the row's first entry in the graph's column array, or with a
-// peer row source the row's address in its block owner's memory / 4 (the
-// serve kernel then addresses rows from a null base)
+// tier t's items live in [t * icap, t * icap + tcnt[t]); tcnt[2] counts the
+// grouped rows
 constexpr int kItemThreads = 256;
-__global__ void __launch_bounds__(kItemThreads) k_dd_items(
-    const int64_t* __restrict__ D_ptr, const int32_t* __restrict__ dv,
-    const int32_t* __restrict__ ddeg, const int32_t* __restrict__ gcnt,
-    const int64_t* __restrict__ rowptr, int64_t* __restrict__ roff, DdItems rows,
-    int64_t icap, unsigned long long* __restrict__ tcnt, DdItem* __restrict__ items,
+__global__ void __launch_bounds__(kItemThreads) k_grp_items(
+    const unsigned long long* __restrict__ dcount, const int32_t* __restrict__ dv,
+    const int64_t* __restrict__ rowptr, int32_t* __restrict__ vcnt, int32_t* __restrict__ roff,
+    int32_t s, int64_t icap, unsigned long long* __restrict__ tcnt, DdItem* __restrict__ items,
     PeerRows peer) {
-  __shared__ int32_t s_wsum[4][kItemThreads / 32];
-  __shared__ int64_t s_base[4];
-  const int64_t D = *D_ptr;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __shared__ int32_t s_wsum[3][kItemThreads / 32];
+  __shared__ int64_t s_base[3];
+  const int64_t D = (int64_t)*dcount;
+  const int lane = lane_id(), wid = threadIdx.x >> 5;
   for (int64_t g0 = blockIdx.x * (int64_t)kItemThreads; g0 < D;
        g0 += (int64_t)gridDim.x * kItemThreads) {
     const int64_t g = g0 + threadIdx.x;
-    int t = 0, n = 0, gc = 0;
-    int64_t d = 0;
+    int t = 0, n = 0, gc = 0, v = 0, per = 1;
+    int64_t d = 0, a0 = 0;
     if (g < D) {
-      d = ddeg[g];
-      t = dd_tier(d);
-      gc = gcnt[g];
-      n = (gc + rows.rows[t] - 1) / rows.rows[t];
+      v = dv[g];
+      a0 = rowptr[v];
+      d = rowptr[v + 1] - a0;
+      gc = vcnt[v];
+      vcnt[v] = 0;  // ready for the next layer
+      t = d <= kTierAHi ? 0 : 1;
+      per = rows_item(d, s);
+      n = (gc + per - 1) / per;
     }
-    // per-tier item offsets and the group's row range (z = 3) inside the block
-    int incl[4];
+    // per-tier item offsets and the group's row range (z = 2) inside the block
+    int incl[3];
 #pragma unroll
-    for (int z = 0; z < 4; ++z) {
-      incl[z] = warp_incl_scan(z == 3 ? gc : t == z ? n : 0);
+    for (int z = 0; z < 3; ++z) {
+      incl[z] = warp_incl_scan(z == 2 ? gc : t == z ? n : 0);
       if (lane == 31) s_wsum[z][wid] = incl[z];
     }
     __syncthreads();
-    if (threadIdx.x < 4) {
+    if (threadIdx.x < 3) {
       int tot = 0;
       for (int w = 0; w < kItemThreads / 32; ++w) tot += s_wsum[threadIdx.x][w];
       s_base[threadIdx.x] =
@@ -669,27 +635,23 @@ __global__ void __launch_bounds__(kItemThreads) k_dd_items(
     }
     __syncthreads();
     if (n) {
-      int64_t o0 = s_base[t] + incl[t] - n, r0 = s_base[3] + incl[3] - gc;
-      for (int w = 0; w < wid; ++w) { o0 += s_wsum[t][w]; r0 += s_wsum[3][w]; }
+      int64_t o0 = s_base[t] + incl[t] - n, r0 = s_base[2] + incl[2] - gc;
+      for (int w = 0; w < wid; ++w) { o0 += s_wsum[t][w]; r0 += s_wsum[2][w]; }
       o0 += (int64_t)t * icap;
-      roff[g] = r0;
-      const int32_t v = dv[g];
-      int64_t a0;
+      roff[v] = (int32_t)r0;
       if (peer.nblk) {
         int b = 0;
         while (b + 1 < peer.nblk && peer.bounds[b + 1] <= v) ++b;
         const int64_t* brp = peer.brp[b];
         a0 = ((int64_t)(uintptr_t)(peer.bcol[b] + brp[v - peer.bounds[b]])) >> 2;
-      } else {
-        a0 = rowptr[v];
       }
-      const int64_t r1 = r0 + gc, per = rows.rows[t];
+      const int64_t r1 = r0 + gc;
       for (int o = 0; o < n; ++o) {
         DdItem it;
         it.a0 = a0;
         it.d = (int32_t)d;
-        it.q0 = (int32_t)(r0 + o * per);
-        it.nrows = (int32_t)min(per, r1 - it.q0);
+        it.q0 = (int32_t)(r0 + (int64_t)o * per);
+        it.nrows = (int32_t)min((int64_t)per, r1 - it.q0);
         it.pad[0] = it.pad[1] = it.pad[2] = 0;
         items[o0 + o] = it;
       }
@@ -698,24 +660,74 @@ __global__ void __launch_bounds__(kItemThreads) k_dd_items(
   }
 }
 
-struct DdArgs {
-  const int64_t* D_ptr;  // (col == nullptr: item a0 is an address / 4, peer rows)
-  const int32_t* col;
-  const unsigned long long* tcnt;  // items per tier; tier t's at [t * icap, ..)
-  int64_t icap;
-  const DdItem* items;
-  const int32_t* pidx;   // sorted picks of grouped row q at pidx[q * s ..]
-  const int2* rbf;       // (batch, frontier offset) of grouped row q at [2q + 1]
-  int32_t s;
-  int32_t chunk;         // A-row entries staged per pass
-  int32_t* fcol;
-  uint32_t* bitmap;
-  int64_t nwords;
-};
+__global__ void k_grp_rows(const int64_t* __restrict__ R_ptr, const int32_t* __restrict__ rowv,
+                           const int32_t* __restrict__ deg, const int64_t* __restrict__ fptr,
+                           const int64_t* __restrict__ brow, int64_t k,
+                           const int64_t* __restrict__ rowkeys, int64_t batch_offset,
+                           int64_t stride, const int32_t* __restrict__ rslot,
+                           const int32_t* __restrict__ roff, int4* __restrict__ rrec) {
+  __shared__ int64_t s_brow[kBrowSmem];
+  const bool sm = k + 1 <= kBrowSmem;
+  if (sm)
+    for (int64_t i = threadIdx.x; i <= k; i += blockDim.x) s_brow[i] = brow[i];
+  __syncthreads();
+  const int64_t R = *R_ptr;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    if (deg[r] > 0) {
+      const int32_t pos = roff[rowv[r]] + rslot[r];
+      int64_t b = 0, key;
+      if (rowkeys) {
+        key = rowkeys[r];
+      } else {
+        b = batch_of(s_brow, brow, k, r);
+        key = (batch_offset + b) * stride + (r - (sm ? s_brow[b] : brow[b]));
+      }
+      rrec[pos] = make_int4((int32_t)(uint32_t)key, (int32_t)((uint64_t)key >> 32),
+                            (int32_t)fptr[r], (int32_t)b);
+    }
+  }
+}
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+// ---------------------------------------------------------------- staging
+// One-dimensional TMA: cp.async.bulk global -> shared, completion counted in
+// bytes on an mbarrier (arrive.expect_tx by one thread, try_wait.parity by
+// all).  Rows are staged from their 16-B aligned start to the 16-B aligned
+// end (col arrays are 16-B aligned and padded by GB_COL_PAD).
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_row(void* smem, const void* gmem, uint32_t bytes,
+                                        uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(smem)),
+      "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 // staged entries of an A row (16-B granules from the aligned start)
@@ -723,180 +735,240 @@ __device__ __forceinline__ int dd_row_len(int64_t a0, int32_t d) {
   return (int)(((a0 + d) - (a0 & ~3LL) + 3) & ~3LL);
 }
 
-// Warp tier, batched: a warp takes 32 consecutive work items (one
-// descriptor per lane), packs as many of their rows as fit into its buffer
-// (one cp.async group), and serves all their picks lane-parallel — pair p
-// of the group finds its item by a search over the per-warp group table.
-// Per-item latency chains and instruction overhead are amortised over the
-// group (layer-3 tier-0 items carry ~12 picks each).
-constexpr int kGrpInts = 6 * 33;
+struct DdArgs {
+  const int32_t* col;              // nullptr: item a0 is a peer address / 4
+  const unsigned long long* tcnt;  // items per tier; tier t's at [t * icap, ..)
+  int64_t icap;
+  const DdItem* items;
+  const int4* rrec;                // grouped rows: (key lo, key hi, frontier offset, batch)
+  SageTabs T;
+  int32_t s;
+  uint64_t seed, epoch, depth;
+  int32_t* fcol;
+  uint32_t* bitmap;
+  int64_t nwords;
+  unsigned int* ticket;            // k_dd_batch work counter (zeroed per layer)
+  int32_t chunk;                   // k_dd_hub: A-row entries staged per pass
+};
 
-__device__ void dd_serve_warp(const DdArgs& A, int32_t* buf, int B, int32_t* gi) {
-  int32_t* g_pst = gi;            // pair start per item (+ sentinel)
-  int32_t* g_rof = gi + 33;       // row base in buf (16-B alignment shift included)
-  int32_t* g_q0 = gi + 66;        // first grouped row
-  int32_t* g_tk = gi + 99;        // take, negated when take == d (every entry)
-  uint32_t* g_mg = (uint32_t*)(gi + 132);  // ceil(2^32 / take)
-  // 32-bit indexing: frontier entries, grouped rows * s and k * nwords are
-  // all < 2^31 (host checks)
-  const int lane = lane_id(), s = A.s;
+// picks of grouped row q (take < d: sage_draws; take == d: every index)
+template <int MAXF>
+__device__ __forceinline__ void dd_row_picks(const DdArgs& A, const int4 rec, int32_t d,
+                                             int32_t take, int32_t (&sorted)[MAXF]) {
+#pragma unroll
+  for (int z = 0; z < MAXF; ++z) sorted[z] = z;
+  if (take < d) {
+    const uint64_t key = (uint64_t)(uint32_t)rec.x | ((uint64_t)(uint32_t)rec.y << 32);
+    sage_draws<MAXF>(A.T, key, d, take, A.seed, A.epoch, A.depth, sorted);
+  }
+}
+
+// frontier entries and (batch, vertex) bits of one row from its staged copy
+// (buf[idx + sh] holds entry idx; entries outside [lo, hi) are skipped)
+template <int MAXF>
+__device__ __forceinline__ void dd_row_serve(const DdArgs& A, const int4 rec, int32_t take,
+                                             const int32_t (&sorted)[MAXF], const int32_t* buf,
+                                             int32_t sh, int32_t lo, int32_t hi) {
   const uint32_t NW = (uint32_t)A.nwords;
-  const int64_t D = *A.D_ptr;
-  const int64_t i0 = 0, it1 = (int64_t)A.tcnt[0];
-  (void)D;
-  const int64_t nblk = (it1 - i0 + 31) / 32;
-  for (int64_t blk = global_warp(); blk < nblk; blk += grid_warps()) {
-    const int64_t it = i0 + blk * 32 + lane;
-    const int nitems = (int)min((int64_t)32, it1 - (i0 + blk * 32));
-    DdItem c{};
-    const bool valid = lane < nitems;
-    if (valid) c = A.items[it];
-    const int len = valid ? dd_row_len(c.a0, c.d) : 0;
-    const int take = valid ? min(c.d, s) : 0;
-    const int np = valid ? c.nrows * take : 0;
-    for (int j0 = 0; j0 < nitems;) {
-      // sub-group [j0, j1): rows packed while they fit (always at least one)
-      const int lz = lane >= j0 ? len : 0;
-      const int incl = warp_incl_scan(lz);
-      const unsigned fit = __ballot_sync(0xffffffffu, lane >= j0 && lane < nitems && incl <= B);
-      const int j1 = fit ? 32 - __clz(fit) : j0 + 1;
-      const bool in = lane >= j0 && lane < j1;
-      const int pz = in ? np : 0;
-      const int pinc = warp_incl_scan(pz);
-      const int P = __shfl_sync(0xffffffffu, pinc, j1 - 1);
-      if (in) {
-        const int j = lane - j0;
-        g_pst[j] = pinc - pz;
-        g_rof[j] = incl - lz + (int)(c.a0 & 3);
-        g_q0[j] = c.q0;
-        g_tk[j] = take == c.d ? -take : take;
-        g_mg[j] = 0xffffffffu / (uint32_t)take + 1u;
-      }
-      if (lane == 0) g_pst[j1 - j0] = P;
-      for (int j = j0; j < j1; ++j) {
-        const int64_t a0 = __shfl_sync(0xffffffffu, c.a0, j);
-        const int32_t d = __shfl_sync(0xffffffffu, c.d, j);
-        const int o = __shfl_sync(0xffffffffu, incl - lz, j);
-        const int64_t al0 = a0 & ~3LL;
-        for (int64_t e = al0 + 4 * lane; e < a0 + d; e += 128)
-          cp_async16(buf + o + (int)(e - al0), A.col + e);
-      }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      __syncwarp();
-      const int ng = j1 - j0;
-      auto meta = [&](int p, int32_t& idx, int32_t& fp, int32_t& bb, int32_t& t, int32_t& ro) {
-        int lo = 0, hi = ng;
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (g_pst[mid] <= p) lo = mid; else hi = mid;
+  uint32_t* bm = A.bitmap + (uint32_t)rec.w * NW;
+  int32_t* out = A.fcol + (uint32_t)rec.z;
+#pragma unroll
+  for (int z = 0; z < MAXF; ++z) {
+    if (z < take && sorted[z] >= lo && sorted[z] < hi) {
+      const int32_t cv = buf[sorted[z] + sh];
+      out[z] = cv;
+      atomicOr(bm + pk_word(cv), 1u << (cv & 31));
+    }
+  }
+}
+
+// Tier A: a CTA takes chunks of 256 work items (ticket order), packs as many
+// of their rows as fit into its buffer (one TMA bulk copy per row, one
+// mbarrier), computes the picks of every frontier row of the packed items
+// (thread per row, 256 at a time) while the rows land, then serves them
+// from shared memory.  Rows of an item are found by a search over the
+// block's row prefix.
+template <int MAXF>
+__global__ void __launch_bounds__(kBatchThreads) k_dd_batch(DdArgs A) {
+  __shared__ __align__(128) int32_t buf[kBatchBuf];
+  __shared__ int32_t s_len[kBatchThreads];   // inclusive prefix of staged lengths
+  __shared__ int32_t s_row[kBatchThreads];   // inclusive prefix of rows
+  __shared__ int32_t s_q0[kBatchThreads], s_d[kBatchThreads], s_sh[kBatchThreads];
+  __shared__ int32_t s_wsum[2][kBatchThreads / 32];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ unsigned int s_ticket;
+  const int tid = threadIdx.x, lane = lane_id(), wid = tid >> 5;
+  if (tid == 0) mbar_init(&bar, 1);
+  __syncthreads();
+  uint32_t phase = 0;
+  const int64_t nit = (int64_t)A.tcnt[0];
+  const int s = A.s;
+  for (;;) {
+    if (tid == 0) s_ticket = atomicAdd(A.ticket, 1u);
+    __syncthreads();
+    const int64_t c0 = (int64_t)s_ticket * kBatchThreads;
+    if (c0 >= nit) break;
+    const int cnt = (int)min((int64_t)kBatchThreads, nit - c0);
+    DdItem it{};
+    int len = 0, nr = 0;
+    if (tid < cnt) {
+      it = A.items[c0 + tid];
+      len = dd_row_len(it.a0, it.d);
+      nr = it.nrows;
+    }
+    // block inclusive scans of (staged length, rows)
+    int il = warp_incl_scan(len), ir = warp_incl_scan(nr);
+    if (lane == 31) { s_wsum[0][wid] = il; s_wsum[1][wid] = ir; }
+    __syncthreads();
+    for (int w = 0; w < wid; ++w) { il += s_wsum[0][w]; ir += s_wsum[1][w]; }
+    s_len[tid] = il;
+    s_row[tid] = ir;
+    s_q0[tid] = it.q0;
+    s_d[tid] = it.d;
+    __syncthreads();
+    for (int j0 = 0; j0 < cnt;) {
+      const int lbase = j0 ? s_len[j0 - 1] : 0, rbase = j0 ? s_row[j0 - 1] : 0;
+      // sub-batch [j0, j1): the items whose rows fit the buffer (>= 1)
+      const int fit = __syncthreads_count(tid >= j0 && tid < cnt && il - lbase <= kBatchBuf);
+      const int j1 = j0 + (fit > 0 ? fit : 1);
+      const uint32_t bytes = 4u * (uint32_t)(s_len[j1 - 1] - lbase);
+      if (tid >= j0 && tid < j1) {
+        const int off = il - len - lbase;  // 16-B aligned (lengths are multiples of 4)
+        s_sh[tid] = off + (int)(it.a0 & 3);
+        if (tid == j0) {
+          fence_async_smem();
+          mbar_expect_tx(&bar, bytes);
         }
-        const int tk = g_tk[lo], tkn = tk < 0 ? -tk : tk;
-        const int r = p - g_pst[lo];
-        const int i = tkn == 1 ? r : (int)__umulhi((uint32_t)r, g_mg[lo]);
-        t = r - i * tkn;
-        const int q = g_q0[lo] + i;
-        idx = tk < 0 ? t : A.pidx[q * s + t];
-        const int2 bf = A.rbf[2 * q + 1];
-        bb = bf.x;
-        fp = bf.y;
-        ro = g_rof[lo];
-      };
-      int32_t idx = 0, fp = 0, bb = 0, t = 0, ro = 0;
-      if (lane < P) meta(lane, idx, fp, bb, t, ro);
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-      __syncwarp();
-      for (int p0 = 0; p0 < P; p0 += 32) {
-        int32_t idx2 = 0, fp2 = 0, bb2 = 0, t2 = 0, ro2 = 0;
-        if (p0 + 32 + lane < P) meta(p0 + 32 + lane, idx2, fp2, bb2, t2, ro2);
-        if (p0 + lane < P) {
-          const int32_t cv = buf[ro + idx];
-          A.fcol[(uint32_t)(fp + t)] = cv;
-          atomicOr(A.bitmap + ((uint32_t)bb * NW + pk_word(cv)), 1u << (cv & 31));
-        }
-        idx = idx2; fp = fp2; bb = bb2; t = t2; ro = ro2;
       }
-      __syncwarp();  // buffer and group table free
+      __syncthreads();  // expect_tx before any completion; s_sh visible
+      if (tid >= j0 && tid < j1)
+        tma_row(buf + (il - len - lbase), A.col + (it.a0 & ~3LL), 4u * (uint32_t)len, &bar);
+      const int NR = s_row[j1 - 1] - rbase;
+      for (int p0 = 0; p0 < NR; p0 += kBatchThreads) {
+        const int p = p0 + tid;
+        int4 rec = make_int4(0, 0, 0, 0);
+        int32_t d = 0, take = 0, sh = 0;
+        int32_t sorted[MAXF];
+        if (p < NR) {
+          int lo = j0, hi = j1 - 1;  // first item with s_row > rbase + p
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (s_row[mid] > rbase + p) hi = mid; else lo = mid + 1;
+          }
+          const int q = s_q0[lo] + (rbase + p - (lo ? s_row[lo - 1] : 0));
+          rec = A.rrec[q];
+          d = s_d[lo];
+          sh = s_sh[lo];
+          take = min(d, s);
+          dd_row_picks<MAXF>(A, rec, d, take, sorted);
+        }
+        if (p0 == 0) mbar_wait(&bar, phase);
+        if (p < NR) dd_row_serve<MAXF>(A, rec, take, sorted, buf, sh, 0, d);
+      }
+      phase ^= 1u;
+      __syncthreads();  // buffer free for the next sub-batch
       j0 = j1;
     }
   }
 }
 
-// Q^l A for the distinct rows: per work item, A row v staged in shared
-// memory (16-B cp.async; buf[e - (e0 & ~3)]) — the P row on chip once —
-// then every pick of the item's frontier rows is served from it: frontier
-// write and the (batch, vertex) bit.  The next item's descriptor and each
-// pass's pick metadata are loaded while the staged row is in flight.
-template <int TIER>
-__global__ void __launch_bounds__(DdTier<TIER>::kThreads) k_dd_serve(DdArgs A) {
-  constexpr bool CTA = !DdTier<TIER>::kWarp;
-  extern __shared__ __align__(16) int32_t sbuf[];
-  if constexpr (!CTA) {
-    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    dd_serve_warp(A, sbuf + w * (A.chunk + 8), A.chunk + 8,
-                  sbuf + nw * (A.chunk + 8) + w * kGrpInts);
-    return;
-  }
+// Tier B (hubs, d > kTierAHi): one CTA of 1024 threads per work item; every
+// thread computes one frontier row's picks, then the row is staged in
+// chunks of A.chunk entries (TMA bulk copies) and each chunk serves the
+// picks that fall into it.
+template <int MAXF>
+__global__ void __launch_bounds__(kHubThreads) k_dd_hub(DdArgs A) {
+  extern __shared__ __align__(128) int32_t hbuf[];
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x;
+  if (tid == 0) mbar_init(&bar, 1);
+  __syncthreads();
+  uint32_t phase = 0;
+  const int64_t it1 = A.icap + (int64_t)A.tcnt[1];
   const int chunk = A.chunk, s = A.s;
-  const int tid = CTA ? threadIdx.x : lane_id();
-  const int nthr = CTA ? blockDim.x : 32;
-  int32_t* buf = sbuf + (CTA ? 0 : (threadIdx.x >> 5) * (chunk + 8));
-  const int64_t D = *A.D_ptr;
-  const int64_t it1 = TIER * A.icap + (int64_t)A.tcnt[TIER];
-  (void)D;
-  const int64_t step = CTA ? gridDim.x : grid_warps();
-  int64_t it = TIER * A.icap + (CTA ? blockIdx.x : global_warp());
-  DdItem cur;
-  if (it < it1) cur = A.items[it];
-  for (; it < it1; it += step) {
-    DdItem nxt;
-    if (it + step < it1) nxt = A.items[it + step];
-    const int64_t a0 = cur.a0;
-    const int32_t d = cur.d, nrows = cur.nrows;
-    const int64_t q0 = cur.q0;
-    const int32_t take = min(d, s);
-    const bool all = take == d;  // exhaustion: every entry, in order
-    const int npairs = nrows * take;
-    for (int64_t c0 = 0; c0 < d; c0 += chunk) {
-      const int64_t c1 = min(c0 + (int64_t)chunk, (int64_t)d);
-      const int64_t al0 = (a0 + c0) & ~3LL;
-      for (int64_t e = al0 + 4 * tid; e < a0 + c1; e += 4 * nthr)
-        cp_async16(buf + (e - al0), A.col + e);
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      // first pass's pick metadata while the row lands
-      int p = tid;
-      int32_t idx = 0, fp = 0, bb = 0, t = 0;
-      if (p < npairs) {
-        const int i = p / take;
-        t = p - i * take;
-        idx = all ? t : A.pidx[(q0 + i) * s + t];
-        const int2 bf = A.rbf[2 * (q0 + i) + 1];
-        bb = bf.x;
-        fp = bf.y;
+  for (int64_t i = A.icap + blockIdx.x; i < it1; i += gridDim.x) {
+    const DdItem it = A.items[i];
+    const int32_t d = it.d, take = min(d, s);
+    int4 rec = make_int4(0, 0, 0, 0);
+    int32_t sorted[MAXF];
+    for (int32_t c0 = 0; c0 < d; c0 += chunk) {
+      const int32_t c1 = min(c0 + chunk, d);
+      const int64_t al0 = (it.a0 + c0) & ~3LL;
+      if (tid == 0) {
+        const uint32_t bytes = 4u * (uint32_t)dd_row_len(it.a0 + c0, c1 - c0);
+        fence_async_smem();
+        mbar_expect_tx(&bar, bytes);
+        tma_row(hbuf, A.col + al0, bytes, &bar);
       }
-      asm volatile("cp.async.wait_all;" ::: "memory");
-      if (CTA) __syncthreads(); else __syncwarp();
-      const int32_t sh = (int32_t)((a0 + c0) - al0 - c0);  // buf[idx + sh], idx in [c0, c1)
-      while (p < npairs) {
-        const int pn = p + nthr;
-        int32_t idx2 = 0, fp2 = 0, bb2 = 0, t2 = 0;
-        if (pn < npairs) {
-          const int i = pn / take;
-          t2 = pn - i * take;
-          idx2 = all ? t2 : A.pidx[(q0 + i) * s + t2];
-          const int2 bf = A.rbf[2 * (q0 + i) + 1];
-          bb2 = bf.x;
-          fp2 = bf.y;
-        }
-        if (idx >= c0 && idx < c1) {
-          const int32_t c = buf[idx + sh];
-          A.fcol[fp + t] = c;
-          atomicOr(A.bitmap + (int64_t)bb * A.nwords + pk_word(c), 1u << (c & 31));
-        }
-        p = pn; idx = idx2; fp = fp2; bb = bb2; t = t2;
+      if (c0 == 0 && tid < it.nrows) {
+        rec = A.rrec[it.q0 + tid];
+        dd_row_picks<MAXF>(A, rec, d, take, sorted);
       }
-      if (CTA) __syncthreads(); else __syncwarp();
+      mbar_wait(&bar, phase);
+      phase ^= 1u;
+      if (tid < it.nrows)
+        dd_row_serve<MAXF>(A, rec, take, sorted, hbuf, (int32_t)(it.a0 + c0 - al0) - c0, c0, c1);
+      __syncthreads();  // buffer free
     }
-    cur = nxt;
+  }
+}
+
+// Fanouts above 32 (no register-resident pick list): thread per frontier
+// row, the sorted picks kept in the row's own frontier slot (insertion,
+// O(s^2) per row), then replaced by their columns — P-free, same output.
+__global__ void __launch_bounds__(kPickThreads) k_sage_pick_big(SageArgs A,
+                                                              const int64_t* __restrict__ R_ptr) {
+  const int64_t R = *R_ptr;
+  const SageTabs T{A.deg_slot, A.run_j0, A.run_sd, A.run_n, A.run_lower};
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t deg = A.deg[r];
+    if (deg == 0) continue;
+    const int32_t take = min(deg, A.s);
+    int32_t* sl = A.fcol + A.fptr[r];
+    if (take == deg) {
+      for (int z = 0; z < take; ++z) sl[z] = z;
+    } else {
+      const int64_t b = batch_of(A.brow, A.brow, A.k, r);
+      const uint64_t key = (uint64_t)((A.batch_offset + b) * A.stride + (r - A.brow[b]));
+      const int32_t slot = __ldg(T.deg_slot + deg);
+      GTable tab;
+      tab.j0 = T.run_j0 + (int64_t)slot * (kMaxRuns + 1);
+      tab.sd = T.run_sd + (int64_t)slot * kMaxRuns;
+      tab.lower = T.run_lower + (int64_t)slot * kBinades;
+      tab.nr = __ldg(T.run_n + slot);
+      tab.top = binade(__ldg(tab.sd + tab.nr - 1).x);
+      uint64_t w4[4] = {0, 0, 0, 0};
+      for (int t = 0; t < take; ++t) {
+        if ((t & 3) == 0) {
+          w4[0] = key; w4[1] = A.depth; w4[2] = (uint64_t)(t >> 2); w4[3] = 0;
+          philox4x64_10(w4[0], w4[1], w4[2], w4[3], A.seed, A.epoch);
+        }
+        const double u = (double)(w4[t & 3] >> 11) * 0x1.0p-53;
+        const int64_t n_live = deg - t;
+        // S[n_live] through the table (first j with S[j] > S[n_live] - 0 is
+        // n_live + 1, so S[n_live] = value of run holding n_live)
+        int rS = tab.nr - 1;
+        while (__ldg(tab.j0 + rS) > n_live) --rS;
+        const double2 sdS = __ldg(tab.sd + rS);
+        const double target = __dmul_rn(
+            u, __dadd_rn(sdS.x, __dmul_rn((double)(n_live - __ldg(tab.j0 + rS)), sdS.y)));
+        int64_t j = gt_first_gt(tab, target);
+        if (j > n_live) j = n_live;
+        int32_t x = (int32_t)(j - 1);
+        int i = 0;
+        while (i < t && sl[i] <= x) { ++x; ++i; }
+        for (int z = t; z > i; --z) sl[z] = sl[z - 1];
+        sl[i] = x;
+      }
+    }
+    const int64_t rs = A.rowptr[A.rowv[r]];
+    const int64_t b = A.bitmap ? batch_of(A.brow, A.brow, A.k, r) : 0;
+    for (int z = 0; z < take; ++z) {
+      const int32_t cv = __ldg(A.col + rs + sl[z]);
+      sl[z] = cv;
+      if (A.bitmap) atomicOr(A.bitmap + b * A.nwords + pk_word(cv), 1u << (cv & 31));
+    }
   }
 }
 
@@ -1189,29 +1261,24 @@ int graph_build_tables(Graph* g, cudaStream_t st) {
 
 // ---------------------------------------------------------- workspace plan
 struct SageWs {
-  int32_t* pidx;
+  int32_t* pidx;     // stream mode: row-relative picks
   int32_t* deg;
   int64_t* gstart;
   int64_t* scan_ws;
   uint32_t* bitmap;   // (batch, vertex) bits and their popcount prefix, two sets:
-  int32_t* wpre;      // layer l's extraction overlaps layer l + 1's sampling
-  uint32_t* bitmap2;
-  int32_t* wpre2;
+  uint32_t* bitmap2;  // layer l's extraction overlaps layer l + 1's sampling
   int64_t* scan_ws2;  // scans of the extraction stream
   int64_t* d_W;
   // dedup mode
-  uint32_t* vbits;   // one bit per vertex
-  int32_t* vpre;     // popcount prefix of vbits
-  int64_t* d_nw;     // device scalars: nwords, D
-  int32_t* dv;       // distinct vertices
-  int32_t* gcnt;     // frontier rows per distinct vertex
-  int2* rslot;       // per frontier row: (group, slot in the group)
-  int64_t* roff;     // group offsets into rrec
-  unsigned long long* tcnt;  // work items per tier [3], then grouped rows in total
+  int32_t* vcnt;     // [n] rows per vertex (zero between layers)
+  int32_t* roff;     // [n] group row range start per vertex
+  int32_t* rslot;    // per frontier row: slot in its vertex group
+  int32_t* dv;       // distinct row vertices (unordered)
+  unsigned long long* cnts;  // [0] distinct count, [1..3] tier items, grouped rows
+  unsigned int* ticket;      // k_dd_batch work counter
   int64_t icap;      // work-item capacity per tier
   DdItem* items;     // work-item descriptors
-  int4* rrec;        // per grouped row: (row, degree, batch, frontier offset)
-  int32_t* ddeg;     // degree per distinct vertex
+  int4* rrec;        // per grouped row: (key lo, key hi, frontier offset, batch)
   size_t bytes;
 };
 
@@ -1231,24 +1298,19 @@ static SageWs sage_ws_layout(char* base, int64_t k, int64_t n, int64_t r_cap_max
   w.gstart = (int64_t*)take(sizeof(int64_t) * (r_cap_max + 1));
   w.scan_ws = (int64_t*)take(sizeof(int64_t) * scan_workspace_elems<int64_t>(scan_n + 1));
   w.bitmap = (uint32_t*)take(sizeof(uint32_t) * (W + 8));
-  w.wpre = (int32_t*)take(sizeof(int32_t) * (W + 1));
   w.bitmap2 = (uint32_t*)take(sizeof(uint32_t) * (W + 8));
-  w.wpre2 = (int32_t*)take(sizeof(int32_t) * (W + 1));
   w.scan_ws2 = (int64_t*)take(sizeof(int64_t) * scan_workspace_elems<int64_t>(W + 1));
   w.d_W = (int64_t*)take(sizeof(int64_t));
-  w.vbits = (uint32_t*)take(sizeof(uint32_t) * (nwords + 1));
-  w.vpre = (int32_t*)take(sizeof(int32_t) * (nwords + 1));
-  w.d_nw = (int64_t*)take(sizeof(int64_t) * 3);
+  w.vcnt = (int32_t*)take(sizeof(int32_t) * (n + 1));
+  w.roff = (int32_t*)take(sizeof(int32_t) * (n + 1));
+  w.rslot = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
   w.dv = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
-  w.gcnt = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
-  w.rslot = (int2*)take(sizeof(int2) * (r_cap_max + 1));
-  w.roff = (int64_t*)take(sizeof(int64_t) * (r_cap_max + 1));
-  w.tcnt = (unsigned long long*)take(sizeof(unsigned long long) * 4);
-  // items <= groups + rows / 32 <= 2 * rows, per tier region
+  w.cnts = (unsigned long long*)take(sizeof(unsigned long long) * 8);
+  w.ticket = (unsigned int*)take(sizeof(unsigned int) * 8);
+  // items <= groups + rows / rows_item(min) <= 2 * rows, per tier region
   w.icap = 2 * r_cap_max + 2;
-  w.items = (DdItem*)take(sizeof(DdItem) * 3 * w.icap);
+  w.items = (DdItem*)take(sizeof(DdItem) * 2 * w.icap);
   w.rrec = (int4*)take(sizeof(int4) * (r_cap_max + 1));
-  w.ddeg = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
   w.bytes = off;
   return w;
 }
@@ -1257,99 +1319,109 @@ __global__ void k_sage_eoff(const int64_t* __restrict__ brow, int64_t k,
                             const int64_t* __restrict__ fptr, int64_t* __restrict__ eoff);
 
 template <typename K>
-static int persistent_grid(K kernel, int threads);
-
-__global__ void k_i32_to_i64(const int32_t* __restrict__ src, int64_t* __restrict__ dst) {
-  *dst = *src;
+static int persistent_grid(K kernel, int threads, size_t smem = 0) {
+  int o = 0, dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kernel, threads, smem);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return (o < 1 ? 1 : o) * (sms > 0 ? sms : kNumSMs);
 }
 
-struct VPopF {
-  const uint32_t* b;
-  __device__ int64_t operator()(int64_t i) const { return __popc(b[i]); }
+// Per-device launch configuration of the serve kernels (attributes are per
+// device; grids from the occupancy of the current device).
+constexpr int kMaxDevices = 16;
+struct ServeCfg {
+  bool init = false;
+  int batch_grid[5] = {0, 0, 0, 0, 0};
+  int hub_grid[5] = {0, 0, 0, 0, 0};
+  int hub_chunk = 0;
+  size_t hub_smem = 0;
 };
+static ServeCfg g_serve[kMaxDevices];
 
-static DdItems dd_items(int32_t s) {
-  DdItems it;
-  it.rows[0] = max(1, DdTier<0>::kPicks / s);
-  it.rows[1] = max(1, DdTier<1>::kPicks / s);
-  it.rows[2] = max(1, DdTier<2>::kPicks / s);
-  return it;
+template <int MAXF>
+static void serve_setup(ServeCfg& c, int bucket) {
+  c.batch_grid[bucket] = persistent_grid(k_dd_batch<MAXF>, kBatchThreads);
+  cudaFuncSetAttribute(k_dd_hub<MAXF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)c.hub_smem);
+  c.hub_grid[bucket] = persistent_grid(k_dd_hub<MAXF>, kHubThreads, c.hub_smem);
 }
 
-// Dedup step 1: distinct row vertices, the frontier rows of each grouped
-// together, and the tier-major work items of the serve kernels.
-static int dedup_prepare(const Graph* g, SageWs& ws, const int64_t* R_ptr, const int32_t* rowv,
-                         const int64_t* fptr, const int64_t* brow, int64_t k, int32_t s,
-                         int64_t r_cap, int64_t nwords, const PeerRows& peer, cudaStream_t st) {
-  const int64_t gw = 16 * kNumSMs;
-  // (vertex bitmap already marked by k_sage_prep)
-  // distinct row vertices D <= min(rows, n): group arrays sized by that
-  const int64_t dcap = r_cap < g->n ? r_cap : g->n;
-  GB_CUDA(cudaMemsetAsync(ws.gcnt, 0, sizeof(int32_t) * (dcap + 1), st));
-  int rc = device_exclusive_scan<int64_t>(ws.d_nw, nwords, VPopF{ws.vbits}, ws.vpre, ws.scan_ws,
-                                          st);
-  if (rc) return rc;
-  k_dd_3d<<<1, 1, 0, st>>>(ws.vpre + nwords, ws.d_nw + 1);
-  k_dd_list<<<grid_for(nwords, 256, gw), 256, 0, st>>>(nwords, ws.vbits, ws.vpre, g->rowptr,
-                                                      ws.dv, ws.ddeg);
-  k_dd_rcount<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, ws.vbits, ws.vpre,
-                                                       ws.gcnt, ws.rslot);
-  // work items and each group's row range (roff) in one pass, then the
-  // grouped row records
-  GB_CUDA(cudaMemsetAsync(ws.tcnt, 0, sizeof(unsigned long long) * 4, st));
-  k_dd_items<<<grid_for(dcap, kItemThreads, gw), kItemThreads, 0, st>>>(
-      ws.d_nw + 1, ws.dv, ws.ddeg, ws.gcnt, g->rowptr, ws.roff, dd_items(s), ws.icap, ws.tcnt,
-      ws.items, peer);
-  k_dd_rows<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, fptr, brow, k,
-                                                     ws.rslot, ws.roff, ws.rrec);
-  GB_LAUNCH_CHECK("dedup prepare");
-  count_launches(5);  // 3d, list, rcount, rows, items (scans count themselves)
-  return GB_OK;
-}
-
-template <int T>
-static int launch_serve(DdArgs A, cudaStream_t st) {
-  using Tr = DdTier<T>;
-  static int max_smem = 0;
-  if (!max_smem) {
-    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, 0);
+static ServeCfg& serve_cfg() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  ServeCfg& c = g_serve[dev < kMaxDevices ? dev : 0];
+  if (!c.init) {
+    int max_smem = 0;
+    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (max_smem <= 0) max_smem = 227 * 1024;
-    cudaFuncSetAttribute(k_dd_serve<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+    // hub chunk: all of shared memory but the static mbarrier
+    c.hub_chunk = ((max_smem - 256) / 4 - 8) & ~3;
+    c.hub_smem = sizeof(int32_t) * (c.hub_chunk + 8);
+    serve_setup<5>(c, 0);
+    serve_setup<8>(c, 1);
+    serve_setup<10>(c, 2);
+    serve_setup<16>(c, 3);
+    serve_setup<32>(c, 4);
+    c.init = true;
   }
-  // chunk: the whole row for tiers 0 / 1, all of shared memory for hubs
-  A.chunk = T == 2 ? ((max_smem / 4 - 8) & ~3) : Tr::kHi;
-  const size_t smem = sizeof(int32_t) * (A.chunk + 8 + (Tr::kWarp ? kGrpInts : 0)) *
-                      (Tr::kWarp ? Tr::kThreads / 32 : 1);
-  static int grid = 0;  // smem is fixed per tier
-  if (!grid) {
-    int occ = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_dd_serve<T>, Tr::kThreads, smem);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    grid = (occ > 0 ? occ : 1) * (sms > 0 ? sms : kNumSMs);
-  }
-  k_dd_serve<T><<<grid, Tr::kThreads, smem, st>>>(A);
-  GB_LAUNCH_CHECK("k_dd_serve");
-  return GB_OK;
+  return c;
 }
 
-// Dedup step 2 (after k_sage_pick<2> wrote the grouped picks): each
-// distinct row on chip, three size tiers.
-static int dedup_serve(const Graph* g, SageWs& ws, const SageArgs& S, bool peer_rows,
-                       cudaStream_t st) {
+static int fan_bucket(int32_t s) { return s <= 5 ? 0 : s <= 8 ? 1 : s <= 10 ? 2 : s <= 16 ? 3 : 4; }
+
+template <int MAXF>
+static void launch_serve_maxf(const DdArgs& A, const ServeCfg& c, int b, cudaStream_t st,
+                              cudaStream_t hs) {
+  k_dd_batch<MAXF><<<c.batch_grid[b], kBatchThreads, 0, st>>>(A);
+  k_dd_hub<MAXF><<<c.hub_grid[b], kHubThreads, c.hub_smem, hs>>>(A);
+}
+
+// One dedup layer: grouping (count, items, rows), then the fused NORM +
+// SAMPLE + serve kernels (tier A batched, tier B hubs on a forked stream;
+// they touch disjoint frontier entries and commutative bitmap ORs).
+static int dedup_layer(const Graph* g, SageWs& ws, const int64_t* R_ptr, const int32_t* rowv,
+                       const int64_t* fptr, const int64_t* brow, int64_t k, int32_t s,
+                       int64_t stride, int64_t batch_offset, uint64_t seed, uint64_t epoch,
+                       uint64_t depth, int64_t r_cap, const PeerRows& peer, int32_t* fcol,
+                       uint32_t* bitmap, int64_t nwords8, cudaStream_t st) {
+  const int64_t gw = 16 * kNumSMs;
+  k_grp_items<<<grid_for(r_cap < g->n ? r_cap : g->n, kItemThreads, gw), kItemThreads, 0, st>>>(
+      ws.cnts, ws.dv, g->rowptr, ws.vcnt, ws.roff, s, ws.icap, ws.cnts + 1, ws.items, peer);
+  k_grp_rows<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, fptr, brow, k,
+                                                      nullptr, batch_offset, stride, ws.rslot,
+                                                      ws.roff, ws.rrec);
+  GB_LAUNCH_CHECK("dedup grouping");
   DdArgs A{};
-  A.D_ptr = ws.d_nw + 1; A.col = peer_rows ? nullptr : g->col; A.tcnt = ws.tcnt; A.icap = ws.icap;
+  A.col = peer.nblk ? nullptr : g->col;
+  A.tcnt = ws.cnts + 1;
+  A.icap = ws.icap;
   A.items = ws.items;
-  A.pidx = ws.pidx; A.rbf = (const int2*)ws.rrec;
-  A.s = S.s; A.fcol = S.fcol; A.bitmap = S.bitmap; A.nwords = S.nwords;
-  // the tiers touch disjoint frontier entries (and commutative bitmap ORs):
-  // run them concurrently so each tier's tail overlaps the others
-  fork_begin(st, 2);
-  int rc = launch_serve<0>(A, st);
-  if (!rc) rc = launch_serve<1>(A, fork_stream(0));
-  if (!rc) rc = launch_serve<2>(A, fork_stream(1));
-  fork_join(st, 2);
-  count_launches(3);
-  return rc;
+  A.rrec = ws.rrec;
+  A.T = SageTabs{g->deg_slot, g->run_j0, g->run_sd, g->run_n, g->run_lower};
+  A.s = s;
+  A.seed = seed; A.epoch = epoch; A.depth = depth;
+  A.fcol = fcol;
+  A.bitmap = bitmap;
+  A.nwords = nwords8;
+  A.ticket = ws.ticket;
+  const ServeCfg& c = serve_cfg();
+  A.chunk = c.hub_chunk;
+  prof_mark(st);
+  cudaStream_t hs = fork_begin(st, 1);
+  const int b = fan_bucket(s);
+  switch (b) {
+    case 0: launch_serve_maxf<5>(A, c, b, st, hs); break;
+    case 1: launch_serve_maxf<8>(A, c, b, st, hs); break;
+    case 2: launch_serve_maxf<10>(A, c, b, st, hs); break;
+    case 3: launch_serve_maxf<16>(A, c, b, st, hs); break;
+    default: launch_serve_maxf<32>(A, c, b, st, hs); break;
+  }
+  GB_LAUNCH_CHECK("k_dd_batch / k_dd_hub");
+  fork_join(st, 1);
+  prof_mark(st);
+  count_launches(4);  // items, rows, batch, hub
+  return GB_OK;
 }
 
 static int64_t sage_rcap_max(int64_t r1_cap, int32_t layers, const int64_t* fanouts) {
@@ -1377,18 +1449,13 @@ int sage_workspace(const Graph* g, int64_t k, int64_t r1_cap, int32_t layers,
   return GB_OK;
 }
 
-template <typename K>
-static int persistent_grid(K kernel, int threads) {
-  int o = 0, sms = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kernel, threads, 0);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  return (o < 1 ? 1 : o) * (sms > 0 ? sms : kNumSMs);
-}
-
 static int stream_grid() {
-  static int g = 0;
-  if (!g) g = persistent_grid(k_sage_stream, kStreamThreads);
-  return g;
+  static int g[kMaxDevices] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& x = g[dev < kMaxDevices ? dev : 0];
+  if (!x) x = persistent_grid(k_sage_stream, kStreamThreads);
+  return x;
 }
 
 int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d_bverts,
@@ -1437,9 +1504,9 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
   }
   GB_CUDA(cudaMemsetAsync(ws.bitmap, 0, sizeof(uint32_t) * (W + 8), st));
   GB_CUDA(cudaMemsetAsync(ws.bitmap2, 0, sizeof(uint32_t) * (W + 8), st));
+  if (dedup) GB_CUDA(cudaMemsetAsync(ws.vcnt, 0, sizeof(int32_t) * (g->n + 1), st));
   k_set_i64<<<1, 1, 0, st>>>(ws.d_W, NS);
-  k_set_i64<<<1, 1, 0, st>>>(ws.d_nw, nwords);
-  count_launches(2);
+  count_launches(1);
   // extraction of layer l (popcount scan, rank, enumerate) runs on a side
   // stream while layer l + 1 samples; layer l + 2 reuses layer l's bitmap
   // only after that extraction (ring events) — graph-capturable
@@ -1450,50 +1517,51 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     const int32_t d = l + 1;
     if (l > 0) stride *= fanouts[l - 1];
     gb_sage_layer_out& o = L[l];
-    // layer 1's rows are the batch vertices, all distinct: the duplicate-row
-    // pass has nothing to merge there, every P row is streamed on chip once
-    const bool ldedup = dedup && (l > 0 || peer.nblk);
-    const bool lstream = stream || (dedup && !ldedup);
+    const int32_t s = (int32_t)fanouts[l];
+    // fanouts above 32 take the P-free thread-per-row kernel in every mode
+    const bool big = s > 32;
+    const bool ldedup = dedup && !big;
+    const bool lstream = stream && !big;
     const int32_t* rowv = l == 0 ? d_bverts : L[l - 1].fcol;
     const int64_t* brow = l == 0 ? d_bptr : L[l - 1].eoff;
     const int64_t* R_ptr = brow + k;
-    const int32_t s = (int32_t)fanouts[l];
     uint32_t* bm = (l & 1) ? ws.bitmap2 : ws.bitmap;
     if (l >= 2) GB_CUDA(cudaStreamWaitEvent(st, ring_event(l - 2), 0));
-    if (ldedup) GB_CUDA(cudaMemsetAsync(ws.vbits, 0, sizeof(uint32_t) * (nwords + 1), st));
-    k_sage_prep<<<grid_for(r_cap, 256, 16 * kNumSMs), 256, 0, st>>>(R_ptr, rowv, g->rowptr, ws.deg,
-                                                                     ldedup ? ws.vbits : nullptr);
-    GB_LAUNCH_CHECK("k_sage_prep");
+    if (ldedup) {
+      GB_CUDA(cudaMemsetAsync(ws.cnts, 0, sizeof(unsigned long long) * 8, st));
+      GB_CUDA(cudaMemsetAsync(ws.ticket, 0, sizeof(unsigned int) * 8, st));
+      k_grp_count<<<grid_for(r_cap, 256, 16 * kNumSMs), 256, 0, st>>>(
+          R_ptr, rowv, g->rowptr, ws.deg, ws.vcnt, ws.rslot, ws.dv, ws.cnts);
+      GB_LAUNCH_CHECK("k_grp_count");
+    } else {
+      k_sage_prep<<<grid_for(r_cap, 256, 16 * kNumSMs), 256, 0, st>>>(R_ptr, rowv, g->rowptr,
+                                                                       ws.deg, nullptr);
+      GB_LAUNCH_CHECK("k_sage_prep");
+    }
     int rc = device_exclusive_scan<int64_t>(R_ptr, r_cap, TakeF{ws.deg, s}, o.fptr, ws.scan_ws, st);
     if (rc) return rc;
     if (lstream) {
       rc = device_exclusive_scan<int64_t>(R_ptr, r_cap, DegF{ws.deg}, ws.gstart, ws.scan_ws, st);
       if (rc) return rc;
     }
-    SageArgs A{};
-    A.rowptr = g->rowptr; A.col = g->col;
-    A.deg_slot = g->deg_slot; A.run_j0 = g->run_j0; A.run_sd = g->run_sd;
-    A.run_n = g->run_n; A.run_lower = g->run_lower;
-    A.rowv = rowv; A.deg = ws.deg; A.fptr = o.fptr; A.gstart = ws.gstart;
-    A.brow = brow; A.k = k; A.s = s; A.stride = stride; A.batch_offset = batch_offset;
-    A.seed = seed; A.epoch = epoch; A.depth = (uint64_t)d;
-    A.bitmap = bm; A.nwords = nw8; A.fcol = o.fcol; A.pidx = ws.pidx;
-    const int pick_grid = grid_for(r_cap, kPickThreads, 64 * kNumSMs);
     if (ldedup) {
-      rc = dedup_prepare(g, ws, R_ptr, rowv, o.fptr, brow, k, s, r_cap, nwords, peer, st);
+      rc = dedup_layer(g, ws, R_ptr, rowv, o.fptr, brow, k, s, stride, batch_offset, seed, epoch,
+                       (uint64_t)d, r_cap, peer, o.fcol, bm, nw8, st);
       if (rc) return rc;
-      A.D_ptr = ws.d_nw + 1; A.grows = ws.tcnt + 3; A.rrec = ws.rrec;
-      prof_mark(st);
-      launch_pick<2>(pick_grid, A, R_ptr, st);
-      GB_LAUNCH_CHECK("k_sage_pick");
-      prof_mark(st);
-      prof_mark(st);
-      rc = dedup_serve(g, ws, A, peer.nblk > 0, st);
-      if (rc) return rc;
-      prof_mark(st);
     } else {
+      SageArgs A{};
+      A.rowptr = g->rowptr; A.col = g->col;
+      A.deg_slot = g->deg_slot; A.run_j0 = g->run_j0; A.run_sd = g->run_sd;
+      A.run_n = g->run_n; A.run_lower = g->run_lower;
+      A.rowv = rowv; A.deg = ws.deg; A.fptr = o.fptr; A.gstart = ws.gstart;
+      A.brow = brow; A.k = k; A.s = s; A.stride = stride; A.batch_offset = batch_offset;
+      A.seed = seed; A.epoch = epoch; A.depth = (uint64_t)d;
+      A.bitmap = bm; A.nwords = nw8; A.fcol = o.fcol; A.pidx = ws.pidx;
+      const int pick_grid = grid_for(r_cap, kPickThreads, 64 * kNumSMs);
       prof_mark(st);
-      if (lstream)
+      if (big)
+        k_sage_pick_big<<<pick_grid, kPickThreads, 0, st>>>(A, R_ptr);
+      else if (lstream)
         launch_pick<0>(pick_grid, A, R_ptr, st);
       else
         launch_pick<1>(pick_grid, A, R_ptr, st);
@@ -1506,6 +1574,7 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
         prof_mark(st);
         count_launches(1);
       }
+      count_launches(1);
     }
     // next layer's batch row offsets, on the sampling stream
     k_sage_eoff<<<grid_for(k + 1, 128, 64), 128, 0, st>>>(brow, k, o.fptr, o.eoff);
@@ -1528,7 +1597,7 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
                                                                        o.colv);
     GB_LAUNCH_CHECK("k_sage_enumerate8");
     GB_CUDA(cudaEventRecord(ring_event(l), xs));
-    count_launches(6);  // prep, sample, eoff, cols, rank, enumerate
+    count_launches(5);  // prep/count, eoff, cols, rank, enumerate
     r_cap = f_cap;
   }
   stream_wait(st, xs);

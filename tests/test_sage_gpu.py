@@ -224,3 +224,45 @@ def test_sage_per_edge_inclusion_law():
           for h in hits.values()]
     # 24 independent tests at 1%: allow one rejection
     assert sum(p < 0.01 for p in pv) <= 1
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("fan", [(40, 3), (7, 100), (33,)])
+def test_sage_fanouts_above_32(mode, fan):
+    """The reference has no fanout cap (sampler.py:56-66): fanouts above 32
+    run the thread-per-row kernel with the sorted picks in the frontier slot;
+    bit-exact with the oracle in every mode."""
+    gb = _pkg()
+    rng = np.random.default_rng(len(fan) + fan[0])
+    n, rowptr, col = _rmat(12, 60000, seed=4)
+    G = _graph(n, rowptr, col)
+    b, k = 48, 4
+    batches = [rng.permutation(n)[: rng.integers(1, b + 1)] for _ in range(k)]
+    cfg = gb.SamplerConfig.sage(len(fan), b, fan, bulk_count=k, seed=17)
+    ep = gb.sample_epoch_bulk(G, cfg, batches, epoch=1, batch_offset=2, mode=mode)
+    want = O.sage_bulk(n, rowptr, col, batches, b, fan, 17, 1, 2)
+    assert O.compare_epochs(want, ep.to_arrays()) == []
+
+
+def test_sage_hub_rows_dedup_matches_oracle():
+    """Rows longer than the tier-A buffer (hub kernel: chunked TMA staging)
+    and rows exactly at the tier boundaries, every mode bit-exact."""
+    gb = _pkg()
+    rng = np.random.default_rng(77)
+    n = 60000
+    hubs = {0: 20000, 1: 8192, 2: 8193, 3: 1024, 4: 1025, 5: 70000}
+    src, dst = [], []
+    for h, d in hubs.items():
+        nb = rng.choice(np.arange(6, n), size=min(d, n - 6), replace=False)
+        src += [h] * len(nb) + list(nb)
+        dst += list(nb) + [h] * len(nb)
+    src = np.array(src)
+    dst = np.array(dst)
+    A = gb.SparseMatrix.from_coo(n, n, src, dst, np.ones(src.size), dedup="first")
+    G = gb.Graph(A)
+    batches = [np.array([0, 1, 2, 3, 4, 5, 7, 9]), np.arange(6, 300), np.array([5, 5, 0, 1])]
+    cfg = gb.SamplerConfig.sage(3, 300, (15, 10, 5), bulk_count=3, seed=2)
+    want = O.sage_bulk(n, A.row_offsets, A.col_indices, batches, 300, (15, 10, 5), 2, 0, 0)
+    for mode in MODES:
+        ep = gb.sample_epoch_bulk(G, cfg, batches, mode=mode)
+        assert O.compare_epochs(want, ep.to_arrays()) == [], mode
