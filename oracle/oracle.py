@@ -192,9 +192,13 @@ def uniform(seed, epoch, depth, row, t):
 # -- golden fixtures ----------------------------------------------------------
 
 
-def load_golden(path):
-    """Load an epoch fixture written by tests/golden/make_golden.py."""
+def load_golden(path, prefix=""):
+    """Load an epoch fixture written by tests/golden/make_golden.py (keys
+    under `prefix` for the epochs inside pipeline.npz)."""
     z = np.load(path)
+    if prefix:
+        z = {k[len(prefix):]: v for k, v in z.items() if k.startswith(prefix)} | {
+            k: v for k, v in z.items() if k.startswith("A_")}
     layers = []
     for li in range(int(z["n_layers"])):
         p = f"L{li}_"
@@ -202,6 +206,9 @@ def load_golden(path):
         for key in LAYER_KEYS:
             d[key] = z[p + key]
         layers.append(d)
+    if prefix:
+        return {"n": int(z["A_shape"][0]), "rowptr": z["A_ptr"], "col": z["A_col"],
+                "kind": str(z["kind"])}, layers
     g = {
         "n": int(z["A_shape"][0]),
         "rowptr": z["A_ptr"],

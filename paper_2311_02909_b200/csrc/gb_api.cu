@@ -1,3 +1,4 @@
+#include <stdlib.h>
 // extern "C" boundary of libgnnbulk_b200.so (include/gnnbulk_b200.h).
 #include <stdarg.h>
 #include <stdio.h>
@@ -81,6 +82,15 @@ void fork_join(cudaStream_t st, int n) {
     cudaEventRecord(f.ev[i], f.s[i]);
     cudaStreamWaitEvent(st, f.ev[i], 0);
   }
+}
+
+bool sync_debug() {
+  static int flag = -1;
+  if (flag < 0) {
+    const char* v = getenv("GB_SYNC_DEBUG");
+    flag = (v && v[0] == '1') ? 1 : 0;
+  }
+  return flag == 1;
 }
 
 int cuda_status(cudaError_t e, const char* what) {

@@ -18,9 +18,14 @@ int cuda_status(cudaError_t e, const char* what);
     cudaError_t _e = (call);                             \
     if (_e != cudaSuccess) return gb::cuda_status(_e, #call); \
   } while (0)
+// GB_SYNC_DEBUG=1 in the environment: every checked launch also
+// synchronises the device and reports a fault against the launch that
+// caused it (debugging only; breaks CUDA-graph capture).
+bool sync_debug();
 #define GB_LAUNCH_CHECK(what)                                      \
   do {                                                             \
     cudaError_t _e = cudaGetLastError();                           \
+    if (_e == cudaSuccess && gb::sync_debug()) _e = cudaDeviceSynchronize(); \
     if (_e != cudaSuccess) return gb::cuda_status(_e, what);       \
   } while (0)
 

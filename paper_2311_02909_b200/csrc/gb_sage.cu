@@ -517,60 +517,86 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k_sage_stream(SageArgs A,
 // Frontier rows repeat vertices heavily (hub bias: 3.5M rows over 0.55M
 // distinct vertices in layer 3 at products scale), and identical rows of
 // Q^l give identical rows of P = Q^l A.  Each distinct P row is formed on
-// chip once per work item — the A row staged in shared memory by a TMA bulk
-// copy (cp.async.bulk + mbarrier) — and the NORM + SAMPLE of every frontier
-// row that references it runs in the same kernel while the row lands, its
-// picks served from shared memory: no intermediate pick records.
+// chip once per work item — the A row staged in shared memory by TMA bulk
+// copies (cp.async.bulk + mbarrier, double-buffered) — and the picks of
+// every frontier row that references it are served from there.
 //
 // Grouping (three passes over the layer's rows, no vertex bitmap):
 //   k_grp_count  degree of each row; rows per vertex counted in a per-vertex
 //                counter (the row keeps its slot); a vertex's first row
-//                appends it to the distinct list
+//                appends it to the distinct list (block-aggregated)
 //   k_grp_items  per distinct vertex: its work items (tier by degree) and its
 //                rows' range, reserved by block-aggregated atomics (item and
 //                row order are free: every frontier row is independent);
 //                clears the counter for the next layer
-//   k_grp_rows   16-B record (key lo, key hi, frontier offset, batch) of each
-//                row at its group's range + slot
+//   k_grp_rows   16-B record (local row, degree, frontier offset, batch) of
+//                each row at its group's range + slot
+// then NORM + SAMPLE per grouped row (k_dd_pick, whole-GPU thread per row,
+// rows of one vertex in adjacent lanes share the replay-table loads) and
+// the serve kernel (k_dd_serve: short rows packed into bins, long rows cut
+// into chunk bins, TMA ring with a producer warp).
 
-__global__ void k_grp_count(const int64_t* __restrict__ R_ptr, const int32_t* __restrict__ rowv,
-                            const int64_t* __restrict__ rowptr, int32_t* __restrict__ deg,
-                            int32_t* __restrict__ vcnt, int32_t* __restrict__ rslot,
-                            int32_t* __restrict__ dv, unsigned long long* __restrict__ dcount) {
+constexpr int kGrpThreads = 256;
+constexpr int kGrpU = 4;  // rows / distinct vertices per thread, gathers issued together
+__global__ void __launch_bounds__(kGrpThreads) k_grp_count(
+    const int64_t* __restrict__ R_ptr, const int32_t* __restrict__ rowv,
+    const int64_t* __restrict__ rowptr, int32_t* __restrict__ deg, int32_t* __restrict__ vcnt,
+    int32_t* __restrict__ rslot, int32_t* __restrict__ dv, unsigned long long* __restrict__ dcount) {
+  __shared__ int32_t s_w[kGrpThreads / 32];
+  __shared__ unsigned long long s_base;
   const int64_t R = *R_ptr;
-  const int lane = lane_id();
-  for (int64_t r0 = (int64_t)global_warp() * 32; r0 < R; r0 += (int64_t)grid_warps() * 32) {
-    const int64_t r = r0 + lane;
-    int32_t v = -1, d = 0, slot = -1;
-    if (r < R) {
-      v = rowv[r];
-      d = (int32_t)(rowptr[v + 1] - rowptr[v]);
-      deg[r] = d;
-      if (d > 0) slot = atomicAdd(vcnt + v, 1);
-      rslot[r] = slot;
+  const int lane = lane_id(), wid = threadIdx.x >> 5;
+  constexpr int64_t kBlk = (int64_t)kGrpThreads * kGrpU;
+  for (int64_t r0 = (int64_t)blockIdx.x * kBlk; r0 < R; r0 += (int64_t)gridDim.x * kBlk) {
+    int32_t v[kGrpU], d[kGrpU], slot[kGrpU];
+#pragma unroll
+    for (int u = 0; u < kGrpU; ++u) {
+      const int64_t r = r0 + u * kGrpThreads + threadIdx.x;
+      v[u] = r < R ? rowv[r] : -1;
     }
-    const unsigned first = __ballot_sync(0xffffffffu, slot == 0);
-    if (first) {
-      unsigned long long base = 0;
-      if (lane == 0) base = atomicAdd(dcount, (unsigned long long)__popc(first));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (slot == 0) dv[base + __popc(first & ((1u << lane) - 1u))] = v;
+#pragma unroll
+    for (int u = 0; u < kGrpU; ++u)
+      d[u] = v[u] >= 0 ? (int32_t)(rowptr[v[u] + 1] - rowptr[v[u]]) : 0;
+#pragma unroll
+    for (int u = 0; u < kGrpU; ++u) slot[u] = d[u] > 0 ? atomicAdd(vcnt + v[u], 1) : -1;
+    int nf = 0;
+#pragma unroll
+    for (int u = 0; u < kGrpU; ++u) {
+      const int64_t r = r0 + u * kGrpThreads + threadIdx.x;
+      if (r < R) {
+        deg[r] = d[u];
+        rslot[r] = slot[u];
+      }
+      nf += slot[u] == 0;
     }
+    // distinct list: one atomic per block round
+    const int incl = warp_incl_scan(nf);
+    if (lane == 31) s_w[wid] = incl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int tot = 0;
+      for (int w = 0; w < kGrpThreads / 32; ++w) { const int c = s_w[w]; s_w[w] = tot; tot += c; }
+      s_base = tot ? atomicAdd(dcount, (unsigned long long)tot) : 0ull;
+    }
+    __syncthreads();
+    int64_t o = (int64_t)s_base + s_w[wid] + incl - nf;
+#pragma unroll
+    for (int u = 0; u < kGrpU; ++u)
+      if (slot[u] == 0) dv[o++] = v[u];
+    __syncthreads();
   }
 }
 
-// Work tiers by row degree d: A (d <= kTierAHi) staged whole, many rows per
-// CTA batch (k_dd_batch); B (hubs) staged in chunks, one CTA per item
-// (k_dd_hub).  An item serves at most rows_item(d) frontier rows.
-constexpr int kTierAHi = 8192;
-constexpr int kBatchThreads = 256;
-constexpr int kBatchBuf = kTierAHi + 8;  // ints: one whole tier-A row + alignment
-constexpr int kHubThreads = 1024;
+// Work tiers by row degree d: A (d <= kTierAHi) packed into bins of the
+// serve ring, B (longer rows) staged in chunks.  An item serves at most
+// rows_item(d) frontier rows (about 512 / 2048 / 8192 picks).
+constexpr int kTierAHi = 4096;
+constexpr int kServeUnroll = 4;  // picks in flight per serve thread
 
 __host__ __device__ __forceinline__ int32_t rows_item(int64_t d, int32_t s) {
   const int32_t p = d <= 1024 ? 512 : d <= kTierAHi ? 2048 : 8192;
   const int32_t r = p / s;
-  return r < 1 ? 1 : (d > kTierAHi && r > kHubThreads ? kHubThreads : r);
+  return r < 1 ? 1 : r;
 }
 
 // Work-item descriptor: everything the serve kernels need before the first
@@ -593,7 +619,8 @@ struct PeerRows {
 };
 
 // tier t's items live in [t * icap, t * icap + tcnt[t]); tcnt[2] counts the
-// grouped rows
+// grouped rows.  kGrpU distinct vertices per thread, their gathers issued
+// together (the pass is latency-bound on random rowptr / counter loads).
 constexpr int kItemThreads = 256;
 __global__ void __launch_bounds__(kItemThreads) k_grp_items(
     const unsigned long long* __restrict__ dcount, const int32_t* __restrict__ dv,
@@ -604,88 +631,155 @@ __global__ void __launch_bounds__(kItemThreads) k_grp_items(
   __shared__ int64_t s_base[3];
   const int64_t D = (int64_t)*dcount;
   const int lane = lane_id(), wid = threadIdx.x >> 5;
-  for (int64_t g0 = blockIdx.x * (int64_t)kItemThreads; g0 < D;
-       g0 += (int64_t)gridDim.x * kItemThreads) {
-    const int64_t g = g0 + threadIdx.x;
-    int t = 0, n = 0, gc = 0, v = 0, per = 1;
-    int64_t d = 0, a0 = 0;
-    if (g < D) {
-      v = dv[g];
-      a0 = rowptr[v];
-      d = rowptr[v + 1] - a0;
-      gc = vcnt[v];
-      vcnt[v] = 0;  // ready for the next layer
-      t = d <= kTierAHi ? 0 : 1;
-      per = rows_item(d, s);
-      n = (gc + per - 1) / per;
+  constexpr int64_t kBlk = (int64_t)kItemThreads * kGrpU;
+  for (int64_t g0 = blockIdx.x * kBlk; g0 < D; g0 += (int64_t)gridDim.x * kBlk) {
+    int32_t v[kGrpU], gc[kGrpU], n[kGrpU], t[kGrpU], per[kGrpU];
+    int64_t a0[kGrpU], d[kGrpU];
+#pragma unroll
+    for (int u = 0; u < kGrpU; ++u) {
+      const int64_t g = g0 + u * kItemThreads + threadIdx.x;
+      v[u] = g < D ? dv[g] : -1;
     }
-    // per-tier item offsets and the group's row range (z = 2) inside the block
+#pragma unroll
+    for (int u = 0; u < kGrpU; ++u) {
+      gc[u] = 0;
+      a0[u] = d[u] = 0;
+      if (v[u] >= 0) {
+        a0[u] = rowptr[v[u]];
+        d[u] = rowptr[v[u] + 1];
+        gc[u] = vcnt[v[u]];
+      }
+    }
+    int tot[3] = {0, 0, 0};
+#pragma unroll
+    for (int u = 0; u < kGrpU; ++u) {
+      n[u] = 0;
+      t[u] = 0;
+      per[u] = 1;
+      if (v[u] >= 0) {
+        vcnt[v[u]] = 0;  // ready for the next layer
+        d[u] -= a0[u];
+        t[u] = d[u] <= kTierAHi ? 0 : 1;
+        per[u] = rows_item(d[u], s);
+        n[u] = (gc[u] + per[u] - 1) / per[u];
+        tot[0] += t[u] ? 0 : n[u];
+        tot[1] += t[u] ? n[u] : 0;
+        tot[2] += gc[u];
+      }
+    }
+    // per-tier item offsets and the rows' range (z = 2) inside the block
     int incl[3];
 #pragma unroll
     for (int z = 0; z < 3; ++z) {
-      incl[z] = warp_incl_scan(z == 2 ? gc : t == z ? n : 0);
+      incl[z] = warp_incl_scan(tot[z]);
       if (lane == 31) s_wsum[z][wid] = incl[z];
     }
     __syncthreads();
     if (threadIdx.x < 3) {
-      int tot = 0;
-      for (int w = 0; w < kItemThreads / 32; ++w) tot += s_wsum[threadIdx.x][w];
+      int all = 0;
+      for (int w = 0; w < kItemThreads / 32; ++w) all += s_wsum[threadIdx.x][w];
       s_base[threadIdx.x] =
-          tot ? (int64_t)atomicAdd(tcnt + threadIdx.x, (unsigned long long)tot) : 0;
+          all ? (int64_t)atomicAdd(tcnt + threadIdx.x, (unsigned long long)all) : 0;
     }
     __syncthreads();
-    if (n) {
-      int64_t o0 = s_base[t] + incl[t] - n, r0 = s_base[2] + incl[2] - gc;
-      for (int w = 0; w < wid; ++w) { o0 += s_wsum[t][w]; r0 += s_wsum[2][w]; }
-      o0 += (int64_t)t * icap;
-      roff[v] = (int32_t)r0;
+    int64_t o[3];
+#pragma unroll
+    for (int z = 0; z < 3; ++z) {
+      o[z] = s_base[z] + incl[z] - tot[z];
+      for (int w = 0; w < wid; ++w) o[z] += s_wsum[z][w];
+    }
+#pragma unroll
+    for (int u = 0; u < kGrpU; ++u) {
+      if (!n[u]) continue;
+      const int64_t r0 = o[2], oi = t[u] ? o[1] + icap : o[0];
+      o[2] += gc[u];
+      if (t[u]) o[1] += n[u]; else o[0] += n[u];
+      roff[v[u]] = (int32_t)r0;
+      int64_t ad = a0[u];
       if (peer.nblk) {
         int b = 0;
-        while (b + 1 < peer.nblk && peer.bounds[b + 1] <= v) ++b;
+        while (b + 1 < peer.nblk && peer.bounds[b + 1] <= v[u]) ++b;
         const int64_t* brp = peer.brp[b];
-        a0 = ((int64_t)(uintptr_t)(peer.bcol[b] + brp[v - peer.bounds[b]])) >> 2;
+        ad = ((int64_t)(uintptr_t)(peer.bcol[b] + brp[v[u] - peer.bounds[b]])) >> 2;
       }
-      const int64_t r1 = r0 + gc;
-      for (int o = 0; o < n; ++o) {
+      const int64_t r1 = r0 + gc[u];
+      for (int q = 0; q < n[u]; ++q) {
         DdItem it;
-        it.a0 = a0;
-        it.d = (int32_t)d;
-        it.q0 = (int32_t)(r0 + (int64_t)o * per);
-        it.nrows = (int32_t)min((int64_t)per, r1 - it.q0);
+        it.a0 = ad;
+        it.d = (int32_t)d[u];
+        it.q0 = (int32_t)(r0 + (int64_t)q * per[u]);
+        it.nrows = (int32_t)min((int64_t)per[u], r1 - it.q0);
         it.pad[0] = it.pad[1] = it.pad[2] = 0;
-        items[o0 + o] = it;
+        items[oi + q] = it;
       }
     }
     __syncthreads();  // s_wsum / s_base reused by the next round
   }
 }
 
+// grouped row records: (row within its batch, degree, frontier offset, batch)
 __global__ void k_grp_rows(const int64_t* __restrict__ R_ptr, const int32_t* __restrict__ rowv,
                            const int32_t* __restrict__ deg, const int64_t* __restrict__ fptr,
                            const int64_t* __restrict__ brow, int64_t k,
-                           const int64_t* __restrict__ rowkeys, int64_t batch_offset,
-                           int64_t stride, const int32_t* __restrict__ rslot,
-                           const int32_t* __restrict__ roff, int4* __restrict__ rrec) {
+                           const int32_t* __restrict__ rslot, const int32_t* __restrict__ roff,
+                           int4* __restrict__ rrec) {
   __shared__ int64_t s_brow[kBrowSmem];
   const bool sm = k + 1 <= kBrowSmem;
   if (sm)
     for (int64_t i = threadIdx.x; i <= k; i += blockDim.x) s_brow[i] = brow[i];
   __syncthreads();
   const int64_t R = *R_ptr;
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < R;
-       r += (int64_t)gridDim.x * blockDim.x) {
-    if (deg[r] > 0) {
-      const int32_t pos = roff[rowv[r]] + rslot[r];
-      int64_t b = 0, key;
-      if (rowkeys) {
-        key = rowkeys[r];
-      } else {
-        b = batch_of(s_brow, brow, k, r);
-        key = (batch_offset + b) * stride + (r - (sm ? s_brow[b] : brow[b]));
+  const int64_t blk = (int64_t)blockDim.x * kGrpU;
+  for (int64_t r0 = blockIdx.x * blk + threadIdx.x; r0 < R; r0 += (int64_t)gridDim.x * blk) {
+    int32_t d[kGrpU], v[kGrpU], sl[kGrpU], pos[kGrpU];
+#pragma unroll
+    for (int u = 0; u < kGrpU; ++u) {
+      const int64_t r = r0 + u * (int64_t)blockDim.x;
+      d[u] = 0;
+      if (r < R) {
+        d[u] = deg[r];
+        v[u] = rowv[r];
+        sl[u] = rslot[r];
       }
-      rrec[pos] = make_int4((int32_t)(uint32_t)key, (int32_t)((uint64_t)key >> 32),
-                            (int32_t)fptr[r], (int32_t)b);
     }
+#pragma unroll
+    for (int u = 0; u < kGrpU; ++u)
+      if (d[u] > 0) pos[u] = roff[v[u]] + sl[u];
+#pragma unroll
+    for (int u = 0; u < kGrpU; ++u) {
+      if (d[u] > 0) {
+        const int64_t r = r0 + u * (int64_t)blockDim.x;
+        const int64_t b = batch_of(s_brow, brow, k, r);
+        rrec[pos[u]] = make_int4((int32_t)(r - (sm ? s_brow[b] : brow[b])), d[u],
+                                 (int32_t)fptr[r], (int32_t)b);
+      }
+    }
+  }
+}
+
+// NORM + SAMPLE of every grouped row with take < d: sorted picks at
+// pidx[q * s ..] (rows of one vertex sit in adjacent lanes and share their
+// replay-table loads); exhausted rows are served in order without picks.
+template <int MAXF>
+__global__ void __launch_bounds__(kPickThreads) k_dd_pick(
+    const unsigned long long* __restrict__ grows, const int4* __restrict__ rrec, SageTabs T,
+    int32_t s, int64_t batch_offset, int64_t stride, uint64_t seed, uint64_t epoch,
+    uint64_t depth, int32_t* __restrict__ pidx) {
+  const int64_t R = (int64_t)*grows;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < R;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int4 rec = rrec[q];
+    const int32_t d = rec.y, take = min(d, s);
+    if (take == d) continue;
+    const uint64_t key = (uint64_t)((batch_offset + rec.w) * stride + rec.x);
+    int32_t sorted[MAXF];
+#pragma unroll
+    for (int z = 0; z < MAXF; ++z) sorted[z] = z;
+    sage_draws<MAXF>(T, key, d, take, seed, epoch, depth, sorted);
+    int32_t* out = pidx + q * s;
+#pragma unroll
+    for (int z = 0; z < MAXF; ++z)
+      if (z < take) out[z] = sorted[z];
   }
 }
 
@@ -740,176 +834,212 @@ struct DdArgs {
   const unsigned long long* tcnt;  // items per tier; tier t's at [t * icap, ..)
   int64_t icap;
   const DdItem* items;
-  const int4* rrec;                // grouped rows: (key lo, key hi, frontier offset, batch)
-  SageTabs T;
+  const int4* rrec;                // grouped rows: (local row, degree, frontier offset, batch)
+  const int32_t* pidx;             // sorted picks of grouped row q at pidx[q * s ..]
   int32_t s;
-  uint64_t seed, epoch, depth;
   int32_t* fcol;
   uint32_t* bitmap;
   int64_t nwords;
-  unsigned int* ticket;            // k_dd_batch work counter (zeroed per layer)
-  int32_t chunk;                   // k_dd_hub: A-row entries staged per pass
+  unsigned int* ticket;            // k_dd_serve work counter (zeroed per layer)
 };
 
-// picks of grouped row q (take < d: sage_draws; take == d: every index)
-template <int MAXF>
-__device__ __forceinline__ void dd_row_picks(const DdArgs& A, const int4 rec, int32_t d,
-                                             int32_t take, int32_t (&sorted)[MAXF]) {
-#pragma unroll
-  for (int z = 0; z < MAXF; ++z) sorted[z] = z;
-  if (take < d) {
-    const uint64_t key = (uint64_t)(uint32_t)rec.x | ((uint64_t)(uint32_t)rec.y << 32);
-    sage_draws<MAXF>(A.T, key, d, take, A.seed, A.epoch, A.depth, sorted);
-  }
+// pick (row i of an item, draw t): entry index, frontier position, batch
+__device__ __forceinline__ void dd_pair(const DdArgs& A, int32_t q, int32_t t, int32_t take,
+                                        bool all, int32_t& idx, int32_t& fp, int32_t& bb) {
+  idx = all ? t : A.pidx[(uint32_t)q * (uint32_t)A.s + (uint32_t)t];
+  const int4 rec = A.rrec[q];
+  fp = rec.z + t;
+  bb = rec.w;
 }
 
-// frontier entries and (batch, vertex) bits of one row from its staged copy
-// (buf[idx + sh] holds entry idx; entries outside [lo, hi) are skipped)
-template <int MAXF>
-__device__ __forceinline__ void dd_row_serve(const DdArgs& A, const int4 rec, int32_t take,
-                                             const int32_t (&sorted)[MAXF], const int32_t* buf,
-                                             int32_t sh, int32_t lo, int32_t hi) {
-  const uint32_t NW = (uint32_t)A.nwords;
-  uint32_t* bm = A.bitmap + (uint32_t)rec.w * NW;
-  int32_t* out = A.fcol + (uint32_t)rec.z;
-#pragma unroll
-  for (int z = 0; z < MAXF; ++z) {
-    if (z < take && sorted[z] >= lo && sorted[z] < hi) {
-      const int32_t cv = buf[sorted[z] + sh];
-      out[z] = cv;
-      atomicOr(bm + pk_word(cv), 1u << (cv & 31));
-    }
-  }
+__device__ __forceinline__ void dd_put(const DdArgs& A, int32_t fp, int32_t bb, int32_t cv) {
+  A.fcol[(uint32_t)fp] = cv;
+  atomicOr(A.bitmap + (uint32_t)bb * (uint32_t)A.nwords + pk_word(cv), 1u << (cv & 31));
 }
 
-// Tier A: a CTA takes chunks of 256 work items (ticket order), packs as many
-// of their rows as fit into its buffer (one TMA bulk copy per row, one
-// mbarrier), computes the picks of every frontier row of the packed items
-// (thread per row, 256 at a time) while the rows land, then serves them
-// from shared memory.  Rows of an item are found by a search over the
-// block's row prefix.
-template <int MAXF>
-__global__ void __launch_bounds__(kBatchThreads) k_dd_batch(DdArgs A) {
-  __shared__ __align__(128) int32_t buf[kBatchBuf];
-  __shared__ int32_t s_len[kBatchThreads];   // inclusive prefix of staged lengths
-  __shared__ int32_t s_row[kBatchThreads];   // inclusive prefix of rows
-  __shared__ int32_t s_q0[kBatchThreads], s_d[kBatchThreads], s_sh[kBatchThreads];
-  __shared__ int32_t s_wsum[2][kBatchThreads / 32];
-  __shared__ __align__(8) uint64_t bar;
-  __shared__ unsigned int s_ticket;
+// Serve: producer / consumer over a ring of TMA stages.  Warp 0 of each CTA
+// is the producer: it takes 32 work items at a time (ticket order over both
+// tiers), packs consecutive short rows into the open bin of the ring (one
+// TMA bulk copy per row, bytes announced with mbarrier.expect_tx) and cuts
+// long rows into chunk bins, then arrives on the bin's full barrier; the
+// other warps consume bins in ring order — every pick of the bin's items
+// served from shared memory (frontier entry + (batch, vertex) bit) — and
+// release the stage on its empty barrier.  Stages land while earlier bins
+// are served, so each CTA keeps kStages - 1 row panels in flight.
+constexpr int kSvThreads = 256;                     // warp 0 producer, 7 consumer warps
+constexpr int kSvConsumers = kSvThreads - 32;
+constexpr int kStages = 3;
+constexpr int kLongChunk = 8192;                    // entries per chunk bin of a long row
+constexpr int kSvStageInts = kLongChunk + 16;       // one chunk or a packed bin
+constexpr int kBinItems = 128;                      // items per packed bin
+
+struct SvStage {
+  int32_t buf[kSvStageInts];
+  int4 meta[kBinItems];  // (shift into buf, first grouped row, take (neg: every entry), pick prefix)
+  int32_t nitems, npicks, lo, hi;  // hi < 0: end of the work
+};
+
+__device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__global__ void __launch_bounds__(kSvThreads) k_dd_serve(DdArgs A) {
+  extern __shared__ __align__(128) unsigned char svraw[];
+  SvStage* st = reinterpret_cast<SvStage*>(svraw);
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
   const int tid = threadIdx.x, lane = lane_id(), wid = tid >> 5;
-  if (tid == 0) mbar_init(&bar, 1);
-  __syncthreads();
-  uint32_t phase = 0;
-  const int64_t nit = (int64_t)A.tcnt[0];
-  const int s = A.s;
-  for (;;) {
-    if (tid == 0) s_ticket = atomicAdd(A.ticket, 1u);
-    __syncthreads();
-    const int64_t c0 = (int64_t)s_ticket * kBatchThreads;
-    if (c0 >= nit) break;
-    const int cnt = (int)min((int64_t)kBatchThreads, nit - c0);
-    DdItem it{};
-    int len = 0, nr = 0;
-    if (tid < cnt) {
-      it = A.items[c0 + tid];
-      len = dd_row_len(it.a0, it.d);
-      nr = it.nrows;
-    }
-    // block inclusive scans of (staged length, rows)
-    int il = warp_incl_scan(len), ir = warp_incl_scan(nr);
-    if (lane == 31) { s_wsum[0][wid] = il; s_wsum[1][wid] = ir; }
-    __syncthreads();
-    for (int w = 0; w < wid; ++w) { il += s_wsum[0][w]; ir += s_wsum[1][w]; }
-    s_len[tid] = il;
-    s_row[tid] = ir;
-    s_q0[tid] = it.q0;
-    s_d[tid] = it.d;
-    __syncthreads();
-    for (int j0 = 0; j0 < cnt;) {
-      const int lbase = j0 ? s_len[j0 - 1] : 0, rbase = j0 ? s_row[j0 - 1] : 0;
-      // sub-batch [j0, j1): the items whose rows fit the buffer (>= 1)
-      const int fit = __syncthreads_count(tid >= j0 && tid < cnt && il - lbase <= kBatchBuf);
-      const int j1 = j0 + (fit > 0 ? fit : 1);
-      const uint32_t bytes = 4u * (uint32_t)(s_len[j1 - 1] - lbase);
-      if (tid >= j0 && tid < j1) {
-        const int off = il - len - lbase;  // 16-B aligned (lengths are multiples of 4)
-        s_sh[tid] = off + (int)(it.a0 & 3);
-        if (tid == j0) {
-          fence_async_smem();
-          mbar_expect_tx(&bar, bytes);
-        }
-      }
-      __syncthreads();  // expect_tx before any completion; s_sh visible
-      if (tid >= j0 && tid < j1)
-        tma_row(buf + (il - len - lbase), A.col + (it.a0 & ~3LL), 4u * (uint32_t)len, &bar);
-      const int NR = s_row[j1 - 1] - rbase;
-      for (int p0 = 0; p0 < NR; p0 += kBatchThreads) {
-        const int p = p0 + tid;
-        int4 rec = make_int4(0, 0, 0, 0);
-        int32_t d = 0, take = 0, sh = 0;
-        int32_t sorted[MAXF];
-        if (p < NR) {
-          int lo = j0, hi = j1 - 1;  // first item with s_row > rbase + p
-          while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (s_row[mid] > rbase + p) hi = mid; else lo = mid + 1;
-          }
-          const int q = s_q0[lo] + (rbase + p - (lo ? s_row[lo - 1] : 0));
-          rec = A.rrec[q];
-          d = s_d[lo];
-          sh = s_sh[lo];
-          take = min(d, s);
-          dd_row_picks<MAXF>(A, rec, d, take, sorted);
-        }
-        if (p0 == 0) mbar_wait(&bar, phase);
-        if (p < NR) dd_row_serve<MAXF>(A, rec, take, sorted, buf, sh, 0, d);
-      }
-      phase ^= 1u;
-      __syncthreads();  // buffer free for the next sub-batch
-      j0 = j1;
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kSvConsumers / 32);
     }
   }
-}
-
-// Tier B (hubs, d > kTierAHi): one CTA of 1024 threads per work item; every
-// thread computes one frontier row's picks, then the row is staged in
-// chunks of A.chunk entries (TMA bulk copies) and each chunk serves the
-// picks that fall into it.
-template <int MAXF>
-__global__ void __launch_bounds__(kHubThreads) k_dd_hub(DdArgs A) {
-  extern __shared__ __align__(128) int32_t hbuf[];
-  __shared__ __align__(8) uint64_t bar;
-  const int tid = threadIdx.x;
-  if (tid == 0) mbar_init(&bar, 1);
   __syncthreads();
-  uint32_t phase = 0;
-  const int64_t it1 = A.icap + (int64_t)A.tcnt[1];
-  const int chunk = A.chunk, s = A.s;
-  for (int64_t i = A.icap + blockIdx.x; i < it1; i += gridDim.x) {
-    const DdItem it = A.items[i];
-    const int32_t d = it.d, take = min(d, s);
-    int4 rec = make_int4(0, 0, 0, 0);
-    int32_t sorted[MAXF];
-    for (int32_t c0 = 0; c0 < d; c0 += chunk) {
-      const int32_t c1 = min(c0 + chunk, d);
-      const int64_t al0 = (it.a0 + c0) & ~3LL;
-      if (tid == 0) {
-        const uint32_t bytes = 4u * (uint32_t)dd_row_len(it.a0 + c0, c1 - c0);
-        fence_async_smem();
-        mbar_expect_tx(&bar, bytes);
-        tma_row(hbuf, A.col + al0, bytes, &bar);
+  const int s = A.s;
+  const int64_t n0 = (int64_t)A.tcnt[0], n1 = (int64_t)A.tcnt[1], ntot = n0 + n1;
+  if (wid == 0) {
+    // ------------------------------------------------------------ producer
+    int64_t bin = 0;          // bins opened so far (ring position)
+    int open = 0;             // a packed bin is open in slot (bin - 1) % kStages
+    int cur_ints = 0, cur_items = 0, cur_picks = 0;
+    auto open_bin = [&]() -> SvStage& {
+      const int sl = (int)(bin % kStages);
+      if (bin >= kStages) mbar_wait(&empty[sl], (uint32_t)((bin / kStages - 1) & 1));
+      ++bin;
+      return st[sl];
+    };
+    auto commit = [&](SvStage& S, int nitems, int npicks, int lo, int hi) {
+      __syncwarp();  // every lane's meta / expect_tx before the arrive
+      if (lane == 0) {
+        S.nitems = nitems; S.npicks = npicks; S.lo = lo; S.hi = hi;
+        mbar_arrive(&full[(int)((bin - 1) % kStages)]);
       }
-      if (c0 == 0 && tid < it.nrows) {
-        rec = A.rrec[it.q0 + tid];
-        dd_row_picks<MAXF>(A, rec, d, take, sorted);
+      __syncwarp();
+    };
+    SvStage* S = nullptr;
+    // a contiguous share of the items per CTA (no shared work counter)
+    const int64_t my0 = ntot * blockIdx.x / gridDim.x, my1 = ntot * (blockIdx.x + 1) / gridDim.x;
+    for (int64_t base = my0; base < my1; base += 32) {
+      const int64_t gi = base + lane;
+      const bool valid = gi < my1;
+      DdItem it{};
+      if (valid) it = A.items[gi < n0 ? gi : A.icap + (gi - n0)];
+      const bool longrow = valid && it.d > kTierAHi;
+      const int take = valid ? min(it.d, s) : 0;
+      const int len = valid && !longrow ? dd_row_len(it.a0, it.d) : 0;
+      const int np = valid ? it.nrows * take : 0;
+      // lanes in order: runs of short rows packed, long rows one by one
+      unsigned todo = __ballot_sync(0xffffffffu, valid);
+      while (todo) {
+        const int first = __ffs(todo) - 1;
+        const unsigned longs = __ballot_sync(0xffffffffu, longrow) & todo;
+        if (longs & (1u << first)) {
+          // long row: its own chunk bins (the open packed bin is committed first)
+          if (open) { commit(*S, cur_items, cur_picks, 0, 0x7fffffff); open = 0; }
+          const int64_t a0 = __shfl_sync(0xffffffffu, it.a0, first);
+          const int32_t d = __shfl_sync(0xffffffffu, it.d, first);
+          const int32_t q0 = __shfl_sync(0xffffffffu, it.q0, first);
+          const int32_t npf = __shfl_sync(0xffffffffu, np, first);
+          const int32_t tkf = __shfl_sync(0xffffffffu, take, first);
+          for (int32_t e0 = 0; e0 < d; e0 += kLongChunk) {
+            const int32_t e1 = min(e0 + kLongChunk, d);
+            SvStage& C = open_bin();
+            if (lane == 0) {
+              const int64_t al0 = (a0 + e0) & ~3LL;
+              const uint32_t bytes = 4u * (uint32_t)dd_row_len(a0 + e0, e1 - e0);
+              C.meta[0] = make_int4((int32_t)(a0 + e0 - al0) - e0, q0, tkf, 0);
+              fence_async_smem();
+              mbar_expect_tx_only(&full[(int)((bin - 1) % kStages)], bytes);
+              tma_row(C.buf, A.col + al0, bytes, &full[(int)((bin - 1) % kStages)]);
+            }
+            commit(C, 1, npf, e0, e1);
+          }
+          todo &= ~(1u << first);
+          continue;
+        }
+        // the run of short rows starting at `first` (up to the next long row)
+        const unsigned nextlong = longs & ~((2u << first) - 1u);
+        const int end = nextlong ? __ffs(nextlong) - 1 : 32;
+        const bool inrun = lane >= first && lane < end && valid;
+        if (!open) {
+          S = &open_bin();
+          open = 1;
+          cur_ints = cur_items = cur_picks = 0;
+        }
+        const int li = warp_incl_scan(inrun ? len : 0);
+        const int pi = warp_incl_scan(inrun ? np : 0);
+        const int ci = warp_incl_scan(inrun ? 1 : 0);
+        const bool fits = inrun && cur_ints + li <= kSvStageInts && cur_items + ci <= kBinItems;
+        const unsigned fm = __ballot_sync(0xffffffffu, fits);
+        if (fits) {
+          const int off = cur_ints + li - len;
+          const int sl = (int)((bin - 1) % kStages);
+          S->meta[cur_items + ci - 1] =
+              make_int4(off + (int)(it.a0 & 3), it.q0, take == it.d ? -take : take,
+                        cur_picks + pi - np);
+          fence_async_smem();
+          mbar_expect_tx_only(&full[sl], 4u * (uint32_t)len);
+          tma_row(S->buf + off, A.col + (it.a0 & ~3LL), 4u * (uint32_t)len, &full[sl]);
+        }
+        if (fm) {
+          const int lastfit = 31 - __clz(fm);
+          cur_ints += __shfl_sync(0xffffffffu, li, lastfit);
+          cur_picks += __shfl_sync(0xffffffffu, pi, lastfit);
+          cur_items += __shfl_sync(0xffffffffu, ci, lastfit);
+          todo &= ~fm;
+        }
+        const unsigned runmask = end == 32 ? 0xffffffffu : (1u << end) - 1u;
+        if ((todo & (1u << first)) || (fm && (todo & ~longs & runmask))) {
+          // the bin is full: commit, the rest of the run goes to a new bin
+          commit(*S, cur_items, cur_picks, 0, 0x7fffffff);
+          open = 0;
+        }
       }
-      mbar_wait(&bar, phase);
-      phase ^= 1u;
-      if (tid < it.nrows)
-        dd_row_serve<MAXF>(A, rec, take, sorted, hbuf, (int32_t)(it.a0 + c0 - al0) - c0, c0, c1);
-      __syncthreads();  // buffer free
     }
+    if (open) commit(*S, cur_items, cur_picks, 0, 0x7fffffff);
+    SvStage& E = open_bin();
+    commit(E, 0, 0, 0, -1);  // end of the work
+    return;
+  }
+  // -------------------------------------------------------------- consumers
+  const int ctid = tid - 32;
+  for (int64_t bin = 0;; ++bin) {
+    const int sl = (int)(bin % kStages);
+    mbar_wait(&full[sl], (uint32_t)((bin / kStages) & 1));
+    const SvStage& S = st[sl];
+    const int nitems = S.nitems, NP = S.npicks, lo = S.lo, hi = S.hi;
+    if (hi < 0) break;
+    for (int p0 = ctid; p0 < NP; p0 += kSvConsumers * kServeUnroll) {
+      int32_t idx[kServeUnroll], fp[kServeUnroll], bb[kServeUnroll], sh[kServeUnroll];
+#pragma unroll
+      for (int u = 0; u < kServeUnroll; ++u) {
+        const int p = p0 + u * kSvConsumers;
+        idx[u] = -1;
+        if (p < NP) {
+          int a = 0, b = nitems - 1;  // last item with pick prefix <= p
+          while (a < b) {
+            const int mid = (a + b + 1) >> 1;
+            if (S.meta[mid].w <= p) a = mid; else b = mid - 1;
+          }
+          const int4 m = S.meta[a];
+          const int tkn = m.z < 0 ? -m.z : m.z;
+          const int r = p - m.w;
+          const int i = r / tkn, t = r - i * tkn;
+          dd_pair(A, m.y + i, t, tkn, m.z < 0, idx[u], fp[u], bb[u]);
+          sh[u] = m.x;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kServeUnroll; ++u)
+        if (idx[u] >= lo && idx[u] < hi) dd_put(A, fp[u], bb[u], S.buf[sh[u] + idx[u]]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[sl]);
   }
 }
 
@@ -1275,7 +1405,7 @@ struct SageWs {
   int32_t* rslot;    // per frontier row: slot in its vertex group
   int32_t* dv;       // distinct row vertices (unordered)
   unsigned long long* cnts;  // [0] distinct count, [1..3] tier items, grouped rows
-  unsigned int* ticket;      // k_dd_batch work counter
+  unsigned int* ticket;      // serve kernels' work counters
   int64_t icap;      // work-item capacity per tier
   DdItem* items;     // work-item descriptors
   int4* rrec;        // per grouped row: (key lo, key hi, frontier offset, batch)
@@ -1327,42 +1457,31 @@ static int persistent_grid(K kernel, int threads, size_t smem = 0) {
   return (o < 1 ? 1 : o) * (sms > 0 ? sms : kNumSMs);
 }
 
-// Per-device launch configuration of the serve kernels (attributes are per
+// Per-device launch configuration of the dedup kernels (attributes are per
 // device; grids from the occupancy of the current device).
 constexpr int kMaxDevices = 16;
 struct ServeCfg {
   bool init = false;
-  int batch_grid[5] = {0, 0, 0, 0, 0};
-  int hub_grid[5] = {0, 0, 0, 0, 0};
-  int hub_chunk = 0;
-  size_t hub_smem = 0;
+  int pick_grid[5] = {0, 0, 0, 0, 0};
+  int serve_grid = 0;
+  size_t serve_smem = 0;
 };
 static ServeCfg g_serve[kMaxDevices];
-
-template <int MAXF>
-static void serve_setup(ServeCfg& c, int bucket) {
-  c.batch_grid[bucket] = persistent_grid(k_dd_batch<MAXF>, kBatchThreads);
-  cudaFuncSetAttribute(k_dd_hub<MAXF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)c.hub_smem);
-  c.hub_grid[bucket] = persistent_grid(k_dd_hub<MAXF>, kHubThreads, c.hub_smem);
-}
 
 static ServeCfg& serve_cfg() {
   int dev = 0;
   cudaGetDevice(&dev);
   ServeCfg& c = g_serve[dev < kMaxDevices ? dev : 0];
   if (!c.init) {
-    int max_smem = 0;
-    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    if (max_smem <= 0) max_smem = 227 * 1024;
-    // hub chunk: all of shared memory but the static mbarrier
-    c.hub_chunk = ((max_smem - 256) / 4 - 8) & ~3;
-    c.hub_smem = sizeof(int32_t) * (c.hub_chunk + 8);
-    serve_setup<5>(c, 0);
-    serve_setup<8>(c, 1);
-    serve_setup<10>(c, 2);
-    serve_setup<16>(c, 3);
-    serve_setup<32>(c, 4);
+    c.serve_smem = kStages * sizeof(SvStage);
+    cudaFuncSetAttribute(k_dd_serve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)c.serve_smem);
+    c.serve_grid = persistent_grid(k_dd_serve, kSvThreads, c.serve_smem);
+    c.pick_grid[0] = persistent_grid(k_dd_pick<5>, kPickThreads);
+    c.pick_grid[1] = persistent_grid(k_dd_pick<8>, kPickThreads);
+    c.pick_grid[2] = persistent_grid(k_dd_pick<10>, kPickThreads);
+    c.pick_grid[3] = persistent_grid(k_dd_pick<16>, kPickThreads);
+    c.pick_grid[4] = persistent_grid(k_dd_pick<32>, kPickThreads);
     c.init = true;
   }
   return c;
@@ -1370,57 +1489,56 @@ static ServeCfg& serve_cfg() {
 
 static int fan_bucket(int32_t s) { return s <= 5 ? 0 : s <= 8 ? 1 : s <= 10 ? 2 : s <= 16 ? 3 : 4; }
 
-template <int MAXF>
-static void launch_serve_maxf(const DdArgs& A, const ServeCfg& c, int b, cudaStream_t st,
-                              cudaStream_t hs) {
-  k_dd_batch<MAXF><<<c.batch_grid[b], kBatchThreads, 0, st>>>(A);
-  k_dd_hub<MAXF><<<c.hub_grid[b], kHubThreads, c.hub_smem, hs>>>(A);
-}
-
-// One dedup layer: grouping (count, items, rows), then the fused NORM +
-// SAMPLE + serve kernels (tier A batched, tier B hubs on a forked stream;
-// they touch disjoint frontier entries and commutative bitmap ORs).
+// One dedup layer: grouping (count already ran; items, rows), NORM + SAMPLE
+// per grouped row, then the serve kernels (tier A bins, tier B chunks on a
+// forked stream; they touch disjoint frontier entries and commutative
+// bitmap ORs).
 static int dedup_layer(const Graph* g, SageWs& ws, const int64_t* R_ptr, const int32_t* rowv,
                        const int64_t* fptr, const int64_t* brow, int64_t k, int32_t s,
                        int64_t stride, int64_t batch_offset, uint64_t seed, uint64_t epoch,
                        uint64_t depth, int64_t r_cap, const PeerRows& peer, int32_t* fcol,
                        uint32_t* bitmap, int64_t nwords8, cudaStream_t st) {
   const int64_t gw = 16 * kNumSMs;
-  k_grp_items<<<grid_for(r_cap < g->n ? r_cap : g->n, kItemThreads, gw), kItemThreads, 0, st>>>(
+  k_grp_items<<<grid_for((r_cap < g->n ? r_cap : g->n + 0) / kGrpU + 1, kItemThreads, gw),
+                kItemThreads, 0, st>>>(
       ws.cnts, ws.dv, g->rowptr, ws.vcnt, ws.roff, s, ws.icap, ws.cnts + 1, ws.items, peer);
-  k_grp_rows<<<grid_for(r_cap, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, fptr, brow, k,
-                                                      nullptr, batch_offset, stride, ws.rslot,
-                                                      ws.roff, ws.rrec);
+  GB_LAUNCH_CHECK("k_grp_items");
+  k_grp_rows<<<grid_for(r_cap / kGrpU + 1, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, fptr,
+                                                                   brow, k,
+                                                      ws.rslot, ws.roff, ws.rrec);
   GB_LAUNCH_CHECK("dedup grouping");
+  const ServeCfg& c = serve_cfg();
+  const SageTabs T{g->deg_slot, g->run_j0, g->run_sd, g->run_n, g->run_lower};
+  const int b = fan_bucket(s);
+  const int pg = c.pick_grid[b];
+  const unsigned long long* grows = ws.cnts + 3;
+  prof_mark(st);
+  switch (b) {
+    case 0: k_dd_pick<5><<<pg, kPickThreads, 0, st>>>(grows, ws.rrec, T, s, batch_offset, stride, seed, epoch, depth, ws.pidx); break;
+    case 1: k_dd_pick<8><<<pg, kPickThreads, 0, st>>>(grows, ws.rrec, T, s, batch_offset, stride, seed, epoch, depth, ws.pidx); break;
+    case 2: k_dd_pick<10><<<pg, kPickThreads, 0, st>>>(grows, ws.rrec, T, s, batch_offset, stride, seed, epoch, depth, ws.pidx); break;
+    case 3: k_dd_pick<16><<<pg, kPickThreads, 0, st>>>(grows, ws.rrec, T, s, batch_offset, stride, seed, epoch, depth, ws.pidx); break;
+    default: k_dd_pick<32><<<pg, kPickThreads, 0, st>>>(grows, ws.rrec, T, s, batch_offset, stride, seed, epoch, depth, ws.pidx); break;
+  }
+  GB_LAUNCH_CHECK("k_dd_pick");
+  prof_mark(st);
   DdArgs A{};
   A.col = peer.nblk ? nullptr : g->col;
   A.tcnt = ws.cnts + 1;
   A.icap = ws.icap;
   A.items = ws.items;
   A.rrec = ws.rrec;
-  A.T = SageTabs{g->deg_slot, g->run_j0, g->run_sd, g->run_n, g->run_lower};
+  A.pidx = ws.pidx;
   A.s = s;
-  A.seed = seed; A.epoch = epoch; A.depth = depth;
   A.fcol = fcol;
   A.bitmap = bitmap;
   A.nwords = nwords8;
   A.ticket = ws.ticket;
-  const ServeCfg& c = serve_cfg();
-  A.chunk = c.hub_chunk;
   prof_mark(st);
-  cudaStream_t hs = fork_begin(st, 1);
-  const int b = fan_bucket(s);
-  switch (b) {
-    case 0: launch_serve_maxf<5>(A, c, b, st, hs); break;
-    case 1: launch_serve_maxf<8>(A, c, b, st, hs); break;
-    case 2: launch_serve_maxf<10>(A, c, b, st, hs); break;
-    case 3: launch_serve_maxf<16>(A, c, b, st, hs); break;
-    default: launch_serve_maxf<32>(A, c, b, st, hs); break;
-  }
-  GB_LAUNCH_CHECK("k_dd_batch / k_dd_hub");
-  fork_join(st, 1);
+  k_dd_serve<<<c.serve_grid, kSvThreads, c.serve_smem, st>>>(A);
+  GB_LAUNCH_CHECK("k_dd_serve");
   prof_mark(st);
-  count_launches(4);  // items, rows, batch, hub
+  count_launches(4);  // items, rows, pick, serve
   return GB_OK;
 }
 
@@ -1530,7 +1648,7 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     if (ldedup) {
       GB_CUDA(cudaMemsetAsync(ws.cnts, 0, sizeof(unsigned long long) * 8, st));
       GB_CUDA(cudaMemsetAsync(ws.ticket, 0, sizeof(unsigned int) * 8, st));
-      k_grp_count<<<grid_for(r_cap, 256, 16 * kNumSMs), 256, 0, st>>>(
+      k_grp_count<<<grid_for(r_cap / kGrpU + 1, kGrpThreads, 16 * kNumSMs), kGrpThreads, 0, st>>>(
           R_ptr, rowv, g->rowptr, ws.deg, ws.vcnt, ws.rslot, ws.dv, ws.cnts);
       GB_LAUNCH_CHECK("k_grp_count");
     } else {

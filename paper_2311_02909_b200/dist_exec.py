@@ -46,19 +46,64 @@ def _torch():
     return torch
 
 
+def _staged():
+    """gloo process group: device tensors travel through host copies (the
+    single-GPU multi-process parity test and the CPU host-logic tests)."""
+    import torch.distributed as dist
+
+    return dist.get_backend() == "gloo"
+
+
+def _all_reduce(t, op=None, group=None):
+    import torch.distributed as dist
+
+    op = dist.ReduceOp.SUM if op is None else op
+    if _staged() and t.is_cuda:
+        h = t.cpu()
+        dist.all_reduce(h, op=op, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=op, group=group)
+
+
+def _all_gather(parts, t, group=None):
+    import torch.distributed as dist
+
+    if _staged() and t.is_cuda:
+        hp = [p.cpu() for p in parts]
+        dist.all_gather(hp, t.cpu(), group=group)
+        for p, h in zip(parts, hp):
+            p.copy_(h)
+    else:
+        dist.all_gather(parts, t, group=group)
+
+
+def _all_gather_into(out, t):
+    import torch.distributed as dist
+
+    if _staged():
+        parts = list(out.view(-1, t.numel()).unbind(0))
+        _all_gather(parts, t)
+    else:
+        dist.all_gather_into_tensor(out, t)
+
+
 def exchange(sends, recv_sizes, group_ranks, dtype, device):
     """Point-to-point exchange inside a group: sends {peer: tensor},
     recv_sizes {peer: count}; returns {peer: tensor}.  Grouped isend/irecv
-    (NCCL group on GPUs, gloo on CPU for the host-logic tests)."""
+    (NCCL over NVLink on GPUs; gloo through host copies for the single-GPU
+    multi-process and CPU tests)."""
     import torch.distributed as dist
 
     torch = _torch()
+    staged = _staged()
+    wire = torch.device("cpu") if staged else device
     ops, out = [], {}
     me = dist.get_rank()
     for peer, n in recv_sizes.items():
         if peer == me:
             continue
-        buf = torch.empty(int(n), dtype=dtype, device=device)
+        buf = torch.empty(int(n), dtype=dtype, device=wire)
         out[peer] = buf
         if n:
             ops.append(dist.P2POp(dist.irecv, buf, peer))
@@ -67,10 +112,12 @@ def exchange(sends, recv_sizes, group_ranks, dtype, device):
             out[peer] = t
             continue
         if t.numel():
-            ops.append(dist.P2POp(dist.isend, t.contiguous(), peer))
+            ops.append(dist.P2POp(dist.isend, t.contiguous().to(wire), peer))
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()
+    if staged:
+        out = {p: (t if p == me else t.to(device)) for p, t in out.items()}
     return out
 
 
@@ -86,23 +133,95 @@ def exchange_counts(sends, group_ranks, device):
     return {p: int(got[p].item()) if p != me else int(cnt_out[me].item()) for p in group_ranks}
 
 
+class BlockGraph:
+    """This rank's share of a 1.5D-partitioned graph (partition_block_rows,
+    dist.py:200-214): the block row of its grid row — rows [lo, hi) of A as
+    a CSR with global column ids — plus the global degree metadata the
+    sampler needs (degrees all-gathered once over the process group, the
+    global row offsets scanned from them, the per-degree replay tables built
+    from them).  No other block's columns are resident on this GPU.
+
+    `tables` is a DeviceGraph whose rowptr is the global one and whose
+    column array is a stub: every column read of the 1.5D samplers goes to
+    a block CSR (local, fetched or a peer's).
+    """
+
+    def __init__(self, n, grid: ProcessGrid, row0, brp, bcol, nnz):
+        import torch.distributed as dist
+
+        from .sparse import DeviceGraph
+
+        torch = _torch()
+        self.n, self.grid = int(n), grid
+        self.row0, self.brp, self.nnz = int(row0), brp, int(nnz)
+        self.bcol = bcol  # padded by GB_COL_PAD (16-B streaming loads)
+        bounds = _bounds(self.n, grid.rows)
+        sizes = np.diff(bounds)
+        maxb = int(sizes.max())
+        dev = brp.device
+        mine = torch.zeros(maxb, dtype=torch.int32, device=dev)
+        mine[: brp.numel() - 1] = (brp[1:] - brp[:-1]).to(torch.int32)
+        allb = torch.empty(grid.p * maxb, dtype=torch.int32, device=dev)
+        _all_gather_into(allb, mine)
+        allb = allb.view(grid.p, maxb)
+        self.gdeg = torch.cat([allb[grid.rank(i, 0), : int(sizes[i])] for i in range(grid.rows)])
+        rowptr = torch.zeros(self.n + 1, dtype=torch.int64, device=dev)
+        torch.cumsum(self.gdeg.long(), 0, out=rowptr[1:])
+        stub = torch.zeros(_lib.GB_COL_PAD, dtype=torch.int32, device=dev)
+        self.tables = DeviceGraph(self.n, rowptr, stub, int(rowptr[-1].item()))
+
+    @classmethod
+    def rmat(cls, n, m, symmetric, grid: ProcessGrid, seed=0):
+        """Block row of the synthetic R-MAT graph (gb_rmat_block): only the
+        block is built on this GPU."""
+        import torch.distributed as dist
+
+        from .graphgen import rmat_device_block
+
+        i, _ = grid.coords(dist.get_rank())
+        bounds = _bounds(int(n), grid.rows)
+        lo, hi = int(bounds[i]), int(bounds[i + 1])
+        brp, bcol, nnz = rmat_device_block(n, m, symmetric, lo, hi, seed=seed)
+        return cls(n, grid, lo, brp, bcol, nnz)
+
+    @classmethod
+    def from_full(cls, full, grid: ProcessGrid):
+        """Cut this rank's block out of a replicated DeviceGraph (tests)."""
+        import torch.distributed as dist
+
+        torch = _torch()
+        i, _ = grid.coords(dist.get_rank())
+        bounds = _bounds(full.n, grid.rows)
+        lo, hi = int(bounds[i]), int(bounds[i + 1])
+        a0, a1 = int(full.rowptr[lo].item()), int(full.rowptr[hi].item())
+        brp = (full.rowptr[lo:hi + 1] - a0).contiguous()
+        bcol = torch.zeros(a1 - a0 + _lib.GB_COL_PAD, dtype=torch.int32, device=brp.device)
+        bcol[: a1 - a0] = full.col[a0:a1]
+        return cls(full.n, grid, lo, brp, bcol, a1 - a0)
+
+    def resident_bytes(self):
+        """Graph bytes held on this GPU: block CSR + global degree metadata."""
+        return int(self.brp.numel() * 8 + self.bcol.numel() * 4 + self.gdeg.numel() * 4 +
+                   self.tables.rowptr.numel() * 8)
+
+
 class Sage15D:
     """1.5D partitioned GraphSAGE bulk sampler over real processes.
 
-    full: a DeviceGraph of the whole graph on this GPU — used once to build
-    the global degree array and replay tables and to cut out this rank's
-    block row (a deployment would load only the block and all-gather the
-    degrees; the sampling data path below touches only the local block and
-    fetched rows).
+    part: this rank's BlockGraph (only its grid row's block resident), or a
+    replicated DeviceGraph from which the block is cut (tests).
     """
 
-    def __init__(self, full, grid: ProcessGrid, fanouts, batch_size, mode="pfree",
+    def __init__(self, part, grid: ProcessGrid, fanouts, batch_size, mode="pfree",
                  ledger=None, fetch="rows"):
         import torch.distributed as dist
 
         torch = _torch()
         if not dist.is_initialized() or dist.get_world_size() != grid.p:
             raise ContractViolation("Sage15D needs torch.distributed with world_size == grid.p")
+        if not isinstance(part, BlockGraph):
+            part = BlockGraph.from_full(part, grid)
+        self.part = part
         self.grid, self.fanouts, self.b = grid, tuple(int(s) for s in fanouts), int(batch_size)
         self.mode, self.ledger = mode, ledger
         if fetch not in ("rows", "owner", "p2p", "split"):
@@ -115,15 +234,13 @@ class Sage15D:
         self._p2p = None
         self.rank = dist.get_rank()
         self.i, self.j = grid.coords(self.rank)
-        self.n = full.n
-        self.tables = full  # replay tables built on the global degree set
-        self.gdeg = (full.rowptr[1:] - full.rowptr[:-1]).to(torch.int32)
+        self.n = part.n
+        self.tables = part.tables  # global rowptr + replay tables, no columns
+        self.gdeg = part.gdeg
         self.bounds = _bounds(self.n, grid.rows)
-        lo, hi = int(self.bounds[self.i]), int(self.bounds[self.i + 1])
-        a0, a1 = int(full.rowptr[lo].item()), int(full.rowptr[hi].item())
-        self.row0 = lo
-        self.brp = (full.rowptr[lo:hi + 1] - a0).contiguous()
-        self.bcol = full.col[a0:a1].clone()
+        self.row0 = part.row0
+        self.brp = part.brp
+        self.bcol = part.bcol[: part.nnz]
         st = grid.stages
         self.V0 = int(self.bounds[self.j * st])
         self.V1 = int(self.bounds[(self.j + 1) * st])
@@ -161,13 +278,18 @@ class Sage15D:
             return self._pblk
         sz = torch.tensor([self.brp.numel(), self.bcol.numel()], dtype=torch.int64,
                           device=self.dev)
-        dist.all_reduce(sz, op=dist.ReduceOp.MAX)
+        _all_reduce(sz, op=dist.ReduceOp.MAX)
         nr, nc = (int(x) for x in sz.tolist())
         grp = dist.group.WORLD.group_name
         rp = symm_mem.empty(max(nr, 1), dtype=torch.int64, device=self.dev)
         cl = symm_mem.empty(max(nc, 1) + _lib.GB_COL_PAD, dtype=torch.int32, device=self.dev)
         rp[: self.brp.numel()].copy_(self.brp)
         cl[: self.bcol.numel()].copy_(self.bcol)
+        cl[self.bcol.numel():].zero_()
+        # the block lives only in symmetric memory from here on
+        nb, nc = self.brp.numel(), self.bcol.numel()
+        self.brp, self.bcol = rp[:nb], cl[:nc]
+        self.part.brp, self.part.bcol = rp[:nb], cl
         self._pblk = {"rp": rp, "rp_h": symm_mem.rendezvous(rp, grp), "cl": cl,
                       "cl_h": symm_mem.rendezvous(cl, grp)}
         self._pblk["rp_h"].barrier(channel=0)
@@ -419,8 +541,8 @@ class Sage15D:
         boffs[self.rank] = batch_offset
         boffs[grid.p] = k
         kmax = boffs[grid.p:].clone()
-        dist.all_reduce(boffs)
-        dist.all_reduce(kmax, op=dist.ReduceOp.MAX)
+        _all_reduce(boffs)
+        _all_reduce(kmax, op=dist.ReduceOp.MAX)
         boffs, kmax = boffs.tolist(), int(kmax.item())
         if boffs[grid.p] != k * grid.p or kmax != k:
             raise ContractViolation("fetch='p2p' needs the same number of batches on every grid row")
@@ -596,7 +718,7 @@ class Sage15D:
             # step 2: sample-then-reduce inside the grid row
             if self.grid.c > 1 and F:
                 t0 = self._phase(None, 0.0)
-                dist.all_reduce(fcol[:F], op=dist.ReduceOp.SUM,
+                _all_reduce(fcol[:F], op=dist.ReduceOp.SUM,
                                 group=self.row_groups[self.i])
                 self._phase("reduce", t0)
                 self.stats["reduce_words"] += F
@@ -782,10 +904,10 @@ class Ladies15D(Sage15D):
                            "gb_ladies_race_topk")
             nb = (moff[1:] - moff[:-1]).clone()
             if c > 1:
-                dist.all_reduce(nb, group=rg)
+                _all_reduce(nb, group=rg)
                 pack = torch.cat([take, Sv[:k * s].long(), (Sk[:k * s].long() & 0xffffffff)])
                 parts = [torch.empty_like(pack) for _ in range(c)]
-                dist.all_gather(parts, pack, group=rg)
+                _all_gather(parts, pack, group=rg)
             else:
                 parts = [torch.cat([take, Sv[:k * s].long(), Sk[:k * s].long() & 0xffffffff])]
             ct, cv, ck, cb = [], [], [], []
@@ -832,8 +954,8 @@ class Ladies15D(Sage15D):
                                                     _lib.ptr(slots), _lib.ptr(rcnt),
                                                     _lib.stream_ptr()), "gb_ladies_extract_rows")
             if c > 1 and QN:
-                dist.all_reduce(slots, group=rg)
-                dist.all_reduce(rcnt, group=rg)
+                _all_reduce(slots, group=rg)
+                _all_reduce(rcnt, group=rg)
                 self.stats["reduce_words"] += slots.numel() + rcnt.numel()
             aptr = torch.zeros(QN + 1, dtype=torch.int64, device=dev)
             aptr[1:] = torch.cumsum(rcnt[:QN].long(), 0)

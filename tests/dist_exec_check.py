@@ -22,16 +22,25 @@ def main():
 
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
-    dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
+    # GB_DIST_BACKEND=gloo: every rank shares cuda:0 and the exchanges travel
+    # through host copies — the executors' partitioning, keys and message
+    # logic checked on a one-GPU box (the peer-memory modes need NCCL)
+    gloo = os.environ.get("GB_DIST_BACKEND", "nccl") == "gloo"
+    torch.cuda.set_device(0 if gloo else int(os.environ.get("LOCAL_RANK", rank)))
+    if gloo:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl",
+                                device_id=torch.device("cuda", torch.cuda.current_device()))
     import paper_2311_02909_b200 as gb
     from paper_2311_02909_b200 import graphgen
     from paper_2311_02909_b200.dist import CommLedger, ProcessGrid, _bounds
-    from paper_2311_02909_b200.dist_exec import (Ladies15D, PeerFeatures, Sage15D,
+    from paper_2311_02909_b200.dist_exec import (BlockGraph, Ladies15D, PeerFeatures, Sage15D,
                                                  fetch_features_nccl, fetch_features_p2p,
                                                  ladies_epoch_15d, sage_epoch_15d)
 
-    dg = graphgen.rmat_device_graph(1 << 14, 200_000, symmetric=True, seed=3)
+    shape = (1 << 14, 200_000, True)
+    dg = graphgen.rmat_device_graph(*shape, seed=3)
     G = gb.Graph.from_device(dg)
     rng = np.random.default_rng(0)
     batches = [rng.permutation(dg.n)[:64] for _ in range(8)]
@@ -39,12 +48,30 @@ def main():
     serial = gb.sample_epoch_bulk(G, cfg, batches, epoch=1, batch_offset=5)
     ok = True
     grids = [(world, c) for c in (1, 2) if world % c == 0 and c * c <= world and world % (c * c) == 0]
+    modes = (("pfree", "rows"), ("stream", "rows"), ("pfree", "owner"))
+    if not gloo:
+        modes += (("pfree", "p2p"), ("dedup", "split"))
     for p, c in grids:
         grid = ProcessGrid(p, c)
-        for mode, fetch in (("pfree", "rows"), ("stream", "rows"), ("pfree", "owner"),
-                            ("pfree", "p2p"), ("dedup", "split")):
+        # block-only partition (gb_rmat_block): this rank's block equals the
+        # replicated graph's rows, the global degree metadata is exact, and
+        # only the block's columns are resident
+        part = BlockGraph.rmat(*shape, grid, seed=3)
+        full = BlockGraph.from_full(dg, grid)
+        same = (torch.equal(part.brp, full.brp) and
+                torch.equal(part.bcol[:part.nnz], full.bcol[:full.nnz]) and
+                torch.equal(part.tables.rowptr, dg.rowptr) and
+                part.tables.max_degree == dg.max_degree and
+                part.tables.table_slots == dg.table_slots)
+        ok &= same
+        if rank == 0:
+            print(f"grid ({p},{c}) block partition: {'PASS' if same else 'FAIL'} "
+                  f"resident {part.resident_bytes()} B vs replicated "
+                  f"{dg.rowptr.numel() * 8 + dg.nnz * 4} B", flush=True)
+        for mode, fetch in modes:
             led = CommLedger(p)
-            s = Sage15D(dg, grid, cfg.fanouts, cfg.batch_size, mode=mode, ledger=led, fetch=fetch)
+            src = part if fetch != "rows" else dg
+            s = Sage15D(src, grid, cfg.fanouts, cfg.batch_size, mode=mode, ledger=led, fetch=fetch)
             ep = sage_epoch_15d(s, cfg, batches, epoch=1, batch_offset=5)
             same = serial.equals(ep)
             ok &= same
@@ -54,8 +81,8 @@ def main():
         # LADIES (race) on the grid == single-GPU race sampler
         lcfg = gb.SamplerConfig.ladies(3, 64, 48, bulk_count=8, seed=4)
         lser = gb.sample_epoch_bulk(G, lcfg, batches, epoch=1, batch_offset=5, mode="race")
-        for lf in ("rows", "p2p"):
-            ls = Ladies15D(dg, grid, lcfg.fanouts, lcfg.batch_size, fetch=lf)
+        for lf in (("rows",) if gloo else ("rows", "p2p")):
+            ls = Ladies15D(part, grid, lcfg.fanouts, lcfg.batch_size, fetch=lf)
             lep = ladies_epoch_15d(ls, lcfg, batches, epoch=1, batch_offset=5)
             same = lser.equals(lep)
             ok &= same
@@ -74,15 +101,17 @@ def main():
         ok &= same
         if rank == 0:
             print(f"grid ({p},{c}) fetch_features: {'PASS' if same else 'FAIL'}", flush=True)
-        peer = PeerFeatures(Hb, rs, grid)
-        got = fetch_features_p2p(want, peer)
-        torch.cuda.synchronize()
-        same = bool(torch.equal(got, H[torch.as_tensor(want).cuda()]))
-        ok &= same
-        if rank == 0:
-            print(f"grid ({p},{c}) fetch_features p2p: {'PASS' if same else 'FAIL'}", flush=True)
-        peer.handle.barrier(channel=0)
-    t = torch.tensor([1 if ok else 0], device="cuda")
+        if not gloo:
+            peer = PeerFeatures(Hb, rs, grid)
+            got = fetch_features_p2p(want, peer)
+            torch.cuda.synchronize()
+            same = bool(torch.equal(got, H[torch.as_tensor(want).cuda()]))
+            ok &= same
+            if rank == 0:
+                print(f"grid ({p},{c}) fetch_features p2p: {'PASS' if same else 'FAIL'}",
+                      flush=True)
+            peer.handle.barrier(channel=0)
+    t = torch.tensor([1 if ok else 0], device="cpu" if gloo else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MIN)
     if rank == 0:
         print("ALL PASS" if int(t.item()) else "SOME FAILED", flush=True)

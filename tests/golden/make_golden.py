@@ -238,6 +238,75 @@ def spgemm_cases():
     print("spgemm: 40 cases")
 
 
+def pipeline_cases():
+    """The reference's epoch pipeline (pipeline.py:78-130, 200-305) on the
+    injected-uniform epochs: per-batch fetch_features + _propagate_batch
+    outputs (float64) for SAGE and LADIES bulks, fetch_features on a 4 x 2
+    grid with its ledger, and run_epoch's accounting on three grids."""
+    from gnnbulk import pipeline as ref_pipeline
+    from gnnbulk.dist import CommLedger, ProcessGrid
+
+    n, src, dst = rmat_edges(10, 6000, seed=1)
+    G = Graph.from_edges(n, src, dst)
+    H = gnnbulk.synthesize_features(n, 8, 5)
+    out = {}
+    pack_csr("A", G.adjacency, out, values=False)
+    out["H"] = H
+    rng = np.random.default_rng(12)
+    for kind in ("sage", "ladies"):
+        if kind == "sage":
+            cfg = gnnbulk.SamplerConfig.sage(3, 16, (6, 4, 3), bulk_count=4, seed=3)
+            batches = [rng.permutation(n)[: rng.integers(1, 17)] for _ in range(4)]
+        else:
+            cfg = gnnbulk.SamplerConfig.ladies(2, 16, 12, bulk_count=4, seed=3)
+            batches = [np.sort(rng.permutation(n)[: rng.integers(1, 17)]) for _ in range(4)]
+        ep = gnnbulk.sample_epoch_bulk(G, cfg, batches, epoch=2, batch_offset=3)
+        grid = ProcessGrid(1, 1)
+        Hp = ref_pipeline.FeaturePartition.partition(H, grid)
+        ys = []
+        for b in range(len(batches)):
+            X = ref_pipeline.fetch_features(ep.layers[-1].col_vertices[b], Hp, grid)
+            ys.append(ref_pipeline._propagate_batch(ep, b, X))
+        pack_ragged(f"{kind}_batches", batches, out)
+        out[f"{kind}_cfg"] = np.array([cfg.layers, cfg.batch_size, cfg.seed] + list(cfg.fanouts),
+                                      dtype=np.int64)
+        out[f"{kind}_Y"] = np.concatenate(ys)
+        out[f"{kind}_Yoff"] = np.cumsum([0] + [y.shape[0] for y in ys])
+        sub = {}
+        pack_epoch(ep, sub)
+        for key, val in sub.items():
+            out[f"{kind}_ep_{key}"] = val
+    grid = ProcessGrid(4, 2)
+    Hp = ref_pipeline.FeaturePartition.partition(H, grid)
+    verts = rng.integers(0, n, size=400)
+    out["fetch_verts"] = verts
+    words = np.zeros((4, 4), dtype=np.int64)  # requester x process
+    msgs = np.zeros((4, 4), dtype=np.int64)
+    for req in range(4):
+        led = CommLedger(4)
+        rows = ref_pipeline.fetch_features(verts, Hp, grid, led, req)
+        assert np.array_equal(rows, H[verts])
+        for proc in range(4):
+            words[req, proc] = led.words(phase="all-to-allv", process=proc)
+            msgs[req, proc] = led.messages(phase="all-to-allv", process=proc)
+    out["fetch_words"], out["fetch_msgs"] = words, msgs
+    cfg = gnnbulk.SamplerConfig.sage(2, 64, (5, 3), bulk_count=4, seed=6)
+    acc = []
+    for p, c, mode in ((1, 1, "replicated"), (4, 1, "replicated"), (4, 2, "partitioned")):
+        grid = ProcessGrid(p, c)
+        rep = ref_pipeline.run_epoch(G, ref_pipeline.FeaturePartition.partition(H, grid), cfg,
+                                     grid, mode=mode, epoch=1)
+        led = rep.ledger
+        row = [p, c, rep.n_batches, rep.chunks, rep.spgemm_calls]
+        row += list(rep.batches_per_process) + [0] * (4 - p)
+        row += [led.messages(phase=ph) for ph in gnnbulk.PHASES]
+        row += [led.words(phase=ph) for ph in gnnbulk.PHASES]
+        acc.append(row)
+    out["run_epoch"] = np.array(acc, dtype=np.int64)
+    np.savez_compressed(os.path.join(HERE, "pipeline.npz"), **out)
+    print("pipeline: propagate (sage, ladies), fetch 4x2, run_epoch x3")
+
+
 def main():
     patch_rng()
     fig = figure_graph()
@@ -257,6 +326,7 @@ def main():
     epoch_case("rmat12_ladies", mid, "ladies", 2, 64, 32, 3, seed=0, batch_seed=7)
     its_cases()
     spgemm_cases()
+    pipeline_cases()
 
 
 if __name__ == "__main__":

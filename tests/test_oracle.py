@@ -65,3 +65,45 @@ def test_oracle_threads_do_not_change_output():
         got = O.sage_bulk(g["n"], g["rowptr"], g["col"], g["batches"], g["batch_size"],
                           g["fanouts"], g["seed"], threads=th)
         assert O.compare_epochs(want, got) == []
+
+
+def _pipeline_golden():
+    z = dict(np.load(os.path.join(GOLDEN, "pipeline.npz")))
+    return z
+
+
+def _ragged(z, name):
+    off, cat = z[name + "_off"], z[name + "_cat"]
+    return [cat[off[i]:off[i + 1]] for i in range(len(off) - 1)]
+
+
+def test_pipeline_restatement_matches_reference_outputs():
+    """oracle/pipeline_ref.py (the pipeline checker of the GPU tests) against
+    the reference's own fetch_features + _propagate_batch outputs
+    (pipeline.py:78-130, 273-305) on injected-uniform epochs, SAGE and
+    LADIES — pins the pipeline oracle."""
+    from oracle import pipeline_ref as PR
+
+    z = _pipeline_golden()
+    H = z["H"]
+    for kind in ("sage", "ladies"):
+        _, layers = O.load_golden(os.path.join(GOLDEN, "pipeline.npz"), prefix=f"{kind}_ep_")
+        Y, Yoff = z[f"{kind}_Y"], z[f"{kind}_Yoff"]
+        deep = layers[-1]
+        for b in range(len(Yoff) - 1):
+            X = H[deep["colv_cat"][deep["colv_off"][b]:deep["colv_off"][b + 1]]]
+            got = PR.propagate_batch(layers, b, X)
+            assert np.allclose(got, Y[Yoff[b]:Yoff[b + 1]], rtol=1e-12, atol=1e-12), (kind, b)
+
+
+def test_pipeline_fetch_ledger_matches_reference():
+    from oracle import pipeline_ref as PR
+
+    z = _pipeline_golden()
+    n = int(z["A_shape"][0])
+    rs = np.linspace(0, n, 3).astype(np.int64)  # FeaturePartition bounds, 4 x 2 grid
+    for req in range(4):
+        want = PR.fetch_words(z["fetch_verts"], rs, z["H"].shape[1], 2, 2, req)
+        for proc in range(4):
+            m, w = want.get(proc, (0, 0))
+            assert (m, w) == (z["fetch_msgs"][req, proc], z["fetch_words"][req, proc])

@@ -129,3 +129,86 @@ def test_run_epoch_accounting():
                 want[PR.trainer_of_batch(local, size, p, grid.rows, c, mode == "replicated")] += 1
         assert rep.batches_per_process == want
         assert set(rep.durations) == {"sample", "fetch", "propagate"}
+
+
+def _pipeline_golden():
+    import os
+
+    from conftest import GOLDEN
+
+    return os.path.join(GOLDEN, "pipeline.npz"), dict(np.load(os.path.join(GOLDEN,
+                                                                         "pipeline.npz")))
+
+
+@pytest.mark.parametrize("kind", ["sage", "ladies"])
+def test_propagate_matches_reference_outputs(kind):
+    """The device pipeline against the reference's own fetch_features +
+    _propagate_batch outputs (tests/golden/pipeline.npz, make_golden.py):
+    the bulk's epoch is bit-exact with the reference epoch, the propagated
+    rows agree within 1e-5 (device fp32, reference fp64)."""
+    import torch
+
+    from oracle import oracle as O
+
+    gb = _gb()
+    path, z = _pipeline_golden()
+    g, want_layers = O.load_golden(path, prefix=f"{kind}_ep_")
+    G = gb.Graph(gb.SparseMatrix(g["n"], g["n"], g["rowptr"], g["col"], np.ones(len(g["col"])),
+                                 validate=False))
+    c = z[f"{kind}_cfg"]
+    off, cat = z[f"{kind}_batches_off"], z[f"{kind}_batches_cat"]
+    batches = [cat[off[i]:off[i + 1]] for i in range(len(off) - 1)]
+    if kind == "sage":
+        cfg = gb.SamplerConfig.sage(int(c[0]), int(c[1]), tuple(int(x) for x in c[3:]),
+                                    bulk_count=len(batches), seed=int(c[2]))
+        mode = "dedup"
+    else:
+        cfg = gb.SamplerConfig.ladies(int(c[0]), int(c[1]), int(c[3]), bulk_count=len(batches),
+                                      seed=int(c[2]))
+        mode = "exact"
+    ep = gb.sample_epoch_bulk(G, cfg, batches, epoch=2, batch_offset=3, mode=mode)
+    assert O.compare_epochs(want_layers, ep.to_arrays()) == []
+    H = z["H"]
+    deep = want_layers[-1]
+    X = torch.as_tensor(H[deep["colv_cat"]].astype(np.float32)).cuda()
+    Y = gb.propagate_bulk(ep, X).cpu().numpy().astype(np.float64)
+    Yw, Yoff = z[f"{kind}_Y"], z[f"{kind}_Yoff"]
+    roff = want_layers[0]["rowv_off"]
+    for b in range(len(batches)):
+        _close(Y[roff[b]:roff[b + 1]], Yw[Yoff[b]:Yoff[b + 1]])
+
+
+def test_fetch_and_run_epoch_match_reference_ledger():
+    """fetch_features on a 4 x 2 grid (rows and all-to-allv ledger) and
+    run_epoch's accounting (batches, chunks, spgemm calls, per-process
+    counts, ledger messages / words per phase) against the reference's own
+    outputs (tests/golden/pipeline.npz)."""
+    gb = _gb()
+    from paper_2311_02909_b200.dist import PHASES, CommLedger, ProcessGrid
+
+    path, z = _pipeline_golden()
+    n = int(z["A_shape"][0])
+    G = gb.Graph(gb.SparseMatrix(n, n, z["A_ptr"], z["A_col"], np.ones(len(z["A_col"])),
+                                 validate=False))
+    H = z["H"]
+    grid = ProcessGrid(4, 2)
+    Hp = gb.FeaturePartition.partition(H, grid)
+    for req in range(4):
+        led = CommLedger(4)
+        rows = gb.fetch_features(z["fetch_verts"], Hp, grid, led, req)
+        _close(rows, H[z["fetch_verts"]])
+        for proc in range(4):
+            assert led.words(phase="all-to-allv", process=proc) == z["fetch_words"][req, proc]
+            assert led.messages(phase="all-to-allv", process=proc) == z["fetch_msgs"][req, proc]
+    cfg = gb.SamplerConfig.sage(2, 64, (5, 3), bulk_count=4, seed=6)
+    for row in z["run_epoch"]:
+        p, c = int(row[0]), int(row[1])
+        mode = "replicated" if (p, c) != (4, 2) else "partitioned"
+        grid = ProcessGrid(p, c)
+        rep = gb.run_epoch(G, gb.FeaturePartition.partition(H, grid), cfg, grid, mode=mode,
+                           epoch=1)
+        got = [p, c, rep.n_batches, rep.chunks, rep.spgemm_calls]
+        got += list(rep.batches_per_process) + [0] * (4 - p)
+        got += [rep.ledger.messages(phase=ph) for ph in PHASES]
+        got += [rep.ledger.words(phase=ph) for ph in PHASES]
+        assert got == [int(x) for x in row], (p, c, mode)

@@ -266,3 +266,58 @@ def test_sage_hub_rows_dedup_matches_oracle():
     for mode in MODES:
         ep = gb.sample_epoch_bulk(G, cfg, batches, mode=mode)
         assert O.compare_epochs(want, ep.to_arrays()) == [], mode
+
+
+def _baseline_graph(shape):
+    gb = _pkg()
+    from paper_2311_02909_b200.graphgen import SHAPES, rmat_device_graph
+
+    n, m, sym = SHAPES[shape]
+    dg = rmat_device_graph(n, m, symmetric=sym, seed=0)
+    return gb.Graph.from_device(dg), dg
+
+
+def _baseline_batches(n, k):
+    from paper_2311_02909_b200.pipeline import make_batches
+
+    return make_batches(np.arange(n), 1024, seed=0, epoch=0)[:k]
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_cfg1_bulk_matches_oracle(mode):
+    """BASELINE configs[0] exactly: R-MAT scale 16 (65,536 vertices, 2^20
+    undirected pairs), b = 1024, (15, 10, 5), k = 8 — bit-exact with the C
+    oracle (which is pinned to the reference's own outputs)."""
+    G, dg = _baseline_graph("cfg1")
+    batches = _baseline_batches(dg.n, 8)
+    cfg = _pkg().SamplerConfig.sage(3, 1024, (15, 10, 5), bulk_count=8, seed=0)
+    ep = _pkg().sample_epoch_bulk(G, cfg, batches, mode=mode)
+    rowptr = dg.rowptr.cpu().numpy()
+    col = dg.col[: dg.nnz].cpu().numpy()
+    want = O.sage_bulk(dg.n, rowptr, col, batches, 1024, (15, 10, 5), 0, 0, 0, threads=8)
+    assert O.compare_epochs(want, ep.to_arrays()) == []
+
+
+def test_cfg2_full_size_bulk_matches_oracle():
+    """BASELINE configs[1] at full size: products-shape R-MAT (2,449,029
+    vertices, 123.7M entries), b = 1024, (15, 10, 5), k = 64 through the
+    bench's engine path (SageBulk, dedup Alg. 1) — every layer bit-exact with
+    the C oracle on all 64 minibatches."""
+    import torch
+
+    from paper_2311_02909_b200.engine import SageBulk, upload_batches
+
+    G, dg = _baseline_graph("products")
+    batches = _baseline_batches(dg.n, 64)
+    d_off, d_cat, r1 = upload_batches(batches, dg.n, 1024)
+    bulk = SageBulk(dg, 64, r1, 1024, (15, 10, 5), mode="dedup")
+    bulk.launch(d_off, d_cat, 0, 0, 0)
+    torch.cuda.synchronize()
+    from paper_2311_02909_b200.sampler import SampledEpoch, SamplerKind
+
+    got = SampledEpoch(SamplerKind.SAGE, 0, batches, bulk.layers(d_off, d_cat), 3).to_arrays()
+    rowptr = dg.rowptr.cpu().numpy()
+    col = dg.col[: dg.nnz].cpu().numpy()
+    want = O.sage_bulk(dg.n, rowptr, col, batches, 1024, (15, 10, 5), 0, 0, 0,
+                       threads=os.cpu_count() or 8)
+    assert O.compare_epochs(want, got) == []

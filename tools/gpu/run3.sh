@@ -1,0 +1,8 @@
+set -x
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail -30 gpurun_out/build.log; exit 1; }
+timeout 900 python -m pytest tests/test_sage_gpu.py -x -q > gpurun_out/pytest_sage.log 2>&1
+tail -15 gpurun_out/pytest_sage.log
+timeout 300 python tools/profile_bulk.py --mode dedup > gpurun_out/pb.log 2>&1 && \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_dedup.csv \
+    python tools/profile_bulk.py --mode dedup --warm 1 > gpurun_out/ncu_a.log 2>&1
+python tools/bulk_launches.py gpurun_out/launches_dedup.csv k_set_i64 2>&1 | tail -45
