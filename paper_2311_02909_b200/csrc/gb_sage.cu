@@ -587,14 +587,14 @@ __global__ void __launch_bounds__(kGrpThreads) k_grp_count(
   }
 }
 
-// Work tiers by row degree d: A (d <= kTierAHi) packed into bins of the
-// serve ring, B (longer rows) staged in chunks.  An item serves at most
-// rows_item(d) frontier rows (about 512 / 2048 / 8192 picks).
-constexpr int kTierAHi = 4096;
-constexpr int kServeUnroll = 4;  // picks in flight per serve thread
-
+// Serve tiers by row degree d (DdTier below): 0 d <= 1K, 1 d <= 8K, 2 hubs.
+// An item serves at most rows_item(d) frontier rows (about 512 / 2048 /
+// 8192 picks).
+__host__ __device__ __forceinline__ int dd_tier(int64_t d) {
+  return d <= 1024 ? 0 : d <= 8192 ? 1 : 2;
+}
 __host__ __device__ __forceinline__ int32_t rows_item(int64_t d, int32_t s) {
-  const int32_t p = d <= 1024 ? 512 : d <= kTierAHi ? 2048 : 8192;
+  const int32_t p = d <= 1024 ? 512 : d <= 8192 ? 2048 : 8192;
   const int32_t r = p / s;
   return r < 1 ? 1 : r;
 }
@@ -618,17 +618,18 @@ struct PeerRows {
   const int32_t* const* bcol;
 };
 
-// tier t's items live in [t * icap, t * icap + tcnt[t]); tcnt[2] counts the
-// grouped rows.  kGrpU distinct vertices per thread, their gathers issued
-// together (the pass is latency-bound on random rowptr / counter loads).
+// tier t's items live in [t * icap, t * icap + tcnt[t]) (t = serve tier by
+// degree); tcnt[3] counts the grouped rows.  kGrpU distinct vertices per
+// thread, their gathers issued together (the pass is latency-bound on
+// random rowptr / counter loads).
 constexpr int kItemThreads = 256;
 __global__ void __launch_bounds__(kItemThreads) k_grp_items(
     const unsigned long long* __restrict__ dcount, const int32_t* __restrict__ dv,
     const int64_t* __restrict__ rowptr, int32_t* __restrict__ vcnt, int32_t* __restrict__ roff,
     int32_t s, int64_t icap, unsigned long long* __restrict__ tcnt, DdItem* __restrict__ items,
     PeerRows peer) {
-  __shared__ int32_t s_wsum[3][kItemThreads / 32];
-  __shared__ int64_t s_base[3];
+  __shared__ int32_t s_wsum[4][kItemThreads / 32];
+  __shared__ int64_t s_base[4];
   const int64_t D = (int64_t)*dcount;
   const int lane = lane_id(), wid = threadIdx.x >> 5;
   constexpr int64_t kBlk = (int64_t)kItemThreads * kGrpU;
@@ -650,7 +651,7 @@ __global__ void __launch_bounds__(kItemThreads) k_grp_items(
         gc[u] = vcnt[v[u]];
       }
     }
-    int tot[3] = {0, 0, 0};
+    int tot[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int u = 0; u < kGrpU; ++u) {
       n[u] = 0;
@@ -659,41 +660,43 @@ __global__ void __launch_bounds__(kItemThreads) k_grp_items(
       if (v[u] >= 0) {
         vcnt[v[u]] = 0;  // ready for the next layer
         d[u] -= a0[u];
-        t[u] = d[u] <= kTierAHi ? 0 : 1;
+        t[u] = dd_tier(d[u]);
         per[u] = rows_item(d[u], s);
         n[u] = (gc[u] + per[u] - 1) / per[u];
-        tot[0] += t[u] ? 0 : n[u];
-        tot[1] += t[u] ? n[u] : 0;
-        tot[2] += gc[u];
+        tot[0] += t[u] == 0 ? n[u] : 0;
+        tot[1] += t[u] == 1 ? n[u] : 0;
+        tot[2] += t[u] == 2 ? n[u] : 0;
+        tot[3] += gc[u];
       }
     }
-    // per-tier item offsets and the rows' range (z = 2) inside the block
-    int incl[3];
+    // per-tier item offsets and the rows' range (z = 3) inside the block
+    int incl[4];
 #pragma unroll
-    for (int z = 0; z < 3; ++z) {
+    for (int z = 0; z < 4; ++z) {
       incl[z] = warp_incl_scan(tot[z]);
       if (lane == 31) s_wsum[z][wid] = incl[z];
     }
     __syncthreads();
-    if (threadIdx.x < 3) {
+    if (threadIdx.x < 4) {
       int all = 0;
       for (int w = 0; w < kItemThreads / 32; ++w) all += s_wsum[threadIdx.x][w];
       s_base[threadIdx.x] =
           all ? (int64_t)atomicAdd(tcnt + threadIdx.x, (unsigned long long)all) : 0;
     }
     __syncthreads();
-    int64_t o[3];
+    int64_t o[4];
 #pragma unroll
-    for (int z = 0; z < 3; ++z) {
+    for (int z = 0; z < 4; ++z) {
       o[z] = s_base[z] + incl[z] - tot[z];
       for (int w = 0; w < wid; ++w) o[z] += s_wsum[z][w];
     }
 #pragma unroll
     for (int u = 0; u < kGrpU; ++u) {
       if (!n[u]) continue;
-      const int64_t r0 = o[2], oi = t[u] ? o[1] + icap : o[0];
-      o[2] += gc[u];
-      if (t[u]) o[1] += n[u]; else o[0] += n[u];
+      const int64_t r0 = o[3];
+      const int64_t oi = (t[u] == 0 ? o[0] : t[u] == 1 ? o[1] : o[2]) + (int64_t)t[u] * icap;
+      o[3] += gc[u];
+      if (t[u] == 0) o[0] += n[u]; else if (t[u] == 1) o[1] += n[u]; else o[2] += n[u];
       roff[v[u]] = (int32_t)r0;
       int64_t ad = a0[u];
       if (peer.nblk) {
@@ -840,7 +843,8 @@ struct DdArgs {
   int32_t* fcol;
   uint32_t* bitmap;
   int64_t nwords;
-  unsigned int* ticket;            // k_dd_serve work counter (zeroed per layer)
+  unsigned int* ticket;            // (unused by the tiered serve)
+  int32_t chunk;                   // staged entries per pass (tier 2), row buffer (tier 0 / 1)
 };
 
 // pick (row i of an item, draw t): entry index, frontier position, batch
@@ -857,189 +861,195 @@ __device__ __forceinline__ void dd_put(const DdArgs& A, int32_t fp, int32_t bb, 
   atomicOr(A.bitmap + (uint32_t)bb * (uint32_t)A.nwords + pk_word(cv), 1u << (cv & 31));
 }
 
-// Serve: producer / consumer over a ring of TMA stages.  Warp 0 of each CTA
-// is the producer: it takes 32 work items at a time (ticket order over both
-// tiers), packs consecutive short rows into the open bin of the ring (one
-// TMA bulk copy per row, bytes announced with mbarrier.expect_tx) and cuts
-// long rows into chunk bins, then arrives on the bin's full barrier; the
-// other warps consume bins in ring order — every pick of the bin's items
-// served from shared memory (frontier entry + (batch, vertex) bit) — and
-// release the stage on its empty barrier.  Stages land while earlier bins
-// are served, so each CTA keeps kStages - 1 row panels in flight.
-constexpr int kSvThreads = 256;                     // warp 0 producer, 7 consumer warps
-constexpr int kSvConsumers = kSvThreads - 32;
-constexpr int kStages = 3;
-constexpr int kLongChunk = 8192;                    // entries per chunk bin of a long row
-constexpr int kSvStageInts = kLongChunk + 16;       // one chunk or a packed bin
-constexpr int kBinItems = 128;                      // items per packed bin
-
-struct SvStage {
-  int32_t buf[kSvStageInts];
-  int4 meta[kBinItems];  // (shift into buf, first grouped row, take (neg: every entry), pick prefix)
-  int32_t nitems, npicks, lo, hi;  // hi < 0: end of the work
+// Serve, three size tiers of distinct rows (degree d): 0 warp-batched
+// (d <= 1K: a warp takes 32 work items, packs as many of their rows as fit
+// its 4 KB buffer with 16-B cp.async granules and serves all their picks
+// lane-parallel — short rows are too small for a bulk copy each), 1 CTA-256
+// per item (d <= 8K: the row is one TMA bulk copy), 2 CTA-1024 per item
+// (hubs: TMA chunks as large as shared memory allows).  The next item's
+// descriptor and each pass's pick metadata load while the row lands.
+template <int T> struct DdTier;
+template <> struct DdTier<0> {
+  static constexpr int kThreads = 256, kHi = 1024;
+  static constexpr bool kWarp = true;
+};
+template <> struct DdTier<1> {
+  static constexpr int kThreads = 256, kHi = 8192;
+  static constexpr bool kWarp = false;
+};
+template <> struct DdTier<2> {
+  static constexpr int kThreads = 1024, kHi = 0x7fffffff;
+  static constexpr bool kWarp = false;
 };
 
-__device__ __forceinline__ void mbar_expect_tx_only(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem));
 }
 
-__global__ void __launch_bounds__(kSvThreads) k_dd_serve(DdArgs A) {
-  extern __shared__ __align__(128) unsigned char svraw[];
-  SvStage* st = reinterpret_cast<SvStage*>(svraw);
-  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
-  const int tid = threadIdx.x, lane = lane_id(), wid = tid >> 5;
-  if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kSvConsumers / 32);
-    }
-  }
-  __syncthreads();
-  const int s = A.s;
-  const int64_t n0 = (int64_t)A.tcnt[0], n1 = (int64_t)A.tcnt[1], ntot = n0 + n1;
-  if (wid == 0) {
-    // ------------------------------------------------------------ producer
-    int64_t bin = 0;          // bins opened so far (ring position)
-    int open = 0;             // a packed bin is open in slot (bin - 1) % kStages
-    int cur_ints = 0, cur_items = 0, cur_picks = 0;
-    auto open_bin = [&]() -> SvStage& {
-      const int sl = (int)(bin % kStages);
-      if (bin >= kStages) mbar_wait(&empty[sl], (uint32_t)((bin / kStages - 1) & 1));
-      ++bin;
-      return st[sl];
-    };
-    auto commit = [&](SvStage& S, int nitems, int npicks, int lo, int hi) {
-      __syncwarp();  // every lane's meta / expect_tx before the arrive
-      if (lane == 0) {
-        S.nitems = nitems; S.npicks = npicks; S.lo = lo; S.hi = hi;
-        mbar_arrive(&full[(int)((bin - 1) % kStages)]);
+constexpr int kGrpInts = 6 * 33;  // per-warp group table of the warp tier
+
+// (frontier offset, batch) of grouped row q: the second half of its record
+__device__ __forceinline__ int2 dd_fb(const DdArgs& A, int32_t q) {
+  return reinterpret_cast<const int2*>(A.rrec)[2 * (uint32_t)q + 1];
+}
+
+__device__ void dd_serve_warp(const DdArgs& A, int32_t* buf, int B, int32_t* gi) {
+  int32_t* g_pst = gi;            // pair start per item (+ sentinel)
+  int32_t* g_rof = gi + 33;       // row base in buf (16-B alignment shift included)
+  int32_t* g_q0 = gi + 66;        // first grouped row
+  int32_t* g_tk = gi + 99;        // take, negated when take == d (every entry)
+  uint32_t* g_mg = (uint32_t*)(gi + 132);  // ceil(2^32 / take)
+  const int lane = lane_id(), s = A.s;
+  const uint32_t NW = (uint32_t)A.nwords;
+  const int64_t it1 = (int64_t)A.tcnt[0];
+  const int64_t nblk = (it1 + 31) / 32;
+  for (int64_t blk = global_warp(); blk < nblk; blk += grid_warps()) {
+    const int64_t it = blk * 32 + lane;
+    const int nitems = (int)min((int64_t)32, it1 - blk * 32);
+    DdItem c{};
+    const bool valid = lane < nitems;
+    if (valid) c = A.items[it];
+    const int len = valid ? dd_row_len(c.a0, c.d) : 0;
+    const int take = valid ? min(c.d, s) : 0;
+    const int np = valid ? c.nrows * take : 0;
+    for (int j0 = 0; j0 < nitems;) {
+      // sub-group [j0, j1): rows packed while they fit (always at least one)
+      const int lz = lane >= j0 ? len : 0;
+      const int incl = warp_incl_scan(lz);
+      const unsigned fit = __ballot_sync(0xffffffffu, lane >= j0 && lane < nitems && incl <= B);
+      const int j1 = fit ? 32 - __clz(fit) : j0 + 1;
+      const bool in = lane >= j0 && lane < j1;
+      const int pz = in ? np : 0;
+      const int pinc = warp_incl_scan(pz);
+      const int P = __shfl_sync(0xffffffffu, pinc, j1 - 1);
+      if (in) {
+        const int j = lane - j0;
+        g_pst[j] = pinc - pz;
+        g_rof[j] = incl - lz + (int)(c.a0 & 3);
+        g_q0[j] = c.q0;
+        g_tk[j] = take == c.d ? -take : take;
+        g_mg[j] = 0xffffffffu / (uint32_t)take + 1u;
       }
+      if (lane == 0) g_pst[j1 - j0] = P;
+      for (int j = j0; j < j1; ++j) {
+        const int64_t a0 = __shfl_sync(0xffffffffu, c.a0, j);
+        const int32_t d = __shfl_sync(0xffffffffu, c.d, j);
+        const int o = __shfl_sync(0xffffffffu, incl - lz, j);
+        const int64_t al0 = a0 & ~3LL;
+        for (int64_t e = al0 + 4 * lane; e < a0 + d; e += 128)
+          cp_async16(buf + o + (int)(e - al0), A.col + e);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
       __syncwarp();
-    };
-    SvStage* S = nullptr;
-    // a contiguous share of the items per CTA (no shared work counter)
-    const int64_t my0 = ntot * blockIdx.x / gridDim.x, my1 = ntot * (blockIdx.x + 1) / gridDim.x;
-    for (int64_t base = my0; base < my1; base += 32) {
-      const int64_t gi = base + lane;
-      const bool valid = gi < my1;
-      DdItem it{};
-      if (valid) it = A.items[gi < n0 ? gi : A.icap + (gi - n0)];
-      const bool longrow = valid && it.d > kTierAHi;
-      const int take = valid ? min(it.d, s) : 0;
-      const int len = valid && !longrow ? dd_row_len(it.a0, it.d) : 0;
-      const int np = valid ? it.nrows * take : 0;
-      // lanes in order: runs of short rows packed, long rows one by one
-      unsigned todo = __ballot_sync(0xffffffffu, valid);
-      while (todo) {
-        const int first = __ffs(todo) - 1;
-        const unsigned longs = __ballot_sync(0xffffffffu, longrow) & todo;
-        if (longs & (1u << first)) {
-          // long row: its own chunk bins (the open packed bin is committed first)
-          if (open) { commit(*S, cur_items, cur_picks, 0, 0x7fffffff); open = 0; }
-          const int64_t a0 = __shfl_sync(0xffffffffu, it.a0, first);
-          const int32_t d = __shfl_sync(0xffffffffu, it.d, first);
-          const int32_t q0 = __shfl_sync(0xffffffffu, it.q0, first);
-          const int32_t npf = __shfl_sync(0xffffffffu, np, first);
-          const int32_t tkf = __shfl_sync(0xffffffffu, take, first);
-          for (int32_t e0 = 0; e0 < d; e0 += kLongChunk) {
-            const int32_t e1 = min(e0 + kLongChunk, d);
-            SvStage& C = open_bin();
-            if (lane == 0) {
-              const int64_t al0 = (a0 + e0) & ~3LL;
-              const uint32_t bytes = 4u * (uint32_t)dd_row_len(a0 + e0, e1 - e0);
-              C.meta[0] = make_int4((int32_t)(a0 + e0 - al0) - e0, q0, tkf, 0);
-              fence_async_smem();
-              mbar_expect_tx_only(&full[(int)((bin - 1) % kStages)], bytes);
-              tma_row(C.buf, A.col + al0, bytes, &full[(int)((bin - 1) % kStages)]);
-            }
-            commit(C, 1, npf, e0, e1);
-          }
-          todo &= ~(1u << first);
-          continue;
+      const int ng = j1 - j0;
+      auto meta = [&](int p, int32_t& idx, int32_t& fp, int32_t& bb, int32_t& ro) {
+        int lo = 0, hi = ng;
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (g_pst[mid] <= p) lo = mid; else hi = mid;
         }
-        // the run of short rows starting at `first` (up to the next long row)
-        const unsigned nextlong = longs & ~((2u << first) - 1u);
-        const int end = nextlong ? __ffs(nextlong) - 1 : 32;
-        const bool inrun = lane >= first && lane < end && valid;
-        if (!open) {
-          S = &open_bin();
-          open = 1;
-          cur_ints = cur_items = cur_picks = 0;
+        const int tk = g_tk[lo], tkn = tk < 0 ? -tk : tk;
+        const int r = p - g_pst[lo];
+        const int i = tkn == 1 ? r : (int)__umulhi((uint32_t)r, g_mg[lo]);
+        const int t = r - i * tkn;
+        const int q = g_q0[lo] + i;
+        idx = tk < 0 ? t : A.pidx[(uint32_t)q * (uint32_t)s + (uint32_t)t];
+        const int2 fb = dd_fb(A, q);
+        fp = fb.x + t;
+        bb = fb.y;
+        ro = g_rof[lo];
+      };
+      int32_t idx = 0, fp = 0, bb = 0, ro = 0;
+      if (lane < P) meta(lane, idx, fp, bb, ro);
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+      __syncwarp();
+      for (int p0 = 0; p0 < P; p0 += 32) {
+        int32_t idx2 = 0, fp2 = 0, bb2 = 0, ro2 = 0;
+        if (p0 + 32 + lane < P) meta(p0 + 32 + lane, idx2, fp2, bb2, ro2);
+        if (p0 + lane < P) {
+          const int32_t cv = buf[ro + idx];
+          A.fcol[(uint32_t)fp] = cv;
+          atomicOr(A.bitmap + ((uint32_t)bb * NW + pk_word(cv)), 1u << (cv & 31));
         }
-        const int li = warp_incl_scan(inrun ? len : 0);
-        const int pi = warp_incl_scan(inrun ? np : 0);
-        const int ci = warp_incl_scan(inrun ? 1 : 0);
-        const bool fits = inrun && cur_ints + li <= kSvStageInts && cur_items + ci <= kBinItems;
-        const unsigned fm = __ballot_sync(0xffffffffu, fits);
-        if (fits) {
-          const int off = cur_ints + li - len;
-          const int sl = (int)((bin - 1) % kStages);
-          S->meta[cur_items + ci - 1] =
-              make_int4(off + (int)(it.a0 & 3), it.q0, take == it.d ? -take : take,
-                        cur_picks + pi - np);
-          fence_async_smem();
-          mbar_expect_tx_only(&full[sl], 4u * (uint32_t)len);
-          tma_row(S->buf + off, A.col + (it.a0 & ~3LL), 4u * (uint32_t)len, &full[sl]);
-        }
-        if (fm) {
-          const int lastfit = 31 - __clz(fm);
-          cur_ints += __shfl_sync(0xffffffffu, li, lastfit);
-          cur_picks += __shfl_sync(0xffffffffu, pi, lastfit);
-          cur_items += __shfl_sync(0xffffffffu, ci, lastfit);
-          todo &= ~fm;
-        }
-        const unsigned runmask = end == 32 ? 0xffffffffu : (1u << end) - 1u;
-        if ((todo & (1u << first)) || (fm && (todo & ~longs & runmask))) {
-          // the bin is full: commit, the rest of the run goes to a new bin
-          commit(*S, cur_items, cur_picks, 0, 0x7fffffff);
-          open = 0;
-        }
+        idx = idx2; fp = fp2; bb = bb2; ro = ro2;
       }
+      __syncwarp();  // buffer and group table free
+      j0 = j1;
     }
-    if (open) commit(*S, cur_items, cur_picks, 0, 0x7fffffff);
-    SvStage& E = open_bin();
-    commit(E, 0, 0, 0, -1);  // end of the work
-    return;
   }
-  // -------------------------------------------------------------- consumers
-  const int ctid = tid - 32;
-  for (int64_t bin = 0;; ++bin) {
-    const int sl = (int)(bin % kStages);
-    mbar_wait(&full[sl], (uint32_t)((bin / kStages) & 1));
-    const SvStage& S = st[sl];
-    const int nitems = S.nitems, NP = S.npicks, lo = S.lo, hi = S.hi;
-    if (hi < 0) break;
-    for (int p0 = ctid; p0 < NP; p0 += kSvConsumers * kServeUnroll) {
-      int32_t idx[kServeUnroll], fp[kServeUnroll], bb[kServeUnroll], sh[kServeUnroll];
-#pragma unroll
-      for (int u = 0; u < kServeUnroll; ++u) {
-        const int p = p0 + u * kSvConsumers;
-        idx[u] = -1;
-        if (p < NP) {
-          int a = 0, b = nitems - 1;  // last item with pick prefix <= p
-          while (a < b) {
-            const int mid = (a + b + 1) >> 1;
-            if (S.meta[mid].w <= p) a = mid; else b = mid - 1;
-          }
-          const int4 m = S.meta[a];
-          const int tkn = m.z < 0 ? -m.z : m.z;
-          const int r = p - m.w;
-          const int i = r / tkn, t = r - i * tkn;
-          dd_pair(A, m.y + i, t, tkn, m.z < 0, idx[u], fp[u], bb[u]);
-          sh[u] = m.x;
+}
+
+// CTA tiers: per work item the A row (tier 2: a chunk of it) lands by TMA
+// while the first pass's pick metadata loads; every pick is served from
+// shared memory.  Tier t's items live at [t * icap, t * icap + tcnt[t]).
+template <int TIER>
+__global__ void __launch_bounds__(DdTier<TIER>::kThreads) k_dd_serve(DdArgs A) {
+  constexpr bool CTA = !DdTier<TIER>::kWarp;
+  extern __shared__ __align__(128) int32_t sbuf[];
+  if constexpr (!CTA) {
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    dd_serve_warp(A, sbuf + w * (A.chunk + 8), A.chunk + 8,
+                  sbuf + nw * (A.chunk + 8) + w * kGrpInts);
+    return;
+  } else {
+    __shared__ __align__(8) uint64_t bar;
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    if (tid == 0) mbar_init(&bar, 1);
+    __syncthreads();
+    uint32_t phase = 0;
+    const int chunk = A.chunk, s = A.s;
+    const int64_t it1 = TIER * A.icap + (int64_t)A.tcnt[TIER];
+    const int64_t step = gridDim.x;
+    int64_t it = TIER * A.icap + blockIdx.x;
+    DdItem cur;
+    if (it < it1) cur = A.items[it];
+    for (; it < it1; it += step) {
+      DdItem nxt;
+      if (it + step < it1) nxt = A.items[it + step];
+      const int64_t a0 = cur.a0;
+      const int32_t d = cur.d, nrows = cur.nrows;
+      const int32_t q0 = cur.q0;
+      const int32_t take = min(d, s);  // < d: CTA-tier rows are longer than any fanout
+      const int npairs = nrows * take;
+      for (int32_t c0 = 0; c0 < d; c0 += chunk) {
+        const int32_t c1 = min(c0 + chunk, d);
+        const int64_t al0 = (a0 + c0) & ~3LL;
+        if (tid == 0) {
+          const uint32_t bytes = 4u * (uint32_t)dd_row_len(a0 + c0, c1 - c0);
+          fence_async_smem();
+          mbar_expect_tx(&bar, bytes);
+          tma_row(sbuf, A.col + al0, bytes, &bar);
         }
+        // first pass's pick metadata while the row lands
+        int p = tid;
+        int32_t idx = 0, fp = 0, bb = 0;
+        if (p < npairs) {
+          const int i = p / take, t = p - i * take;
+          idx = A.pidx[(uint32_t)(q0 + i) * (uint32_t)s + (uint32_t)t];
+          const int2 fb = dd_fb(A, q0 + i);
+          fp = fb.x + t;
+          bb = fb.y;
+        }
+        mbar_wait(&bar, phase);
+        phase ^= 1u;
+        const int32_t sh = (int32_t)((a0 + c0) - al0 - c0);  // sbuf[idx + sh], idx in [c0, c1)
+        while (p < npairs) {
+          const int pn = p + nthr;
+          int32_t idx2 = 0, fp2 = 0, bb2 = 0;
+          if (pn < npairs) {
+            const int i = pn / take, t = pn - i * take;
+            idx2 = A.pidx[(uint32_t)(q0 + i) * (uint32_t)s + (uint32_t)t];
+            const int2 fb = dd_fb(A, q0 + i);
+            fp2 = fb.x + t;
+            bb2 = fb.y;
+          }
+          if (idx >= c0 && idx < c1) dd_put(A, fp, bb, sbuf[idx + sh]);
+          p = pn; idx = idx2; fp = fp2; bb = bb2;
+        }
+        __syncthreads();  // buffer free for the next chunk / item
       }
-#pragma unroll
-      for (int u = 0; u < kServeUnroll; ++u)
-        if (idx[u] >= lo && idx[u] < hi) dd_put(A, fp[u], bb[u], S.buf[sh[u] + idx[u]]);
+      cur = nxt;
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[sl]);
   }
 }
 
@@ -1439,7 +1449,7 @@ static SageWs sage_ws_layout(char* base, int64_t k, int64_t n, int64_t r_cap_max
   w.ticket = (unsigned int*)take(sizeof(unsigned int) * 8);
   // items <= groups + rows / rows_item(min) <= 2 * rows, per tier region
   w.icap = 2 * r_cap_max + 2;
-  w.items = (DdItem*)take(sizeof(DdItem) * 2 * w.icap);
+  w.items = (DdItem*)take(sizeof(DdItem) * 3 * w.icap);
   w.rrec = (int4*)take(sizeof(int4) * (r_cap_max + 1));
   w.bytes = off;
   return w;
@@ -1463,20 +1473,36 @@ constexpr int kMaxDevices = 16;
 struct ServeCfg {
   bool init = false;
   int pick_grid[5] = {0, 0, 0, 0, 0};
-  int serve_grid = 0;
-  size_t serve_smem = 0;
+  int grid[3] = {0, 0, 0};
+  int chunk[3] = {0, 0, 0};
+  size_t smem[3] = {0, 0, 0};
 };
 static ServeCfg g_serve[kMaxDevices];
+
+template <int T>
+static void serve_tier_setup(ServeCfg& c, int max_smem) {
+  using Tr = DdTier<T>;
+  // tier 0: a 4 KB row buffer (+ group table) per warp; tier 1: the whole
+  // row; tier 2: all of shared memory (chunks) but the static mbarrier
+  c.chunk[T] = T == 2 ? (((max_smem - 256) / 4 - 8) & ~3) : Tr::kHi;
+  c.smem[T] = sizeof(int32_t) * (c.chunk[T] + 8 + (Tr::kWarp ? kGrpInts : 0)) *
+              (Tr::kWarp ? Tr::kThreads / 32 : 1);
+  cudaFuncSetAttribute(k_dd_serve<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)c.smem[T]);
+  c.grid[T] = persistent_grid(k_dd_serve<T>, Tr::kThreads, c.smem[T]);
+}
 
 static ServeCfg& serve_cfg() {
   int dev = 0;
   cudaGetDevice(&dev);
   ServeCfg& c = g_serve[dev < kMaxDevices ? dev : 0];
   if (!c.init) {
-    c.serve_smem = kStages * sizeof(SvStage);
-    cudaFuncSetAttribute(k_dd_serve, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)c.serve_smem);
-    c.serve_grid = persistent_grid(k_dd_serve, kSvThreads, c.serve_smem);
+    int max_smem = 0;
+    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (max_smem <= 0) max_smem = 227 * 1024;
+    serve_tier_setup<0>(c, max_smem);
+    serve_tier_setup<1>(c, max_smem);
+    serve_tier_setup<2>(c, max_smem);
     c.pick_grid[0] = persistent_grid(k_dd_pick<5>, kPickThreads);
     c.pick_grid[1] = persistent_grid(k_dd_pick<8>, kPickThreads);
     c.pick_grid[2] = persistent_grid(k_dd_pick<10>, kPickThreads);
@@ -1511,7 +1537,7 @@ static int dedup_layer(const Graph* g, SageWs& ws, const int64_t* R_ptr, const i
   const SageTabs T{g->deg_slot, g->run_j0, g->run_sd, g->run_n, g->run_lower};
   const int b = fan_bucket(s);
   const int pg = c.pick_grid[b];
-  const unsigned long long* grows = ws.cnts + 3;
+  const unsigned long long* grows = ws.cnts + 4;
   prof_mark(st);
   switch (b) {
     case 0: k_dd_pick<5><<<pg, kPickThreads, 0, st>>>(grows, ws.rrec, T, s, batch_offset, stride, seed, epoch, depth, ws.pidx); break;
@@ -1535,10 +1561,21 @@ static int dedup_layer(const Graph* g, SageWs& ws, const int64_t* R_ptr, const i
   A.nwords = nwords8;
   A.ticket = ws.ticket;
   prof_mark(st);
-  k_dd_serve<<<c.serve_grid, kSvThreads, c.serve_smem, st>>>(A);
-  GB_LAUNCH_CHECK("k_dd_serve");
+  // the tiers touch disjoint frontier entries (and commutative bitmap ORs):
+  // run them concurrently so each tier's tail overlaps the others
+  fork_begin(st, 2);
+  A.chunk = c.chunk[0];
+  k_dd_serve<0><<<c.grid[0], DdTier<0>::kThreads, c.smem[0], st>>>(A);
+  GB_LAUNCH_CHECK("k_dd_serve<0>");
+  A.chunk = c.chunk[1];
+  k_dd_serve<1><<<c.grid[1], DdTier<1>::kThreads, c.smem[1], fork_stream(0)>>>(A);
+  GB_LAUNCH_CHECK("k_dd_serve<1>");
+  A.chunk = c.chunk[2];
+  k_dd_serve<2><<<c.grid[2], DdTier<2>::kThreads, c.smem[2], fork_stream(1)>>>(A);
+  GB_LAUNCH_CHECK("k_dd_serve<2>");
+  fork_join(st, 2);
   prof_mark(st);
-  count_launches(4);  // items, rows, pick, serve
+  count_launches(6);  // items, rows, pick, serve x3
   return GB_OK;
 }
 
