@@ -198,12 +198,14 @@ __device__ __forceinline__ int32_t vrank(const uint32_t* vbits, const int32_t* v
   return vpre[v >> 5] + __popc(vbits[v >> 5] & ((1u << (v & 31)) - 1u));
 }
 
-// (batch, vertex) bitmap of the bulk: each 32-B sector holds 7 bit words
-// (224 vertices) and, after the extraction scan, their batch-row prefix in
-// word 7 — a rank is one sector load.  Word of vertex v in a batch row:
+// (batch, vertex) bitmap of the bulk: one 16-B record per 96 vertices —
+// three bit words and, after the extraction scan, the number of set bits
+// before the record in its batch row — so the block-diagonal rank of a
+// picked vertex is one 16-B load and at most three popcounts.  uint32 index
+// of vertex v's bit word inside its batch row:
 __device__ __forceinline__ uint32_t pk_word(int32_t v) {
-  const uint32_t w = (uint32_t)v >> 5;
-  return w + w / 7u;
+  const uint32_t w = (uint32_t)v >> 5, r = w / 3u;
+  return (r << 2) + (w - 3u * r);
 }
 
 constexpr int kPickThreads = 128;
@@ -851,9 +853,9 @@ struct DdArgs {
 __device__ __forceinline__ void dd_pair(const DdArgs& A, int32_t q, int32_t t, int32_t take,
                                         bool all, int32_t& idx, int32_t& fp, int32_t& bb) {
   idx = all ? t : A.pidx[(uint32_t)q * (uint32_t)A.s + (uint32_t)t];
-  const int4 rec = A.rrec[q];
-  fp = rec.z + t;
-  bb = rec.w;
+  const int2 fb = reinterpret_cast<const int2*>(A.rrec)[2 * (uint32_t)q + 1];
+  fp = fb.x + t;
+  bb = fb.y;
 }
 
 __device__ __forceinline__ void dd_put(const DdArgs& A, int32_t fp, int32_t bb, int32_t cv) {
@@ -1138,22 +1140,6 @@ __global__ void k_sage_layer_meta(const int64_t* __restrict__ brow, int64_t k,
   }
 }
 
-// coloff and sizes only (eoff already written on the sampling stream)
-__global__ void k_sage_layer_cols(const int64_t* __restrict__ brow, int64_t k,
-                                  const int64_t* __restrict__ fptr,
-                                  const int32_t* __restrict__ wpre, int64_t nwords,
-                                  int64_t* __restrict__ coloff, int64_t* __restrict__ sizes) {
-  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b <= k;
-       b += (int64_t)gridDim.x * blockDim.x) {
-    coloff[b] = wpre[b * nwords];
-    if (b == k) {
-      sizes[0] = brow[k];
-      sizes[1] = fptr[brow[k]];
-      sizes[2] = wpre[k * nwords];
-    }
-  }
-}
-
 // acol[e] = block-diagonal column of frontier entry e:
 //   coloff[batch] + rank of fcol[e] among the batch's sorted unique columns
 // (compact_columns sparse.py:352-357 + block_diag sparse.py:321-342)
@@ -1205,49 +1191,95 @@ __global__ void k_sage_rank(const int64_t* __restrict__ F_ptr, const int64_t* __
   }
 }
 
-// Sector-granular extraction (the bulk path, pk_word layout): the scan
-// runs over sectors and writes each sector's prefix into its word 7, so a
-// rank and an enumeration step are one 32-B sector load each.
-struct SecPopF {
-  const uint4* sec;  // 2 uint4 per sector
-  __device__ int64_t operator()(int64_t i) const {
-    const uint4 a = sec[2 * i], b = sec[2 * i + 1];
-    return __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w) + __popc(b.x) + __popc(b.y) +
-           __popc(b.z);
+// Record extraction (the bulk path, pk_word layout).  Per batch row one CTA
+// scans its records (no cross-row look-back: rows are independent), writing
+// each record's within-row prefix into its fourth word and the row total;
+// the column offsets are the scan of the row totals.
+constexpr int kRecScanThreads = 1024;
+constexpr int kRecScanU = 4;
+__global__ void __launch_bounds__(kRecScanThreads) k_rec_scan(uint4* __restrict__ rec,
+                                                            int64_t NR,
+                                                            int64_t* __restrict__ tot) {
+  __shared__ int64_t sw[33];
+  uint4* r = rec + (int64_t)blockIdx.x * NR;
+  uint32_t* r32 = reinterpret_cast<uint32_t*>(r);
+  int64_t base = 0;
+  for (int64_t i0 = 0; i0 < NR; i0 += (int64_t)kRecScanThreads * kRecScanU) {
+    int c[kRecScanU];
+    int tsum = 0;
+#pragma unroll
+    for (int u = 0; u < kRecScanU; ++u) {
+      const int64_t i = i0 + (int64_t)threadIdx.x * kRecScanU + u;
+      c[u] = 0;
+      if (i < NR) {
+        const uint4 x = r[i];
+        c[u] = __popc(x.x) + __popc(x.y) + __popc(x.z);
+      }
+      tsum += c[u];
+    }
+    int64_t total;
+    int64_t run = base + block_excl_scan<int64_t>(tsum, sw, total);
+#pragma unroll
+    for (int u = 0; u < kRecScanU; ++u) {
+      const int64_t i = i0 + (int64_t)threadIdx.x * kRecScanU + u;
+      if (i < NR) r32[4 * i + 3] = (uint32_t)run;
+      run += c[u];
+    }
+    base += total;
   }
-};
-
-// (1 << bits) - 1, all ones for bits >= 32 (one BMSK)
-__device__ __forceinline__ uint32_t low_mask(int32_t bits) {
-  uint32_t m;
-  asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(m) : "r"(bits));
-  return m;
+  if (threadIdx.x == 0) tot[blockIdx.x] = base;
 }
 
-// acol[e] = sector prefix + rank inside the sector (same contract as
-// k_sage_rank; compact_columns sparse.py:352-357 + block_diag :321-342)
-__global__ void k_sage_rank8(const int64_t* __restrict__ F_ptr, const int64_t* __restrict__ eoff,
-                             int64_t k, const int32_t* __restrict__ fcol,
-                             const uint4* __restrict__ sec, int64_t nsec,
-                             int32_t* __restrict__ acol) {
-  constexpr int U = 4;
-  __shared__ int32_t s_eoff[kBrowSmem];
+// coloff[b] = sum of the row totals before b; sizes = (R, F, U).  One CTA.
+__global__ void k_layer_cols(const int64_t* __restrict__ brow, int64_t k,
+                             const int64_t* __restrict__ fptr, const int64_t* __restrict__ tot,
+                             int64_t* __restrict__ coloff, int64_t* __restrict__ sizes) {
+  __shared__ int64_t sw[33];
+  int64_t base = 0;
+  for (int64_t b0 = 0; b0 < k; b0 += blockDim.x) {
+    const int64_t b = b0 + threadIdx.x;
+    int64_t total;
+    const int64_t ex = block_excl_scan<int64_t>(b < k ? tot[b] : 0, sw, total);
+    if (b < k) coloff[b] = base + ex;
+    base += total;
+  }
+  if (threadIdx.x == 0) {
+    coloff[k] = base;
+    sizes[0] = brow[k];
+    sizes[1] = fptr[brow[k]];
+    sizes[2] = base;
+  }
+}
+
+// acol[e] = coloff[batch] + record prefix + rank inside the record
+// (compact_columns sparse.py:352-357 + block_diag :321-342); U entries per
+// thread, their record loads issued together
+__global__ void k_sage_rank128(const int64_t* __restrict__ F_ptr, const int64_t* __restrict__ eoff,
+                               const int64_t* __restrict__ coloff, int64_t k,
+                               const int32_t* __restrict__ fcol, const uint4* __restrict__ rec,
+                               int64_t NR, int32_t* __restrict__ acol) {
+  constexpr int U = 8;
+  __shared__ int32_t s_eoff[kBrowSmem], s_col[kBrowSmem];
   const bool sm = k + 1 <= kBrowSmem;
   if (sm)
-    for (int i = threadIdx.x; i <= k; i += blockDim.x) s_eoff[i] = (int32_t)eoff[i];
+    for (int i = threadIdx.x; i <= k; i += blockDim.x) {
+      s_eoff[i] = (int32_t)eoff[i];
+      s_col[i] = (int32_t)coloff[i];
+    }
   __syncthreads();
   const int32_t F = (int32_t)*F_ptr;
-  const int32_t K = (int32_t)k, NS = (int32_t)nsec;
+  const int32_t K = (int32_t)k, nr = (int32_t)NR;
   auto eo = [&](int32_t i) { return sm ? s_eoff[i] : (int32_t)eoff[i]; };
   for (int32_t e0 = blockIdx.x * blockDim.x * U + threadIdx.x; e0 < F;
        e0 += gridDim.x * blockDim.x * U) {
-    int32_t v[U], si[U], wi[U];
+    int32_t v[U], bt[U];
+    uint4 x[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int32_t e = e0 + u * (int32_t)blockDim.x;
       v[u] = e < F ? fcol[e] : 0;
     }
-    int32_t a = 0, b = K;
+    int32_t a = 0, b = K;  // last batch with eoff <= e0
     while (b - a > 1) {
       const int32_t mid = (a + b) >> 1;
       if (eo(mid) <= e0) a = mid; else b = mid;
@@ -1256,50 +1288,46 @@ __global__ void k_sage_rank8(const int64_t* __restrict__ F_ptr, const int64_t* _
     for (int u = 0; u < U; ++u) {
       const int32_t e = e0 + u * (int32_t)blockDim.x;
       while (a + 1 < K && eo(a + 1) <= e) ++a;
-      const uint32_t q = ((uint32_t)v[u] >> 5) / 7u;
-      si[u] = a * NS + (int32_t)q;
-      wi[u] = v[u] - 224 * (int32_t)q;  // bit position inside the sector
+      bt[u] = a;
+      if (e < F) x[u] = rec[a * nr + (int32_t)(((uint32_t)v[u] >> 5) / 3u)];
     }
-    uint4 lo[U], hi[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (e0 + u * (int32_t)blockDim.x < F) { lo[u] = sec[2 * si[u]]; hi[u] = sec[2 * si[u] + 1]; }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int32_t e = e0 + u * (int32_t)blockDim.x;
       if (e < F) {
-        const uint32_t x[7] = {lo[u].x, lo[u].y, lo[u].z, lo[u].w, hi[u].x, hi[u].y, hi[u].z};
-        int32_t r = (int32_t)hi[u].w;
-#pragma unroll
-        for (int j = 0; j < 7; ++j) r += __popc(x[j] & low_mask(max(wi[u] - 32 * j, 0)));
-        acol[e] = r;
+        const uint32_t w = (uint32_t)v[u] >> 5, j = w - 3u * (w / 3u);
+        const uint32_t m = (1u << (v[u] & 31)) - 1u;
+        const uint32_t wj = j == 0 ? x[u].x : j == 1 ? x[u].y : x[u].z;
+        const int32_t below = (j > 0 ? __popc(x[u].x) : 0) + (j > 1 ? __popc(x[u].y) : 0);
+        acol[e] = (sm ? s_col[bt[u]] : (int32_t)coloff[bt[u]]) + (int32_t)x[u].w + below +
+                  __popc(wj & m);
       }
     }
   }
 }
 
-// col_vertices from the sector bitmap, thread per sector; clears the bits
-// (word 7 is rewritten by the next scan)
-__global__ void k_sage_enumerate8(int64_t NSt, int64_t nsec, uint4* __restrict__ sec,
-                                  int32_t* __restrict__ colv) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < NSt;
+// col_vertices from the records, thread per record; clears the bits (the
+// prefix word is rewritten by the next scan)
+__global__ void k_sage_enumerate128(int64_t NRt, int64_t NR, uint4* __restrict__ rec,
+                                    const int64_t* __restrict__ coloff,
+                                    int32_t* __restrict__ colv) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < NRt;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const uint4 a = sec[2 * i], b = sec[2 * i + 1];
-    if (!(a.x | a.y | a.z | a.w | b.x | b.y | b.z)) continue;
-    const int64_t bt = i / nsec;
-    const int32_t vb = (int32_t)((i - bt * nsec) * 224);
-    const uint32_t w[7] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z};
-    int32_t o = (int32_t)b.w;
+    const uint4 r = rec[i];
+    if (!(r.x | r.y | r.z)) continue;
+    const int64_t bt = i / NR;
+    const int32_t vb = (int32_t)((i - bt * NR) * 96);
+    int32_t o = (int32_t)(coloff[bt] + r.w);
+    const uint32_t w[3] = {r.x, r.y, r.z};
 #pragma unroll
-    for (int j = 0; j < 7; ++j) {
+    for (int j = 0; j < 3; ++j) {
       uint32_t x = w[j];
       while (x) {
         colv[o++] = vb + 32 * j + __ffs(x) - 1;
         x &= x - 1;
       }
     }
-    sec[2 * i] = make_uint4(0, 0, 0, 0);
-    sec[2 * i + 1] = make_uint4(0, 0, 0, 0);
+    rec[i] = make_uint4(0u, 0u, 0u, r.w);
   }
 }
 
@@ -1409,6 +1437,8 @@ struct SageWs {
   uint32_t* bitmap2;  // layer l's extraction overlaps layer l + 1's sampling
   int64_t* scan_ws2;  // scans of the extraction stream
   int64_t* d_W;
+  int64_t* clean;    // clean mark after a completed bulk (bit words, counters clear)
+  int64_t* btot;     // set bits per batch row (extraction)
   // dedup mode
   int32_t* vcnt;     // [n] rows per vertex (zero between layers)
   int32_t* roff;     // [n] group row range start per vertex
@@ -1418,7 +1448,7 @@ struct SageWs {
   unsigned int* ticket;      // serve kernels' work counters
   int64_t icap;      // work-item capacity per tier
   DdItem* items;     // work-item descriptors
-  int4* rrec;        // per grouped row: (key lo, key hi, frontier offset, batch)
+  int4* rrec;        // per grouped row: (local row, degree, frontier offset, batch)
   size_t bytes;
 };
 
@@ -1428,7 +1458,7 @@ static SageWs sage_ws_layout(char* base, int64_t k, int64_t n, int64_t r_cap_max
                              int64_t f_cap_max) {
   SageWs w{};
   const int64_t nwords = (n + 31) / 32;
-  const int64_t W = k * 8 * ((nwords + 6) / 7);  // pk_word sectors per batch row
+  const int64_t W = k * 4 * ((nwords + 2) / 3);  // pk_word records: 16 B per 96 vertices
   int64_t scan_n = 3 * r_cap_max > W ? 3 * r_cap_max : W;
   if (nwords > scan_n) scan_n = nwords;
   size_t off = 0;
@@ -1441,6 +1471,8 @@ static SageWs sage_ws_layout(char* base, int64_t k, int64_t n, int64_t r_cap_max
   w.bitmap2 = (uint32_t*)take(sizeof(uint32_t) * (W + 8));
   w.scan_ws2 = (int64_t*)take(sizeof(int64_t) * scan_workspace_elems<int64_t>(W + 1));
   w.d_W = (int64_t*)take(sizeof(int64_t));
+  w.clean = (int64_t*)take(sizeof(int64_t));
+  w.btot = (int64_t*)take(sizeof(int64_t) * (k + 1));
   w.vcnt = (int32_t*)take(sizeof(int32_t) * (n + 1));
   w.roff = (int32_t*)take(sizeof(int32_t) * (n + 1));
   w.rslot = (int32_t*)take(sizeof(int32_t) * (r_cap_max + 1));
@@ -1458,6 +1490,25 @@ static SageWs sage_ws_layout(char* base, int64_t k, int64_t n, int64_t r_cap_max
 __global__ void k_sage_eoff(const int64_t* __restrict__ brow, int64_t k,
                             const int64_t* __restrict__ fptr, int64_t* __restrict__ eoff);
 
+constexpr int64_t kWsClean = 0x636c65616e6d6b31LL;
+// the clean mark certifies one layout (bitmap and counter sizes)
+__host__ __device__ __forceinline__ int64_t ws_clean_mark(int64_t nb, int64_t nv) {
+  return kWsClean ^ (nb * 0x9E3779B97F4A7C15LL) ^ (nv << 17);
+}
+__global__ void k_ws_clear(const int64_t* __restrict__ clean, uint32_t* __restrict__ b1,
+                           uint32_t* __restrict__ b2, int64_t nb, int32_t* __restrict__ vcnt,
+                           int64_t nv) {
+  if (*clean == ws_clean_mark(nb, nv)) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nb;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    b1[i] = 0u;
+    b2[i] = 0u;
+  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv;
+       i += (int64_t)gridDim.x * blockDim.x)
+    vcnt[i] = 0;
+}
+
 template <typename K>
 static int persistent_grid(K kernel, int threads, size_t smem = 0) {
   int o = 0, dev = 0, sms = 0;
@@ -1472,7 +1523,6 @@ static int persistent_grid(K kernel, int threads, size_t smem = 0) {
 constexpr int kMaxDevices = 16;
 struct ServeCfg {
   bool init = false;
-  int pick_grid[5] = {0, 0, 0, 0, 0};
   int grid[3] = {0, 0, 0};
   int chunk[3] = {0, 0, 0};
   size_t smem[3] = {0, 0, 0};
@@ -1503,11 +1553,6 @@ static ServeCfg& serve_cfg() {
     serve_tier_setup<0>(c, max_smem);
     serve_tier_setup<1>(c, max_smem);
     serve_tier_setup<2>(c, max_smem);
-    c.pick_grid[0] = persistent_grid(k_dd_pick<5>, kPickThreads);
-    c.pick_grid[1] = persistent_grid(k_dd_pick<8>, kPickThreads);
-    c.pick_grid[2] = persistent_grid(k_dd_pick<10>, kPickThreads);
-    c.pick_grid[3] = persistent_grid(k_dd_pick<16>, kPickThreads);
-    c.pick_grid[4] = persistent_grid(k_dd_pick<32>, kPickThreads);
     c.init = true;
   }
   return c;
@@ -1530,22 +1575,26 @@ static int dedup_layer(const Graph* g, SageWs& ws, const int64_t* R_ptr, const i
       ws.cnts, ws.dv, g->rowptr, ws.vcnt, ws.roff, s, ws.icap, ws.cnts + 1, ws.items, peer);
   GB_LAUNCH_CHECK("k_grp_items");
   k_grp_rows<<<grid_for(r_cap / kGrpU + 1, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, fptr,
-                                                                   brow, k,
-                                                      ws.rslot, ws.roff, ws.rrec);
-  GB_LAUNCH_CHECK("dedup grouping");
+                                                                   brow, k, ws.rslot, ws.roff,
+                                                                   ws.rrec);
+  GB_LAUNCH_CHECK("k_grp_rows");
   const ServeCfg& c = serve_cfg();
   const SageTabs T{g->deg_slot, g->run_j0, g->run_sd, g->run_n, g->run_lower};
   const int b = fan_bucket(s);
-  const int pg = c.pick_grid[b];
+  const int pgrid = grid_for(r_cap, kPickThreads, 64 * kNumSMs);
   const unsigned long long* grows = ws.cnts + 4;
   prof_mark(st);
+#define GB_DD_PICK(MF)                                                                   \
+  k_dd_pick<MF><<<pgrid, kPickThreads, 0, st>>>(grows, ws.rrec, T, s, batch_offset, stride, \
+                                               seed, epoch, depth, ws.pidx)
   switch (b) {
-    case 0: k_dd_pick<5><<<pg, kPickThreads, 0, st>>>(grows, ws.rrec, T, s, batch_offset, stride, seed, epoch, depth, ws.pidx); break;
-    case 1: k_dd_pick<8><<<pg, kPickThreads, 0, st>>>(grows, ws.rrec, T, s, batch_offset, stride, seed, epoch, depth, ws.pidx); break;
-    case 2: k_dd_pick<10><<<pg, kPickThreads, 0, st>>>(grows, ws.rrec, T, s, batch_offset, stride, seed, epoch, depth, ws.pidx); break;
-    case 3: k_dd_pick<16><<<pg, kPickThreads, 0, st>>>(grows, ws.rrec, T, s, batch_offset, stride, seed, epoch, depth, ws.pidx); break;
-    default: k_dd_pick<32><<<pg, kPickThreads, 0, st>>>(grows, ws.rrec, T, s, batch_offset, stride, seed, epoch, depth, ws.pidx); break;
+    case 0: GB_DD_PICK(5); break;
+    case 1: GB_DD_PICK(8); break;
+    case 2: GB_DD_PICK(10); break;
+    case 3: GB_DD_PICK(16); break;
+    default: GB_DD_PICK(32); break;
   }
+#undef GB_DD_PICK
   GB_LAUNCH_CHECK("k_dd_pick");
   prof_mark(st);
   DdArgs A{};
@@ -1629,9 +1678,10 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     peer = PeerRows{peer_host->nblk, peer_host->bounds, peer_host->brp, peer_host->bcol};
   }
   const int64_t nwords = (g->n + 31) / 32;
-  // (batch, vertex) bitmaps in pk_word sectors (7 bit words + prefix word)
-  const int64_t nw8 = 8 * ((nwords + 6) / 7);
-  const int64_t W = k * nw8, NS = W / 8;
+  // (batch, vertex) bitmaps as pk_word records (3 bit words, prefix)
+  const int64_t NR = (nwords + 2) / 3;  // records per batch row
+  const int64_t nw8 = 4 * NR;           // uint32 per batch row
+  const int64_t W = k * nw8, NS = k * NR;
   if (W >= ((int64_t)1 << 31)) {
     set_error("bulk: k * ceil(n / 32) = %lld (batch, vertex) words exceeds int32 indexing",
               (long long)W);
@@ -1657,11 +1707,15 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     }
     r_cap = f_cap;
   }
-  GB_CUDA(cudaMemsetAsync(ws.bitmap, 0, sizeof(uint32_t) * (W + 8), st));
-  GB_CUDA(cudaMemsetAsync(ws.bitmap2, 0, sizeof(uint32_t) * (W + 8), st));
-  if (dedup) GB_CUDA(cudaMemsetAsync(ws.vcnt, 0, sizeof(int32_t) * (g->n + 1), st));
+  // the bit words and vertex counters are left clear by a completed bulk
+  // (enumerate / items clear what they used): zero them only when the
+  // workspace's clean mark is absent (first use, or an aborted bulk)
+  k_ws_clear<<<4 * kNumSMs, 256, 0, st>>>(ws.clean, ws.bitmap, ws.bitmap2, W + 8, ws.vcnt,
+                                         g->n + 1);
+  GB_LAUNCH_CHECK("k_ws_clear");
   k_set_i64<<<1, 1, 0, st>>>(ws.d_W, NS);
-  count_launches(1);
+  k_set_i64<<<1, 1, 0, st>>>(ws.clean, 0);
+  count_launches(3);
   // extraction of layer l (popcount scan, rank, enumerate) runs on a side
   // stream while layer l + 1 samples; layer l + 2 reuses layer l's bitmap
   // only after that extraction (ring events) — graph-capturable
@@ -1735,27 +1789,28 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     k_sage_eoff<<<grid_for(k + 1, 128, 64), 128, 0, st>>>(brow, k, o.fptr, o.eoff);
     GB_LAUNCH_CHECK("k_sage_eoff");
     stream_wait(xs, st);
-    // popcount prefix of each sector into its word 7 (total after the last)
-    int32_t* spre = (int32_t*)bm + 7;
-    rc = device_exclusive_scan<int64_t, 8>(ws.d_W, NS, SecPopF{(const uint4*)bm}, spre,
-                                           ws.scan_ws2, xs);
-    if (rc) return rc;
+    // per batch row: record prefixes and the row total; column offsets
     int64_t* sizes = d_sizes + 3 * l;
-    k_sage_layer_cols<<<grid_for(k + 1, 128, 64), 128, 0, xs>>>(brow, k, o.fptr, spre, nw8,
-                                                                 o.coloff, sizes);
-    GB_LAUNCH_CHECK("k_sage_layer_cols");
+    if (k > 0) {
+      k_rec_scan<<<(unsigned)k, kRecScanThreads, 0, xs>>>((uint4*)bm, NR, ws.btot);
+      GB_LAUNCH_CHECK("k_rec_scan");
+    }
+    k_layer_cols<<<1, 1024, 0, xs>>>(brow, k, o.fptr, ws.btot, o.coloff, sizes);
+    GB_LAUNCH_CHECK("k_layer_cols");
     const int64_t f_cap = r_cap * s;
-    k_sage_rank8<<<grid_for(f_cap, 256, 16 * kNumSMs), 256, 0, xs>>>(
-        sizes + 1, o.eoff, k, o.fcol, (const uint4*)bm, nw8 / 8, o.acol);
-    GB_LAUNCH_CHECK("k_sage_rank8");
-    k_sage_enumerate8<<<grid_for(NS, 256, 16 * kNumSMs), 256, 0, xs>>>(NS, nw8 / 8, (uint4*)bm,
-                                                                       o.colv);
-    GB_LAUNCH_CHECK("k_sage_enumerate8");
+    k_sage_rank128<<<grid_for(f_cap / 8 + 1, 256, 16 * kNumSMs), 256, 0, xs>>>(
+        sizes + 1, o.eoff, o.coloff, k, o.fcol, (const uint4*)bm, NR, o.acol);
+    GB_LAUNCH_CHECK("k_sage_rank128");
+    k_sage_enumerate128<<<grid_for(NS, 256, 16 * kNumSMs), 256, 0, xs>>>(NS, NR, (uint4*)bm,
+                                                                         o.coloff, o.colv);
+    GB_LAUNCH_CHECK("k_sage_enumerate128");
     GB_CUDA(cudaEventRecord(ring_event(l), xs));
     count_launches(5);  // prep/count, eoff, cols, rank, enumerate
     r_cap = f_cap;
   }
   stream_wait(st, xs);
+  k_set_i64<<<1, 1, 0, st>>>(ws.clean, ws_clean_mark(W + 8, g->n + 1));
+  count_launches(1);
   return GB_OK;
 }
 
