@@ -171,13 +171,20 @@ def kernel_bytes(s, kernel):
     if kernel == "stream":
         return 32 * s["R"] + 4 * s["G"] + 8 * s["F"]
     if kernel == "dedup":
-        # k_dd_serve: per distinct row vertex 4 + row_ptr 8 + row-list offset
-        # 8, per frontier row its offset 4 + batch 4, 4 per entry of every
-        # DISTINCT row, pick idx 4 + col write 4 + batch bit 4 per pick
-        return 20 * s["D"] + 8 * s["R"] + 4 * s["G_distinct"] + 12 * s["F"]
+        # k_dd_serve<0,1,2>: a 32-B work-item descriptor per distinct row
+        # (about D items), 4 per entry of every DISTINCT row (the P row formed
+        # on chip once), per pick its index 4 + (frontier offset, batch) 8 +
+        # frontier write 4 + batch bit 4
+        return 32 * s["D"] + 4 * s["G_distinct"] + 20 * s["F"]
     if kernel == "pick":
         return 12 * s["R"] + 4 * s["F"]
     return 24 * s["R"] + 8 * s["F"]
+
+
+def dedup_bytes(st):
+    """Compulsory bytes of the dedup bulk: SURVEY.md §8(d)'s per-layer terms
+    with the gathered entries of the DISTINCT rows only."""
+    return sum(28 * s["R"] + 4 * s["G_distinct"] + 12 * s["F"] + 4 * s["U"] + 8 for s in st)
 
 
 def oracle_prefix(layers, kc):
@@ -474,9 +481,7 @@ def run_ours(args, rank, world, local_rank):
     agg = measure_aggregation(bulk, d_off, d_cat, sizes, st, n, k, peak) \
         if not args.no_aggregation else None
     KERNEL = {"stream": "k_sage_stream", "dedup": "k_dd_serve", "pfree": "k_sage_pick<true>"}
-    # dedup streams layer 1 (its rows, the batch vertices, are all distinct)
-    kb = [kernel_bytes(s_, "stream" if args.mode == "dedup" and li == 0 else args.mode)
-          for li, s_ in enumerate(st)]
+    kb = [kernel_bytes(s_, args.mode) for s_ in st]
     kern_avg = kern_ms.mean(axis=0)[:, -1]  # dominant kernel, per layer
     pick_avg = kern_ms.mean(axis=0)[:, 0]
     achieved = sum(kb) / (kern_avg.sum() / 1e3) / 1e9
@@ -507,14 +512,18 @@ def run_ours(args, rank, world, local_rank):
         "roofline": {
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "traffic": traffic,
-            "traffic_note": "dram__bytes_read+write summed over the 3 layer launches of one bulk "
-                            "(ncu --set full, profiles/ncu_traffic.json); achieved/per_layer_bytes "
-                            "aggregate the same 3 launches",
+            "traffic_note": "dram__bytes_read+write of the dominant kernel's launches of one "
+                            "bulk (ncu, profiles/ncu_traffic.json); achieved/per_layer_bytes "
+                            "aggregate the same launches",
             "kernel": KERNEL[args.mode],
             "pick_kernel_ms": [round(x, 4) for x in pick_avg.tolist()],
             "per_layer_ms": [round(x, 4) for x in kern_avg.tolist()],
             "per_layer_bytes": kb, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)",
             "kernel_share_of_step": float(kern_avg.sum() / (total_ms / args.steps)),
+            # the whole step against the bytes Alg. 1 with duplicate-row
+            # elimination must move (28R + 4G_distinct + 12F + 4U + 8)
+            "step_bytes_dedup": dedup_bytes(st),
+            "step_frac_dedup": dedup_bytes(st) / (total_ms / args.steps / 1e3) / 1e9 / peak,
         },
     }
     # the other SAGE kernel modes on the same workload (identical outputs)
@@ -563,12 +572,19 @@ def run_ours(args, rank, world, local_rank):
     # the epoch loop: sample_stream overlaps bulk j's device->host copy with
     # bulk j + 1's sampling (every bulk still uploads its batches and reads
     # back all its arrays)
+    def consume(ep):
+        # the reference's output types, as a trainer reads them
+        # (LayerSample fields, sampler.py:240-261): zero-copy views here
+        for layer in ep.layers:
+            layer.frontier, layer.adjacency
+            layer.row_vertices, layer.col_vertices, layer.sampled_vertices
+
     for ep in bs.sample_stream([(batches, boff)] * 2):
-        pass
+        consume(ep)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for ep in bs.sample_stream([(batches, boff)] * nst):
-        pass
+        consume(ep)
     e2e_s = (time.perf_counter() - t0) / nst
     if world > 1:
         t = torch.tensor([e2e_s, e2e_sync], device=dev, dtype=torch.float64)
@@ -576,8 +592,9 @@ def run_ours(args, rank, world, local_rank):
         e2e_s, e2e_sync = (float(x) for x in t.tolist())
     line["e2e"] = {"value": world * k / e2e_s, "unit": UNIT, "h2d_bytes_per_step": bs.h2d_bytes,
                    "d2h_bytes_per_step": bs.d2h_bytes,
-                   "api": "paper_2311_02909_b200.engine.BulkSampler.sample_stream (host batches "
-                          "-> host SampledEpoch arrays, copy of bulk j overlapping bulk j+1)",
+                   "api": "paper_2311_02909_b200.BulkSampler.sample_stream (host batches -> "
+                          "host SampledEpoch with every LayerSample field read as the reference "
+                          "types; copy of bulk j overlapping bulk j+1)",
                    "sync_call": {"value": world * k / e2e_sync, "unit": UNIT,
                                  "api": "BulkSampler.sample, one blocking call per bulk"}}
     # CPU baseline (oracle port) on rank 0 at N=1, with a full-size parity check
@@ -600,14 +617,21 @@ def run_15d(args, rank, world, local_rank):
 
     from paper_2311_02909_b200 import graphgen
     from paper_2311_02909_b200.dist import ProcessGrid
-    from paper_2311_02909_b200.dist_exec import Sage15D
+    from paper_2311_02909_b200.dist_exec import BlockGraph, Sage15D
 
     c = args.c if (world % args.c == 0 and args.c ** 2 <= world and
                    world % (args.c ** 2) == 0) else 1
     grid = ProcessGrid(world, c)
     torch.cuda.set_device(local_rank)
     n, m, sym = graphgen.SHAPES[args.workload]
-    dg = graphgen.rmat_device_graph(n, m, symmetric=sym, seed=0)
+    # only this rank's block row is built and kept (gb_rmat_block); the
+    # global degrees are all-gathered (partition_block_rows, dist.py:200-214)
+    t0 = time.perf_counter()
+    dg = BlockGraph.rmat(n, m, sym, grid, seed=0)
+    t_part = time.perf_counter() - t0
+    torch.cuda.empty_cache()
+    resident = dg.resident_bytes()
+    full_bytes = 8 * (n + 1) + 4 * (2 * m if sym else m)
     k = args.k or default_k(args.workload)
     allb = make_batches_for(n, k * grid.rows)
     # the grid samples row by row at the owner: stream or P-free kernels
@@ -710,6 +734,12 @@ def run_15d(args, rank, world, local_rank):
                                    f"b=1024, k={k} per grid row",
                        "parallelism": f"1.5D grid {grid.rows}x{grid.c} (p={world}, c={grid.c})",
                        "mode": m15, "fetch": args.fetch},
+            "graph_per_rank": {"resident_bytes_rank0": resident,
+                               "replicated_graph_bytes": full_bytes,
+                               "fraction": resident / full_bytes,
+                               "build_s": t_part,
+                               "how": "BlockGraph.rmat: block row only (gb_rmat_block) + "
+                                      "all-gathered global degrees"},
             "traffic_rank0": {k2: int(v) for k2, v in s.stats.items()},
             "feature_fetch_rank0_group": fetch_line,
         })

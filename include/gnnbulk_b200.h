@@ -93,6 +93,11 @@ typedef struct {
   int64_t f_cap;
 } gb_sage_layer_out;
 
+/* Workspace contract: d_ws is zero-filled before its first bulk and not
+ * modified by the caller between bulks — a completed bulk leaves its bit
+ * maps and vertex counters clear (and marks the workspace so), so the next
+ * bulk on it skips clearing them.  A workspace the caller reused for other
+ * data must be zero-filled again. */
 int gb_sage_bulk_workspace(const gb_graph* g, int64_t k, int64_t r1_cap, int32_t layers,
                            const int64_t* h_fanouts, size_t* h_bytes);
 int gb_sage_bulk(const gb_graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d_bverts,
@@ -154,6 +159,11 @@ int gb_gather_features(int64_t m, const int32_t* d_ids, int64_t row0, const floa
  *   gb_first_occurrence first[j] = smallest entry e with column index j
  *                       (col[e] + shift[b(e)], batch offsets d_entry_batch),
  *                       or e itself when d_colidx is NULL; unset = INT32_MAX */
+/* gb_spmm_f64 — forward_aggregate (pipeline.py:123-130): Y = A X in float64
+ * with A's values (any, not only 0/1), the reference's scipy csr_matvecs
+ * order (per row, entries in order, product then sum): bit-identical. */
+int gb_spmm_f64(int64_t R, const int64_t* d_rowptr, const int32_t* d_col, const double* d_val,
+                const double* d_X, int64_t f, double* d_Y, void* stream);
 int gb_spmm_rows(int64_t R, const int64_t* d_rowptr, const int32_t* d_col,
                  const int64_t* d_row_batch, const int64_t* d_shift, int64_t k, const float* d_X,
                  int64_t f, float* d_Y, void* stream);

@@ -106,6 +106,7 @@ SIGNATURES = {
     "gb_rmat_edges": (ctypes.c_int, [_u64, _i32, _i64, _i64, _i64, ctypes.c_double,
                                      ctypes.c_double, ctypes.c_double, _p, _p, _p]),
     "gb_hash64": (ctypes.c_int, [_u64, _p, _i64, _p, _p]),
+    "gb_spmm_f64": (ctypes.c_int, [_i64, _p, _p, _p, _p, _i64, _p, _p]),
     "gb_csr_from_edges_workspace": (ctypes.c_size_t, [_i64, _i64]),
     "gb_csr_from_edges": (ctypes.c_int, [_i64, _i64, _p, _p, _p, _p, ctypes.POINTER(_i64), _p,
                                          ctypes.c_size_t, _p]),

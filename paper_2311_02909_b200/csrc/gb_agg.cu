@@ -104,6 +104,39 @@ int spmm_rows(int64_t R, const int64_t* rowptr, const int32_t* col, const int64_
   return GB_OK;
 }
 
+// forward_aggregate (pipeline.py:123-130) = scipy `A.to_scipy() @ H` in
+// float64 with A's values: warp per row, lanes over the feature columns,
+// y[c] = y[c] + v_e * X[col_e, c] over the row's entries in order, the
+// product and the sum rounded separately — scipy's csr_matvecs loop, so the
+// result is bit-identical to the reference's.
+__global__ void __launch_bounds__(256) k_spmm_f64(int64_t R, const int64_t* __restrict__ rowptr,
+                                                const int32_t* __restrict__ col,
+                                                const double* __restrict__ val,
+                                                const double* __restrict__ X, int64_t f,
+                                                double* __restrict__ Y) {
+  const int lane = lane_id();
+  for (int64_t r = global_warp(); r < R; r += grid_warps()) {
+    const int64_t e0 = rowptr[r], e1 = rowptr[r + 1];
+    for (int64_t c0 = 0; c0 < f; c0 += 32) {
+      const int64_t c = c0 + lane;
+      double y = 0.0;
+      if (c < f)
+        for (int64_t e = e0; e < e1; ++e)
+          y = __dadd_rn(y, __dmul_rn(__ldg(val + e), __ldg(X + (int64_t)__ldg(col + e) * f + c)));
+      if (c < f) Y[r * f + c] = y;
+    }
+  }
+}
+
+int spmm_f64(int64_t R, const int64_t* rowptr, const int32_t* col, const double* val,
+             const double* X, int64_t f, double* Y, cudaStream_t st) {
+  if (R == 0 || f == 0) return GB_OK;
+  k_spmm_f64<<<agg_grid(R * 32, 256), 256, 0, st>>>(R, rowptr, col, val, X, f, Y);
+  GB_LAUNCH_CHECK("k_spmm_f64");
+  count_launches(1);
+  return GB_OK;
+}
+
 int first_occurrence(int64_t F, const int32_t* colidx, const int64_t* eb, const int64_t* shift,
                      int64_t k, int64_t ncols, int32_t* first, cudaStream_t st) {
   GB_CUDA(cudaMemsetAsync(first, 0x7f, sizeof(int32_t) * (ncols > 0 ? ncols : 1), st));

@@ -321,6 +321,15 @@ int gb_spmm_rows(int64_t R, const int64_t* d_rowptr, const int32_t* d_col,
   return spmm_rows(R, d_rowptr, d_col, d_row_batch, d_shift, k, d_X, f, d_Y, (cudaStream_t)stream);
 }
 
+int gb_spmm_f64(int64_t R, const int64_t* d_rowptr, const int32_t* d_col, const double* d_val,
+                const double* d_X, int64_t f, double* d_Y, void* stream) {
+  if (R < 0 || f < 0 || (R > 0 && (!d_rowptr || !d_Y))) {
+    set_error("spmm_f64: bad arguments");
+    return GB_ERR_CONTRACT;
+  }
+  return spmm_f64(R, d_rowptr, d_col, d_val, d_X, f, d_Y, (cudaStream_t)stream);
+}
+
 size_t gb_sage_owner_p2p_workspace(int64_t r_cap) { return sage_owner_p2p_ws(r_cap); }
 
 int gb_sage_owner_p2p(const gb_graph* tables, int64_t ngroups, const int32_t* const* h_rows,

@@ -53,6 +53,8 @@ int csr_from_keys(uint64_t* keys, int64_t m, uint64_t end, int sb, int64_t n, in
 int spmm_rows(int64_t R, const int64_t* rowptr, const int32_t* col, const int64_t* rowb,
               const int64_t* shift, int64_t k, const float* X, int64_t f, float* Y,
               cudaStream_t st);
+int spmm_f64(int64_t R, const int64_t* rowptr, const int32_t* col, const double* val,
+             const double* X, int64_t f, double* Y, cudaStream_t st);
 int segment_copy(int64_t m, const int64_t* rows, const int64_t* src_off, const int32_t* lens,
                  const int32_t* src, const int64_t* dst_off, int32_t* dst, cudaStream_t st);
 size_t sage_owner_p2p_ws(int64_t r_cap);

@@ -1195,39 +1195,53 @@ __global__ void k_sage_rank(const int64_t* __restrict__ F_ptr, const int64_t* __
 // scans its records (no cross-row look-back: rows are independent), writing
 // each record's within-row prefix into its fourth word and the row total;
 // the column offsets are the scan of the row totals.
-constexpr int kRecScanThreads = 1024;
-constexpr int kRecScanU = 4;
-__global__ void __launch_bounds__(kRecScanThreads) k_rec_scan(uint4* __restrict__ rec,
-                                                            int64_t NR,
-                                                            int64_t* __restrict__ tot) {
+constexpr int kRsThreads = 256, kRsU = 8, kRsTile = kRsThreads * kRsU;
+// tiles of kRsTile records never straddle a batch row: tile t is segment
+// t % tpr of row t / tpr, and its look-back stops at the row's first tile,
+// so the 64 rows' chains advance concurrently (st zeroed before the launch)
+__global__ void __launch_bounds__(kRsThreads) k_rec_scan(uint4* __restrict__ rec, int64_t NR,
+                                                       int64_t k, int64_t* __restrict__ tot,
+                                                       unsigned long long* __restrict__ st) {
   __shared__ int64_t sw[33];
-  uint4* r = rec + (int64_t)blockIdx.x * NR;
-  uint32_t* r32 = reinterpret_cast<uint32_t*>(r);
-  int64_t base = 0;
-  for (int64_t i0 = 0; i0 < NR; i0 += (int64_t)kRecScanThreads * kRecScanU) {
-    int c[kRecScanU];
+  __shared__ int64_t s_tile, s_prefix;
+  const int64_t tpr = (NR + kRsTile - 1) / kRsTile;
+  const int64_t ntiles = tpr * k;
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = (int64_t)atomicAdd(st, 1ull);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    if (tile >= ntiles) return;
+    const int64_t row = tile / tpr, seg = tile - row * tpr;
+    uint4* r = rec + row * NR;
+    uint32_t* r32 = reinterpret_cast<uint32_t*>(r);
+    const int64_t i0 = seg * kRsTile + (int64_t)threadIdx.x * kRsU;
+    int c[kRsU];
     int tsum = 0;
 #pragma unroll
-    for (int u = 0; u < kRecScanU; ++u) {
-      const int64_t i = i0 + (int64_t)threadIdx.x * kRecScanU + u;
+    for (int u = 0; u < kRsU; ++u) {
       c[u] = 0;
-      if (i < NR) {
-        const uint4 x = r[i];
+      if (i0 + u < NR) {
+        const uint4 x = r[i0 + u];
         c[u] = __popc(x.x) + __popc(x.y) + __popc(x.z);
       }
       tsum += c[u];
     }
     int64_t total;
-    int64_t run = base + block_excl_scan<int64_t>(tsum, sw, total);
+    int64_t run = block_excl_scan<int64_t>(tsum, sw, total);
+    if (threadIdx.x < 32) {
+      const int64_t pre = tile_lookback(st, tile, row * tpr, total);
+      if (threadIdx.x == 0) s_prefix = pre;
+    }
+    __syncthreads();
+    run += s_prefix;
 #pragma unroll
-    for (int u = 0; u < kRecScanU; ++u) {
-      const int64_t i = i0 + (int64_t)threadIdx.x * kRecScanU + u;
-      if (i < NR) r32[4 * i + 3] = (uint32_t)run;
+    for (int u = 0; u < kRsU; ++u) {
+      if (i0 + u < NR) r32[4 * (i0 + u) + 3] = (uint32_t)run;
       run += c[u];
     }
-    base += total;
+    if (seg == tpr - 1 && threadIdx.x == 0) tot[row] = s_prefix + total;
+    __syncthreads();
   }
-  if (threadIdx.x == 0) tot[blockIdx.x] = base;
 }
 
 // coloff[b] = sum of the row totals before b; sizes = (R, F, U).  One CTA.
@@ -1469,7 +1483,10 @@ static SageWs sage_ws_layout(char* base, int64_t k, int64_t n, int64_t r_cap_max
   w.scan_ws = (int64_t*)take(sizeof(int64_t) * scan_workspace_elems<int64_t>(scan_n + 1));
   w.bitmap = (uint32_t*)take(sizeof(uint32_t) * (W + 8));
   w.bitmap2 = (uint32_t*)take(sizeof(uint32_t) * (W + 8));
-  w.scan_ws2 = (int64_t*)take(sizeof(int64_t) * scan_workspace_elems<int64_t>(W + 1));
+  const int64_t NRr = (nwords + 2) / 3;  // bitmap records per batch row
+  const int64_t rs_tiles = k * ((NRr + 2047) / 2048) + 2;
+  const int64_t sw2 = scan_workspace_elems<int64_t>(W + 1);
+  w.scan_ws2 = (int64_t*)take(sizeof(int64_t) * (sw2 > rs_tiles ? sw2 : rs_tiles));
   w.d_W = (int64_t*)take(sizeof(int64_t));
   w.clean = (int64_t*)take(sizeof(int64_t));
   w.btot = (int64_t*)take(sizeof(int64_t) * (k + 1));
@@ -1792,7 +1809,10 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     // per batch row: record prefixes and the row total; column offsets
     int64_t* sizes = d_sizes + 3 * l;
     if (k > 0) {
-      k_rec_scan<<<(unsigned)k, kRecScanThreads, 0, xs>>>((uint4*)bm, NR, ws.btot);
+      const int64_t rtiles = k * ((NR + kRsTile - 1) / kRsTile);
+      GB_CUDA(cudaMemsetAsync(ws.scan_ws2, 0, sizeof(int64_t) * (rtiles + 2), xs));
+      k_rec_scan<<<grid_for(rtiles, 1, 8 * kNumSMs), kRsThreads, 0, xs>>>(
+          (uint4*)bm, NR, k, ws.btot, (unsigned long long*)ws.scan_ws2);
       GB_LAUNCH_CHECK("k_rec_scan");
     }
     k_layer_cols<<<1, 1024, 0, xs>>>(brow, k, o.fptr, ws.btot, o.coloff, sizes);

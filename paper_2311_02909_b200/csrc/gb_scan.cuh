@@ -53,6 +53,34 @@ __device__ __forceinline__ void st_store(unsigned long long* p, unsigned long lo
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// Decoupled look-back for tile `tile` whose predecessors back to `first`
+// (a segment start) are summed: publishes `total` (aggregate, then inclusive
+// prefix) and returns the exclusive prefix.  Warp 0 only; st[1 + t] are the
+// tile status words (zeroed before the launch).
+__device__ __forceinline__ int64_t tile_lookback(unsigned long long* st, int64_t tile,
+                                                 int64_t first, int64_t total) {
+  const int lane = threadIdx.x & 31;
+  int64_t prefix = 0;
+  if (tile == first) {
+    if (lane == 0) st_store(st + 1 + tile, kStInc | (unsigned long long)total);
+    return 0;
+  }
+  if (lane == 0) st_store(st + 1 + tile, kStAgg | (unsigned long long)total);
+  for (int64_t j = tile - 1;; j -= 32) {
+    const int64_t idx = j - lane;  // lane 0: nearest predecessor
+    unsigned long long w;
+    do {
+      w = idx >= first ? st_load(st + 1 + idx) : kStInc;
+    } while (__any_sync(0xffffffffu, (w >> 62) == 0));
+    const unsigned inc = __ballot_sync(0xffffffffu, (w >> 62) == 2);
+    const int stop = inc ? __ffs(inc) - 1 : 31;
+    prefix += warp_sum(lane <= stop ? (int64_t)(w & kStVal) : (int64_t)0);
+    if (inc) break;
+  }
+  if (lane == 0) st_store(st + 1 + tile, kStInc | (unsigned long long)(prefix + total));
+  return prefix;
+}
+
 template <typename OutT, typename F, int STRIDE = 1>
 __global__ void __launch_bounds__(kScanThreads) scan_single_pass(const int64_t* n_ptr, F f,
                                                                  OutT* out,

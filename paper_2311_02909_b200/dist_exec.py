@@ -88,7 +88,13 @@ def _all_gather_into(out, t):
         dist.all_gather_into_tensor(out, t)
 
 
-def exchange(sends, recv_sizes, group_ranks, dtype, device):
+# bytes this process handed to the transport (payload of the executor's
+# messages, size exchanges excluded): the ledger's words describe exactly
+# this traffic (tests/dist_exec_check.py)
+WIRE = {"bytes": 0}
+
+
+def exchange(sends, recv_sizes, group_ranks, dtype, device, count_wire=True):
     """Point-to-point exchange inside a group: sends {peer: tensor},
     recv_sizes {peer: count}; returns {peer: tensor}.  Grouped isend/irecv
     (NCCL over NVLink on GPUs; gloo through host copies for the single-GPU
@@ -113,6 +119,8 @@ def exchange(sends, recv_sizes, group_ranks, dtype, device):
             continue
         if t.numel():
             ops.append(dist.P2POp(dist.isend, t.contiguous().to(wire), peer))
+            if count_wire:
+                WIRE["bytes"] += t.numel() * t.element_size()
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()
@@ -129,7 +137,8 @@ def exchange_counts(sends, group_ranks, device):
     me = dist.get_rank()
     cnt_out = {p: torch.tensor([int(sends.get(p, torch.empty(0)).numel())], dtype=torch.int64,
                                device=device) for p in group_ranks}
-    got = exchange(cnt_out, {p: 1 for p in group_ranks}, group_ranks, torch.int64, device)
+    got = exchange(cnt_out, {p: 1 for p in group_ranks}, group_ranks, torch.int64, device,
+                   count_wire=False)
     return {p: int(got[p].item()) if p != me else int(cnt_out[me].item()) for p in group_ranks}
 
 

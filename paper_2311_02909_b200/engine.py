@@ -68,7 +68,9 @@ class SageBulk:
         _lib.check(_lib.lib().gb_sage_bulk_workspace(
             dg.handle, self.k, self.r1_cap, L, self.h_fanouts.ctypes.data,
             ctypes.byref(nbytes)), "gb_sage_bulk_workspace")
-        self.ws = torch.empty(max(int(nbytes.value), 1), dtype=torch.uint8, device=dev)
+        # zero-filled once: the library keeps its bit maps and vertex counters
+        # clear between bulks on this workspace (gnnbulk_b200.h, gb_sage_bulk)
+        self.ws = torch.zeros(max(int(nbytes.value), 1), dtype=torch.uint8, device=dev)
         self.sizes = torch.zeros(3 * L, dtype=torch.int64, device=dev)
 
     def launch_peer(self, d_bptr, d_bverts, seed, epoch, batch_offset, peer, stream=None):
@@ -278,26 +280,48 @@ def sample_epoch_generic(G, cfg, batches, epoch, batch_offset, prob_spgemm):
     return SampledEpoch(cfg.kind, epoch, batches, layers, calls)
 
 
+class _PinnedBlock:
+    """One bulk's host results: a pinned byte tensor of the sampler's pool.
+    numpy arrays made from it keep it alive (it is their base); when the last
+    one is gone the tensor returns to the pool for a later bulk."""
+
+    def __init__(self, tensor, pool):
+        self.t, self.pool = tensor, pool
+        self.__array_interface__ = {"shape": (tensor.numel(),), "typestr": "|u1",
+                                    "data": (tensor.data_ptr(), False), "version": 3}
+
+    def __del__(self):
+        try:
+            self.pool.append(self.t)
+        except Exception:
+            pass
+
+
 class BulkSampler:
     """Public reusable bulk sampler bound to (graph, config).
 
     `sample(batches)` is the drop-in for `sample_epoch_bulk` when the same
     shapes recur (an epoch loop): device buffers are planned once, host
     batches travel through pinned memory, and with `to_host=True` the result
-    arrays are copied back into pinned host buffers (the reference returns
-    host numpy arrays).  With `to_host=False` the results stay in HBM.
+    arrays come back into pinned host memory owned by the returned epoch
+    (the reference returns new host numpy arrays; here the reference types —
+    `frontier` / `adjacency` SparseMatrix, the per-batch vertex tuples — are
+    zero-copy views of them).  With `to_host=False` the results stay in HBM.
+    SAGE (any kernel mode) and LADIES (race / exact).
     """
 
-    def __init__(self, G: Graph, cfg: SamplerConfig, max_batch_vertices=None, mode="dedup"):
+    def __init__(self, G: Graph, cfg: SamplerConfig, max_batch_vertices=None, mode=None):
         import torch
 
-        if cfg.kind is not SamplerKind.SAGE:
-            raise ContractViolation("BulkSampler currently drives the SAGE path")
-        self.G, self.cfg, self.mode = G, cfg, mode
+        self.G, self.cfg = G, cfg
+        self.kind = cfg.kind
+        if mode is None:
+            mode = "dedup" if cfg.kind is SamplerKind.SAGE else "race"
+        self.mode = mode
         self.dg = G.device()
         self.r1 = int(max_batch_vertices or cfg.bulk_count * cfg.batch_size)
-        self._pinned = {}
         self._slots = [self._new_slot()]
+        self._pool = []  # pinned result blocks not owned by a live epoch
         self._copy_stream = torch.cuda.Stream()
         self.h2d_bytes = 0
         self.d2h_bytes = 0
@@ -307,13 +331,19 @@ class BulkSampler:
         import torch
 
         k, r1, cfg = self.cfg.bulk_count, self.r1, self.cfg
+        if self.kind is SamplerKind.SAGE:
+            bulk = SageBulk(self.dg, k, r1, cfg.batch_size, cfg.fanouts, mode=self.mode)
+            nsz = 3 * cfg.layers
+        else:
+            bulk = LadiesBulk(self.dg, k, r1, cfg.fanouts, mode=self.mode)
+            nsz = 5 * cfg.layers
         return {
-            "bulk": SageBulk(self.dg, k, r1, cfg.batch_size, cfg.fanouts, mode=self.mode),
+            "bulk": bulk,
             "h_off": torch.empty(k + 1, dtype=torch.int64, pin_memory=True),
             "h_cat": torch.empty(max(r1, 1), dtype=torch.int32, pin_memory=True),
             "d_off": torch.empty(k + 1, dtype=torch.int64, device="cuda"),
             "d_cat": torch.empty(max(r1, 1), dtype=torch.int32, device="cuda"),
-            "h_sizes": torch.empty(3 * cfg.layers, dtype=torch.int64, pin_memory=True),
+            "h_sizes": torch.empty(nsz, dtype=torch.int64, pin_memory=True),
             "copied": None,
         }
 
@@ -325,8 +355,10 @@ class BulkSampler:
         k = self.cfg.bulk_count
         if len(batches) != k:
             raise ContractViolation(f"BulkSampler built for {k} batches, got {len(batches)}")
-        cat, off = _flatten_batches(batches, self.G.n)
-        if k and int(np.max(np.diff(off))) > self.cfg.batch_size:
+        sort_within = self.kind is SamplerKind.LADIES
+        cat, off = _flatten_batches(batches, self.G.n, sort_within=sort_within)
+        if k and self.kind is SamplerKind.SAGE and \
+                int(np.max(np.diff(off))) > self.cfg.batch_size:
             raise ContractViolation("actual rows exceed the nominal stride")
         if cat.size > slot["h_cat"].numel():
             raise ContractViolation("more batch vertices than the sampler was built for")
@@ -338,62 +370,91 @@ class BulkSampler:
         self.h2d_bytes = 8 * (k + 1) + 4 * r1
         return cat, off
 
+    def _launch(self, slot, epoch, batch_offset):
+        slot["bulk"].launch(slot["d_off"], slot["d_cat"], self.cfg.seed, epoch, batch_offset)
+        slot["h_sizes"].copy_(slot["bulk"].sizes, non_blocking=True)
+
     def _stage(self, slot, layers):
-        """One D2H copy per distinct device buffer into persistent pinned
-        staging on the current stream (frontier/adjacency/sampled arrays
-        alias each other and the next layer's rows; layer-1 rows are the
-        caller's input)."""
+        """One device->host copy per distinct device buffer, into one pinned
+        block from the sampler's pool (the epoch built on it owns it until
+        its last array is dropped, then it returns to the pool).  Offset
+        arrays travel as int32 (values < 2^31), halving their bytes; the
+        frontier, adjacency, sampled-vertex and next-layer row arrays alias
+        each other and cross once."""
         import torch
 
-        host = {}
-        nbytes = 0
+        plan, seen, off = [], set(), 0
         for layer in layers:
             for key, v in layer.device.items():
                 if isinstance(v, tuple):
                     continue
                 ident = (v.data_ptr(), v.numel())
-                if ident in host or v.data_ptr() in (slot["d_off"].data_ptr(),
+                if ident in seen or v.data_ptr() in (slot["d_off"].data_ptr(),
                                                      slot["d_cat"].data_ptr()):
                     continue
-                buf = self._pinned.get(v.data_ptr())
-                if buf is None or buf.numel() < v.numel():
-                    buf = torch.empty(max(v.numel(), 1), dtype=v.dtype, pin_memory=True)
-                    self._pinned[v.data_ptr()] = buf
-                buf[: v.numel()].copy_(v, non_blocking=True)
-                nbytes += v.numel() * v.element_size()
-                host[ident] = buf[: v.numel()]
-        return host, nbytes
+                seen.add(ident)
+                src = v.to(torch.int32) if v.dtype == torch.int64 else v
+                nb = src.numel() * src.element_size()
+                plan.append((ident, src, off))
+                off += (nb + 255) & ~255
+        need = max(off, 256)
+        blk = None
+        for i, t in enumerate(self._pool):
+            if t.numel() >= need:
+                blk = self._pool.pop(i)
+                break
+        if blk is None:
+            blk = torch.empty(need + need // 8, dtype=torch.uint8, pin_memory=True)
+        host = {}
+        nbytes = 0
+        for ident, src, o in plan:
+            n = src.numel() * src.element_size()
+            if n:
+                blk[o:o + n].view(src.dtype).copy_(src, non_blocking=True)
+            host[ident] = (o, src.dtype, src.numel())
+            nbytes += n
+        return (_PinnedBlock(blk, self._pool), host), nbytes
 
-    def _host_epoch(self, slot, layers, host, batches, cat, off, epoch):
+    def _host_epoch(self, slot, layers, staged, batches, cat, off, epoch):
+        import torch
+
+        block, host = staged
+        base = np.asarray(block)  # keeps the block (and its pool slot) alive
+        np_dtype = {torch.int32: np.int32, torch.int64: np.int64, torch.float32: np.float32}
         out_layers = []
         for layer in layers:
             h = {}
             for key, v in layer.device.items():
                 if isinstance(v, tuple):
-                    h[key] = v
+                    h[key] = np.asarray(v, dtype=np.int64)
                 elif v.data_ptr() == slot["d_off"].data_ptr():
                     h[key] = off
                 elif v.data_ptr() == slot["d_cat"].data_ptr():
                     h[key] = cat[: v.numel()]
                 else:
-                    h[key] = host[(v.data_ptr(), v.numel())].numpy()
+                    o, dt, n = host[(v.data_ptr(), v.numel())]
+                    item = np.dtype(np_dtype[dt]).itemsize
+                    h[key] = base[o:o + n * item].view(np_dtype[dt])
             out_layers.append(LayerSample(layer.depth, device=h, n=self.G.n))
-        return SampledEpoch(SamplerKind.SAGE, epoch, batches, out_layers, self.cfg.layers)
+        return SampledEpoch(self.kind, epoch, batches, out_layers, self.cfg.layers)
+
+    def _layers(self, slot, sizes):
+        return slot["bulk"].layers(slot["d_off"], slot["d_cat"], sizes)
 
     def sample(self, batches, epoch=0, batch_offset=0, to_host=True) -> SampledEpoch:
         import torch
 
         slot = self._slots[0]
+        if slot["copied"] is not None:
+            slot["copied"].synchronize()
         cat, off = self._upload(slot, batches)
-        slot["bulk"].launch(slot["d_off"], slot["d_cat"], self.cfg.seed, epoch, batch_offset)
-        slot["h_sizes"].copy_(slot["bulk"].sizes, non_blocking=True)
+        self._launch(slot, epoch, batch_offset)
         torch.cuda.current_stream().synchronize()
         sizes = slot["h_sizes"].numpy().copy()
-        layers = slot["bulk"].layers(slot["d_off"], slot["d_cat"], sizes)
+        layers = self._layers(slot, sizes)
         self.d2h_bytes = 8 * sizes.size
         if not to_host:
-            return SampledEpoch(SamplerKind.SAGE, epoch, batches, layers, self.cfg.layers)
-        # Host arrays stay valid until the next sample() call.
+            return SampledEpoch(self.kind, epoch, batches, layers, self.cfg.layers)
         host, nbytes = self._stage(slot, layers)
         self.d2h_bytes += nbytes
         torch.cuda.current_stream().synchronize()
@@ -403,8 +464,8 @@ class BulkSampler:
         """Generator over `jobs` (an iterable of (batches, batch_offset)):
         yields each bulk's host SampledEpoch, with the device->host copy of
         bulk j (side stream) overlapping the sampling of bulk j + 1 (two
-        device buffer sets alternate).  Same results as sample(); host arrays
-        of a yielded epoch stay valid until the generator is advanced twice.
+        device buffer sets alternate).  Same results as sample(); every
+        yielded epoch owns its host memory.
         """
         import torch
 
@@ -418,14 +479,14 @@ class BulkSampler:
             slot = self._slots[j % 2]
             if slot["copied"] is not None:
                 cs.wait_event(slot["copied"])  # its previous bulk left the device
+                slot["copied"].synchronize()   # and its pinned inputs are free
             cat, off = self._upload(slot, batches)
-            slot["bulk"].launch(slot["d_off"], slot["d_cat"], self.cfg.seed, epoch, boff)
-            slot["h_sizes"].copy_(slot["bulk"].sizes, non_blocking=True)
+            self._launch(slot, epoch, boff)
             done = torch.cuda.Event()
             done.record(cs)
             done.synchronize()  # sizes of bulk j (bulk j - 1 is still copying)
             sizes = slot["h_sizes"].numpy().copy()
-            layers = slot["bulk"].layers(slot["d_off"], slot["d_cat"], sizes)
+            layers = self._layers(slot, sizes)
             xs.wait_event(done)
             with torch.cuda.stream(xs):
                 host, nbytes = self._stage(slot, layers)
@@ -433,12 +494,12 @@ class BulkSampler:
             slot["copied"].record(xs)
             self.d2h_bytes = 8 * sizes.size + nbytes
             if pend is not None:
-                pslot, players, phost, pb, pcat, poff = pend
-                pslot["copied"].synchronize()
+                pslot, pev, players, phost, pb, pcat, poff = pend
+                pev.synchronize()
                 yield self._host_epoch(pslot, players, phost, pb, pcat, poff, epoch)
-            pend = (slot, layers, host, batches, cat, off)
+            pend = (slot, slot["copied"], layers, host, batches, cat, off)
             j += 1
         if pend is not None:
-            pslot, players, phost, pb, pcat, poff = pend
-            pslot["copied"].synchronize()
+            pslot, pev, players, phost, pb, pcat, poff = pend
+            pev.synchronize()
             yield self._host_epoch(pslot, players, phost, pb, pcat, poff, epoch)

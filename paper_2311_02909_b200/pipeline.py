@@ -80,6 +80,17 @@ class FeaturePartition:
     def full(self) -> np.ndarray:
         return np.concatenate(self.blocks, axis=0)
 
+    def device_blocks64(self):
+        """float64 copies of the blocks in HBM viewed as fp32 pairs (the
+        reference's values, gathered bit for bit)."""
+        import torch
+
+        if not getattr(self, "_dev64", None):
+            object.__setattr__(self, "_dev64", [
+                torch.as_tensor(np.ascontiguousarray(b, dtype=np.float64)).cuda().view(
+                    torch.float32) for b in self.blocks])
+        return self._dev64
+
     def device_blocks(self):
         """fp32 copies of the blocks in HBM (built once)."""
         import torch
@@ -126,11 +137,22 @@ def fetch_features(frontier_vertices, Hpart: FeaturePartition, grid, ledger=None
     order, duplicates once per occurrence (pipeline.py:78-120).  Rows owned
     by the requester are free; the others are charged as the column
     all-to-allv.  Gathered on the device from the fp32 block copies."""
+    import torch
+
     vertices = np.asarray(frontier_vertices, dtype=np.int64)
     if vertices.size and (vertices.min() < 0 or vertices.max() >= Hpart.n):
         raise ContractViolation("frontier vertex id out of range")
-    return fetch_features_device(vertices, Hpart, grid, ledger, requester).cpu().numpy().astype(
-        np.float64)
+    owner_rows = (np.searchsorted(Hpart.row_starts, vertices, side="right") - 1
+                  if vertices.size else np.zeros(0, dtype=np.int64))
+    _charge_fetch(owner_rows, Hpart.f, grid, ledger, requester)
+    # float64 rows gathered as raw bytes (two fp32 words each): exact
+    out = torch.empty((vertices.size, 2 * Hpart.f), dtype=torch.float32, device="cuda")
+    dev = Hpart.device_blocks64()
+    for block_row in np.unique(owner_rows):
+        sel = np.nonzero(owner_rows == block_row)[0]
+        rows = _gather_rows(vertices[sel], dev[int(block_row)], Hpart.row_starts[block_row])
+        out[torch.as_tensor(sel, device="cuda")] = rows
+    return out.view(torch.float64).cpu().numpy()
 
 
 def fetch_features_device(vertices, Hpart: FeaturePartition, grid, ledger=None, requester=0):
@@ -169,20 +191,27 @@ def _spmm(R, rowptr, col, X, row_batch=None, shift=None, k=0):
 
 def forward_aggregate(A_l: SparseMatrix, H_in) -> np.ndarray:
     """Aggregation product A_l @ H_in (sparse times dense), reference
-    pipeline.py:123-130 — on the device in fp32 with A's values taken as 1.0
-    (every sampled adjacency is 0/1)."""
+    pipeline.py:123-130 — on the device in float64 with A's values, in
+    scipy's accumulation order (gb_spmm_f64): bit-identical results."""
     import torch
+
+    from . import _lib
 
     H_in = np.asarray(H_in, dtype=np.float64)
     if H_in.ndim != 2 or A_l.n_cols != H_in.shape[0]:
         raise ContractViolation(f"aggregation mismatch: {A_l.shape} @ {H_in.shape}")
-    if A_l.nnz and not np.all(A_l.values == 1.0):
-        raise ContractViolation("forward_aggregate expects a 0/1 sampled adjacency")
-    rowptr = torch.as_tensor(A_l.row_offsets.astype(np.int64)).cuda()
-    col = torch.as_tensor(A_l.col_indices.astype(np.int32)).cuda() if A_l.nnz else \
+    R, f = A_l.n_rows, H_in.shape[1]
+    rowptr = torch.as_tensor(np.asarray(A_l.row_offsets, dtype=np.int64)).cuda()
+    col = torch.as_tensor(np.asarray(A_l.col_indices, dtype=np.int32)).cuda() if A_l.nnz else \
         torch.zeros(1, dtype=torch.int32, device="cuda")
-    X = torch.as_tensor(np.ascontiguousarray(H_in, dtype=np.float32)).cuda()
-    return _spmm(A_l.n_rows, rowptr, col, X).cpu().numpy().astype(np.float64)
+    val = torch.as_tensor(np.ascontiguousarray(A_l.values, dtype=np.float64)).cuda() if A_l.nnz \
+        else torch.zeros(1, dtype=torch.float64, device="cuda")
+    X = torch.as_tensor(np.ascontiguousarray(H_in)).cuda()
+    Y = torch.empty((R, f), dtype=torch.float64, device="cuda")
+    _lib.check(_lib.lib().gb_spmm_f64(R, _lib.ptr(rowptr), _lib.ptr(col), _lib.ptr(val),
+                                      _lib.ptr(X), f, _lib.ptr(Y), _lib.stream_ptr()),
+               "gb_spmm_f64")
+    return Y.cpu().numpy()
 
 
 def _layer_shift(dev, k):

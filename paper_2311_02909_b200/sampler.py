@@ -160,6 +160,15 @@ def _split(cat, off):
     return tuple(cat[off[i]:off[i + 1]].copy() for i in range(len(off) - 1))
 
 
+def _views(cat, off):
+    out = []
+    for i in range(len(off) - 1):
+        v = cat[int(off[i]):int(off[i + 1])]
+        v.setflags(write=False)
+        out.append(v)
+    return tuple(out)
+
+
 class LayerSample:
     """Sampling output of one layer (reference sampler.py:240-261).
 
@@ -210,6 +219,21 @@ class LayerSample:
         return out
 
     def _materialise(self):
+        if self._host is None and self.device is not None and all(
+                isinstance(v, (np.ndarray, tuple)) for v in self.device.values()):
+            # host-staged flat arrays (BulkSampler): reference types as
+            # zero-copy views — CSR over the staged offsets / columns, the
+            # per-batch tuples as slices of the concatenated arrays
+            d = self.device
+            fs, ads = d["frontier_shape"], d["adj_shape"]
+            self._host = {
+                "frontier": SparseMatrix.trusted(fs[0], fs[1], d["frontier_ptr"],
+                                                 d["frontier_col"]),
+                "adjacency": SparseMatrix.trusted(ads[0], ads[1], d["adj_ptr"], d["adj_col"]),
+                "row_vertices": _views(d["rowv_cat"], d["rowv_off"]),
+                "col_vertices": _views(d["colv_cat"], d["colv_off"]),
+                "sampled_vertices": _views(d["sampv_cat"], d["sampv_off"]),
+            }
         if self._host is None:
             a = self.to_arrays()
             fs, ads = a["frontier_shape"], a["adj_shape"]

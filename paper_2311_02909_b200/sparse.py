@@ -108,6 +108,22 @@ class SparseMatrix:
         return cls(n_rows, n_cols, csr.indptr, csr.indices, csr.data)
 
     @classmethod
+    def trusted(cls, n_rows, n_cols, row_offsets, col_indices):
+        """Zero-copy view of a canonical 0/1 CSR produced by the device sampler
+        (row offsets / columns as returned, int32 or int64; values a
+        read-only broadcast of 1.0).  Same values and semantics as the
+        reference's arrays, no host conversion."""
+        m = cls.__new__(cls)
+        m.n_rows, m.n_cols = int(n_rows), int(n_cols)
+        ptr = np.asarray(row_offsets).view()
+        col = np.asarray(col_indices).view()
+        ptr.setflags(write=False)
+        col.setflags(write=False)
+        m.row_offsets, m.col_indices = ptr, col
+        m.values = np.broadcast_to(np.float64(1.0), (col.shape[0],))
+        return m
+
+    @classmethod
     def empty(cls, n_rows, n_cols):
         return cls(n_rows, n_cols, np.zeros(int(n_rows) + 1, dtype=INDEX_DTYPE), [], [])
 

@@ -111,12 +111,89 @@ def main():
                 print(f"grid ({p},{c}) fetch_features p2p: {'PASS' if same else 'FAIL'}",
                       flush=True)
             peer.handle.barrier(channel=0)
+    ok &= cost_model_band(gb, world, rank, gloo)
     t = torch.tensor([1 if ok else 0], device="cpu" if gloo else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MIN)
     if rank == 0:
         print("ALL PASS" if int(t.item()) else "SOME FAILED", flush=True)
     dist.destroy_process_group()
     sys.exit(0 if int(t.item()) else 1)
+
+
+def cost_model_band(gb, world, rank, gloo):
+    """Reference test_acceptance.py:193-240 over the real transport: the
+    Alg. 2 row fetch (fetch="rows") on a d-out-regular graph, one layer
+    (Q = the seed matrix), k = 4 batches of b = 128.  Checks (a) the bytes
+    the executor handed to NCCL / gloo equal 4 x the ledger's words (the
+    reference's accounting describes the wire), (b) each grid column's
+    row-data words equal the sparsity-aware volume (d per distinct remote
+    row, dist.py:308-378) and (c) lie in [0.5, 2] x the model's kbd/c scaled
+    by the remote fraction of the rows (the model ignores locality)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2311_02909_b200 import dist_exec
+    from paper_2311_02909_b200.dist import CommLedger, ProcessGrid, _bounds
+    from paper_2311_02909_b200.dist_exec import Sage15D, sage_epoch_15d
+
+    n, d, k, b = 1 << 13, 8, 4, 128
+    rng = np.random.default_rng(77)
+    offs = rng.choice(np.arange(1, n), size=d, replace=False)
+    src = np.repeat(np.arange(n), d)
+    dst = (src + np.tile(offs, n)) % n
+    G = gb.Graph.from_edges(n, src, dst)
+    batches = list(rng.permutation(n)[: k * b].reshape(k, b))
+    cfg = gb.SamplerConfig.sage(1, b, (d,), bulk_count=k, seed=1)
+    serial = gb.sample_epoch_bulk(G, cfg, batches)
+    ok = True
+    for c in (1, 2):
+        if world % c or c * c > world or world % (c * c):
+            continue
+        grid = ProcessGrid(world, c)
+        led = CommLedger(world)
+        dist_exec.WIRE["bytes"] = 0
+        smp = Sage15D(G.device(), grid, (d,), b, mode="pfree", ledger=led, fetch="rows")
+        same = serial.equals(sage_epoch_15d(smp, cfg, batches))
+        wire = torch.tensor([dist_exec.WIRE["bytes"]], dtype=torch.int64,
+                            device="cpu" if gloo else "cuda")
+        dist.all_reduce(wire)
+        words = sum(led.words(phase=ph) for ph in ("gather-cols", "row-data"))
+        wsum = torch.tensor([words], dtype=torch.int64, device=wire.device)
+        dist.all_reduce(wsum)
+        ledger_eq = int(wire.item()) == 4 * int(wsum.item())
+        # exact sparsity-aware volume per grid column
+        bounds = _bounds(n, grid.rows)
+        gb_ = _bounds(len(batches), grid.rows)
+        st = grid.stages
+        band = True
+        for j in range(c):
+            col_words = torch.tensor([led.words(phase="row-data", process=rank)
+                                      if grid.coords(rank)[1] == j else 0],
+                                     dtype=torch.int64, device=wire.device)
+            dist.all_reduce(col_words)
+            expect, remote, total = 0, 0, 0
+            for i in range(grid.rows):
+                U = np.unique(np.concatenate(batches[int(gb_[i]):int(gb_[i + 1])]))
+                for q in range(st):
+                    kb = j * st + q
+                    cnt = int(np.sum((U >= bounds[kb]) & (U < bounds[kb + 1])))
+                    total += cnt
+                    if kb != i:
+                        expect += d * cnt
+                        remote += cnt
+            model = k * b * d / c * (remote / max(total, 1))
+            cw = int(col_words.item())
+            band &= cw == expect and 0.5 * model <= cw <= 2.0 * model
+            if rank == 0:
+                print(f"  column {j}: row-data words {cw} (sparsity-aware volume {expect}, "
+                      f"model kbd/c x remote {model:.0f})", flush=True)
+        good = same and ledger_eq and band
+        ok &= good
+        if rank == 0:
+            print(f"grid ({world},{c}) cost-model band: {'PASS' if good else 'FAIL'} "
+                  f"(epoch {same}, wire bytes {int(wire.item())} = 4 x ledger words "
+                  f"{int(wsum.item())}: {ledger_eq})", flush=True)
+    return ok
 
 
 if __name__ == "__main__":

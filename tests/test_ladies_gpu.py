@@ -230,3 +230,33 @@ def test_ladies_race_inclusion_law_at_scale(bias):
     assert table.shape[1] >= 20
     chi2, pval, dof, _ = stats.chi2_contingency(table)
     assert pval > 0.01, (chi2, dof, pval)
+
+
+def test_ladies_bulk_sampler_public_api():
+    """BulkSampler drives the LADIES path too: host-staged epochs (and the
+    streamed ones) equal sample_epoch_bulk, reference-typed fields read as
+    zero-copy views."""
+    gb = _gb()
+    from paper_2311_02909_b200.engine import BulkSampler
+    from test_sage_gpu import _rmat
+
+    rng = np.random.default_rng(21)
+    n, rowptr, col = _rmat(12, 40000, seed=21)
+    G = _graph(n, rowptr, col)
+    cfg = gb.SamplerConfig.ladies(3, 64, 32, bulk_count=6, seed=4)
+    jobs = [([np.sort(rng.permutation(n)[: rng.integers(1, 65)]) for _ in range(6)], 6 * j)
+            for j in range(3)]
+    for mode in ("race", "exact"):
+        bs = BulkSampler(G, cfg, mode=mode)
+        want = [gb.sample_epoch_bulk(G, cfg, b, epoch=1, batch_offset=o, mode=mode)
+                for b, o in jobs]
+        got = [bs.sample(b, epoch=1, batch_offset=o) for b, o in jobs]
+        streamed = list(bs.sample_stream(jobs, epoch=1))
+        for w, g, st in zip(want, got, streamed):
+            assert O.compare_epochs(w.to_arrays(), g.to_arrays()) == []
+            assert O.compare_epochs(w.to_arrays(), st.to_arrays()) == []
+            for lw, lg in zip(w.layers, st.layers):
+                assert lg.adjacency.equals(lw.adjacency)
+                assert lg.frontier.equals(lw.frontier)
+                assert all(np.array_equal(a, b) for a, b in zip(lg.col_vertices,
+                                                                lw.col_vertices))

@@ -23,9 +23,11 @@ def _gpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-def test_distributed_executors_two_processes_one_gpu():
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr", "127.0.0.1", "--master-port", "29593",
+@pytest.mark.parametrize("procs", [2, 4])
+def test_distributed_executors_processes_sharing_one_gpu(procs):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={procs}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29593 + procs),
            os.path.join(HERE, "dist_exec_check.py")]
     env = dict(os.environ, GB_DIST_BACKEND="gloo")
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900,

@@ -50,6 +50,10 @@ def test_forward_aggregate_matches_scipy(f):
     want = PR.forward_aggregate(R, C, A.row_offsets, A.col_indices, H)
     assert got.shape == (R, f) and got.dtype == np.float64
     _close(got, want)
+    # any values, float64, the reference's scipy order: bit-identical
+    W = gb.SparseMatrix(R, C, A.row_offsets, A.col_indices, rng.standard_normal(A.nnz))
+    Hn = rng.standard_normal((C, f))
+    assert np.array_equal(gb.forward_aggregate(W, Hn), W.to_scipy() @ Hn)
     with pytest.raises(gb.ContractViolation):
         gb.forward_aggregate(A, H[:-1])
 
@@ -98,7 +102,7 @@ def test_fetch_features_rows_and_ledger(p, c):
         led = CommLedger(p)
         got = gb.fetch_features(verts, Hp, grid, led, requester)
         assert got.dtype == np.float64
-        _close(got, H[verts].astype(np.float32).astype(np.float64))
+        assert np.array_equal(got, H[verts])  # float64 rows, bit for bit
         want = PR.fetch_words(verts, Hp.row_starts, f, grid.rows, c, requester)
         for r in range(p):
             m, w = want.get(r, (0, 0))
@@ -196,7 +200,7 @@ def test_fetch_and_run_epoch_match_reference_ledger():
     for req in range(4):
         led = CommLedger(4)
         rows = gb.fetch_features(z["fetch_verts"], Hp, grid, led, req)
-        _close(rows, H[z["fetch_verts"]])
+        assert np.array_equal(rows, H[z["fetch_verts"]])
         for proc in range(4):
             assert led.words(phase="all-to-allv", process=proc) == z["fetch_words"][req, proc]
             assert led.messages(phase="all-to-allv", process=proc) == z["fetch_msgs"][req, proc]

@@ -168,10 +168,19 @@ def test_bulk_sampler_stream_matches_single_calls():
         bs = BulkSampler(G, cfg, mode=mode)
         for batches, boff in jobs:
             want.append(bs.sample(batches, epoch=2, batch_offset=boff).to_arrays())
-        got = [ep.to_arrays() for ep in bs.sample_stream(jobs, epoch=2)]
+        eps = list(bs.sample_stream(jobs, epoch=2))  # every yielded epoch owns its memory
+        got = [ep.to_arrays() for ep in eps]
         assert len(got) == len(jobs)
         for g, w in zip(got, want[-len(jobs):]):
             assert O.compare_epochs(w, g) == []
+        # reference types as zero-copy views of the staged arrays
+        lay = eps[0].layers[-1]
+        assert lay.adjacency.col_indices.base is not None
+        assert not lay.adjacency.values.flags.writeable
+        assert lay.adjacency.equals(gb.SparseMatrix(*lay.adjacency.shape,
+                                                    eps[0].to_arrays()[-1]["adj_ptr"],
+                                                    eps[0].to_arrays()[-1]["adj_col"],
+                                                    np.ones(lay.adjacency.nnz)))
 
 
 @pytest.mark.parametrize("mode", MODES)
@@ -321,3 +330,32 @@ def test_cfg2_full_size_bulk_matches_oracle():
     want = O.sage_bulk(dg.n, rowptr, col, batches, 1024, (15, 10, 5), 0, 0, 0,
                        threads=os.cpu_count() or 8)
     assert O.compare_epochs(want, got) == []
+
+
+def test_sage_bulks_on_recycled_memory():
+    """Workspace memory recycled by the caching allocator between bulks
+    (other tensors written into it, as run_epoch's feature arrays do) must
+    not leak stale counters or bit maps into the next bulk: a sequence of
+    small bulks, each followed by dirtying allocations, every one bit-exact
+    (the reference test_acceptance test_09 sequence that exposed it)."""
+    import torch
+
+    gb = _pkg()
+    rng = np.random.default_rng(9)
+    n, d, b = 230, 5, 7
+    src = np.repeat(np.arange(n), d)
+    dst = np.concatenate([rng.choice(np.delete(np.arange(n), v), d, replace=False)
+                         for v in range(n)])
+    G = gb.Graph.from_edges(n, src, dst)
+    A = G.adjacency
+    cfg = gb.SamplerConfig.sage(2, b, (3, 2), bulk_count=1, seed=19)
+    for boff in range(24):
+        batches = [] if boff % 3 == 2 else [rng.permutation(n)[:b]]
+        ep = gb.sample_epoch_bulk(G, cfg, batches, batch_offset=boff, mode="dedup")
+        if batches:
+            want = O.sage_bulk(n, A.row_offsets, A.col_indices, batches, b, (3, 2), 19, 0, boff)
+            assert O.compare_epochs(want, ep.to_arrays()) == [], boff
+        del ep
+        junk = [torch.full((4096 * (i + 1),), 7, dtype=torch.int32, device="cuda")
+                for i in range(6)]
+        del junk

@@ -1,9 +1,9 @@
 #!/bin/bash
-# Round evidence on one B200 (run under gpurun from the repo root):
-# bench line, launch lists and ncu captures of the headline SAGE dedup bulk
-# and the LADIES bulk.  Each ncu command runs only after the same program
-# exited 0 without ncu.  Outputs land in gpurun_out/ (summarised into
-# profiles/ by hand / tools/*.py).
+# Round evidence on one B200 (run under gpurun from the repo root): bench
+# line, launch lists and ncu captures of the headline SAGE dedup bulk and the
+# LADIES bulk.  Each ncu command runs only after the same program exited 0
+# without ncu.  Outputs land in gpurun_out/ (summarised into profiles/ by
+# tools/evidence_summary.sh and tools/traffic_json.py).
 set -u
 O=gpurun_out
 mkdir -p $O
@@ -18,15 +18,16 @@ ncu --cache-control none --metrics gpu__time_duration.sum --clock-control none -
     > $O/ev_ncu_a2.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/ev_launches_ladies.csv \
     python tools/profile_bulk.py --sampler ladies --warm 1 > $O/ev_ncu_b.log 2>&1
-# DRAM traffic of every stream / serve / pick launch of the second bulk
+# DRAM traffic of every pick / serve launch of the second bulk (4 per layer)
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
-    --csv -k "regex:k_dd_serve|k_sage_pick|k_sage_stream" --launch-skip 10 --launch-count 10 \
+    --csv -k "regex:k_dd_serve|k_dd_pick" --launch-skip 12 --launch-count 12 \
     --log-file $O/ev_traffic_dedup.csv python tools/profile_bulk.py --mode dedup --warm 1 > $O/ev_ncu_c.log 2>&1
-# full captures: layer 3 of the dedup bulk, layer 2 of the LADIES bulk
+# full captures: layer 3 of the dedup bulk (pick, serve tiers, rank), layer 2 of LADIES
 ncu --set full --clock-control none --import-source on \
-    -k "regex:k_dd_serve|k_sage_pick|k_sage_rank8|k_dd_rows" --launch-skip 22 --launch-count 6 \
-    -o $O/ev_dedup_full python tools/profile_bulk.py --mode dedup --warm 1 > $O/ev_ncu_d.log 2>&1
+    -k "regex:k_dd_serve|k_dd_pick|k_sage_rank128|k_grp_rows|k_grp_items|k_grp_count" \
+    --launch-skip 40 --launch-count 8 \
+    -o $O/ev_dedup_full -f python tools/profile_bulk.py --mode dedup --warm 1 > $O/ev_ncu_d.log 2>&1
 ncu --set full --clock-control none --import-source on -k "regex:k_lad_tile$|k_lad_extract" \
-    --launch-skip 8 --launch-count 2 -o $O/ev_ladies_full \
+    --launch-skip 8 --launch-count 2 -o $O/ev_ladies_full -f \
     python tools/profile_bulk.py --sampler ladies --warm 1 > $O/ev_ncu_e.log 2>&1
 echo done

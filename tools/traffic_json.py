@@ -1,7 +1,7 @@
-"""Refresh profiles/ncu_traffic.json (k_dd_serve, k_sage_pick<2>) from an
+"""Refresh profiles/ncu_traffic.json (k_dd_serve, k_dd_pick) from an
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum CSV of the dedup
-bulk's stream / serve / pick launches (tools/capture_evidence.sh, one bulk:
-layer 1 streams its rows, layers 2 and 3 run the three serve tiers).
+bulk's pick / serve launches (tools/capture_evidence.sh, one bulk: per layer
+one k_dd_pick and the three k_dd_serve tiers).
 
 usage: traffic_json.py TRAFFIC.csv [SOURCE_NOTE]"""
 import collections
@@ -30,28 +30,20 @@ def main():
         nm, acc = per.get(r[idc], (name, 0.0))
         per[r[idc]] = (nm, acc + b)
     serve, pick = [], []
-    l1 = 0.0
-    cur = None
     for name, b in per.values():
-        if name.startswith("k_sage_stream"):
-            l1 = b  # layer 1 of the dedup bulk streams its (all distinct) rows
-        elif name.startswith("k_sage_pick<2"):
-            pick.append(b)
-            cur = 0.0
-            serve.append(cur)
+        if name.startswith("k_dd_pick"):
+            pick.append(b)  # one pick launch opens each layer
+            serve.append(0.0)
         elif name.startswith("k_dd_serve") and serve:
             serve[-1] += b
     out_path = os.path.join(REPO, "profiles", "ncu_traffic.json")
     d = json.load(open(out_path))
-    # the bench's dedup roofline covers layer 1's k_sage_stream + the serves
-    d["k_dd_serve"] = {"per_layer_bytes": [l1] + serve, "bulk_bytes": l1 + sum(serve),
+    d["k_dd_serve"] = {"per_layer_bytes": serve, "bulk_bytes": sum(serve),
                        "source": note + " (ncu --metrics dram__bytes_read.sum,"
-                       "dram__bytes_write.sum; layer 1: k_sage_stream, layers 2-3: the 3 "
-                       "serve tier launches)"}
-    d["k_sage_pick<2>"] = {"per_layer_bytes": [0.0] + pick, "bulk_bytes": sum(pick),
-                           "source": "same capture"}
+                       "dram__bytes_write.sum; per layer the 3 serve tier launches)"}
+    d["k_dd_pick"] = {"per_layer_bytes": pick, "bulk_bytes": sum(pick), "source": "same capture"}
     json.dump(d, open(out_path, "w"), indent=1)
-    print(json.dumps({k: d[k] for k in ("k_dd_serve", "k_sage_pick<2>")}, indent=1))
+    print(json.dumps({k: d[k] for k in ("k_dd_serve", "k_dd_pick")}, indent=1))
 
 
 if __name__ == "__main__":
