@@ -558,8 +558,9 @@ def run_ours(args, rank, world, local_rank):
     G = gb.Graph.from_device(dg)
     cfg = gb.SamplerConfig.sage(3, BATCH, FANOUTS, bulk_count=k, seed=0)
     bs = BulkSampler(G, cfg, mode=args.mode)
-    for _ in range(2):
-        bs.sample(batches, 0, boff)
+    ep = None
+    for _ in range(3):  # steady state: the held epoch's block + one pooled block
+        ep = bs.sample(batches, 0, boff)
     torch.cuda.synchronize()
     nst = max(3, min(args.steps, 10))
     # one synchronous call per bulk (latency)
