@@ -30,6 +30,7 @@
 //   GB_SAGE_PFREE: the P-free fast path: only the picked
 //     entries of A are read.
 #include <stdarg.h>
+#include <stdlib.h>
 #include <stdio.h>
 
 #include "gb_common.cuh"
@@ -589,14 +590,17 @@ __global__ void __launch_bounds__(kGrpThreads) k_grp_count(
   }
 }
 
-// Serve tiers by row degree d (DdTier below): 0 d <= 1K, 1 d <= 8K, 2 hubs.
-// An item serves at most rows_item(d) frontier rows (about 512 / 2048 /
-// 8192 picks).
-__host__ __device__ __forceinline__ int dd_tier(int64_t d) {
-  return d <= 1024 ? 0 : d <= 8192 ? 1 : 2;
+// Serve tiers by row degree d (DdTier below): 0 d <= hi0 (1K), 1 d <= hi1
+// (8K), 2 hubs.  An item serves at most rows_item(d) frontier rows (about
+// 512 / 2048 / 8192 picks).
+struct DdTiers {
+  int32_t hi0, hi1;
+};
+__host__ __device__ __forceinline__ int dd_tier(int64_t d, DdTiers t) {
+  return d <= t.hi0 ? 0 : d <= t.hi1 ? 1 : 2;
 }
-__host__ __device__ __forceinline__ int32_t rows_item(int64_t d, int32_t s) {
-  const int32_t p = d <= 1024 ? 512 : d <= 8192 ? 2048 : 8192;
+__host__ __device__ __forceinline__ int32_t rows_item(int64_t d, int32_t s, DdTiers t) {
+  const int32_t p = d <= t.hi0 ? 512 : d <= t.hi1 ? 2048 : 8192;
   const int32_t r = p / s;
   return r < 1 ? 1 : r;
 }
@@ -629,7 +633,7 @@ __global__ void __launch_bounds__(kItemThreads) k_grp_items(
     const unsigned long long* __restrict__ dcount, const int32_t* __restrict__ dv,
     const int64_t* __restrict__ rowptr, int32_t* __restrict__ vcnt, int32_t* __restrict__ roff,
     int32_t s, int64_t icap, unsigned long long* __restrict__ tcnt, DdItem* __restrict__ items,
-    PeerRows peer) {
+    PeerRows peer, DdTiers tiers) {
   __shared__ int32_t s_wsum[4][kItemThreads / 32];
   __shared__ int64_t s_base[4];
   const int64_t D = (int64_t)*dcount;
@@ -662,8 +666,8 @@ __global__ void __launch_bounds__(kItemThreads) k_grp_items(
       if (v[u] >= 0) {
         vcnt[v[u]] = 0;  // ready for the next layer
         d[u] -= a0[u];
-        t[u] = dd_tier(d[u]);
-        per[u] = rows_item(d[u], s);
+        t[u] = dd_tier(d[u], tiers);
+        per[u] = rows_item(d[u], s, tiers);
         n[u] = (gc[u] + per[u] - 1) / per[u];
         tot[0] += t[u] == 0 ? n[u] : 0;
         tot[1] += t[u] == 1 ? n[u] : 0;
@@ -1540,6 +1544,7 @@ static int persistent_grid(K kernel, int threads, size_t smem = 0) {
 constexpr int kMaxDevices = 16;
 struct ServeCfg {
   bool init = false;
+  DdTiers tiers{1024, 8192};
   int grid[3] = {0, 0, 0};
   int chunk[3] = {0, 0, 0};
   size_t smem[3] = {0, 0, 0};
@@ -1549,9 +1554,9 @@ static ServeCfg g_serve[kMaxDevices];
 template <int T>
 static void serve_tier_setup(ServeCfg& c, int max_smem) {
   using Tr = DdTier<T>;
-  // tier 0: a 4 KB row buffer (+ group table) per warp; tier 1: the whole
-  // row; tier 2: all of shared memory (chunks) but the static mbarrier
-  c.chunk[T] = T == 2 ? (((max_smem - 256) / 4 - 8) & ~3) : Tr::kHi;
+  // tier 0: a row buffer (+ group table) per warp; tier 1: the whole row;
+  // tier 2: all of shared memory (chunks) but the static mbarrier
+  c.chunk[T] = T == 2 ? (((max_smem - 256) / 4 - 8) & ~3) : T == 0 ? c.tiers.hi0 : c.tiers.hi1;
   c.smem[T] = sizeof(int32_t) * (c.chunk[T] + 8 + (Tr::kWarp ? kGrpInts : 0)) *
               (Tr::kWarp ? Tr::kThreads / 32 : 1);
   cudaFuncSetAttribute(k_dd_serve<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1567,6 +1572,14 @@ static ServeCfg& serve_cfg() {
     int max_smem = 0;
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (max_smem <= 0) max_smem = 227 * 1024;
+    // tier bounds (GB_SERVE_TIERS="hi0,hi1" overrides, for tuning sweeps)
+    if (const char* e = getenv("GB_SERVE_TIERS")) {
+      int a = 0, b2 = 0;
+      if (sscanf(e, "%d,%d", &a, &b2) == 2 && a >= 16 && b2 > a && b2 <= 16384) {
+        c.tiers.hi0 = a & ~3;
+        c.tiers.hi1 = b2 & ~3;
+      }
+    }
     serve_tier_setup<0>(c, max_smem);
     serve_tier_setup<1>(c, max_smem);
     serve_tier_setup<2>(c, max_smem);
@@ -1589,7 +1602,8 @@ static int dedup_layer(const Graph* g, SageWs& ws, const int64_t* R_ptr, const i
   const int64_t gw = 16 * kNumSMs;
   k_grp_items<<<grid_for((r_cap < g->n ? r_cap : g->n + 0) / kGrpU + 1, kItemThreads, gw),
                 kItemThreads, 0, st>>>(
-      ws.cnts, ws.dv, g->rowptr, ws.vcnt, ws.roff, s, ws.icap, ws.cnts + 1, ws.items, peer);
+      ws.cnts, ws.dv, g->rowptr, ws.vcnt, ws.roff, s, ws.icap, ws.cnts + 1, ws.items, peer,
+      serve_cfg().tiers);
   GB_LAUNCH_CHECK("k_grp_items");
   k_grp_rows<<<grid_for(r_cap / kGrpU + 1, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, fptr,
                                                                    brow, k, ws.rslot, ws.roff,
