@@ -590,9 +590,9 @@ __global__ void __launch_bounds__(kGrpThreads) k_grp_count(
   }
 }
 
-// Serve tiers by row degree d (DdTier below): 0 d <= hi0 (1K), 1 d <= hi1
-// (8K), 2 hubs.  An item serves at most rows_item(d) frontier rows (about
-// 512 / 2048 / 8192 picks).
+// Serve tiers by row degree d (DdTier below): 0 d <= hi0 (1.5K), 1 d <= hi1
+// (4K), 2 hubs; bounds from the sweep in DESIGN.md §6.  An item serves at
+// most rows_item(d) frontier rows (about 512 / 2048 / 8192 picks).
 struct DdTiers {
   int32_t hi0, hi1;
 };
@@ -1544,7 +1544,7 @@ static int persistent_grid(K kernel, int threads, size_t smem = 0) {
 constexpr int kMaxDevices = 16;
 struct ServeCfg {
   bool init = false;
-  DdTiers tiers{1024, 8192};
+  DdTiers tiers{1536, 4096};
   int grid[3] = {0, 0, 0};
   int chunk[3] = {0, 0, 0};
   size_t smem[3] = {0, 0, 0};
