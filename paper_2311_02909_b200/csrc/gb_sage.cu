@@ -306,7 +306,7 @@ __device__ __forceinline__ void sage_draws(const SageTabs& T, uint64_t key, int3
   double2 sdS = __ldg(tab.sd + rS);
   tab.top = binade(sdS.x);
   uint64_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;
-  for (int t = 0; t < take; ++t) {
+  auto draw = [&](int t) {
     if ((t & 3) == 0) {
       w0 = key; w1 = depth; w2 = (uint64_t)(t >> 2); w3 = 0;
       philox4x64_10(w0, w1, w2, w3, seed, epoch);
@@ -332,6 +332,15 @@ __device__ __forceinline__ void sage_draws(const SageTabs& T, uint64_t key, int3
     for (int z = MAXF - 1; z > 0; --z)  // shift up and insert in one pass
       sorted[z] = (z > i && z <= t) ? sorted[z - 1] : (z == i ? x : sorted[z]);
     if (i == 0) sorted[0] = x;
+  };
+  if constexpr (MAXF <= 10) {
+    // small buckets: unrolled, so draw t's Philox word, the skip over the t
+    // removed indices and the insertion are all static
+#pragma unroll
+    for (int t = 0; t < MAXF; ++t)
+      if (t < take) draw(t);
+  } else {
+    for (int t = 0; t < take; ++t) draw(t);
   }
 }
 
