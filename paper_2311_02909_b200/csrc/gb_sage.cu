@@ -902,6 +902,7 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 
 constexpr int kGrpInts = 6 * 33;  // per-warp group table of the warp tier
+constexpr int kDdU = 4;            // picks per lane whose loads are in flight together
 
 // (frontier offset, batch) of grouped row q: the second half of its record
 __device__ __forceinline__ int2 dd_fb(const DdArgs& A, int32_t q) {
@@ -957,7 +958,10 @@ __device__ void dd_serve_warp(const DdArgs& A, int32_t* buf, int B, int32_t* gi)
       asm volatile("cp.async.commit_group;" ::: "memory");
       __syncwarp();
       const int ng = j1 - j0;
-      auto meta = [&](int p, int32_t& idx, int32_t& fp, int32_t& bb, int32_t& ro) {
+      // pick p of the sub-group: entry index, (frontier offset, batch) of its
+      // row, draw t, row base in buf.  The global loads are only issued here;
+      // their first use is in the serve loop below, kDdU picks later.
+      auto meta = [&](int p, int32_t& idx, int2& fb, int32_t& t, int32_t& ro) {
         int lo = 0, hi = ng;
         while (hi - lo > 1) {
           const int mid = (lo + hi) >> 1;
@@ -966,27 +970,32 @@ __device__ void dd_serve_warp(const DdArgs& A, int32_t* buf, int B, int32_t* gi)
         const int tk = g_tk[lo], tkn = tk < 0 ? -tk : tk;
         const int r = p - g_pst[lo];
         const int i = tkn == 1 ? r : (int)__umulhi((uint32_t)r, g_mg[lo]);
-        const int t = r - i * tkn;
+        t = r - i * tkn;
         const int q = g_q0[lo] + i;
         idx = tk < 0 ? t : A.pidx[(uint32_t)q * (uint32_t)s + (uint32_t)t];
-        const int2 fb = dd_fb(A, q);
-        fp = fb.x + t;
-        bb = fb.y;
+        fb = dd_fb(A, q);
         ro = g_rof[lo];
       };
-      int32_t idx = 0, fp = 0, bb = 0, ro = 0;
-      if (lane < P) meta(lane, idx, fp, bb, ro);
+      int32_t idx[kDdU], t[kDdU], ro[kDdU];
+      int2 fb[kDdU];
+      auto batch = [&](int p0) {
+#pragma unroll
+        for (int u = 0; u < kDdU; ++u)
+          if (p0 + 32 * u + lane < P) meta(p0 + 32 * u + lane, idx[u], fb[u], t[u], ro[u]);
+      };
+      batch(0);  // while the rows land
       asm volatile("cp.async.wait_group 0;" ::: "memory");
       __syncwarp();
-      for (int p0 = 0; p0 < P; p0 += 32) {
-        int32_t idx2 = 0, fp2 = 0, bb2 = 0, ro2 = 0;
-        if (p0 + 32 + lane < P) meta(p0 + 32 + lane, idx2, fp2, bb2, ro2);
-        if (p0 + lane < P) {
-          const int32_t cv = buf[ro + idx];
-          A.fcol[(uint32_t)fp] = cv;
-          atomicOr(A.bitmap + ((uint32_t)bb * NW + pk_word(cv)), 1u << (cv & 31));
+      for (int p0 = 0; p0 < P; p0 += 32 * kDdU) {
+        if (p0) batch(p0);
+#pragma unroll
+        for (int u = 0; u < kDdU; ++u) {
+          if (p0 + 32 * u + lane < P) {
+            const int32_t cv = buf[ro[u] + idx[u]];
+            A.fcol[(uint32_t)(fb[u].x + t[u])] = cv;
+            atomicOr(A.bitmap + ((uint32_t)fb[u].y * NW + pk_word(cv)), 1u << (cv & 31));
+          }
         }
-        idx = idx2; fp = fp2; bb = bb2; ro = ro2;
       }
       __syncwarp();  // buffer and group table free
       j0 = j1;
@@ -1035,31 +1044,32 @@ __global__ void __launch_bounds__(DdTier<TIER>::kThreads) k_dd_serve(DdArgs A) {
           mbar_expect_tx(&bar, bytes);
           tma_row(sbuf, A.col + al0, bytes, &bar);
         }
-        // first pass's pick metadata while the row lands
-        int p = tid;
-        int32_t idx = 0, fp = 0, bb = 0;
-        if (p < npairs) {
-          const int i = p / take, t = p - i * take;
-          idx = A.pidx[(uint32_t)(q0 + i) * (uint32_t)s + (uint32_t)t];
-          const int2 fb = dd_fb(A, q0 + i);
-          fp = fb.x + t;
-          bb = fb.y;
-        }
+        // pick metadata, kDdU picks per thread in flight; the first batch
+        // loads while the row lands
+        int32_t idx[kDdU], t[kDdU];
+        int2 fb[kDdU];
+        auto batch = [&](int p0) {
+#pragma unroll
+          for (int u = 0; u < kDdU; ++u) {
+            const int p = p0 + u * nthr + tid;
+            if (p < npairs) {
+              const int i = p / take;
+              t[u] = p - i * take;
+              idx[u] = A.pidx[(uint32_t)(q0 + i) * (uint32_t)s + (uint32_t)t[u]];
+              fb[u] = dd_fb(A, q0 + i);
+            }
+          }
+        };
+        batch(0);
         mbar_wait(&bar, phase);
         phase ^= 1u;
         const int32_t sh = (int32_t)((a0 + c0) - al0 - c0);  // sbuf[idx + sh], idx in [c0, c1)
-        while (p < npairs) {
-          const int pn = p + nthr;
-          int32_t idx2 = 0, fp2 = 0, bb2 = 0;
-          if (pn < npairs) {
-            const int i = pn / take, t = pn - i * take;
-            idx2 = A.pidx[(uint32_t)(q0 + i) * (uint32_t)s + (uint32_t)t];
-            const int2 fb = dd_fb(A, q0 + i);
-            fp2 = fb.x + t;
-            bb2 = fb.y;
-          }
-          if (idx >= c0 && idx < c1) dd_put(A, fp, bb, sbuf[idx + sh]);
-          p = pn; idx = idx2; fp = fp2; bb = bb2;
+        for (int p0 = 0; p0 < npairs; p0 += kDdU * nthr) {
+          if (p0) batch(p0);
+#pragma unroll
+          for (int u = 0; u < kDdU; ++u)
+            if (p0 + u * nthr + tid < npairs && idx[u] >= c0 && idx[u] < c1)
+              dd_put(A, fb[u].x + t[u], fb[u].y, sbuf[idx[u] + sh]);
         }
         __syncthreads();  // buffer free for the next chunk / item
       }
