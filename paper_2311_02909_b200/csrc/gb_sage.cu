@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k_sage_stream(SageArgs A,
 // distinct vertices in layer 3 at products scale), and identical rows of
 // Q^l give identical rows of P = Q^l A.  Each distinct P row is formed on
 // chip once per work item — the A row staged in shared memory by TMA bulk
-// copies (cp.async.bulk + mbarrier, double-buffered) — and the picks of
+// copies (cp.async.bulk + mbarrier) — and the picks of
 // every frontier row that references it are served from there.
 //
 // Grouping (three passes over the layer's rows, no vertex bitmap):
@@ -858,7 +858,6 @@ struct DdArgs {
   int32_t* fcol;
   uint32_t* bitmap;
   int64_t nwords;
-  unsigned int* ticket;            // (unused by the tiered serve)
   int32_t chunk;                   // staged entries per pass (tier 2), row buffer (tier 0 / 1)
 };
 
@@ -876,32 +875,28 @@ __device__ __forceinline__ void dd_put(const DdArgs& A, int32_t fp, int32_t bb, 
   atomicOr(A.bitmap + (uint32_t)bb * (uint32_t)A.nwords + pk_word(cv), 1u << (cv & 31));
 }
 
-// Serve, three size tiers of distinct rows (degree d): 0 warp-batched
-// (d <= 1K: a warp takes 32 work items, packs as many of their rows as fit
-// its 4 KB buffer with 16-B cp.async granules and serves all their picks
-// lane-parallel — short rows are too small for a bulk copy each), 1 CTA-256
-// per item (d <= 8K: the row is one TMA bulk copy), 2 CTA-1024 per item
-// (hubs: TMA chunks as large as shared memory allows).  The next item's
-// descriptor and each pass's pick metadata load while the row lands.
+// Serve, three size tiers of distinct rows (degree d, bounds DdTiers): 0
+// warp-batched (a warp takes 32 work items, packs as many of their rows as
+// fit its buffer, one TMA bulk copy per row, and serves all their picks
+// lane-parallel), 1 CTA-256 per item (the row is one TMA bulk copy), 2
+// CTA-1024 per item (hubs: TMA chunks as large as shared memory allows).
+// The next item's descriptor and each pass's pick metadata load while the
+// row lands.
 template <int T> struct DdTier;
 template <> struct DdTier<0> {
-  static constexpr int kThreads = 256, kHi = 1024;
+  static constexpr int kThreads = 256;
   static constexpr bool kWarp = true;
 };
 template <> struct DdTier<1> {
-  static constexpr int kThreads = 256, kHi = 8192;
+  static constexpr int kThreads = 256;
   static constexpr bool kWarp = false;
 };
 template <> struct DdTier<2> {
-  static constexpr int kThreads = 1024, kHi = 0x7fffffff;
+  static constexpr int kThreads = 1024;
   static constexpr bool kWarp = false;
 };
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem));
-}
-
-constexpr int kGrpInts = 6 * 33;  // per-warp group table of the warp tier
+constexpr int kGrpInts = 2;  // per-warp mbarrier of the warp tier (in ints)
 constexpr int kDdU = 4;            // picks per lane whose loads are in flight together
 
 // (frontier offset, batch) of grouped row q: the second half of its record
@@ -909,16 +904,23 @@ __device__ __forceinline__ int2 dd_fb(const DdArgs& A, int32_t q) {
   return reinterpret_cast<const int2*>(A.rrec)[2 * (uint32_t)q + 1];
 }
 
-__device__ void dd_serve_warp(const DdArgs& A, int32_t* buf, int B, int32_t* gi) {
-  int32_t* g_pst = gi;            // pair start per item (+ sentinel)
-  int32_t* g_rof = gi + 33;       // row base in buf (16-B alignment shift included)
-  int32_t* g_q0 = gi + 66;        // first grouped row
-  int32_t* g_tk = gi + 99;        // take, negated when take == d (every entry)
-  uint32_t* g_mg = (uint32_t*)(gi + 132);  // ceil(2^32 / take)
+// Warp tier.  A warp takes 32 work items (lane j holds item j) and packs as
+// many of their rows as fit its buffer; every row is staged by its own lane
+// with one bulk copy (TMA, completion counted on the warp's mbarrier; 16-B
+// cp.async granules measured slower at every row length).  Pick p of the
+// sub-group belongs to the item whose pick range holds it: found for 32
+// consecutive picks at once by a ballot (items starting at or before the
+// first) and an OR-reduction of the start bits inside the window, then the
+// item's fields are shuffled from its lane — no tables, no searches.
+__device__ void dd_serve_warp(const DdArgs& A, int32_t* buf, int B, uint64_t* bar) {
+  constexpr unsigned FULL = 0xffffffffu;
   const int lane = lane_id(), s = A.s;
   const uint32_t NW = (uint32_t)A.nwords;
   const int64_t it1 = (int64_t)A.tcnt[0];
   const int64_t nblk = (it1 + 31) / 32;
+  if (lane == 0) mbar_init(bar, 1);
+  __syncwarp();
+  uint32_t phase = 0;
   for (int64_t blk = global_warp(); blk < nblk; blk += grid_warps()) {
     const int64_t it = blk * 32 + lane;
     const int nitems = (int)min((int64_t)32, it1 - blk * 32);
@@ -926,66 +928,62 @@ __device__ void dd_serve_warp(const DdArgs& A, int32_t* buf, int B, int32_t* gi)
     const bool valid = lane < nitems;
     if (valid) c = A.items[it];
     const int len = valid ? dd_row_len(c.a0, c.d) : 0;
-    const int take = valid ? min(c.d, s) : 0;
+    const int take = valid ? min(c.d, s) : 1;
     const int np = valid ? c.nrows * take : 0;
+    const bool all = take == c.d;  // every entry, no picks stored
+    const uint32_t mg = 0xffffffffu / (uint32_t)take + 1u;  // r / take = umulhi(r, mg)
     for (int j0 = 0; j0 < nitems;) {
       // sub-group [j0, j1): rows packed while they fit (always at least one)
       const int lz = lane >= j0 ? len : 0;
       const int incl = warp_incl_scan(lz);
-      const unsigned fit = __ballot_sync(0xffffffffu, lane >= j0 && lane < nitems && incl <= B);
+      const unsigned fit = __ballot_sync(FULL, lane >= j0 && lane < nitems && incl <= B);
       const int j1 = fit ? 32 - __clz(fit) : j0 + 1;
       const bool in = lane >= j0 && lane < j1;
       const int pz = in ? np : 0;
       const int pinc = warp_incl_scan(pz);
-      const int P = __shfl_sync(0xffffffffu, pinc, j1 - 1);
-      if (in) {
-        const int j = lane - j0;
-        g_pst[j] = pinc - pz;
-        g_rof[j] = incl - lz + (int)(c.a0 & 3);
-        g_q0[j] = c.q0;
-        g_tk[j] = take == c.d ? -take : take;
-        g_mg[j] = 0xffffffffu / (uint32_t)take + 1u;
-      }
-      if (lane == 0) g_pst[j1 - j0] = P;
-      for (int j = j0; j < j1; ++j) {
-        const int64_t a0 = __shfl_sync(0xffffffffu, c.a0, j);
-        const int32_t d = __shfl_sync(0xffffffffu, c.d, j);
-        const int o = __shfl_sync(0xffffffffu, incl - lz, j);
-        const int64_t al0 = a0 & ~3LL;
-        for (int64_t e = al0 + 4 * lane; e < a0 + d; e += 128)
-          cp_async16(buf + o + (int)(e - al0), A.col + e);
-      }
-      asm volatile("cp.async.commit_group;" ::: "memory");
+      const int P = __shfl_sync(FULL, pinc, j1 - 1);
+      const int pst = pinc - pz;                         // item's first pick
+      const int rof = incl - lz + (int)(c.a0 & 3);       // item's row base in buf
+      // every packed row: one bulk copy issued by its own lane
+      const uint32_t bytes = warp_sum(in ? 4u * (uint32_t)len : 0u);
+      if (lane == 0) mbar_expect_tx(bar, bytes);
       __syncwarp();
-      const int ng = j1 - j0;
-      // pick p of the sub-group: entry index, (frontier offset, batch) of its
-      // row, draw t, row base in buf.  The global loads are only issued here;
-      // their first use is in the serve loop below, kDdU picks later.
-      auto meta = [&](int p, int32_t& idx, int2& fb, int32_t& t, int32_t& ro) {
-        int lo = 0, hi = ng;
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (g_pst[mid] <= p) lo = mid; else hi = mid;
-        }
-        const int tk = g_tk[lo], tkn = tk < 0 ? -tk : tk;
-        const int r = p - g_pst[lo];
-        const int i = tkn == 1 ? r : (int)__umulhi((uint32_t)r, g_mg[lo]);
-        t = r - i * tkn;
-        const int q = g_q0[lo] + i;
-        idx = tk < 0 ? t : A.pidx[(uint32_t)q * (uint32_t)s + (uint32_t)t];
-        fb = dd_fb(A, q);
-        ro = g_rof[lo];
-      };
+      if (in) {
+        fence_async_smem();
+        tma_row(buf + (incl - lz), A.col + (c.a0 & ~3LL), 4u * (uint32_t)len, bar);
+      }
+      // pick metadata of kDdU windows of 32 picks; the global loads are
+      // issued here and first used in the serve loop below
       int32_t idx[kDdU], t[kDdU], ro[kDdU];
       int2 fb[kDdU];
       auto batch = [&](int p0) {
 #pragma unroll
-        for (int u = 0; u < kDdU; ++u)
-          if (p0 + 32 * u + lane < P) meta(p0 + 32 * u + lane, idx[u], fb[u], t[u], ro[u]);
+        for (int u = 0; u < kDdU; ++u) {
+          const int base = p0 + 32 * u;
+          const unsigned le = __ballot_sync(FULL, in && pst <= base);
+          const bool st = in && pst > base && pst < base + 32;
+          const unsigned M = __reduce_or_sync(FULL, st ? 1u << (pst - base) : 0u);
+          const int item = j0 + __popc(le) - 1 + __popc(M & ((2u << lane) - 1u));
+          const int ps = __shfl_sync(FULL, pst, item);
+          const int tk = __shfl_sync(FULL, take, item);
+          const uint32_t m = __shfl_sync(FULL, mg, item);
+          const int q0 = __shfl_sync(FULL, c.q0, item);
+          const int al = __shfl_sync(FULL, (int)all, item);
+          ro[u] = __shfl_sync(FULL, rof, item);
+          const int p = base + lane;
+          if (p < P) {
+            const int r = p - ps;
+            const int i = tk == 1 ? r : (int)__umulhi((uint32_t)r, m);
+            t[u] = r - i * tk;
+            const int q = q0 + i;
+            idx[u] = al ? t[u] : A.pidx[(uint32_t)q * (uint32_t)s + (uint32_t)t[u]];
+            fb[u] = dd_fb(A, q);
+          }
+        }
       };
       batch(0);  // while the rows land
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-      __syncwarp();
+      mbar_wait(bar, phase);
+      phase ^= 1u;
       for (int p0 = 0; p0 < P; p0 += 32 * kDdU) {
         if (p0) batch(p0);
 #pragma unroll
@@ -997,7 +995,7 @@ __device__ void dd_serve_warp(const DdArgs& A, int32_t* buf, int B, int32_t* gi)
           }
         }
       }
-      __syncwarp();  // buffer and group table free
+      __syncwarp();  // buffer free
       j0 = j1;
     }
   }
@@ -1013,7 +1011,7 @@ __global__ void __launch_bounds__(DdTier<TIER>::kThreads) k_dd_serve(DdArgs A) {
   if constexpr (!CTA) {
     const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     dd_serve_warp(A, sbuf + w * (A.chunk + 8), A.chunk + 8,
-                  sbuf + nw * (A.chunk + 8) + w * kGrpInts);
+                  reinterpret_cast<uint64_t*>(sbuf + nw * (A.chunk + 8) + w * kGrpInts));
     return;
   } else {
     __shared__ __align__(8) uint64_t bar;
@@ -1658,7 +1656,6 @@ static int dedup_layer(const Graph* g, SageWs& ws, const int64_t* R_ptr, const i
   A.fcol = fcol;
   A.bitmap = bitmap;
   A.nwords = nwords8;
-  A.ticket = ws.ticket;
   prof_mark(st);
   // the tiers touch disjoint frontier entries (and commutative bitmap ORs):
   // run them concurrently so each tier's tail overlaps the others
