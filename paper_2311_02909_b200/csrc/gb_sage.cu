@@ -642,7 +642,7 @@ __global__ void __launch_bounds__(kItemThreads) k_grp_items(
     const unsigned long long* __restrict__ dcount, const int32_t* __restrict__ dv,
     const int64_t* __restrict__ rowptr, int32_t* __restrict__ vcnt, int32_t* __restrict__ roff,
     int32_t s, int64_t icap, unsigned long long* __restrict__ tcnt, DdItem* __restrict__ items,
-    PeerRows peer, DdTiers tiers) {
+    PeerRows peer, DdTiers tiers, int32_t direct_ratio) {
   __shared__ int32_t s_wsum[4][kItemThreads / 32];
   __shared__ int64_t s_base[4];
   const int64_t D = (int64_t)*dcount;
@@ -667,17 +667,24 @@ __global__ void __launch_bounds__(kItemThreads) k_grp_items(
       }
     }
     int tot[4] = {0, 0, 0, 0};
+    bool dir[kGrpU];
 #pragma unroll
     for (int u = 0; u < kGrpU; ++u) {
       n[u] = 0;
       t[u] = 0;
       per[u] = 1;
+      dir[u] = false;
       if (v[u] >= 0) {
         vcnt[v[u]] = 0;  // ready for the next layer
         d[u] -= a0[u];
         t[u] = dd_tier(d[u], tiers);
         per[u] = rows_item(d[u], s, tiers);
-        n[u] = (gc[u] + per[u] - 1) / per[u];
+        // direct: the rows' picks cover so little of the A row that reading
+        // them in place (a sector each) moves fewer bytes than staging it
+        const int64_t take = d[u] < s ? d[u] : s;
+        dir[u] = direct_ratio > 0 && !peer.nblk &&
+                 (int64_t)gc[u] * take * direct_ratio < 8 * d[u];
+        n[u] = dir[u] ? 0 : (gc[u] + per[u] - 1) / per[u];
         tot[0] += t[u] == 0 ? n[u] : 0;
         tot[1] += t[u] == 1 ? n[u] : 0;
         tot[2] += t[u] == 2 ? n[u] : 0;
@@ -707,12 +714,13 @@ __global__ void __launch_bounds__(kItemThreads) k_grp_items(
     }
 #pragma unroll
     for (int u = 0; u < kGrpU; ++u) {
-      if (!n[u]) continue;
+      if (!gc[u]) continue;
       const int64_t r0 = o[3];
-      const int64_t oi = (t[u] == 0 ? o[0] : t[u] == 1 ? o[1] : o[2]) + (int64_t)t[u] * icap;
       o[3] += gc[u];
+      roff[v[u]] = dir[u] ? ~(int32_t)r0 : (int32_t)r0;  // < 0: direct rows
+      if (!n[u]) continue;
+      const int64_t oi = (t[u] == 0 ? o[0] : t[u] == 1 ? o[1] : o[2]) + (int64_t)t[u] * icap;
       if (t[u] == 0) o[0] += n[u]; else if (t[u] == 1) o[1] += n[u]; else o[2] += n[u];
-      roff[v[u]] = (int32_t)r0;
       int64_t ad = a0[u];
       if (peer.nblk) {
         int b = 0;
@@ -735,7 +743,8 @@ __global__ void __launch_bounds__(kItemThreads) k_grp_items(
   }
 }
 
-// grouped row records: (row within its batch, degree, frontier offset, batch)
+// grouped row records: (row within its batch, degree — or ~vertex for a
+// direct row —, frontier offset, batch)
 __global__ void k_grp_rows(const int64_t* __restrict__ R_ptr, const int32_t* __restrict__ rowv,
                            const int32_t* __restrict__ deg, const int64_t* __restrict__ fptr,
                            const int64_t* __restrict__ brow, int64_t k,
@@ -762,14 +771,16 @@ __global__ void k_grp_rows(const int64_t* __restrict__ R_ptr, const int32_t* __r
     }
 #pragma unroll
     for (int u = 0; u < kGrpU; ++u)
-      if (d[u] > 0) pos[u] = roff[v[u]] + sl[u];
+      if (d[u] > 0) pos[u] = roff[v[u]];
 #pragma unroll
     for (int u = 0; u < kGrpU; ++u) {
       if (d[u] > 0) {
         const int64_t r = r0 + u * (int64_t)blockDim.x;
         const int64_t b = batch_of(s_brow, brow, k, r);
-        rrec[pos[u]] = make_int4((int32_t)(r - (sm ? s_brow[b] : brow[b])), d[u],
-                                 (int32_t)fptr[r], (int32_t)b);
+        const bool dir = pos[u] < 0;
+        rrec[(dir ? ~pos[u] : pos[u]) + sl[u]] =
+            make_int4((int32_t)(r - (sm ? s_brow[b] : brow[b])), dir ? ~v[u] : d[u],
+                      (int32_t)fptr[r], (int32_t)b);
       }
     }
   }
@@ -778,26 +789,57 @@ __global__ void k_grp_rows(const int64_t* __restrict__ R_ptr, const int32_t* __r
 // NORM + SAMPLE of every grouped row with take < d: sorted picks at
 // pidx[q * s ..] (rows of one vertex sit in adjacent lanes and share their
 // replay-table loads); exhausted rows are served in order without picks.
+// Direct rows (record .y = ~vertex) read their picked columns in place and
+// finish the frontier entries and batch bits here.
+struct DdPickOut {
+  int32_t* pidx;
+  const int64_t* rowptr;
+  const int32_t* col;
+  int32_t* fcol;
+  uint32_t* bitmap;
+  int64_t nwords;
+};
 template <int MAXF>
 __global__ void __launch_bounds__(kPickThreads) k_dd_pick(
     const unsigned long long* __restrict__ grows, const int4* __restrict__ rrec, SageTabs T,
     int32_t s, int64_t batch_offset, int64_t stride, uint64_t seed, uint64_t epoch,
-    uint64_t depth, int32_t* __restrict__ pidx) {
+    uint64_t depth, DdPickOut O) {
   const int64_t R = (int64_t)*grows;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < R;
        q += (int64_t)gridDim.x * blockDim.x) {
     const int4 rec = rrec[q];
-    const int32_t d = rec.y, take = min(d, s);
-    if (take == d) continue;
+    int32_t d = rec.y;
+    int64_t a0 = -1;
+    if (d < 0) {
+      const int32_t v = ~d;
+      a0 = O.rowptr[v];
+      d = (int32_t)(O.rowptr[v + 1] - a0);
+    }
+    const int32_t take = min(d, s);
+    if (take == d && a0 < 0) continue;
     const uint64_t key = (uint64_t)((batch_offset + rec.w) * stride + rec.x);
     int32_t sorted[MAXF];
 #pragma unroll
     for (int z = 0; z < MAXF; ++z) sorted[z] = z;
-    sage_draws<MAXF>(T, key, d, take, seed, epoch, depth, sorted);
-    int32_t* out = pidx + q * s;
+    if (take < d) sage_draws<MAXF>(T, key, d, take, seed, epoch, depth, sorted);
+    if (a0 < 0) {
+      int32_t* out = O.pidx + q * s;
 #pragma unroll
-    for (int z = 0; z < MAXF; ++z)
-      if (z < take) out[z] = sorted[z];
+      for (int z = 0; z < MAXF; ++z)
+        if (z < take) out[z] = sorted[z];
+    } else {
+      int32_t cv[MAXF];
+#pragma unroll
+      for (int z = 0; z < MAXF; ++z)
+        if (z < take) cv[z] = __ldg(O.col + a0 + sorted[z]);
+      uint32_t* bm = O.bitmap + (int64_t)rec.w * O.nwords;
+#pragma unroll
+      for (int z = 0; z < MAXF; ++z)
+        if (z < take) {
+          O.fcol[rec.z + z] = cv[z];
+          atomicOr(bm + pk_word(cv[z]), 1u << (cv[z] & 31));
+        }
+    }
   }
 }
 
@@ -897,7 +939,10 @@ template <> struct DdTier<2> {
 };
 
 constexpr int kGrpInts = 2;  // per-warp mbarrier of the warp tier (in ints)
-constexpr int kDdU = 4;            // picks per lane whose loads are in flight together
+#ifndef GB_DDU
+#define GB_DDU 4  // swept 2 / 4 / 6 / 8: 4 best
+#endif
+constexpr int kDdU = GB_DDU;  // picks per lane whose loads are in flight together
 
 // (frontier offset, batch) of grouped row q: the second half of its record
 __device__ __forceinline__ int2 dd_fb(const DdArgs& A, int32_t q) {
@@ -1562,6 +1607,9 @@ constexpr int kMaxDevices = 16;
 struct ServeCfg {
   bool init = false;
   DdTiers tiers{1536, 4096};
+  // a vertex's rows read their picks in place when rows x take x ratio <
+  // 8 d (0: always staged)
+  int32_t direct_ratio = 2;  // swept 1 / 2 / 4 / 8
   int grid[3] = {0, 0, 0};
   int chunk[3] = {0, 0, 0};
   size_t smem[3] = {0, 0, 0};
@@ -1597,6 +1645,7 @@ static ServeCfg& serve_cfg() {
         c.tiers.hi1 = b2 & ~3;
       }
     }
+    if (const char* e = getenv("GB_DIRECT_RATIO")) c.direct_ratio = atoi(e) > 0 ? atoi(e) : 0;
     serve_tier_setup<0>(c, max_smem);
     serve_tier_setup<1>(c, max_smem);
     serve_tier_setup<2>(c, max_smem);
@@ -1620,7 +1669,7 @@ static int dedup_layer(const Graph* g, SageWs& ws, const int64_t* R_ptr, const i
   k_grp_items<<<grid_for((r_cap < g->n ? r_cap : g->n + 0) / kGrpU + 1, kItemThreads, gw),
                 kItemThreads, 0, st>>>(
       ws.cnts, ws.dv, g->rowptr, ws.vcnt, ws.roff, s, ws.icap, ws.cnts + 1, ws.items, peer,
-      serve_cfg().tiers);
+      serve_cfg().tiers, serve_cfg().direct_ratio);
   GB_LAUNCH_CHECK("k_grp_items");
   k_grp_rows<<<grid_for(r_cap / kGrpU + 1, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, fptr,
                                                                    brow, k, ws.rslot, ws.roff,
@@ -1632,9 +1681,10 @@ static int dedup_layer(const Graph* g, SageWs& ws, const int64_t* R_ptr, const i
   const int pgrid = grid_for(r_cap, kPickThreads, 64 * kNumSMs);
   const unsigned long long* grows = ws.cnts + 4;
   prof_mark(st);
+  const DdPickOut PO{ws.pidx, g->rowptr, g->col, fcol, bitmap, nwords8};
 #define GB_DD_PICK(MF)                                                                   \
   k_dd_pick<MF><<<pgrid, kPickThreads, 0, st>>>(grows, ws.rrec, T, s, batch_offset, stride, \
-                                               seed, epoch, depth, ws.pidx)
+                                               seed, epoch, depth, PO)
   switch (b) {
     case 0: GB_DD_PICK(5); break;
     case 1: GB_DD_PICK(8); break;
@@ -1709,6 +1759,18 @@ static int stream_grid() {
   return x;
 }
 
+// first layer sampled by the dedup kernels in dedup mode (GB_DEDUP_FROM
+// overrides, for sweeps)
+static int dedup_from() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GB_DEDUP_FROM");
+    v = e ? atoi(e) : 1;
+    if (v < 0) v = 0;
+  }
+  return v;
+}
+
 int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d_bverts,
               int64_t r1_cap, int64_t batch_size, int32_t layers, const int64_t* fanouts,
               uint64_t seed, uint64_t epoch, int64_t batch_offset, int32_t mode,
@@ -1774,9 +1836,12 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     if (l > 0) stride *= fanouts[l - 1];
     gb_sage_layer_out& o = L[l];
     const int32_t s = (int32_t)fanouts[l];
-    // fanouts above 32 take the P-free thread-per-row kernel in every mode
+    // fanouts above 32 take the P-free thread-per-row kernel in every mode;
+    // dedup mode samples its first dedup_from() layers P-free too (the seed
+    // rows repeat little across batches, so the grouping pass costs more
+    // than the shared rows save — measured)
     const bool big = s > 32;
-    const bool ldedup = dedup && !big;
+    const bool ldedup = dedup && !big && (peer.nblk || l >= dedup_from());
     const bool lstream = stream && !big;
     const int32_t* rowv = l == 0 ? d_bverts : L[l - 1].fcol;
     const int64_t* brow = l == 0 ? d_bptr : L[l - 1].eoff;
@@ -1829,6 +1894,9 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
         GB_LAUNCH_CHECK("k_sage_stream");
         prof_mark(st);
         count_launches(1);
+      } else if (dedup) {  // P-free layer of a dedup bulk: empty serve interval
+        prof_mark(st);
+        prof_mark(st);
       }
       count_launches(1);
     }
