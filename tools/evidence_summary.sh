@@ -14,7 +14,7 @@ echo "## Full captures (layer 3 of the dedup bulk; layer 2 of the LADIES bulk)";
 python tools/ncu_summary.py $O/ev_dedup_full.ncu-rep | sed 's|## gpurun_out/|### |'; echo
 python tools/ncu_summary.py $O/ev_ladies_full.ncu-rep | sed 's|## gpurun_out/|### |'; echo
 echo "## Where the time goes (source lines, warp-stall samples)"; echo
-for f in "k_dd_pick<(int)5" "k_dd_serve<(int)0" "k_sage_rank128" "k_grp_rows"; do
+for f in "k_dd_pick<(int)5" "k_sage_rank128" "k_grp_rows" "k_grp_count"; do
   timeout 300 python tools/ncu_lines.py $O/ev_dedup_full.ncu-rep "$f" 10; echo
 done
 for f in "k_lad_tile" "k_lad_extract"; do

@@ -1,7 +1,9 @@
-"""Refresh profiles/ncu_traffic.json (k_dd_serve, k_dd_pick) from an
-ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum CSV of the dedup
-bulk's pick / serve launches (tools/capture_evidence.sh, one bulk: per layer
-one k_dd_pick and the three k_dd_serve tiers).
+"""Refresh profiles/ncu_traffic.json from an ncu --metrics
+dram__bytes_read.sum,dram__bytes_write.sum CSV of one dedup bulk's sampling
+launches (tools/capture_evidence.sh): layer 1 k_sage_pick<1> (P-free), then
+per layer one k_dd_pick and the three k_dd_serve tiers.  Writes
+"dedup_sampling" (all of them, per layer: the bench's roofline kernel),
+"k_dd_pick" and "k_dd_serve".
 
 usage: traffic_json.py TRAFFIC.csv [SOURCE_NOTE]"""
 import collections
@@ -29,21 +31,26 @@ def main():
         b = float(r[mv].replace(",", ""))
         nm, acc = per.get(r[idc], (name, 0.0))
         per[r[idc]] = (nm, acc + b)
-    serve, pick = [], []
+    serve, pick, core = [], [], []
     for name, b in per.values():
-        if name.startswith("k_dd_pick"):
+        if name.startswith("k_dd_pick") or name.startswith("k_sage_pick"):
             pick.append(b)  # one pick launch opens each layer
             serve.append(0.0)
+            core.append(b)
         elif name.startswith("k_dd_serve") and serve:
             serve[-1] += b
+            core[-1] += b
     out_path = os.path.join(REPO, "profiles", "ncu_traffic.json")
     d = json.load(open(out_path))
     d["k_dd_serve"] = {"per_layer_bytes": serve, "bulk_bytes": sum(serve),
                        "source": note + " (ncu --metrics dram__bytes_read.sum,"
                        "dram__bytes_write.sum; per layer the 3 serve tier launches)"}
     d["k_dd_pick"] = {"per_layer_bytes": pick, "bulk_bytes": sum(pick), "source": "same capture"}
+    d["dedup_sampling"] = {"per_layer_bytes": core, "bulk_bytes": sum(core),
+                           "source": "same capture: per layer the pick launch (layer 1 "
+                                     "k_sage_pick<1>, then k_dd_pick) and the serve tiers"}
     json.dump(d, open(out_path, "w"), indent=1)
-    print(json.dumps({k: d[k] for k in ("k_dd_serve", "k_dd_pick")}, indent=1))
+    print(json.dumps({k: d[k] for k in ("dedup_sampling", "k_dd_serve", "k_dd_pick")}, indent=1))
 
 
 if __name__ == "__main__":
