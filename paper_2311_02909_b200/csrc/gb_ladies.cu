@@ -180,14 +180,41 @@ struct TileF {
 struct RaceKey {
   uint64_t seed, epoch, depth;
   int64_t key0;  // batch_offset + g0
-  __device__ __forceinline__ uint32_t operator()(int64_t j, int32_t v, uint32_t e) const {
+  __device__ __forceinline__ uint32_t word(int64_t j, int32_t v) const {
     // Philox4x32-10, counter (v, batch key lo/hi, depth), key (seed ^ epoch mix)
     const uint64_t bk = (uint64_t)(key0 + j);
     uint32_t c0 = (uint32_t)v, c1 = (uint32_t)bk, c2 = (uint32_t)(bk >> 32),
              c3 = (uint32_t)depth | 0x80000000u;
     philox4x32_10(c0, c1, c2, c3, (uint32_t)seed ^ (uint32_t)(seed >> 32),
                   (uint32_t)epoch ^ (uint32_t)(epoch >> 32) ^ 0x6c616479u);
-    return __float_as_uint(race_exp(c0) / ((float)e * (float)e));
+    return c0;
+  }
+  __device__ __forceinline__ uint32_t operator()(int64_t j, int32_t v, uint32_t e) const {
+    return __float_as_uint(race_exp(word(j, v)) / ((float)e * (float)e));
+  }
+  // (exact histogram bin of the key) << 20 | e, e < 2^20, without the
+  // accurate logarithm for almost every entry: E from the fast MUFU log
+  // (relative error < 2^-15: |log2 x| >= 0.02 on the log branch, 2^-22.6
+  // absolute error there; a 3-term series below V = 2^-6) brackets the key
+  // within +-2^-12; only a bracket that straddles a bin edge (~0.1% of
+  // entries) falls back to the exact key.  The exact key of an entry that
+  // can be selected is formed later from (v, e) (k_lad_filter_tiles).
+  __device__ __forceinline__ uint32_t bin_key(int64_t j, int32_t v, uint32_t e) const {
+    const uint32_t x = word(j, v);
+    float E;
+    if (x < 0x80000000u) {
+      const float V = ((float)x + 0.5f) * 0x1.0p-32f;
+      E = V < 0x1.0p-6f ? V * (1.0f + V * (0.5f + V * (1.0f / 3.0f)))
+                        : -__log2f(1.0f - V) * 0.69314718f;
+    } else {
+      E = -__log2f(((float)(0xffffffffu - x) + 0.5f) * 0x1.0p-32f) * 0.69314718f;
+    }
+    const float ka = __fdividef(E, (float)e * (float)e);
+    const uint32_t lo = __float_as_uint(ka * (1.0f - 0x1.0p-12f)) >> 20;
+    const uint32_t hi = __float_as_uint(ka * (1.0f + 0x1.0p-12f)) >> 20;
+    const uint32_t bin =
+        lo == hi ? lo : __float_as_uint(race_exp(x) / ((float)e * (float)e)) >> 20;
+    return (bin << 20) | e;
   }
 };
 
@@ -593,7 +620,7 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
           if (e) {
             const int pos = atomicAdd(&s_emit, 1);
             const int32_t v = v0 + off;
-            const uint32_t key = A.rk(j, v, e);
+            const uint32_t key = A.rk.bin_key(j, v, e);
             A.pv[slot + pos] = v;
             A.keys[slot + pos] = key;
             atomicAdd(s_h + (key >> 20), 1u);
@@ -644,7 +671,7 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
         for (int p = lane; p < cnt; p += 32) {
           const uint32_t rec = stg[p];
           const int32_t v = v0 + (int32_t)(rec >> 16);
-          const uint32_t key = A.rk(j, v, rec & 0xffffu);
+          const uint32_t key = A.rk.bin_key(j, v, rec & 0xffffu);
           A.pv[slot + base + p] = v;
           A.keys[slot + base + p] = key;
           atomicAdd(s_h + (key >> 20), 1u);
@@ -848,13 +875,17 @@ __global__ void k_lad_filter(LadiesSampleArgs A, const int32_t* __restrict__ bou
 }
 
 // k_lad_filter over the tiled layout: one CTA per (batch, tile) slot
+// The tiled pass stores (exact bin, e) per entry (RaceKey::bin_key): every
+// entry at or below the boundary bin gets its exact key here, before the
+// refinement / emission read it.
 __global__ void __launch_bounds__(256) k_lad_filter_tiles(LadiesSampleArgs A,
                                                         const int32_t* __restrict__ tb,
                                                         const int64_t* __restrict__ ntiles_p,
                                                         int64_t n, const int32_t* __restrict__ tcnt,
                                                         const int32_t* __restrict__ bound,
                                                         int32_t* __restrict__ cand,
-                                                        int32_t* __restrict__ ncand) {
+                                                        int32_t* __restrict__ ncand,
+                                                        RaceKey rk) {
   const int64_t ntiles = *ntiles_p;
   for (int64_t pr = blockIdx.x; pr < A.gn * ntiles; pr += gridDim.x) {
     const int32_t cnt = tcnt[pr];
@@ -865,7 +896,9 @@ __global__ void __launch_bounds__(256) k_lad_filter_tiles(LadiesSampleArgs A,
     const int b = bound[2 * j];
     for (int x = threadIdx.x; x < cnt; x += blockDim.x) {
       const int64_t p = slot + x;
-      const int bin = b == kBins ? -1 : (int)(A.keys[p] >> 20);
+      const uint32_t kb = A.keys[p];
+      const int bin = (int)(kb >> 20);
+      if (b == kBins || bin <= b) A.keys[p] = rk(j, A.pv[p], kb & 0xfffffu);
       if (b == kBins || bin < b)
         A.sel[i * A.s + atomicAdd(A.nsel + i, 1)] = (int32_t)p;
       else if (bin == b)
@@ -1515,7 +1548,7 @@ int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t*
         k_lad_boundary<<<(int)gn, 256, 0, st>>>(A, ws.hist, ws.bound);
         if (P.tiled)
           k_lad_filter_tiles<<<16 * sms, 256, 0, st>>>(A, ws.tb, ws.ntiles, n, ws.tcnt, ws.bound,
-                                                       ws.cand, ws.ncand);
+                                                       ws.cand, ws.ncand, rk);
         else
           k_lad_filter<<<16 * sms, 256, 0, st>>>(A, ws.bound, ws.cand, ws.ncand);
         k_lad_refine<<<(int)gn, 1024, 0, st>>>(A, ws.bound, ws.cand, ws.ncand, ws.overflow);
