@@ -368,7 +368,7 @@ def build_column_extraction(sampled_cols, n: int) -> SparseMatrix:
             raise ContractViolation("sampled vertex id out of range")
         if np.unique(s).size != s.size:
             raise ContractViolation("sampled vertex ids must be distinct")
-    d = torch.as_tensor(s).cuda()
+    d = torch.as_tensor(s if s.flags.writeable else s.copy()).cuda()
     order = torch.argsort(d, stable=True)
     rows = d[order]
     ptr = torch.zeros(n + 1, dtype=torch.int64, device="cuda")
