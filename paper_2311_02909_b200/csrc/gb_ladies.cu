@@ -345,7 +345,7 @@ constexpr int kLRowsSmem = 1024;  // rows whose cursors fit in shared memory
 constexpr int kLUnroll = 4;       // 32-entry loads in flight per row
 constexpr int kLList = 2048;      // touched offsets remembered per tile (sparse compaction)
 constexpr int kLShort = 16;       // expected entries per tile below which a row is "short"
-constexpr int kLShortRows = 4;    // short rows per warp step (8 lanes each)
+constexpr int kLShortU = 8;        // entries of a short row loaded at once (thread per row)
 
 // One ticket = batch j and a run of kLTileRun consecutive column tiles.  Per
 // tile: counts in shared memory (warp per A row, from the row's cursor, which
@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
   int32_t* s_rc = s_rl + kLRowsSmem;                 // row cursor (relative)
   int32_t* s_nv = s_rc + kLRowsSmem;                 // column at the cursor (INT32_MAX: done)
   int16_t* s_act = (int16_t*)(s_nv + kLRowsSmem);    // rows with entries in the tile
-  __shared__ int s_nact, s_lcnt, s_emit, s_rnext, s_nshort, s_snext;
+  __shared__ int s_nact, s_lcnt, s_emit, s_rnext, s_nshort;
   __shared__ uint16_t s_list[kLList];               // column offsets touched (sparse tiles)
   __shared__ int32_t s_wcnt[kLTileThreads / 32 + 1];
   __shared__ uint32_t s_stage[kLTileThreads / 32 * 64];
@@ -371,6 +371,35 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
   const int64_t nruns = (ntiles + kLTileRun - 1) / kLTileRun;
   const int64_t nt = A.gn * nruns;
   for (int w = threadIdx.x; w < kLTileW / 2; w += blockDim.x) s_cnt[w] = 0;
+  // count column c (inside the tile when `in`) and, while the tile is sparse
+  // (lc <= kLList, warp-uniform), list it for the sparse compaction — only
+  // at its counter's 0 -> 1 step (`ft`; measured: papers-shape LADIES 1.3K
+  // -> 2.4K minibatches/s, a sparse batch's tiles then list distinct
+  // columns and stay within kLList), or every entry (`ft` false).  The
+  // compaction reads and clears each listed counter, so repeats are
+  // harmless; a list count past kLList marks the tile dense.
+  // Warp-collective.
+  auto count = [&](int32_t c, bool in, int lc, int32_t v0, bool ft) {
+    const uint32_t off = (uint32_t)(c - v0), sh = (off & 1u) << 4;
+    if (lc <= kLList) {
+      bool first = in;
+      if (in) {
+        if (ft)
+          first = ((atomicAdd(s_cnt + (off >> 1), 1u << sh) >> sh) & 0xffffu) == 0u;
+        else
+          atomicAdd(s_cnt + (off >> 1), 1u << sh);
+      }
+      const unsigned m = __ballot_sync(FULL, first);
+      if (m) {
+        int lb = 0;
+        if (lane == 0) lb = atomicAdd(&s_lcnt, __popc(m));
+        lb = __shfl_sync(FULL, lb, 0) + __popc(m & ((1u << lane) - 1u));
+        if (first && lb < kLList) s_list[lb] = (uint16_t)off;
+      }
+    } else if (in) {
+      atomicAdd(s_cnt + (off >> 1), 1u << sh);
+    }
+  };
   for (;;) {
     if (threadIdx.x == 0) {
       s_ticket = (int64_t)atomicAdd(A.ticket, 1ull);
@@ -412,14 +441,13 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
         s_emit = 0;
         s_rnext = 0;
         s_nshort = 0;
-        s_snext = 0;
       }
       __syncthreads();
       // rows whose next column falls in this tile (cursor mode): tiles a
       // row has no entries in cost one shared-memory read
       // Rows expected to hold few entries in the tile (deg * width / n <
       // kLShort, columns are spread uniformly by the relabel) are listed from
-      // the back and counted kLShortRows per warp, 8 lanes each.
+      // the back and counted a thread per row.
       int nact = (int)(q1 - q0), nshort = 0;
       if (cur) {
         const int64_t wn = (int64_t)(v1 - v0);
@@ -434,6 +462,7 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
         nact = s_nact;
         nshort = s_nshort;
       }
+      auto lcnow = [&]() { return __shfl_sync(FULL, s_lcnt, 0); };
       // ---- e_v for v in [v0, v1)
       // cursor mode: the first kLUnroll x 32 entries of the warp's next row
       // are loaded while the current row is counted (two rows in flight)
@@ -487,16 +516,8 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
               if (done) break;
               const int32_t c = cv[u];
               const bool in = c < v1;
-              if (in) atomicAdd(s_cnt + ((c - v0) >> 1), 1u << (((c - v0) & 1) << 4));
+              count(c, in, lcnow(), v0, true);
               const unsigned out = __ballot_sync(FULL, !in);
-              const int lc = __shfl_sync(FULL, s_lcnt, 0);
-              if (lc <= kLList && ~out) {
-                const unsigned m = ~out;
-                int lb = 0;
-                if (lane == 0) lb = atomicAdd(&s_lcnt, __popc(m));
-                lb = __shfl_sync(FULL, lb, 0) + __popc(m & ((1u << lane) - 1u));
-                if (in && lb < kLList) s_list[lb] = (uint16_t)(c - v0);
-              }
               if (out) {
                 const int src = __ffs(out) - 1;
                 const int32_t nv = __shfl_sync(FULL, c, src);
@@ -511,48 +532,44 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
           }
           ai = anext;
         }
-        // short rows: kLShortRows rows per warp step, 8 lanes (one 32-B
-        // sector of columns) per row per step
-        const int g = lane >> 3, sl = lane & 7;
-        for (;;) {
-          int base = 0;
-          if (lane == 0) base = atomicAdd(&s_snext, kLShortRows);
-          base = __shfl_sync(FULL, base, 0);
-          if (base >= nshort) break;
-          const int si = base + g;
-          bool gdone = si >= nshort;
+        // short rows: a thread per row, kLShortU of its entries loaded at
+        // once — every short row's loads are in flight together, one memory
+        // round trip per tile rather than one per warp step (the rows of a
+        // sparse batch hold a few entries per tile: papers shape ~7)
+        for (int si0 = 0; si0 < nshort; si0 += blockDim.x) {
+          const int si = si0 + (int)threadIdx.x;
+          bool live = si < nshort;
           int64_t q = q0, a = 0, b = 0, e = 0;
-          if (!gdone) {
+          if (live) {
             q = q0 + (int64_t)s_act[kLRowsSmem - 1 - si];
             a = s_ra[q - q0];
             b = a + s_rl[q - q0];
-            e = a + s_rc[q - q0] + sl;
+            e = a + s_rc[q - q0];
           }
-          for (;;) {
-            const int32_t c = !gdone && e < b ? __ldg(A.col + e) : 0x7fffffff;
-            const bool in = !gdone && c < v1;
-            if (in) atomicAdd(s_cnt + ((c - v0) >> 1), 1u << (((c - v0) & 1) << 4));
-            const unsigned inb = __ballot_sync(FULL, in);
-            const int lc = __shfl_sync(FULL, s_lcnt, 0);
-            if (lc <= kLList && inb) {
-              int lb = 0;
-              if (lane == 0) lb = atomicAdd(&s_lcnt, __popc(inb));
-              lb = __shfl_sync(FULL, lb, 0) + __popc(inb & ((1u << lane) - 1u));
-              if (in && lb < kLList) s_list[lb] = (uint16_t)(c - v0);
-            }
-            const unsigned outb = __ballot_sync(FULL, !gdone && !in);
-            const unsigned gout = (outb >> (8 * g)) & 0xffu;
-            const int src = gout ? __ffs(gout) - 1 : 0;
-            const int32_t nv = __shfl_sync(FULL, c, 8 * g + src);  // next column
-            if (gout) {
-              if (sl == 0) {
-                s_rc[q - q0] = (int32_t)(e - a + src);
+          while (__any_sync(FULL, live)) {
+            int32_t c[kLShortU];
+#pragma unroll
+            for (int z = 0; z < kLShortU; ++z)
+              c[z] = live && e + z < b ? __ldg(A.col + e + z) : 0x7fffffff;
+            int nin = 0;  // columns are sorted: the in-tile entries are a prefix
+#pragma unroll
+            for (int z = 0; z < kLShortU; ++z) nin += c[z] < v1 ? 1 : 0;
+            const int lc = lcnow();
+#pragma unroll
+            for (int z = 0; z < kLShortU; ++z) count(c[z], live && z < nin, lc, v0, true);
+            if (live) {
+              if (nin < kLShortU) {  // the row leaves the tile (or ends) here
+                int32_t nv = 0x7fffffff;
+#pragma unroll
+                for (int z = 0; z < kLShortU; ++z)
+                  if (z == nin) nv = c[z];
+                s_rc[q - q0] = (int32_t)(e + nin - a);
                 s_nv[q - q0] = nv;
+                live = false;
+              } else {
+                e += kLShortU;
               }
-              gdone = true;
             }
-            e += 8;
-            if (__all_sync(FULL, gdone)) break;
           }
         }
       } else
@@ -582,18 +599,8 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
             if (done) break;
             const int32_t c = cv[u];
             const bool in = c < v1;
-            if (in) atomicAdd(s_cnt + ((c - v0) >> 1), 1u << (((c - v0) & 1) << 4));
+            count(c, in, lcnow(), v0, true);
             const unsigned out = __ballot_sync(FULL, !in);
-            // sparse tiles: remember the touched offsets while they fit (a
-            // count past kLList, even by skipped appends, marks the tile dense)
-            const int lc = __shfl_sync(FULL, s_lcnt, 0);
-            if (lc <= kLList && ~out) {
-              const unsigned m = ~out;
-              int lb = 0;
-              if (lane == 0) lb = atomicAdd(&s_lcnt, __popc(m));
-              lb = __shfl_sync(FULL, lb, 0) + __popc(m & ((1u << lane) - 1u));
-              if (in && lb < kLList) s_list[lb] = (uint16_t)(c - v0);
-            }
             if (out) {
               const int src = __ffs(out) - 1;
               const int32_t nv = __shfl_sync(FULL, c, src);  // next column (or INT32_MAX)
