@@ -272,8 +272,16 @@ __global__ void __launch_bounds__(256) k_lad_compact_write(uint32_t* __restrict_
 // degree mass (columns near hubs are narrow) so CTAs carry similar work;
 // CTAs take (batch, tile) tickets in order and chain their output offsets by
 // decoupled look-back, so P comes out in (batch, v) order in one pass.
-constexpr int kLTileW = 32768;      // columns per tile (64 KB of 16-bit counters)
-constexpr int kLTileThreads = 512;
+// Tile geometry and the sparse list (build-time knobs, swept round 2):
+// 32K columns x 512 threads, 2048 listed columns keeps two CTAs per SM; 64K
+// x 1024 with a 6144 list gained 5% on the papers shape and lost 7% on the
+// products shape; a 4096 list alone drops to one CTA per SM (-30%).
+#ifndef GB_LTILE_W
+#define GB_LTILE_W 32768
+#define GB_LTILE_T 512
+#endif
+constexpr int kLTileW = GB_LTILE_W;  // columns per tile (16-bit counters: 2 B each)
+constexpr int kLTileThreads = GB_LTILE_T;
 constexpr int kLMassTiles = 64;     // extra cuts by degree mass
 
 // cut before v when v is a multiple of kLTileW or crosses a mass quantile
@@ -343,7 +351,10 @@ struct LadTileArgs {
 constexpr int kLTileRun = 16;     // consecutive tiles per ticket (row cursors carried over)
 constexpr int kLRowsSmem = 1024;  // rows whose cursors fit in shared memory
 constexpr int kLUnroll = 4;       // 32-entry loads in flight per row
-constexpr int kLList = 2048;      // touched offsets remembered per tile (sparse compaction)
+#ifndef GB_LLIST
+#define GB_LLIST 2048
+#endif
+constexpr int kLList = GB_LLIST;  // touched offsets remembered per tile (sparse compaction)
 constexpr int kLShort = 16;       // expected entries per tile below which a row is "short"
 constexpr int kLShortU = 8;        // entries of a short row loaded at once (thread per row)
 

@@ -1,6 +1,6 @@
 # Build, LADIES parity tests, LADIES cfg3 bench value.
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail -30 gpurun_out/build.log; exit 1; }
-timeout 900 python -m pytest tests/test_ladies_gpu.py -m gpu -x -q > gpurun_out/ql_pytest.log 2>&1; tail -2 gpurun_out/ql_pytest.log
+[ -z "$NOTEST" ] && { timeout 900 python -m pytest tests/test_ladies_gpu.py -m gpu -x -q > gpurun_out/ql_pytest.log 2>&1; tail -2 gpurun_out/ql_pytest.log; }
 for i in 1 2; do
 timeout 600 python bench.py --steps 10 --warmup 3 --no-pfree --no-cpu-baseline --no-aggregation > gpurun_out/ql_bench.json 2> gpurun_out/ql_bench.err
 python -c "
