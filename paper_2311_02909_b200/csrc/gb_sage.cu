@@ -1311,6 +1311,138 @@ __global__ void __launch_bounds__(kRsThreads) k_rec_scan(uint4* __restrict__ rec
 }
 
 // coloff[b] = sum of the row totals before b; sizes = (R, F, U).  One CTA.
+// ---- sparse extraction (large n: the (batch, vertex) bit rows are almost
+// empty, e.g. papers shape: 7.1 G bits for <= 6.4 M set).  One touch bit per
+// 16-B record, set from the layer's picks; the scan and the enumeration then
+// visit touched records only instead of streaming every record.
+constexpr int kTouchB = 8;  // touched records whose loads are in flight together
+// touch bit of every pick's record: batch row walked as in k_sage_rank128
+__global__ void k_touch(const int64_t* __restrict__ brow, const int64_t* __restrict__ fptr,
+                        const int64_t* __restrict__ eoff, int64_t k,
+                        const int32_t* __restrict__ fcol, int64_t TW,
+                        uint32_t* __restrict__ touch) {
+  const int64_t F = fptr[brow[k]];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < F;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a = 0, b = k;  // last batch with eoff <= e
+    while (b - a > 1) {
+      const int64_t mid = (a + b) >> 1;
+      if (eoff[mid] <= e) a = mid; else b = mid;
+    }
+    const uint32_t r = (uint32_t)fcol[e] / 96u;  // record of the vertex in its batch row
+    atomicOr(touch + a * TW + (r >> 5), 1u << (r & 31));
+  }
+}
+// k_rec_scan over touched records only: tile = kRsThreads touch words of
+// one batch row, look-back chained within the row
+__global__ void __launch_bounds__(kRsThreads) k_rec_scan_touch(
+    uint4* __restrict__ rec, int64_t NR, int64_t k, const uint32_t* __restrict__ touch,
+    int64_t TW, int64_t* __restrict__ tot, unsigned long long* __restrict__ st) {
+  __shared__ int64_t sw[33];
+  __shared__ int64_t s_tile, s_prefix;
+  __shared__ uint8_t s_c8[32 * kRsThreads];  // set bits of each touched record
+  constexpr int64_t kTile = kRsThreads;  // touch words per tile
+  const int64_t tpr = (TW + kTile - 1) / kTile;
+  const int64_t ntiles = tpr * k;
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = (int64_t)atomicAdd(st, 1ull);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    if (tile >= ntiles) return;
+    const int64_t row = tile / tpr, seg = tile - row * tpr;
+    uint4* r = rec + row * NR;
+    const uint32_t* tw = touch + row * TW;
+    const int64_t w0 = seg * kTile + (int64_t)threadIdx.x;  // a touch word per thread
+    const uint32_t t = w0 < TW ? tw[w0] : 0u;
+    // the word's touched records in order, kTouchB at a time: their loads in
+    // flight together (one record load per iteration would serialise)
+    auto each = [&](auto&& fn) {
+      for (uint32_t m = t; m;) {
+        int32_t idx[kTouchB];
+        int nb = 0;
+#pragma unroll
+        for (int z = 0; z < kTouchB; ++z)
+          if (m) {
+            idx[z] = (int32_t)(w0 * 32) + __ffs(m) - 1;
+            m &= m - 1;
+            nb = z + 1;
+          }
+        uint4 x[kTouchB];
+#pragma unroll
+        for (int z = 0; z < kTouchB; ++z)
+          if (z < nb) x[z] = r[idx[z]];
+#pragma unroll
+        for (int z = 0; z < kTouchB; ++z)
+          if (z < nb) fn(idx[z], __popc(x[z].x) + __popc(x[z].y) + __popc(x[z].z));
+      }
+    };
+    int csum = 0, nt = 0;
+    each([&](int32_t, int c) {
+      s_c8[nt++ * kRsThreads + threadIdx.x] = (uint8_t)c;  // <= 96 per record
+      csum += c;
+    });
+    int64_t total;
+    int64_t run = block_excl_scan<int64_t>(csum, sw, total);
+    if (threadIdx.x < 32) {
+      const int64_t pre = tile_lookback(st, tile, row * tpr, total);
+      if (threadIdx.x == 0) s_prefix = pre;
+    }
+    __syncthreads();
+    run += s_prefix;
+    // prefixes from the counts kept in shared memory (no record reloads)
+    uint32_t* r32 = reinterpret_cast<uint32_t*>(r);
+    int j = 0;
+    for (uint32_t m = t; m; m &= m - 1, ++j) {
+      const int64_t i = w0 * 32 + __ffs(m) - 1;
+      r32[4 * i + 3] = (uint32_t)run;
+      run += s_c8[j * kRsThreads + threadIdx.x];
+    }
+    if (seg == tpr - 1 && threadIdx.x == 0) tot[row] = s_prefix + total;
+    __syncthreads();
+  }
+}
+// k_sage_enumerate128 over touched records; clears their bits and the touch
+// words (the workspace's clean state)
+__global__ void k_enum_touch(int64_t k, int64_t NR, uint4* __restrict__ rec,
+                             uint32_t* __restrict__ touch, int64_t TW,
+                             const int64_t* __restrict__ coloff, int32_t* __restrict__ colv) {
+  for (int64_t wi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; wi < k * TW;
+       wi += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t t = touch[wi];
+    if (!t) continue;
+    const int64_t bt = wi / TW, wr = wi - bt * TW;
+    const int64_t cb = coloff[bt];
+    for (uint32_t m = t; m;) {
+      // kTouchB touched records at a time, their loads in flight together
+      int32_t ri[kTouchB];
+      int nb = 0;
+#pragma unroll
+      for (int z = 0; z < kTouchB; ++z)
+        if (m) {
+          ri[z] = (int32_t)(wr * 32) + __ffs(m) - 1;  // record within the batch row
+          m &= m - 1;
+          nb = z + 1;
+        }
+      uint4 x[kTouchB];
+#pragma unroll
+      for (int z = 0; z < kTouchB; ++z)
+        if (z < nb) x[z] = rec[bt * NR + ri[z]];
+#pragma unroll
+      for (int z = 0; z < kTouchB; ++z) {
+        if (z >= nb) break;
+        const int32_t vb = ri[z] * 96;
+        int32_t o = (int32_t)(cb + x[z].w);
+        const uint32_t w[3] = {x[z].x, x[z].y, x[z].z};
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          for (uint32_t b = w[j]; b; b &= b - 1) colv[o++] = vb + 32 * j + __ffs(b) - 1;
+        rec[bt * NR + ri[z]] = make_uint4(0u, 0u, 0u, x[z].w);
+      }
+    }
+    touch[wi] = 0u;
+  }
+}
+
 __global__ void k_layer_cols(const int64_t* __restrict__ brow, int64_t k,
                              const int64_t* __restrict__ fptr, const int64_t* __restrict__ tot,
                              int64_t* __restrict__ coloff, int64_t* __restrict__ sizes) {
@@ -1529,6 +1661,9 @@ struct SageWs {
   int64_t icap;      // work-item capacity per tier
   DdItem* items;     // work-item descriptors
   int4* rrec;        // per grouped row: (local row, degree, frontier offset, batch)
+  uint32_t* touch;   // sparse extraction: touch bit per record, one set per bitmap set
+  uint32_t* touch2;
+  int64_t TW;        // touch words per batch row
   size_t bytes;
 };
 
@@ -1566,6 +1701,9 @@ static SageWs sage_ws_layout(char* base, int64_t k, int64_t n, int64_t r_cap_max
   w.icap = 2 * r_cap_max + 2;
   w.items = (DdItem*)take(sizeof(DdItem) * 3 * w.icap);
   w.rrec = (int4*)take(sizeof(int4) * (r_cap_max + 1));
+  w.TW = (NRr + 31) / 32;
+  w.touch = (uint32_t*)take(sizeof(uint32_t) * (k * w.TW + 1));
+  w.touch2 = (uint32_t*)take(sizeof(uint32_t) * (k * w.TW + 1));
   w.bytes = off;
   return w;
 }
@@ -1580,12 +1718,18 @@ __host__ __device__ __forceinline__ int64_t ws_clean_mark(int64_t nb, int64_t nv
 }
 __global__ void k_ws_clear(const int64_t* __restrict__ clean, uint32_t* __restrict__ b1,
                            uint32_t* __restrict__ b2, int64_t nb, int32_t* __restrict__ vcnt,
-                           int64_t nv) {
+                           int64_t nv, uint32_t* __restrict__ t1, uint32_t* __restrict__ t2,
+                           int64_t nt) {
   if (*clean == ws_clean_mark(nb, nv)) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nb;
        i += (int64_t)gridDim.x * blockDim.x) {
     b1[i] = 0u;
     b2[i] = 0u;
+  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nt;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    t1[i] = 0u;
+    t2[i] = 0u;
   }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -1820,11 +1964,16 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
   // (enumerate / items clear what they used): zero them only when the
   // workspace's clean mark is absent (first use, or an aborted bulk)
   k_ws_clear<<<4 * kNumSMs, 256, 0, st>>>(ws.clean, ws.bitmap, ws.bitmap2, W + 8, ws.vcnt,
-                                         g->n + 1);
+                                         g->n + 1, ws.touch, ws.touch2, k * ws.TW + 1);
   GB_LAUNCH_CHECK("k_ws_clear");
   k_set_i64<<<1, 1, 0, st>>>(ws.d_W, NS);
   k_set_i64<<<1, 1, 0, st>>>(ws.clean, 0);
   count_launches(3);
+  // sparse extraction (touched records only) when the (batch, vertex) bit
+  // rows are long: n >= 2^23 (papers shape: 1.2 GB of records per layer for
+  // a few million set bits); GB_SPARSE_EXTRACT=0/1 forces either
+  bool sparse = g->n >= ((int64_t)1 << 23);
+  if (const char* e = getenv("GB_SPARSE_EXTRACT")) sparse = atoi(e) != 0;
   // extraction of layer l (popcount scan, rank, enumerate) runs on a side
   // stream while layer l + 1 samples; layer l + 2 reuses layer l's bitmap
   // only after that extraction (ring events) — graph-capturable
@@ -1906,7 +2055,19 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     stream_wait(xs, st);
     // per batch row: record prefixes and the row total; column offsets
     int64_t* sizes = d_sizes + 3 * l;
-    if (k > 0) {
+    uint32_t* tch = (l & 1) ? ws.touch2 : ws.touch;
+    const int64_t f_cap0 = r_cap * s;
+    if (k > 0 && sparse) {
+      k_touch<<<grid_for(f_cap0, 256, 16 * kNumSMs), 256, 0, xs>>>(brow, o.fptr, o.eoff, k,
+                                                                  o.fcol, ws.TW, tch);
+      GB_LAUNCH_CHECK("k_touch");
+      const int64_t ttiles = k * ((ws.TW + kRsThreads - 1) / kRsThreads);
+      GB_CUDA(cudaMemsetAsync(ws.scan_ws2, 0, sizeof(int64_t) * (ttiles + 2), xs));
+      k_rec_scan_touch<<<grid_for(ttiles, 1, 8 * kNumSMs), kRsThreads, 0, xs>>>(
+          (uint4*)bm, NR, k, tch, ws.TW, ws.btot, (unsigned long long*)ws.scan_ws2);
+      GB_LAUNCH_CHECK("k_rec_scan_touch");
+      count_launches(1);
+    } else if (k > 0) {
       const int64_t rtiles = k * ((NR + kRsTile - 1) / kRsTile);
       GB_CUDA(cudaMemsetAsync(ws.scan_ws2, 0, sizeof(int64_t) * (rtiles + 2), xs));
       k_rec_scan<<<grid_for(rtiles, 1, 8 * kNumSMs), kRsThreads, 0, xs>>>(
@@ -1919,9 +2080,15 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     k_sage_rank128<<<grid_for(f_cap / 8 + 1, 256, 16 * kNumSMs), 256, 0, xs>>>(
         sizes + 1, o.eoff, o.coloff, k, o.fcol, (const uint4*)bm, NR, o.acol);
     GB_LAUNCH_CHECK("k_sage_rank128");
-    k_sage_enumerate128<<<grid_for(NS, 256, 16 * kNumSMs), 256, 0, xs>>>(NS, NR, (uint4*)bm,
-                                                                         o.coloff, o.colv);
-    GB_LAUNCH_CHECK("k_sage_enumerate128");
+    if (sparse) {
+      k_enum_touch<<<grid_for(k * ws.TW, 256, 16 * kNumSMs), 256, 0, xs>>>(
+          k, NR, (uint4*)bm, tch, ws.TW, o.coloff, o.colv);
+      GB_LAUNCH_CHECK("k_enum_touch");
+    } else {
+      k_sage_enumerate128<<<grid_for(NS, 256, 16 * kNumSMs), 256, 0, xs>>>(NS, NR, (uint4*)bm,
+                                                                           o.coloff, o.colv);
+      GB_LAUNCH_CHECK("k_sage_enumerate128");
+    }
     GB_CUDA(cudaEventRecord(ring_event(l), xs));
     count_launches(5);  // prep/count, eoff, cols, rank, enumerate
     r_cap = f_cap;

@@ -359,3 +359,51 @@ def test_sage_bulks_on_recycled_memory():
         junk = [torch.full((4096 * (i + 1),), 7, dtype=torch.int32, device="cuda")
                 for i in range(6)]
         del junk
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_sparse_extraction_forced_matches_oracle(mode, monkeypatch):
+    """The touched-record extraction (k_touch / k_rec_scan_touch /
+    k_enum_touch, the default for n >= 2^23) forced on small graphs: random
+    cases, hub rows and several fanout buckets bit-exact with the oracle,
+    then the dense extraction again on the same (clean) workspace."""
+    gb = _pkg()
+    monkeypatch.setenv("GB_SPARSE_EXTRACT", "1")
+    for case in range(3):
+        rng = np.random.default_rng(300 + case)
+        n, rowptr, col = _rmat(12 + case % 2, 30000 * (1 + case), seed=case + 11)
+        G = _graph(n, rowptr, col)
+        b, k = [40, 128, 300][case], [2, 7, 4][case]
+        fan = [(15, 10, 5), (3, 2), (25, 1, 8)][case]
+        batches = [rng.permutation(n)[: rng.integers(1, b + 1)] for _ in range(k)]
+        cfg = gb.SamplerConfig.sage(len(fan), b, fan, bulk_count=k, seed=case + 5)
+        want = O.sage_bulk(n, rowptr, col, batches, b, fan, case + 5, 1, 2)
+        ep = gb.sample_epoch_bulk(G, cfg, batches, epoch=1, batch_offset=2, mode=mode)
+        assert O.compare_epochs(want, ep.to_arrays()) == [], case
+        monkeypatch.setenv("GB_SPARSE_EXTRACT", "0")
+        ep = gb.sample_epoch_bulk(G, cfg, batches, epoch=1, batch_offset=2, mode=mode)
+        assert O.compare_epochs(want, ep.to_arrays()) == [], case
+        monkeypatch.setenv("GB_SPARSE_EXTRACT", "1")
+
+
+def test_sparse_extraction_default_on_large_n():
+    """n >= 2^23 takes the touched-record extraction by default: a sparse
+    random graph over 2^23 + 5 vertices, k = 6, bit-exact with the oracle."""
+    gb = _pkg()
+    rng = np.random.default_rng(9)
+    n = (1 << 23) + 5
+    m = 600000
+    src = rng.integers(0, n, m)
+    dst = rng.integers(0, n, m)
+    hub = rng.integers(0, n, 20)
+    src = np.concatenate([src, np.repeat(hub, 3000), rng.integers(0, n, 60000)])
+    dst = np.concatenate([dst, rng.integers(0, n, 60000), np.repeat(hub, 3000)])
+    G = gb.Graph.from_edges(n, np.concatenate([src, dst]), np.concatenate([dst, src]))
+    A = G.adjacency
+    batches = [np.concatenate([hub[:5], rng.integers(0, n, 200)]) for _ in range(6)]
+    batches = [np.unique(x) for x in batches]
+    cfg = gb.SamplerConfig.sage(3, 256, (15, 10, 5), bulk_count=6, seed=4)
+    want = O.sage_bulk(n, A.row_offsets, A.col_indices, batches, 256, (15, 10, 5), 4, 0, 0)
+    for mode in MODES:
+        ep = gb.sample_epoch_bulk(G, cfg, batches, mode=mode)
+        assert O.compare_epochs(want, ep.to_arrays()) == [], mode
