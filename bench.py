@@ -58,8 +58,7 @@ def parse():
     p.add_argument("--fetch", default="auto", choices=["auto", "rows", "owner", "p2p", "split"],
                    help="1.5D SAGE: Alg. 2 row fetch / owner-computes over NCCL, owner "
                         "sampling over peer memory (p2p), replicas splitting the batches "
-                        "with rows read from peer memory (split); auto = split if c > 1 on "
-                        "products, else p2p")
+                        "with rows read from peer memory (split); auto = split")
     return p.parse_args()
 
 
@@ -658,12 +657,12 @@ def run_15d(args, rank, world, local_rank):
     k = args.k or default_k(args.workload)
     allb = make_batches_for(n, k * grid.rows)
     # the grid samples row by row at the owner: stream or P-free kernels
-    # auto: replicas split the batches when c > 1 and the bulk's rows repeat
-    # enough for the dedup pass (products shape), else owner sampling over
-    # peer memory (measured: products 2x2 52.1K vs 35.3K; papers 2x2 12.7K vs
-    # 14.4K; products 4x1 58.2K vs 60.5K)
-    fetch = args.fetch if args.fetch != "auto" else (
-        "split" if c > 1 and args.workload != "papers" else "p2p")
+    # auto: the grid row's replicas split its batches and run the dedup bulk
+    # with rows staged from the owners' peer memory (round 2, split vs owner
+    # sampling over peer memory: products 2x2 88.7K vs -, 4x1 104.0K vs
+    # 56.5K, 2x1 67.5K vs 50.0K; papers 2x2 32.2K vs 14.3K, 2x1 23.2K vs
+    # 15.2K)
+    fetch = args.fetch if args.fetch != "auto" else "split"
     args.fetch = fetch
     m15 = "dedup" if fetch == "split" else ("stream" if args.mode == "stream" else "pfree")
     s = Sage15D(dg, grid, FANOUTS, BATCH, mode=m15, fetch=args.fetch)
