@@ -502,6 +502,10 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
           }
         }
         while (ai < nact) {
+          // the list state once per row (a stale count only lags: appends
+          // past kLList are dropped and still mark the tile dense), so no
+          // shared load sits in front of every step's atomic
+          const int lcr = lcnow();
           const int64_t q = qn, a = an, b = bn, e0 = e0n;
           int32_t cv[kLUnroll];
 #pragma unroll
@@ -527,7 +531,7 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
               if (done) break;
               const int32_t c = cv[u];
               const bool in = c < v1;
-              count(c, in, lcnow(), v0, true);
+              count(c, in, lcr, v0, true);
               const unsigned out = __ballot_sync(FULL, !in);
               if (out) {
                 const int src = __ffs(out) - 1;
@@ -585,6 +589,7 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
         }
       } else
       for (int ai = warp; ai < nact; ai += nwarps) {
+        const int lcr = lcnow();
         const int64_t q = q0 + (cur ? (int64_t)s_act[ai] : (int64_t)ai);
         int64_t a, b, e0;
         if (cur) {
@@ -610,7 +615,7 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
             if (done) break;
             const int32_t c = cv[u];
             const bool in = c < v1;
-            count(c, in, lcnow(), v0, true);
+            count(c, in, lcr, v0, true);
             const unsigned out = __ballot_sync(FULL, !in);
             if (out) {
               const int src = __ffs(out) - 1;
