@@ -348,14 +348,26 @@ struct LadTileArgs {
   int64_t* nnz_b;          // nonzeros per batch
 };
 
-constexpr int kLTileRun = 16;     // consecutive tiles per ticket (row cursors carried over)
+// build-time knobs, swept round 2 (cfg3 / papers minibatches/s): kLUnroll 2
+// 12.8K, 4 13.0K, 8 12.8K; kLTileRun 8 12.7K / 2.24K, 16 13.0K / 2.36K, 32
+// 11.7K / 2.35K; kLShort 8 12.8K / 2.22K, 16 13.0K / 2.36K, 32 13.1K / 1.95K
+#ifndef GB_LRUN
+#define GB_LRUN 16
+#endif
+constexpr int kLTileRun = GB_LRUN;     // consecutive tiles per ticket (row cursors carried over)
 constexpr int kLRowsSmem = 1024;  // rows whose cursors fit in shared memory
-constexpr int kLUnroll = 4;       // 32-entry loads in flight per row
+#ifndef GB_LUNROLL
+#define GB_LUNROLL 4
+#endif
+constexpr int kLUnroll = GB_LUNROLL;       // 32-entry loads in flight per row
 #ifndef GB_LLIST
 #define GB_LLIST 2048
 #endif
 constexpr int kLList = GB_LLIST;  // touched offsets remembered per tile (sparse compaction)
-constexpr int kLShort = 16;       // expected entries per tile below which a row is "short"
+#ifndef GB_LSHORT
+#define GB_LSHORT 16
+#endif
+constexpr int kLShort = GB_LSHORT;       // expected entries per tile below which a row is "short"
 constexpr int kLShortU = 8;        // entries of a short row loaded at once (thread per row)
 
 // One ticket = batch j and a run of kLTileRun consecutive column tiles.  Per
