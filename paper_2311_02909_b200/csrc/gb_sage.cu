@@ -1466,11 +1466,14 @@ __global__ void k_layer_cols(const int64_t* __restrict__ brow, int64_t k,
 // acol[e] = coloff[batch] + record prefix + rank inside the record
 // (compact_columns sparse.py:352-357 + block_diag :321-342); U entries per
 // thread, their record loads issued together
+#ifndef GB_RANK_U
+#define GB_RANK_U 4
+#endif
 __global__ void k_sage_rank128(const int64_t* __restrict__ F_ptr, const int64_t* __restrict__ eoff,
                                const int64_t* __restrict__ coloff, int64_t k,
                                const int32_t* __restrict__ fcol, const uint4* __restrict__ rec,
                                int64_t NR, int32_t* __restrict__ acol) {
-  constexpr int U = 8;
+  constexpr int U = GB_RANK_U;  // entries per thread, loads in flight together (swept 2 / 4 / 6 / 8 / 16: 4 best)
   __shared__ int32_t s_eoff[kBrowSmem], s_col[kBrowSmem];
   const bool sm = k + 1 <= kBrowSmem;
   if (sm)
@@ -2077,7 +2080,7 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     k_layer_cols<<<1, 1024, 0, xs>>>(brow, k, o.fptr, ws.btot, o.coloff, sizes);
     GB_LAUNCH_CHECK("k_layer_cols");
     const int64_t f_cap = r_cap * s;
-    k_sage_rank128<<<grid_for(f_cap / 8 + 1, 256, 16 * kNumSMs), 256, 0, xs>>>(
+    k_sage_rank128<<<grid_for(f_cap / GB_RANK_U + 1, 256, 16 * kNumSMs), 256, 0, xs>>>(
         sizes + 1, o.eoff, o.coloff, k, o.fcol, (const uint4*)bm, NR, o.acol);
     GB_LAUNCH_CHECK("k_sage_rank128");
     if (sparse) {
