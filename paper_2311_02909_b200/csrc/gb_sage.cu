@@ -549,7 +549,10 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k_sage_stream(SageArgs A,
 // into chunk bins, TMA ring with a producer warp).
 
 constexpr int kGrpThreads = 256;
-constexpr int kGrpU = 4;  // rows / distinct vertices per thread, gathers issued together
+#ifndef GB_GRP_U
+#define GB_GRP_U 2  // swept 1 / 2 / 4 / 8: 2 best
+#endif
+constexpr int kGrpU = GB_GRP_U;  // rows / distinct vertices per thread, gathers issued together
 __global__ void __launch_bounds__(kGrpThreads) k_grp_count(
     const int64_t* __restrict__ R_ptr, const int32_t* __restrict__ rowv,
     const int64_t* __restrict__ rowptr, int32_t* __restrict__ deg, int32_t* __restrict__ vcnt,
@@ -1261,7 +1264,10 @@ __global__ void k_sage_rank(const int64_t* __restrict__ F_ptr, const int64_t* __
 // scans its records (no cross-row look-back: rows are independent), writing
 // each record's within-row prefix into its fourth word and the row total;
 // the column offsets are the scan of the row totals.
-constexpr int kRsThreads = 256, kRsU = 8, kRsTile = kRsThreads * kRsU;
+#ifndef GB_RS_U
+#define GB_RS_U 4  // swept 2 / 4 / 8 / 16: 4 best
+#endif
+constexpr int kRsThreads = 256, kRsU = GB_RS_U, kRsTile = kRsThreads * kRsU;
 // tiles of kRsTile records never straddle a batch row: tile t is segment
 // t % tpr of row t / tpr, and its look-back stops at the row's first tile,
 // so the 64 rows' chains advance concurrently (st zeroed before the launch)
@@ -1688,7 +1694,7 @@ static SageWs sage_ws_layout(char* base, int64_t k, int64_t n, int64_t r_cap_max
   w.bitmap = (uint32_t*)take(sizeof(uint32_t) * (W + 8));
   w.bitmap2 = (uint32_t*)take(sizeof(uint32_t) * (W + 8));
   const int64_t NRr = (nwords + 2) / 3;  // bitmap records per batch row
-  const int64_t rs_tiles = k * ((NRr + 2047) / 2048) + 2;
+  const int64_t rs_tiles = k * ((NRr + kRsTile - 1) / kRsTile) + 2;
   const int64_t sw2 = scan_workspace_elems<int64_t>(W + 1);
   w.scan_ws2 = (int64_t*)take(sizeof(int64_t) * (sw2 > rs_tiles ? sw2 : rs_tiles));
   w.d_W = (int64_t*)take(sizeof(int64_t));
