@@ -209,7 +209,19 @@ __device__ __forceinline__ uint32_t pk_word(int32_t v) {
   return (r << 2) + (w - 3u * r);
 }
 
-constexpr int kPickThreads = 128;
+#ifndef GB_PICK_T
+#define GB_PICK_T 128  // pick CTA (swept 64 / 128 / 256)
+#endif
+#ifndef GB_PICK_GRID
+#define GB_PICK_GRID 64  // pick grid x SMs (swept 8 / 16 / 64 / 128 / 1024)
+#endif
+#ifndef GB_GRP_GRID
+#define GB_GRP_GRID 16  // grouping grids x SMs (swept 8 / 16 / 32)
+#endif
+#ifndef GB_X_GRID
+#define GB_X_GRID 32  // extraction grids x SMs (swept 8 / 16 / 32 / 64 / 128)
+#endif
+constexpr int kPickThreads = GB_PICK_T;
 constexpr int kStreamThreads = 256;
 constexpr int kRowCost = 48;       // merge-path weight of one row (in entries)
 constexpr int kStreamUnroll = 8;   // 16-B loads in flight per lane
@@ -1818,7 +1830,7 @@ static int dedup_layer(const Graph* g, SageWs& ws, const int64_t* R_ptr, const i
                        int64_t stride, int64_t batch_offset, uint64_t seed, uint64_t epoch,
                        uint64_t depth, int64_t r_cap, const PeerRows& peer, int32_t* fcol,
                        uint32_t* bitmap, int64_t nwords8, cudaStream_t st) {
-  const int64_t gw = 16 * kNumSMs;
+  const int64_t gw = GB_GRP_GRID * kNumSMs;
   k_grp_items<<<grid_for((r_cap < g->n ? r_cap : g->n + 0) / kGrpU + 1, kItemThreads, gw),
                 kItemThreads, 0, st>>>(
       ws.cnts, ws.dv, g->rowptr, ws.vcnt, ws.roff, s, ws.icap, ws.cnts + 1, ws.items, peer,
@@ -1831,7 +1843,7 @@ static int dedup_layer(const Graph* g, SageWs& ws, const int64_t* R_ptr, const i
   const ServeCfg& c = serve_cfg();
   const SageTabs T{g->deg_slot, g->run_j0, g->run_sd, g->run_n, g->run_lower};
   const int b = fan_bucket(s);
-  const int pgrid = grid_for(r_cap, kPickThreads, 64 * kNumSMs);
+  const int pgrid = grid_for(r_cap, kPickThreads, GB_PICK_GRID * kNumSMs);
   const unsigned long long* grows = ws.cnts + 4;
   prof_mark(st);
   const DdPickOut PO{ws.pidx, g->rowptr, g->col, fcol, bitmap, nwords8};
@@ -2009,7 +2021,7 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     if (ldedup) {
       GB_CUDA(cudaMemsetAsync(ws.cnts, 0, sizeof(unsigned long long) * 8, st));
       GB_CUDA(cudaMemsetAsync(ws.ticket, 0, sizeof(unsigned int) * 8, st));
-      k_grp_count<<<grid_for(r_cap / kGrpU + 1, kGrpThreads, 16 * kNumSMs), kGrpThreads, 0, st>>>(
+      k_grp_count<<<grid_for(r_cap / kGrpU + 1, kGrpThreads, GB_GRP_GRID * kNumSMs), kGrpThreads, 0, st>>>(
           R_ptr, rowv, g->rowptr, ws.deg, ws.vcnt, ws.rslot, ws.dv, ws.cnts);
       GB_LAUNCH_CHECK("k_grp_count");
     } else {
@@ -2036,7 +2048,7 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
       A.brow = brow; A.k = k; A.s = s; A.stride = stride; A.batch_offset = batch_offset;
       A.seed = seed; A.epoch = epoch; A.depth = (uint64_t)d;
       A.bitmap = bm; A.nwords = nw8; A.fcol = o.fcol; A.pidx = ws.pidx;
-      const int pick_grid = grid_for(r_cap, kPickThreads, 64 * kNumSMs);
+      const int pick_grid = grid_for(r_cap, kPickThreads, GB_PICK_GRID * kNumSMs);
       prof_mark(st);
       if (big)
         k_sage_pick_big<<<pick_grid, kPickThreads, 0, st>>>(A, R_ptr);
@@ -2086,7 +2098,7 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     k_layer_cols<<<1, 1024, 0, xs>>>(brow, k, o.fptr, ws.btot, o.coloff, sizes);
     GB_LAUNCH_CHECK("k_layer_cols");
     const int64_t f_cap = r_cap * s;
-    k_sage_rank128<<<grid_for(f_cap / GB_RANK_U + 1, 256, 16 * kNumSMs), 256, 0, xs>>>(
+    k_sage_rank128<<<grid_for(f_cap / GB_RANK_U + 1, 256, GB_X_GRID * kNumSMs), 256, 0, xs>>>(
         sizes + 1, o.eoff, o.coloff, k, o.fcol, (const uint4*)bm, NR, o.acol);
     GB_LAUNCH_CHECK("k_sage_rank128");
     if (sparse) {
@@ -2094,7 +2106,7 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
           k, NR, (uint4*)bm, tch, ws.TW, o.coloff, o.colv);
       GB_LAUNCH_CHECK("k_enum_touch");
     } else {
-      k_sage_enumerate128<<<grid_for(NS, 256, 16 * kNumSMs), 256, 0, xs>>>(NS, NR, (uint4*)bm,
+      k_sage_enumerate128<<<grid_for(NS, 256, GB_X_GRID * kNumSMs), 256, 0, xs>>>(NS, NR, (uint4*)bm,
                                                                            o.coloff, o.colv);
       GB_LAUNCH_CHECK("k_sage_enumerate128");
     }
