@@ -12,8 +12,11 @@
 namespace gb {
 
 constexpr int kScanThreads = 256;
-constexpr int kScanItems = 8;
-constexpr int kScanTile = kScanThreads * kScanItems;  // 2048
+#ifndef GB_SCAN_ITEMS
+#define GB_SCAN_ITEMS 8
+#endif
+constexpr int kScanItems = GB_SCAN_ITEMS;
+constexpr int kScanTile = kScanThreads * kScanItems;
 
 template <typename T>
 __device__ __forceinline__ T block_excl_scan(T v, T* smem_warp, T& total) {
