@@ -1819,6 +1819,19 @@ static ServeCfg& serve_cfg() {
   return c;
 }
 
+// per distinct vertex: work items and group row ranges (k_grp_items); runs
+// on its own stream next to the frontier-offset scan
+static int launch_items(const Graph* g, SageWs& ws, int32_t s, int64_t r_cap,
+                        const PeerRows& peer, cudaStream_t st) {
+  const int64_t gw = GB_GRP_GRID * kNumSMs;
+  k_grp_items<<<grid_for((r_cap < g->n ? r_cap : g->n + 0) / kGrpU + 1, kItemThreads, gw),
+                kItemThreads, 0, st>>>(
+      ws.cnts, ws.dv, g->rowptr, ws.vcnt, ws.roff, s, ws.icap, ws.cnts + 1, ws.items, peer,
+      serve_cfg().tiers, serve_cfg().direct_ratio);
+  GB_LAUNCH_CHECK("k_grp_items");
+  return GB_OK;
+}
+
 static int fan_bucket(int32_t s) { return s <= 5 ? 0 : s <= 8 ? 1 : s <= 10 ? 2 : s <= 16 ? 3 : 4; }
 
 // One dedup layer: grouping (count already ran; items, rows), NORM + SAMPLE
@@ -1831,11 +1844,6 @@ static int dedup_layer(const Graph* g, SageWs& ws, const int64_t* R_ptr, const i
                        uint64_t depth, int64_t r_cap, const PeerRows& peer, int32_t* fcol,
                        uint32_t* bitmap, int64_t nwords8, cudaStream_t st) {
   const int64_t gw = GB_GRP_GRID * kNumSMs;
-  k_grp_items<<<grid_for((r_cap < g->n ? r_cap : g->n + 0) / kGrpU + 1, kItemThreads, gw),
-                kItemThreads, 0, st>>>(
-      ws.cnts, ws.dv, g->rowptr, ws.vcnt, ws.roff, s, ws.icap, ws.cnts + 1, ws.items, peer,
-      serve_cfg().tiers, serve_cfg().direct_ratio);
-  GB_LAUNCH_CHECK("k_grp_items");
   k_grp_rows<<<grid_for(r_cap / kGrpU + 1, 256, gw), 256, 0, st>>>(R_ptr, rowv, ws.deg, fptr,
                                                                    brow, k, ws.rslot, ws.roff,
                                                                    ws.rrec);
@@ -2029,8 +2037,15 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
                                                                        ws.deg, nullptr);
       GB_LAUNCH_CHECK("k_sage_prep");
     }
+    // the distinct vertices' items (dedup) overlap the frontier-offset scan
+    if (ldedup) {
+      fork_begin(st, 1);
+      int rc0 = launch_items(g, ws, s, r_cap, peer, fork_stream(0));
+      if (rc0) return rc0;
+    }
     int rc = device_exclusive_scan<int64_t>(R_ptr, r_cap, TakeF{ws.deg, s}, o.fptr, ws.scan_ws, st);
     if (rc) return rc;
+    if (ldedup) fork_join(st, 1);
     if (lstream) {
       rc = device_exclusive_scan<int64_t>(R_ptr, r_cap, DegF{ws.deg}, ws.gstart, ws.scan_ws, st);
       if (rc) return rc;
