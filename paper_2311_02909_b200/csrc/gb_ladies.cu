@@ -1143,6 +1143,9 @@ constexpr int kXRows = 64;
 constexpr int kXSlots = 2 * kSmaxSmem;  // 2048
 constexpr int kXUnroll = 4;
 
+#ifndef GB_XHUB
+#define GB_XHUB 4  // hub rows (searched per sampled vertex) when d > GB_XHUB * take; swept 2 / 4 / 8 / 16
+#endif
 constexpr int kXSearch = 8;  // hub-row binary searches in flight per lane
 
 __device__ __forceinline__ uint32_t xhash(int32_t v) {
@@ -1188,7 +1191,7 @@ __global__ void __launch_bounds__(kLadiesThreads) k_lad_extract_hash(
       const int64_t a0 = rowptr[u], d = rowptr[u + 1] - a0;
       int32_t* out = slots + slot[q];
       int64_t o = 0;
-      if (d > 4 * take) {
+      if (d > GB_XHUB * take) {
         // hub row: search each sampled vertex in A[u,:] (sorted), kXSearch
         // searches per lane in lock-step so their loads are in flight together
         // (log2 d round trips per kXSearch * 32 sampled vertices)
