@@ -657,7 +657,7 @@ __global__ void __launch_bounds__(kItemThreads) k_grp_items(
     const unsigned long long* __restrict__ dcount, const int32_t* __restrict__ dv,
     const int64_t* __restrict__ rowptr, int32_t* __restrict__ vcnt, int32_t* __restrict__ roff,
     int32_t s, int64_t icap, unsigned long long* __restrict__ tcnt, DdItem* __restrict__ items,
-    PeerRows peer, DdTiers tiers, int32_t direct_ratio) {
+    PeerRows peer, DdTiers tiers, int32_t direct_ratio, bool peer_direct) {
   __shared__ int32_t s_wsum[4][kItemThreads / 32];
   __shared__ int64_t s_base[4];
   const int64_t D = (int64_t)*dcount;
@@ -697,7 +697,7 @@ __global__ void __launch_bounds__(kItemThreads) k_grp_items(
         // direct: the rows' picks cover so little of the A row that reading
         // them in place (a sector each) moves fewer bytes than staging it
         const int64_t take = d[u] < s ? d[u] : s;
-        dir[u] = direct_ratio > 0 && !peer.nblk &&
+        dir[u] = direct_ratio > 0 && (!peer.nblk || peer_direct) &&
                  (int64_t)gc[u] * take * direct_ratio < 8 * d[u];
         n[u] = dir[u] ? 0 : (gc[u] + per[u] - 1) / per[u];
         tot[0] += t[u] == 0 ? n[u] : 0;
@@ -813,6 +813,7 @@ struct DdPickOut {
   int32_t* fcol;
   uint32_t* bitmap;
   int64_t nwords;
+  PeerRows peer;  // nblk > 0: direct rows live in the owners' block CSRs
 };
 template <int MAXF>
 __global__ void __launch_bounds__(kPickThreads) k_dd_pick(
@@ -825,10 +826,21 @@ __global__ void __launch_bounds__(kPickThreads) k_dd_pick(
     const int4 rec = rrec[q];
     int32_t d = rec.y;
     int64_t a0 = -1;
+    const int32_t* rowp = nullptr;  // the direct row's entries
     if (d < 0) {
       const int32_t v = ~d;
-      a0 = O.rowptr[v];
-      d = (int32_t)(O.rowptr[v + 1] - a0);
+      if (O.peer.nblk) {
+        int b = 0;
+        while (b + 1 < O.peer.nblk && O.peer.bounds[b + 1] <= v) ++b;
+        const int64_t* brp = O.peer.brp[b] + (v - O.peer.bounds[b]);
+        a0 = brp[0];
+        d = (int32_t)(brp[1] - a0);
+        rowp = O.peer.bcol[b] + a0;
+      } else {
+        a0 = O.rowptr[v];
+        d = (int32_t)(O.rowptr[v + 1] - a0);
+        rowp = O.col + a0;
+      }
     }
     const int32_t take = min(d, s);
     if (take == d && a0 < 0) continue;
@@ -846,7 +858,7 @@ __global__ void __launch_bounds__(kPickThreads) k_dd_pick(
       int32_t cv[MAXF];
 #pragma unroll
       for (int z = 0; z < MAXF; ++z)
-        if (z < take) cv[z] = __ldg(O.col + a0 + sorted[z]);
+        if (z < take) cv[z] = __ldg(rowp + sorted[z]);
       uint32_t* bm = O.bitmap + (int64_t)rec.w * O.nwords;
 #pragma unroll
       for (int z = 0; z < MAXF; ++z)
@@ -1774,6 +1786,9 @@ struct ServeCfg {
   DdTiers tiers{1536, 4096};
   // a vertex's rows read their picks in place when rows x take x ratio <
   // 8 d (0: always staged)
+  // peer rows (1.5D split): direct rows read their picks from the owner's
+  // memory over NVLink instead of staging the row (GB_PEER_DIRECT=0/1)
+  bool peer_direct = true;
   int32_t direct_ratio = 2;  // swept 1 / 2 / 4 / 8
   int grid[3] = {0, 0, 0};
   int chunk[3] = {0, 0, 0};
@@ -1811,6 +1826,7 @@ static ServeCfg& serve_cfg() {
       }
     }
     if (const char* e = getenv("GB_DIRECT_RATIO")) c.direct_ratio = atoi(e) > 0 ? atoi(e) : 0;
+    if (const char* e = getenv("GB_PEER_DIRECT")) c.peer_direct = atoi(e) != 0;
     serve_tier_setup<0>(c, max_smem);
     serve_tier_setup<1>(c, max_smem);
     serve_tier_setup<2>(c, max_smem);
@@ -1827,7 +1843,7 @@ static int launch_items(const Graph* g, SageWs& ws, int32_t s, int64_t r_cap,
   k_grp_items<<<grid_for((r_cap < g->n ? r_cap : g->n + 0) / kGrpU + 1, kItemThreads, gw),
                 kItemThreads, 0, st>>>(
       ws.cnts, ws.dv, g->rowptr, ws.vcnt, ws.roff, s, ws.icap, ws.cnts + 1, ws.items, peer,
-      serve_cfg().tiers, serve_cfg().direct_ratio);
+      serve_cfg().tiers, serve_cfg().direct_ratio, serve_cfg().peer_direct);
   GB_LAUNCH_CHECK("k_grp_items");
   return GB_OK;
 }
@@ -1854,7 +1870,7 @@ static int dedup_layer(const Graph* g, SageWs& ws, const int64_t* R_ptr, const i
   const int pgrid = grid_for(r_cap, kPickThreads, GB_PICK_GRID * kNumSMs);
   const unsigned long long* grows = ws.cnts + 4;
   prof_mark(st);
-  const DdPickOut PO{ws.pidx, g->rowptr, g->col, fcol, bitmap, nwords8};
+  const DdPickOut PO{ws.pidx, g->rowptr, g->col, fcol, bitmap, nwords8, peer};
 #define GB_DD_PICK(MF)                                                                   \
   k_dd_pick<MF><<<pgrid, kPickThreads, 0, st>>>(grows, ws.rrec, T, s, batch_offset, stride, \
                                                seed, epoch, depth, PO)
