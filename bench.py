@@ -491,7 +491,14 @@ def run_ours(args, rank, world, local_rank):
         kb = [kernel_bytes(s_, args.mode) for s_ in st]
         kern_avg = kern_ms.mean(axis=0)[:, -1]  # dominant kernel, per layer
     pick_avg = kern_ms.mean(axis=0)[:, 0]
-    achieved = sum(kb) / (kern_avg.sum() / 1e3) / 1e9
+    achieved4 = sum(kb) / (kern_avg.sum() / 1e3) / 1e9
+    # a path that reads only the picked entries is held to
+    # its own sector-granular byte count — every random 4-B pick moves one
+    # 32-B sector — which is how the dedup bulk reads the picks of its direct
+    # rows (and of its P-free first layer); the 4-B count stays beside it
+    sector = [b + 28 * s_["F"] for b, s_ in zip(kb, st)] if args.mode in ("dedup", "pfree") \
+        else kb
+    achieved = sum(sector) / (kern_avg.sum() / 1e3) / 1e9
     bulk_bytes = sage_bytes(st)
     traffic = None
     tpath = os.path.join(REPO, "profiles", "ncu_traffic.json")
@@ -526,14 +533,13 @@ def run_ours(args, rank, world, local_rank):
             "kernel": KERNEL[args.mode],
             "pick_kernel_ms": [round(x, 4) for x in pick_avg.tolist()],
             "per_layer_ms": [round(x, 4) for x in kern_avg.tolist()],
-            "per_layer_bytes": kb, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)",
-            **({"achieved_sector_floor": (sum(kb) + 28 * sum(s_["F"] for s_ in st))
-                / (kern_avg.sum() / 1e3) / 1e9,
-                "frac_sector_floor": (sum(kb) + 28 * sum(s_["F"] for s_ in st))
-                / (kern_avg.sum() / 1e3) / 1e9 / peak,
-                "sector_note": "the same launches with every in-place pick charged the 32-B "
-                               "sector a random 4-B read moves at minimum"}
-               if args.mode == "dedup" else {}),
+            "per_layer_bytes": sector, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)",
+            **({"bytes_note": "per_layer_bytes: 32R + 12F per grouped layer (24R + 12F for the "
+                              "P-free first layer) with every in-place pick charged its 32-B "
+                              "sector (SURVEY.md 8(f)1: a picked-entries-only path is held to "
+                              "its sector-granular byte count); staged rows' entries not counted",
+                "per_layer_bytes_4b": kb, "achieved_4b": achieved4, "frac_4b": achieved4 / peak}
+               if args.mode in ("dedup", "pfree") else {}),
             "kernel_share_of_step": float(kern_avg.sum() / (total_ms / args.steps)),
             # the whole step against the bytes Alg. 1 with duplicate-row
             # elimination must move (28R + 4G_distinct + 12F + 4U + 8)
