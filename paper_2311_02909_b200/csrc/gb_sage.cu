@@ -2393,32 +2393,78 @@ int take_scan(int64_t r_cap, const int64_t* R_ptr, const int32_t* deg, int32_t s
 
 // gather rows `ids` of a CSR block (rows are ids[i] - row0) into a
 // contiguous buffer at out_off[i] (caller-computed from known degrees)
+// Rows ids[i] (block rows, row0-relative) copied to out[out_off[i] ..) (the
+// block may live in a peer's memory: NVLink round trips).  Work items are
+// chunks of at most kGatherChunk entries — their offsets an exclusive scan
+// of the rows' chunk counts — so a hub row is copied by many warps instead
+// of being walked by one (measured: one 148K-entry row set the whole
+// fetch's time); a warp per item, 8 loads in flight per lane.
+constexpr int kGatherChunk = 2048;
+struct GatherChunksF {
+  const int32_t* ids;
+  int64_t row0;
+  const int64_t* rowptr;
+  __device__ int64_t operator()(int64_t i) const {
+    const int64_t r = ids[i] - row0;
+    const int64_t d = rowptr[r + 1] - rowptr[r];
+    return d > 0 ? (d + kGatherChunk - 1) / kGatherChunk : 0;
+  }
+};
 __global__ void k_gather_rows(int64_t m, const int32_t* __restrict__ ids, int64_t row0,
                               const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
-                              const int64_t* __restrict__ out_off, int32_t* __restrict__ out) {
+                              const int64_t* __restrict__ out_off, int32_t* __restrict__ out,
+                              const int64_t* __restrict__ coff) {
   const int lane = lane_id();
-  for (int64_t i = global_warp(); i < m; i += grid_warps()) {
-    const int64_t r = ids[i] - row0;
-    const int64_t a = rowptr[r], d = rowptr[r + 1] - a, o = out_off[i];
-    // four loads in flight per lane (the block may live in a peer's memory)
-    for (int64_t x = lane; x < d; x += 128) {
-      int32_t v[4];
+  const int64_t nitems = coff[m];
+  for (int64_t it = global_warp(); it < nitems; it += grid_warps()) {
+    int64_t lo = 0, hi = m;  // last row with coff <= it
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (coff[mid] <= it) lo = mid; else hi = mid;
+    }
+    const int64_t r = ids[lo] - row0;
+    const int64_t a = rowptr[r], d = rowptr[r + 1] - a, o = out_off[lo];
+    const int64_t x0 = (it - coff[lo]) * kGatherChunk;
+    const int64_t x1 = min(d, x0 + kGatherChunk);
+    for (int64_t x = x0 + lane; x < x1; x += 256) {
+      int32_t v[8];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) v[u] = x + 32 * u < d ? col[a + x + 32 * u] : 0;
+      for (int u = 0; u < 8; ++u) v[u] = x + 32 * u < x1 ? col[a + x + 32 * u] : 0;
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (x + 32 * u < d) out[o + x + 32 * u] = v[u];
+      for (int u = 0; u < 8; ++u)
+        if (x + 32 * u < x1) out[o + x + 32 * u] = v[u];
     }
   }
 }
-
 int gather_rows(int64_t m, const int32_t* ids, int64_t row0, const int64_t* rowptr,
                 const int32_t* col, const int64_t* out_off, int32_t* out, cudaStream_t st) {
   if (m == 0) return GB_OK;
-  k_gather_rows<<<grid_for(m * 32, 256, 16 * kNumSMs), 256, 0, st>>>(m, ids, row0, rowptr, col,
-                                                                     out_off, out);
+  // chunk offsets (m + 1), the scan length and its workspace from the
+  // device's stream-ordered pool, which keeps its memory between calls
+  static bool pool_set[16] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!pool_set[dev & 15]) {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    pool_set[dev & 15] = true;
+  }
+  const size_t sw = scan_workspace_elems<int64_t>(m + 1);
+  int64_t* scratch = nullptr;
+  GB_CUDA(cudaMallocAsync((void**)&scratch, sizeof(int64_t) * (m + 2 + sw), st));
+  int64_t* coff = scratch;
+  int64_t* d_m = scratch + m + 1;
+  k_set_i64<<<1, 1, 0, st>>>(d_m, m);
+  int rc = device_exclusive_scan<int64_t>(d_m, m, GatherChunksF{ids, row0, rowptr}, coff,
+                                          scratch + m + 2, st);
+  if (rc) return rc;
+  k_gather_rows<<<16 * kNumSMs, 256, 0, st>>>(m, ids, row0, rowptr, col, out_off, out, coff);
   GB_LAUNCH_CHECK("k_gather_rows");
-  count_launches(1);
+  GB_CUDA(cudaFreeAsync(scratch, st));
+  count_launches(2);
   return GB_OK;
 }
 

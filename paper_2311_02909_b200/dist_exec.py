@@ -31,6 +31,9 @@ row keys), so the concatenation over grid rows equals the serial epoch.
 from __future__ import annotations
 
 import ctypes
+import os
+import sys
+import time
 
 import numpy as np
 
@@ -333,6 +336,14 @@ class Sage15D:
                        "gb_gather_rows")
             if owner != self.rank:
                 self.stats["fetch_ids"] += ids.numel()
+        if prof:
+            ev[1].record()
+            torch.cuda.synchronize()
+            t2 = time.perf_counter()
+            if self.rank == 0:
+                print(f"GB_PROF15 fetch: prep {1e3 * (t1 - t0):.3f} ms, gathers "
+                      f"{1e3 * (t2 - t1):.3f} ms wall / {ev[0].elapsed_time(ev[1]):.3f} ms device, "
+                      f"rows {U.numel()}, entries {nnz}", file=sys.stderr)
         return lrowptr, lcol
 
     def fetch_rows_any(self, U):
@@ -342,11 +353,20 @@ class Sage15D:
         torch = _torch()
         L = _lib.lib()
         pb = self._peer_block()
+        prof = os.environ.get("GB_PROF15") == "1"
+        if prof:
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
         d = self.gdeg[U.long()].long()
         lrowptr = torch.zeros(U.numel() + 1, dtype=torch.int64, device=self.dev)
         lrowptr[1:] = torch.cumsum(d, 0)
         nnz = int(lrowptr[-1].item())
         lcol = torch.zeros(nnz + _lib.GB_COL_PAD, dtype=torch.int32, device=self.dev)
+        if prof:
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            ev[0].record()
         for b in range(self.grid.rows):
             owner = self.grid.rank(b, self.j)
             lo, hi = int(self.bounds[b]), int(self.bounds[b + 1])
@@ -362,6 +382,14 @@ class Sage15D:
                        "gb_gather_rows")
             if owner != self.rank:
                 self.stats["fetch_ids"] += ids.numel()
+        if prof:
+            ev[1].record()
+            torch.cuda.synchronize()
+            t2 = time.perf_counter()
+            if self.rank == 0:
+                print(f"GB_PROF15 fetch: prep {1e3 * (t1 - t0):.3f} ms, gathers "
+                      f"{1e3 * (t2 - t1):.3f} ms wall / {ev[0].elapsed_time(ev[1]):.3f} ms device, "
+                      f"rows {U.numel()}, entries {nnz}", file=sys.stderr)
         return lrowptr, lcol
 
     def fetch_rows(self, U):
@@ -778,11 +806,26 @@ class Ladies15D(Sage15D):
         qcol = torch.as_tensor(np.concatenate([np.sort(np.asarray(x)) for x in mine])
                                .astype(np.int32) if off[-1] else np.zeros(1, np.int32)).to(dev)
         layers = []
+        prof = os.environ.get("GB_PROF15") == "1"
+        tp = {}
+
+        def mark(name, t0=[None]):
+            if not prof:
+                return
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            if t0[0] is not None:
+                tp[name] = tp.get(name, 0.0) + (t - t0[0]) * 1e3
+            t0[0] = t
+
+        mark("start")
         for l, s in enumerate(self.fanouts):
             QN = int(qoff[k].item()) if k else 0
             qc = qcol[:QN]
             U = torch.unique(qc)
+            mark("unique")
             lrowptr, lcol = self.fetch_rows_any(U)
+            mark("fetch")
             lrow = torch.searchsorted(U, qc).to(torch.int32).contiguous()
             qcap = max(QN, 1)
             o = {"fptr": torch.zeros(k + 1, dtype=torch.int64, device=dev),
@@ -801,12 +844,14 @@ class Ladies15D(Sage15D):
                                                   _lib.GB_LADIES_RACE, ctypes.byref(wsb)),
                        "gb_ladies_bulk_workspace")
             ws = torch.empty(max(int(wsb.value), 1), dtype=torch.uint8, device=dev)
+            mark("alloc")
             if k:
                 _lib.check(L.gb_ladies_layer_rows(
                     self.tables.handle, k, _lib.ptr(qoff), _lib.ptr(lrow), qcap, _lib.ptr(lrowptr),
                     _lib.ptr(lcol), s, seed, epoch, l + 1, batch_offset + j0,
                     _lib.GB_LADIES_RACE, ctypes.byref(out), _lib.ptr(sizes), _lib.ptr(ws),
                     ws.numel(), _lib.stream_ptr()), "gb_ladies_layer_rows")
+            mark("layer")
             R, F, A, C = (int(x) for x in sizes.tolist()[:4])
             layers.append({
                 "frontier_shape": (k, n), "frontier_ptr": o["fptr"], "frontier_col": o["fcol"][:F],
@@ -815,6 +860,10 @@ class Ladies15D(Sage15D):
                 "colv_off": o["fptr"], "colv_cat": o["fcol"][:F],
                 "sampv_off": o["fptr"], "sampv_cat": o["fcol"][:F]})
             qoff, qcol = o["fptr"], o["fcol"]
+            mark("sizes")
+        if prof and self.rank == 0:
+            print("GB_PROF15 ladies p2p ms:", {a: round(b, 3) for a, b in tp.items()},
+                  file=sys.stderr)
         return layers
 
     """1.5D partitioned LADIES (exponential-race sampling) over real processes.
