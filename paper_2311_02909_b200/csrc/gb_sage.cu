@@ -1363,15 +1363,25 @@ __global__ void k_touch(const int64_t* __restrict__ brow, const int64_t* __restr
     atomicOr(touch + a * TW + (r >> 5), 1u << (r & 31));
   }
 }
-// k_rec_scan over touched records only: tile = kRsThreads touch words of
+#ifndef GB_TS_T
+#define GB_TS_T 1024  // swept 128 / 256 / 512 / 1024 (papers: 1024 best)
+#endif
+#ifndef GB_ET_GRID
+#define GB_ET_GRID 16  // swept 8 / 16 / 32 / 64 (flat)
+#endif
+#ifndef GB_TS_GRID
+#define GB_TS_GRID 8
+#endif
+constexpr int kTsThreads = GB_TS_T;  // touched-record scan CTA = touch words per tile
+// k_rec_scan over touched records only: tile = kTsThreads touch words of
 // one batch row, look-back chained within the row
-__global__ void __launch_bounds__(kRsThreads) k_rec_scan_touch(
+__global__ void __launch_bounds__(kTsThreads) k_rec_scan_touch(
     uint4* __restrict__ rec, int64_t NR, int64_t k, const uint32_t* __restrict__ touch,
     int64_t TW, int64_t* __restrict__ tot, unsigned long long* __restrict__ st) {
   __shared__ int64_t sw[33];
   __shared__ int64_t s_tile, s_prefix;
-  __shared__ uint8_t s_c8[32 * kRsThreads];  // set bits of each touched record
-  constexpr int64_t kTile = kRsThreads;  // touch words per tile
+  __shared__ uint8_t s_c8[32 * kTsThreads];  // set bits of each touched record
+  constexpr int64_t kTile = kTsThreads;  // touch words per tile
   const int64_t tpr = (TW + kTile - 1) / kTile;
   const int64_t ntiles = tpr * k;
   for (;;) {
@@ -1408,7 +1418,7 @@ __global__ void __launch_bounds__(kRsThreads) k_rec_scan_touch(
     };
     int csum = 0, nt = 0;
     each([&](int32_t, int c) {
-      s_c8[nt++ * kRsThreads + threadIdx.x] = (uint8_t)c;  // <= 96 per record
+      s_c8[nt++ * kTsThreads + threadIdx.x] = (uint8_t)c;  // <= 96 per record
       csum += c;
     });
     int64_t total;
@@ -1425,7 +1435,7 @@ __global__ void __launch_bounds__(kRsThreads) k_rec_scan_touch(
     for (uint32_t m = t; m; m &= m - 1, ++j) {
       const int64_t i = w0 * 32 + __ffs(m) - 1;
       r32[4 * i + 3] = (uint32_t)run;
-      run += s_c8[j * kRsThreads + threadIdx.x];
+      run += s_c8[j * kTsThreads + threadIdx.x];
     }
     if (seg == tpr - 1 && threadIdx.x == 0) tot[row] = s_prefix + total;
     __syncthreads();
@@ -2113,9 +2123,9 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
       k_touch<<<grid_for(f_cap0, 256, 16 * kNumSMs), 256, 0, xs>>>(brow, o.fptr, o.eoff, k,
                                                                   o.fcol, ws.TW, tch);
       GB_LAUNCH_CHECK("k_touch");
-      const int64_t ttiles = k * ((ws.TW + kRsThreads - 1) / kRsThreads);
+      const int64_t ttiles = k * ((ws.TW + kTsThreads - 1) / kTsThreads);
       GB_CUDA(cudaMemsetAsync(ws.scan_ws2, 0, sizeof(int64_t) * (ttiles + 2), xs));
-      k_rec_scan_touch<<<grid_for(ttiles, 1, 8 * kNumSMs), kRsThreads, 0, xs>>>(
+      k_rec_scan_touch<<<grid_for(ttiles, 1, GB_TS_GRID * kNumSMs), kTsThreads, 0, xs>>>(
           (uint4*)bm, NR, k, tch, ws.TW, ws.btot, (unsigned long long*)ws.scan_ws2);
       GB_LAUNCH_CHECK("k_rec_scan_touch");
       count_launches(1);
@@ -2133,7 +2143,7 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
         sizes + 1, o.eoff, o.coloff, k, o.fcol, (const uint4*)bm, NR, o.acol);
     GB_LAUNCH_CHECK("k_sage_rank128");
     if (sparse) {
-      k_enum_touch<<<grid_for(k * ws.TW, 256, 16 * kNumSMs), 256, 0, xs>>>(
+      k_enum_touch<<<grid_for(k * ws.TW, 256, GB_ET_GRID * kNumSMs), 256, 0, xs>>>(
           k, NR, (uint4*)bm, tch, ws.TW, o.coloff, o.colv);
       GB_LAUNCH_CHECK("k_enum_touch");
     } else {
