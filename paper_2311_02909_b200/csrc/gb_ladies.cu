@@ -1012,10 +1012,39 @@ __global__ void __launch_bounds__(1024) k_lad_refine(LadiesSampleArgs A,
 // (and, for the distributed top-s merge, their race keys Kfix)
 __global__ void __launch_bounds__(256) k_lad_emit(LadiesSampleArgs A, int32_t* __restrict__ Sfix,
                                                 uint32_t* __restrict__ Kfix) {
+  // the selected entries of a batch in vertex order: a bitonic sort of
+  // (v, slot) pairs in shared memory when they fit, else rank by counting
+  __shared__ unsigned long long s_kv[kSmaxSmem];
   for (int64_t j = blockIdx.x; j < A.gn; j += gridDim.x) {
     const int64_t i = A.g0 + j;
     const int64_t take = A.take[i];
     const int32_t* si = A.sel + i * A.s;
+    if (take <= kSmaxSmem) {
+      int np = 1;
+      while (np < take) np <<= 1;
+      for (int a = threadIdx.x; a < np; a += blockDim.x)
+        s_kv[a] = a < take ? ((unsigned long long)(uint32_t)A.pv[si[a]] << 32) | (uint32_t)si[a]
+                           : ~0ull;
+      __syncthreads();
+      for (int kk = 2; kk <= np; kk <<= 1)
+        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+          for (int a = threadIdx.x; a < np; a += blockDim.x) {
+            const int b = a ^ jj;
+            if (b > a) {
+              const unsigned long long x = s_kv[a], y = s_kv[b];
+              if (((a & kk) == 0) == (x > y)) { s_kv[a] = y; s_kv[b] = x; }
+            }
+          }
+          __syncthreads();
+        }
+      for (int a = threadIdx.x; a < take; a += blockDim.x) {
+        const unsigned long long kv = s_kv[a];
+        Sfix[i * A.s + a] = (int32_t)(kv >> 32);
+        if (Kfix) Kfix[i * A.s + a] = A.keys[(uint32_t)kv];
+      }
+      __syncthreads();
+      continue;
+    }
     for (int64_t a = threadIdx.x; a < take; a += blockDim.x) {
       const int32_t x = si[a];
       const int32_t vx = A.pv[x];
