@@ -22,13 +22,19 @@
 //     the block-diagonal renumbering, and an enumerate pass for
 //     col_vertices.
 //
-// Two modes of the SAMPLE kernel, identical outputs:
+// Three modes of the SAMPLE kernels, identical outputs:
+//   GB_SAGE_DEDUP (default): rows grouped by vertex, each distinct P row
+//     sampled once per group; its picks read in place or the row staged
+//     by TMA (below).
 //   GB_SAGE_STREAM: P row formed on chip — the warp streams the whole A row
 //     (coalesced 16-B loads, merge-path balanced over rows+entries) and
 //     catches the picked entries out of registers.  This is Alg. 1 with P
 //     never written to HBM; its algorithmic bytes are SURVEY.md §8(d).
 //   GB_SAGE_PFREE: the P-free fast path: only the picked
 //     entries of A are read.
+// Extraction is dense (every bitmap record scanned) or, for n >= 2^23,
+// over the touched records only (k_touch / k_rec_scan_touch /
+// k_enum_touch).
 #include <stdarg.h>
 #include <stdlib.h>
 #include <stdio.h>
@@ -540,10 +546,14 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k_sage_stream(SageArgs A,
 // ============================================ deduplicated P rows (GB_SAGE_DEDUP)
 // Frontier rows repeat vertices heavily (hub bias: 3.5M rows over 0.55M
 // distinct vertices in layer 3 at products scale), and identical rows of
-// Q^l give identical rows of P = Q^l A.  Each distinct P row is formed on
-// chip once per work item — the A row staged in shared memory by TMA bulk
-// copies (cp.async.bulk + mbarrier) — and the picks of
-// every frontier row that references it are served from there.
+// Q^l give identical rows of P = Q^l A.  Rows are grouped by vertex and a
+// group's picks reach A one of two ways, chosen per vertex by bytes moved
+// (k_grp_items): "direct" — every pick read in place by the pick kernel (a
+// 32-B sector each; most vertices), or "staged" — the A row formed on chip
+// once per work item by TMA bulk copies (cp.async.bulk + mbarrier) and the
+// picks of every frontier row that references it served from there
+// (heavily re-referenced rows).  The first layer (seed rows) is sampled
+// P-free without grouping (dedup_from).
 //
 // Grouping (three passes over the layer's rows, no vertex bitmap):
 //   k_grp_count  degree of each row; rows per vertex counted in a per-vertex
@@ -553,12 +563,13 @@ __global__ void __launch_bounds__(kStreamThreads, 4) k_sage_stream(SageArgs A,
 //                rows' range, reserved by block-aggregated atomics (item and
 //                row order are free: every frontier row is independent);
 //                clears the counter for the next layer
-//   k_grp_rows   16-B record (local row, degree, frontier offset, batch) of
-//                each row at its group's range + slot
+//   k_grp_rows   16-B record (local row, degree or ~vertex for a direct
+//                row, frontier offset, batch) of each row at its group's
+//                range + slot
 // then NORM + SAMPLE per grouped row (k_dd_pick, whole-GPU thread per row,
-// rows of one vertex in adjacent lanes share the replay-table loads) and
-// the serve kernel (k_dd_serve: short rows packed into bins, long rows cut
-// into chunk bins, TMA ring with a producer warp).
+// rows of one vertex in adjacent lanes share the replay-table loads; direct
+// rows finish their frontier entries and batch bits there) and the serve
+// tiers for the staged rows (k_dd_serve<0,1,2>).
 
 constexpr int kGrpThreads = 256;
 #ifndef GB_GRP_U
