@@ -2139,13 +2139,14 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
       k_rec_scan_touch<<<grid_for(ttiles, 1, GB_TS_GRID * kNumSMs), kTsThreads, 0, xs>>>(
           (uint4*)bm, NR, k, tch, ws.TW, ws.btot, (unsigned long long*)ws.scan_ws2);
       GB_LAUNCH_CHECK("k_rec_scan_touch");
-      count_launches(1);
+      count_launches(2);
     } else if (k > 0) {
       const int64_t rtiles = k * ((NR + kRsTile - 1) / kRsTile);
       GB_CUDA(cudaMemsetAsync(ws.scan_ws2, 0, sizeof(int64_t) * (rtiles + 2), xs));
       k_rec_scan<<<grid_for(rtiles, 1, 8 * kNumSMs), kRsThreads, 0, xs>>>(
           (uint4*)bm, NR, k, ws.btot, (unsigned long long*)ws.scan_ws2);
       GB_LAUNCH_CHECK("k_rec_scan");
+      count_launches(1);
     }
     k_layer_cols<<<1, 1024, 0, xs>>>(brow, k, o.fptr, ws.btot, o.coloff, sizes);
     GB_LAUNCH_CHECK("k_layer_cols");
