@@ -1168,14 +1168,20 @@ __global__ void __launch_bounds__(kLadiesThreads) k_lad_extract(
 // kXUnroll loads in flight per lane) and probed — no per-entry binary search,
 // hub rows read sequentially instead of searched per sampled vertex.  Hits
 // come out in row order (ascending v), i.e. the sorted intersection.
-constexpr int kXRows = 64;
+#ifndef GB_XROWS
+#define GB_XROWS 64  // swept 16 / 32 / 64 (flat above 16)
+#endif
+constexpr int kXRows = GB_XROWS;
 constexpr int kXSlots = 2 * kSmaxSmem;  // 2048
 constexpr int kXUnroll = 4;
 
 #ifndef GB_XHUB
 #define GB_XHUB 4  // hub rows (searched per sampled vertex) when d > GB_XHUB * take; swept 2 / 4 / 8 / 16
 #endif
-constexpr int kXSearch = 8;  // hub-row binary searches in flight per lane
+#ifndef GB_XSEARCH
+#define GB_XSEARCH 4  // swept 2 / 4 / 8 / 16 (cfg3: 13.1 / 13.6 / 13.4 / 12.7K)
+#endif
+constexpr int kXSearch = GB_XSEARCH;  // hub-row binary searches in flight per lane
 
 __device__ __forceinline__ uint32_t xhash(int32_t v) {
   return ((uint32_t)v * 0x9E3779B1u) >> (32 - 11);  // kXSlots = 2^11
