@@ -1175,6 +1175,9 @@ constexpr int kXRows = GB_XROWS;
 constexpr int kXSlots = 2 * kSmaxSmem;  // 2048
 constexpr int kXUnroll = 4;
 
+#ifndef GB_LFILT_GRID
+#define GB_LFILT_GRID 32  // filter grid x SMs (swept 8 / 16 / 32 / 64: 32-64 best)
+#endif
 #ifndef GB_XHUB
 #define GB_XHUB 4  // hub rows (searched per sampled vertex) when d > GB_XHUB * take; swept 2 / 4 / 8 / 16
 #endif
@@ -1620,7 +1623,7 @@ int ladies_bulk(const Graph* g, int64_t k, const int64_t* d_qoff, const int32_t*
         }
         k_lad_boundary<<<(int)gn, 256, 0, st>>>(A, ws.hist, ws.bound);
         if (P.tiled)
-          k_lad_filter_tiles<<<16 * sms, 256, 0, st>>>(A, ws.tb, ws.ntiles, n, ws.tcnt, ws.bound,
+          k_lad_filter_tiles<<<GB_LFILT_GRID * sms, 256, 0, st>>>(A, ws.tb, ws.ntiles, n, ws.tcnt, ws.bound,
                                                        ws.cand, ws.ncand, rk);
         else
           k_lad_filter<<<16 * sms, 256, 0, st>>>(A, ws.bound, ws.cand, ws.ncand);
