@@ -351,6 +351,14 @@ struct LadTileArgs {
 // build-time knobs, swept round 2 (cfg3 / papers minibatches/s): kLUnroll 2
 // 12.8K, 4 13.0K, 8 12.8K; kLTileRun 8 12.7K / 2.24K, 16 13.0K / 2.36K, 32
 // 11.7K / 2.35K; kLShort 8 12.8K / 2.22K, 16 13.0K / 2.36K, 32 13.1K / 1.95K
+#ifndef GB_LTAIL
+#define GB_LTAIL 16  // swept (tail, run): (0,-) 13.7K · (8,4) 13.7K · (16,2) 14.0K · (16,4) 14.1K · (24,4) 14.1K · (32,4) 14.0K · (16,8) 13.6K
+#endif
+#ifndef GB_LTAILRUN
+#define GB_LTAILRUN 4
+#endif
+constexpr int kLTail = GB_LTAIL;        // last tiles of every batch in short runs
+constexpr int kLTailRun = GB_LTAILRUN;  // their run length
 #ifndef GB_LRUN
 #define GB_LRUN 16
 #endif
@@ -391,8 +399,14 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
   const unsigned FULL = 0xffffffffu;
   const int lane = lane_id(), warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int64_t ntiles = *A.ntiles;
-  const int64_t nruns = (ntiles + kLTileRun - 1) / kLTileRun;
-  const int64_t nt = A.gn * nruns;
+  // tickets: every batch's first tiles in runs of kLTileRun (cursors carried
+  // over a run), then — after all of those — its last kLTail tiles in runs
+  // of kLTailRun, so the final round of tickets is fine-grained
+  const int64_t tail = ntiles < kLTail ? ntiles : kLTail;
+  const int64_t nlong = (ntiles - tail) / kLTileRun;
+  const int64_t tail0 = nlong * kLTileRun;  // first tile of the short runs
+  const int64_t nshortr = (ntiles - tail0 + kLTailRun - 1) / kLTailRun;
+  const int64_t nt = A.gn * (nlong + nshortr);
   for (int w = threadIdx.x; w < kLTileW / 2; w += blockDim.x) s_cnt[w] = 0;
   // count column c (inside the tile when `in`) and, while the tile is sparse
   // (lc <= kLList, warp-uniform), list it for the sparse compaction — only
@@ -432,8 +446,17 @@ __global__ void __launch_bounds__(kLTileThreads) k_lad_tile(LadTileArgs A) {
     __syncthreads();
     const int64_t ticket = s_ticket;
     if (ticket >= nt) return;
-    const int64_t j = ticket / nruns, run = ticket - j * nruns;
-    const int64_t t0 = run * kLTileRun, t1 = min(t0 + kLTileRun, ntiles);
+    int64_t j, t0, t1;
+    if (ticket < A.gn * nlong) {
+      j = ticket / nlong;
+      t0 = (ticket - j * nlong) * kLTileRun;
+      t1 = t0 + kLTileRun;
+    } else {
+      const int64_t x = ticket - A.gn * nlong;
+      j = x / nshortr;
+      t0 = tail0 + (x - j * nshortr) * kLTailRun;
+      t1 = min(t0 + kLTailRun, ntiles);
+    }
     const int64_t q0 = A.qoff[A.g0 + j], q1 = A.qoff[A.g0 + j + 1];
     const bool cur = q1 - q0 <= kLRowsSmem;
     if (cur) {
