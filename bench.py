@@ -485,7 +485,12 @@ def run_ours(args, rank, world, local_rank):
     KERNEL = {"stream": "k_sage_stream", "pfree": "k_sage_pick<true>",
               "dedup": "k_dd_pick + k_dd_serve (layer 1: k_sage_pick<true>)"}
     if args.mode == "dedup":
-        kb = [kernel_bytes(s_, "dedup_first" if i == 0 else "dedup") for i, s_ in enumerate(st)]
+        # which layers the library grouped (gb_sage.cu group_pays: the layer's
+        # row bound >= 0.25 n, and never the first layer); the others ran
+        # the P-free pick
+        rcap = [k * BATCH * int(np.prod(FANOUTS[:i])) for i in range(len(FANOUTS))]
+        kb = [kernel_bytes(s_, "dedup" if i >= 1 and rcap[i] >= 0.25 * n else "dedup_first")
+              for i, s_ in enumerate(st)]
         kern_avg = kern_ms.mean(axis=0).sum(axis=1)  # pick + serve intervals, per layer
     else:
         kb = [kernel_bytes(s_, args.mode) for s_ in st]
