@@ -168,6 +168,13 @@ struct DegF {
   __device__ int64_t operator()(int64_t i) const { return deg[i]; }
 };
 
+struct PeerRows {
+  int nblk;
+  const int64_t* bounds;
+  const int64_t* const* brp;
+  const int32_t* const* bcol;
+};
+
 struct SageArgs {
   const int64_t* rowptr;
   const int32_t* col;
@@ -199,6 +206,7 @@ struct SageArgs {
   // P-free (OUT 1) extra destinations: peer frontiers written over NVLink
   int32_t* dst[8];
   int ndst;
+  PeerRows peer;  // nblk > 0 (1.5D split): A rows live in the owners' block CSRs
 };
 
 __device__ __forceinline__ int32_t vrank(const uint32_t* vbits, const int32_t* vpre, int32_t v) {
@@ -398,11 +406,19 @@ __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
       sage_draws<MAXF>(T, key, deg, take, A.seed, A.epoch, A.depth, sorted);
     }
     if (OUT == 1) {
-      const int64_t rs = A.rowptr[A.rowv[r]];
+      const int32_t v = A.rowv[r];
+      const int32_t* rowp;
+      if (A.peer.nblk) {
+        int pb = 0;
+        while (pb + 1 < A.peer.nblk && A.peer.bounds[pb + 1] <= v) ++pb;
+        rowp = A.peer.bcol[pb] + A.peer.brp[pb][v - A.peer.bounds[pb]];
+      } else {
+        rowp = A.col + A.rowptr[v];
+      }
       int32_t cv[MAXF];
 #pragma unroll
       for (int z = 0; z < MAXF; ++z)
-        if (z < take) cv[z] = __ldg(A.col + rs + sorted[z]);
+        if (z < take) cv[z] = __ldg(rowp + sorted[z]);
       if (A.fcol) {
 #pragma unroll
         for (int z = 0; z < MAXF; ++z)
@@ -652,12 +668,6 @@ struct __align__(16) DdItem {
 
 // row source of the 1.5D batch-split mode: rows of block b (vertices
 // [bounds[b], bounds[b+1])) live in a peer's memory as CSR brp[b] / bcol[b]
-struct PeerRows {
-  int nblk;
-  const int64_t* bounds;
-  const int64_t* const* brp;
-  const int32_t* const* bcol;
-};
 
 // tier t's items live in [t * icap, t * icap + tcnt[t]) (t = serve tier by
 // degree); tcnt[3] counts the grouped rows.  kGrpU distinct vertices per
@@ -2009,6 +2019,11 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
       return GB_ERR_UNSUPPORTED;
     }
     peer = PeerRows{peer_host->nblk, peer_host->bounds, peer_host->brp, peer_host->bcol};
+    for (int32_t l = 0; l < layers; ++l)
+      if (fanouts[l] > 32) {
+        set_error("sage bulk: peer rows support fanouts up to 32");
+        return GB_ERR_UNSUPPORTED;
+      }
   }
   const int64_t nwords = (g->n + 31) / 32;
   // (batch, vertex) bitmaps as pk_word records (3 bit words, prefix)
@@ -2070,8 +2085,7 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     // rows repeat little across batches, so the grouping pass costs more
     // than the shared rows save — measured)
     const bool big = s > 32;
-    const bool ldedup =
-        dedup && !big && (peer.nblk || (l >= dedup_from() && group_pays(r_cap, g->n)));
+    const bool ldedup = dedup && !big && l >= dedup_from() && group_pays(r_cap, g->n);
     const bool lstream = stream && !big;
     const int32_t* rowv = l == 0 ? d_bverts : L[l - 1].fcol;
     const int64_t* brow = l == 0 ? d_bptr : L[l - 1].eoff;
@@ -2108,7 +2122,7 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
       if (rc) return rc;
     } else {
       SageArgs A{};
-      A.rowptr = g->rowptr; A.col = g->col;
+      A.rowptr = g->rowptr; A.col = g->col; A.peer = peer;
       A.deg_slot = g->deg_slot; A.run_j0 = g->run_j0; A.run_sd = g->run_sd;
       A.run_n = g->run_n; A.run_lower = g->run_lower;
       A.rowv = rowv; A.deg = ws.deg; A.fptr = o.fptr; A.gstart = ws.gstart;
