@@ -1856,7 +1856,6 @@ static ServeCfg& serve_cfg() {
         c.tiers.hi1 = b2 & ~3;
       }
     }
-    if (const char* e = getenv("GB_DIRECT_RATIO")) c.direct_ratio = atoi(e) > 0 ? atoi(e) : 0;
     if (const char* e = getenv("GB_PEER_DIRECT")) c.peer_direct = atoi(e) != 0;
     serve_tier_setup<0>(c, max_smem);
     serve_tier_setup<1>(c, max_smem);
@@ -1864,6 +1863,14 @@ static ServeCfg& serve_cfg() {
     c.init = true;
   }
   return c;
+}
+
+// staged/direct threshold: GB_DIRECT_RATIO read per bulk (tests force either)
+static int32_t direct_ratio() {
+  const char* e = getenv("GB_DIRECT_RATIO");
+  if (!e) return serve_cfg().direct_ratio;
+  const int v = atoi(e);
+  return v > 0 ? v : 0;
 }
 
 // per distinct vertex: work items and group row ranges (k_grp_items); runs
@@ -1874,7 +1881,7 @@ static int launch_items(const Graph* g, SageWs& ws, int32_t s, int64_t r_cap,
   k_grp_items<<<grid_for((r_cap < g->n ? r_cap : g->n + 0) / kGrpU + 1, kItemThreads, gw),
                 kItemThreads, 0, st>>>(
       ws.cnts, ws.dv, g->rowptr, ws.vcnt, ws.roff, s, ws.icap, ws.cnts + 1, ws.items, peer,
-      serve_cfg().tiers, serve_cfg().direct_ratio, serve_cfg().peer_direct);
+      serve_cfg().tiers, direct_ratio(), serve_cfg().peer_direct);
   GB_LAUNCH_CHECK("k_grp_items");
   return GB_OK;
 }
@@ -1982,13 +1989,9 @@ static int stream_grid() {
 // first layer sampled by the dedup kernels in dedup mode (GB_DEDUP_FROM
 // overrides, for sweeps)
 static int dedup_from() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("GB_DEDUP_FROM");
-    v = e ? atoi(e) : 1;
-    if (v < 0) v = 0;
-  }
-  return v;
+  const char* e = getenv("GB_DEDUP_FROM");  // read per bulk (tests force either way)
+  const int v = e ? atoi(e) : 1;
+  return v < 0 ? 0 : v;
 }
 
 // Grouping a layer's rows by vertex pays when they repeat vertices: when
@@ -1997,11 +2000,8 @@ static int dedup_from() {
 // (bound 0.09 n: 1.46M rows over 0.93M vertices) P-free 1.59 vs 1.89 ms
 // per bulk.
 static bool group_pays(int64_t r_cap, int64_t n) {
-  static double ratio = -1.0;
-  if (ratio < 0.0) {
-    const char* e = getenv("GB_GROUP_RATIO");
-    ratio = e ? atof(e) : 0.25;
-  }
+  const char* e = getenv("GB_GROUP_RATIO");  // read per bulk (tests force either way)
+  const double ratio = e ? atof(e) : 0.25;
   return (double)r_cap >= ratio * (double)n;
 }
 

@@ -407,3 +407,26 @@ def test_sparse_extraction_default_on_large_n():
     for mode in MODES:
         ep = gb.sample_epoch_bulk(G, cfg, batches, mode=mode)
         assert O.compare_epochs(want, ep.to_arrays()) == [], mode
+
+
+def test_grouped_path_forced_everywhere(monkeypatch):
+    """The dedup bulk's grouped path (count / items / rows / pick / serve
+    tiers) forced on every layer — including layers the default rule samples
+    P-free — on random cases and the hub-row graph, with everything staged
+    and with everything direct: bit-exact with the oracle."""
+    gb = _pkg()
+    monkeypatch.setenv("GB_DEDUP_FROM", "0")
+    monkeypatch.setenv("GB_GROUP_RATIO", "0")
+    for case in range(3):
+        rng = np.random.default_rng(500 + case)
+        n, rowptr, col = _rmat(12 + case % 2, 30000 * (1 + case), seed=case + 21)
+        G = _graph(n, rowptr, col)
+        b, k = [40, 128, 300][case], [2, 7, 4][case]
+        fan = [(15, 10, 5), (3, 2), (25, 1, 8)][case]
+        batches = [rng.permutation(n)[: rng.integers(1, b + 1)] for _ in range(k)]
+        cfg = gb.SamplerConfig.sage(len(fan), b, fan, bulk_count=k, seed=case + 9)
+        want = O.sage_bulk(n, rowptr, col, batches, b, fan, case + 9, 2, 1)
+        for ratio in ("0", "1"):  # every row staged / direct wherever picks < 8 d
+            monkeypatch.setenv("GB_DIRECT_RATIO", ratio)
+            ep = gb.sample_epoch_bulk(G, cfg, batches, epoch=2, batch_offset=1, mode="dedup")
+            assert O.compare_epochs(want, ep.to_arrays()) == [], (case, ratio)
