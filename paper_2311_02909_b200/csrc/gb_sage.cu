@@ -1309,6 +1309,9 @@ __global__ void k_sage_rank(const int64_t* __restrict__ F_ptr, const int64_t* __
 // scans its records (no cross-row look-back: rows are independent), writing
 // each record's within-row prefix into its fourth word and the row total;
 // the column offsets are the scan of the row totals.
+#ifndef GB_RS_GRID
+#define GB_RS_GRID 8  // record-scan grid x SMs (swept 4 / 8 / 16: flat)
+#endif
 #ifndef GB_RS_U
 #define GB_RS_U 4  // swept 2 / 4 / 8 / 16: 4 best
 #endif
@@ -2172,7 +2175,7 @@ int sage_bulk(const Graph* g, int64_t k, const int64_t* d_bptr, const int32_t* d
     } else if (k > 0) {
       const int64_t rtiles = k * ((NR + kRsTile - 1) / kRsTile);
       GB_CUDA(cudaMemsetAsync(ws.scan_ws2, 0, sizeof(int64_t) * (rtiles + 2), xs));
-      k_rec_scan<<<grid_for(rtiles, 1, 8 * kNumSMs), kRsThreads, 0, xs>>>(
+      k_rec_scan<<<grid_for(rtiles, 1, GB_RS_GRID * kNumSMs), kRsThreads, 0, xs>>>(
           (uint4*)bm, NR, k, ws.btot, (unsigned long long*)ws.scan_ws2);
       GB_LAUNCH_CHECK("k_rec_scan");
       count_launches(1);
