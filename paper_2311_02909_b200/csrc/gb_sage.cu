@@ -842,9 +842,12 @@ __global__ void __launch_bounds__(kPickThreads) k_dd_pick(
     int32_t s, int64_t batch_offset, int64_t stride, uint64_t seed, uint64_t epoch,
     uint64_t depth, DdPickOut O) {
   const int64_t R = (int64_t)*grows;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < R;
-       q += (int64_t)gridDim.x * blockDim.x) {
-    const int4 rec = rrec[q];
+  const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int4 rec_n = q < R ? rrec[q] : make_int4(0, 0, 0, 0);  // the next row's record in flight
+  for (; q < R; q += gs) {
+    const int4 rec = rec_n;
+    if (q + gs < R) rec_n = rrec[q + gs];
     int32_t d = rec.y;
     int64_t a0 = -1;
     const int32_t* rowp = nullptr;  // the direct row's entries
