@@ -390,6 +390,19 @@ __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
     if (deg == 0) continue;  // empty P row (sample_rows_ordered, sampler.py:202-204)
     const int32_t take = min(deg, A.s);
     const int64_t fp = A.fptr[r];
+    // P-free: the row's start in A, loaded before the draws so its latency
+    // (rowv -> row_ptr, or the owner's block table) hides behind them
+    const int32_t* rowp = nullptr;
+    if (OUT == 1) {
+      const int32_t v = A.rowv[r];
+      if (A.peer.nblk) {
+        int pb = 0;
+        while (pb + 1 < A.peer.nblk && A.peer.bounds[pb + 1] <= v) ++pb;
+        rowp = A.peer.bcol[pb] + A.peer.brp[pb][v - A.peer.bounds[pb]];
+      } else {
+        rowp = A.col + A.rowptr[v];
+      }
+    }
     const int64_t bb = keyed ? 0 : batch_of(s_brow, A.brow, A.k, r);
     int32_t sorted[MAXF];
 #pragma unroll
@@ -406,15 +419,6 @@ __global__ void __launch_bounds__(kPickThreads) k_sage_pick(SageArgs A,
       sage_draws<MAXF>(T, key, deg, take, A.seed, A.epoch, A.depth, sorted);
     }
     if (OUT == 1) {
-      const int32_t v = A.rowv[r];
-      const int32_t* rowp;
-      if (A.peer.nblk) {
-        int pb = 0;
-        while (pb + 1 < A.peer.nblk && A.peer.bounds[pb + 1] <= v) ++pb;
-        rowp = A.peer.bcol[pb] + A.peer.brp[pb][v - A.peer.bounds[pb]];
-      } else {
-        rowp = A.col + A.rowptr[v];
-      }
       int32_t cv[MAXF];
 #pragma unroll
       for (int z = 0; z < MAXF; ++z)
