@@ -138,3 +138,38 @@ def test_structural_helpers():
         gb.build_column_extraction([1, 1], 6)
     f = gb.frontier_from_rows([[3, 1], [], [2]], 5)
     assert f.row_offsets.tolist() == [0, 2, 2, 3] and f.col_indices.tolist() == [1, 3, 2]
+
+
+def test_gather_rows_chunks_hub_rows():
+    """gb_gather_rows (the 1.5D row fetch / rows_subset reply): rows longer
+    than one 2048-entry work item — hub rows split over many warps — rows of
+    one entry, empty rows and repeated ids, each packed at its own offset,
+    equal to the numpy gather."""
+    import ctypes
+
+    import torch
+
+    from paper_2311_02909_b200 import _lib
+
+    rng = np.random.default_rng(3)
+    nrows, row0 = 300, 1000
+    deg = rng.integers(0, 40, nrows)
+    deg[[5, 77, 150]] = [2048, 9000, 150000]  # exactly one item, several, many
+    deg[[6, 7]] = [1, 0]
+    rowptr = np.zeros(nrows + 1, np.int64)
+    rowptr[1:] = np.cumsum(deg)
+    col = rng.integers(0, 1 << 30, int(rowptr[-1])).astype(np.int32)
+    ids = np.concatenate([rng.permutation(nrows), [150, 5, 7, 77]]).astype(np.int32) + row0
+    lens = deg[ids - row0]
+    off = np.zeros(ids.size, np.int64)
+    off[1:] = np.cumsum(lens)[:-1]
+    d = {k: torch.as_tensor(v).cuda() for k, v in
+         (("ids", ids), ("rp", rowptr), ("col", col), ("off", off))}
+    out = torch.full((int(lens.sum()) + 1,), -7, dtype=torch.int32, device="cuda")
+    L = _lib.lib()
+    _lib.check(L.gb_gather_rows(ids.size, _lib.ptr(d["ids"]), row0, _lib.ptr(d["rp"]),
+                                _lib.ptr(d["col"]), _lib.ptr(d["off"]), _lib.ptr(out),
+                                _lib.stream_ptr()), "gb_gather_rows")
+    got = out.cpu().numpy()
+    want = np.concatenate([col[rowptr[i - row0]:rowptr[i - row0 + 1]] for i in ids])
+    assert np.array_equal(got[:-1], want) and got[-1] == -7
